@@ -1,0 +1,237 @@
+"""CPU oracle for the CrypTen Beaver ring-GEMM hot path (arXiv 2109.00984).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  It wraps ``oracle/liboracle.so`` (built from ``oracle/oracle.c`` by
+``oracle.build()``), which shares no code with the CUDA path.
+
+All functions simulate every party in one process; party-indexed arrays are
+numpy ``uint64`` of shape ``(P, ...)``.  Each wrapper only marshals arguments;
+the arithmetic, with its citations into PAPER.md, lives in ``oracle.c``.
+
+Parity pins: ``tests/test_oracle_pins.py`` (Philox KAT, frozen PRG table,
+numpy / big-int GEMM, the paper's §4.3 float64 block GEMM, Beaver identity,
+P=1 closed form, Alg. 1 identity, encode/decode examples).  "Parity unpinned":
+only the PRG *layout* choice (any PRG is allowed), which is pinned
+to the frozen table of SURVEY.md Appendix A.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+TAG_PRZS, TAG_A, TAG_B, TAG_C, TAG_R, TAG_THETA = 1, 2, 3, 4, 5, 6
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so with plain gcc -O2 -fopenmp."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        u64p = ctypes.POINTER(ctypes.c_uint64)
+        i64 = ctypes.c_int64
+        L.oracle_prg_at.restype = ctypes.c_uint64
+        L.oracle_prg_at.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64]
+        L.oracle_stream_id.restype = ctypes.c_uint64
+        L.oracle_stream_id.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64]
+        L.oracle_prg.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, i64, u64p]
+        L.oracle_derive_keys.argtypes = [ctypes.c_uint64, ctypes.c_int, u64p, u64p]
+        L.oracle_encode.restype = ctypes.c_int
+        L.oracle_truncate_local.restype = ctypes.c_int
+        L.oracle_truncate_alg1.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _u64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint64))
+
+
+# ---------------------------------------------------------------- O1 PRG
+def philox4x32_10(ctr, key) -> list[int]:
+    c = (ctypes.c_uint32 * 4)(*[int(v) & 0xFFFFFFFF for v in ctr])
+    k = (ctypes.c_uint32 * 2)(*[int(v) & 0xFFFFFFFF for v in key])
+    o = (ctypes.c_uint32 * 4)()
+    lib().oracle_philox4x32_10(c, k, o)
+    return [int(o[i]) for i in range(4)]
+
+
+def stream_id(tag: int, party: int, ident: int) -> int:
+    return int(lib().oracle_stream_id(tag, party, ident & 0xFFFFFFFFFFFFFFFF))
+
+
+def prg(key: int, stream: int, n: int, start: int = 0) -> np.ndarray:
+    out = np.zeros(n, dtype=np.uint64)
+    lib().oracle_prg(ctypes.c_uint64(key), ctypes.c_uint64(stream), ctypes.c_uint64(start),
+                     ctypes.c_int64(n), out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
+    return out
+
+
+def derive_keys(master: int, P: int) -> tuple[np.ndarray, int]:
+    kp = np.zeros(max(P, 1), dtype=np.uint64)
+    kt = np.zeros(1, dtype=np.uint64)
+    lib().oracle_derive_keys(ctypes.c_uint64(master), P,
+                             kp.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                             kt.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
+    return kp[:P], int(kt[0])
+
+
+# ---------------------------------------------------------------- O2
+def encode(x, frac_bits: int = 16) -> np.ndarray:
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    out = np.zeros(x.shape, dtype=np.uint64)
+    rc = lib().oracle_encode(_p(x), _p(out), ctypes.c_int64(x.size), frac_bits)
+    if rc != 0:
+        raise OverflowError("encode: |x|*2^f >= 2^63")
+    return out
+
+
+def decode(v, frac_bits: int = 16) -> np.ndarray:
+    v = _u64(v)
+    out = np.zeros(v.shape, dtype=np.float64)
+    lib().oracle_decode(_p(v), _p(out), ctypes.c_int64(v.size), frac_bits)
+    return out
+
+
+# ---------------------------------------------------------------- O3 / O8
+def share(P: int, master: int, x, src: int, share_id: int) -> np.ndarray:
+    """PRZS shares of the src party's ring tensor x: array (P, *x.shape)."""
+    x = _u64(x)
+    kp, _ = derive_keys(master, P)
+    kp = np.ascontiguousarray(kp)
+    out = np.zeros((P,) + x.shape, dtype=np.uint64)
+    lib().oracle_share(P, _p(kp), _p(x), src, ctypes.c_uint64(share_id), ctypes.c_int64(x.size), _p(out))
+    return out
+
+
+def reveal(shares) -> np.ndarray:
+    s = _u64(shares)
+    P = s.shape[0]
+    out = np.zeros(s.shape[1:], dtype=np.uint64)
+    lib().oracle_reveal(P, _p(s), ctypes.c_int64(out.size), _p(out))
+    return out
+
+
+# ---------------------------------------------------------------- GEMM
+def ring_matmul(A, B) -> np.ndarray:
+    A, B = _u64(A), _u64(B)
+    M, K = A.shape
+    K2, N = B.shape
+    assert K == K2
+    C = np.zeros((M, N), dtype=np.uint64)
+    lib().oracle_ring_matmul(_p(A), _p(B), _p(C), ctypes.c_int64(M), ctypes.c_int64(K), ctypes.c_int64(N))
+    return C
+
+
+# ---------------------------------------------------------------- O4
+def ttp_triple(P: int, master: int, triple_id: int, M: int, K: int, N: int, rows=None):
+    """Beaver matmul triple (a: (P,R,K), b: (P,K,N), c: (P,R,N)); R = M or len(rows)."""
+    _, kt = derive_keys(master, P)
+    if rows is None:
+        R = M
+        rp = None
+    else:
+        rows = np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
+        R = rows.size
+        rp = _p(rows)
+    a = np.zeros((P, R, K), dtype=np.uint64)
+    b = np.zeros((P, K, N), dtype=np.uint64)
+    c = np.zeros((P, R, N), dtype=np.uint64)
+    lib().oracle_ttp_triple(P, ctypes.c_uint64(kt), ctypes.c_uint64(triple_id), ctypes.c_int64(M),
+                            ctypes.c_int64(K), ctypes.c_int64(N), rp, ctypes.c_int64(R),
+                            _p(a), _p(b), _p(c))
+    return a, b, c
+
+
+# ---------------------------------------------------------------- O5
+def beaver_matmul(x, y, a, b, c, want_intermediates: bool = False):
+    """Un-truncated Beaver matmul shares z: (P, M, N) (scale 2^(2f))."""
+    x, y, a, b, c = (_u64(t) for t in (x, y, a, b, c))
+    P, M, K = x.shape
+    N = y.shape[2]
+    z = np.zeros((P, M, N), dtype=np.uint64)
+    e = np.zeros((P, M, K), dtype=np.uint64)
+    d = np.zeros((P, K, N), dtype=np.uint64)
+    eps = np.zeros((M, K), dtype=np.uint64)
+    delta = np.zeros((K, N), dtype=np.uint64)
+    lib().oracle_beaver_matmul(P, _p(x), _p(y), _p(a), _p(b), _p(c), ctypes.c_int64(M), ctypes.c_int64(K),
+                               ctypes.c_int64(N), _p(e), _p(d), _p(eps), _p(delta), _p(z))
+    if want_intermediates:
+        return z, dict(e=e, d=d, eps=eps, delta=delta)
+    return z
+
+
+# ---------------------------------------------------------------- O6 / O7
+def truncate_local(x, bits: int = 16) -> np.ndarray:
+    x = _u64(x)
+    out = np.zeros_like(x)
+    rc = lib().oracle_truncate_local(x.shape[0], _p(x), ctypes.c_int64(x[0].size), bits, _p(out))
+    if rc != 0:
+        raise ValueError("truncate_local: bad bits")
+    return out
+
+
+def wrap_count(x) -> np.ndarray:
+    """Exact θ_x = (Σ signed([x]_p) − signed(x)) / 2^64 per element."""
+    x = _u64(x)
+    th = np.zeros(x.shape[1:], dtype=np.int64)
+    lib().oracle_wrap_count(x.shape[0], _p(x), ctypes.c_int64(th.size), _p(th))
+    return th
+
+
+def wrap_pair(P: int, master: int, wrap_id: int, n: int):
+    _, kt = derive_keys(master, P)
+    r = np.zeros((P, n), dtype=np.uint64)
+    th = np.zeros((P, n), dtype=np.uint64)
+    lib().oracle_wrap_pair(P, ctypes.c_uint64(kt), ctypes.c_uint64(wrap_id), ctypes.c_int64(n), _p(r), _p(th))
+    return r, th
+
+
+def truncate_alg1(x, r, theta_r, bits: int = 16, diagnostics: bool = False):
+    x, r, theta_r = _u64(x), _u64(r), _u64(theta_r)
+    P = x.shape[0]
+    n = x[0].size
+    out = np.zeros_like(x)
+    z = np.zeros(x.shape[1:], dtype=np.uint64)
+    eta = np.zeros(x.shape[1:], dtype=np.int64)
+    rc = lib().oracle_truncate_alg1(P, _p(x), _p(r), _p(theta_r), ctypes.c_int64(n), bits, _p(out), _p(z), _p(eta))
+    if rc != 0:
+        raise ValueError("truncate_alg1: bad arguments")
+    if diagnostics:
+        return out, dict(z=z, eta=eta)
+    return out
+
+
+def truncate(x, bits: int = 16, master: int | None = None, wrap_id: int = 0, diagnostics: bool = False):
+    """Protocol truncation: local for P <= 2, Alg. 1 for P > 2."""
+    x = _u64(x)
+    P = x.shape[0]
+    if P <= 2:
+        out = truncate_local(x, bits)
+        return (out, dict(theta=wrap_count(x))) if diagnostics else out
+    r, th = wrap_pair(P, master, wrap_id, x[0].size)
+    r = r.reshape(x.shape)
+    th = th.reshape(x.shape)
+    return truncate_alg1(x, r, th, bits, diagnostics)

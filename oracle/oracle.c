@@ -1,0 +1,381 @@
+/*
+ * oracle/oracle.c — plain, slow, obviously-correct CPU oracle for the CrypTen
+ * Beaver ring-GEMM hot path (arXiv 2109.00984).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * It shares no code, header, table or constant generator with the CUDA path
+ * (paper_2109_00984_b200/csrc); neither side includes or links the other.
+ *
+ * Every function simulates ALL |P| parties in one process.  Party-indexed
+ * buffers are laid out [P][n] (party-major, row-major inside each party).
+ * Arithmetic is in the ring Z/QZ with Q = 2^64 (§7 "the size of
+ * the ring, Q = 2^64"): uint64_t wrap-around IS the ring.  Signed
+ * representatives are int64_t two's complement (reading R9).
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n (section named beside
+ * it); "S:n" = SPEC.md line n; "§8(c) Ox" = the oracle step in SURVEY.md.
+ *
+ * Parity pins (tests/test_oracle_*.py): Philox KAT vectors, the frozen PRG
+ * table, numpy uint64 matmul, Python big-int brute force, the paper's own
+ * §4.3 float64 16-bit-block GEMM, the Beaver identity, the P=1 closed form,
+ * the Alg. 1 identity against big-int recomputation.  "Parity unpinned": only
+ * the *choice* of PRG layout (the paper allows any PRG); it is pinned
+ * to the frozen table in SURVEY.md Appendix A.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+
+typedef __int128 i128;
+
+#define ORACLE_OK 0
+#define ORACLE_ERR_ARG 1
+#define ORACLE_ERR_OVERFLOW 3
+
+/* ------------------------------------------------------------------------
+ * O1  PRG: Philox4x32-10 (Salmon et al., SC'11 "Random123").  The paper only
+ * asks for seeded pseudorandomness ("sync random seeds", Fig. 2;
+ * "pseudorandom zero-share", §4.1); the primitive and the counter layout
+ * are our reading R5, frozen in SURVEY.md §8(c) O1.
+ * ---------------------------------------------------------------------- */
+void oracle_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4])
+{
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int round = 0; round < 10; round++) {
+        if (round > 0) {            /* key schedule: Weyl sequence bump */
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        uint32_t n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* stream word = tag<<56 | party<<48 | (id mod 2^48)   (§8(c) O1) */
+uint64_t oracle_stream_id(uint32_t tag, uint32_t party, uint64_t id)
+{
+    return ((uint64_t)(tag & 0xFFu) << 56) | ((uint64_t)(party & 0xFFu) << 48)
+         | (id & 0xFFFFFFFFFFFFull);
+}
+
+/* G(key, stream)[start .. start+n): element 2j = o1*2^32 + o0, element
+ * 2j+1 = o3*2^32 + o2, where (o0..o3) = Philox(ctr = (lo(j), hi(j),
+ * lo(stream), hi(stream)), key = (lo(key), hi(key))).  One element at a
+ * time, no batching. */
+uint64_t oracle_prg_at(uint64_t key, uint64_t stream, uint64_t i)
+{
+    uint64_t j = i / 2;
+    uint32_t ctr[4] = { (uint32_t)j, (uint32_t)(j >> 32), (uint32_t)stream, (uint32_t)(stream >> 32) };
+    uint32_t k[2] = { (uint32_t)key, (uint32_t)(key >> 32) };
+    uint32_t o[4];
+    oracle_philox4x32_10(ctr, k, o);
+    if (i % 2 == 0) return ((uint64_t)o[1] << 32) | o[0];
+    return ((uint64_t)o[3] << 32) | o[2];
+}
+
+void oracle_prg(uint64_t key, uint64_t stream, uint64_t start, int64_t n, uint64_t* out)
+{
+    for (int64_t t = 0; t < n; t++) out[t] = oracle_prg_at(key, stream, start + (uint64_t)t);
+}
+
+/* Keys: k_p = G(master, 0xFF||p||0)[0] (party p's PRZS key),
+ *       k_ttp = G(master, 0xFE||0||0)[0].  Reproducibility convention only
+ * (§8(c) O1); a deployment agrees these pairwise at init. */
+void oracle_derive_keys(uint64_t master, int P, uint64_t* k_party, uint64_t* k_ttp)
+{
+    for (int p = 0; p < P; p++) k_party[p] = oracle_prg_at(master, oracle_stream_id(0xFF, (uint32_t)p, 0), 0);
+    *k_ttp = oracle_prg_at(master, oracle_stream_id(0xFE, 0, 0), 0);
+}
+
+enum { TAG_PRZS = 1, TAG_A = 2, TAG_B = 3, TAG_C = 4, TAG_R = 5, TAG_THETA = 6 };
+
+/* ------------------------------------------------------------------------
+ * O2  Fixed-point encode / decode (§4.1 "x = ⌊B x_R⌉, B = 2^L";
+ * P:563-567 App. A.1.1; default L = 16, §7).  Ties round half away
+ * from zero (reading R2); |x|·2^L ≥ 2^63 (or NaN) is an overflow error
+ * (reading R3).
+ * ---------------------------------------------------------------------- */
+int oracle_encode(const double* x, uint64_t* out, int64_t n, int frac_bits)
+{
+    const double scale = ldexp(1.0, frac_bits);
+    for (int64_t i = 0; i < n; i++) {
+        double v = x[i] * scale;                 /* exact: power-of-two scale */
+        if (!(fabs(v) < 9223372036854775808.0)) return ORACLE_ERR_OVERFLOW;   /* also NaN */
+        out[i] = (uint64_t)(int64_t)llround(v);   /* C99 llround: nearest, ties away from 0 */
+    }
+    return ORACLE_OK;
+}
+
+/* decode: x_R ≈ signed(x) / B */
+void oracle_decode(const uint64_t* v, double* out, int64_t n, int frac_bits)
+{
+    const double scale = ldexp(1.0, frac_bits);
+    for (int64_t i = 0; i < n; i++) out[i] = (double)(int64_t)v[i] / scale;
+}
+
+/* ------------------------------------------------------------------------
+ * O3  share via pseudorandom zero-share (§4.1: "the parties
+ * generate a pseudorandom zero-share with |P| random numbers that sum to 0.
+ * The party that possesses the value x adds x to their share").
+ * [x]_p[i] = G(k_p, PRZS||0||id)[i] − G(k_{p−1 mod P}, PRZS||0||id)[i]
+ *            + [p = src]·x[i]                                    (reading R4)
+ * ---------------------------------------------------------------------- */
+void oracle_share(int P, const uint64_t* k_party, const uint64_t* x, int src,
+                  uint64_t share_id, int64_t n, uint64_t* shares)
+{
+    uint64_t stream = oracle_stream_id(TAG_PRZS, 0, share_id);
+    for (int p = 0; p < P; p++) {
+        int prev = (p + P - 1) % P;
+        for (int64_t i = 0; i < n; i++) {
+            uint64_t v = oracle_prg_at(k_party[p], stream, (uint64_t)i)
+                       - oracle_prg_at(k_party[prev], stream, (uint64_t)i);
+            if (p == src && x != NULL) v += x[i];
+            shares[(int64_t)p * n + i] = v;
+        }
+    }
+}
+
+/* O8  reveal: x = Σ_p [x]_p mod Q (§4.1; Fig. 2) */
+void oracle_reveal(int P, const uint64_t* shares, int64_t n, uint64_t* out)
+{
+    for (int64_t i = 0; i < n; i++) {
+        uint64_t s = 0;
+        for (int p = 0; p < P; p++) s += shares[(int64_t)p * n + i];
+        out[i] = s;
+    }
+}
+
+/* ------------------------------------------------------------------------
+ * Ring GEMM: C = A @ B mod 2^64, A: M×K, B: K×N, row-major.  The textbook
+ * triple loop (i, k, j) with wrapping uint64 multiply-add — the definition
+ * of a matrix product in Z/2^64Z.  (The paper computes it with float64
+ * blocks, §4.3; that route is a *test* cross-check here.)
+ * OpenMP over rows only; each output element is summed in index order.
+ * ---------------------------------------------------------------------- */
+void oracle_ring_matmul(const uint64_t* A, const uint64_t* B, uint64_t* C,
+                        int64_t M, int64_t K, int64_t N)
+{
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < M; i++) {
+        uint64_t* c = C + i * N;
+        for (int64_t j = 0; j < N; j++) c[j] = 0;
+        for (int64_t k = 0; k < K; k++) {
+            uint64_t a = A[i * K + k];
+            const uint64_t* b = B + k * N;
+            for (int64_t j = 0; j < N; j++) c[j] += a * b[j];
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------
+ * O4  TTP Beaver triple for f = matmul (§3 TTP footnote; P:200-201
+ * §4.2; App. A.1.1 "generated in an offline preprocessing phase";
+ * "holds for any linear function f ... matrix multiplication").
+ *   a_p = G(k_ttp, A||p||id), b_p = G(k_ttp, B||p||id) (uniform)
+ *   c   = (Σ_p a_p) @ (Σ_p b_p)
+ *   c_p = G(k_ttp, C||p||id) for p ≥ 1, c_0 = c − Σ_{p≥1} c_p  (reading R6)
+ * rows != NULL selects a subset of the M rows of a and c (same values as
+ * the full triple's rows; b is always full).  a: [P][nrows*K], c: [P][nrows*N].
+ * ---------------------------------------------------------------------- */
+void oracle_ttp_triple(int P, uint64_t k_ttp, uint64_t triple_id,
+                       int64_t M, int64_t K, int64_t N,
+                       const int64_t* rows, int64_t nrows,
+                       uint64_t* a, uint64_t* b, uint64_t* c)
+{
+    if (rows == NULL) nrows = M;
+    for (int p = 0; p < P; p++) {
+        uint64_t sa = oracle_stream_id(TAG_A, (uint32_t)p, triple_id);
+        uint64_t sb = oracle_stream_id(TAG_B, (uint32_t)p, triple_id);
+        for (int64_t r = 0; r < nrows; r++) {
+            int64_t i = rows ? rows[r] : r;
+            oracle_prg(k_ttp, sa, (uint64_t)(i * K), K, a + (int64_t)p * nrows * K + r * K);
+        }
+        oracle_prg(k_ttp, sb, 0, K * N, b + (int64_t)p * K * N);
+    }
+    uint64_t* asum = (uint64_t*)calloc((size_t)(nrows * K > 0 ? nrows * K : 1), 8);
+    uint64_t* bsum = (uint64_t*)calloc((size_t)(K * N > 0 ? K * N : 1), 8);
+    uint64_t* cfull = (uint64_t*)calloc((size_t)(nrows * N > 0 ? nrows * N : 1), 8);
+    oracle_reveal(P, a, nrows * K, asum);
+    oracle_reveal(P, b, K * N, bsum);
+    oracle_ring_matmul(asum, bsum, cfull, nrows, K, N);
+    for (int64_t r = 0; r < nrows * N; r++) c[r] = cfull[r];
+    for (int p = 1; p < P; p++) {
+        uint64_t sc = oracle_stream_id(TAG_C, (uint32_t)p, triple_id);
+        for (int64_t r = 0; r < nrows; r++) {
+            int64_t i = rows ? rows[r] : r;
+            uint64_t* cp = c + (int64_t)p * nrows * N + r * N;
+            oracle_prg(k_ttp, sc, (uint64_t)(i * N), N, cp);
+            for (int64_t j = 0; j < N; j++) c[r * N + j] -= cp[j];   /* c_0 −= c_p */
+        }
+    }
+    free(asum); free(bsum); free(cfull);
+}
+
+/* ------------------------------------------------------------------------
+ * O5  Beaver private matmul (§4.2; App. A.1.1):
+ *   [ε]_p = [x]_p − [a]_p,  [δ]_p = [y]_p − [b]_p
+ *   ε = Σ_p [ε]_p,  δ = Σ_p [δ]_p   ("decrypt ε and δ", one round)
+ *   [z]_p = [c]_p + ε@[b]_p + [a]_p@δ + [p = 0]·ε@δ        (
+ *           readings R7, R8: party 0 adds the public ε@δ; operand order
+ *           ε@b and a@δ for the non-commutative matmul)
+ * No truncation here (z is at scale 2^(2f)); see O6/O7.
+ * x: [P][M*K], y: [P][K*N], a: [P][M*K], b: [P][K*N], c: [P][M*N].
+ * eps_out (M*K), delta_out (K*N), e_out/d_out ([P][..]) may be NULL.
+ * ---------------------------------------------------------------------- */
+void oracle_beaver_matmul(int P, const uint64_t* x, const uint64_t* y,
+                          const uint64_t* a, const uint64_t* b, const uint64_t* c,
+                          int64_t M, int64_t K, int64_t N,
+                          uint64_t* e_out, uint64_t* d_out,
+                          uint64_t* eps_out, uint64_t* delta_out, uint64_t* z)
+{
+    int64_t nx = M * K, ny = K * N, nz = M * N;
+    uint64_t* e = (uint64_t*)malloc((size_t)(P * (nx > 0 ? nx : 1)) * 8);
+    uint64_t* d = (uint64_t*)malloc((size_t)(P * (ny > 0 ? ny : 1)) * 8);
+    uint64_t* eps = (uint64_t*)malloc((size_t)(nx > 0 ? nx : 1) * 8);
+    uint64_t* delta = (uint64_t*)malloc((size_t)(ny > 0 ? ny : 1) * 8);
+    uint64_t* t = (uint64_t*)malloc((size_t)(nz > 0 ? nz : 1) * 8);
+    for (int p = 0; p < P; p++) {
+        for (int64_t i = 0; i < nx; i++) e[p * nx + i] = x[p * nx + i] - a[p * nx + i];
+        for (int64_t i = 0; i < ny; i++) d[p * ny + i] = y[p * ny + i] - b[p * ny + i];
+    }
+    oracle_reveal(P, e, nx, eps);
+    oracle_reveal(P, d, ny, delta);
+    for (int p = 0; p < P; p++) {
+        uint64_t* zp = z + (int64_t)p * nz;
+        for (int64_t i = 0; i < nz; i++) zp[i] = c[p * nz + i];
+        oracle_ring_matmul(eps, b + (int64_t)p * ny, t, M, K, N);        /* ε@[b]_p */
+        for (int64_t i = 0; i < nz; i++) zp[i] += t[i];
+        oracle_ring_matmul(a + (int64_t)p * nx, delta, t, M, K, N);      /* [a]_p@δ */
+        for (int64_t i = 0; i < nz; i++) zp[i] += t[i];
+        if (p == 0) {
+            oracle_ring_matmul(eps, delta, t, M, K, N);                  /* ε@δ, party 0 */
+            for (int64_t i = 0; i < nz; i++) zp[i] += t[i];
+        }
+    }
+    if (e_out) memcpy(e_out, e, (size_t)(P * nx) * 8);
+    if (d_out) memcpy(d_out, d, (size_t)(P * ny) * 8);
+    if (eps_out) memcpy(eps_out, eps, (size_t)nx * 8);
+    if (delta_out) memcpy(delta_out, delta, (size_t)ny * 8);
+    free(e); free(d); free(eps); free(delta); free(t);
+}
+
+/* ------------------------------------------------------------------------
+ * Per-share division by ℓ = 2^bits with round-half-up on the signed
+ * representative: (signed(v) >> bits) + bit_{bits−1}(v)   (reading R10).
+ * Arithmetic right shift of int64 written out as floor division.
+ * ---------------------------------------------------------------------- */
+static uint64_t div_pow2_round(uint64_t v, int bits)
+{
+    if (bits == 0) return v;
+    int64_t s = (int64_t)v;
+    int64_t q;
+    int64_t den = (int64_t)1 << bits;
+    /* floor(s / 2^bits) */
+    q = s / den;
+    if ((s % den) != 0 && s < 0) q -= 1;
+    uint64_t half = (v >> (bits - 1)) & 1u;
+    return (uint64_t)q + half;
+}
+
+/* O6  truncation, P ≤ 2: "divide the share of each party by ℓ" (P:597
+ * App. A.1.1 Truncation); 0 rounds at P = 2 (Table 3 footnote).
+ * Fails with probability |x|/Q; see oracle_wrap_count. */
+int oracle_truncate_local(int P, const uint64_t* x, int64_t n, int bits, uint64_t* out)
+{
+    if (bits < 0 || bits > 62 || P < 1) return ORACLE_ERR_ARG;
+    for (int64_t i = 0; i < (int64_t)P * n; i++) out[i] = div_pow2_round(x[i], bits);
+    return ORACLE_OK;
+}
+
+/* θ_x = (Σ_p signed([x]_p) − signed(x)) / Q, exact in 128-bit
+ * (definition: x = Σ_p [x]_p − θ_x Q; signed reps, R9). */
+void oracle_wrap_count(int P, const uint64_t* x, int64_t n, int64_t* theta)
+{
+    for (int64_t i = 0; i < n; i++) {
+        i128 s = 0;
+        uint64_t u = 0;
+        for (int p = 0; p < P; p++) { s += (i128)(int64_t)x[(int64_t)p * n + i]; u += x[(int64_t)p * n + i]; }
+        i128 diff = s - (i128)(int64_t)u;
+        theta[i] = (int64_t)(diff >> 64);      /* diff is an exact multiple of 2^64 */
+    }
+}
+
+/* Wrap pair for Alg. 1 (inputs "secret shared random value [r] and its wrap
+ * count"):  r_p = G(k_ttp, R||p||id);
+ *   θ_r = (Σ_p signed(r_p) − signed(Σ_p r_p)) / Q;
+ *   [θ_r]_p = G(k_ttp, THETA||p||id) for p ≥ 1, [θ_r]_0 = θ_r − Σ_{p≥1}[θ_r]_p. */
+void oracle_wrap_pair(int P, uint64_t k_ttp, uint64_t wrap_id, int64_t n,
+                      uint64_t* r, uint64_t* theta_r)
+{
+    for (int p = 0; p < P; p++)
+        oracle_prg(k_ttp, oracle_stream_id(TAG_R, (uint32_t)p, wrap_id), 0, n, r + (int64_t)p * n);
+    int64_t* th = (int64_t*)malloc((size_t)(n > 0 ? n : 1) * 8);
+    oracle_wrap_count(P, r, n, th);
+    for (int64_t i = 0; i < n; i++) theta_r[i] = (uint64_t)th[i];
+    for (int p = 1; p < P; p++) {
+        oracle_prg(k_ttp, oracle_stream_id(TAG_THETA, (uint32_t)p, wrap_id), 0, n, theta_r + (int64_t)p * n);
+        for (int64_t i = 0; i < n; i++) theta_r[i] -= theta_r[(int64_t)p * n + i];
+    }
+    free(th);
+}
+
+/* ------------------------------------------------------------------------
+ * O7  truncation for P > 2 by Algorithm 1 and the correction
+ * x/ℓ = [y] − [θ_x]·Q/ℓ, with η_xr skipped:
+ *   [z]_p = [x]_p + [r]_p
+ *   [β]_p = (signed([x]_p) + signed([r]_p) − signed([z]_p)) / Q
+ *   z = reveal([z]);   θ_z = (Σ_p signed([z]_p) − signed(z)) / Q
+ *   [θ_x]_p = [β]_p − [θ_r]_p + [p=0]·θ_z          (η := 0)
+ *   out_p = div_round([x]_p, ℓ) − [θ_x]_p · 2^(64−bits)
+ * Diagnostics (may be NULL): z_out (revealed z), eta_out (η_xr = wraps of
+ * the plaintexts x + r, i.e. (signed(x)+signed(r)−signed(z))/Q — the term
+ * the paper skips; η ≠ 0 marks a possible failure event).
+ * ---------------------------------------------------------------------- */
+int oracle_truncate_alg1(int P, const uint64_t* x, const uint64_t* r, const uint64_t* theta_r,
+                         int64_t n, int bits, uint64_t* out, uint64_t* z_out, int64_t* eta_out)
+{
+    if (bits < 1 || bits > 62 || P < 1) return ORACLE_ERR_ARG;
+    uint64_t* zs = (uint64_t*)malloc((size_t)(P * (n > 0 ? n : 1)) * 8);
+    uint64_t* beta = (uint64_t*)malloc((size_t)(P * (n > 0 ? n : 1)) * 8);
+    int64_t* theta_z = (int64_t*)malloc((size_t)(n > 0 ? n : 1) * 8);
+    uint64_t* z = (uint64_t*)malloc((size_t)(n > 0 ? n : 1) * 8);
+    for (int64_t i = 0; i < (int64_t)P * n; i++) {
+        zs[i] = x[i] + r[i];
+        i128 s = (i128)(int64_t)x[i] + (i128)(int64_t)r[i] - (i128)(int64_t)zs[i];
+        beta[i] = (uint64_t)(int64_t)(s >> 64);
+    }
+    oracle_reveal(P, zs, n, z);
+    oracle_wrap_count(P, zs, n, theta_z);
+    for (int p = 0; p < P; p++) {
+        for (int64_t i = 0; i < n; i++) {
+            int64_t k = (int64_t)p * n + i;
+            uint64_t th = beta[k] - theta_r[k] + (p == 0 ? (uint64_t)theta_z[i] : 0u);
+            out[k] = div_pow2_round(x[k], bits) - th * ((uint64_t)1 << (64 - bits));
+        }
+    }
+    if (z_out) memcpy(z_out, z, (size_t)n * 8);
+    if (eta_out) {
+        uint64_t* xs = (uint64_t*)malloc((size_t)(n > 0 ? n : 1) * 8);
+        uint64_t* rs = (uint64_t*)malloc((size_t)(n > 0 ? n : 1) * 8);
+        oracle_reveal(P, x, n, xs);
+        oracle_reveal(P, r, n, rs);
+        for (int64_t i = 0; i < n; i++) {
+            i128 s = (i128)(int64_t)xs[i] + (i128)(int64_t)rs[i] - (i128)(int64_t)z[i];
+            eta_out[i] = (int64_t)(s >> 64);
+        }
+        free(xs); free(rs);
+    }
+    free(zs); free(beta); free(theta_z); free(z);
+    return ORACLE_OK;
+}

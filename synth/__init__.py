@@ -1,0 +1,70 @@
+"""Seeded synthetic workloads shared by the oracle tests, the GPU parity tests and bench.py.
+
+This module holds NONE of the method's arithmetic (no sharing, no PRG, no ring
+GEMM): it only draws plaintext fixed-point inputs with numpy's seeded
+generator and lists the paper's layer shapes.  Recipe: DESIGN.md §"Input
+recipe".
+"""
+from __future__ import annotations
+
+import numpy as np
+
+MASTER_SEED = 210900984          # §8(d): master seed of every config
+FRAC_BITS = 16                   # P:244 §7 "L = 16 by default"
+
+
+def to_ring(v_int: np.ndarray) -> np.ndarray:
+    """Two's-complement view of signed integers as ring elements (uint64)."""
+    return np.ascontiguousarray(np.asarray(v_int, dtype=np.int64).view(np.uint64))
+
+
+def uniform_fixed(shape, seed: int, bound: float = 8.0, frac_bits: int = FRAC_BITS) -> np.ndarray:
+    """Integer fixed-point values U{-bound*2^f .. bound*2^f} as uint64 (configs C1/C2/C5)."""
+    rng = np.random.default_rng(seed)
+    lim = int(bound * (1 << frac_bits))
+    return to_ring(rng.integers(-lim, lim + 1, size=shape, dtype=np.int64))
+
+
+def gaussian_fixed(shape, seed: int, std: float, lo: float, hi: float, absval: bool = False,
+                   frac_bits: int = FRAC_BITS) -> np.ndarray:
+    """Clipped Gaussian values already on the 2^-f grid (configs C3/C4)."""
+    rng = np.random.default_rng(seed)
+    v = rng.standard_normal(size=shape) * std
+    if absval:
+        v = np.abs(v)
+    v = np.clip(v, lo, hi)
+    return to_ring(np.rint(v * (1 << frac_bits)).astype(np.int64))
+
+
+def uniform_ring(shape, seed: int) -> np.ndarray:
+    """Full-range uniform ring elements (edge/stress cases)."""
+    rng = np.random.default_rng(seed)
+    return rng.integers(0, 2**64 - 1, size=shape, dtype=np.uint64, endpoint=True)
+
+
+# --- layer shapes (M, K, N, count), SURVEY.md §8(d) C3/C4 -----------------
+RESNET50_B1 = [
+    ("conv1", 12544, 147, 64, 1),
+    ("l1.c1", 3136, 64, 64, 1), ("l1.c2", 3136, 576, 64, 3), ("l1.c3", 3136, 64, 256, 4),
+    ("l1.c1b", 3136, 256, 64, 2),
+    ("l2.c1", 3136, 256, 128, 1), ("l2.c2", 784, 1152, 128, 4), ("l2.c3", 784, 128, 512, 4),
+    ("l2.ds", 784, 256, 512, 1), ("l2.c1b", 784, 512, 128, 3),
+    ("l3.c1", 784, 512, 256, 1), ("l3.c2", 196, 2304, 256, 6), ("l3.c3", 196, 256, 1024, 6),
+    ("l3.ds", 196, 512, 1024, 1), ("l3.c1b", 196, 1024, 256, 5),
+    ("l4.c1", 196, 1024, 512, 1), ("l4.c2", 49, 4608, 512, 3), ("l4.c3", 49, 512, 2048, 3),
+    ("l4.ds", 49, 1024, 2048, 1), ("l4.c1b", 49, 2048, 512, 2),
+    ("fc", 1, 2048, 1000, 1),
+]
+
+VIT_B16 = [
+    ("patch_embed", 196, 768, 768, 1),
+    ("qkv", 197, 768, 2304, 12), ("proj", 197, 768, 768, 12),
+    ("fc1", 197, 768, 3072, 12), ("fc2", 197, 3072, 768, 12),
+    ("head", 1, 768, 1000, 1),
+]
+
+CONFIGS = {
+    "C1": dict(M=64, K=64, N=64, P=2, seed=1001),
+    "C2": dict(M=4096, K=4096, N=4096, P=2, seed=1002),
+    "C5": dict(M=8192, K=8192, N=8192, P=8, seed=1005),
+}
