@@ -1,0 +1,173 @@
+/*
+ * mpc_ring.h — C-ABI of the B200-native Beaver ring-GEMM library
+ * (libmpc_ring.so, built from paper_2109_00984_b200/csrc).
+ *
+ * What it computes: the arithmetic-secret-sharing hot path of CrypTen
+ * (arXiv 2109.00984), in the ring Z/QZ with Q = 2^64 (§7) and
+ * fixed-point scale 2^f, f = 16 by default (PAPER.md:176-177 §4.1, :244 §7).
+ * "P:n" below cites /root/reference/PAPER.md line n; DESIGN.md lists every
+ * reading (R1..R19) taken where the paper is silent.
+ *
+ * Conventions shared by every entry point
+ * ----------------------------------------
+ * Memory.   Every tensor argument is a caller-owned CUDA DEVICE buffer on the
+ *           context's device (torch tensors in practice), row-major, 8-byte
+ *           aligned; ring elements are little-endian uint64.  The library never
+ *           allocates or frees caller memory.  Work buffers are passed in as
+ *           `workspace` (size from mpc_workspace_bytes / mpc_ttp_workspace_bytes,
+ *           256-byte aligned).
+ * Parties.  A context is either
+ *             - one party of P (rank in [0, P)): one process and one GPU per
+ *               party, reveals are NCCL sum-allreduces (P:64, P:72 footnote,
+ *               P:377-378); every share argument is that party's share, or
+ *             - all P parties on one device (rank == MPC_ALL_PARTIES): every
+ *               share argument is P contiguous party buffers, layout [P][n];
+ *               reveals are local sums.  Bit-identical results either way.
+ * Streams.  All calls are asynchronous and stream-ordered on the stream set by
+ *           mpc_set_stream (default: the legacy default stream).  Outputs are
+ *           valid once that stream has synchronised.
+ * Errors.   Every call returns an mpc_status and never throws across the ABI.
+ *           Argument / shape / overflow errors are detected on the host before
+ *           any launch and leave outputs untouched.  CUDA / NCCL failures return
+ *           MPC_ERR_CUDA / MPC_ERR_NCCL; the message is in mpc_last_error().  After
+ *           a failed collective the context is in MPC_ERR_STATE: only
+ *           mpc_destroy is allowed.
+ * Rounds.   mpc_stats counts communication rounds (Table 3): reveal = 1,
+ *           beaver_matmul = 1, truncation = 0 for P <= 2 and 1 for P > 2.
+ * Ids.      share_id / triple_id / wrap_id are caller-chosen 48-bit ids that select
+ *           PRG streams (R5): equal seeds and ids give bit-identical
+ *           shares.  Triples and wrap pairs are single-use.
+ */
+#ifndef MPC_RING_H
+#define MPC_RING_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mpc_ctx_s* mpc_ctx;               /* opaque, library-owned */
+
+typedef enum {
+    MPC_OK = 0,
+    MPC_ERR_ARG = 1,          /* bad pointer / enum / id / rank */
+    MPC_ERR_SHAPE = 2,        /* negative or inconsistent sizes, workspace too small */
+    MPC_ERR_OVERFLOW = 3,     /* encode: |x| * 2^f >= 2^63 or NaN (R3) */
+    MPC_ERR_CUDA = 4,
+    MPC_ERR_NCCL = 5,
+    MPC_ERR_STATE = 6,        /* context unusable after an earlier collective failure */
+    MPC_ERR_UNSUPPORTED = 7   /* no sm_100a device, or a mode this build does not have */
+} mpc_status;
+
+#define MPC_ALL_PARTIES (-1)
+
+/* ---- context ------------------------------------------------------------
+ * world_size P in [1, 16]; rank in [0, P) or MPC_ALL_PARTIES.  nccl_id: the
+ * 128-byte ncclUniqueId created by rank 0 (mpc_nccl_unique_id) and broadcast by
+ * the caller (through torch.distributed); ignored when rank == MPC_ALL_PARTIES or
+ * P == 1.  NULL with one party of P > 1 creates a context WITHOUT a communicator:
+ * the local steps (share, ttp_triples, ttp_wrap_pairs, encode/decode, local
+ * truncation) work, every call that needs a reveal returns MPC_ERR_STATE.
+ * master_seed: every PRZS / TTP key is derived from it (R5; "sync random
+ * seeds").  frac_bits f in [1, 30] (default 16).  Fails with
+ * MPC_ERR_UNSUPPORTED if `device` is not a compute-capability 10.0 GPU. */
+mpc_status mpc_create(mpc_ctx* out, int world_size, int rank, int device,
+                      const void* nccl_id, uint64_t master_seed, int frac_bits);
+mpc_status mpc_destroy(mpc_ctx ctx);
+mpc_status mpc_set_stream(mpc_ctx ctx, void* cuda_stream);
+const char* mpc_last_error(mpc_ctx ctx);      /* never NULL; valid until the next call on ctx */
+/* rounds and bytes SENT by this process's party/parties since creation (R19) */
+mpc_status mpc_stats(mpc_ctx ctx, uint64_t* rounds, uint64_t* bytes_sent);
+/* 1 if ctx is one party per GPU, 0 if all parties share this device */
+int mpc_world_size(mpc_ctx ctx);
+int mpc_rank(mpc_ctx ctx);
+/* Writes a fresh 128-byte ncclUniqueId (rank 0 calls this, then broadcasts it to
+ * the other parties before mpc_create).  MPC_ERR_NCCL on failure. */
+mpc_status mpc_nccl_unique_id(void* out128);
+
+/* ---- fixed point (§4.1; App. A.1.1) ----------------
+ * encode: out[i] = round_half_away(x[i] * 2^f) as two's complement u64;
+ *   MPC_ERR_OVERFLOW if any |x[i]| * 2^f >= 2^63 or NaN (checked on the device;
+ *   the call synchronises the stream to report it).  Public values, not shares.
+ * decode: out[i] = (double)(int64)v[i] / 2^f. */
+mpc_status mpc_encode(mpc_ctx ctx, const double* x, uint64_t* out, int64_t n);
+mpc_status mpc_decode(mpc_ctx ctx, const uint64_t* v, double* out, int64_t n);
+
+/* ---- share: pseudorandom zero-share + src adds x (§4.1) ------
+ * [x]_p[i] = G(k_p, PRZS||0||share_id)[i] - G(k_{p-1 mod P}, PRZS||0||share_id)[i]
+ *            + [p == src] * x[i]                                     (0 rounds)
+ * x_or_null: n ring elements held by party `src` (read only by src; NULL allowed for
+ * other ranks).  share_out: n (one party) or [P][n] (all parties). */
+mpc_status mpc_share(mpc_ctx ctx, const uint64_t* x_or_null, int src, uint64_t share_id,
+                     uint64_t* share_out, int64_t n);
+
+/* ---- reveal: x = sum_p [x]_p mod 2^64 (Fig. 2) -------
+ * share: n or [P][n]; out: n.  1 round (NCCL uint64 sum-allreduce), 8n bytes sent. */
+mpc_status mpc_reveal(mpc_ctx ctx, const uint64_t* share, uint64_t* out, int64_t n);
+
+/* ---- offline TTP: Beaver matmul triple -----
+ * a_p = G(k_ttp, A||p||id) (M x K), b_p = G(k_ttp, B||p||id) (K x N),
+ * c = (sum a_p) @ (sum b_p) mod 2^64 computed by the ring GEMM, c_p = G(k_ttp, C||p||id)
+ * for p >= 1, c_0 = c - sum_{p>=1} c_p  (R6).  a, b, c: this party's
+ * (or [P][..] for all parties).  In the one-party-per-GPU mode rank 0 also acts as the
+ * TTP and regenerates every party's a_q, b_q to form c_0.  workspace: at least
+ * mpc_ttp_workspace_bytes(ctx, M, K, N) bytes (only rank 0 / all-parties use it). */
+size_t mpc_ttp_workspace_bytes(mpc_ctx ctx, int64_t M, int64_t K, int64_t N);
+mpc_status mpc_ttp_triples(mpc_ctx ctx, uint64_t triple_id, int64_t M, int64_t K, int64_t N,
+                           uint64_t* a, uint64_t* b, uint64_t* c,
+                           void* workspace, size_t workspace_bytes);
+
+/* ---- offline TTP: wrap pair for Alg. 1 (DESIGN.md a9) ---------
+ * r_p = G(k_ttp, R||p||id); theta_r = (sum signed(r_p) - signed(sum r_p)) / 2^64;
+ * [theta_r]_p = G(k_ttp, THETA||p||id) for p >= 1, [theta_r]_0 = theta_r - sum_{p>=1}.
+ * mpc_truncate regenerates exactly these values from wrap_id; this entry point
+ * materialises them (tests, inspection). */
+mpc_status mpc_ttp_wrap_pairs(mpc_ctx ctx, uint64_t wrap_id, int64_t n,
+                              uint64_t* r, uint64_t* theta_r);
+
+/* ---- Beaver private matmul (§4.2; App. A.1.1) -------
+ * e_p = x_p - a_p, d_p = y_p - b_p; eps = sum e_p, delta = sum d_p (one round);
+ * z_p = c_p + eps @ b_p + a_p @ delta + [p == 0] eps @ delta  (R7, R8),
+ * then, if truncate != 0, fixed-point truncation by 2^f: local
+ * per-share round-half-up division for P <= 2 (P:597, 0 rounds), Alg. 1
+ * with eta skipped for P > 2 (P:606-663, 1 more round) using wrap pair wrap_id.
+ * x: M x K, y: K x N, a: M x K, b: K x N, c and z: M x N (per party, or [P][..]).
+ * z may not alias any input.  workspace >= mpc_workspace_bytes(ctx, M, K, N).
+ * The ring GEMM is the tcgen05 u8-limb kernel (36 limb pairs). */
+size_t mpc_workspace_bytes(mpc_ctx ctx, int64_t M, int64_t K, int64_t N);
+mpc_status mpc_beaver_matmul(mpc_ctx ctx, const uint64_t* x, const uint64_t* y,
+                             const uint64_t* a, const uint64_t* b, const uint64_t* c,
+                             uint64_t* z, int64_t M, int64_t K, int64_t N,
+                             int truncate, uint64_t wrap_id,
+                             void* workspace, size_t workspace_bytes);
+
+/* ---- truncation by 2^bits (App. A.1.1 "Truncation") ----------
+ * In place on x (n or [P][n]).  bits in [1, 62].  P <= 2: out_p =
+ * (signed(x_p) >> bits) + bit_{bits-1}(x_p) (0 rounds).  P > 2: Alg. 1 with the wrap
+ * pair wrap_id, eta skipped (1 round). */
+mpc_status mpc_truncate(mpc_ctx ctx, uint64_t* x_inout, int64_t n, int bits, uint64_t wrap_id);
+
+/* ---- plain ring GEMM C = A @ B mod 2^64 (building block of ttp_triples) ---
+ * A: M x K, B: K x N, C: M x N, device buffers; not a protocol step (no shares).
+ * workspace >= mpc_ring_matmul_workspace_bytes(M, K, N). */
+size_t mpc_ring_matmul_workspace_bytes(int64_t M, int64_t K, int64_t N);
+mpc_status mpc_ring_matmul(mpc_ctx ctx, const uint64_t* A, const uint64_t* B, uint64_t* C,
+                           int64_t M, int64_t K, int64_t N, void* workspace, size_t workspace_bytes);
+
+/* ---- measurement hooks (bench.py) ----------------------------------------
+ * When enabled, the library brackets every launch of kernel class `cls` with CUDA
+ * events on the launching stream and accumulates its device time.
+ * cls: 0 = ring GEMM (tcgen05), 1 = limb split / mask / local reveal,
+ *      2 = truncation, 3 = PRG (share / triples / wrap pairs), 4 = encode/decode,
+ *      5 = collectives (NCCL).  mpc_profile_read synchronises the stream.
+ * mpc_launch_count: number of the library's own kernel launches since creation. */
+mpc_status mpc_profile_enable(mpc_ctx ctx, int enable);
+mpc_status mpc_profile_read(mpc_ctx ctx, int cls, double* total_ms, uint64_t* launches);
+uint64_t mpc_launch_count(mpc_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPC_RING_H */

@@ -116,13 +116,15 @@ def decode(v, frac_bits: int = 16) -> np.ndarray:
 
 
 # ---------------------------------------------------------------- O3 / O8
-def share(P: int, master: int, x, src: int, share_id: int) -> np.ndarray:
-    """PRZS shares of the src party's ring tensor x: array (P, *x.shape)."""
+def share(P: int, master: int, x, src: int, share_id: int, start: int = 0) -> np.ndarray:
+    """PRZS shares of the src party's ring tensor x: array (P, *x.shape).
+    start > 0: x holds elements [start, start + x.size) of a larger tensor."""
     x = _u64(x)
     kp, _ = derive_keys(master, P)
     kp = np.ascontiguousarray(kp)
     out = np.zeros((P,) + x.shape, dtype=np.uint64)
-    lib().oracle_share(P, _p(kp), _p(x), src, ctypes.c_uint64(share_id), ctypes.c_int64(x.size), _p(out))
+    lib().oracle_share_range(P, _p(kp), _p(x), src, ctypes.c_uint64(share_id), ctypes.c_int64(start),
+                             ctypes.c_int64(x.size), _p(out))
     return out
 
 

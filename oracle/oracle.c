@@ -131,19 +131,26 @@ void oracle_decode(const uint64_t* v, double* out, int64_t n, int frac_bits)
  * [x]_p[i] = G(k_p, PRZS||0||id)[i] − G(k_{p−1 mod P}, PRZS||0||id)[i]
  *            + [p = src]·x[i]                                    (reading R4)
  * ---------------------------------------------------------------------- */
-void oracle_share(int P, const uint64_t* k_party, const uint64_t* x, int src,
-                  uint64_t share_id, int64_t n, uint64_t* shares)
+/* elements [start, start+n) of the shared tensor (start > 0: a row sample) */
+void oracle_share_range(int P, const uint64_t* k_party, const uint64_t* x, int src,
+                        uint64_t share_id, int64_t start, int64_t n, uint64_t* shares)
 {
     uint64_t stream = oracle_stream_id(TAG_PRZS, 0, share_id);
     for (int p = 0; p < P; p++) {
         int prev = (p + P - 1) % P;
         for (int64_t i = 0; i < n; i++) {
-            uint64_t v = oracle_prg_at(k_party[p], stream, (uint64_t)i)
-                       - oracle_prg_at(k_party[prev], stream, (uint64_t)i);
+            uint64_t v = oracle_prg_at(k_party[p], stream, (uint64_t)(start + i))
+                       - oracle_prg_at(k_party[prev], stream, (uint64_t)(start + i));
             if (p == src && x != NULL) v += x[i];
             shares[(int64_t)p * n + i] = v;
         }
     }
+}
+
+void oracle_share(int P, const uint64_t* k_party, const uint64_t* x, int src,
+                  uint64_t share_id, int64_t n, uint64_t* shares)
+{
+    oracle_share_range(P, k_party, x, src, share_id, 0, n, shares);
 }
 
 /* O8  reveal: x = Σ_p [x]_p mod Q (§4.1; Fig. 2) */

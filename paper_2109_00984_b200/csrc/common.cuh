@@ -1,0 +1,111 @@
+// common.cuh — device-side building blocks of libmpc_ring.so (sm_100a only).
+//
+// Shares nothing with oracle/ (the CPU oracle is independent test
+// infrastructure).  Citations: "P:n" = PAPER.md line n; "R#" = a reading
+// listed in DESIGN.md.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "libmpc_ring targets sm_100a only (compile with -gencode arch=compute_100a,code=sm_100a)"
+#endif
+
+namespace mpc {
+
+// ---------------------------------------------------------------- PRG (R5)
+// Philox4x32-10 (Random123).  G(key, stream)[i]: counter (lo(i/2), hi(i/2),
+// lo(stream), hi(stream)), key (lo(key), hi(key)); element 2j = o1<<32|o0,
+// element 2j+1 = o3<<32|o2.  stream = tag<<56 | party<<48 | id (48 bits).
+enum : uint32_t { kTagPRZS = 1, kTagA = 2, kTagB = 3, kTagC = 4, kTagR = 5, kTagTheta = 6,
+                  kTagKeyParty = 0xFF, kTagKeyTTP = 0xFE };
+
+__host__ __device__ __forceinline__ uint64_t stream_word(uint32_t tag, uint32_t party, uint64_t id) {
+    return ((uint64_t)(tag & 0xFFu) << 56) | ((uint64_t)(party & 0xFFu) << 48) | (id & 0xFFFFFFFFFFFFull);
+}
+
+__host__ __device__ __forceinline__ void philox_pair(uint64_t key, uint64_t stream, uint64_t j,
+                                                     uint64_t& e0, uint64_t& e1) {
+    uint32_t c0 = (uint32_t)j, c1 = (uint32_t)(j >> 32), c2 = (uint32_t)stream, c3 = (uint32_t)(stream >> 32);
+    uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+#ifdef __CUDA_ARCH__
+        uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+        uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+#else
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0, hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+#endif
+        uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+    e0 = ((uint64_t)c1 << 32) | c0;
+    e1 = ((uint64_t)c3 << 32) | c2;
+}
+
+__host__ __device__ __forceinline__ uint64_t philox_at(uint64_t key, uint64_t stream, uint64_t i) {
+    uint64_t e0, e1;
+    philox_pair(key, stream, i >> 1, e0, e1);
+    return (i & 1) ? e1 : e0;
+}
+
+// ------------------------------------------------------- limb-plane layout
+// A u64 operand with R rows (M for left operands, N for right operands) and
+// reduction length K is stored as 8 u8 planes (plane l = byte l of every
+// element), K-major, tiled so that one (128-row tile, 32-K block) of all 8
+// planes is 8 contiguous 4 KiB blocks, each already in the UMMA canonical
+// K-major SWIZZLE_NONE layout: [row/8][k/16][row%8][k%16] (core matrices of
+// 8 rows x 16 B; LBO = 128 B between the two K halves, SBO = 256 B between
+// 8-row groups).  Zero padding to 128 rows / 32 K.
+constexpr int kRowTile = 128;
+constexpr int kKBlock = 32;
+constexpr int kPlaneTileBytes = kRowTile * kKBlock;     // 4096
+
+__host__ __device__ __forceinline__ int64_t pad_rows(int64_t r) { return (r + kRowTile - 1) / kRowTile * kRowTile; }
+__host__ __device__ __forceinline__ int64_t num_kb(int64_t k) { return (k + kKBlock - 1) / kKBlock; }
+__host__ __device__ __forceinline__ int64_t planes_bytes(int64_t rows, int64_t k) {
+    return pad_rows(rows) * num_kb(k) * kKBlock * 8;
+}
+__host__ __device__ __forceinline__ int64_t plane_offset(int64_t row, int64_t k, int limb, int64_t KB) {
+    int64_t rt = row >> 7, rr = row & 127, kb = k >> 5, kk = k & 31;
+    return ((rt * KB + kb) * 8 + limb) * (int64_t)kPlaneTileBytes
+         + (rr >> 3) * 256 + (kk >> 4) * 128 + (rr & 7) * 16 + (kk & 15);
+}
+
+// 4x4 byte transpose: in a,b,c,d (byte 0 = LSB) -> o[l] = [a_l b_l c_l d_l]
+__device__ __forceinline__ void transpose4x4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t o[4]) {
+    uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
+    uint32_t t2 = __byte_perm(c, d, 0x5140), t3 = __byte_perm(c, d, 0x7362);
+    o[0] = __byte_perm(t0, t2, 0x5410); o[1] = __byte_perm(t0, t2, 0x7632);
+    o[2] = __byte_perm(t1, t3, 0x5410); o[3] = __byte_perm(t1, t3, 0x7632);
+}
+
+// 16 consecutive-k elements of one row -> 8 limb vectors of 16 bytes, stored
+// at their plane positions.  k0 must be a multiple of 16.
+__device__ __forceinline__ void store_limbs16(uint8_t* planes, int64_t row, int64_t k0, int64_t KB,
+                                              const uint64_t v[16]) {
+    uint32_t w[8][4];  // w[limb][word]
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        uint32_t lo[4], hi[4];
+        transpose4x4((uint32_t)v[4 * g], (uint32_t)v[4 * g + 1], (uint32_t)v[4 * g + 2], (uint32_t)v[4 * g + 3], lo);
+        transpose4x4((uint32_t)(v[4 * g] >> 32), (uint32_t)(v[4 * g + 1] >> 32), (uint32_t)(v[4 * g + 2] >> 32),
+                     (uint32_t)(v[4 * g + 3] >> 32), hi);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) { w[l][g] = lo[l]; w[4 + l][g] = hi[l]; }
+    }
+    int64_t base = plane_offset(row, k0, 0, KB);
+#pragma unroll
+    for (int l = 0; l < 8; ++l)
+        *reinterpret_cast<uint4*>(planes + base + (int64_t)l * kPlaneTileBytes) = make_uint4(w[l][0], w[l][1], w[l][2], w[l][3]);
+}
+
+// ------------------------------------------------------------ signed helpers
+// floor(signed(v) / 2^bits) + bit_{bits-1}(v): per-share round-half-up division (R10)
+__host__ __device__ __forceinline__ uint64_t div_pow2_round(uint64_t v, int bits) {
+    return (uint64_t)((int64_t)v >> bits) + ((v >> (bits - 1)) & 1ull);
+}
+
+}  // namespace mpc

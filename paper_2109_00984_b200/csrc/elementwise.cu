@@ -1,0 +1,446 @@
+// elementwise.cu — coalesced uint64 kernels of the protocol (HBM/ALU bound).
+//
+// Every kernel here is one of the §8(a) rows a1..a6, a8..a10 of SURVEY.md:
+// fixed-point encode/decode, PRZS share, local reveal
+// (P:171-173), the Beaver mask e = x - a, d = y - b fused with the
+// local reveal and the u8 limb split that feeds the tcgen05 ring GEMM,
+// TTP triple / wrap-pair generation (Alg. 1
+// inputs P:611-612) and truncation.
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "common.cuh"
+#include "elementwise.h"
+
+namespace mpc {
+
+static inline unsigned grid_for(int64_t work, int threads = 256) {
+    int64_t g = (work + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > 148 * 16) g = 148 * 16;
+    return (unsigned)g;
+}
+
+// ------------------------------------------------------------------ a1 / a10
+__global__ void encode_kernel(const double* __restrict__ x, uint64_t* __restrict__ out, int64_t n,
+                              double scale, int* __restrict__ err) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double v = x[i] * scale;                       // exact: power-of-two scale
+        if (!(fabs(v) < 9223372036854775808.0)) { atomicExch(err, 1); continue; }
+        out[i] = (uint64_t)llround(v);                  // nearest, ties away from zero (R2)
+    }
+}
+__global__ void decode_kernel(const uint64_t* __restrict__ v, double* __restrict__ out, int64_t n, double inv_scale) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (double)(int64_t)v[i] * inv_scale;
+}
+cudaError_t launch_encode(const double* x, uint64_t* out, int64_t n, int frac_bits, int* err, cudaStream_t st) {
+    encode_kernel<<<grid_for(n), 256, 0, st>>>(x, out, n, ldexp(1.0, frac_bits), err);
+    return cudaGetLastError();
+}
+cudaError_t launch_decode(const uint64_t* v, double* out, int64_t n, int frac_bits, cudaStream_t st) {
+    decode_kernel<<<grid_for(n), 256, 0, st>>>(v, out, n, ldexp(1.0, -frac_bits));
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a2 share
+// [x]_p = G(k_p, s)[i] - G(k_{p-1}, s)[i] + [p == src] x[i]   (R4)
+// One thread per element pair (one Philox call yields two elements).
+__global__ void share_kernel(KeySet keys, int P, int party_lo, int party_hi, const uint64_t* __restrict__ x, int src,
+                             uint64_t stream, uint64_t* __restrict__ out, int64_t n) {
+    const int64_t npairs = (n + 1) / 2;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npairs; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i0 = 2 * j;
+        const bool has1 = i0 + 1 < n;
+        uint64_t g0, g1, h0, h1;
+        // previous neighbour of the first party computed
+        philox_pair(keys.k[(party_lo + P - 1) % P], stream, (uint64_t)j, h0, h1);
+        for (int p = party_lo; p < party_hi; ++p) {
+            philox_pair(keys.k[p], stream, (uint64_t)j, g0, g1);
+            uint64_t v0 = g0 - h0, v1 = g1 - h1;
+            if (p == src && x) { v0 += x[i0]; if (has1) v1 += x[i0 + 1]; }
+            uint64_t* o = out + (int64_t)(p - party_lo) * n;
+            o[i0] = v0;
+            if (has1) o[i0 + 1] = v1;
+            h0 = g0; h1 = g1;
+        }
+    }
+}
+cudaError_t launch_share(const KeySet& keys, int P, int party_lo, int party_hi, const uint64_t* x, int src,
+                         uint64_t stream, uint64_t* out, int64_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    share_kernel<<<grid_for((n + 1) / 2), 256, 0, st>>>(keys, P, party_lo, party_hi, x, src, stream, out, n);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ reveal (local sum)
+__global__ void sum_parties_kernel(const uint64_t* __restrict__ s, int P, int64_t n, uint64_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t acc = 0;
+        for (int p = 0; p < P; ++p) acc += s[(int64_t)p * n + i];
+        out[i] = acc;
+    }
+}
+cudaError_t launch_sum_parties(const uint64_t* s, int P, int64_t n, uint64_t* out, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    sum_parties_kernel<<<grid_for(n), 256, 0, st>>>(s, P, n, out);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a4 mask (one party)
+// e = x - a (n1 elements) and d = y - b (n2 elements) into one contiguous
+// buffer [e | d] that is then revealed by a single allreduce (one round).
+__global__ void mask_kernel(const uint64_t* __restrict__ x, const uint64_t* __restrict__ a, int64_t n1,
+                            const uint64_t* __restrict__ y, const uint64_t* __restrict__ b, int64_t n2,
+                            uint64_t* __restrict__ ed) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n1 + n2; i += (int64_t)gridDim.x * blockDim.x)
+        ed[i] = (i < n1) ? x[i] - a[i] : y[i - n1] - b[i - n1];
+}
+cudaError_t launch_mask(const uint64_t* x, const uint64_t* a, int64_t n1, const uint64_t* y, const uint64_t* b,
+                        int64_t n2, uint64_t* ed, cudaStream_t st) {
+    if (n1 + n2 == 0) return cudaSuccess;
+    mask_kernel<<<grid_for(n1 + n2), 256, 0, st>>>(x, a, n1, y, b, n2, ed);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a4+a5+a6 left split
+// Left operands (rows = M, K contiguous): eps = sum_{p<Psum} (plus_p - minus_p)
+// -> eps planes; copies: planes of cp_src party q for q < Pcopy.
+// A warp covers 8 rows x 64 K: lane -> (row = lane & 7, 16-K chunk = lane >> 3):
+// each row's 512 B are read contiguously and each limb's 8 rows x 16 B are
+// written as one contiguous 128 B run.
+__global__ void split_left_kernel(LeftSplitArgs a) {
+    const int64_t KB = num_kb(a.K);
+    const int64_t row_groups = (a.M + 7) / 8;
+    const int64_t kgroups = (a.K + 63) / 64;
+    const int64_t warps_total = row_groups * kgroups;
+    const int lane = threadIdx.x & 31;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < warps_total;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t rg = w / kgroups, kg = w % kgroups;
+        const int64_t row = rg * 8 + (lane & 7);
+        const int64_t k0 = kg * 64 + (lane >> 3) * 16;
+        if (row >= a.M || k0 >= a.K) continue;
+        const bool full = (k0 + 16 <= a.K);
+        uint64_t v[16];
+        if (a.Psum > 0) {
+#pragma unroll
+            for (int m = 0; m < 16; ++m) v[m] = 0;
+            for (int p = 0; p < a.Psum; ++p) {
+                const uint64_t* pl = a.plus + p * a.party_stride + row * a.K + k0;
+                const uint64_t* mi = a.minus ? a.minus + p * a.party_stride + row * a.K + k0 : nullptr;
+#pragma unroll
+                for (int m = 0; m < 16; ++m)
+                    if (full || k0 + m < a.K) v[m] += pl[m] - (mi ? mi[m] : 0ull);
+            }
+            store_limbs16(a.sum_planes, row, k0, KB, v);
+        }
+        for (int q = 0; q < a.Pcopy; ++q) {
+            const uint64_t* src = a.cp_src + q * a.party_stride + row * a.K + k0;
+#pragma unroll
+            for (int m = 0; m < 16; ++m) v[m] = (full || k0 + m < a.K) ? src[m] : 0ull;
+            store_limbs16(a.cp_planes + q * a.cp_planes_stride, row, k0, KB, v);
+        }
+    }
+}
+cudaError_t launch_split_left(const LeftSplitArgs& a, cudaStream_t st) {
+    if (a.M == 0 || a.K == 0) return cudaSuccess;
+    const int64_t warps = ((a.M + 7) / 8) * ((a.K + 63) / 64);
+    split_left_kernel<<<grid_for(warps * 32), 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a4+a5+a6 right split
+// Right operands (K x N row-major, planes have rows = N: a transpose):
+// delta = sum_{p<Psum} (plus_p - minus_p) -> delta planes; copies:
+// planes of (b_q + [q == 0 && add_delta_first] delta) for q < Pcopy
+// (R8: party 0 folds the public eps@delta into eps @ (b_0 + delta)).
+// A warp covers 32 consecutive n x 16 K: every read y[k][n0..n0+31] is a
+// contiguous 256 B run, every limb write is 4 runs of 128 B.
+__global__ void split_right_kernel(RightSplitArgs a) {
+    const int64_t KB = num_kb(a.K);
+    const int64_t ngroups = (a.N + 31) / 32;
+    const int64_t kchunks = (a.K + 15) / 16;
+    const int64_t warps_total = ngroups * kchunks;
+    const int lane = threadIdx.x & 31;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < warps_total;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t kc = w / ngroups, ng = w % ngroups;
+        const int64_t n = ng * 32 + lane;
+        const int64_t k0 = kc * 16;
+        if (n >= a.N) continue;
+        uint64_t d[16];
+#pragma unroll
+        for (int m = 0; m < 16; ++m) d[m] = 0;
+        for (int p = 0; p < a.Psum; ++p) {
+            const uint64_t* pl = a.plus + p * a.party_stride;
+            const uint64_t* mi = a.minus ? a.minus + p * a.party_stride : nullptr;
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const int64_t k = k0 + m;
+                if (k < a.K) d[m] += pl[k * a.N + n] - (mi ? mi[k * a.N + n] : 0ull);
+            }
+        }
+        if (a.sum_planes) store_limbs16(a.sum_planes, n, k0, KB, d);
+        for (int q = 0; q < a.Pcopy; ++q) {
+            const uint64_t* src = a.cp_src + q * a.party_stride;
+            uint64_t v[16];
+            const bool addd = (q == 0) && a.add_delta_first;
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const int64_t k = k0 + m;
+                v[m] = (k < a.K) ? src[k * a.N + n] + (addd ? d[m] : 0ull) : 0ull;
+            }
+            store_limbs16(a.cp_planes + q * a.cp_planes_stride, n, k0, KB, v);
+        }
+    }
+}
+cudaError_t launch_split_right(const RightSplitArgs& a, cudaStream_t st) {
+    if (a.N == 0 || a.K == 0) return cudaSuccess;
+    const int64_t warps = ((a.N + 31) / 32) * ((a.K + 15) / 16);
+    split_right_kernel<<<grid_for(warps * 32), 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a3 TTP triples
+// Left factor a (M x K): a_q = G(k_ttp, A||q||id)[row*K + k].  Writes the
+// parties' u64 shares for q in [out_lo, out_hi) and, if sum_planes != null,
+// the limb planes of a = sum_{q<P} a_q (the TTP's view, R6).
+__global__ void ttp_left_kernel(TtpGenArgs g) {
+    const int64_t KB = num_kb(g.K);
+    const int64_t row_groups = (g.rows + 7) / 8;
+    const int64_t kgroups = (g.K + 63) / 64;
+    const int lane = threadIdx.x & 31;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < row_groups * kgroups;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t rg = w / kgroups, kg = w % kgroups;
+        const int64_t row = rg * 8 + (lane & 7);
+        const int64_t k0 = kg * 64 + (lane >> 3) * 16;
+        if (row >= g.rows || k0 >= g.K) continue;
+        uint64_t sum[16];
+#pragma unroll
+        for (int m = 0; m < 16; ++m) sum[m] = 0;
+        const int qhi = g.sum_planes ? g.P : g.out_hi;
+        const int qlo = g.sum_planes ? 0 : g.out_lo;
+        for (int q = qlo; q < qhi; ++q) {
+            const uint64_t s = stream_word(g.tag, (uint32_t)q, g.id);
+            const bool wr = (q >= g.out_lo && q < g.out_hi);
+            uint64_t* o = wr ? g.out + (int64_t)(q - g.out_lo) * g.rows * g.K + row * g.K : nullptr;
+            uint64_t e0 = 0, e1 = 0;
+            int64_t have = -1;
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const int64_t k = k0 + m;
+                if (k < g.K) {
+                    const uint64_t i = (uint64_t)(row * g.K + k);
+                    if ((int64_t)(i >> 1) != have) { philox_pair(g.key, s, i >> 1, e0, e1); have = (int64_t)(i >> 1); }
+                    const uint64_t v = (i & 1) ? e1 : e0;
+                    sum[m] += v;
+                    if (wr) o[k] = v;
+                }
+            }
+        }
+        if (g.sum_planes) store_limbs16(g.sum_planes, row, k0, KB, sum);
+    }
+}
+// Right factor b (K x N row-major): b_q = G(k_ttp, B||q||id)[k*N + n];
+// planes of b = sum_q b_q are transposed (rows = N).
+__global__ void ttp_right_kernel(TtpGenArgs g) {
+    const int64_t KB = num_kb(g.K);
+    const int64_t N = g.rows;
+    const int64_t ngroups = (N + 31) / 32;
+    const int64_t kchunks = (g.K + 15) / 16;
+    const int lane = threadIdx.x & 31;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < ngroups * kchunks;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t kc = w / ngroups, ng = w % ngroups;
+        const int64_t n = ng * 32 + lane;
+        const int64_t k0 = kc * 16;
+        if (n >= N) continue;
+        uint64_t sum[16];
+#pragma unroll
+        for (int m = 0; m < 16; ++m) sum[m] = 0;
+        const int qhi = g.sum_planes ? g.P : g.out_hi;
+        const int qlo = g.sum_planes ? 0 : g.out_lo;
+        for (int q = qlo; q < qhi; ++q) {
+            const uint64_t s = stream_word(g.tag, (uint32_t)q, g.id);
+            const bool wr = (q >= g.out_lo && q < g.out_hi);
+            uint64_t* o = wr ? g.out + (int64_t)(q - g.out_lo) * N * g.K : nullptr;
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const int64_t k = k0 + m;
+                if (k < g.K) {
+                    const uint64_t v = philox_at(g.key, s, (uint64_t)(k * N + n));
+                    sum[m] += v;
+                    if (wr) o[k * N + n] = v;
+                }
+            }
+        }
+        if (g.sum_planes) store_limbs16(g.sum_planes, n, k0, KB, sum);
+    }
+}
+cudaError_t launch_ttp_left(const TtpGenArgs& g, cudaStream_t st) {
+    if (g.rows == 0 || g.K == 0) return cudaSuccess;
+    const int64_t warps = ((g.rows + 7) / 8) * ((g.K + 63) / 64);
+    ttp_left_kernel<<<grid_for(warps * 32), 256, 0, st>>>(g);
+    return cudaGetLastError();
+}
+cudaError_t launch_ttp_right(const TtpGenArgs& g, cudaStream_t st) {
+    if (g.rows == 0 || g.K == 0) return cudaSuccess;
+    const int64_t warps = ((g.rows + 31) / 32) * ((g.K + 15) / 16);
+    ttp_right_kernel<<<grid_for(warps * 32), 256, 0, st>>>(g);
+    return cudaGetLastError();
+}
+
+// c_q = G(k_ttp, C||q||id) for q >= 1; c_0 = c - sum_{q>=1} c_q.
+// out: parties [out_lo, out_hi); c0_full (in/out) holds c on entry if the
+// TTP view is requested (fix_c0), and receives c_0.
+__global__ void ttp_c_kernel(uint64_t key, uint64_t id, int P, int out_lo, int out_hi, uint64_t* __restrict__ out,
+                             uint64_t* __restrict__ c0, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t acc = 0;
+        for (int q = 1; q < P; ++q) {
+            const bool wr = (q >= out_lo && q < out_hi);
+            if (!wr && !c0) continue;
+            const uint64_t v = philox_at(key, stream_word(kTagC, (uint32_t)q, id), (uint64_t)i);
+            acc += v;
+            if (wr) out[(int64_t)(q - out_lo) * n + i] = v;
+        }
+        if (c0) c0[i] -= acc;
+    }
+}
+cudaError_t launch_ttp_c(uint64_t key, uint64_t id, int P, int out_lo, int out_hi, uint64_t* out, uint64_t* c0,
+                         int64_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    ttp_c_kernel<<<grid_for(n), 256, 0, st>>>(key, id, P, out_lo, out_hi, out, c0, n);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a9 wrap pairs
+// theta_r of the r shares, exactly: (sum signed(r_q) - signed(sum r_q)) / 2^64
+__device__ __forceinline__ int64_t theta_r_at(uint64_t key, uint64_t id, int P, int64_t i) {
+    __int128 s = 0;
+    uint64_t u = 0;
+    for (int q = 0; q < P; ++q) {
+        const uint64_t r = philox_at(key, stream_word(kTagR, (uint32_t)q, id), (uint64_t)i);
+        s += (__int128)(int64_t)r;
+        u += r;
+    }
+    return (int64_t)((s - (__int128)(int64_t)u) >> 64);
+}
+// [theta_r]_q: q >= 1 -> G(THETA||q||id), q = 0 -> theta_r - sum_{q>=1}
+__device__ __forceinline__ uint64_t theta_share_at(uint64_t key, uint64_t id, int P, int q, int64_t i) {
+    if (q > 0) return philox_at(key, stream_word(kTagTheta, (uint32_t)q, id), (uint64_t)i);
+    uint64_t t = (uint64_t)theta_r_at(key, id, P, i);
+    for (int s = 1; s < P; ++s) t -= philox_at(key, stream_word(kTagTheta, (uint32_t)s, id), (uint64_t)i);
+    return t;
+}
+__global__ void wrap_pair_kernel(uint64_t key, uint64_t id, int P, int lo, int hi, uint64_t* __restrict__ r,
+                                 uint64_t* __restrict__ th, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        for (int q = lo; q < hi; ++q) {
+            r[(int64_t)(q - lo) * n + i] = philox_at(key, stream_word(kTagR, (uint32_t)q, id), (uint64_t)i);
+            th[(int64_t)(q - lo) * n + i] = theta_share_at(key, id, P, q, i);
+        }
+}
+cudaError_t launch_wrap_pair(uint64_t key, uint64_t id, int P, int lo, int hi, uint64_t* r, uint64_t* th, int64_t n,
+                             cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    wrap_pair_kernel<<<grid_for(n), 256, 0, st>>>(key, id, P, lo, hi, r, th, n);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a8 truncation, P <= 2
+__global__ void trunc_local_kernel(uint64_t* __restrict__ x, int64_t n, int bits) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = div_pow2_round(x[i], bits);
+}
+cudaError_t launch_trunc_local(uint64_t* x, int64_t n, int bits, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    trunc_local_kernel<<<grid_for(n), 256, 0, st>>>(x, n, bits);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a9 truncation, P > 2, all parties
+// Alg. 1 + correction, eta skipped, for
+// every party of element i in one thread (local reveal of z).
+__global__ void trunc_alg1_all_kernel(uint64_t* __restrict__ x, int P, int64_t n, int bits, uint64_t key, uint64_t id) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t zsum = 0;
+        __int128 zs_signed = 0;
+        for (int q = 0; q < P; ++q) {
+            const uint64_t r = philox_at(key, stream_word(kTagR, (uint32_t)q, id), (uint64_t)i);
+            const uint64_t z = x[(int64_t)q * n + i] + r;
+            zsum += z;
+            zs_signed += (__int128)(int64_t)z;
+        }
+        const int64_t theta_z = (int64_t)((zs_signed - (__int128)(int64_t)zsum) >> 64);
+        const int64_t theta_r = theta_r_at(key, id, P, i);
+        uint64_t th_sum = 0;  // sum of [theta_r]_q for q >= 1
+        for (int q = P - 1; q >= 0; --q) {
+            const uint64_t xq = x[(int64_t)q * n + i];
+            const uint64_t r = philox_at(key, stream_word(kTagR, (uint32_t)q, id), (uint64_t)i);
+            const uint64_t z = xq + r;
+            const __int128 bs = (__int128)(int64_t)xq + (__int128)(int64_t)r - (__int128)(int64_t)z;
+            const uint64_t beta = (uint64_t)(int64_t)(bs >> 64);
+            uint64_t thq;
+            if (q > 0) { thq = philox_at(key, stream_word(kTagTheta, (uint32_t)q, id), (uint64_t)i); th_sum += thq; }
+            else thq = (uint64_t)theta_r - th_sum;
+            const uint64_t theta_x = beta - thq + (q == 0 ? (uint64_t)theta_z : 0ull);
+            x[(int64_t)q * n + i] = div_pow2_round(xq, bits) - theta_x * (1ull << (64 - bits));
+        }
+    }
+}
+cudaError_t launch_trunc_alg1_all(uint64_t* x, int P, int64_t n, int bits, uint64_t key, uint64_t id, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    trunc_alg1_all_kernel<<<grid_for(n), 256, 0, st>>>(x, P, n, bits, key, id);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a9 truncation, P > 2, one party
+// Phase A: z_p = x_p + r_p -> zbuf (u64, to be sum-allreduced) and the top
+// nibble h_p = signed(z_p) >> 60 -> hbuf (int8, sum-allreduced; exact for P <= 16).
+__global__ void trunc_alg1_a_kernel(const uint64_t* __restrict__ x, int64_t n, uint64_t key, uint64_t id, int party,
+                                    uint64_t* __restrict__ zbuf, int8_t* __restrict__ hbuf) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t z = x[i] + philox_at(key, stream_word(kTagR, (uint32_t)party, id), (uint64_t)i);
+        zbuf[i] = z;
+        hbuf[i] = (int8_t)((int64_t)z >> 60);
+    }
+}
+// Phase B: with z = sum z_q and H = sum h_q: S = sum signed(z_q) = (H + kappa) 2^60
+// + (z mod 2^60), kappa = ((z >> 60) - H) mod 16; theta_z = (S - signed(z)) / 2^64.
+__global__ void trunc_alg1_b_kernel(uint64_t* __restrict__ x, int64_t n, int bits, uint64_t key, uint64_t id, int P,
+                                    int party, const uint64_t* __restrict__ zsum, const int8_t* __restrict__ hsum) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t xq = x[i];
+        const uint64_t r = philox_at(key, stream_word(kTagR, (uint32_t)party, id), (uint64_t)i);
+        const uint64_t zq = xq + r;
+        const __int128 bs = (__int128)(int64_t)xq + (__int128)(int64_t)r - (__int128)(int64_t)zq;
+        const uint64_t beta = (uint64_t)(int64_t)(bs >> 64);
+        uint64_t theta_z = 0;
+        if (party == 0) {
+            const uint64_t z = zsum[i];
+            const int64_t H = hsum[i];
+            const int64_t kappa = (((int64_t)(z >> 60) - H) % 16 + 16) % 16;
+            const __int128 S = (__int128)(H + kappa) * ((__int128)1 << 60) + (__int128)(z & ((1ull << 60) - 1));
+            theta_z = (uint64_t)(int64_t)((S - (__int128)(int64_t)z) >> 64);
+        }
+        const uint64_t thq = theta_share_at(key, id, P, party, i);
+        const uint64_t theta_x = beta - thq + theta_z;
+        x[i] = div_pow2_round(xq, bits) - theta_x * (1ull << (64 - bits));
+    }
+}
+cudaError_t launch_trunc_alg1_a(const uint64_t* x, int64_t n, uint64_t key, uint64_t id, int party, uint64_t* zbuf,
+                                int8_t* hbuf, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    trunc_alg1_a_kernel<<<grid_for(n), 256, 0, st>>>(x, n, key, id, party, zbuf, hbuf);
+    return cudaGetLastError();
+}
+cudaError_t launch_trunc_alg1_b(uint64_t* x, int64_t n, int bits, uint64_t key, uint64_t id, int P, int party,
+                                const uint64_t* zsum, const int8_t* hsum, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    trunc_alg1_b_kernel<<<grid_for(n), 256, 0, st>>>(x, n, bits, key, id, P, party, zsum, hsum);
+    return cudaGetLastError();
+}
+
+}  // namespace mpc

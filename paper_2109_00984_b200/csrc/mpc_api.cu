@@ -1,0 +1,472 @@
+// mpc_api.cu — the C-ABI of include/mpc_ring.h: host orchestration of the
+// protocol steps (argument checks, workspace carving, stream ordering, NCCL
+// reveals, round/byte accounting, profiling hooks).  All arithmetic runs in
+// the kernels of elementwise.cu and ring_gemm.cu.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mpc_ring.h"
+#include "common.cuh"
+#include "elementwise.h"
+#include "ring_gemm.h"
+
+using namespace mpc;
+
+struct ProfEvent { cudaEvent_t a, b; int cls; };
+
+struct mpc_ctx_s {
+    int P = 1, rank = 0, device = 0, frac = 16;
+    bool all = false;                    // all parties on this device
+    uint64_t master = 0;
+    KeySet kp{};
+    uint64_t kttp = 0;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+    bool broken = false;
+    std::string err;
+    uint64_t rounds = 0, bytes = 0, launches = 0;
+    bool prof = false;
+    std::vector<ProfEvent> pending;
+    std::vector<cudaEvent_t> pool;
+    double prof_ms[6] = {0, 0, 0, 0, 0, 0};
+    uint64_t prof_n[6] = {0, 0, 0, 0, 0, 0};
+    int* d_err = nullptr;
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+};
+
+namespace {
+
+constexpr int kClsGemm = 0, kClsSplit = 1, kClsTrunc = 2, kClsPrg = 3, kClsCodec = 4, kClsComm = 5;
+
+mpc_status fail(mpc_ctx c, mpc_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    return s;
+}
+
+cudaEvent_t take_event(mpc_ctx c) {
+    if (!c->pool.empty()) { cudaEvent_t e = c->pool.back(); c->pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Run one launch of class `cls`; brackets it with events when profiling.
+template <class F>
+mpc_status run(mpc_ctx c, int cls, const char* what, F&& f) {
+    ProfEvent ev{nullptr, nullptr, cls};
+    if (c->prof) { ev.a = take_event(c); ev.b = take_event(c); cudaEventRecord(ev.a, c->stream); }
+    cudaError_t e = f();
+    if (c->prof) { cudaEventRecord(ev.b, c->stream); c->pending.push_back(ev); }
+    if (cls != kClsComm) c->launches++;
+    if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return MPC_OK;
+}
+
+mpc_status nccl_allreduce(mpc_ctx c, const void* send, void* recv, size_t count, ncclDataType_t dt, const char* what) {
+    if (!c->comm) return fail(c, MPC_ERR_STATE, "%s: context has no communicator (created without nccl_id)", what);
+    ProfEvent ev{nullptr, nullptr, kClsComm};
+    if (c->prof) { ev.a = take_event(c); ev.b = take_event(c); cudaEventRecord(ev.a, c->stream); }
+    ncclResult_t r = ncclAllReduce(send, recv, count, dt, ncclSum, c->comm, c->stream);
+    if (c->prof) { cudaEventRecord(ev.b, c->stream); c->pending.push_back(ev); }
+    if (r != ncclSuccess) {
+        c->broken = true;
+        ncclCommAbort(c->comm);
+        c->comm = nullptr;
+        return fail(c, MPC_ERR_NCCL, "%s: %s", what, ncclGetErrorString(r));
+    }
+    return MPC_OK;
+}
+
+#define CHECK(call)                                   \
+    do {                                              \
+        mpc_status _s = (call);                       \
+        if (_s != MPC_OK) return _s;                  \
+    } while (0)
+
+mpc_status enter(mpc_ctx c) {
+    if (!c) return MPC_ERR_ARG;
+    if (c->broken) return fail(c, MPC_ERR_STATE, "context unusable after a failed collective");
+    c->err.clear();
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+    return MPC_OK;
+}
+
+bool one_party_comm(mpc_ctx c) { return !c->all && c->P > 1; }
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Carve {
+    uint8_t* base; size_t off = 0;
+    explicit Carve(void* b) : base(static_cast<uint8_t*>(b)) {}
+    uint8_t* take(size_t n) { uint8_t* p = base ? base + off : nullptr; off += align256(n); return p; }
+};
+
+// workspace layout of beaver_matmul (see mpc_workspace_bytes)
+struct BeaverWs {
+    uint8_t *eps_pl, *delta_pl, *a_pl, *b_pl;
+    uint64_t* ed;        // one-party mode: [e | d] reveal buffer
+    uint64_t* zbuf;      // one-party, P > 2, truncation: z reveal
+    int8_t* hbuf;        // one-party, P > 2, truncation: top nibbles
+    size_t total;
+};
+
+BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N) {
+    const int Pl = c->all ? c->P : 1;
+    Carve cv(ws);
+    BeaverWs w{};
+    w.eps_pl = cv.take(planes_bytes(M, K));
+    w.delta_pl = cv.take(planes_bytes(N, K));
+    w.a_pl = cv.take((size_t)Pl * planes_bytes(M, K));
+    w.b_pl = cv.take((size_t)Pl * planes_bytes(N, K));
+    w.ed = reinterpret_cast<uint64_t*>(c->all ? nullptr : cv.take(8 * (size_t)(M * K + K * N)));
+    const bool alg1_one = !c->all && c->P > 2;
+    w.zbuf = reinterpret_cast<uint64_t*>(alg1_one ? cv.take(8 * (size_t)(M * N)) : nullptr);
+    w.hbuf = reinterpret_cast<int8_t*>(alg1_one ? cv.take((size_t)(M * N)) : nullptr);
+    w.total = cv.off;
+    return w;
+}
+
+mpc_status gemm_run(mpc_ctx c, RingGemmParams& p, int parties) {
+    for (int q = 0; q < 4; ++q) p.kb_chunk[q] = ring_gemm_kb_chunk(q);
+    return run(c, kClsGemm, "ring_gemm", [&] { return ring_gemm_launch(p, parties, c->stream); });
+}
+
+mpc_status ensure_scratch(mpc_ctx c, size_t bytes) {
+    if (c->scratch_bytes >= bytes) return MPC_OK;
+    if (c->scratch) { cudaStreamSynchronize(c->stream); cudaFree(c->scratch); c->scratch = nullptr; c->scratch_bytes = 0; }
+    cudaError_t e = cudaMalloc(&c->scratch, bytes);
+    if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "scratch alloc: %s", cudaGetErrorString(e));
+    c->scratch_bytes = bytes;
+    return MPC_OK;
+}
+
+// Truncation of x ([P][n] or n) by `bits` with wrap pair `wrap_id`.
+mpc_status truncate_impl(mpc_ctx c, uint64_t* x, int64_t n, int bits, uint64_t wrap_id, uint64_t* zbuf, int8_t* hbuf) {
+    if (c->P <= 2) {
+        const int64_t tot = n * (c->all ? c->P : 1);
+        return run(c, kClsTrunc, "trunc_local", [&] { return launch_trunc_local(x, tot, bits, c->stream); });
+    }
+    c->rounds += 1;
+    if (c->all) {
+        c->bytes += 8ull * (uint64_t)n * c->P + (uint64_t)n * c->P;
+        return run(c, kClsTrunc, "trunc_alg1_all",
+                   [&] { return launch_trunc_alg1_all(x, c->P, n, bits, c->kttp, wrap_id, c->stream); });
+    }
+    c->bytes += 9ull * (uint64_t)n;
+    CHECK(run(c, kClsTrunc, "trunc_alg1_a",
+              [&] { return launch_trunc_alg1_a(x, n, c->kttp, wrap_id, c->rank, zbuf, hbuf, c->stream); }));
+    CHECK(nccl_allreduce(c, zbuf, zbuf, (size_t)n, ncclUint64, "truncate z reveal"));
+    CHECK(nccl_allreduce(c, hbuf, hbuf, (size_t)n, ncclInt8, "truncate top-bit reveal"));
+    return run(c, kClsTrunc, "trunc_alg1_b", [&] {
+        return launch_trunc_alg1_b(x, n, bits, c->kttp, wrap_id, c->P, c->rank, zbuf, hbuf, c->stream);
+    });
+}
+
+}  // namespace
+
+extern "C" {
+
+mpc_status mpc_create(mpc_ctx* out, int world_size, int rank, int device, const void* nccl_id,
+                      uint64_t master_seed, int frac_bits) {
+    if (!out) return MPC_ERR_ARG;
+    *out = nullptr;
+    if (world_size < 1 || world_size > kMaxParties) return MPC_ERR_ARG;
+    if (rank != MPC_ALL_PARTIES && (rank < 0 || rank >= world_size)) return MPC_ERR_ARG;
+    if (frac_bits < 1 || frac_bits > 30) return MPC_ERR_ARG;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return MPC_ERR_UNSUPPORTED;
+    if (prop.major != 10 || prop.minor != 0) return MPC_ERR_UNSUPPORTED;   // sm_100a kernels only
+    if (cudaSetDevice(device) != cudaSuccess) return MPC_ERR_CUDA;
+    mpc_ctx c = new mpc_ctx_s();
+    c->P = world_size;
+    c->rank = rank == MPC_ALL_PARTIES ? 0 : rank;
+    c->all = (rank == MPC_ALL_PARTIES);
+    c->device = device;
+    c->frac = frac_bits;
+    c->master = master_seed;
+    for (int p = 0; p < world_size; ++p) c->kp.k[p] = philox_at(master_seed, stream_word(kTagKeyParty, p, 0), 0);
+    c->kttp = philox_at(master_seed, stream_word(kTagKeyTTP, 0, 0), 0);
+    if (cudaMalloc(&c->d_err, sizeof(int)) != cudaSuccess) { delete c; return MPC_ERR_CUDA; }
+    if (one_party_comm(c) && nccl_id) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        if (ncclCommInitRank(&c->comm, world_size, id, rank) != ncclSuccess) {
+            cudaFree(c->d_err); delete c; return MPC_ERR_NCCL;
+        }
+    }
+    *out = c;
+    return MPC_OK;
+}
+
+mpc_status mpc_destroy(mpc_ctx c) {
+    if (!c) return MPC_ERR_ARG;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream); else cudaDeviceSynchronize();
+    if (c->comm) ncclCommDestroy(c->comm);
+    for (auto& e : c->pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+    for (auto e : c->pool) cudaEventDestroy(e);
+    if (c->d_err) cudaFree(c->d_err);
+    if (c->scratch) cudaFree(c->scratch);
+    delete c;
+    return MPC_OK;
+}
+
+mpc_status mpc_set_stream(mpc_ctx c, void* s) {
+    if (!c) return MPC_ERR_ARG;
+    c->stream = static_cast<cudaStream_t>(s);
+    return MPC_OK;
+}
+
+const char* mpc_last_error(mpc_ctx c) { return c ? c->err.c_str() : "null context"; }
+
+mpc_status mpc_stats(mpc_ctx c, uint64_t* rounds, uint64_t* bytes_sent) {
+    if (!c) return MPC_ERR_ARG;
+    if (rounds) *rounds = c->rounds;
+    if (bytes_sent) *bytes_sent = c->bytes;
+    return MPC_OK;
+}
+
+mpc_status mpc_nccl_unique_id(void* out128) {
+    if (!out128) return MPC_ERR_ARG;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return MPC_ERR_NCCL;
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof(id));
+    return MPC_OK;
+}
+
+int mpc_world_size(mpc_ctx c) { return c ? c->P : -1; }
+int mpc_rank(mpc_ctx c) { return c ? (c->all ? MPC_ALL_PARTIES : c->rank) : -2; }
+
+mpc_status mpc_encode(mpc_ctx c, const double* x, uint64_t* out, int64_t n) {
+    CHECK(enter(c));
+    if (n < 0) return fail(c, MPC_ERR_SHAPE, "encode: n < 0");
+    if (n == 0) return MPC_OK;
+    if (!x || !out) return fail(c, MPC_ERR_ARG, "encode: null pointer");
+    cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream);
+    CHECK(run(c, kClsCodec, "encode", [&] { return launch_encode(x, out, n, c->frac, c->d_err, c->stream); }));
+    int h = 0;
+    cudaMemcpyAsync(&h, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "encode: %s", cudaGetErrorString(e));
+    if (h) return fail(c, MPC_ERR_OVERFLOW, "encode: |x| * 2^%d >= 2^63 or NaN", c->frac);
+    return MPC_OK;
+}
+
+mpc_status mpc_decode(mpc_ctx c, const uint64_t* v, double* out, int64_t n) {
+    CHECK(enter(c));
+    if (n < 0) return fail(c, MPC_ERR_SHAPE, "decode: n < 0");
+    if (n == 0) return MPC_OK;
+    if (!v || !out) return fail(c, MPC_ERR_ARG, "decode: null pointer");
+    return run(c, kClsCodec, "decode", [&] { return launch_decode(v, out, n, c->frac, c->stream); });
+}
+
+mpc_status mpc_share(mpc_ctx c, const uint64_t* x, int src, uint64_t share_id, uint64_t* out, int64_t n) {
+    CHECK(enter(c));
+    if (n < 0) return fail(c, MPC_ERR_SHAPE, "share: n < 0");
+    if (src < 0 || src >= c->P) return fail(c, MPC_ERR_ARG, "share: src %d out of range", src);
+    if (n == 0) return MPC_OK;
+    if (!out) return fail(c, MPC_ERR_ARG, "share: null output");
+    const bool holds = c->all || c->rank == src;
+    if (holds && !x) return fail(c, MPC_ERR_ARG, "share: src party must supply x");
+    const int lo = c->all ? 0 : c->rank, hi = c->all ? c->P : c->rank + 1;
+    const uint64_t s = stream_word(kTagPRZS, 0, share_id);
+    return run(c, kClsPrg, "share",
+               [&] { return launch_share(c->kp, c->P, lo, hi, holds ? x : nullptr, src, s, out, n, c->stream); });
+}
+
+mpc_status mpc_reveal(mpc_ctx c, const uint64_t* share, uint64_t* out, int64_t n) {
+    CHECK(enter(c));
+    if (n < 0) return fail(c, MPC_ERR_SHAPE, "reveal: n < 0");
+    c->rounds += 1;
+    c->bytes += 8ull * (uint64_t)n * (c->all ? c->P : 1);
+    if (n == 0) return MPC_OK;
+    if (!share || !out) return fail(c, MPC_ERR_ARG, "reveal: null pointer");
+    if (c->all) return run(c, kClsSplit, "reveal_sum", [&] { return launch_sum_parties(share, c->P, n, out, c->stream); });
+    if (c->P == 1) {
+        cudaError_t e = cudaMemcpyAsync(out, share, 8 * (size_t)n, cudaMemcpyDeviceToDevice, c->stream);
+        return e == cudaSuccess ? MPC_OK : fail(c, MPC_ERR_CUDA, "reveal copy: %s", cudaGetErrorString(e));
+    }
+    return nccl_allreduce(c, share, out, (size_t)n, ncclUint64, "reveal");
+}
+
+size_t mpc_ttp_workspace_bytes(mpc_ctx c, int64_t M, int64_t K, int64_t N) {
+    (void)c;
+    if (M < 0 || K < 0 || N < 0) return 0;
+    return align256(planes_bytes(M, K)) + align256(planes_bytes(N, K));
+}
+
+mpc_status mpc_ttp_triples(mpc_ctx c, uint64_t id, int64_t M, int64_t K, int64_t N, uint64_t* a, uint64_t* b,
+                           uint64_t* cc, void* ws, size_t ws_bytes) {
+    CHECK(enter(c));
+    if (M < 0 || K < 0 || N < 0) return fail(c, MPC_ERR_SHAPE, "ttp_triples: negative size");
+    if ((M * K && !a) || (K * N && !b) || (M * N && !cc)) return fail(c, MPC_ERR_ARG, "ttp_triples: null output");
+    const bool ttp = c->all || c->rank == 0;       // holds the TTP view: needs a, b sums and c
+    if (ttp && ws_bytes < mpc_ttp_workspace_bytes(c, M, K, N)) return fail(c, MPC_ERR_SHAPE, "ttp_triples: workspace too small");
+    if (ttp && !ws && (M * K + K * N) > 0) return fail(c, MPC_ERR_ARG, "ttp_triples: null workspace");
+    const int lo = c->all ? 0 : c->rank, hi = c->all ? c->P : c->rank + 1;
+    Carve cv(ws);
+    uint8_t* a_pl = ttp ? cv.take(planes_bytes(M, K)) : nullptr;
+    uint8_t* b_pl = ttp ? cv.take(planes_bytes(N, K)) : nullptr;
+    TtpGenArgs ga{c->kttp, id, kTagA, c->P, M, K, lo, hi, a, a_pl};
+    CHECK(run(c, kClsPrg, "ttp_a", [&] { return launch_ttp_left(ga, c->stream); }));
+    TtpGenArgs gb{c->kttp, id, kTagB, c->P, N, K, lo, hi, b, b_pl};
+    CHECK(run(c, kClsPrg, "ttp_b", [&] { return launch_ttp_right(gb, c->stream); }));
+    if (M == 0 || N == 0) return MPC_OK;
+    if (ttp) {
+        // c = (sum a) @ (sum b) into party 0's c slot, on the tensor cores
+        RingGemmParams p{};
+        p.seg[0] = RingGemmSegment{a_pl, b_pl, (int)num_kb(K), 0, 0};
+        p.nseg = 1;
+        p.M = M; p.N = N; p.C = nullptr; p.Z = cc;
+        p.party_stride_c = p.party_stride_z = 0;
+        p.trunc_bits = 0;
+        CHECK(gemm_run(c, p, 1));
+    }
+    uint64_t* c_out = c->all ? cc + M * N : cc;    // parties >= 1
+    const int out_lo = c->all ? 1 : c->rank, out_hi = c->all ? c->P : (c->rank == 0 ? 0 : c->rank + 1);
+    return run(c, kClsPrg, "ttp_c", [&] {
+        return launch_ttp_c(c->kttp, id, c->P, out_lo, out_hi, c_out, ttp ? cc : nullptr, M * N, c->stream);
+    });
+}
+
+mpc_status mpc_ttp_wrap_pairs(mpc_ctx c, uint64_t id, int64_t n, uint64_t* r, uint64_t* th) {
+    CHECK(enter(c));
+    if (n < 0) return fail(c, MPC_ERR_SHAPE, "wrap_pairs: n < 0");
+    if (n == 0) return MPC_OK;
+    if (!r || !th) return fail(c, MPC_ERR_ARG, "wrap_pairs: null output");
+    const int lo = c->all ? 0 : c->rank, hi = c->all ? c->P : c->rank + 1;
+    return run(c, kClsPrg, "wrap_pairs", [&] { return launch_wrap_pair(c->kttp, id, c->P, lo, hi, r, th, n, c->stream); });
+}
+
+size_t mpc_workspace_bytes(mpc_ctx c, int64_t M, int64_t K, int64_t N) {
+    if (!c || M < 0 || K < 0 || N < 0) return 0;
+    return carve_beaver(c, nullptr, M, K, N).total;
+}
+
+mpc_status mpc_beaver_matmul(mpc_ctx c, const uint64_t* x, const uint64_t* y, const uint64_t* a, const uint64_t* b,
+                             const uint64_t* cc, uint64_t* z, int64_t M, int64_t K, int64_t N, int truncate,
+                             uint64_t wrap_id, void* ws, size_t ws_bytes) {
+    CHECK(enter(c));
+    if (M < 0 || K < 0 || N < 0) return fail(c, MPC_ERR_SHAPE, "beaver_matmul: negative size");
+    if (K > (int64_t)1 << 30 || M > (int64_t)1 << 31 || N > (int64_t)1 << 31) return fail(c, MPC_ERR_SHAPE, "beaver_matmul: too large");
+    const BeaverWs w = carve_beaver(c, ws, M, K, N);
+    if (ws_bytes < w.total) return fail(c, MPC_ERR_SHAPE, "beaver_matmul: workspace %zu < %zu", ws_bytes, w.total);
+    const int Pl = c->all ? c->P : 1;
+    c->rounds += 1;                                   // eps || delta: one batched reveal
+    c->bytes += 8ull * (uint64_t)(M * K + K * N) * Pl;
+    if (M == 0 || N == 0) return MPC_OK;
+    if ((M * K && (!x || !a)) || (K * N && (!y || !b)) || !cc || !z || (!ws && w.total))
+        return fail(c, MPC_ERR_ARG, "beaver_matmul: null pointer");
+    const int64_t sMK = M * K, sKN = K * N, sMN = M * N;
+    if (c->all) {
+        LeftSplitArgs L{M, K, sMK, x, a, c->P, w.eps_pl, a, c->P, w.a_pl, planes_bytes(M, K)};
+        CHECK(run(c, kClsSplit, "mask+reveal+split eps", [&] { return launch_split_left(L, c->stream); }));
+        RightSplitArgs R{K, N, sKN, y, b, c->P, w.delta_pl, b, c->P, 1, w.b_pl, planes_bytes(N, K)};
+        CHECK(run(c, kClsSplit, "mask+reveal+split delta", [&] { return launch_split_right(R, c->stream); }));
+    } else {
+        CHECK(run(c, kClsSplit, "mask", [&] { return launch_mask(x, a, sMK, y, b, sKN, w.ed, c->stream); }));
+        if (c->P > 1) CHECK(nccl_allreduce(c, w.ed, w.ed, (size_t)(sMK + sKN), ncclUint64, "eps/delta reveal"));
+        LeftSplitArgs L{M, K, 0, w.ed, nullptr, 1, w.eps_pl, a, 1, w.a_pl, 0};
+        CHECK(run(c, kClsSplit, "split eps", [&] { return launch_split_left(L, c->stream); }));
+        RightSplitArgs R{K, N, 0, w.ed + sMK, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0};
+        CHECK(run(c, kClsSplit, "split delta", [&] { return launch_split_right(R, c->stream); }));
+    }
+    RingGemmParams p{};
+    p.seg[0] = RingGemmSegment{w.a_pl, w.delta_pl, (int)num_kb(K), planes_bytes(M, K), 0};   // a_p @ delta
+    p.seg[1] = RingGemmSegment{w.eps_pl, w.b_pl, (int)num_kb(K), 0, planes_bytes(N, K)};     // eps @ b'_p
+    p.nseg = 2;
+    p.M = M; p.N = N; p.C = cc; p.Z = z;
+    p.party_stride_c = p.party_stride_z = sMN;
+    p.trunc_bits = (truncate && c->P <= 2) ? c->frac : 0;                                     // fused, 0 rounds
+    CHECK(gemm_run(c, p, Pl));
+    if (truncate && c->P > 2) CHECK(truncate_impl(c, z, sMN, c->frac, wrap_id, w.zbuf, w.hbuf));
+    return MPC_OK;
+}
+
+mpc_status mpc_truncate(mpc_ctx c, uint64_t* x, int64_t n, int bits, uint64_t wrap_id) {
+    CHECK(enter(c));
+    if (n < 0) return fail(c, MPC_ERR_SHAPE, "truncate: n < 0");
+    if (bits < 1 || bits > 62) return fail(c, MPC_ERR_ARG, "truncate: bits %d out of [1, 62]", bits);
+    if (n == 0) return MPC_OK;
+    if (!x) return fail(c, MPC_ERR_ARG, "truncate: null pointer");
+    uint64_t* zb = nullptr;
+    int8_t* hb = nullptr;
+    if (!c->all && c->P > 2) {
+        CHECK(ensure_scratch(c, align256(8 * (size_t)n) + (size_t)n));
+        zb = static_cast<uint64_t*>(c->scratch);
+        hb = reinterpret_cast<int8_t*>(static_cast<uint8_t*>(c->scratch) + align256(8 * (size_t)n));
+    }
+    return truncate_impl(c, x, n, bits, wrap_id, zb, hb);
+}
+
+size_t mpc_ring_matmul_workspace_bytes(int64_t M, int64_t K, int64_t N) {
+    if (M < 0 || K < 0 || N < 0) return 0;
+    return align256(planes_bytes(M, K)) + align256(planes_bytes(N, K));
+}
+
+mpc_status mpc_ring_matmul(mpc_ctx c, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t M, int64_t K,
+                           int64_t N, void* ws, size_t ws_bytes) {
+    CHECK(enter(c));
+    if (M < 0 || K < 0 || N < 0) return fail(c, MPC_ERR_SHAPE, "ring_matmul: negative size");
+    if (ws_bytes < mpc_ring_matmul_workspace_bytes(M, K, N)) return fail(c, MPC_ERR_SHAPE, "ring_matmul: workspace too small");
+    if (M == 0 || N == 0) return MPC_OK;
+    if (!C || (K && (!A || !B || !ws))) return fail(c, MPC_ERR_ARG, "ring_matmul: null pointer");
+    Carve cv(ws);
+    uint8_t* a_pl = cv.take(planes_bytes(M, K));
+    uint8_t* b_pl = cv.take(planes_bytes(N, K));
+    LeftSplitArgs L{M, K, 0, A, nullptr, 1, a_pl, nullptr, 0, nullptr, 0};
+    CHECK(run(c, kClsSplit, "split A", [&] { return launch_split_left(L, c->stream); }));
+    RightSplitArgs R{K, N, 0, B, nullptr, 1, b_pl, nullptr, 0, 0, nullptr, 0};
+    CHECK(run(c, kClsSplit, "split B", [&] { return launch_split_right(R, c->stream); }));
+    RingGemmParams p{};
+    p.seg[0] = RingGemmSegment{a_pl, b_pl, (int)num_kb(K), 0, 0};
+    p.nseg = 1;
+    p.M = M; p.N = N; p.C = nullptr; p.Z = C;
+    return gemm_run(c, p, 1);
+}
+
+mpc_status mpc_profile_enable(mpc_ctx c, int enable) {
+    if (!c) return MPC_ERR_ARG;
+    c->prof = enable != 0;
+    return MPC_OK;
+}
+
+mpc_status mpc_profile_read(mpc_ctx c, int cls, double* total_ms, uint64_t* launches) {
+    if (!c || cls < 0 || cls > 5) return MPC_ERR_ARG;
+    cudaSetDevice(c->device);
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "profile_read: %s", cudaGetErrorString(e));
+    for (auto& ev : c->pending) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev.a, ev.b);
+        c->prof_ms[ev.cls] += ms;
+        c->prof_n[ev.cls] += 1;
+        c->pool.push_back(ev.a);
+        c->pool.push_back(ev.b);
+    }
+    c->pending.clear();
+    if (total_ms) *total_ms = c->prof_ms[cls];
+    if (launches) *launches = c->prof_n[cls];
+    c->prof_ms[cls] = 0;
+    c->prof_n[cls] = 0;
+    return MPC_OK;
+}
+
+uint64_t mpc_launch_count(mpc_ctx c) { return c ? c->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,31 @@
+// ring_gemm.h — host interface of the tcgen05 limb-plane ring GEMM (internal).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mpc {
+
+struct RingGemmSegment {
+    const uint8_t* A;        // left limb planes  (rows = M), common.cuh layout
+    const uint8_t* B;        // right limb planes (rows = N), common.cuh layout
+    int kb;                  // number of 32-K blocks of this segment (both operands)
+    int64_t party_stride_A;  // bytes between parties' A planes (0 = shared, e.g. eps)
+    int64_t party_stride_B;
+};
+
+struct RingGemmParams {
+    RingGemmSegment seg[2];
+    int nseg;
+    int64_t M, N;                       // logical output size
+    const uint64_t* C;                  // optional addend [party][M][N] (Beaver c_p)
+    uint64_t* Z;                        // output [party][M][N]
+    int64_t party_stride_c, party_stride_z;  // elements
+    int trunc_bits;                     // 0 = none; else per-share round-half-up division (R10)
+    int kb_chunk[4];                    // max 32-K blocks per accumulation unit of pass q
+};
+
+int ring_gemm_kb_chunk(int q);
+size_t ring_gemm_smem_bytes();
+cudaError_t ring_gemm_launch(const RingGemmParams& p, int parties, cudaStream_t stream);
+
+}  // namespace mpc

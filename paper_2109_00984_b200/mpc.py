@@ -1,0 +1,203 @@
+"""Thin Python binding of include/mpc_ring.h (argument marshalling only).
+
+Every method below forwards to the C-ABI entry point of the same name in
+``libmpc_ring.so``; all arithmetic runs in the library's sm_100a kernels.
+PyTorch supplies device memory, the current CUDA stream and (for one party
+per GPU) the process group used to broadcast the NCCL unique id.  There is no
+CPU or PyTorch fallback: if the native library is missing the import fails.
+
+Tensors are CUDA ``torch.uint64`` (or ``torch.int64``, same bits) and
+contiguous.  With ``rank=ALL_PARTIES`` share arguments carry a leading party
+dimension ``P``; with one party per process they are that party's share.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import torch
+
+from . import _native
+
+ALL_PARTIES = -1
+DEFAULT_FRAC_BITS = 16          # P:244 §7, "L = 16 by default"
+
+_STATUS = {0: "MPC_OK", 1: "MPC_ERR_ARG", 2: "MPC_ERR_SHAPE", 3: "MPC_ERR_OVERFLOW", 4: "MPC_ERR_CUDA",
+           5: "MPC_ERR_NCCL", 6: "MPC_ERR_STATE", 7: "MPC_ERR_UNSUPPORTED"}
+
+PROFILE_CLASSES = {"gemm": 0, "split": 1, "trunc": 2, "prg": 3, "codec": 4, "comm": 5}
+
+
+class MpcError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("libmpc_ring takes CUDA device tensors")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    if t.dtype not in (torch.uint64, torch.int64, torch.float64, torch.uint8, torch.int8):
+        raise TypeError(f"unsupported dtype {t.dtype}")
+    return t.data_ptr()
+
+
+def _u64(shape, device) -> torch.Tensor:
+    return torch.empty(shape, dtype=torch.uint64, device=device)
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId from the native library's NCCL (rank 0 calls this)."""
+    return _native.nccl_unique_id()
+
+
+class Context:
+    """An mpc_ctx: one party of P (rank >= 0) or all P parties (rank = ALL_PARTIES) on `device`."""
+
+    def __init__(self, world_size: int, rank: int = ALL_PARTIES, device: int = 0,
+                 master_seed: int = 210900984, frac_bits: int = DEFAULT_FRAC_BITS,
+                 nccl_id: Optional[bytes] = None):
+        self._lib = _native.lib()
+        self.P = world_size
+        self.rank = rank
+        self.all_parties = rank == ALL_PARTIES
+        self.device = torch.device("cuda", device)
+        self.frac_bits = frac_bits
+        h = ctypes.c_void_p()
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        st = self._lib.mpc_create(ctypes.byref(h), world_size, rank, device, idbuf,
+                                  ctypes.c_uint64(master_seed), frac_bits)
+        if st != 0:
+            raise MpcError(st, "mpc_create failed (needs an sm_100 GPU; nccl_id for one party per GPU)")
+        self._h = h
+        self._ws = None
+
+    # ------------------------------------------------------------ plumbing
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.mpc_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _call(self, fn, *args):
+        self._lib.mpc_set_stream(self._h, ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
+        st = fn(self._h, *args)
+        if st != 0:
+            raise MpcError(st, self._lib.mpc_last_error(self._h).decode())
+
+    def _workspace(self, nbytes: int) -> torch.Tensor:
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def _lead(self):
+        return (self.P,) if self.all_parties else ()
+
+    # ------------------------------------------------------------ fixed point
+    def encode(self, x: torch.Tensor) -> torch.Tensor:
+        x = x.to(device=self.device, dtype=torch.float64).contiguous()
+        out = _u64(x.shape, self.device)
+        self._call(self._lib.mpc_encode, _ptr(x), _ptr(out), ctypes.c_int64(x.numel()))
+        return out
+
+    def decode(self, v: torch.Tensor) -> torch.Tensor:
+        out = torch.empty(v.shape, dtype=torch.float64, device=self.device)
+        self._call(self._lib.mpc_decode, _ptr(v), _ptr(out), ctypes.c_int64(v.numel()))
+        return out
+
+    # ------------------------------------------------------------ share / reveal
+    def share(self, x: Optional[torch.Tensor], src: int, share_id: int, shape=None) -> torch.Tensor:
+        shape = tuple(x.shape) if x is not None else tuple(shape)
+        n = 1
+        for s in shape:
+            n *= s
+        out = _u64(self._lead() + shape, self.device)
+        self._call(self._lib.mpc_share, _ptr(x), src, ctypes.c_uint64(share_id), _ptr(out), ctypes.c_int64(n))
+        return out
+
+    def reveal(self, shares: torch.Tensor) -> torch.Tensor:
+        shape = tuple(shares.shape[1:]) if self.all_parties else tuple(shares.shape)
+        out = _u64(shape, self.device)
+        self._call(self._lib.mpc_reveal, _ptr(shares), _ptr(out), ctypes.c_int64(out.numel()))
+        return out
+
+    # ------------------------------------------------------------ offline TTP
+    def ttp_triples(self, triple_id: int, M: int, K: int, N: int):
+        a = _u64(self._lead() + (M, K), self.device)
+        b = _u64(self._lead() + (K, N), self.device)
+        c = _u64(self._lead() + (M, N), self.device)
+        nb = self._lib.mpc_ttp_workspace_bytes(self._h, M, K, N)
+        ws = self._workspace(nb)
+        self._call(self._lib.mpc_ttp_triples, ctypes.c_uint64(triple_id), ctypes.c_int64(M), ctypes.c_int64(K),
+                   ctypes.c_int64(N), _ptr(a), _ptr(b), _ptr(c), _ptr(ws), ctypes.c_size_t(ws.numel()))
+        return a, b, c
+
+    def ttp_wrap_pairs(self, wrap_id: int, n: int):
+        r = _u64(self._lead() + (n,), self.device)
+        th = _u64(self._lead() + (n,), self.device)
+        self._call(self._lib.mpc_ttp_wrap_pairs, ctypes.c_uint64(wrap_id), ctypes.c_int64(n), _ptr(r), _ptr(th))
+        return r, th
+
+    # ------------------------------------------------------------ online
+    def workspace_bytes(self, M: int, K: int, N: int) -> int:
+        return int(self._lib.mpc_workspace_bytes(self._h, M, K, N))
+
+    def beaver_matmul(self, x, y, a, b, c, truncate: bool = True, wrap_id: int = 0,
+                      out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        M, K = x.shape[-2], x.shape[-1]
+        N = y.shape[-1]
+        z = out if out is not None else _u64(self._lead() + (M, N), self.device)
+        ws = self._workspace(self.workspace_bytes(M, K, N))
+        self._call(self._lib.mpc_beaver_matmul, _ptr(x), _ptr(y), _ptr(a), _ptr(b), _ptr(c), _ptr(z),
+                   ctypes.c_int64(M), ctypes.c_int64(K), ctypes.c_int64(N), int(bool(truncate)),
+                   ctypes.c_uint64(wrap_id), _ptr(ws), ctypes.c_size_t(ws.numel()))
+        return z
+
+    def truncate(self, x: torch.Tensor, bits: Optional[int] = None, wrap_id: int = 0) -> torch.Tensor:
+        """In place; returns x."""
+        n = x[0].numel() if self.all_parties else x.numel()
+        self._call(self._lib.mpc_truncate, _ptr(x), ctypes.c_int64(n), int(bits or self.frac_bits),
+                   ctypes.c_uint64(wrap_id))
+        return x
+
+    def ring_matmul(self, A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
+        M, K = A.shape
+        N = B.shape[1]
+        C = _u64((M, N), self.device)
+        nb = self._lib.mpc_ring_matmul_workspace_bytes(M, K, N)
+        ws = self._workspace(nb)
+        self._call(self._lib.mpc_ring_matmul, _ptr(A), _ptr(B), _ptr(C), ctypes.c_int64(M), ctypes.c_int64(K),
+                   ctypes.c_int64(N), _ptr(ws), ctypes.c_size_t(ws.numel()))
+        return C
+
+    # ------------------------------------------------------------ accounting
+    def stats(self) -> tuple[int, int]:
+        r, b = ctypes.c_uint64(), ctypes.c_uint64()
+        self._lib.mpc_stats(self._h, ctypes.byref(r), ctypes.byref(b))
+        return int(r.value), int(b.value)
+
+    def profile_enable(self, on: bool = True):
+        self._lib.mpc_profile_enable(self._h, int(on))
+
+    def profile_read(self, cls: str) -> tuple[float, int]:
+        ms, n = ctypes.c_double(), ctypes.c_uint64()
+        self._call(self._lib.mpc_profile_read, PROFILE_CLASSES[cls], ctypes.byref(ms), ctypes.byref(n))
+        return float(ms.value), int(n.value)
+
+    def launch_count(self) -> int:
+        return int(self._lib.mpc_launch_count(self._h))
+
+
+def create(world_size: int, rank: int = ALL_PARTIES, **kw) -> Context:
+    return Context(world_size, rank, **kw)

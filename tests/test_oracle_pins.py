@@ -348,3 +348,10 @@ def test_alg1_failure_rate_matches_paper():
     rate = float(np.mean(dg["eta"] != 0))
     sigma = (0.0625 * 0.9375 / n) ** 0.5
     assert abs(rate - 0.0625) < 6 * sigma
+
+
+def test_share_range_matches_full():
+    x = synth.uniform_ring((10, 7), seed=3)
+    full = oracle.share(3, MASTER, x, 1, 21)
+    part = oracle.share(3, MASTER, x[4:6], 1, 21, start=4 * 7)
+    assert np.array_equal(part, full[:, 4:6])
