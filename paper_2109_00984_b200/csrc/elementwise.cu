@@ -111,7 +111,7 @@ cudaError_t launch_mask(const uint64_t* x, const uint64_t* a, int64_t n1, const 
 __global__ void split_left_kernel(LeftSplitArgs a) {
     const int64_t KB = num_kb(a.K);
     const int64_t row_groups = (a.M + 7) / 8;
-    const int64_t kgroups = (a.K + 63) / 64;
+    const int64_t kgroups = (KB * kKBlock + 63) / 64;      // whole padded K: pad limbs must be 0
     const int64_t warps_total = row_groups * kgroups;
     const int lane = threadIdx.x & 31;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < warps_total;
@@ -119,7 +119,7 @@ __global__ void split_left_kernel(LeftSplitArgs a) {
         const int64_t rg = w / kgroups, kg = w % kgroups;
         const int64_t row = rg * 8 + (lane & 7);
         const int64_t k0 = kg * 64 + (lane >> 3) * 16;
-        if (row >= a.M || k0 >= a.K) continue;
+        if (row >= a.M || k0 >= KB * kKBlock) continue;
         const bool full = (k0 + 16 <= a.K);
         uint64_t v[16];
         if (a.Psum > 0) {
@@ -144,7 +144,7 @@ __global__ void split_left_kernel(LeftSplitArgs a) {
 }
 cudaError_t launch_split_left(const LeftSplitArgs& a, cudaStream_t st) {
     if (a.M == 0 || a.K == 0) return cudaSuccess;
-    const int64_t warps = ((a.M + 7) / 8) * ((a.K + 63) / 64);
+    const int64_t warps = ((a.M + 7) / 8) * ((num_kb(a.K) * kKBlock + 63) / 64);
     split_left_kernel<<<grid_for(warps * 32), 256, 0, st>>>(a);
     return cudaGetLastError();
 }
@@ -159,7 +159,7 @@ cudaError_t launch_split_left(const LeftSplitArgs& a, cudaStream_t st) {
 __global__ void split_right_kernel(RightSplitArgs a) {
     const int64_t KB = num_kb(a.K);
     const int64_t ngroups = (a.N + 31) / 32;
-    const int64_t kchunks = (a.K + 15) / 16;
+    const int64_t kchunks = KB * 2;                         // whole padded K
     const int64_t warps_total = ngroups * kchunks;
     const int lane = threadIdx.x & 31;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < warps_total;
@@ -196,7 +196,7 @@ __global__ void split_right_kernel(RightSplitArgs a) {
 }
 cudaError_t launch_split_right(const RightSplitArgs& a, cudaStream_t st) {
     if (a.N == 0 || a.K == 0) return cudaSuccess;
-    const int64_t warps = ((a.N + 31) / 32) * ((a.K + 15) / 16);
+    const int64_t warps = ((a.N + 31) / 32) * (num_kb(a.K) * 2);
     split_right_kernel<<<grid_for(warps * 32), 256, 0, st>>>(a);
     return cudaGetLastError();
 }
@@ -208,14 +208,14 @@ cudaError_t launch_split_right(const RightSplitArgs& a, cudaStream_t st) {
 __global__ void ttp_left_kernel(TtpGenArgs g) {
     const int64_t KB = num_kb(g.K);
     const int64_t row_groups = (g.rows + 7) / 8;
-    const int64_t kgroups = (g.K + 63) / 64;
+    const int64_t kgroups = (KB * kKBlock + 63) / 64;
     const int lane = threadIdx.x & 31;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < row_groups * kgroups;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t rg = w / kgroups, kg = w % kgroups;
         const int64_t row = rg * 8 + (lane & 7);
         const int64_t k0 = kg * 64 + (lane >> 3) * 16;
-        if (row >= g.rows || k0 >= g.K) continue;
+        if (row >= g.rows || k0 >= KB * kKBlock) continue;
         uint64_t sum[16];
 #pragma unroll
         for (int m = 0; m < 16; ++m) sum[m] = 0;
@@ -248,7 +248,7 @@ __global__ void ttp_right_kernel(TtpGenArgs g) {
     const int64_t KB = num_kb(g.K);
     const int64_t N = g.rows;
     const int64_t ngroups = (N + 31) / 32;
-    const int64_t kchunks = (g.K + 15) / 16;
+    const int64_t kchunks = KB * 2;
     const int lane = threadIdx.x & 31;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < ngroups * kchunks;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -280,13 +280,13 @@ __global__ void ttp_right_kernel(TtpGenArgs g) {
 }
 cudaError_t launch_ttp_left(const TtpGenArgs& g, cudaStream_t st) {
     if (g.rows == 0 || g.K == 0) return cudaSuccess;
-    const int64_t warps = ((g.rows + 7) / 8) * ((g.K + 63) / 64);
+    const int64_t warps = ((g.rows + 7) / 8) * ((num_kb(g.K) * kKBlock + 63) / 64);
     ttp_left_kernel<<<grid_for(warps * 32), 256, 0, st>>>(g);
     return cudaGetLastError();
 }
 cudaError_t launch_ttp_right(const TtpGenArgs& g, cudaStream_t st) {
     if (g.rows == 0 || g.K == 0) return cudaSuccess;
-    const int64_t warps = ((g.rows + 31) / 32) * ((g.K + 15) / 16);
+    const int64_t warps = ((g.rows + 31) / 32) * (num_kb(g.K) * 2);
     ttp_right_kernel<<<grid_for(warps * 32), 256, 0, st>>>(g);
     return cudaGetLastError();
 }
