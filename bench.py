@@ -41,7 +41,7 @@ WORKLOAD = "2-party Beaver ring GEMM 4096x4096x4096 (configs[1]), fixed point 2^
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--M", type=int, default=4096)
@@ -62,30 +62,42 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.rows = []
-        self._stop = threading.Event()
+        self._proc = None
         self._t = None
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.rows.append([t.strip() for t in out.stdout.strip().split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+    def _reader(self):
+        for line in self._proc.stdout:
+            t = [v.strip() for v in line.strip().split(",")]
+            if len(t) >= 9:
+                self.rows.append(t)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                           "--format=csv,noheader,nounits", "-lms", "50"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._reader, daemon=True)
+            self._t.start()
+            time.sleep(0.3)          # first sample lands before the timed region starts
+        except Exception:
+            self._proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
+            self._t.join(timeout=5)
+
+    def mark(self):
+        self._mark = len(self.rows)
 
     def summary(self):
+        rows = self.rows[getattr(self, "_mark", 0):] or self.rows[-1:]
+        self.rows = rows
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
         sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
@@ -119,25 +131,42 @@ def load_traffic():
 
 
 # ---------------------------------------------------------------- CPU oracle leg
-def oracle_sample(M, K, N, rows_n, P=2):
-    """Time the CPU oracle (as it stands) on a bounded sample: every party's
-    output rows `rows` of the same workload (full delta reveal, sampled eps rows)."""
-    import oracle
-    rows = np.arange(rows_n, dtype=np.int64)
-    X = synth.uniform_fixed((M, K), 1002)
-    Y = synth.uniform_fixed((K, N), 1003)
-    xs = np.stack([oracle.share(P, synth.MASTER_SEED, X[r], 0, 1, start=int(r) * K) for r in rows], axis=1)
-    ys = oracle.share(P, synth.MASTER_SEED, Y, 1, 2)
-    a, b, c = oracle.ttp_triple(P, synth.MASTER_SEED, 1, M, K, N, rows=rows)
-    t0 = time.perf_counter()
-    z = oracle.beaver_matmul(xs, ys, a, b, c)
-    z = oracle.truncate(z, 16)
-    t = time.perf_counter() - t0
-    cores = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
-    ops = 2.0 * rows_n * K * N
-    return {"value": ops / t / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{rows_n} of {M} output rows of both parties' shares (full {K}x{N} delta reveal), "
-                      f"online Beaver + truncation, {t:.2f} s"}
+class OracleSample:
+    """The CPU oracle (as it stands) on a bounded sample of the workload: both
+    parties' output rows 0..rows_n-1 (full K x N delta reveal, sampled eps
+    rows).  Inputs are prepared once, untimed; run() times the online Beaver
+    matmul + truncation of the sample."""
+
+    def __init__(self, M, K, N, rows_n, P=2):
+        import oracle
+        self.oracle = oracle
+        self.M, self.K, self.N, self.rows_n = M, K, N, rows_n
+        rows = np.arange(rows_n, dtype=np.int64)
+        X = synth.uniform_fixed((M, K), 1002)
+        Y = synth.uniform_fixed((K, N), 1003)
+        self.xs = np.stack([oracle.share(P, synth.MASTER_SEED, X[r], 0, 1, start=int(r) * K) for r in rows], axis=1)
+        self.ys = oracle.share(P, synth.MASTER_SEED, Y, 1, 2)
+        self.a, self.b, self.c = oracle.ttp_triple(P, synth.MASTER_SEED, 1, M, K, N, rows=rows)
+
+    def run(self):
+        t0 = time.perf_counter()
+        z = self.oracle.beaver_matmul(self.xs, self.ys, self.a, self.b, self.c)
+        self.oracle.truncate(z, 16)
+        t = time.perf_counter() - t0
+        cores = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
+        ops = 2.0 * self.rows_n * self.K * self.N
+        return {"value": ops / t / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle", "seconds": t,
+                "sample": f"{self.rows_n} of {self.M} output rows of both parties' shares (full {self.K}x{self.N} "
+                          f"delta reveal), online Beaver + truncation, {t:.2f} s"}
+
+
+def oracle_baseline(M, K, N, target_s=10.0):
+    """cpu_baseline: size the row sample so the timed oracle work is ~target_s."""
+    probe = OracleSample(M, K, N, 8).run()
+    rows_n = int(min(M, max(8, 8 * target_s / max(probe["seconds"], 1e-3))))
+    r = OracleSample(M, K, N, rows_n).run()
+    r.pop("seconds")
+    return r
 
 
 def run_reference(args):
@@ -145,10 +174,11 @@ def run_reference(args):
     if rank != 0:
         return
     M, K, N = args.M, args.K, args.N
-    times = []
     rows_n = max(1, args.sample_rows // 4)
+    sample = OracleSample(M, K, N, rows_n)
+    times = []
     for i in range(args.warmup + args.steps):
-        r = oracle_sample(M, K, N, rows_n)
+        r = sample.run()
         if i >= args.warmup:
             times.append(r)
     v = statistics.median([t["value"] for t in times])
@@ -239,6 +269,7 @@ def main():
     sampler = ClockSampler(local)
     with sampler:
         sync_all()
+        sampler.mark()
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for _ in range(args.steps):
@@ -333,7 +364,7 @@ def main():
     if e2e:
         line["e2e"] = e2e
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = oracle_sample(M, K, N, args.sample_rows)
+        line["cpu_baseline"] = oracle_baseline(M, K, N)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -63,7 +63,9 @@ constexpr int kRowTile = 128;
 constexpr int kKBlock = 32;
 constexpr int kPlaneTileBytes = kRowTile * kKBlock;     // 4096
 
-__host__ __device__ __forceinline__ int64_t pad_rows(int64_t r) { return (r + kRowTile - 1) / kRowTile * kRowTile; }
+// planes are allocated for whole 256-row tiles (one tcgen05 cta_group::2 tile = 2 x 128 rows)
+constexpr int kRowPad = 256;
+__host__ __device__ __forceinline__ int64_t pad_rows(int64_t r) { return (r + kRowPad - 1) / kRowPad * kRowPad; }
 __host__ __device__ __forceinline__ int64_t num_kb(int64_t k) { return (k + kKBlock - 1) / kKBlock; }
 __host__ __device__ __forceinline__ int64_t planes_bytes(int64_t rows, int64_t k) {
     return pad_rows(rows) * num_kb(k) * kKBlock * 8;
