@@ -54,25 +54,37 @@ __host__ __device__ __forceinline__ uint64_t philox_at(uint64_t key, uint64_t st
 // ------------------------------------------------------- limb-plane layout
 // A u64 operand with R rows (M for left operands, N for right operands) and
 // reduction length K is stored as 8 u8 planes (plane l = byte l of every
-// element), K-major, tiled so that one (128-row tile, 32-K block) of all 8
-// planes is 8 contiguous 4 KiB blocks, each already in the UMMA canonical
-// K-major SWIZZLE_NONE layout: [row/8][k/16][row%8][k%16] (core matrices of
-// 8 rows x 16 B; LBO = 128 B between the two K halves, SBO = 256 B between
-// 8-row groups).  Zero padding to 128 rows / 32 K.
-constexpr int kRowTile = 128;
+// element), K-major, blocked so that one (row block, 32-K block) of all 8
+// planes is 8 contiguous blocks, each already in the UMMA canonical K-major
+// SWIZZLE_NONE layout: [row/8][k/16][row%8][k%16] (core matrices of 8 rows x
+// 16 B; LBO = 128 B between the two K halves, SBO = 256 B between 8-row
+// groups).  The row block is what one CTA of a tcgen05 cta_group::2 pair
+// loads per 32-K block:
+//   left  operands (Layout::Left):  128-row blocks (4 KiB per plane),
+//   right operands (Layout::Right):  64-row blocks (2 KiB per plane).
+// Rows are padded to one cluster tile (256 left rows, 128 right rows) and K
+// to 32; the K padding is written as zeros, the row padding is never read
+// into a stored output.
 constexpr int kKBlock = 32;
-constexpr int kPlaneTileBytes = kRowTile * kKBlock;     // 4096
+enum class Layout : int { Left = 0, Right = 1 };
+template <Layout L> struct PlaneGeom;
+template <> struct PlaneGeom<Layout::Left>  { static constexpr int kRows = 128, kBlock = 128 * 32, kPad = 256; };
+template <> struct PlaneGeom<Layout::Right> { static constexpr int kRows = 64, kBlock = 64 * 32, kPad = 128; };
 
-// planes are allocated for whole 256-row tiles (one tcgen05 cta_group::2 tile = 2 x 128 rows)
-constexpr int kRowPad = 256;
-__host__ __device__ __forceinline__ int64_t pad_rows(int64_t r) { return (r + kRowPad - 1) / kRowPad * kRowPad; }
 __host__ __device__ __forceinline__ int64_t num_kb(int64_t k) { return (k + kKBlock - 1) / kKBlock; }
-__host__ __device__ __forceinline__ int64_t planes_bytes(int64_t rows, int64_t k) {
-    return pad_rows(rows) * num_kb(k) * kKBlock * 8;
+template <Layout L>
+__host__ __device__ __forceinline__ int64_t pad_rows(int64_t r) {
+    return (r + PlaneGeom<L>::kPad - 1) / PlaneGeom<L>::kPad * PlaneGeom<L>::kPad;
 }
+template <Layout L>
+__host__ __device__ __forceinline__ int64_t planes_bytes(int64_t rows, int64_t k) {
+    return pad_rows<L>(rows) * num_kb(k) * kKBlock * 8;
+}
+template <Layout L>
 __host__ __device__ __forceinline__ int64_t plane_offset(int64_t row, int64_t k, int limb, int64_t KB) {
-    int64_t rt = row >> 7, rr = row & 127, kb = k >> 5, kk = k & 31;
-    return ((rt * KB + kb) * 8 + limb) * (int64_t)kPlaneTileBytes
+    constexpr int R = PlaneGeom<L>::kRows;
+    const int64_t rb = row / R, rr = row % R, kb = k >> 5, kk = k & 31;
+    return ((rb * KB + kb) * 8 + limb) * (int64_t)PlaneGeom<L>::kBlock
          + (rr >> 3) * 256 + (kk >> 4) * 128 + (rr & 7) * 16 + (kk & 15);
 }
 
@@ -86,6 +98,7 @@ __device__ __forceinline__ void transpose4x4(uint32_t a, uint32_t b, uint32_t c,
 
 // 16 consecutive-k elements of one row -> 8 limb vectors of 16 bytes, stored
 // at their plane positions.  k0 must be a multiple of 16.
+template <Layout L>
 __device__ __forceinline__ void store_limbs16(uint8_t* planes, int64_t row, int64_t k0, int64_t KB,
                                               const uint64_t v[16]) {
     uint32_t w[8][4];  // w[limb][word]
@@ -98,10 +111,11 @@ __device__ __forceinline__ void store_limbs16(uint8_t* planes, int64_t row, int6
 #pragma unroll
         for (int l = 0; l < 4; ++l) { w[l][g] = lo[l]; w[4 + l][g] = hi[l]; }
     }
-    int64_t base = plane_offset(row, k0, 0, KB);
+    int64_t base = plane_offset<L>(row, k0, 0, KB);
 #pragma unroll
     for (int l = 0; l < 8; ++l)
-        *reinterpret_cast<uint4*>(planes + base + (int64_t)l * kPlaneTileBytes) = make_uint4(w[l][0], w[l][1], w[l][2], w[l][3]);
+        *reinterpret_cast<uint4*>(planes + base + (int64_t)l * PlaneGeom<L>::kBlock) =
+            make_uint4(w[l][0], w[l][1], w[l][2], w[l][3]);
 }
 
 // ------------------------------------------------------------ signed helpers

@@ -132,13 +132,13 @@ __global__ void split_left_kernel(LeftSplitArgs a) {
                 for (int m = 0; m < 16; ++m)
                     if (full || k0 + m < a.K) v[m] += pl[m] - (mi ? mi[m] : 0ull);
             }
-            store_limbs16(a.sum_planes, row, k0, KB, v);
+            store_limbs16<Layout::Left>(a.sum_planes, row, k0, KB, v);
         }
         for (int q = 0; q < a.Pcopy; ++q) {
             const uint64_t* src = a.cp_src + q * a.party_stride + row * a.K + k0;
 #pragma unroll
             for (int m = 0; m < 16; ++m) v[m] = (full || k0 + m < a.K) ? src[m] : 0ull;
-            store_limbs16(a.cp_planes + q * a.cp_planes_stride, row, k0, KB, v);
+            store_limbs16<Layout::Left>(a.cp_planes + q * a.cp_planes_stride, row, k0, KB, v);
         }
     }
 }
@@ -180,7 +180,7 @@ __global__ void split_right_kernel(RightSplitArgs a) {
                 if (k < a.K) d[m] += pl[k * a.N + n] - (mi ? mi[k * a.N + n] : 0ull);
             }
         }
-        if (a.sum_planes) store_limbs16(a.sum_planes, n, k0, KB, d);
+        if (a.sum_planes) store_limbs16<Layout::Right>(a.sum_planes, n, k0, KB, d);
         for (int q = 0; q < a.Pcopy; ++q) {
             const uint64_t* src = a.cp_src + q * a.party_stride;
             uint64_t v[16];
@@ -190,7 +190,7 @@ __global__ void split_right_kernel(RightSplitArgs a) {
                 const int64_t k = k0 + m;
                 v[m] = (k < a.K) ? src[k * a.N + n] + (addd ? d[m] : 0ull) : 0ull;
             }
-            store_limbs16(a.cp_planes + q * a.cp_planes_stride, n, k0, KB, v);
+            store_limbs16<Layout::Right>(a.cp_planes + q * a.cp_planes_stride, n, k0, KB, v);
         }
     }
 }
@@ -239,7 +239,7 @@ __global__ void ttp_left_kernel(TtpGenArgs g) {
                 }
             }
         }
-        if (g.sum_planes) store_limbs16(g.sum_planes, row, k0, KB, sum);
+        if (g.sum_planes) store_limbs16<Layout::Left>(g.sum_planes, row, k0, KB, sum);
     }
 }
 // Right factor b (K x N row-major): b_q = G(k_ttp, B||q||id)[k*N + n];
@@ -275,7 +275,7 @@ __global__ void ttp_right_kernel(TtpGenArgs g) {
                 }
             }
         }
-        if (g.sum_planes) store_limbs16(g.sum_planes, n, k0, KB, sum);
+        if (g.sum_planes) store_limbs16<Layout::Right>(g.sum_planes, n, k0, KB, sum);
     }
 }
 cudaError_t launch_ttp_left(const TtpGenArgs& g, cudaStream_t st) {

@@ -108,6 +108,9 @@ mpc_status enter(mpc_ctx c) {
 bool one_party_comm(mpc_ctx c) { return !c->all && c->P > 1; }
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+// limb-plane buffer sizes of left (M x K) and right (N x K) ring-GEMM operands
+inline int64_t lp(int64_t rows, int64_t k) { return planes_bytes<Layout::Left>(rows, k); }
+inline int64_t rp(int64_t rows, int64_t k) { return planes_bytes<Layout::Right>(rows, k); }
 
 struct Carve {
     uint8_t* base; size_t off = 0;
@@ -128,10 +131,10 @@ BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N) {
     const int Pl = c->all ? c->P : 1;
     Carve cv(ws);
     BeaverWs w{};
-    w.eps_pl = cv.take(planes_bytes(M, K));
-    w.delta_pl = cv.take(planes_bytes(N, K));
-    w.a_pl = cv.take((size_t)Pl * planes_bytes(M, K));
-    w.b_pl = cv.take((size_t)Pl * planes_bytes(N, K));
+    w.eps_pl = cv.take(lp(M, K));
+    w.delta_pl = cv.take(rp(N, K));
+    w.a_pl = cv.take((size_t)Pl * lp(M, K));
+    w.b_pl = cv.take((size_t)Pl * rp(N, K));
     w.ed = reinterpret_cast<uint64_t*>(c->all ? nullptr : cv.take(8 * (size_t)(M * K + K * N)));
     const bool alg1_one = !c->all && c->P > 2;
     w.zbuf = reinterpret_cast<uint64_t*>(alg1_one ? cv.take(8 * (size_t)(M * N)) : nullptr);
@@ -141,7 +144,7 @@ BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N) {
 }
 
 mpc_status gemm_run(mpc_ctx c, RingGemmParams& p, int parties) {
-    for (int q = 0; q < 4; ++q) p.kb_chunk[q] = ring_gemm_kb_chunk(q);
+    p.kc = ring_gemm_default_kc(p.seg[0].kb + (p.nseg > 1 ? p.seg[1].kb : 0));
     return run(c, kClsGemm, "ring_gemm", [&] { return ring_gemm_launch(p, parties, c->stream); });
 }
 
@@ -307,7 +310,7 @@ mpc_status mpc_reveal(mpc_ctx c, const uint64_t* share, uint64_t* out, int64_t n
 size_t mpc_ttp_workspace_bytes(mpc_ctx c, int64_t M, int64_t K, int64_t N) {
     (void)c;
     if (M < 0 || K < 0 || N < 0) return 0;
-    return align256(planes_bytes(M, K)) + align256(planes_bytes(N, K));
+    return align256(lp(M, K)) + align256(rp(N, K));
 }
 
 mpc_status mpc_ttp_triples(mpc_ctx c, uint64_t id, int64_t M, int64_t K, int64_t N, uint64_t* a, uint64_t* b,
@@ -320,8 +323,8 @@ mpc_status mpc_ttp_triples(mpc_ctx c, uint64_t id, int64_t M, int64_t K, int64_t
     if (ttp && !ws && (M * K + K * N) > 0) return fail(c, MPC_ERR_ARG, "ttp_triples: null workspace");
     const int lo = c->all ? 0 : c->rank, hi = c->all ? c->P : c->rank + 1;
     Carve cv(ws);
-    uint8_t* a_pl = ttp ? cv.take(planes_bytes(M, K)) : nullptr;
-    uint8_t* b_pl = ttp ? cv.take(planes_bytes(N, K)) : nullptr;
+    uint8_t* a_pl = ttp ? cv.take(lp(M, K)) : nullptr;
+    uint8_t* b_pl = ttp ? cv.take(rp(N, K)) : nullptr;
     TtpGenArgs ga{c->kttp, id, kTagA, c->P, M, K, lo, hi, a, a_pl};
     CHECK(run(c, kClsPrg, "ttp_a", [&] { return launch_ttp_left(ga, c->stream); }));
     TtpGenArgs gb{c->kttp, id, kTagB, c->P, N, K, lo, hi, b, b_pl};
@@ -374,9 +377,9 @@ mpc_status mpc_beaver_matmul(mpc_ctx c, const uint64_t* x, const uint64_t* y, co
         return fail(c, MPC_ERR_ARG, "beaver_matmul: null pointer");
     const int64_t sMK = M * K, sKN = K * N, sMN = M * N;
     if (c->all) {
-        LeftSplitArgs L{M, K, sMK, x, a, c->P, w.eps_pl, a, c->P, w.a_pl, planes_bytes(M, K)};
+        LeftSplitArgs L{M, K, sMK, x, a, c->P, w.eps_pl, a, c->P, w.a_pl, lp(M, K)};
         CHECK(run(c, kClsSplit, "mask+reveal+split eps", [&] { return launch_split_left(L, c->stream); }));
-        RightSplitArgs R{K, N, sKN, y, b, c->P, w.delta_pl, b, c->P, 1, w.b_pl, planes_bytes(N, K)};
+        RightSplitArgs R{K, N, sKN, y, b, c->P, w.delta_pl, b, c->P, 1, w.b_pl, rp(N, K)};
         CHECK(run(c, kClsSplit, "mask+reveal+split delta", [&] { return launch_split_right(R, c->stream); }));
     } else {
         CHECK(run(c, kClsSplit, "mask", [&] { return launch_mask(x, a, sMK, y, b, sKN, w.ed, c->stream); }));
@@ -387,8 +390,8 @@ mpc_status mpc_beaver_matmul(mpc_ctx c, const uint64_t* x, const uint64_t* y, co
         CHECK(run(c, kClsSplit, "split delta", [&] { return launch_split_right(R, c->stream); }));
     }
     RingGemmParams p{};
-    p.seg[0] = RingGemmSegment{w.a_pl, w.delta_pl, (int)num_kb(K), planes_bytes(M, K), 0};   // a_p @ delta
-    p.seg[1] = RingGemmSegment{w.eps_pl, w.b_pl, (int)num_kb(K), 0, planes_bytes(N, K)};     // eps @ b'_p
+    p.seg[0] = RingGemmSegment{w.a_pl, w.delta_pl, (int)num_kb(K), lp(M, K), 0};   // a_p @ delta
+    p.seg[1] = RingGemmSegment{w.eps_pl, w.b_pl, (int)num_kb(K), 0, rp(N, K)};     // eps @ b'_p
     p.nseg = 2;
     p.M = M; p.N = N; p.C = cc; p.Z = z;
     p.party_stride_c = p.party_stride_z = sMN;
@@ -416,7 +419,7 @@ mpc_status mpc_truncate(mpc_ctx c, uint64_t* x, int64_t n, int bits, uint64_t wr
 
 size_t mpc_ring_matmul_workspace_bytes(int64_t M, int64_t K, int64_t N) {
     if (M < 0 || K < 0 || N < 0) return 0;
-    return align256(planes_bytes(M, K)) + align256(planes_bytes(N, K));
+    return align256(lp(M, K)) + align256(rp(N, K));
 }
 
 mpc_status mpc_ring_matmul(mpc_ctx c, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t M, int64_t K,
@@ -427,8 +430,8 @@ mpc_status mpc_ring_matmul(mpc_ctx c, const uint64_t* A, const uint64_t* B, uint
     if (M == 0 || N == 0) return MPC_OK;
     if (!C || (K && (!A || !B || !ws))) return fail(c, MPC_ERR_ARG, "ring_matmul: null pointer");
     Carve cv(ws);
-    uint8_t* a_pl = cv.take(planes_bytes(M, K));
-    uint8_t* b_pl = cv.take(planes_bytes(N, K));
+    uint8_t* a_pl = cv.take(lp(M, K));
+    uint8_t* b_pl = cv.take(rp(N, K));
     LeftSplitArgs L{M, K, 0, A, nullptr, 1, a_pl, nullptr, 0, nullptr, 0};
     CHECK(run(c, kClsSplit, "split A", [&] { return launch_split_left(L, c->stream); }));
     RightSplitArgs R{K, N, 0, B, nullptr, 1, b_pl, nullptr, 0, 0, nullptr, 0};

@@ -10,29 +10,35 @@
 // segments: (a_p, delta) and (eps, b_p + [p=0] delta), i.e.
 //     z_p = c_p + a_p @ delta + eps @ b'_p.
 //
-// Exactness: acc_s <= (s+1) * K_r * 255^2.  The s32
-// accumulator wraps mod 2^32 (no .sat), so reading it as u32 is exact while
-// acc_s < 2^32; for s >= 4 only acc_s mod 2^(64-8s) <= 2^32 matters, so the
-// wrap is harmless.  The host splits K into chunks of at most
-// floor((2^32-1) / ((s+1) * 65025)) for the low shift s of each pass and the
-// epilogue drains every chunk into the u64 result.
+// Exactness: acc_s <= (s+1) * K_r * 255^2 where K_r is
+// the reduction length of one accumulation unit.  The s32 accumulator wraps
+// mod 2^32 (no .sat), so reading it as u32 is exact while acc_s < 2^32, i.e.
+// K_r <= 16512 for s = 3; for s >= 4 only acc_s mod 2^(64-8s) <= 2^32 matters,
+// so the wrap is harmless.  Every unit covers at most ring_gemm_max_kc() 32-K
+// blocks and is drained into a u64 running sum.
 //
-// Schedule.  A cluster of 2 CTAs (one per SM of a TPC) computes a 256 x 256
-// output tile with tcgen05.mma.cta_group::2 (UMMA M = 256, N = 256, K = 32):
-// CTA r holds rows 128r..128r+127 of the left planes and rows 128r..+127 of
-// the right planes of the tile in its shared memory, and its half of the
-// accumulator (128 TMEM lanes) — each CTA moves half the operand bytes of a
-// 1-CTA 128 x 256 tile for twice the MACs.  The 36 limb products are issued as
-// 4 passes q = 0..3, each accumulating the shift pair {q, 7-q} (q+1 + 8-q = 9
-// MMAs per 32-K block) into two 256-column TMEM accumulators (all 512
-// columns); a pass needs only limb planes 0..7-q.  The kernel is persistent:
-// 74 clusters walk the tiles in a grouped order (parties and 4 row tiles
-// innermost) so concurrently running clusters share operand planes in L2.
+// Schedule.  A cluster of 2 CTAs (one TPC) computes a 256 x 128 output tile
+// with tcgen05.mma.cta_group::2 (UMMA M = 256, N = 128, K = 32): CTA r holds
+// rows 128r..128r+127 of the left planes (4 KiB per plane and 32-K block) and
+// rows 64r..64r+63 of the right planes (2 KiB) in shared memory, and its
+// 128-lane half of the accumulators.  TMEM (512 columns) holds 4 accumulators
+// of 128 columns, so the 8 shifts run as 2 super-passes per K chunk:
+// {0, 7, 1, 6} (18 MMAs per 32-K block, limb planes 0..7) and {2, 5, 3, 4}
+// (18 MMAs, planes 0..5) — 14 plane loads per 32-K block instead of the 26 a
+// 2-accumulator schedule needs, which keeps the per-SM L2->SM feed at about
+// 36 B/clk for 8192 MAC/clk.  Units (K chunk, super-pass) are ordered chunk
+// major so the second super-pass re-reads a K window still resident in L2.
+// The u64 running sum of a tile lives in the registers of 8 epilogue warps
+// (64 columns x 1 row per thread; setmaxnreg gives them 224 registers) and is
+// written once, with the Beaver c_p addend and the fused truncation, at the
+// tile end.  The kernel is persistent: 74 clusters walk the tiles in a grouped
+// order (4 row tiles x all column tiles x parties per group).
 //
-// Warp roles (256 threads per CTA): warp 0 = bulk-copy producer (both CTAs),
+// Warp roles (384 threads per CTA): warp 0 = bulk-copy producer (both CTAs),
 // warp 1 = MMA issuer (leader CTA) / stage relay (peer CTA), warp 2 = TMEM
-// allocator, warps 4..7 = epilogue (one TMEM lane = one output row per thread).
+// allocator, warps 4..11 = epilogue.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include "common.cuh"
 #include "ring_gemm.h"
@@ -40,17 +46,22 @@
 namespace mpc {
 namespace gemm {
 
-constexpr int kTileM = 256;              // UMMA M (cta_group::2): 128 rows per CTA
-constexpr int kTileN = 256;              // UMMA N: 128 right-operand rows per CTA
-constexpr int kHalfBytes = 8 * kPlaneTileBytes;        // 8 planes x (128 rows x 32 K) = 32 KiB
-constexpr int kStageBytes = 2 * kHalfBytes;            // A + B planes of one 32-K block = 64 KiB
-constexpr int kStages = 3;
-constexpr int kThreads = 256;
+using GL = PlaneGeom<Layout::Left>;
+using GR = PlaneGeom<Layout::Right>;
+constexpr int kTileM = 256;                       // UMMA M (cta_group::2): 128 rows per CTA
+constexpr int kTileN = 128;                       // UMMA N: 64 right-operand rows per CTA
+constexpr int kAStage = 8 * GL::kBlock;           // 32 KiB
+constexpr int kBStage = 8 * GR::kBlock;           // 16 KiB
+constexpr int kStageBytes = kAStage + kBStage;    // 48 KiB
+constexpr int kStages = 4;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 128 + 32 * kEpiWarps;    // 384
 constexpr int kTmemCols = 512;
-constexpr int kGroupM = 4;               // row tiles per scheduling group
-constexpr uint32_t kIdesc = (2u << 4)            // D format: S32
-                          | (0u << 7)            // A: unsigned 8-bit
-                          | (0u << 10)           // B: unsigned 8-bit
+constexpr int kGroupM = 4;                        // row tiles per scheduling group
+constexpr int kPasses = 2;                        // super-passes of 4 shifts each
+constexpr uint32_t kIdesc = (2u << 4)             // D format: S32
+                          | (0u << 7)             // A: unsigned 8-bit
+                          | (0u << 10)            // B: unsigned 8-bit
                           | ((uint32_t)(kTileN >> 3) << 17)
                           | ((uint32_t)(kTileM >> 4) << 24);
 
@@ -131,15 +142,12 @@ __device__ __forceinline__ void mma_u8_2cta(uint32_t tmem_d, uint64_t adesc, uin
         "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}"
         :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate) : "memory");
 }
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -161,32 +169,188 @@ struct TileMap {
     }
 };
 
-__device__ __forceinline__ int total_kb(const RingGemmParams& p) { return p.seg[0].kb + (p.nseg > 1 ? p.seg[1].kb : 0); }
+struct Bars {
+    uint8_t* stage_base;
+    uint64_t *full, *empty, *tfull, *tempty;
+};
+
+// Super-pass g accumulates 4 shifts into TMEM slots 0..3 (128 columns each):
+// g = 0: shifts {0, 7, 1, 6} (1+8+2+7 = 18 MMAs per 32-K block, planes 0..7)
+// g = 1: shifts {2, 5, 3, 4} (3+6+4+5 = 18 MMAs per 32-K block, planes 0..5)
+__device__ __forceinline__ int slot_shift(int g, int a) {
+    return g == 0 ? ((a & 1) ? 7 - (a >> 1) : (a >> 1)) : ((a & 1) ? 5 - (a >> 1) : 2 + (a >> 1));
+}
+__device__ __forceinline__ int pass_planes(int g) { return g == 0 ? 8 : 6; }
+
+// ---------------------------------------------------------------- control warpgroup
+__device__ __forceinline__ void control_roles(const RingGemmParams& p, const TileMap& tm, int ntiles, int tkb, int kc,
+                                              int nchunks, int warp, int lane, uint32_t rank, uint32_t tmem_base,
+                                              const Bars& B) {
+    const bool leader = rank == 0;
+    if (warp == 0 && lane == 0) {
+        // ------------------------------------------------ producer (both CTAs: own halves)
+        int s = 0; uint32_t ph = 0;
+        for (int t = cluster_id(); t < ntiles; t += nclusters()) {
+            int party, m, n;
+            tm.decode(t, party, m, n);
+            const int64_t rbA = (int64_t)m * 2 + rank;       // 128-row left block
+            const int64_t rbB = (int64_t)n * 2 + rank;       // 64-row right block
+            for (int c = 0; c < nchunks; ++c) {
+                const int k0 = c * kc, k1 = min(tkb, k0 + kc);
+                for (int g = 0; g < kPasses; ++g) {
+                    const uint32_t bytesA = (uint32_t)pass_planes(g) * GL::kBlock;
+                    const uint32_t bytesB = (uint32_t)pass_planes(g) * GR::kBlock;
+                    for (int kt = k0; kt < k1; ++kt) {
+                        const int sg = (kt < p.seg[0].kb) ? 0 : 1;
+                        const RingGemmSegment& S = p.seg[sg];
+                        const int kb = kt - (sg ? p.seg[0].kb : 0);
+                        const uint8_t* srcA = S.A + party * S.party_stride_A + (rbA * S.kb + kb) * (8 * GL::kBlock);
+                        const uint8_t* srcB = S.B + party * S.party_stride_B + (rbB * S.kb + kb) * (8 * GR::kBlock);
+                        mbar_wait(&B.empty[s], ph ^ 1);
+                        mbar_expect_tx(&B.full[s], bytesA + bytesB);
+                        uint8_t* st = B.stage_base + s * kStageBytes;
+                        bulk_g2s(st, srcA, bytesA, &B.full[s]);
+                        bulk_g2s(st + kAStage, srcB, bytesB, &B.full[s]);
+                        if (++s == kStages) { s = 0; ph ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1 && lane == 0 && !leader) {
+        // ------------------------------------------------ peer: relay "stage full" to the leader
+        int s = 0; uint32_t ph = 0;
+        const uint32_t leader_full0 = mapa(smem_u32(&B.full[0]), 0);
+        for (int t = cluster_id(); t < ntiles; t += nclusters())
+            for (int i = 0; i < kPasses * tkb; ++i) {
+                mbar_wait(&B.full[s], ph);
+                mbar_arrive_cluster(leader_full0 + s * 8);
+                if (++s == kStages) { s = 0; ph ^= 1; }
+            }
+    } else if (warp == 1 && lane == 0) {
+        // ------------------------------------------------ leader: MMA issuer (one thread)
+        int s = 0; uint32_t ph = 0; uint32_t u = 0;
+        for (int t = cluster_id(); t < ntiles; t += nclusters()) {
+            for (int c = 0; c < nchunks; ++c) {
+                const int k0 = c * kc, k1 = min(tkb, k0 + kc);
+                for (int g = 0; g < kPasses; ++g, ++u) {
+                    mbar_wait_cluster(B.tempty, (u & 1) ^ 1);        // both epilogues drained TMEM
+                    tc_fence_after();
+                    for (int kt = k0; kt < k1; ++kt) {
+                        mbar_wait_cluster(&B.full[s], ph);
+                        tc_fence_after();
+                        const uint32_t a0 = smem_u32(B.stage_base + s * kStageBytes);
+                        const uint32_t b0 = a0 + kAStage;
+                        const bool first = (kt == k0);
+#pragma unroll
+                        for (int a = 0; a < 4; ++a) {
+                            const int sh = slot_shift(g, a);
+                            const uint32_t d = tmem_base + a * 128;
+                            for (int i = 0; i <= sh; ++i)
+                                mma_u8_2cta(d, smem_desc(a0 + i * GL::kBlock), smem_desc(b0 + (sh - i) * GR::kBlock),
+                                            !(first && i == 0));
+                        }
+                        tc_commit_both(&B.empty[s]);
+                        if (++s == kStages) { s = 0; ph ^= 1; }
+                    }
+                    tc_commit_both(B.tfull);
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- epilogue warpgroups
+__device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const TileMap& tm, int ntiles, int nchunks,
+                                              int warp, int lane, uint32_t rank, uint32_t tmem_base, const Bars& B) {
+    const int wq = warp & 3;                       // TMEM lane quadrant of this warp
+    const int half = (warp - 4) >> 2;              // column half: 64 columns each
+    const int row = wq * 32 + lane;
+    const uint32_t tempty_leader = mapa(smem_u32(B.tempty), 0);
+    const bool vec = (p.N & 1) == 0;
+    const uint32_t tbase = tmem_base + ((uint32_t)(wq * 32) << 16) + half * 64;
+    uint32_t u = 0;
+    for (int t = cluster_id(); t < ntiles; t += nclusters()) {
+        int party, m, n;
+        tm.decode(t, party, m, n);
+        uint64_t run[64];
+#pragma unroll
+        for (int j = 0; j < 64; ++j) run[j] = 0;
+        for (int c = 0; c < nchunks; ++c) {
+            for (int g = 0; g < kPasses; ++g, ++u) {
+                mbar_wait(B.tfull, u & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int a = 0; a < 4; a += 2) {
+                    const int s0 = 8 * slot_shift(g, a), s1 = 8 * slot_shift(g, a + 1);
+#pragma unroll
+                    for (int cc = 0; cc < 64; cc += 16) {
+                        uint32_t v0[16], v1[16];
+                        tmem_ld16(tbase + a * 128 + cc, v0);
+                        tmem_ld16(tbase + (a + 1) * 128 + cc, v1);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            run[cc + j] += ((uint64_t)v0[j] << s0) + ((uint64_t)v1[j] << s1);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tempty_leader);
+            }
+        }
+        // tile end: z = trunc(c + sum of all units) — one write per element
+        const int64_t grow = (int64_t)m * kTileM + rank * 128 + row;
+        if (grow < p.M) {
+            uint64_t* zrow = p.Z + party * p.party_stride_z + grow * p.N;
+            const uint64_t* crow = p.C ? p.C + party * p.party_stride_c + grow * p.N : nullptr;
+            const int64_t gc0 = (int64_t)n * kTileN + half * 64;
+            if (vec && gc0 + 64 <= p.N) {
+#pragma unroll
+                for (int j = 0; j < 64; j += 2) {
+                    ulonglong2 v = crow ? *reinterpret_cast<const ulonglong2*>(crow + gc0 + j) : make_ulonglong2(0, 0);
+                    v.x += run[j]; v.y += run[j + 1];
+                    if (p.trunc_bits) { v.x = div_pow2_round(v.x, p.trunc_bits); v.y = div_pow2_round(v.y, p.trunc_bits); }
+                    *reinterpret_cast<ulonglong2*>(zrow + gc0 + j) = v;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 64; ++j) {
+                    if (gc0 + j < p.N) {
+                        uint64_t v = (crow ? crow[gc0 + j] : 0ull) + run[j];
+                        if (p.trunc_bits) v = div_pow2_round(v, p.trunc_bits);
+                        zrow[gc0 + j] = v;
+                    }
+                }
+            }
+        }
+    }
+}
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* stage_base = smem;
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-    uint64_t* empty_bar = full_bar + kStages;
-    uint64_t* tfull_bar = empty_bar + kStages;
-    uint64_t* tempty_bar = tfull_bar + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 1);
+    Bars B;
+    B.stage_base = smem;
+    B.full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    B.empty = B.full + kStages;
+    B.tfull = B.empty + kStages;
+    B.tempty = B.tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(B.tempty + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
     const bool leader = (rank == 0);
-    const TileMap tm{parties, (int)(pad_rows(p.M) / kTileM), (int)(pad_rows(p.N) / kTileN)};
+    const TileMap tm{parties, (int)(pad_rows<Layout::Left>(p.M) / kTileM), (int)(pad_rows<Layout::Right>(p.N) / kTileN)};
     const int ntiles = tm.parties * tm.mt * tm.nt;
-    const int tkb = total_kb(p);
-    int nunits = 0;
-    for (int q = 0; q < 4; ++q) nunits += (tkb + p.kb_chunk[q] - 1) / p.kb_chunk[q];
+    const int tkb = p.seg[0].kb + (p.nseg > 1 ? p.seg[1].kb : 0);
+    const int kc = p.kc;
+    const int nchunks = (tkb + kc - 1) / kc;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) { mbar_init(&full_bar[s], leader ? 2 : 1); mbar_init(&empty_bar[s], 1); }
-        mbar_init(tfull_bar, 1);
-        mbar_init(tempty_bar, 8);          // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+        for (int s = 0; s < kStages; ++s) { mbar_init(&B.full[s], leader ? 2 : 1); mbar_init(&B.empty[s], 1); }
+        mbar_init(B.tfull, 1);
+        mbar_init(B.tempty, 2 * kEpiWarps);   // both CTAs' epilogue warps (leader's copy is used)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
@@ -198,159 +362,13 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-
-    if (warp == 0) {
-        // ------------------------------------------------ producer (both CTAs: own halves)
-        if (lane == 0) {
-            int s = 0; uint32_t ph = 0;
-            for (int t = cluster_id(); t < ntiles; t += nclusters()) {
-                int party, m, n;
-                tm.decode(t, party, m, n);
-                const int64_t rtA = (int64_t)m * 2 + rank, rtB = (int64_t)n * 2 + rank;
-                for (int q = 0; q < 4; ++q) {
-                    const uint32_t bytes = (uint32_t)(8 - q) * kPlaneTileBytes;
-                    for (int kt = 0; kt < tkb; ++kt) {
-                        const int sg = (kt < p.seg[0].kb) ? 0 : 1;
-                        const RingGemmSegment& S = p.seg[sg];
-                        const int kb = kt - (sg ? p.seg[0].kb : 0);
-                        const uint8_t* srcA = S.A + party * S.party_stride_A + (rtA * S.kb + kb) * kHalfBytes;
-                        const uint8_t* srcB = S.B + party * S.party_stride_B + (rtB * S.kb + kb) * kHalfBytes;
-                        mbar_wait(&empty_bar[s], ph ^ 1);
-                        mbar_expect_tx(&full_bar[s], 2 * bytes);
-                        uint8_t* st = stage_base + s * kStageBytes;
-                        bulk_g2s(st, srcA, bytes, &full_bar[s]);
-                        bulk_g2s(st + kHalfBytes, srcB, bytes, &full_bar[s]);
-                        if (++s == kStages) { s = 0; ph ^= 1; }
-                    }
-                }
-            }
-        }
-    } else if (warp == 1 && !leader) {
-        // ------------------------------------------------ peer: relay "stage full" to the leader
-        if (lane == 0) {
-            int s = 0; uint32_t ph = 0;
-            const uint32_t leader_full0 = mapa(smem_u32(&full_bar[0]), 0);
-            for (int t = cluster_id(); t < ntiles; t += nclusters())
-                for (int i = 0; i < 4 * tkb; ++i) {
-                    mbar_wait(&full_bar[s], ph);
-                    mbar_arrive_cluster(leader_full0 + s * 8);
-                    if (++s == kStages) { s = 0; ph ^= 1; }
-                }
-        }
-    } else if (warp == 1) {
-        // ------------------------------------------------ leader: MMA issuer (one thread)
-        if (lane == 0) {
-            int s = 0; uint32_t ph = 0; uint32_t uph = 0;
-            const uint32_t d_lo = tmem_base;             // shift q
-            const uint32_t d_hi = tmem_base + 256;       // shift 7-q
-            for (int t = cluster_id(); t < ntiles; t += nclusters()) {
-                for (int q = 0; q < 4; ++q) {
-                    const int chunk = p.kb_chunk[q];
-                    for (int c0 = 0; c0 < tkb; c0 += chunk) {
-                        const int c1 = min(tkb, c0 + chunk);
-                        mbar_wait_cluster(tempty_bar, uph ^ 1);      // both epilogues drained TMEM
-                        uph ^= 1;
-                        tc_fence_after();
-                        for (int kt = c0; kt < c1; ++kt) {
-                            mbar_wait_cluster(&full_bar[s], ph);
-                            tc_fence_after();
-                            const uint32_t a0 = smem_u32(stage_base + s * kStageBytes);
-                            const uint32_t b0 = a0 + kHalfBytes;
-                            const uint32_t first = (kt == c0);
-                            for (int i = 0; i <= q; ++i)
-                                mma_u8_2cta(d_lo, smem_desc(a0 + i * kPlaneTileBytes),
-                                            smem_desc(b0 + (q - i) * kPlaneTileBytes), !(first && i == 0));
-                            for (int i = 0; i <= 7 - q; ++i)
-                                mma_u8_2cta(d_hi, smem_desc(a0 + i * kPlaneTileBytes),
-                                            smem_desc(b0 + (7 - q - i) * kPlaneTileBytes), !(first && i == 0));
-                            tc_commit_both(&empty_bar[s]);
-                            if (++s == kStages) { s = 0; ph ^= 1; }
-                        }
-                        tc_commit_both(tfull_bar);
-                    }
-                }
-            }
-        }
-    } else if (warp >= 4) {
-        // ------------------------------------------------ epilogue (both CTAs, own 128 rows)
-        const int wq = warp & 3;
-        const int row = wq * 32 + lane;
-        const uint32_t tempty_leader = mapa(smem_u32(tempty_bar), 0);
-        const bool vec = (p.N & 1) == 0;
-        uint32_t uph = 0;
-        for (int t = cluster_id(); t < ntiles; t += nclusters()) {
-            int party, m, n;
-            tm.decode(t, party, m, n);
-            const int64_t grow = (int64_t)m * kTileM + rank * 128 + row;
-            const bool row_ok = grow < p.M;
-            uint64_t* zrow = p.Z + party * p.party_stride_z + grow * p.N;
-            const uint64_t* crow = p.C ? p.C + party * p.party_stride_c + grow * p.N : nullptr;
-            const int64_t col0 = (int64_t)n * kTileN;
-            int unit = 0;
-            for (int q = 0; q < 4; ++q) {
-                const int chunk = p.kb_chunk[q];
-                for (int c0 = 0; c0 < tkb; c0 += chunk, ++unit) {
-                    const bool first_unit = (unit == 0), last_unit = (unit == nunits - 1);
-                    mbar_wait(tfull_bar, uph);
-                    uph ^= 1;
-                    tc_fence_after();
-                    const uint32_t t_lo = tmem_base + ((uint32_t)(wq * 32) << 16);
-                    const uint32_t t_hi = t_lo + 256;
-                    for (int cc = 0; cc < kTileN; cc += 32) {
-                        uint32_t lo[32], hi[32];
-                        tmem_ld32(t_lo + cc, lo);
-                        tmem_ld32(t_hi + cc, hi);
-                        tmem_wait_ld();
-                        if (!row_ok) continue;
-                        const int64_t gc0 = col0 + cc;
-                        if (vec && gc0 + 32 <= p.N) {
-#pragma unroll
-                            for (int j = 0; j < 32; j += 2) {
-                                const uint64_t v0 = ((uint64_t)lo[j] << (8 * q)) + ((uint64_t)hi[j] << (8 * (7 - q)));
-                                const uint64_t v1 = ((uint64_t)lo[j + 1] << (8 * q)) + ((uint64_t)hi[j + 1] << (8 * (7 - q)));
-                                ulonglong2 cur;
-                                if (first_unit) {
-                                    cur = crow ? *reinterpret_cast<const ulonglong2*>(crow + gc0 + j) : make_ulonglong2(0, 0);
-                                } else {
-                                    cur = *reinterpret_cast<const ulonglong2*>(zrow + gc0 + j);
-                                }
-                                cur.x += v0; cur.y += v1;
-                                if (last_unit && p.trunc_bits) {
-                                    cur.x = div_pow2_round(cur.x, p.trunc_bits);
-                                    cur.y = div_pow2_round(cur.y, p.trunc_bits);
-                                }
-                                *reinterpret_cast<ulonglong2*>(zrow + gc0 + j) = cur;
-                            }
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) {
-                                const int64_t gc = gc0 + j;
-                                if (gc < p.N) {
-                                    const uint64_t v = ((uint64_t)lo[j] << (8 * q)) + ((uint64_t)hi[j] << (8 * (7 - q)));
-                                    uint64_t cur = first_unit ? (crow ? crow[gc] : 0ull) : zrow[gc];
-                                    cur += v;
-                                    if (last_unit && p.trunc_bits) cur = div_pow2_round(cur, p.trunc_bits);
-                                    zrow[gc] = cur;
-                                }
-                            }
-                        }
-                    }
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_cluster(tempty_leader);
-                }
-            }
-            if (nunits == 0 && row_ok) {       // K == 0: Z = C (then truncated)
-                for (int j = 0; j < kTileN; ++j) {
-                    const int64_t gc = col0 + j;
-                    if (gc < p.N) {
-                        uint64_t cur = crow ? crow[gc] : 0ull;
-                        if (p.trunc_bits) cur = div_pow2_round(cur, p.trunc_bits);
-                        zrow[gc] = cur;
-                    }
-                }
-            }
-        }
+    // register budget: the control warpgroup needs few, the epilogue holds 64 u64 sums per thread
+    if (warp < 4) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+        control_roles(p, tm, ntiles, tkb, kc, nchunks, warp, lane, rank, tmem_base, B);
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+        epilogue_role(p, tm, ntiles, nchunks, warp, lane, rank, tmem_base, B);
     }
     __syncwarp();
     tc_fence_before();
@@ -363,10 +381,26 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
 
 }  // namespace gemm
 
-int ring_gemm_kb_chunk(int q) {
-    // largest K_r with (q+1) * K_r * 255^2 <= 2^32 - 1, in 32-K blocks
-    const uint64_t lim = 0xFFFFFFFFull / ((uint64_t)(q + 1) * 65025ull);
+int ring_gemm_max_kc() {
+    // largest K_r with 4 * K_r * 255^2 <= 2^32 - 1 (shift 3, the tightest exact one), in 32-K blocks
+    const uint64_t lim = 0xFFFFFFFFull / (4ull * 65025ull);
     return (int)(lim / kKBlock);
+}
+
+int ring_gemm_default_kc(int total_kb) {
+    // 64 blocks = 2048 K per unit: long enough that the TMEM drain between units
+    // costs ~2% of the MMA time, short enough that the concurrent clusters' K
+    // window stays in L2 for the second super-pass.  Short reductions run as
+    // one chunk.  MPC_GEMM_KC overrides (tuning experiments).
+    static int env_kc = -1;
+    if (env_kc < 0) {
+        const char* e = getenv("MPC_GEMM_KC");
+        env_kc = e ? atoi(e) : 0;
+    }
+    int kc = env_kc > 0 ? env_kc : 64;
+    if (total_kb <= kc + kc / 2) kc = total_kb;
+    if (kc > ring_gemm_max_kc()) kc = ring_gemm_max_kc();
+    return kc < 1 ? 1 : kc;
 }
 
 size_t ring_gemm_smem_bytes() {
@@ -383,9 +417,11 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
         if (e != cudaSuccess) return e;
         attr_dev = dev;
     }
+    if (prm.kc < 1 || prm.kc > ring_gemm_max_kc()) return cudaErrorInvalidValue;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t tiles = (int64_t)parties * (pad_rows(prm.M) / gemm::kTileM) * (pad_rows(prm.N) / gemm::kTileN);
+    const int64_t tiles = (int64_t)parties * (pad_rows<Layout::Left>(prm.M) / gemm::kTileM) *
+                          (pad_rows<Layout::Right>(prm.N) / gemm::kTileN);
     int64_t clusters = sms / 2;
     if (tiles < clusters) clusters = tiles;
     if (clusters < 1) clusters = 1;

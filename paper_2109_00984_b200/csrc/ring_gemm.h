@@ -6,8 +6,8 @@
 namespace mpc {
 
 struct RingGemmSegment {
-    const uint8_t* A;        // left limb planes  (rows = M), common.cuh layout
-    const uint8_t* B;        // right limb planes (rows = N), common.cuh layout
+    const uint8_t* A;        // left limb planes  (rows = M), Layout::Left
+    const uint8_t* B;        // right limb planes (rows = N), Layout::Right
     int kb;                  // number of 32-K blocks of this segment (both operands)
     int64_t party_stride_A;  // bytes between parties' A planes (0 = shared, e.g. eps)
     int64_t party_stride_B;
@@ -21,10 +21,13 @@ struct RingGemmParams {
     uint64_t* Z;                        // output [party][M][N]
     int64_t party_stride_c, party_stride_z;  // elements
     int trunc_bits;                     // 0 = none; else per-share round-half-up division (R10)
-    int kb_chunk[4];                    // max 32-K blocks per accumulation unit of pass q
+    int kc;                             // 32-K blocks per accumulation unit (<= ring_gemm_max_kc())
 };
 
-int ring_gemm_kb_chunk(int q);
+// Largest unit length (32-K blocks) for which every s32 accumulator stays exact.
+int ring_gemm_max_kc();
+// Unit length used for a fused reduction of `total_kb` blocks (L2-window sized).
+int ring_gemm_default_kc(int total_kb);
 size_t ring_gemm_smem_bytes();
 cudaError_t ring_gemm_launch(const RingGemmParams& p, int parties, cudaStream_t stream);
 
