@@ -38,6 +38,7 @@
 // warp 1 = MMA issuer (leader CTA) / stage relay (peer CTA), warp 2 = TMEM
 // allocator, warps 4..11 = epilogue.
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cuda_runtime.h>
 #include "common.cuh"
@@ -177,10 +178,29 @@ struct Bars {
 // Super-pass g accumulates 4 shifts into TMEM slots 0..3 (128 columns each):
 // g = 0: shifts {0, 7, 1, 6} (1+8+2+7 = 18 MMAs per 32-K block, planes 0..7)
 // g = 1: shifts {2, 5, 3, 4} (3+6+4+5 = 18 MMAs per 32-K block, planes 0..5)
-__device__ __forceinline__ int slot_shift(int g, int a) {
+__host__ __device__ constexpr int slot_shift(int g, int a) {
     return g == 0 ? ((a & 1) ? 7 - (a >> 1) : (a >> 1)) : ((a & 1) ? 5 - (a >> 1) : 2 + (a >> 1));
 }
 __device__ __forceinline__ int pass_planes(int g) { return g == 0 ? 8 : 6; }
+
+// The 18 limb MMAs of one 32-K block of super-pass G, fully unrolled: every
+// descriptor is the stage's base descriptor plus a compile-time offset (A
+// plane i at +4 KiB * i, B plane j at +2 KiB * j; the 14-bit address field
+// never carries for smem addresses < 256 KiB).  FIRST: the block starts a unit,
+// so the first product of each shift overwrites its accumulator.
+template <int G, bool FIRST>
+__device__ __forceinline__ void issue_kblock(uint64_t da, uint64_t db, uint32_t tmem_base) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int sh = slot_shift(G, a);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (i <= sh)
+                mma_u8_2cta(tmem_base + a * 128, da + (uint64_t)(i * (GL::kBlock >> 4)),
+                            db + (uint64_t)((sh - i) * (GR::kBlock >> 4)), (FIRST && i == 0) ? 0u : 1u);
+        }
+    }
+}
 
 // ---------------------------------------------------------------- control warpgroup
 __device__ __forceinline__ void control_roles(const RingGemmParams& p, const TileMap& tm, int ntiles, int tkb, int kc,
@@ -190,6 +210,7 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Til
     if (warp == 0 && lane == 0) {
         // ------------------------------------------------ producer (both CTAs: own halves)
         int s = 0; uint32_t ph = 0;
+        long long st_empty = 0;
         for (int t = cluster_id(); t < ntiles; t += nclusters()) {
             int party, m, n;
             tm.decode(t, party, m, n);
@@ -206,7 +227,8 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Til
                         const int kb = kt - (sg ? p.seg[0].kb : 0);
                         const uint8_t* srcA = S.A + party * S.party_stride_A + (rbA * S.kb + kb) * (8 * GL::kBlock);
                         const uint8_t* srcB = S.B + party * S.party_stride_B + (rbB * S.kb + kb) * (8 * GR::kBlock);
-                        mbar_wait(&B.empty[s], ph ^ 1);
+                        if (p.dbg) { const long long w0 = clock64(); mbar_wait(&B.empty[s], ph ^ 1); st_empty += clock64() - w0; }
+                        else mbar_wait(&B.empty[s], ph ^ 1);
                         mbar_expect_tx(&B.full[s], bytesA + bytesB);
                         uint8_t* st = B.stage_base + s * kStageBytes;
                         bulk_g2s(st, srcA, bytesA, &B.full[s]);
@@ -216,6 +238,7 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Til
                 }
             }
         }
+        if (p.dbg) atomicAdd(&p.dbg[0], (unsigned long long)st_empty);
     } else if (warp == 1 && lane == 0 && !leader) {
         // ------------------------------------------------ peer: relay "stage full" to the leader
         int s = 0; uint32_t ph = 0;
@@ -229,25 +252,32 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Til
     } else if (warp == 1 && lane == 0) {
         // ------------------------------------------------ leader: MMA issuer (one thread)
         int s = 0; uint32_t ph = 0; uint32_t u = 0;
+        long long st_tempty = 0, st_full = 0;
+        const long long t_start = clock64();
         for (int t = cluster_id(); t < ntiles; t += nclusters()) {
             for (int c = 0; c < nchunks; ++c) {
                 const int k0 = c * kc, k1 = min(tkb, k0 + kc);
                 for (int g = 0; g < kPasses; ++g, ++u) {
-                    mbar_wait_cluster(B.tempty, (u & 1) ^ 1);        // both epilogues drained TMEM
+                    {   // both epilogues drained TMEM
+                        const long long w0 = p.dbg ? clock64() : 0;
+                        mbar_wait_cluster(B.tempty, (u & 1) ^ 1);
+                        if (p.dbg) st_tempty += clock64() - w0;
+                    }
                     tc_fence_after();
                     for (int kt = k0; kt < k1; ++kt) {
-                        mbar_wait_cluster(&B.full[s], ph);
+                        {
+                            const long long w0 = p.dbg ? clock64() : 0;
+                            mbar_wait_cluster(&B.full[s], ph);
+                            if (p.dbg) st_full += clock64() - w0;
+                        }
                         tc_fence_after();
-                        const uint32_t a0 = smem_u32(B.stage_base + s * kStageBytes);
-                        const uint32_t b0 = a0 + kAStage;
+                        const uint64_t da = smem_desc(smem_u32(B.stage_base + s * kStageBytes));
+                        const uint64_t db = da + (kAStage >> 4);
                         const bool first = (kt == k0);
-#pragma unroll
-                        for (int a = 0; a < 4; ++a) {
-                            const int sh = slot_shift(g, a);
-                            const uint32_t d = tmem_base + a * 128;
-                            for (int i = 0; i <= sh; ++i)
-                                mma_u8_2cta(d, smem_desc(a0 + i * GL::kBlock), smem_desc(b0 + (sh - i) * GR::kBlock),
-                                            !(first && i == 0));
+                        if (g == 0) {
+                            if (first) issue_kblock<0, true>(da, db, tmem_base); else issue_kblock<0, false>(da, db, tmem_base);
+                        } else {
+                            if (first) issue_kblock<1, true>(da, db, tmem_base); else issue_kblock<1, false>(da, db, tmem_base);
                         }
                         tc_commit_both(&B.empty[s]);
                         if (++s == kStages) { s = 0; ph ^= 1; }
@@ -255,6 +285,11 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Til
                     tc_commit_both(B.tfull);
                 }
             }
+        }
+        if (p.dbg) {
+            atomicAdd(&p.dbg[1], (unsigned long long)st_tempty);
+            atomicAdd(&p.dbg[2], (unsigned long long)st_full);
+            atomicAdd(&p.dbg[3], (unsigned long long)(clock64() - t_start));
         }
     }
 }
@@ -425,8 +460,27 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     int64_t clusters = sms / 2;
     if (tiles < clusters) clusters = tiles;
     if (clusters < 1) clusters = 1;
-    gemm::ring_gemm_kernel<<<(unsigned)(clusters * 2), gemm::kThreads, smem, stream>>>(prm, parties);
-    return cudaGetLastError();
+    static const bool debug = getenv("MPC_GEMM_DEBUG") != nullptr;
+    if (!debug) {
+        gemm::ring_gemm_kernel<<<(unsigned)(clusters * 2), gemm::kThreads, smem, stream>>>(prm, parties);
+        return cudaGetLastError();
+    }
+    // diagnostic mode: stall-cycle attribution of the producer and MMA threads
+    RingGemmParams q = prm;
+    cudaMalloc(&q.dbg, 4 * sizeof(unsigned long long));
+    cudaMemsetAsync(q.dbg, 0, 4 * sizeof(unsigned long long), stream);
+    gemm::ring_gemm_kernel<<<(unsigned)(clusters * 2), gemm::kThreads, smem, stream>>>(q, parties);
+    cudaError_t e = cudaGetLastError();
+    unsigned long long h[4] = {0, 0, 0, 0};
+    cudaMemcpyAsync(h, q.dbg, sizeof(h), cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    cudaFree(q.dbg);
+    const double n = (double)clusters;
+    fprintf(stderr, "[ring_gemm] M=%lld N=%lld kb=%d kc=%d clusters=%lld  per MMA thread: total %.0f cyc, "
+            "wait tempty %.1f%%, wait full %.1f%%; producer wait empty %.0f cyc\n",
+            (long long)prm.M, (long long)prm.N, prm.seg[0].kb + (prm.nseg > 1 ? prm.seg[1].kb : 0), prm.kc,
+            (long long)clusters, h[3] / n, 100.0 * h[1] / h[3], 100.0 * h[2] / h[3], h[0] / (2 * n));
+    return e;
 }
 
 }  // namespace mpc

@@ -22,6 +22,7 @@ struct RingGemmParams {
     int64_t party_stride_c, party_stride_z;  // elements
     int trunc_bits;                     // 0 = none; else per-share round-half-up division (R10)
     int kc;                             // 32-K blocks per accumulation unit (<= ring_gemm_max_kc())
+    unsigned long long* dbg;            // optional: per-cluster stall cycles [producer empty, MMA tempty, MMA full]
 };
 
 // Largest unit length (32-K blocks) for which every s32 accumulator stays exact.

@@ -12,7 +12,7 @@ __device__ __forceinline__ uint64_t desc(uint32_t a) {
 }
 
 template <int CG, int M, int N>
-__global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* cycles) {
+__global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* cycles, const uint8_t* gsrc, int copy_bytes) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ uint32_t slot;
     __shared__ __align__(8) uint64_t bar;
@@ -38,6 +38,23 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* c
     else __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tm = slot;
+    __shared__ __align__(8) uint64_t cbar;
+    __shared__ volatile int stop;
+    if (threadIdx.x == 0) { stop = 0; asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&cbar))); }
+    __syncwarp();
+    if (warp == 2 && threadIdx.x == 64 && copy_bytes > 0) {
+        // concurrent L2 -> smem bulk copies (producer-like traffic) into bytes [96K, 96K+copy_bytes)
+        uint32_t ph = 0;
+        size_t off = (size_t)blockIdx.x * 65536;
+        for (int it = 0; it < 1000000 && !stop; ++it) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(&cbar)), "r"(copy_bytes));
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         :: "r"(smem_u32(sm + 96 * 1024)), "l"(gsrc + off), "r"(copy_bytes), "r"(smem_u32(&cbar)) : "memory");
+            asm volatile("{.reg .pred p; WB: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra WB;}" :: "r"(smem_u32(&cbar)), "r"(ph));
+            ph ^= 1;
+            off = (off + copy_bytes) % (16u << 20);
+        }
+    }
     if (warp == 0 && threadIdx.x == 0 && rank == 0) {
         const uint32_t a = smem_u32(sm), b = a + 64 * 1024;
         long long t0 = clock64();
@@ -62,6 +79,7 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* c
         long long t1 = clock64();
         atomicAdd(cycles, (unsigned long long)(t1 - t0));
     }
+    if (threadIdx.x == 0) stop = 1;
     if (CG == 2 && rank == 1 && threadIdx.x == 0)
         asm volatile("{.reg .pred p; W2: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0; @!p bra W2;}" :: "r"(smem_u32(&bar)));
     __syncwarp();
@@ -75,7 +93,7 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* c
 }
 
 template <int CG, int M, int N>
-void run(const char* name) {
+void run(const char* name, const uint8_t* gsrc = nullptr, int copy_bytes = 0) {
     auto k = probe<CG, M, N>;
     const int smem = 160 * 1024;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -96,7 +114,7 @@ void run(const char* name) {
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0); cudaEventCreate(&e1);
         cudaEventRecord(e0);
-        cudaLaunchKernelEx(&cfg, k, iters, dc);
+        cudaLaunchKernelEx(&cfg, k, iters, dc, gsrc, copy_bytes);
         cudaEventRecord(e1);
         cudaError_t err = cudaEventSynchronize(e1);
         float ms = 0; cudaEventElapsedTime(&ms, e0, e1);
@@ -113,6 +131,11 @@ void run(const char* name) {
 }
 
 int main() {
+    uint8_t* g; cudaMalloc(&g, 32u << 20); cudaMemset(g, 1, 32u << 20);
+    run<2, 256, 128>("cg2 M256 N128 +copy 32K", g, 32768);
+    run<2, 256, 128>("cg2 M256 N128 +copy 48K", g, 49152);
+    run<1, 128, 128>("cg1 M128 N128 +copy 32K", g, 32768);
+    run<2, 256, 256>("cg2 M256 N256 +copy 32K", g, 32768);
     run<1, 128, 64>("cg1 M128 N64");
     run<1, 128, 128>("cg1 M128 N128");
     run<1, 128, 256>("cg1 M128 N256");
