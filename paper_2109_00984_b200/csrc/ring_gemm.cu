@@ -183,15 +183,16 @@ __host__ __device__ constexpr int slot_shift(int g, int a) {
 }
 __device__ __forceinline__ int pass_planes(int g) { return g == 0 ? 8 : 6; }
 
-// The 18 limb MMAs of one 32-K block of super-pass G, fully unrolled: every
-// descriptor is the stage's base descriptor plus a compile-time offset (A
-// plane i at +4 KiB * i, B plane j at +2 KiB * j; the 14-bit address field
-// never carries for smem addresses < 256 KiB).  FIRST: the block starts a unit,
-// so the first product of each shift overwrites its accumulator.
-template <int G, bool FIRST>
-__device__ __forceinline__ void issue_kblock(uint64_t da, uint64_t db, uint32_t tmem_base) {
+// The limb MMAs of TMEM slots A0 and A0+1 (one release group) for one 32-K
+// block of super-pass G, fully unrolled (9 MMAs): every descriptor is the
+// stage's base descriptor plus a compile-time offset (A plane i at +4 KiB * i,
+// B plane j at +2 KiB * j; the 14-bit address field never carries for smem
+// addresses < 256 KiB).  FIRST: the block starts a unit, so the first product
+// of each shift overwrites its accumulator.
+template <int G, bool FIRST, int A0>
+__device__ __forceinline__ void issue_slots(uint64_t da, uint64_t db, uint32_t tmem_base) {
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
+    for (int a = A0; a < A0 + 2; ++a) {
         const int sh = slot_shift(G, a);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -200,6 +201,11 @@ __device__ __forceinline__ void issue_kblock(uint64_t da, uint64_t db, uint32_t 
                             db + (uint64_t)((sh - i) * (GR::kBlock >> 4)), (FIRST && i == 0) ? 0u : 1u);
         }
     }
+}
+template <int G>
+__device__ __forceinline__ void issue_kblock(uint64_t da, uint64_t db, uint32_t tmem_base) {
+    issue_slots<G, false, 0>(da, db, tmem_base);
+    issue_slots<G, false, 2>(da, db, tmem_base);
 }
 
 // ---------------------------------------------------------------- control warpgroup
@@ -258,12 +264,6 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Til
             for (int c = 0; c < nchunks; ++c) {
                 const int k0 = c * kc, k1 = min(tkb, k0 + kc);
                 for (int g = 0; g < kPasses; ++g, ++u) {
-                    {   // both epilogues drained TMEM
-                        const long long w0 = p.dbg ? clock64() : 0;
-                        mbar_wait_cluster(B.tempty, (u & 1) ^ 1);
-                        if (p.dbg) st_tempty += clock64() - w0;
-                    }
-                    tc_fence_after();
                     for (int kt = k0; kt < k1; ++kt) {
                         {
                             const long long w0 = p.dbg ? clock64() : 0;
@@ -273,11 +273,21 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Til
                         tc_fence_after();
                         const uint64_t da = smem_desc(smem_u32(B.stage_base + s * kStageBytes));
                         const uint64_t db = da + (kAStage >> 4);
-                        const bool first = (kt == k0);
-                        if (g == 0) {
-                            if (first) issue_kblock<0, true>(da, db, tmem_base); else issue_kblock<0, false>(da, db, tmem_base);
+                        if (kt == k0) {
+                            // first block of the unit: each slot pair may be overwritten once both
+                            // epilogues have drained it (the pair-1 drain overlaps pair-0 MMAs)
+                            const long long w0 = p.dbg ? clock64() : 0;
+                            mbar_wait_cluster(&B.tempty[0], (u & 1) ^ 1);
+                            if (p.dbg) st_tempty += clock64() - w0;
+                            tc_fence_after();
+                            if (g == 0) issue_slots<0, true, 0>(da, db, tmem_base); else issue_slots<1, true, 0>(da, db, tmem_base);
+                            const long long w1 = p.dbg ? clock64() : 0;
+                            mbar_wait_cluster(&B.tempty[1], (u & 1) ^ 1);
+                            if (p.dbg) st_tempty += clock64() - w1;
+                            tc_fence_after();
+                            if (g == 0) issue_slots<0, true, 2>(da, db, tmem_base); else issue_slots<1, true, 2>(da, db, tmem_base);
                         } else {
-                            if (first) issue_kblock<1, true>(da, db, tmem_base); else issue_kblock<1, false>(da, db, tmem_base);
+                            if (g == 0) issue_kblock<0>(da, db, tmem_base); else issue_kblock<1>(da, db, tmem_base);
                         }
                         tc_commit_both(&B.empty[s]);
                         if (++s == kStages) { s = 0; ph ^= 1; }
@@ -295,12 +305,33 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Til
 }
 
 // ---------------------------------------------------------------- epilogue warpgroups
+// run[j] += acc_S[j] * 2^(8S) + acc_{7-S}[j] * 2^(8(7-S))  (mod 2^64) for the 64
+// columns of this thread, with acc read as u32.  Compile-time S: the two 32-bit
+// halves of the contribution are built with constant shifts (the 7-S term only
+// touches the high word), then one 64-bit add.
+template <int S>
+__device__ __forceinline__ void drain_pair(uint64_t (&run)[64], uint32_t t_lo, uint32_t t_hi) {
+#pragma unroll
+    for (int cc = 0; cc < 64; cc += 16) {
+        uint32_t a[16], b[16];
+        tmem_ld16(t_lo + cc, a);
+        tmem_ld16(t_hi + cc, b);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint32_t lo32 = a[j] << (8 * S);
+            const uint32_t hi32 = (S == 0 ? 0u : (a[j] >> (32 - 8 * S))) + (b[j] << (24 - 8 * S));
+            run[cc + j] += ((uint64_t)hi32 << 32) | lo32;
+        }
+    }
+}
+
 __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const TileMap& tm, int ntiles, int nchunks,
                                               int warp, int lane, uint32_t rank, uint32_t tmem_base, const Bars& B) {
     const int wq = warp & 3;                       // TMEM lane quadrant of this warp
     const int half = (warp - 4) >> 2;              // column half: 64 columns each
     const int row = wq * 32 + lane;
-    const uint32_t tempty_leader = mapa(smem_u32(B.tempty), 0);
+    const uint32_t tempty_leader = mapa(smem_u32(B.tempty), 0);   // [0] slots 0-1, [1] slots 2-3
     const bool vec = (p.N & 1) == 0;
     const uint32_t tbase = tmem_base + ((uint32_t)(wq * 32) << 16) + half * 64;
     uint32_t u = 0;
@@ -315,22 +346,19 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Til
                 mbar_wait(B.tfull, u & 1);
                 tc_fence_after();
 #pragma unroll
-                for (int a = 0; a < 4; a += 2) {
-                    const int s0 = 8 * slot_shift(g, a), s1 = 8 * slot_shift(g, a + 1);
-#pragma unroll
-                    for (int cc = 0; cc < 64; cc += 16) {
-                        uint32_t v0[16], v1[16];
-                        tmem_ld16(tbase + a * 128 + cc, v0);
-                        tmem_ld16(tbase + (a + 1) * 128 + cc, v1);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            run[cc + j] += ((uint64_t)v0[j] << s0) + ((uint64_t)v1[j] << s1);
+                for (int h = 0; h < 2; ++h) {
+                    // slot pair h of super-pass g holds shifts (S, 7-S) with S = 2g + h
+                    const uint32_t tl = tbase + (2 * h) * 128, th = tl + 128;
+                    switch (2 * g + h) {
+                        case 0: drain_pair<0>(run, tl, th); break;
+                        case 1: drain_pair<1>(run, tl, th); break;
+                        case 2: drain_pair<2>(run, tl, th); break;
+                        default: drain_pair<3>(run, tl, th); break;
                     }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(tempty_leader + h * 8);   // release this slot pair
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive_cluster(tempty_leader);
             }
         }
         // tile end: z = trunc(c + sum of all units) — one write per element
@@ -370,8 +398,8 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     B.full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
     B.empty = B.full + kStages;
     B.tfull = B.empty + kStages;
-    B.tempty = B.tfull + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(B.tempty + 1);
+    B.tempty = B.tfull + 1;           // [2]: TMEM slots 0-1 / 2-3 drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(B.tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
@@ -385,7 +413,7 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) { mbar_init(&B.full[s], leader ? 2 : 1); mbar_init(&B.empty[s], 1); }
         mbar_init(B.tfull, 1);
-        mbar_init(B.tempty, 2 * kEpiWarps);   // both CTAs' epilogue warps (leader's copy is used)
+        for (int h = 0; h < 2; ++h) mbar_init(&B.tempty[h], 2 * kEpiWarps);   // both CTAs' epilogue warps (leader's copy)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
