@@ -212,14 +212,14 @@ def main():
     M, K, N = args.M, args.K, args.N
     P = 2
     if world > 1:
+        from paper_2109_00984_b200 import dist as mdist
         dist.init_process_group("gloo")
-        assert world % 2 == 0, "one party per GPU: --gpus must be 1 or even"
-        session, party = rank // 2, rank % 2
-        groups = [dist.new_group([2 * s, 2 * s + 1]) for s in range(world // 2)]
-        obj = [mpc.nccl_unique_id() if party == 0 else None]
-        dist.broadcast_object_list(obj, src=2 * session, group=groups[session])
-        ctx = mpc.Context(P, party, device=local, master_seed=synth.MASTER_SEED + session, nccl_id=obj[0])
-        sessions = world // 2
+        lay = mdist.layout(rank, world, P)          # one party per GPU, world/P replica sessions
+        groups = mdist.session_groups(lay)
+        uid = mdist.exchange_unique_id(lay, groups, mpc.nccl_unique_id)
+        party = lay.party
+        ctx = mpc.Context(P, party, device=local, master_seed=synth.MASTER_SEED + lay.session, nccl_id=uid)
+        sessions = lay.sessions
     else:
         party = mpc.ALL_PARTIES
         ctx = mpc.Context(P, mpc.ALL_PARTIES, device=local, master_seed=synth.MASTER_SEED)
