@@ -118,6 +118,26 @@ __device__ __forceinline__ void store_limbs16(uint8_t* planes, int64_t row, int6
             make_uint4(w[l][0], w[l][1], w[l][2], w[l][3]);
 }
 
+// 8 consecutive-k elements of one row -> 8 limb vectors of 8 bytes (k0 % 8 == 0).
+template <Layout L>
+__device__ __forceinline__ void store_limbs8(uint8_t* planes, int64_t row, int64_t k0, int64_t KB,
+                                             const uint64_t v[8]) {
+    uint32_t w[8][2];
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        uint32_t lo[4], hi[4];
+        transpose4x4((uint32_t)v[4 * g], (uint32_t)v[4 * g + 1], (uint32_t)v[4 * g + 2], (uint32_t)v[4 * g + 3], lo);
+        transpose4x4((uint32_t)(v[4 * g] >> 32), (uint32_t)(v[4 * g + 1] >> 32), (uint32_t)(v[4 * g + 2] >> 32),
+                     (uint32_t)(v[4 * g + 3] >> 32), hi);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) { w[l][g] = lo[l]; w[4 + l][g] = hi[l]; }
+    }
+    int64_t base = plane_offset<L>(row, k0, 0, KB);
+#pragma unroll
+    for (int l = 0; l < 8; ++l)
+        *reinterpret_cast<uint2*>(planes + base + (int64_t)l * PlaneGeom<L>::kBlock) = make_uint2(w[l][0], w[l][1]);
+}
+
 // ------------------------------------------------------------ signed helpers
 // floor(signed(v) / 2^bits) + bit_{bits-1}(v): per-share round-half-up division (R10)
 __host__ __device__ __forceinline__ uint64_t div_pow2_round(uint64_t v, int bits) {

@@ -104,41 +104,65 @@ cudaError_t launch_mask(const uint64_t* x, const uint64_t* a, int64_t n1, const 
 
 // ------------------------------------------------------------------ a4+a5+a6 left split
 // Left operands (rows = M, K contiguous): eps = sum_{p<Psum} (plus_p - minus_p)
-// -> eps planes; copies: planes of cp_src party q for q < Pcopy.
-// A warp covers 8 rows x 64 K: lane -> (row = lane & 7, 16-K chunk = lane >> 3):
-// each row's 512 B are read contiguously and each limb's 8 rows x 16 B are
-// written as one contiguous 128 B run.
-__global__ void split_left_kernel(LeftSplitArgs a) {
+// -> eps planes; copies: planes of cp_src party q for q < Pcopy.  When
+// cp_src == minus (all parties on one device) each party's a_p is split from
+// the registers it was loaded into for the mask (read once).
+// A warp covers 8 rows x 64 K: lane -> (row = lane & 7, 16-K chunk = lane >> 3);
+// a thread loads its 128 contiguous bytes with 16-byte loads, all issued
+// before use, and each limb's 8 rows x 16 B are written as one 128 B run.
+__device__ __forceinline__ void load16(const uint64_t* __restrict__ src, bool full, bool vec, int64_t kleft,
+                                       uint64_t (&v)[16]) {
+    if (full && vec) {
+        const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(src);
+        ulonglong2 t[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) t[m] = __ldg(s2 + m);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) { v[2 * m] = t[m].x; v[2 * m + 1] = t[m].y; }
+    } else {
+#pragma unroll
+        for (int m = 0; m < 16; ++m) v[m] = (m < kleft) ? __ldg(src + m) : 0ull;
+    }
+}
+
+__global__ void __launch_bounds__(256) split_left_kernel(LeftSplitArgs a) {
     const int64_t KB = num_kb(a.K);
     const int64_t row_groups = (a.M + 7) / 8;
     const int64_t kgroups = (KB * kKBlock + 63) / 64;      // whole padded K: pad limbs must be 0
     const int64_t warps_total = row_groups * kgroups;
     const int lane = threadIdx.x & 31;
+    const bool vec = (a.K & 1) == 0 && (a.party_stride & 1) == 0;
+    const bool fused_copy = a.cp_src == a.minus && a.Pcopy == a.Psum && a.Psum > 0;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < warps_total;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t rg = w / kgroups, kg = w % kgroups;
         const int64_t row = rg * 8 + (lane & 7);
         const int64_t k0 = kg * 64 + (lane >> 3) * 16;
         if (row >= a.M || k0 >= KB * kKBlock) continue;
-        const bool full = (k0 + 16 <= a.K);
-        uint64_t v[16];
+        const int64_t kleft = a.K - k0;                     // <= 0: pure K padding
+        const bool full = kleft >= 16;
+        uint64_t acc[16], v[16];
         if (a.Psum > 0) {
 #pragma unroll
-            for (int m = 0; m < 16; ++m) v[m] = 0;
+            for (int m = 0; m < 16; ++m) acc[m] = 0;
             for (int p = 0; p < a.Psum; ++p) {
-                const uint64_t* pl = a.plus + p * a.party_stride + row * a.K + k0;
-                const uint64_t* mi = a.minus ? a.minus + p * a.party_stride + row * a.K + k0 : nullptr;
+                load16(a.plus + p * a.party_stride + row * a.K + k0, full, vec, kleft, v);
 #pragma unroll
-                for (int m = 0; m < 16; ++m)
-                    if (full || k0 + m < a.K) v[m] += pl[m] - (mi ? mi[m] : 0ull);
+                for (int m = 0; m < 16; ++m) acc[m] += v[m];
+                if (a.minus) {
+                    load16(a.minus + p * a.party_stride + row * a.K + k0, full, vec, kleft, v);
+#pragma unroll
+                    for (int m = 0; m < 16; ++m) acc[m] -= v[m];
+                    if (fused_copy) store_limbs16<Layout::Left>(a.cp_planes + p * a.cp_planes_stride, row, k0, KB, v);
+                }
             }
-            store_limbs16<Layout::Left>(a.sum_planes, row, k0, KB, v);
+            store_limbs16<Layout::Left>(a.sum_planes, row, k0, KB, acc);
         }
-        for (int q = 0; q < a.Pcopy; ++q) {
-            const uint64_t* src = a.cp_src + q * a.party_stride + row * a.K + k0;
-#pragma unroll
-            for (int m = 0; m < 16; ++m) v[m] = (full || k0 + m < a.K) ? src[m] : 0ull;
-            store_limbs16<Layout::Left>(a.cp_planes + q * a.cp_planes_stride, row, k0, KB, v);
+        if (!fused_copy) {
+            for (int q = 0; q < a.Pcopy; ++q) {
+                load16(a.cp_src + q * a.party_stride + row * a.K + k0, full, vec, kleft, v);
+                store_limbs16<Layout::Left>(a.cp_planes + q * a.cp_planes_stride, row, k0, KB, v);
+            }
         }
     }
 }
@@ -153,44 +177,84 @@ cudaError_t launch_split_left(const LeftSplitArgs& a, cudaStream_t st) {
 // Right operands (K x N row-major, planes have rows = N: a transpose):
 // delta = sum_{p<Psum} (plus_p - minus_p) -> delta planes; copies:
 // planes of (b_q + [q == 0 && add_delta_first] delta) for q < Pcopy
-// (R8: party 0 folds the public eps@delta into eps @ (b_0 + delta)).
-// A warp covers 32 consecutive n x 16 K: every read y[k][n0..n0+31] is a
-// contiguous 256 B run, every limb write is 4 runs of 128 B.
-__global__ void split_right_kernel(RightSplitArgs a) {
+// (R8: party 0 folds the public eps@delta into eps @ (b_0 + delta)).  When
+// cp_src == minus, b_q (q >= 1) is split from the registers loaded for the
+// mask; b_0 is re-read (L1/L2 hit) once delta is complete.
+// A warp covers 32 n x 16 K: lane -> (2 adjacent n = 2 * (lane & 15),
+// 8-K half = lane >> 4); every load is 16 B per lane (256 B contiguous per
+// half-warp and K row) and the two K halves of each 16-byte plane row are
+// written by two lanes of the same warp.
+struct Col2 { uint64_t v[2][8]; };
+
+__device__ __forceinline__ void load_cols(const uint64_t* __restrict__ base, int64_t N, int64_t n, int64_t k0,
+                                          int64_t K, bool vec, bool two, uint64_t (&v)[2][8]) {
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        const int64_t k = k0 + m;
+        if (k < K) {
+            const uint64_t* src = base + k * N + n;
+            if (vec) {
+                const ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(src));
+                v[0][m] = t.x; v[1][m] = t.y;
+            } else {
+                v[0][m] = __ldg(src);
+                v[1][m] = two ? __ldg(src + 1) : 0ull;
+            }
+        } else {
+            v[0][m] = 0; v[1][m] = 0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256, 2) split_right_kernel(RightSplitArgs a) {
     const int64_t KB = num_kb(a.K);
     const int64_t ngroups = (a.N + 31) / 32;
-    const int64_t kchunks = KB * 2;                         // whole padded K
+    const int64_t kchunks = KB * 2;                         // whole padded K, 16 per chunk
     const int64_t warps_total = ngroups * kchunks;
     const int lane = threadIdx.x & 31;
+    const bool fused_copy = a.cp_src == a.minus && a.Pcopy == a.Psum && a.Psum > 0;
+    const bool even = (a.N & 1) == 0 && (a.party_stride & 1) == 0;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < warps_total;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t kc = w / ngroups, ng = w % ngroups;
-        const int64_t n = ng * 32 + lane;
-        const int64_t k0 = kc * 16;
+        const int64_t n = ng * 32 + 2 * (lane & 15);
+        const int64_t k0 = kc * 16 + (lane >> 4) * 8;
         if (n >= a.N) continue;
-        uint64_t d[16];
+        const bool two = n + 1 < a.N;
+        const bool vec = even && two;
+        uint64_t d[2][8], v[2][8];
 #pragma unroll
-        for (int m = 0; m < 16; ++m) d[m] = 0;
+        for (int m = 0; m < 8; ++m) { d[0][m] = 0; d[1][m] = 0; }
         for (int p = 0; p < a.Psum; ++p) {
-            const uint64_t* pl = a.plus + p * a.party_stride;
-            const uint64_t* mi = a.minus ? a.minus + p * a.party_stride : nullptr;
+            load_cols(a.plus + p * a.party_stride, a.N, n, k0, a.K, vec, two, v);
 #pragma unroll
-            for (int m = 0; m < 16; ++m) {
-                const int64_t k = k0 + m;
-                if (k < a.K) d[m] += pl[k * a.N + n] - (mi ? mi[k * a.N + n] : 0ull);
+            for (int m = 0; m < 8; ++m) { d[0][m] += v[0][m]; d[1][m] += v[1][m]; }
+            if (a.minus) {
+                load_cols(a.minus + p * a.party_stride, a.N, n, k0, a.K, vec, two, v);
+#pragma unroll
+                for (int m = 0; m < 8; ++m) { d[0][m] -= v[0][m]; d[1][m] -= v[1][m]; }
+                if (fused_copy && !(p == 0 && a.add_delta_first)) {
+                    uint8_t* pl = a.cp_planes + p * a.cp_planes_stride;
+                    store_limbs8<Layout::Right>(pl, n, k0, KB, v[0]);
+                    if (two) store_limbs8<Layout::Right>(pl, n + 1, k0, KB, v[1]);
+                }
             }
         }
-        if (a.sum_planes) store_limbs16<Layout::Right>(a.sum_planes, n, k0, KB, d);
+        if (a.sum_planes) {
+            store_limbs8<Layout::Right>(a.sum_planes, n, k0, KB, d[0]);
+            if (two) store_limbs8<Layout::Right>(a.sum_planes, n + 1, k0, KB, d[1]);
+        }
         for (int q = 0; q < a.Pcopy; ++q) {
-            const uint64_t* src = a.cp_src + q * a.party_stride;
-            uint64_t v[16];
             const bool addd = (q == 0) && a.add_delta_first;
+            if (fused_copy && !addd) continue;               // already written from registers
+            load_cols(a.cp_src + q * a.party_stride, a.N, n, k0, a.K, vec, two, v);
+            if (addd) {
 #pragma unroll
-            for (int m = 0; m < 16; ++m) {
-                const int64_t k = k0 + m;
-                v[m] = (k < a.K) ? src[k * a.N + n] + (addd ? d[m] : 0ull) : 0ull;
+                for (int m = 0; m < 8; ++m) { v[0][m] += d[0][m]; v[1][m] += d[1][m]; }
             }
-            store_limbs16<Layout::Right>(a.cp_planes + q * a.cp_planes_stride, n, k0, KB, v);
+            uint8_t* pl = a.cp_planes + q * a.cp_planes_stride;
+            store_limbs8<Layout::Right>(pl, n, k0, KB, v[0]);
+            if (two) store_limbs8<Layout::Right>(pl, n + 1, k0, KB, v[1]);
         }
     }
 }
