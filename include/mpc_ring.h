@@ -143,6 +143,22 @@ mpc_status mpc_beaver_matmul(mpc_ctx ctx, const uint64_t* x, const uint64_t* y,
                              int truncate, uint64_t wrap_id,
                              void* workspace, size_t workspace_bytes);
 
+/* ---- the same matmul with its round made explicit (one-party contexts) ----
+ * For callers that reveal with their own communicator (and for testing the
+ * one-party kernels without NCCL):
+ *   mpc_beaver_mask:   ed = [x - a | y - b]   (M*K + K*N u64; 0 rounds, local)
+ *   -- caller: ed <- sum over parties of ed (mod 2^64), i.e. [eps | delta]  (1 round)
+ *   mpc_beaver_finish: z = c_p + a_p @ delta + eps @ (b_p + [p == 0] delta), truncated
+ *                      locally if truncate != 0 (P <= 2 only; for P > 2 call
+ *                      mpc_truncate, which needs the communicator).
+ * Result identical to mpc_beaver_matmul.  MPC_ERR_UNSUPPORTED on an all-parties
+ * context.  workspace: mpc_workspace_bytes(ctx, M, K, N). */
+mpc_status mpc_beaver_mask(mpc_ctx ctx, const uint64_t* x, const uint64_t* y, const uint64_t* a,
+                           const uint64_t* b, uint64_t* ed, int64_t M, int64_t K, int64_t N);
+mpc_status mpc_beaver_finish(mpc_ctx ctx, const uint64_t* ed, const uint64_t* a, const uint64_t* b,
+                             const uint64_t* c, uint64_t* z, int64_t M, int64_t K, int64_t N,
+                             int truncate, void* workspace, size_t workspace_bytes);
+
 /* ---- truncation by 2^bits (App. A.1.1 "Truncation") ----------
  * In place on x (n or [P][n]).  bits in [1, 62].  P <= 2: out_p =
  * (signed(x_p) >> bits) + bit_{bits-1}(x_p) (0 rounds).  P > 2: Alg. 1 with the wrap

@@ -167,6 +167,33 @@ def ttp_triple(P: int, master: int, triple_id: int, M: int, K: int, N: int, rows
     return a, b, c
 
 
+def ttp_triple_sampled(P: int, master: int, triple_id: int, M: int, K: int, N: int, rows, cols):
+    """The triple restricted to rows of a/c and columns of b/c: a (P,R,K), b (P,K,C), c (P,R,C)."""
+    _, kt = derive_keys(master, P)
+    rows = np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
+    cols = np.ascontiguousarray(np.asarray(cols, dtype=np.int64))
+    R, C = rows.size, cols.size
+    a = np.zeros((P, R, K), dtype=np.uint64)
+    b = np.zeros((P, K, C), dtype=np.uint64)
+    c = np.zeros((P, R, C), dtype=np.uint64)
+    lib().oracle_ttp_triple_sampled(P, ctypes.c_uint64(kt), ctypes.c_uint64(triple_id), ctypes.c_int64(M),
+                                    ctypes.c_int64(K), ctypes.c_int64(N), _p(rows), ctypes.c_int64(R), _p(cols),
+                                    ctypes.c_int64(C), _p(a), _p(b), _p(c))
+    return a, b, c
+
+
+def share_indices(P: int, master: int, x_vals, src: int, share_id: int, idx) -> np.ndarray:
+    """PRZS shares of the elements at flat indices idx (x_vals = plaintext there): (P, len(idx))."""
+    x_vals = _u64(x_vals).ravel()
+    idx = np.ascontiguousarray(np.asarray(idx, dtype=np.int64).ravel())
+    kp, _ = derive_keys(master, P)
+    kp = np.ascontiguousarray(kp)
+    out = np.zeros((P, idx.size), dtype=np.uint64)
+    lib().oracle_share_indices(P, _p(kp), _p(x_vals), src, ctypes.c_uint64(share_id), _p(idx),
+                               ctypes.c_int64(idx.size), _p(out))
+    return out
+
+
 # ---------------------------------------------------------------- O5
 def beaver_matmul(x, y, a, b, c, want_intermediates: bool = False):
     """Un-truncated Beaver matmul shares z: (P, M, N) (scale 2^(2f))."""
@@ -208,6 +235,16 @@ def wrap_pair(P: int, master: int, wrap_id: int, n: int):
     r = np.zeros((P, n), dtype=np.uint64)
     th = np.zeros((P, n), dtype=np.uint64)
     lib().oracle_wrap_pair(P, ctypes.c_uint64(kt), ctypes.c_uint64(wrap_id), ctypes.c_int64(n), _p(r), _p(th))
+    return r, th
+
+
+def wrap_pair_indices(P: int, master: int, wrap_id: int, idx):
+    _, kt = derive_keys(master, P)
+    idx = np.ascontiguousarray(np.asarray(idx, dtype=np.int64).ravel())
+    r = np.zeros((P, idx.size), dtype=np.uint64)
+    th = np.zeros((P, idx.size), dtype=np.uint64)
+    lib().oracle_wrap_pair_indices(P, ctypes.c_uint64(kt), ctypes.c_uint64(wrap_id), _p(idx), ctypes.c_int64(idx.size),
+                                   _p(r), _p(th))
     return r, th
 
 

@@ -229,6 +229,58 @@ void oracle_ttp_triple(int P, uint64_t k_ttp, uint64_t triple_id,
     free(asum); free(bsum); free(cfull);
 }
 
+/* The same triple restricted to a sample of rows of a / c and columns of b / c
+ * (for checking single outputs of a large product): a: [P][nrows*K],
+ * b: [P][K*ncols], c: [P][nrows*ncols], values identical to the full triple's. */
+void oracle_ttp_triple_sampled(int P, uint64_t k_ttp, uint64_t triple_id,
+                               int64_t M, int64_t K, int64_t N,
+                               const int64_t* rows, int64_t nrows, const int64_t* cols, int64_t ncols,
+                               uint64_t* a, uint64_t* b, uint64_t* c)
+{
+    (void)M;
+    for (int p = 0; p < P; p++) {
+        uint64_t sa = oracle_stream_id(TAG_A, (uint32_t)p, triple_id);
+        uint64_t sb = oracle_stream_id(TAG_B, (uint32_t)p, triple_id);
+        for (int64_t r = 0; r < nrows; r++)
+            oracle_prg(k_ttp, sa, (uint64_t)(rows[r] * K), K, a + (int64_t)p * nrows * K + r * K);
+        for (int64_t k = 0; k < K; k++)
+            for (int64_t j = 0; j < ncols; j++)
+                b[(int64_t)p * K * ncols + k * ncols + j] = oracle_prg_at(k_ttp, sb, (uint64_t)(k * N + cols[j]));
+    }
+    uint64_t* asum = (uint64_t*)calloc((size_t)(nrows * K > 0 ? nrows * K : 1), 8);
+    uint64_t* bsum = (uint64_t*)calloc((size_t)(K * ncols > 0 ? K * ncols : 1), 8);
+    oracle_reveal(P, a, nrows * K, asum);
+    oracle_reveal(P, b, K * ncols, bsum);
+    oracle_ring_matmul(asum, bsum, c, nrows, K, ncols);
+    for (int p = 1; p < P; p++) {
+        uint64_t sc = oracle_stream_id(TAG_C, (uint32_t)p, triple_id);
+        for (int64_t r = 0; r < nrows; r++)
+            for (int64_t j = 0; j < ncols; j++) {
+                uint64_t v = oracle_prg_at(k_ttp, sc, (uint64_t)(rows[r] * N + cols[j]));
+                c[(int64_t)p * nrows * ncols + r * ncols + j] = v;
+                c[r * ncols + j] -= v;
+            }
+    }
+    free(asum); free(bsum);
+}
+
+/* PRZS shares of selected elements idx[0..n) of a tensor (x_vals = the src
+ * party's plaintext values at those indices), same values as oracle_share. */
+void oracle_share_indices(int P, const uint64_t* k_party, const uint64_t* x_vals, int src,
+                          uint64_t share_id, const int64_t* idx, int64_t n, uint64_t* shares)
+{
+    uint64_t stream = oracle_stream_id(TAG_PRZS, 0, share_id);
+    for (int p = 0; p < P; p++) {
+        int prev = (p + P - 1) % P;
+        for (int64_t t = 0; t < n; t++) {
+            uint64_t v = oracle_prg_at(k_party[p], stream, (uint64_t)idx[t])
+                       - oracle_prg_at(k_party[prev], stream, (uint64_t)idx[t]);
+            if (p == src && x_vals != NULL) v += x_vals[t];
+            shares[(int64_t)p * n + t] = v;
+        }
+    }
+}
+
 /* ------------------------------------------------------------------------
  * O5  Beaver private matmul (§4.2; App. A.1.1):
  *   [ε]_p = [x]_p − [a]_p,  [δ]_p = [y]_p − [b]_p
@@ -334,6 +386,26 @@ void oracle_wrap_pair(int P, uint64_t k_ttp, uint64_t wrap_id, int64_t n,
         oracle_prg(k_ttp, oracle_stream_id(TAG_THETA, (uint32_t)p, wrap_id), 0, n, theta_r + (int64_t)p * n);
         for (int64_t i = 0; i < n; i++) theta_r[i] -= theta_r[(int64_t)p * n + i];
     }
+    free(th);
+}
+
+/* Wrap pair values at selected flat indices idx[0..n) (same values as the
+ * full oracle_wrap_pair at those positions). */
+void oracle_wrap_pair_indices(int P, uint64_t k_ttp, uint64_t wrap_id, const int64_t* idx, int64_t n,
+                              uint64_t* r, uint64_t* theta_r)
+{
+    for (int p = 0; p < P; p++)
+        for (int64_t t = 0; t < n; t++)
+            r[(int64_t)p * n + t] = oracle_prg_at(k_ttp, oracle_stream_id(TAG_R, (uint32_t)p, wrap_id), (uint64_t)idx[t]);
+    int64_t* th = (int64_t*)malloc((size_t)(n > 0 ? n : 1) * 8);
+    oracle_wrap_count(P, r, n, th);
+    for (int64_t t = 0; t < n; t++) theta_r[t] = (uint64_t)th[t];
+    for (int p = 1; p < P; p++)
+        for (int64_t t = 0; t < n; t++) {
+            uint64_t v = oracle_prg_at(k_ttp, oracle_stream_id(TAG_THETA, (uint32_t)p, wrap_id), (uint64_t)idx[t]);
+            theta_r[(int64_t)p * n + t] = v;
+            theta_r[t] -= v;
+        }
     free(th);
 }
 

@@ -143,8 +143,13 @@ BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N) {
     return w;
 }
 
+mpc_status beaver_local(mpc_ctx c, const BeaverWs& w, const uint64_t* ed, const uint64_t* a, const uint64_t* b,
+                        const uint64_t* cc, uint64_t* z, int64_t M, int64_t K, int64_t N, int truncate);
+
 mpc_status gemm_run(mpc_ctx c, RingGemmParams& p, int parties) {
     p.kc = ring_gemm_default_kc(p.seg[0].kb + (p.nseg > 1 ? p.seg[1].kb : 0));
+    static const int prefetch_env = getenv("MPC_GEMM_PREFETCH") ? atoi(getenv("MPC_GEMM_PREFETCH")) : -1;
+    p.prefetch = prefetch_env >= 0 ? prefetch_env : 0;
     return run(c, kClsGemm, "ring_gemm", [&] { return ring_gemm_launch(p, parties, c->stream); });
 }
 
@@ -384,9 +389,54 @@ mpc_status mpc_beaver_matmul(mpc_ctx c, const uint64_t* x, const uint64_t* y, co
     } else {
         CHECK(run(c, kClsSplit, "mask", [&] { return launch_mask(x, a, sMK, y, b, sKN, w.ed, c->stream); }));
         if (c->P > 1) CHECK(nccl_allreduce(c, w.ed, w.ed, (size_t)(sMK + sKN), ncclUint64, "eps/delta reveal"));
-        LeftSplitArgs L{M, K, 0, w.ed, nullptr, 1, w.eps_pl, a, 1, w.a_pl, 0};
+    }
+    CHECK(beaver_local(c, w, w.ed, a, b, cc, z, M, K, N, truncate));
+    if (truncate && c->P > 2) CHECK(truncate_impl(c, z, sMN, c->frac, wrap_id, w.zbuf, w.hbuf));
+    return MPC_OK;
+}
+
+mpc_status mpc_beaver_mask(mpc_ctx c, const uint64_t* x, const uint64_t* y, const uint64_t* a, const uint64_t* b,
+                           uint64_t* ed, int64_t M, int64_t K, int64_t N) {
+    CHECK(enter(c));
+    if (c->all) return fail(c, MPC_ERR_UNSUPPORTED, "beaver_mask: one-party contexts only");
+    if (M < 0 || K < 0 || N < 0) return fail(c, MPC_ERR_SHAPE, "beaver_mask: negative size");
+    if (M * K + K * N == 0) return MPC_OK;
+    if ((M * K && (!x || !a)) || (K * N && (!y || !b)) || !ed) return fail(c, MPC_ERR_ARG, "beaver_mask: null pointer");
+    return run(c, kClsSplit, "mask", [&] { return launch_mask(x, a, M * K, y, b, K * N, ed, c->stream); });
+}
+
+mpc_status mpc_beaver_finish(mpc_ctx c, const uint64_t* ed, const uint64_t* a, const uint64_t* b, const uint64_t* cc,
+                             uint64_t* z, int64_t M, int64_t K, int64_t N, int truncate, void* ws, size_t ws_bytes) {
+    CHECK(enter(c));
+    if (c->all) return fail(c, MPC_ERR_UNSUPPORTED, "beaver_finish: one-party contexts only");
+    if (truncate && c->P > 2) return fail(c, MPC_ERR_UNSUPPORTED, "beaver_finish: P > 2 truncation needs mpc_truncate");
+    if (M < 0 || K < 0 || N < 0) return fail(c, MPC_ERR_SHAPE, "beaver_finish: negative size");
+    const BeaverWs w = carve_beaver(c, ws, M, K, N);
+    if (ws_bytes < w.total) return fail(c, MPC_ERR_SHAPE, "beaver_finish: workspace %zu < %zu", ws_bytes, w.total);
+    c->rounds += 1;                                   // the caller's reveal of eps || delta
+    c->bytes += 8ull * (uint64_t)(M * K + K * N);
+    if (M == 0 || N == 0) return MPC_OK;
+    if ((M * K && (!ed || !a)) || (K * N && (!ed || !b)) || !cc || !z || (!ws && w.total))
+        return fail(c, MPC_ERR_ARG, "beaver_finish: null pointer");
+    return beaver_local(c, w, ed, a, b, cc, z, M, K, N, truncate);
+}
+
+}  // extern "C"
+
+namespace {
+// Everything after the eps || delta reveal: limb split of eps, delta, a_p and
+// b'_p = b_p + [p = 0] delta, then the ring GEMM z_p = c_p + a_p@delta +
+// eps@b'_p with the P <= 2 truncation fused.  ed = revealed [eps | delta]
+// (one-party contexts; ignored in the all-parties mode, whose split kernels
+// already produced the planes).
+mpc_status beaver_local(mpc_ctx c, const BeaverWs& w, const uint64_t* ed, const uint64_t* a, const uint64_t* b,
+                        const uint64_t* cc, uint64_t* z, int64_t M, int64_t K, int64_t N, int truncate) {
+    const int Pl = c->all ? c->P : 1;
+    const int64_t sMK = M * K, sMN = M * N;
+    if (!c->all) {
+        LeftSplitArgs L{M, K, 0, ed, nullptr, 1, w.eps_pl, a, 1, w.a_pl, 0};
         CHECK(run(c, kClsSplit, "split eps", [&] { return launch_split_left(L, c->stream); }));
-        RightSplitArgs R{K, N, 0, w.ed + sMK, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0};
+        RightSplitArgs R{K, N, 0, ed + sMK, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0};
         CHECK(run(c, kClsSplit, "split delta", [&] { return launch_split_right(R, c->stream); }));
     }
     RingGemmParams p{};
@@ -396,10 +446,11 @@ mpc_status mpc_beaver_matmul(mpc_ctx c, const uint64_t* x, const uint64_t* y, co
     p.M = M; p.N = N; p.C = cc; p.Z = z;
     p.party_stride_c = p.party_stride_z = sMN;
     p.trunc_bits = (truncate && c->P <= 2) ? c->frac : 0;                                     // fused, 0 rounds
-    CHECK(gemm_run(c, p, Pl));
-    if (truncate && c->P > 2) CHECK(truncate_impl(c, z, sMN, c->frac, wrap_id, w.zbuf, w.hbuf));
-    return MPC_OK;
+    return gemm_run(c, p, Pl);
 }
+}  // namespace
+
+extern "C" {
 
 mpc_status mpc_truncate(mpc_ctx c, uint64_t* x, int64_t n, int bits, uint64_t wrap_id) {
     CHECK(enter(c));

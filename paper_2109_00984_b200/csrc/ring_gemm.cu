@@ -124,6 +124,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 // commit all prior MMAs of this thread; arrive on `bar` (same offset) in both CTAs
@@ -152,6 +155,23 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
         : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// c_p reads and z writes stream through L2 once: mark them evict-first so they
+// do not push the K window of limb planes (re-read by the second super-pass) out.
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ ulonglong2 ld_stream(const uint64_t* p, uint64_t pol) {
+    ulonglong2 v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
+                 : "=l"(v.x), "=l"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_stream(uint64_t* p, ulonglong2 v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;"
+                 :: "l"(p), "l"(v.x), "l"(v.y), "l"(pol) : "memory");
+}
 
 // Tile t -> (party, m tile, n tile) in the grouped order: groups of kGroupM row
 // tiles; inside a group, n tiles outer, then row tiles, then parties.
@@ -224,6 +244,16 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Til
             const int64_t rbB = (int64_t)n * 2 + rank;       // 64-row right block
             for (int c = 0; c < nchunks; ++c) {
                 const int k0 = c * kc, k1 = min(tkb, k0 + kc);
+                if (p.prefetch) {
+                    // warm L2 with the next K chunk of this tile while this chunk runs
+                    for (int kt = k1; kt < min(tkb, k1 + kc); ++kt) {
+                        const int sg = (kt < p.seg[0].kb) ? 0 : 1;
+                        const RingGemmSegment& S = p.seg[sg];
+                        const int kb = kt - (sg ? p.seg[0].kb : 0);
+                        prefetch_l2(S.A + party * S.party_stride_A + (rbA * S.kb + kb) * (8 * GL::kBlock), 8 * GL::kBlock);
+                        prefetch_l2(S.B + party * S.party_stride_B + (rbB * S.kb + kb) * (8 * GR::kBlock), 8 * GR::kBlock);
+                    }
+                }
                 for (int g = 0; g < kPasses; ++g) {
                     const uint32_t bytesA = (uint32_t)pass_planes(g) * GL::kBlock;
                     const uint32_t bytesB = (uint32_t)pass_planes(g) * GR::kBlock;
@@ -333,6 +363,7 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Til
     const int row = wq * 32 + lane;
     const uint32_t tempty_leader = mapa(smem_u32(B.tempty), 0);   // [0] slots 0-1, [1] slots 2-3
     const bool vec = (p.N & 1) == 0;
+    const uint64_t pol = evict_first_policy();
     const uint32_t tbase = tmem_base + ((uint32_t)(wq * 32) << 16) + half * 64;
     uint32_t u = 0;
     for (int t = cluster_id(); t < ntiles; t += nclusters()) {
@@ -370,10 +401,10 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Til
             if (vec && gc0 + 64 <= p.N) {
 #pragma unroll
                 for (int j = 0; j < 64; j += 2) {
-                    ulonglong2 v = crow ? *reinterpret_cast<const ulonglong2*>(crow + gc0 + j) : make_ulonglong2(0, 0);
+                    ulonglong2 v = crow ? ld_stream(crow + gc0 + j, pol) : make_ulonglong2(0, 0);
                     v.x += run[j]; v.y += run[j + 1];
                     if (p.trunc_bits) { v.x = div_pow2_round(v.x, p.trunc_bits); v.y = div_pow2_round(v.y, p.trunc_bits); }
-                    *reinterpret_cast<ulonglong2*>(zrow + gc0 + j) = v;
+                    st_stream(zrow + gc0 + j, v, pol);
                 }
             } else {
 #pragma unroll

@@ -23,6 +23,7 @@ struct RingGemmParams {
     int trunc_bits;                     // 0 = none; else per-share round-half-up division (R10)
     int kc;                             // 32-K blocks per accumulation unit (<= ring_gemm_max_kc())
     unsigned long long* dbg;            // optional: per-cluster stall cycles [producer empty, MMA tempty, MMA full]
+    int prefetch;                       // 1: producer prefetches the next K chunk into L2
 };
 
 // Largest unit length (32-K blocks) for which every s32 accumulator stays exact.

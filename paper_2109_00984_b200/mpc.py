@@ -164,6 +164,25 @@ class Context:
                    ctypes.c_uint64(wrap_id), _ptr(ws), ctypes.c_size_t(ws.numel()))
         return z
 
+    def beaver_mask(self, x, y, a, b) -> torch.Tensor:
+        """One-party context: [x - a | y - b] (to be revealed by the caller, one round)."""
+        M, K = x.shape[-2], x.shape[-1]
+        N = y.shape[-1]
+        ed = _u64((M * K + K * N,), self.device)
+        self._call(self._lib.mpc_beaver_mask, _ptr(x), _ptr(y), _ptr(a), _ptr(b), _ptr(ed),
+                   ctypes.c_int64(M), ctypes.c_int64(K), ctypes.c_int64(N))
+        return ed
+
+    def beaver_finish(self, ed, a, b, c, truncate: bool = True, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """One-party context: z_p from the revealed [eps | delta] (see mpc_beaver_finish)."""
+        M, K = a.shape[-2], a.shape[-1]
+        N = b.shape[-1]
+        z = out if out is not None else _u64((M, N), self.device)
+        ws = self._workspace(self.workspace_bytes(M, K, N))
+        self._call(self._lib.mpc_beaver_finish, _ptr(ed), _ptr(a), _ptr(b), _ptr(c), _ptr(z), ctypes.c_int64(M),
+                   ctypes.c_int64(K), ctypes.c_int64(N), int(bool(truncate)), _ptr(ws), ctypes.c_size_t(ws.numel()))
+        return z
+
     def truncate(self, x: torch.Tensor, bits: Optional[int] = None, wrap_id: int = 0) -> torch.Tensor:
         """In place; returns x."""
         n = x[0].numel() if self.all_parties else x.numel()

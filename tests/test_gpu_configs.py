@@ -1,0 +1,105 @@
+"""GPU parity at the BASELINE.json configs (beyond configs[0]/[1], which live in
+test_gpu_parity.py): ViT-B/16 and ResNet-50 layer GEMMs (configs[2], [3]),
+and the 4- / 8-party 8192^3 Beaver matmul with Alg. 1 truncation (configs[4]).
+
+Small layers are compared element by element with the oracle; 8192^3 is
+compared on a seeded sample of (row, column) outputs that the oracle computes
+one by one from the corresponding rows of x, a and columns of y, b.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+MASTER = synth.MASTER_SEED
+
+
+@pytest.fixture(scope="module")
+def mpc():
+    from paper_2109_00984_b200 import build
+    build.build()
+    import paper_2109_00984_b200 as m
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    return m
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).cuda().view(torch.uint64)
+
+
+def host(t):
+    return t.view(torch.int64).cpu().numpy().view(np.uint64)
+
+
+def _layer_case(P, M, K, N, kind, seed):
+    if kind == "vit":    # activations N(0,1) clipped to [-8, 8]; weights N(0, 0.02^2)
+        X = synth.gaussian_fixed((M, K), seed, 1.0, -8, 8)
+        Y = synth.gaussian_fixed((K, N), seed + 1, 0.02, -8, 8)
+    else:                # ResNet: |N(0,1)| clipped to [0, 8]; weights N(0, 2/K) clipped (C3)
+        X = synth.gaussian_fixed((M, K), seed, 1.0, 0, 8, absval=True)
+        Y = synth.gaussian_fixed((K, N), seed + 1, (2.0 / K) ** 0.5, -8, 8)
+    return X, Y
+
+
+@pytest.mark.parametrize("name,M,K,N,kind", [
+    ("vit.fc1", 197, 768, 3072, "vit"),
+    ("vit.head", 1, 768, 1000, "vit"),
+    ("resnet.conv1", 12544, 147, 64, "resnet"),
+    ("resnet.l4.c2", 49, 4608, 512, "resnet"),
+    ("resnet.l3.c2", 196, 2304, 256, "resnet"),
+    ("resnet.fc", 1, 2048, 1000, "resnet"),
+])
+def test_layer_gemm_parity(mpc, name, M, K, N, kind):
+    P = 2
+    c = mpc.Context(P, mpc.ALL_PARTIES, device=0, master_seed=MASTER)
+    X, Y = _layer_case(P, M, K, N, kind, seed=len(name) * 7)
+    gx = c.share(dev(X), 0, 1)
+    gy = c.share(dev(Y), 1, 2)
+    ga, gb, gc = c.ttp_triples(5, M, K, N)
+    z = host(c.beaver_matmul(gx, gy, ga, gb, gc, truncate=True))
+    a, b, cc = oracle.ttp_triple(P, MASTER, 5, M, K, N)
+    ez, dg = oracle.truncate(oracle.beaver_matmul(oracle.share(P, MASTER, X, 0, 1), oracle.share(P, MASTER, Y, 1, 2),
+                                                  a, b, cc), 16, diagnostics=True)
+    assert np.array_equal(z, ez), name
+    got = oracle.decode(oracle.reveal(z))
+    exact = (X.view(np.int64).astype(np.float64) / 65536) @ (Y.view(np.int64).astype(np.float64) / 65536)
+    ok = dg["theta"] == 0
+    assert np.all(np.abs(got - exact)[ok] <= 2.0 ** -14)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("P", [4, 8])
+def test_c5_8192_sampled(mpc, P):
+    """configs[4]: P-party 8192^3 Beaver matmul + Alg. 1 truncation (all parties on
+    one device here; one party per GPU uses the same kernels)."""
+    M = K = N = 8192
+    c = mpc.Context(P, mpc.ALL_PARTIES, device=0, master_seed=MASTER)
+    X = synth.uniform_fixed((M, K), 1005)
+    Y = synth.uniform_fixed((K, N), 1006)
+    gx = c.share(dev(X), 0, 1)
+    gy = c.share(dev(Y), 1, 2)
+    del X
+    ga, gb, gc = c.ttp_triples(3, M, K, N)
+    z = c.beaver_matmul(gx, gy, ga, gb, gc, truncate=True, wrap_id=7)
+    rng = np.random.default_rng(P)
+    rows = np.sort(rng.choice(M, 3, replace=False)).astype(np.int64)
+    cols = np.sort(rng.choice(N, 3, replace=False)).astype(np.int64)
+    zi = z.view(torch.int64)
+    zs = zi[:, torch.from_numpy(rows).cuda()][:, :, torch.from_numpy(cols).cuda()].contiguous().cpu().numpy()
+    zs = zs.view(np.uint64)
+    del gx, gy, ga, gb, gc, z
+    torch.cuda.empty_cache()
+    # oracle: the same outputs from the rows of x, a and the columns of y, b
+    Xs = synth.uniform_fixed((M, K), 1005)[rows]
+    Yfull = synth.uniform_fixed((K, N), 1006)
+    Ys = Yfull[:, cols]
+    xs = oracle.share_indices(P, MASTER, Xs.ravel(), 0, 1, (rows[:, None] * K + np.arange(K)[None, :]).ravel())
+    ys = oracle.share_indices(P, MASTER, Ys.ravel(), 1, 2, (np.arange(K)[:, None] * N + cols[None, :]).ravel())
+    a, b, cc = oracle.ttp_triple_sampled(P, MASTER, 3, M, K, N, rows, cols)
+    zraw = oracle.beaver_matmul(xs.reshape(P, 3, K), ys.reshape(P, K, 3), a, b, cc)
+    r, th = oracle.wrap_pair_indices(P, MASTER, 7, (rows[:, None] * N + cols[None, :]).ravel())
+    ez = oracle.truncate_alg1(zraw.reshape(P, 9), r, th, 16).reshape(P, 3, 3)
+    assert np.array_equal(zs, ez)

@@ -211,6 +211,36 @@ def test_truncate_parity(mpc, P):
     assert np.array_equal(host(g), oracle.truncate(xs, 16, MASTER, wrap_id=31))
 
 
+@pytest.mark.parametrize("P", [1, 2, 3])
+@pytest.mark.parametrize("M,K,N", [(64, 64, 64), (300, 100, 260), (1, 45, 3)])
+def test_one_party_contexts_beaver(mpc, P, M, K, N):
+    """The one-party-per-GPU kernels (mask, split of the revealed eps/delta, GEMM)
+    on one device: P one-party contexts (no communicator), the eps||delta reveal
+    done here as a plain uint64 sum, bit-exact with the all-parties oracle."""
+    X, Y, xs, ys, a, b, cc = _beaver_case(P, M, K, N, seed=M + N, tid=40 + P)
+    ctxs = [ctx(mpc, P, rank=r) for r in range(P)]
+    eds = [ctxs[r].beaver_mask(dev(xs[r]), dev(ys[r]), dev(a[r]), dev(b[r])) for r in range(P)]
+    ed = eds[0].clone()
+    for e in eds[1:]:
+        ed = (ed.view(torch.int64) + e.view(torch.int64)).view(torch.uint64)   # wraps mod 2^64
+    trunc = P <= 2
+    zs = [host(ctxs[r].beaver_finish(ed, dev(a[r]), dev(b[r]), dev(cc[r]), truncate=trunc)) for r in range(P)]
+    ez = oracle.beaver_matmul(xs, ys, a, b, cc)
+    if trunc:
+        ez = oracle.truncate(ez, 16)
+    assert np.array_equal(np.stack(zs), ez)
+    if P == 1:   # a 1-party context runs the all-in-one call without any communicator
+        z1 = ctxs[0].beaver_matmul(dev(xs[0]), dev(ys[0]), dev(a[0]), dev(b[0]), dev(cc[0]), truncate=True)
+        assert np.array_equal(host(z1), oracle.truncate(oracle.beaver_matmul(xs, ys, a, b, cc), 16)[0])
+
+
+def test_collective_without_communicator_fails_cleanly(mpc):
+    c = ctx(mpc, 2, rank=0)
+    with pytest.raises(mpc.MpcError) as e:
+        c.reveal(torch.zeros(4, dtype=torch.uint64, device="cuda"))
+    assert e.value.status == 6          # MPC_ERR_STATE
+
+
 @pytest.mark.parametrize("P", [3, 5])
 def test_wrap_pairs_parity(mpc, P):
     c = ctx(mpc, P)

@@ -350,6 +350,28 @@ def test_alg1_failure_rate_matches_paper():
     assert abs(rate - 0.0625) < 6 * sigma
 
 
+def test_sampled_triple_and_shares_match_full():
+    P, M, K, N = 3, 12, 9, 10
+    a, b, c = oracle.ttp_triple(P, MASTER, 6, M, K, N)
+    rows, cols = [11, 0, 5], [9, 2]
+    a2, b2, c2 = oracle.ttp_triple_sampled(P, MASTER, 6, M, K, N, rows, cols)
+    assert np.array_equal(a2, a[:, rows])
+    assert np.array_equal(b2, b[:, :, cols])
+    assert np.array_equal(c2, c[:, rows][:, :, cols])
+    Y = synth.uniform_ring((K, N), 4)
+    full = oracle.share(P, MASTER, Y, 2, 33)
+    idx = np.array([[k * N + j for j in cols] for k in range(K)])
+    part = oracle.share_indices(P, MASTER, Y.ravel()[idx.ravel()], 2, 33, idx)
+    assert np.array_equal(part.reshape(P, K, len(cols)), full[:, :, cols])
+
+
+def test_wrap_pair_indices_match_full():
+    r, th = oracle.wrap_pair(4, MASTER, 17, 50)
+    idx = [49, 3, 0, 17]
+    r2, th2 = oracle.wrap_pair_indices(4, MASTER, 17, idx)
+    assert np.array_equal(r2, r[:, idx]) and np.array_equal(th2, th[:, idx])
+
+
 def test_share_range_matches_full():
     x = synth.uniform_ring((10, 7), seed=3)
     full = oracle.share(3, MASTER, x, 1, 21)
