@@ -148,8 +148,6 @@ mpc_status beaver_local(mpc_ctx c, const BeaverWs& w, const uint64_t* ed, const 
 
 mpc_status gemm_run(mpc_ctx c, RingGemmParams& p, int parties) {
     p.kc = ring_gemm_default_kc(p.seg[0].kb + (p.nseg > 1 ? p.seg[1].kb : 0));
-    static const int prefetch_env = getenv("MPC_GEMM_PREFETCH") ? atoi(getenv("MPC_GEMM_PREFETCH")) : -1;
-    p.prefetch = prefetch_env >= 0 ? prefetch_env : 0;
     return run(c, kClsGemm, "ring_gemm", [&] { return ring_gemm_launch(p, parties, c->stream); });
 }
 

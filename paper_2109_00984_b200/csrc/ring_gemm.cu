@@ -124,9 +124,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 // commit all prior MMAs of this thread; arrive on `bar` (same offset) in both CTAs
@@ -190,6 +187,25 @@ struct TileMap {
     }
 };
 
+// Work item w -> (tile, K range): `splits` contiguous ranges of the fused
+// 32-K block sequence per tile (split-K for shapes with few tiles); the
+// ranges of one tile are consecutive items, so they run concurrently.
+struct WorkMap {
+    TileMap tm;
+    int tkb, kc, splits;
+    __device__ int items() const { return tm.parties * tm.mt * tm.nt * splits; }
+    __device__ void decode(int w, int& party, int& m, int& n, int& klo, int& khi) const {
+        const int t = w / splits, s = w % splits;
+        tm.decode(t, party, m, n);
+        klo = (int)((int64_t)tkb * s / splits);
+        khi = (int)((int64_t)tkb * (s + 1) / splits);
+    }
+    __device__ int item_kb(int w) const {
+        const int s = w % splits;
+        return (int)((int64_t)tkb * (s + 1) / splits) - (int)((int64_t)tkb * s / splits);
+    }
+};
+
 struct Bars {
     uint8_t* stage_base;
     uint64_t *full, *empty, *tfull, *tempty;
@@ -229,31 +245,21 @@ __device__ __forceinline__ void issue_kblock(uint64_t da, uint64_t db, uint32_t 
 }
 
 // ---------------------------------------------------------------- control warpgroup
-__device__ __forceinline__ void control_roles(const RingGemmParams& p, const TileMap& tm, int ntiles, int tkb, int kc,
-                                              int nchunks, int warp, int lane, uint32_t rank, uint32_t tmem_base,
-                                              const Bars& B) {
+__device__ __forceinline__ void control_roles(const RingGemmParams& p, const WorkMap& wm, int warp, int lane,
+                                              uint32_t rank, uint32_t tmem_base, const Bars& B) {
     const bool leader = rank == 0;
+    const int kc = wm.kc;
     if (warp == 0 && lane == 0) {
         // ------------------------------------------------ producer (both CTAs: own halves)
         int s = 0; uint32_t ph = 0;
         long long st_empty = 0;
-        for (int t = cluster_id(); t < ntiles; t += nclusters()) {
-            int party, m, n;
-            tm.decode(t, party, m, n);
+        for (int w = cluster_id(); w < wm.items(); w += nclusters()) {
+            int party, m, n, klo, khi;
+            wm.decode(w, party, m, n, klo, khi);
             const int64_t rbA = (int64_t)m * 2 + rank;       // 128-row left block
             const int64_t rbB = (int64_t)n * 2 + rank;       // 64-row right block
-            for (int c = 0; c < nchunks; ++c) {
-                const int k0 = c * kc, k1 = min(tkb, k0 + kc);
-                if (p.prefetch) {
-                    // warm L2 with the next K chunk of this tile while this chunk runs
-                    for (int kt = k1; kt < min(tkb, k1 + kc); ++kt) {
-                        const int sg = (kt < p.seg[0].kb) ? 0 : 1;
-                        const RingGemmSegment& S = p.seg[sg];
-                        const int kb = kt - (sg ? p.seg[0].kb : 0);
-                        prefetch_l2(S.A + party * S.party_stride_A + (rbA * S.kb + kb) * (8 * GL::kBlock), 8 * GL::kBlock);
-                        prefetch_l2(S.B + party * S.party_stride_B + (rbB * S.kb + kb) * (8 * GR::kBlock), 8 * GR::kBlock);
-                    }
-                }
+            for (int k0 = klo; k0 < khi; k0 += kc) {
+                const int k1 = min(khi, k0 + kc);
                 for (int g = 0; g < kPasses; ++g) {
                     const uint32_t bytesA = (uint32_t)pass_planes(g) * GL::kBlock;
                     const uint32_t bytesB = (uint32_t)pass_planes(g) * GR::kBlock;
@@ -279,8 +285,8 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Til
         // ------------------------------------------------ peer: relay "stage full" to the leader
         int s = 0; uint32_t ph = 0;
         const uint32_t leader_full0 = mapa(smem_u32(&B.full[0]), 0);
-        for (int t = cluster_id(); t < ntiles; t += nclusters())
-            for (int i = 0; i < kPasses * tkb; ++i) {
+        for (int w = cluster_id(); w < wm.items(); w += nclusters())
+            for (int i = 0; i < kPasses * wm.item_kb(w); ++i) {
                 mbar_wait(&B.full[s], ph);
                 mbar_arrive_cluster(leader_full0 + s * 8);
                 if (++s == kStages) { s = 0; ph ^= 1; }
@@ -290,9 +296,11 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Til
         int s = 0; uint32_t ph = 0; uint32_t u = 0;
         long long st_tempty = 0, st_full = 0;
         const long long t_start = clock64();
-        for (int t = cluster_id(); t < ntiles; t += nclusters()) {
-            for (int c = 0; c < nchunks; ++c) {
-                const int k0 = c * kc, k1 = min(tkb, k0 + kc);
+        for (int w = cluster_id(); w < wm.items(); w += nclusters()) {
+            int party, m, n, klo, khi;
+            wm.decode(w, party, m, n, klo, khi);
+            for (int k0 = klo; k0 < khi; k0 += kc) {
+                const int k1 = min(khi, k0 + kc);
                 for (int g = 0; g < kPasses; ++g, ++u) {
                     for (int kt = k0; kt < k1; ++kt) {
                         {
@@ -356,8 +364,12 @@ __device__ __forceinline__ void drain_pair(uint64_t (&run)[64], uint32_t t_lo, u
     }
 }
 
-__device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const TileMap& tm, int ntiles, int nchunks,
-                                              int warp, int lane, uint32_t rank, uint32_t tmem_base, const Bars& B) {
+__device__ __forceinline__ void red_add_u64(uint64_t* p, uint64_t v) {
+    asm volatile("red.global.add.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const WorkMap& wm, int warp, int lane,
+                                              uint32_t rank, uint32_t tmem_base, const Bars& B) {
     const int wq = warp & 3;                       // TMEM lane quadrant of this warp
     const int half = (warp - 4) >> 2;              // column half: 64 columns each
     const int row = wq * 32 + lane;
@@ -366,13 +378,13 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Til
     const uint64_t pol = evict_first_policy();
     const uint32_t tbase = tmem_base + ((uint32_t)(wq * 32) << 16) + half * 64;
     uint32_t u = 0;
-    for (int t = cluster_id(); t < ntiles; t += nclusters()) {
-        int party, m, n;
-        tm.decode(t, party, m, n);
+    for (int w = cluster_id(); w < wm.items(); w += nclusters()) {
+        int party, m, n, klo, khi;
+        wm.decode(w, party, m, n, klo, khi);
         uint64_t run[64];
 #pragma unroll
         for (int j = 0; j < 64; ++j) run[j] = 0;
-        for (int c = 0; c < nchunks; ++c) {
+        for (int k0 = klo; k0 < khi; k0 += wm.kc) {
             for (int g = 0; g < kPasses; ++g, ++u) {
                 mbar_wait(B.tfull, u & 1);
                 tc_fence_after();
@@ -394,7 +406,16 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Til
         }
         // tile end: z = trunc(c + sum of all units) — one write per element
         const int64_t grow = (int64_t)m * kTileM + rank * 128 + row;
-        if (grow < p.M) {
+        if (grow < p.M && wm.splits > 1) {
+            // split-K: add this K range's partial sum into z (zeroed by the host);
+            // ring addition commutes, so the order of the splits does not matter.
+            // c_p and the truncation are applied by ring_gemm_finalize.
+            uint64_t* zrow = p.Z + party * p.party_stride_z + grow * p.N;
+            const int64_t gc0 = (int64_t)n * kTileN + half * 64;
+#pragma unroll
+            for (int j = 0; j < 64; ++j)
+                if (gc0 + j < p.N) red_add_u64(zrow + gc0 + j, run[j]);
+        } else if (grow < p.M) {
             uint64_t* zrow = p.Z + party * p.party_stride_z + grow * p.N;
             const uint64_t* crow = p.C ? p.C + party * p.party_stride_c + grow * p.N : nullptr;
             const int64_t gc0 = (int64_t)n * kTileN + half * 64;
@@ -435,11 +456,11 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
     const bool leader = (rank == 0);
-    const TileMap tm{parties, (int)(pad_rows<Layout::Left>(p.M) / kTileM), (int)(pad_rows<Layout::Right>(p.N) / kTileN)};
-    const int ntiles = tm.parties * tm.mt * tm.nt;
-    const int tkb = p.seg[0].kb + (p.nseg > 1 ? p.seg[1].kb : 0);
-    const int kc = p.kc;
-    const int nchunks = (tkb + kc - 1) / kc;
+    WorkMap wm;
+    wm.tm = TileMap{parties, (int)(pad_rows<Layout::Left>(p.M) / kTileM), (int)(pad_rows<Layout::Right>(p.N) / kTileN)};
+    wm.tkb = p.seg[0].kb + (p.nseg > 1 ? p.seg[1].kb : 0);
+    wm.kc = p.kc;
+    wm.splits = p.splits < 1 ? 1 : p.splits;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) { mbar_init(&B.full[s], leader ? 2 : 1); mbar_init(&B.empty[s], 1); }
@@ -459,10 +480,10 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     // register budget: the control warpgroup needs few, the epilogue holds 64 u64 sums per thread
     if (warp < 4) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
-        control_roles(p, tm, ntiles, tkb, kc, nchunks, warp, lane, rank, tmem_base, B);
+        control_roles(p, wm, warp, lane, rank, tmem_base, B);
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
-        epilogue_role(p, tm, ntiles, nchunks, warp, lane, rank, tmem_base, B);
+        epilogue_role(p, wm, warp, lane, rank, tmem_base, B);
     }
     __syncwarp();
     tc_fence_before();
@@ -516,16 +537,27 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t tiles = (int64_t)parties * (pad_rows<Layout::Left>(prm.M) / gemm::kTileM) *
                           (pad_rows<Layout::Right>(prm.N) / gemm::kTileN);
-    int64_t clusters = sms / 2;
-    if (tiles < clusters) clusters = tiles;
+    const int64_t max_clusters = sms / 2;
+    const int tkb = prm.seg[0].kb + (prm.nseg > 1 ? prm.seg[1].kb : 0);
+    RingGemmParams q = prm;
+    q.splits = ring_gemm_choose_splits(tiles, tkb, max_clusters);
+    if (q.splits > 1) {
+        // split-K: partial sums are red.add-ed into z, then c_p and the truncation are applied
+        cudaError_t e = cudaMemsetAsync(q.Z, 0, (size_t)ring_gemm_out_elems(q, parties) * sizeof(uint64_t), stream);
+        if (e != cudaSuccess) return e;
+        const int64_t kc_split = (tkb + q.splits - 1) / q.splits;
+        if (kc_split < q.kc) q.kc = (int)kc_split;
+    }
+    int64_t clusters = tiles * q.splits < max_clusters ? tiles * q.splits : max_clusters;
     if (clusters < 1) clusters = 1;
     static const bool debug = getenv("MPC_GEMM_DEBUG") != nullptr;
     if (!debug) {
-        gemm::ring_gemm_kernel<<<(unsigned)(clusters * 2), gemm::kThreads, smem, stream>>>(prm, parties);
-        return cudaGetLastError();
+        gemm::ring_gemm_kernel<<<(unsigned)(clusters * 2), gemm::kThreads, smem, stream>>>(q, parties);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess || q.splits <= 1) return e;
+        return ring_gemm_finalize(q, parties, stream);
     }
     // diagnostic mode: stall-cycle attribution of the producer and MMA threads
-    RingGemmParams q = prm;
     cudaMalloc(&q.dbg, 4 * sizeof(unsigned long long));
     cudaMemsetAsync(q.dbg, 0, 4 * sizeof(unsigned long long), stream);
     gemm::ring_gemm_kernel<<<(unsigned)(clusters * 2), gemm::kThreads, smem, stream>>>(q, parties);
@@ -535,11 +567,55 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     cudaStreamSynchronize(stream);
     cudaFree(q.dbg);
     const double n = (double)clusters;
-    fprintf(stderr, "[ring_gemm] M=%lld N=%lld kb=%d kc=%d clusters=%lld  per MMA thread: total %.0f cyc, "
+    fprintf(stderr, "[ring_gemm] M=%lld N=%lld kb=%d kc=%d splits=%d clusters=%lld  per MMA thread: total %.0f cyc, "
             "wait tempty %.1f%%, wait full %.1f%%; producer wait empty %.0f cyc\n",
-            (long long)prm.M, (long long)prm.N, prm.seg[0].kb + (prm.nseg > 1 ? prm.seg[1].kb : 0), prm.kc,
-            (long long)clusters, h[3] / n, 100.0 * h[1] / h[3], 100.0 * h[2] / h[3], h[0] / (2 * n));
-    return e;
+            (long long)prm.M, (long long)prm.N, tkb, q.kc, q.splits, (long long)clusters, h[3] / n,
+            100.0 * h[1] / h[3], 100.0 * h[2] / h[3], h[0] / (2 * n));
+    q.dbg = nullptr;
+    if (e != cudaSuccess || q.splits <= 1) return e;
+    return ring_gemm_finalize(q, parties, stream);
+}
+
+// Split-K factor: minimise (waves of work items) x (blocks per item), with at
+// least 8 blocks per item; ties keep fewer splits (the finalize pass costs an
+// extra read/write of z).
+int ring_gemm_choose_splits(int64_t tiles, int tkb, int64_t clusters) {
+    static const int env = getenv("MPC_GEMM_SPLITS") ? atoi(getenv("MPC_GEMM_SPLITS")) : 0;
+    if (env > 0) return tkb >= env ? env : (tkb > 0 ? tkb : 1);
+    if (tiles <= 0 || tkb < 16 || tiles >= clusters) return 1;
+    int best = 1;
+    double best_cost = 1e30;
+    for (int s = 1; s <= tkb / 8 && s <= 64; ++s) {
+        const int64_t waves = (tiles * s + clusters - 1) / clusters;
+        const double cost = (double)waves * ((tkb + s - 1) / s) * 1.0 + (s > 1 ? 2.0 : 0.0);
+        if (cost < best_cost - 1e-9) { best_cost = cost; best = s; }
+    }
+    return best;
+}
+
+namespace gemm {
+__global__ void finalize_kernel(uint64_t* __restrict__ z, const uint64_t* __restrict__ c, int64_t n, int bits) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t v = z[i] + (c ? c[i] : 0ull);
+        z[i] = bits ? div_pow2_round(v, bits) : v;
+    }
+}
+}  // namespace gemm
+
+// z = trunc(z + c) over all parties after a split-K GEMM (party buffers contiguous).
+int64_t ring_gemm_out_elems(const RingGemmParams& q, int parties) {
+    return parties > 1 ? (int64_t)parties * q.party_stride_z : q.M * q.N;
+}
+
+cudaError_t ring_gemm_finalize(const RingGemmParams& q, int parties, cudaStream_t stream) {
+    const int64_t n = ring_gemm_out_elems(q, parties);
+    if (parties > 1 && (q.party_stride_z != q.M * q.N || (q.C && q.party_stride_c != q.party_stride_z)))
+        return cudaErrorInvalidValue;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    gemm::finalize_kernel<<<(unsigned)blocks, 256, 0, stream>>>(q.Z, q.C, n, q.trunc_bits);
+    return cudaGetLastError();
 }
 
 }  // namespace mpc

@@ -23,7 +23,7 @@ struct RingGemmParams {
     int trunc_bits;                     // 0 = none; else per-share round-half-up division (R10)
     int kc;                             // 32-K blocks per accumulation unit (<= ring_gemm_max_kc())
     unsigned long long* dbg;            // optional: per-cluster stall cycles [producer empty, MMA tempty, MMA full]
-    int prefetch;                       // 1: producer prefetches the next K chunk into L2
+    int splits;                         // K ranges per output tile (split-K); 0/1 = none.  Set by the launcher.
 };
 
 // Largest unit length (32-K blocks) for which every s32 accumulator stays exact.
@@ -31,6 +31,9 @@ int ring_gemm_max_kc();
 // Unit length used for a fused reduction of `total_kb` blocks (L2-window sized).
 int ring_gemm_default_kc(int total_kb);
 size_t ring_gemm_smem_bytes();
+int ring_gemm_choose_splits(int64_t tiles, int tkb, int64_t clusters);
+int64_t ring_gemm_out_elems(const RingGemmParams& q, int parties);
+cudaError_t ring_gemm_finalize(const RingGemmParams& q, int parties, cudaStream_t stream);
 cudaError_t ring_gemm_launch(const RingGemmParams& p, int parties, cudaStream_t stream);
 
 }  // namespace mpc

@@ -1,0 +1,94 @@
+"""Per-layer 2-party Beaver matmul timings for the paper's model workloads
+(configs[2]/[3]: ResNet-50 batch 1 im2col GEMMs, ViT-B/16 linear layers),
+both parties on one GPU, truncation fused.  Reports µs per private matmul,
+ring-TOPS and the share of the layer time spent in the tcgen05 GEMM.
+
+  python scripts/bench_layers.py [--model resnet50|vit|all] [--reps 20] [--graph]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+import paper_2109_00984_b200 as mpc  # noqa: E402
+
+
+def run_layer(ctx, M, K, N, reps, graph):
+    dev = torch.device("cuda", 0)
+    X = synth.uniform_fixed((M, K), 11)
+    Y = synth.uniform_fixed((K, N), 12)
+    x = ctx.share(torch.from_numpy(X.view(np.int64)).to(dev).view(torch.uint64), 0, 1)
+    y = ctx.share(torch.from_numpy(Y.view(np.int64)).to(dev).view(torch.uint64), 1, 2)
+    a, b, c = ctx.ttp_triples(1, M, K, N)
+    z = torch.empty_like(c)
+    ctx.beaver_matmul(x, y, a, b, c, truncate=True, out=z)
+    torch.cuda.synchronize()
+    if graph:
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            ctx.beaver_matmul(x, y, a, b, c, truncate=True, out=z)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                ctx.beaver_matmul(x, y, a, b, c, truncate=True, out=z)
+        step = g.replay
+    else:
+        def step():
+            ctx.beaver_matmul(x, y, a, b, c, truncate=True, out=z)
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    ctx.profile_enable(True)
+    ctx.profile_read("gemm")
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(reps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    gemm_ms, _ = ctx.profile_read("gemm")
+    ctx.profile_enable(False)
+    ms = e0.elapsed_time(e1) / reps
+    return ms, (gemm_ms / reps if not graph else None)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="all", choices=["resnet50", "vit", "all"])
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--graph", action="store_true")
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    ctx = mpc.Context(2, mpc.ALL_PARTIES, device=0, master_seed=synth.MASTER_SEED)
+    models = {"resnet50": synth.RESNET50_B1, "vit": synth.VIT_B16}
+    out = {}
+    for name, layers in models.items():
+        if args.model not in (name, "all"):
+            continue
+        rows, total_ms, total_ops = [], 0.0, 0.0
+        for lname, M, K, N, count in layers:
+            ms, gms = run_layer(ctx, M, K, N, args.reps, args.graph)
+            total_ms += ms * count
+            total_ops += 2.0 * M * K * N * count
+            rows.append({"layer": lname, "M": M, "K": K, "N": N, "count": count, "us": ms * 1e3,
+                         "gemm_us": None if gms is None else gms * 1e3,
+                         "ring_TOPS": 2.0 * M * K * N / (ms * 1e-3) / 1e12})
+            print(f"{name:9s} {lname:12s} {M:6d}x{K:5d}x{N:5d} x{count:2d}  {ms * 1e3:9.1f} us"
+                  + ("" if gms is None else f"  (gemm {gms * 1e3:8.1f} us)")
+                  + f"  {rows[-1]['ring_TOPS']:7.2f} ring-TOPS", flush=True)
+        out[name] = {"layers": rows, "total_ms": total_ms, "ring_TOPS": total_ops / (total_ms * 1e-3) / 1e12,
+                     "graph": args.graph}
+        print(f"{name}: total {total_ms:.3f} ms per private inference's linear layers "
+              f"({out[name]['ring_TOPS']:.2f} ring-TOPS)", flush=True)
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
