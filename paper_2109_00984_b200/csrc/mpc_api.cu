@@ -124,6 +124,7 @@ struct BeaverWs {
     uint64_t* ed;        // one-party mode: [e | d] reveal buffer
     uint64_t* zbuf;      // one-party, P > 2, truncation: z reveal
     int8_t* hbuf;        // one-party, P > 2, truncation: top nibbles
+    uint64_t* partials;  // ring GEMM split-K slabs (small shapes only)
     size_t total;
 };
 
@@ -139,6 +140,8 @@ BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N) {
     const bool alg1_one = !c->all && c->P > 2;
     w.zbuf = reinterpret_cast<uint64_t*>(alg1_one ? cv.take(8 * (size_t)(M * N)) : nullptr);
     w.hbuf = reinterpret_cast<int8_t*>(alg1_one ? cv.take((size_t)(M * N)) : nullptr);
+    const size_t pb = ring_gemm_partials_bytes(Pl, M, N, 2 * (int)num_kb(K));
+    w.partials = reinterpret_cast<uint64_t*>(pb ? cv.take(pb) : nullptr);
     w.total = cv.off;
     return w;
 }
@@ -313,7 +316,7 @@ mpc_status mpc_reveal(mpc_ctx c, const uint64_t* share, uint64_t* out, int64_t n
 size_t mpc_ttp_workspace_bytes(mpc_ctx c, int64_t M, int64_t K, int64_t N) {
     (void)c;
     if (M < 0 || K < 0 || N < 0) return 0;
-    return align256(lp(M, K)) + align256(rp(N, K));
+    return align256(lp(M, K)) + align256(rp(N, K)) + align256(ring_gemm_partials_bytes(1, M, N, (int)num_kb(K)));
 }
 
 mpc_status mpc_ttp_triples(mpc_ctx c, uint64_t id, int64_t M, int64_t K, int64_t N, uint64_t* a, uint64_t* b,
@@ -328,6 +331,8 @@ mpc_status mpc_ttp_triples(mpc_ctx c, uint64_t id, int64_t M, int64_t K, int64_t
     Carve cv(ws);
     uint8_t* a_pl = ttp ? cv.take(lp(M, K)) : nullptr;
     uint8_t* b_pl = ttp ? cv.take(rp(N, K)) : nullptr;
+    const size_t pb = ring_gemm_partials_bytes(1, M, N, (int)num_kb(K));
+    uint64_t* partials = reinterpret_cast<uint64_t*>(ttp && pb ? cv.take(pb) : nullptr);
     TtpGenArgs ga{c->kttp, id, kTagA, c->P, M, K, lo, hi, a, a_pl};
     CHECK(run(c, kClsPrg, "ttp_a", [&] { return launch_ttp_left(ga, c->stream); }));
     TtpGenArgs gb{c->kttp, id, kTagB, c->P, N, K, lo, hi, b, b_pl};
@@ -341,6 +346,7 @@ mpc_status mpc_ttp_triples(mpc_ctx c, uint64_t id, int64_t M, int64_t K, int64_t
         p.M = M; p.N = N; p.C = nullptr; p.Z = cc;
         p.party_stride_c = p.party_stride_z = 0;
         p.trunc_bits = 0;
+        p.partials = partials;
         CHECK(gemm_run(c, p, 1));
     }
     uint64_t* c_out = c->all ? cc + M * N : cc;    // parties >= 1
@@ -440,6 +446,7 @@ mpc_status beaver_local(mpc_ctx c, const BeaverWs& w, const uint64_t* ed, const 
     RingGemmParams p{};
     p.seg[0] = RingGemmSegment{w.a_pl, w.delta_pl, (int)num_kb(K), lp(M, K), 0};   // a_p @ delta
     p.seg[1] = RingGemmSegment{w.eps_pl, w.b_pl, (int)num_kb(K), 0, rp(N, K)};     // eps @ b'_p
+    p.partials = w.partials;
     p.nseg = 2;
     p.M = M; p.N = N; p.C = cc; p.Z = z;
     p.party_stride_c = p.party_stride_z = sMN;
@@ -468,7 +475,7 @@ mpc_status mpc_truncate(mpc_ctx c, uint64_t* x, int64_t n, int bits, uint64_t wr
 
 size_t mpc_ring_matmul_workspace_bytes(int64_t M, int64_t K, int64_t N) {
     if (M < 0 || K < 0 || N < 0) return 0;
-    return align256(lp(M, K)) + align256(rp(N, K));
+    return align256(lp(M, K)) + align256(rp(N, K)) + align256(ring_gemm_partials_bytes(1, M, N, (int)num_kb(K)));
 }
 
 mpc_status mpc_ring_matmul(mpc_ctx c, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t M, int64_t K,
@@ -489,6 +496,8 @@ mpc_status mpc_ring_matmul(mpc_ctx c, const uint64_t* A, const uint64_t* B, uint
     p.seg[0] = RingGemmSegment{a_pl, b_pl, (int)num_kb(K), 0, 0};
     p.nseg = 1;
     p.M = M; p.N = N; p.C = nullptr; p.Z = C;
+    const size_t pb = ring_gemm_partials_bytes(1, M, N, (int)num_kb(K));
+    p.partials = reinterpret_cast<uint64_t*>(pb ? cv.take(pb) : nullptr);
     return gemm_run(c, p, 1);
 }
 

@@ -124,6 +124,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 // commit all prior MMAs of this thread; arrive on `bar` (same offset) in both CTAs
@@ -364,10 +369,6 @@ __device__ __forceinline__ void drain_pair(uint64_t (&run)[64], uint32_t t_lo, u
     }
 }
 
-__device__ __forceinline__ void red_add_u64(uint64_t* p, uint64_t v) {
-    asm volatile("red.global.add.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
-}
-
 __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const WorkMap& wm, int warp, int lane,
                                               uint32_t rank, uint32_t tmem_base, const Bars& B) {
     const int wq = warp & 3;                       // TMEM lane quadrant of this warp
@@ -407,14 +408,20 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Wor
         // tile end: z = trunc(c + sum of all units) — one write per element
         const int64_t grow = (int64_t)m * kTileM + rank * 128 + row;
         if (grow < p.M && wm.splits > 1) {
-            // split-K: add this K range's partial sum into z (zeroed by the host);
-            // ring addition commutes, so the order of the splits does not matter.
-            // c_p and the truncation are applied by ring_gemm_finalize.
-            uint64_t* zrow = p.Z + party * p.party_stride_z + grow * p.N;
+            // split-K: store this K range's partial sum in its own slab of the
+            // partials buffer; ring_gemm_finalize adds the slabs (ring addition
+            // commutes, any order is exact), c_p, and applies the truncation.
+            const int s = w % wm.splits;
+            uint64_t* prow = p.partials + (int64_t)s * p.partial_stride + party * p.M * p.N + grow * p.N;
             const int64_t gc0 = (int64_t)n * kTileN + half * 64;
+            if (vec && gc0 + 64 <= p.N) {
 #pragma unroll
-            for (int j = 0; j < 64; ++j)
-                if (gc0 + j < p.N) red_add_u64(zrow + gc0 + j, run[j]);
+                for (int j = 0; j < 64; j += 2) st_stream(prow + gc0 + j, make_ulonglong2(run[j], run[j + 1]), pol);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 64; ++j)
+                    if (gc0 + j < p.N) prow[gc0 + j] = run[j];
+            }
         } else if (grow < p.M) {
             uint64_t* zrow = p.Z + party * p.party_stride_z + grow * p.N;
             const uint64_t* crow = p.C ? p.C + party * p.party_stride_c + grow * p.N : nullptr;
@@ -445,6 +452,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    if (p.dbg && threadIdx.x == 0) atomicMin(&p.dbg[4], globaltimer());      // timeline (debug mode)
     Bars B;
     B.stage_base = smem;
     B.full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -477,13 +485,16 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (p.dbg && threadIdx.x == 0) atomicMax(&p.dbg[5], globaltimer());
     // register budget: the control warpgroup needs few, the epilogue holds 64 u64 sums per thread
     if (warp < 4) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
         control_roles(p, wm, warp, lane, rank, tmem_base, B);
+        if (p.dbg && warp == 1 && lane == 0 && rank == 0) atomicMax(&p.dbg[6], globaltimer());
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
         epilogue_role(p, wm, warp, lane, rank, tmem_base, B);
+        if (p.dbg && lane == 0) atomicMax(&p.dbg[7], globaltimer());
     }
     __syncwarp();
     tc_fence_before();
@@ -540,11 +551,10 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     const int64_t max_clusters = sms / 2;
     const int tkb = prm.seg[0].kb + (prm.nseg > 1 ? prm.seg[1].kb : 0);
     RingGemmParams q = prm;
-    q.splits = ring_gemm_choose_splits(tiles, tkb, max_clusters);
+    q.splits = prm.partials ? ring_gemm_choose_splits(tiles, tkb, max_clusters) : 1;
     if (q.splits > 1) {
-        // split-K: partial sums are red.add-ed into z, then c_p and the truncation are applied
-        cudaError_t e = cudaMemsetAsync(q.Z, 0, (size_t)ring_gemm_out_elems(q, parties) * sizeof(uint64_t), stream);
-        if (e != cudaSuccess) return e;
+        // split-K: partial sums go to per-split slabs, then finalize adds them, c_p, truncates
+        q.partial_stride = ring_gemm_out_elems(q, parties);
         const int64_t kc_split = (tkb + q.splits - 1) / q.splits;
         if (kc_split < q.kc) q.kc = (int)kc_split;
     }
@@ -558,19 +568,28 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
         return ring_gemm_finalize(q, parties, stream);
     }
     // diagnostic mode: stall-cycle attribution of the producer and MMA threads
-    cudaMalloc(&q.dbg, 4 * sizeof(unsigned long long));
-    cudaMemsetAsync(q.dbg, 0, 4 * sizeof(unsigned long long), stream);
+    unsigned long long h[8] = {0, 0, 0, 0, ~0ull, 0, 0, 0};
+    cudaMalloc(&q.dbg, sizeof(h));
+    cudaMemcpyAsync(q.dbg, h, sizeof(h), cudaMemcpyHostToDevice, stream);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0, stream);
     gemm::ring_gemm_kernel<<<(unsigned)(clusters * 2), gemm::kThreads, smem, stream>>>(q, parties);
+    cudaEventRecord(e1, stream);
     cudaError_t e = cudaGetLastError();
-    unsigned long long h[4] = {0, 0, 0, 0};
     cudaMemcpyAsync(h, q.dbg, sizeof(h), cudaMemcpyDeviceToHost, stream);
     cudaStreamSynchronize(stream);
+    float kms = 0.f;
+    cudaEventElapsedTime(&kms, e0, e1);
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
     cudaFree(q.dbg);
     const double n = (double)clusters;
     fprintf(stderr, "[ring_gemm] M=%lld N=%lld kb=%d kc=%d splits=%d clusters=%lld  per MMA thread: total %.0f cyc, "
-            "wait tempty %.1f%%, wait full %.1f%%; producer wait empty %.0f cyc\n",
+            "wait tempty %.1f%%, wait full %.1f%%; producer wait empty %.0f cyc | event %.1f us, timeline us: "
+            "setup done %.1f, MMA end %.1f, epilogue end %.1f\n",
             (long long)prm.M, (long long)prm.N, tkb, q.kc, q.splits, (long long)clusters, h[3] / n,
-            100.0 * h[1] / h[3], 100.0 * h[2] / h[3], h[0] / (2 * n));
+            100.0 * h[1] / h[3], 100.0 * h[2] / h[3], h[0] / (2 * n), kms * 1e3, (h[5] - h[4]) * 1e-3,
+            (h[6] - h[4]) * 1e-3, (h[7] - h[4]) * 1e-3);
     q.dbg = nullptr;
     if (e != cudaSuccess || q.splits <= 1) return e;
     return ring_gemm_finalize(q, parties, stream);
@@ -593,10 +612,22 @@ int ring_gemm_choose_splits(int64_t tiles, int tkb, int64_t clusters) {
     return best;
 }
 
+size_t ring_gemm_partials_bytes(int parties, int64_t M, int64_t N, int total_kb) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t tiles = (int64_t)parties * (pad_rows<Layout::Left>(M) / gemm::kTileM) *
+                          (pad_rows<Layout::Right>(N) / gemm::kTileN);
+    const int s = ring_gemm_choose_splits(tiles, total_kb, sms / 2);
+    return s > 1 ? (size_t)s * parties * M * N * sizeof(uint64_t) : 0;
+}
+
 namespace gemm {
-__global__ void finalize_kernel(uint64_t* __restrict__ z, const uint64_t* __restrict__ c, int64_t n, int bits) {
+__global__ void finalize_kernel(uint64_t* __restrict__ z, const uint64_t* __restrict__ c,
+                                const uint64_t* __restrict__ part, int splits, int64_t n, int bits) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t v = z[i] + (c ? c[i] : 0ull);
+        uint64_t v = c ? c[i] : 0ull;
+        for (int s = 0; s < splits; ++s) v += part[(int64_t)s * n + i];
         z[i] = bits ? div_pow2_round(v, bits) : v;
     }
 }
@@ -614,7 +645,7 @@ cudaError_t ring_gemm_finalize(const RingGemmParams& q, int parties, cudaStream_
     int64_t blocks = (n + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
-    gemm::finalize_kernel<<<(unsigned)blocks, 256, 0, stream>>>(q.Z, q.C, n, q.trunc_bits);
+    gemm::finalize_kernel<<<(unsigned)blocks, 256, 0, stream>>>(q.Z, q.C, q.partials, q.splits, n, q.trunc_bits);
     return cudaGetLastError();
 }
 

@@ -22,8 +22,13 @@ struct RingGemmParams {
     int64_t party_stride_c, party_stride_z;  // elements
     int trunc_bits;                     // 0 = none; else per-share round-half-up division (R10)
     int kc;                             // 32-K blocks per accumulation unit (<= ring_gemm_max_kc())
-    unsigned long long* dbg;            // optional: per-cluster stall cycles [producer empty, MMA tempty, MMA full]
+    unsigned long long* dbg;            // optional (MPC_GEMM_DEBUG): [0..3] stall cycles (producer empty, MMA
+                                        // tempty, MMA full, MMA total); [4..7] globaltimer: first entry, last
+                                        // setup done, last MMA end, last epilogue end
     int splits;                         // K ranges per output tile (split-K); 0/1 = none.  Set by the launcher.
+    uint64_t* partials;                 // split-K slabs [splits][parties][M][N] (workspace,
+                                        // ring_gemm_partials_bytes); unused when splits <= 1
+    int64_t partial_stride;             // elements per slab (parties * M * N)
 };
 
 // Largest unit length (32-K blocks) for which every s32 accumulator stays exact.
@@ -32,6 +37,8 @@ int ring_gemm_max_kc();
 int ring_gemm_default_kc(int total_kb);
 size_t ring_gemm_smem_bytes();
 int ring_gemm_choose_splits(int64_t tiles, int tkb, int64_t clusters);
+// workspace for the split-K partial sums of a GEMM with these sizes (0 if no split)
+size_t ring_gemm_partials_bytes(int parties, int64_t M, int64_t N, int total_kb);
 int64_t ring_gemm_out_elems(const RingGemmParams& q, int parties);
 cudaError_t ring_gemm_finalize(const RingGemmParams& q, int parties, cudaStream_t stream);
 cudaError_t ring_gemm_launch(const RingGemmParams& p, int parties, cudaStream_t stream);
