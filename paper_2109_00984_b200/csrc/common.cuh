@@ -5,6 +5,8 @@
 // listed in DESIGN.md.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <cuda_runtime.h>
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
@@ -136,6 +138,27 @@ __device__ __forceinline__ void store_limbs8(uint8_t* planes, int64_t row, int64
 #pragma unroll
     for (int l = 0; l < 8; ++l)
         *reinterpret_cast<uint2*>(planes + base + (int64_t)l * PlaneGeom<L>::kBlock) = make_uint2(w[l][0], w[l][1]);
+}
+
+// ------------------------------------------------------------ launches
+// Launch as a programmatic dependent of the previous kernel in the stream
+// (PDL): its CTAs may start while the previous kernel drains; the kernel must
+// execute `griddepcontrol.wait` before reading anything that kernel wrote.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    static const bool off = getenv("MPC_NO_PDL") != nullptr;     // A/B switch for measurements
+    cfg.attrs = attr;
+    cfg.numAttrs = off ? 0 : 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // ------------------------------------------------------------ signed helpers

@@ -6,6 +6,7 @@
 // local reveal and the u8 limb split that feeds the tcgen05 ring GEMM,
 // TTP triple / wrap-pair generation (Alg. 1
 // inputs P:611-612) and truncation.
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "common.cuh"
@@ -125,7 +126,8 @@ __device__ __forceinline__ void load16(const uint64_t* __restrict__ src, bool fu
     }
 }
 
-__global__ void __launch_bounds__(256) split_left_kernel(LeftSplitArgs a) {
+// (bid, nblk): this block's index among the nblk blocks working on the left split
+__device__ __forceinline__ void split_left_body(const LeftSplitArgs& a, int64_t bid, int64_t nblk) {
     const int64_t KB = num_kb(a.K);
     const int64_t row_groups = (a.M + 7) / 8;
     const int64_t kgroups = (KB * kKBlock + 63) / 64;      // whole padded K: pad limbs must be 0
@@ -133,8 +135,7 @@ __global__ void __launch_bounds__(256) split_left_kernel(LeftSplitArgs a) {
     const int lane = threadIdx.x & 31;
     const bool vec = (a.K & 1) == 0 && (a.party_stride & 1) == 0;
     const bool fused_copy = a.cp_src == a.minus && a.Pcopy == a.Psum && a.Psum > 0;
-    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < warps_total;
-         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    for (int64_t w = (bid * blockDim.x + threadIdx.x) >> 5; w < warps_total; w += (nblk * blockDim.x) >> 5) {
         const int64_t rg = w / kgroups, kg = w % kgroups;
         const int64_t row = rg * 8 + (lane & 7);
         const int64_t k0 = kg * 64 + (lane >> 3) * 16;
@@ -165,6 +166,9 @@ __global__ void __launch_bounds__(256) split_left_kernel(LeftSplitArgs a) {
             }
         }
     }
+}
+__global__ void __launch_bounds__(256) split_left_kernel(LeftSplitArgs a) {
+    split_left_body(a, blockIdx.x, gridDim.x);
 }
 cudaError_t launch_split_left(const LeftSplitArgs& a, cudaStream_t st) {
     if (a.M == 0 || a.K == 0) return cudaSuccess;
@@ -206,7 +210,7 @@ __device__ __forceinline__ void load_cols(const uint64_t* __restrict__ base, int
     }
 }
 
-__global__ void __launch_bounds__(256, 2) split_right_kernel(RightSplitArgs a) {
+__device__ __forceinline__ void split_right_body(const RightSplitArgs& a, int64_t bid, int64_t nblk) {
     const int64_t KB = num_kb(a.K);
     const int64_t ngroups = (a.N + 31) / 32;
     const int64_t kchunks = KB * 2;                         // whole padded K, 16 per chunk
@@ -214,8 +218,7 @@ __global__ void __launch_bounds__(256, 2) split_right_kernel(RightSplitArgs a) {
     const int lane = threadIdx.x & 31;
     const bool fused_copy = a.cp_src == a.minus && a.Pcopy == a.Psum && a.Psum > 0;
     const bool even = (a.N & 1) == 0 && (a.party_stride & 1) == 0;
-    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < warps_total;
-         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    for (int64_t w = (bid * blockDim.x + threadIdx.x) >> 5; w < warps_total; w += (nblk * blockDim.x) >> 5) {
         const int64_t kc = w / ngroups, ng = w % ngroups;
         const int64_t n = ng * 32 + 2 * (lane & 15);
         const int64_t k0 = kc * 16 + (lane >> 4) * 8;
@@ -258,10 +261,39 @@ __global__ void __launch_bounds__(256, 2) split_right_kernel(RightSplitArgs a) {
         }
     }
 }
+__global__ void __launch_bounds__(256, 2) split_right_kernel(RightSplitArgs a) {
+    split_right_body(a, blockIdx.x, gridDim.x);
+}
 cudaError_t launch_split_right(const RightSplitArgs& a, cudaStream_t st) {
     if (a.N == 0 || a.K == 0) return cudaSuccess;
     const int64_t warps = ((a.N + 31) / 32) * (num_kb(a.K) * 2);
     split_right_kernel<<<grid_for(warps * 32), 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+// Both splits of one Beaver matmul in a single launch (they are independent):
+// blocks [0, nleft) run the left split, the rest the right split.
+__global__ void __launch_bounds__(256, 2) split_both_kernel(LeftSplitArgs l, RightSplitArgs r, int nleft) {
+    if ((int)blockIdx.x < nleft) split_left_body(l, blockIdx.x, nleft);
+    else split_right_body(r, blockIdx.x - nleft, gridDim.x - nleft);
+    // each block is done: once all are, the ring GEMM (a programmatic dependent)
+    // may launch and run its prologue while the last blocks drain — triggering
+    // earlier would let GEMM CTAs take SMs from the split's tail
+    asm volatile("griddepcontrol.launch_dependents;");
+}
+cudaError_t launch_split_both(const LeftSplitArgs& l, const RightSplitArgs& r, cudaStream_t st) {
+    const bool dl = l.M > 0 && l.K > 0, dr = r.N > 0 && r.K > 0;
+    if (!dl && !dr) return cudaSuccess;
+    if (!dr) return launch_split_left(l, st);
+    if (!dl) return launch_split_right(r, st);
+    const int64_t wl = ((l.M + 7) / 8) * ((num_kb(l.K) * kKBlock + 63) / 64) * 32;
+    const int64_t wr = ((r.N + 31) / 32) * (num_kb(r.K) * 2) * 32;
+    // share the block budget in proportion to the bytes each side moves
+    const int64_t bytes_l = l.M * l.K * (int64_t)(2 * l.Psum + l.Pcopy + 1);
+    const int64_t bytes_r = r.N * r.K * (int64_t)(2 * r.Psum + r.Pcopy + 1);
+    int64_t nl = std::min<int64_t>(grid_for(wl), std::max<int64_t>(1, 148 * 16 * bytes_l / (bytes_l + bytes_r)));
+    int64_t nr = std::min<int64_t>(grid_for(wr), std::max<int64_t>(1, 148 * 16 - nl));
+    split_both_kernel<<<(unsigned)(nl + nr), 256, 0, st>>>(l, r, (int)nl);
     return cudaGetLastError();
 }
 

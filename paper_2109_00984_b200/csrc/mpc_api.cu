@@ -387,9 +387,8 @@ mpc_status mpc_beaver_matmul(mpc_ctx c, const uint64_t* x, const uint64_t* y, co
     const int64_t sMK = M * K, sKN = K * N, sMN = M * N;
     if (c->all) {
         LeftSplitArgs L{M, K, sMK, x, a, c->P, w.eps_pl, a, c->P, w.a_pl, lp(M, K)};
-        CHECK(run(c, kClsSplit, "mask+reveal+split eps", [&] { return launch_split_left(L, c->stream); }));
         RightSplitArgs R{K, N, sKN, y, b, c->P, w.delta_pl, b, c->P, 1, w.b_pl, rp(N, K)};
-        CHECK(run(c, kClsSplit, "mask+reveal+split delta", [&] { return launch_split_right(R, c->stream); }));
+        CHECK(run(c, kClsSplit, "mask+reveal+split", [&] { return launch_split_both(L, R, c->stream); }));
     } else {
         CHECK(run(c, kClsSplit, "mask", [&] { return launch_mask(x, a, sMK, y, b, sKN, w.ed, c->stream); }));
         if (c->P > 1) CHECK(nccl_allreduce(c, w.ed, w.ed, (size_t)(sMK + sKN), ncclUint64, "eps/delta reveal"));
@@ -439,9 +438,8 @@ mpc_status beaver_local(mpc_ctx c, const BeaverWs& w, const uint64_t* ed, const 
     const int64_t sMK = M * K, sMN = M * N;
     if (!c->all) {
         LeftSplitArgs L{M, K, 0, ed, nullptr, 1, w.eps_pl, a, 1, w.a_pl, 0};
-        CHECK(run(c, kClsSplit, "split eps", [&] { return launch_split_left(L, c->stream); }));
         RightSplitArgs R{K, N, 0, ed + sMK, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0};
-        CHECK(run(c, kClsSplit, "split delta", [&] { return launch_split_right(R, c->stream); }));
+        CHECK(run(c, kClsSplit, "split eps/delta", [&] { return launch_split_both(L, R, c->stream); }));
     }
     RingGemmParams p{};
     p.seg[0] = RingGemmSegment{w.a_pl, w.delta_pl, (int)num_kb(K), lp(M, K), 0};   // a_p @ delta
@@ -489,9 +487,8 @@ mpc_status mpc_ring_matmul(mpc_ctx c, const uint64_t* A, const uint64_t* B, uint
     uint8_t* a_pl = cv.take(lp(M, K));
     uint8_t* b_pl = cv.take(rp(N, K));
     LeftSplitArgs L{M, K, 0, A, nullptr, 1, a_pl, nullptr, 0, nullptr, 0};
-    CHECK(run(c, kClsSplit, "split A", [&] { return launch_split_left(L, c->stream); }));
     RightSplitArgs R{K, N, 0, B, nullptr, 1, b_pl, nullptr, 0, 0, nullptr, 0};
-    CHECK(run(c, kClsSplit, "split B", [&] { return launch_split_right(R, c->stream); }));
+    CHECK(run(c, kClsSplit, "split A/B", [&] { return launch_split_both(L, R, c->stream); }));
     RingGemmParams p{};
     p.seg[0] = RingGemmSegment{a_pl, b_pl, (int)num_kb(K), 0, 0};
     p.nseg = 1;

@@ -131,10 +131,20 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-// commit all prior MMAs of this thread; arrive on `bar` (same offset) in both CTAs
+// The role loops run on whole warps (warp-uniform control flow, so descriptor
+// arithmetic stays in uniform registers); single-thread operations are issued
+// by one lane chosen with elect.sync inside the same asm block.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t e;
+    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(e));
+    return e != 0;
+}
+// commit all prior MMAs of the warp's elected lane; arrive on `bar` (same offset) in both CTAs
 __device__ __forceinline__ void tc_commit_both(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-                 :: "r"(smem_u32(bar)), "h"((uint16_t)0x3) : "memory");
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+        :: "r"(smem_u32(bar)), "h"((uint16_t)0x3) : "memory");
 }
 // SWIZZLE_NONE K-major descriptor: LBO = 128 B (K halves), SBO = 256 B (8-row groups), version 1
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
@@ -143,9 +153,10 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
 }
 __device__ __forceinline__ void mma_u8_2cta(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+        "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}"
         :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate) : "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
@@ -199,15 +210,25 @@ struct WorkMap {
     TileMap tm;
     int tkb, kc, splits;
     __device__ int items() const { return tm.parties * tm.mt * tm.nt * splits; }
+    // 32-bit arithmetic only (the launcher uses splits > 1 only for tkb < 2^24),
+    // and results broadcast from lane 0: the role loops must stay provably
+    // warp-uniform for the MMA descriptors to live in uniform registers.
     __device__ void decode(int w, int& party, int& m, int& n, int& klo, int& khi) const {
         const int t = w / splits, s = w % splits;
         tm.decode(t, party, m, n);
-        klo = (int)((int64_t)tkb * s / splits);
-        khi = (int)((int64_t)tkb * (s + 1) / splits);
+        klo = (int)((unsigned)tkb * (unsigned)s / (unsigned)splits);
+        khi = (int)((unsigned)tkb * (unsigned)(s + 1) / (unsigned)splits);
+        party = __shfl_sync(0xffffffffu, party, 0);
+        m = __shfl_sync(0xffffffffu, m, 0);
+        n = __shfl_sync(0xffffffffu, n, 0);
+        klo = __shfl_sync(0xffffffffu, klo, 0);
+        khi = __shfl_sync(0xffffffffu, khi, 0);
     }
     __device__ int item_kb(int w) const {
         const int s = w % splits;
-        return (int)((int64_t)tkb * (s + 1) / splits) - (int)((int64_t)tkb * s / splits);
+        const int kb = (int)((unsigned)tkb * (unsigned)(s + 1) / (unsigned)splits) -
+                       (int)((unsigned)tkb * (unsigned)s / (unsigned)splits);
+        return __shfl_sync(0xffffffffu, kb, 0);
     }
 };
 
@@ -254,8 +275,11 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
                                               uint32_t rank, uint32_t tmem_base, const Bars& B) {
     const bool leader = rank == 0;
     const int kc = wm.kc;
-    if (warp == 0 && lane == 0) {
+    if (warp == 0) {
         // ------------------------------------------------ producer (both CTAs: own halves)
+        // launched as a programmatic dependent of the limb-split kernel: the
+        // prologue overlapped its tail; the planes are read only after it completed
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         int s = 0; uint32_t ph = 0;
         long long st_empty = 0;
         for (int w = cluster_id(); w < wm.items(); w += nclusters()) {
@@ -276,28 +300,32 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
                         const uint8_t* srcB = S.B + party * S.party_stride_B + (rbB * S.kb + kb) * (8 * GR::kBlock);
                         if (p.dbg) { const long long w0 = clock64(); mbar_wait(&B.empty[s], ph ^ 1); st_empty += clock64() - w0; }
                         else mbar_wait(&B.empty[s], ph ^ 1);
-                        mbar_expect_tx(&B.full[s], bytesA + bytesB);
-                        uint8_t* st = B.stage_base + s * kStageBytes;
-                        bulk_g2s(st, srcA, bytesA, &B.full[s]);
-                        bulk_g2s(st + kAStage, srcB, bytesB, &B.full[s]);
+                        if (elect_one()) {
+                            mbar_expect_tx(&B.full[s], bytesA + bytesB);
+                            uint8_t* st = B.stage_base + s * kStageBytes;
+                            bulk_g2s(st, srcA, bytesA, &B.full[s]);
+                            bulk_g2s(st + kAStage, srcB, bytesB, &B.full[s]);
+                        }
+                        __syncwarp();
                         if (++s == kStages) { s = 0; ph ^= 1; }
                     }
                 }
             }
         }
-        if (p.dbg) atomicAdd(&p.dbg[0], (unsigned long long)st_empty);
-    } else if (warp == 1 && lane == 0 && !leader) {
+        if (p.dbg && lane == 0) atomicAdd(&p.dbg[0], (unsigned long long)st_empty);
+    } else if (warp == 1 && !leader) {
         // ------------------------------------------------ peer: relay "stage full" to the leader
         int s = 0; uint32_t ph = 0;
         const uint32_t leader_full0 = mapa(smem_u32(&B.full[0]), 0);
         for (int w = cluster_id(); w < wm.items(); w += nclusters())
             for (int i = 0; i < kPasses * wm.item_kb(w); ++i) {
                 mbar_wait(&B.full[s], ph);
-                mbar_arrive_cluster(leader_full0 + s * 8);
+                if (elect_one()) mbar_arrive_cluster(leader_full0 + s * 8);
+                __syncwarp();
                 if (++s == kStages) { s = 0; ph ^= 1; }
             }
-    } else if (warp == 1 && lane == 0) {
-        // ------------------------------------------------ leader: MMA issuer (one thread)
+    } else if (warp == 1) {
+        // ------------------------------------------------ leader: MMA issuer (one elected lane)
         int s = 0; uint32_t ph = 0; uint32_t u = 0;
         long long st_tempty = 0, st_full = 0;
         const long long t_start = clock64();
@@ -339,7 +367,7 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
                 }
             }
         }
-        if (p.dbg) {
+        if (p.dbg && lane == 0) {
             atomicAdd(&p.dbg[1], (unsigned long long)st_tempty);
             atomicAdd(&p.dbg[2], (unsigned long long)st_full);
             atomicAdd(&p.dbg[3], (unsigned long long)(clock64() - t_start));
@@ -453,6 +481,7 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     if (p.dbg && threadIdx.x == 0) atomicMin(&p.dbg[4], globaltimer());      // timeline (debug mode)
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");  // the split-K finalize may launch
     Bars B;
     B.stage_base = smem;
     B.full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -488,11 +517,11 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     if (p.dbg && threadIdx.x == 0) atomicMax(&p.dbg[5], globaltimer());
     // register budget: the control warpgroup needs few, the epilogue holds 64 u64 sums per thread
     if (warp < 4) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
         control_roles(p, wm, warp, lane, rank, tmem_base, B);
         if (p.dbg && warp == 1 && lane == 0 && rank == 0) atomicMax(&p.dbg[6], globaltimer());
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
         epilogue_role(p, wm, warp, lane, rank, tmem_base, B);
         if (p.dbg && lane == 0) atomicMax(&p.dbg[7], globaltimer());
     }
@@ -562,8 +591,8 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     if (clusters < 1) clusters = 1;
     static const bool debug = getenv("MPC_GEMM_DEBUG") != nullptr;
     if (!debug) {
-        gemm::ring_gemm_kernel<<<(unsigned)(clusters * 2), gemm::kThreads, smem, stream>>>(q, parties);
-        cudaError_t e = cudaGetLastError();
+        cudaError_t e = launch_pdl(gemm::ring_gemm_kernel, dim3((unsigned)(clusters * 2)), dim3(gemm::kThreads), smem,
+                                   stream, q, parties);
         if (e != cudaSuccess || q.splits <= 1) return e;
         return ring_gemm_finalize(q, parties, stream);
     }
@@ -625,6 +654,7 @@ size_t ring_gemm_partials_bytes(int parties, int64_t M, int64_t N, int total_kb)
 namespace gemm {
 __global__ void finalize_kernel(uint64_t* __restrict__ z, const uint64_t* __restrict__ c,
                                 const uint64_t* __restrict__ part, int splits, int64_t n, int bits) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");     // programmatic dependent of the GEMM
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         uint64_t v = c ? c[i] : 0ull;
         for (int s = 0; s < splits; ++s) v += part[(int64_t)s * n + i];
@@ -645,8 +675,8 @@ cudaError_t ring_gemm_finalize(const RingGemmParams& q, int parties, cudaStream_
     int64_t blocks = (n + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
-    gemm::finalize_kernel<<<(unsigned)blocks, 256, 0, stream>>>(q.Z, q.C, q.partials, q.splits, n, q.trunc_bits);
-    return cudaGetLastError();
+    return launch_pdl(gemm::finalize_kernel, dim3((unsigned)blocks), dim3(256), 0, stream, q.Z, q.C,
+                      (const uint64_t*)q.partials, q.splits, n, q.trunc_bits);
 }
 
 }  // namespace mpc
