@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "../../include/mpc_ring.h"
@@ -29,6 +30,8 @@ struct mpc_ctx_s {
     uint64_t kttp = 0;
     cudaStream_t stream = nullptr;
     ncclComm_t comm = nullptr;
+    cudaStream_t comm_stream = nullptr;     // reveals of the overlapped Beaver schedule
+    cudaEvent_t ev_mask = nullptr, ev_delta = nullptr, ev_eps = nullptr;
     bool broken = false;
     std::string err;
     uint64_t rounds = 0, bytes = 0, launches = 0;
@@ -75,12 +78,14 @@ mpc_status run(mpc_ctx c, int cls, const char* what, F&& f) {
     return MPC_OK;
 }
 
-mpc_status nccl_allreduce(mpc_ctx c, const void* send, void* recv, size_t count, ncclDataType_t dt, const char* what) {
+mpc_status nccl_allreduce(mpc_ctx c, const void* send, void* recv, size_t count, ncclDataType_t dt, const char* what,
+                          cudaStream_t st = nullptr) {
     if (!c->comm) return fail(c, MPC_ERR_STATE, "%s: context has no communicator (created without nccl_id)", what);
+    if (!st) st = c->stream;
     ProfEvent ev{nullptr, nullptr, kClsComm};
-    if (c->prof) { ev.a = take_event(c); ev.b = take_event(c); cudaEventRecord(ev.a, c->stream); }
-    ncclResult_t r = ncclAllReduce(send, recv, count, dt, ncclSum, c->comm, c->stream);
-    if (c->prof) { cudaEventRecord(ev.b, c->stream); c->pending.push_back(ev); }
+    if (c->prof) { ev.a = take_event(c); ev.b = take_event(c); cudaEventRecord(ev.a, st); }
+    ncclResult_t r = count ? ncclAllReduce(send, recv, count, dt, ncclSum, c->comm, st) : ncclSuccess;
+    if (c->prof) { cudaEventRecord(ev.b, st); c->pending.push_back(ev); }
     if (r != ncclSuccess) {
         c->broken = true;
         ncclCommAbort(c->comm);
@@ -105,7 +110,8 @@ mpc_status enter(mpc_ctx c) {
     return MPC_OK;
 }
 
-bool one_party_comm(mpc_ctx c) { return !c->all && c->P > 1; }
+constexpr int kCommSms = 16;     // SMs (NCCL CTAs) reserved for a reveal overlapped with the GEMM
+constexpr int kOverlapClusters = (148 - kCommSms) / 2;   // GEMM clusters while a reveal is in flight
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // limb-plane buffer sizes of left (M x K) and right (N x K) ring-GEMM operands
@@ -140,7 +146,10 @@ BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N) {
     const bool alg1_one = !c->all && c->P > 2;
     w.zbuf = reinterpret_cast<uint64_t*>(alg1_one ? cv.take(8 * (size_t)(M * N)) : nullptr);
     w.hbuf = reinterpret_cast<int8_t*>(alg1_one ? cv.take((size_t)(M * N)) : nullptr);
-    const size_t pb = ring_gemm_partials_bytes(Pl, M, N, 2 * (int)num_kb(K));
+    size_t pb = ring_gemm_partials_bytes(Pl, M, N, 2 * (int)num_kb(K));
+    if (!c->all)   // the overlapped schedule runs two half-K GEMMs, the first on fewer SMs
+        pb = std::max({pb, ring_gemm_partials_bytes(1, M, N, (int)num_kb(K), kOverlapClusters),
+                       ring_gemm_partials_bytes(1, M, N, (int)num_kb(K))});
     w.partials = reinterpret_cast<uint64_t*>(pb ? cv.take(pb) : nullptr);
     w.total = cv.off;
     return w;
@@ -148,6 +157,50 @@ BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N) {
 
 mpc_status beaver_local(mpc_ctx c, const BeaverWs& w, const uint64_t* ed, const uint64_t* a, const uint64_t* b,
                         const uint64_t* cc, uint64_t* z, int64_t M, int64_t K, int64_t N, int truncate);
+mpc_status gemm_run(mpc_ctx c, RingGemmParams& p, int parties);
+
+// One party per GPU with a communicator: the reveal overlaps the GEMM terms
+// that do not need it.  Comm stream: delta is revealed first,
+// then eps.  Compute stream: a_p's limb planes are split while delta is in
+// flight; phase 1, z = c_p + a_p @ delta, runs on the SMs NCCL leaves free
+// while eps is revealed; phase 2 adds eps @ (b_p + [p = 0] delta) and
+// truncates.  Bit-identical to the fused single-GEMM schedule (ring addition).
+mpc_status beaver_overlapped(mpc_ctx c, const BeaverWs& w, const uint64_t* x, const uint64_t* y, const uint64_t* a,
+                             const uint64_t* b, const uint64_t* cc, uint64_t* z, int64_t M, int64_t K, int64_t N,
+                             int truncate) {
+    const int64_t sMK = M * K, sKN = K * N;
+    CHECK(run(c, kClsSplit, "mask", [&] { return launch_mask(x, a, sMK, y, b, sKN, w.ed, c->stream); }));
+    cudaEventRecord(c->ev_mask, c->stream);
+    cudaStreamWaitEvent(c->comm_stream, c->ev_mask, 0);
+    CHECK(nccl_allreduce(c, w.ed + sMK, w.ed + sMK, (size_t)sKN, ncclUint64, "delta reveal", c->comm_stream));
+    cudaEventRecord(c->ev_delta, c->comm_stream);
+    CHECK(nccl_allreduce(c, w.ed, w.ed, (size_t)sMK, ncclUint64, "eps reveal", c->comm_stream));
+    cudaEventRecord(c->ev_eps, c->comm_stream);
+    // a_p planes need no reveal
+    LeftSplitArgs La{M, K, 0, nullptr, nullptr, 0, nullptr, a, 1, w.a_pl, 0};
+    CHECK(run(c, kClsSplit, "split a", [&] { return launch_split_left(La, c->stream); }));
+    cudaStreamWaitEvent(c->stream, c->ev_delta, 0);
+    RightSplitArgs R{K, N, 0, w.ed + sMK, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0};
+    CHECK(run(c, kClsSplit, "split delta", [&] { return launch_split_right(R, c->stream); }));
+    RingGemmParams p1{};
+    p1.seg[0] = RingGemmSegment{w.a_pl, w.delta_pl, (int)num_kb(K), 0, 0};      // a_p @ delta
+    p1.nseg = 1;
+    p1.M = M; p1.N = N; p1.C = cc; p1.Z = z;
+    p1.trunc_bits = 0;
+    p1.partials = w.partials;
+    p1.max_clusters = kOverlapClusters;
+    CHECK(gemm_run(c, p1, 1));
+    cudaStreamWaitEvent(c->stream, c->ev_eps, 0);
+    LeftSplitArgs Le{M, K, 0, w.ed, nullptr, 1, w.eps_pl, nullptr, 0, nullptr, 0};
+    CHECK(run(c, kClsSplit, "split eps", [&] { return launch_split_left(Le, c->stream); }));
+    RingGemmParams p2{};
+    p2.seg[0] = RingGemmSegment{w.eps_pl, w.b_pl, (int)num_kb(K), 0, 0};       // eps @ b'_p
+    p2.nseg = 1;
+    p2.M = M; p2.N = N; p2.C = z; p2.Z = z;                                     // z += ..., in place
+    p2.trunc_bits = (truncate && c->P <= 2) ? c->frac : 0;
+    p2.partials = w.partials;
+    return gemm_run(c, p2, 1);
+}
 
 mpc_status gemm_run(mpc_ctx c, RingGemmParams& p, int parties) {
     p.kc = ring_gemm_default_kc(p.seg[0].kb + (p.nseg > 1 ? p.seg[1].kb : 0));
@@ -210,11 +263,24 @@ mpc_status mpc_create(mpc_ctx* out, int world_size, int rank, int device, const 
     for (int p = 0; p < world_size; ++p) c->kp.k[p] = philox_at(master_seed, stream_word(kTagKeyParty, p, 0), 0);
     c->kttp = philox_at(master_seed, stream_word(kTagKeyTTP, 0, 0), 0);
     if (cudaMalloc(&c->d_err, sizeof(int)) != cudaSuccess) { delete c; return MPC_ERR_CUDA; }
-    if (one_party_comm(c) && nccl_id) {
+    if (!c->all && nccl_id) {
+        // One party per process: own communicator (also for P = 1, where the
+        // reveals are 1-rank allreduces).  NCCL gets a bounded CTA count so its
+        // kernels can run beside the ring GEMM, which leaves SMs for them
+        // (kCommSms) while a reveal is in flight.
         ncclUniqueId id;
         std::memcpy(&id, nccl_id, sizeof(id));
-        if (ncclCommInitRank(&c->comm, world_size, id, rank) != ncclSuccess) {
+        ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+        cfg.blocking = 1;
+        cfg.maxCTAs = kCommSms;
+        if (ncclCommInitRankConfig(&c->comm, world_size, id, rank, &cfg) != ncclSuccess) {
             cudaFree(c->d_err); delete c; return MPC_ERR_NCCL;
+        }
+        if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_mask, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_delta, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_eps, cudaEventDisableTiming) != cudaSuccess) {
+            ncclCommDestroy(c->comm); cudaFree(c->d_err); delete c; return MPC_ERR_CUDA;
         }
     }
     *out = c;
@@ -226,6 +292,8 @@ mpc_status mpc_destroy(mpc_ctx c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream); else cudaDeviceSynchronize();
     if (c->comm) ncclCommDestroy(c->comm);
+    if (c->comm_stream) { cudaStreamSynchronize(c->comm_stream); cudaStreamDestroy(c->comm_stream); }
+    for (cudaEvent_t e : {c->ev_mask, c->ev_delta, c->ev_eps}) if (e) cudaEventDestroy(e);
     for (auto& e : c->pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     for (auto e : c->pool) cudaEventDestroy(e);
     if (c->d_err) cudaFree(c->d_err);
@@ -306,7 +374,7 @@ mpc_status mpc_reveal(mpc_ctx c, const uint64_t* share, uint64_t* out, int64_t n
     if (n == 0) return MPC_OK;
     if (!share || !out) return fail(c, MPC_ERR_ARG, "reveal: null pointer");
     if (c->all) return run(c, kClsSplit, "reveal_sum", [&] { return launch_sum_parties(share, c->P, n, out, c->stream); });
-    if (c->P == 1) {
+    if (c->P == 1 && !c->comm) {
         cudaError_t e = cudaMemcpyAsync(out, share, 8 * (size_t)n, cudaMemcpyDeviceToDevice, c->stream);
         return e == cudaSuccess ? MPC_OK : fail(c, MPC_ERR_CUDA, "reveal copy: %s", cudaGetErrorString(e));
     }
@@ -389,6 +457,10 @@ mpc_status mpc_beaver_matmul(mpc_ctx c, const uint64_t* x, const uint64_t* y, co
         LeftSplitArgs L{M, K, sMK, x, a, c->P, w.eps_pl, a, c->P, w.a_pl, lp(M, K)};
         RightSplitArgs R{K, N, sKN, y, b, c->P, w.delta_pl, b, c->P, 1, w.b_pl, rp(N, K)};
         CHECK(run(c, kClsSplit, "mask+reveal+split", [&] { return launch_split_both(L, R, c->stream); }));
+    } else if (c->comm) {
+        CHECK(beaver_overlapped(c, w, x, y, a, b, cc, z, M, K, N, truncate));
+        if (truncate && c->P > 2) CHECK(truncate_impl(c, z, sMN, c->frac, wrap_id, w.zbuf, w.hbuf));
+        return MPC_OK;
     } else {
         CHECK(run(c, kClsSplit, "mask", [&] { return launch_mask(x, a, sMK, y, b, sKN, w.ed, c->stream); }));
         if (c->P > 1) CHECK(nccl_allreduce(c, w.ed, w.ed, (size_t)(sMK + sKN), ncclUint64, "eps/delta reveal"));

@@ -577,7 +577,8 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t tiles = (int64_t)parties * (pad_rows<Layout::Left>(prm.M) / gemm::kTileM) *
                           (pad_rows<Layout::Right>(prm.N) / gemm::kTileN);
-    const int64_t max_clusters = sms / 2;
+    int64_t max_clusters = sms / 2;
+    if (prm.max_clusters > 0 && prm.max_clusters < max_clusters) max_clusters = prm.max_clusters;
     const int tkb = prm.seg[0].kb + (prm.nseg > 1 ? prm.seg[1].kb : 0);
     RingGemmParams q = prm;
     q.splits = prm.partials ? ring_gemm_choose_splits(tiles, tkb, max_clusters) : 1;
@@ -641,13 +642,15 @@ int ring_gemm_choose_splits(int64_t tiles, int tkb, int64_t clusters) {
     return best;
 }
 
-size_t ring_gemm_partials_bytes(int parties, int64_t M, int64_t N, int total_kb) {
+size_t ring_gemm_partials_bytes(int parties, int64_t M, int64_t N, int total_kb, int max_clusters) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t tiles = (int64_t)parties * (pad_rows<Layout::Left>(M) / gemm::kTileM) *
                           (pad_rows<Layout::Right>(N) / gemm::kTileN);
-    const int s = ring_gemm_choose_splits(tiles, total_kb, sms / 2);
+    int64_t clusters = sms / 2;
+    if (max_clusters > 0 && max_clusters < clusters) clusters = max_clusters;
+    const int s = ring_gemm_choose_splits(tiles, total_kb, clusters);
     return s > 1 ? (size_t)s * parties * M * N * sizeof(uint64_t) : 0;
 }
 

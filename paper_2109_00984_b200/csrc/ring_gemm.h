@@ -29,6 +29,8 @@ struct RingGemmParams {
     uint64_t* partials;                 // split-K slabs [splits][parties][M][N] (workspace,
                                         // ring_gemm_partials_bytes); unused when splits <= 1
     int64_t partial_stride;             // elements per slab (parties * M * N)
+    int max_clusters;                   // 0: all SMs; else at most this many 2-CTA clusters (SMs left
+                                        // to NCCL while a reveal overlaps the GEMM)
 };
 
 // Largest unit length (32-K blocks) for which every s32 accumulator stays exact.
@@ -38,7 +40,7 @@ int ring_gemm_default_kc(int total_kb);
 size_t ring_gemm_smem_bytes();
 int ring_gemm_choose_splits(int64_t tiles, int tkb, int64_t clusters);
 // workspace for the split-K partial sums of a GEMM with these sizes (0 if no split)
-size_t ring_gemm_partials_bytes(int parties, int64_t M, int64_t N, int total_kb);
+size_t ring_gemm_partials_bytes(int parties, int64_t M, int64_t N, int total_kb, int max_clusters = 0);
 int64_t ring_gemm_out_elems(const RingGemmParams& q, int parties);
 cudaError_t ring_gemm_finalize(const RingGemmParams& q, int parties, cudaStream_t stream);
 cudaError_t ring_gemm_launch(const RingGemmParams& p, int parties, cudaStream_t stream);

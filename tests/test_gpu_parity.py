@@ -234,6 +234,24 @@ def test_one_party_contexts_beaver(mpc, P, M, K, N):
         assert np.array_equal(host(z1), oracle.truncate(oracle.beaver_matmul(xs, ys, a, b, cc), 16)[0])
 
 
+@pytest.mark.parametrize("M,K,N", [(64, 64, 64), (300, 100, 260), (197, 768, 300), (1024, 2048, 512)])
+def test_one_party_nccl_overlapped_schedule(mpc, M, K, N):
+    """A one-party context WITH a (1-rank) NCCL communicator runs the production
+    one-party-per-GPU schedule: mask, delta then eps reveals on the comm stream,
+    a_p split + phase-1 GEMM (a_p @ delta) on 132 SMs overlapping the eps reveal,
+    phase-2 GEMM (eps @ b'_p) with the fused truncation; reveal via NCCL."""
+    P = 1
+    uid = mpc.nccl_unique_id()
+    c = mpc.Context(P, 0, device=0, master_seed=MASTER, nccl_id=uid)
+    X, Y, xs, ys, a, b, cc = _beaver_case(P, M, K, N, seed=K, tid=60)
+    z = c.beaver_matmul(dev(xs[0]), dev(ys[0]), dev(a[0]), dev(b[0]), dev(cc[0]), truncate=True)
+    ez = oracle.truncate(oracle.beaver_matmul(xs, ys, a, b, cc), 16)[0]
+    assert np.array_equal(host(z), ez)
+    assert np.array_equal(host(c.reveal(z)), ez)          # 1-rank NCCL allreduce
+    r0, _ = c.stats()
+    assert r0 == 2                                        # one round for the matmul, one for the reveal
+
+
 def test_collective_without_communicator_fails_cleanly(mpc):
     c = ctx(mpc, 2, rank=0)
     with pytest.raises(mpc.MpcError) as e:
