@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--M", type=int, default=4096)
     ap.add_argument("--K", type=int, default=4096)
     ap.add_argument("--N", type=int, default=4096)
+    ap.add_argument("--parties", type=int, default=2, help="P; one GPU: all P parties; N GPUs: N/P sessions")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sample-rows", type=int, default=16)
@@ -215,7 +216,11 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     M, K, N = args.M, args.K, args.N
-    P = 2
+    P = args.parties
+    global METRIC, WORKLOAD
+    if (P, M, K, N) != (2, 4096, 4096, 4096):
+        METRIC = f"ring-TOPS of the {P}-party Beaver private ring-GEMM {M}x{K}x{N} (Z_2^64, scale 2^16, truncated)"
+        WORKLOAD = f"{P}-party Beaver ring GEMM {M}x{K}x{N}, fixed point 2^16, uint64 shares, seeded TTP triples"
     if world > 1:
         from paper_2109_00984_b200 import dist as mdist
         dist.init_process_group("gloo")
@@ -245,19 +250,25 @@ def main():
     holds_x = world == 1 or party == 0
     holds_y = world == 1 or party == 1
     pipeline = {}
-    sync_all()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    x = ctx.share(Xd if holds_x else None, 0, 1, shape=(M, K))
-    y = ctx.share(Yd if holds_y else None, 1, 2, shape=(K, N))
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    pipeline["a2_share_ms"] = e0.elapsed_time(e1)
-    e0.record(stream)
-    a, b, c = ctx.ttp_triples(1, M, K, N)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    pipeline["a3_ttp_triples_ms"] = e0.elapsed_time(e1)
+    for rep in range(2):        # the first pass also pays the caching allocator's cudaMallocs
+        sync_all()
+        e0.record(stream)
+        x = ctx.share(Xd if holds_x else None, 0, 1, shape=(M, K))
+        y = ctx.share(Yd if holds_y else None, 1, 2, shape=(K, N))
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        pipeline["a2_share_ms"] = e0.elapsed_time(e1)
+        if rep == 0:
+            del x, y
+    for rep in range(2):
+        e0.record(stream)
+        a, b, c = ctx.ttp_triples(1, M, K, N)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        pipeline["a3_ttp_triples_ms"] = e0.elapsed_time(e1)
+        if rep == 0:
+            del a, b, c
     z = torch.empty_like(c)
 
     def step():
@@ -286,6 +297,7 @@ def main():
     gemm_ms, gemm_n = ctx.profile_read("gemm")
     split_ms, _ = ctx.profile_read("split")
     comm_ms, _ = ctx.profile_read("comm")
+    trunc_ms, _ = ctx.profile_read("trunc")
     ctx.profile_enable(False)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64)
@@ -363,7 +375,7 @@ def main():
                      "gemm_share_of_step": gemm_ms / args.steps / ms,
                      "algorithmic_ops_per_launch": alg_ops},
         "breakdown_ms_per_step": {"ring_gemm": gemm_ms / args.steps, "mask_reveal_split": split_ms / args.steps,
-                                  "nccl": comm_ms / args.steps},
+                                  "nccl": comm_ms / args.steps, "truncation_alg1": trunc_ms / args.steps},
         "pipeline": pipeline,
         "gpu_launches": int(launches),
         "clocks": sampler.summary(),

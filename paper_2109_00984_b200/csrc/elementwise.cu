@@ -459,36 +459,70 @@ cudaError_t launch_trunc_local(uint64_t* x, int64_t n, int bits, cudaStream_t st
 // ------------------------------------------------------------------ a9 truncation, P > 2, all parties
 // Alg. 1 + correction, eta skipped, for
 // every party of element i in one thread (local reveal of z).
-__global__ void trunc_alg1_all_kernel(uint64_t* __restrict__ x, int P, int64_t n, int bits, uint64_t key, uint64_t id) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t zsum = 0;
-        __int128 zs_signed = 0;
-        for (int q = 0; q < P; ++q) {
-            const uint64_t r = philox_at(key, stream_word(kTagR, (uint32_t)q, id), (uint64_t)i);
-            const uint64_t z = x[(int64_t)q * n + i] + r;
-            zsum += z;
-            zs_signed += (__int128)(int64_t)z;
+// One thread per element pair (one Philox block yields both elements' r_q and
+// [theta_r]_q); the parties' r_q stay in registers (P <= 16, unrolled).
+__global__ void __launch_bounds__(128) trunc_alg1_all_kernel(uint64_t* __restrict__ x, int P, int64_t n, int bits,
+                                                            uint64_t key, uint64_t id) {
+    const int64_t npairs = (n + 1) / 2;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npairs; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i0 = 2 * j;
+        const bool has1 = i0 + 1 < n;
+        uint64_t r[kMaxParties][2];
+        uint64_t zsum[2] = {0, 0}, rsum[2] = {0, 0};
+        __int128 zs[2] = {0, 0}, rs[2] = {0, 0};
+#pragma unroll
+        for (int q = 0; q < kMaxParties; ++q) {
+            if (q < P) {
+                philox_pair(key, stream_word(kTagR, (uint32_t)q, id), (uint64_t)j, r[q][0], r[q][1]);
+                const uint64_t* xq = x + (int64_t)q * n + i0;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const uint64_t xv = (e == 0 || has1) ? xq[e] : 0ull;
+                    const uint64_t z = xv + r[q][e];
+                    zsum[e] += z;
+                    zs[e] += (__int128)(int64_t)z;
+                    rsum[e] += r[q][e];
+                    rs[e] += (__int128)(int64_t)r[q][e];
+                }
+            }
         }
-        const int64_t theta_z = (int64_t)((zs_signed - (__int128)(int64_t)zsum) >> 64);
-        const int64_t theta_r = theta_r_at(key, id, P, i);
-        uint64_t th_sum = 0;  // sum of [theta_r]_q for q >= 1
-        for (int q = P - 1; q >= 0; --q) {
-            const uint64_t xq = x[(int64_t)q * n + i];
-            const uint64_t r = philox_at(key, stream_word(kTagR, (uint32_t)q, id), (uint64_t)i);
-            const uint64_t z = xq + r;
-            const __int128 bs = (__int128)(int64_t)xq + (__int128)(int64_t)r - (__int128)(int64_t)z;
-            const uint64_t beta = (uint64_t)(int64_t)(bs >> 64);
-            uint64_t thq;
-            if (q > 0) { thq = philox_at(key, stream_word(kTagTheta, (uint32_t)q, id), (uint64_t)i); th_sum += thq; }
-            else thq = (uint64_t)theta_r - th_sum;
-            const uint64_t theta_x = beta - thq + (q == 0 ? (uint64_t)theta_z : 0ull);
-            x[(int64_t)q * n + i] = div_pow2_round(xq, bits) - theta_x * (1ull << (64 - bits));
+        uint64_t theta_z[2], theta_r[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            theta_z[e] = (uint64_t)(int64_t)((zs[e] - (__int128)(int64_t)zsum[e]) >> 64);   // wraps of z's shares
+            theta_r[e] = (uint64_t)(int64_t)((rs[e] - (__int128)(int64_t)rsum[e]) >> 64);   // wraps of r's shares
+        }
+        uint64_t th_sum[2] = {0, 0};                                                        // sum_{q>=1} [theta_r]_q
+#pragma unroll
+        for (int q = kMaxParties - 1; q >= 0; --q) {
+            if (q < P) {
+                uint64_t th[2];
+                if (q > 0) {
+                    philox_pair(key, stream_word(kTagTheta, (uint32_t)q, id), (uint64_t)j, th[0], th[1]);
+                    th_sum[0] += th[0];
+                    th_sum[1] += th[1];
+                } else {
+                    th[0] = theta_r[0] - th_sum[0];
+                    th[1] = theta_r[1] - th_sum[1];
+                }
+                uint64_t* xq = x + (int64_t)q * n + i0;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    if (e == 1 && !has1) break;
+                    const uint64_t xv = xq[e];
+                    const uint64_t z = xv + r[q][e];
+                    const __int128 bs = (__int128)(int64_t)xv + (__int128)(int64_t)r[q][e] - (__int128)(int64_t)z;
+                    const uint64_t beta = (uint64_t)(int64_t)(bs >> 64);
+                    const uint64_t theta_x = beta - th[e] + (q == 0 ? theta_z[e] : 0ull);
+                    xq[e] = div_pow2_round(xv, bits) - theta_x * (1ull << (64 - bits));
+                }
+            }
         }
     }
 }
 cudaError_t launch_trunc_alg1_all(uint64_t* x, int P, int64_t n, int bits, uint64_t key, uint64_t id, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    trunc_alg1_all_kernel<<<grid_for(n), 256, 0, st>>>(x, P, n, bits, key, id);
+    trunc_alg1_all_kernel<<<grid_for((n + 1) / 2, 128), 128, 0, st>>>(x, P, n, bits, key, id);
     return cudaGetLastError();
 }
 
