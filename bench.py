@@ -121,6 +121,18 @@ def load_peaks():
             "source": "fallback of B200_PROFILING.md (1.4 PF/s sustained bf16 x 2)"}
 
 
+def load_cublas_int8():
+    """cuBLASLt int8 GEMM (torch._int_mm 8192^3) burst / sustained TOPS measured on this pool
+    by scripts/probe_peaks.py (context for the derived int8 peak)."""
+    p = os.path.join(ROOT, "profiles", "r01", "peaks_cublas.json")
+    try:
+        d = json.load(open(p))["int8 torch._int_mm (cuBLASLt)"]
+        return {"burst_tops": d["burst_tops"], "sustained_tops": d["sustained_tops"],
+                "sustained_sm_mhz": d["sm_mhz_median_sustained"]}
+    except Exception:
+        return None
+
+
 def load_traffic():
     p = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(p):
@@ -372,6 +384,7 @@ def main():
                      "frac_of_tensor_probe_peak": achieved / 4500.0,
                      "tensor_probe_peak_note": "scripts/mma_probe: 8190 MAC/clk/SM = 4.5 POPS int8 at 1965 MHz "
                                                "(profiles/r01/README.md); the GEMM runs power-capped near 1.56 GHz",
+                     "int8_cublas_measured": load_cublas_int8(),
                      "gemm_share_of_step": gemm_ms / args.steps / ms,
                      "algorithmic_ops_per_launch": alg_ops},
         "breakdown_ms_per_step": {"ring_gemm": gemm_ms / args.steps, "mask_reveal_split": split_ms / args.steps,

@@ -93,14 +93,14 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* c
 }
 
 template <int CG, int M, int N>
-void run(const char* name, const uint8_t* gsrc = nullptr, int copy_bytes = 0) {
+void run(const char* name, const uint8_t* gsrc = nullptr, int copy_bytes = 0, int iters_ = 2000) {
     auto k = probe<CG, M, N>;
     const int smem = 160 * 1024;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (CG == 2) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
     unsigned long long* dc;
     cudaMalloc(&dc, 8);
-    const int iters = 2000;
+    const int iters = iters_;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(148);
     cfg.blockDim = dim3(128);
@@ -123,14 +123,19 @@ void run(const char* name, const uint8_t* gsrc = nullptr, int copy_bytes = 0) {
         const double cyc_per_mma = (double)cyc / issuers / (iters * 8.0);
         const double macs = (double)M * N * 32;
         const double tops = 2.0 * macs * iters * 8 * issuers / (ms * 1e-3) / 1e12;
-        if (rep == 1)
+        if (rep == 1 && name[0])
             printf("%-28s err=%d  cycles/MMA=%7.2f  MAC/clk/SM=%7.0f  chip=%7.0f TOPS (%.3f ms)\n", name, (int)err,
                    cyc_per_mma, macs / cyc_per_mma / CG, tops, ms);
     }
     cudaFree(dc);
 }
 
-int main() {
+int main(int argc, char** argv) {
+    if (argc > 1) {   // sustained mode: the GEMM's MMA shape back-to-back for ~4 s
+        const int reps = 40;
+        for (int r = 0; r < reps; ++r) run<2, 256, 128>(r + 1 == reps ? "cg2 M256 N128 sustained" : "", nullptr, 0, 60000);
+        return 0;
+    }
     uint8_t* g; cudaMalloc(&g, 32u << 20); cudaMemset(g, 1, 32u << 20);
     run<2, 256, 128>("cg2 M256 N128 +copy 32K", g, 32768);
     run<2, 256, 128>("cg2 M256 N128 +copy 48K", g, 49152);
