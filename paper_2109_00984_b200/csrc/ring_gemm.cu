@@ -185,6 +185,15 @@ __device__ __forceinline__ void st_stream(uint64_t* p, ulonglong2 v, uint64_t po
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;"
                  :: "l"(p), "l"(v.x), "l"(v.y), "l"(pol) : "memory");
 }
+// 32-byte (one full sector) variants; p must be 32-byte aligned
+__device__ __forceinline__ void ld_stream4(const uint64_t* p, uint64_t pol, uint64_t* v) {
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u64 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void st_stream4(uint64_t* p, const uint64_t* v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u64 [%0], {%1, %2, %3, %4}, %5;"
+                 :: "l"(p), "l"(v[0]), "l"(v[1]), "l"(v[2]), "l"(v[3]), "l"(pol) : "memory");
+}
 
 // Tile t -> (party, m tile, n tile) in the grouped order: groups of kGroupM row
 // tiles; inside a group, n tiles outer, then row tiles, then parties.
@@ -403,7 +412,10 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Wor
     const int half = (warp - 4) >> 2;              // column half: 64 columns each
     const int row = wq * 32 + lane;
     const uint32_t tempty_leader = mapa(smem_u32(B.tempty), 0);   // [0] slots 0-1, [1] slots 2-3
-    const bool vec = (p.N & 1) == 0;
+    // full-sector (32-byte) accesses when every row start is 32-byte aligned
+    const bool vec = (p.N & 3) == 0 && (p.party_stride_z & 3) == 0 && (p.party_stride_c & 3) == 0 &&
+                     (p.partial_stride & 3) == 0 && (reinterpret_cast<uintptr_t>(p.Z) & 31) == 0 &&
+                     (reinterpret_cast<uintptr_t>(p.C) & 31) == 0 && (reinterpret_cast<uintptr_t>(p.partials) & 31) == 0;
     const uint64_t pol = evict_first_policy();
     const uint32_t tbase = tmem_base + ((uint32_t)(wq * 32) << 16) + half * 64;
     uint32_t u = 0;
@@ -444,32 +456,46 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Wor
             const int64_t gc0 = (int64_t)n * kTileN + half * 64;
             if (vec && gc0 + 64 <= p.N) {
 #pragma unroll
-                for (int j = 0; j < 64; j += 2) st_stream(prow + gc0 + j, make_ulonglong2(run[j], run[j + 1]), pol);
+                for (int j = 0; j < 64; j += 4) st_stream4(prow + gc0 + j, &run[j], pol);
             } else {
 #pragma unroll
                 for (int j = 0; j < 64; ++j)
                     if (gc0 + j < p.N) prow[gc0 + j] = run[j];
             }
         } else if (grow < p.M) {
+            // z = trunc(c + run).  z may alias c (in-place second phase): each
+            // element is read before it is written by the same thread.  Batches of
+            // 16 columns: all loads of a batch are issued before its stores, so a
+            // row costs 4 memory round trips, not 32.
             uint64_t* zrow = p.Z + party * p.party_stride_z + grow * p.N;
             const uint64_t* crow = p.C ? p.C + party * p.party_stride_c + grow * p.N : nullptr;
             const int64_t gc0 = (int64_t)n * kTileN + half * 64;
-            if (vec && gc0 + 64 <= p.N) {
+            const bool full = vec && gc0 + 64 <= p.N;
 #pragma unroll
-                for (int j = 0; j < 64; j += 2) {
-                    ulonglong2 v = crow ? ld_stream(crow + gc0 + j, pol) : make_ulonglong2(0, 0);
-                    v.x += run[j]; v.y += run[j + 1];
-                    if (p.trunc_bits) { v.x = div_pow2_round(v.x, p.trunc_bits); v.y = div_pow2_round(v.y, p.trunc_bits); }
-                    st_stream(zrow + gc0 + j, v, pol);
-                }
-            } else {
+            for (int jb = 0; jb < 64; jb += 16) {
+                uint64_t v[16];
+                if (full) {
 #pragma unroll
-                for (int j = 0; j < 64; ++j) {
-                    if (gc0 + j < p.N) {
-                        uint64_t v = (crow ? crow[gc0 + j] : 0ull) + run[j];
-                        if (p.trunc_bits) v = div_pow2_round(v, p.trunc_bits);
-                        zrow[gc0 + j] = v;
+                    for (int q = 0; q < 16; q += 4) {
+                        if (crow) ld_stream4(crow + gc0 + jb + q, pol, &v[q]);
+                        else v[q] = v[q + 1] = v[q + 2] = v[q + 3] = 0ull;
                     }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = (crow && gc0 + jb + j < p.N) ? crow[gc0 + jb + j] : 0ull;
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    v[j] += run[jb + j];
+                    if (p.trunc_bits) v[j] = div_pow2_round(v[j], p.trunc_bits);
+                }
+                if (full) {
+#pragma unroll
+                    for (int q = 0; q < 16; q += 4) st_stream4(zrow + gc0 + jb + q, &v[q], pol);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (gc0 + jb + j < p.N) zrow[gc0 + jb + j] = v[j];
                 }
             }
         }

@@ -50,6 +50,14 @@ def _u64(shape, device) -> torch.Tensor:
     return torch.empty(shape, dtype=torch.uint64, device=device)
 
 
+def _check_out(t: torch.Tensor, shape, dtype) -> torch.Tensor:
+    """Caller-provided output buffer: must match exactly (the library writes through the raw pointer)."""
+    if tuple(t.shape) != tuple(shape) or t.dtype != dtype or not t.is_contiguous() or t.device.type != "cuda":
+        raise ValueError(f"out tensor {tuple(t.shape)} {t.dtype} does not match {tuple(shape)} {dtype} "
+                         "(contiguous, on the context's device)")
+    return t
+
+
 def nccl_unique_id() -> bytes:
     """128-byte ncclUniqueId from the native library's NCCL (rank 0 calls this)."""
     return _native.nccl_unique_id()
@@ -105,38 +113,48 @@ class Context:
         return (self.P,) if self.all_parties else ()
 
     # ------------------------------------------------------------ fixed point
-    def encode(self, x: torch.Tensor) -> torch.Tensor:
+    def encode(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         x = x.to(device=self.device, dtype=torch.float64).contiguous()
-        out = _u64(x.shape, self.device)
+        out = _u64(x.shape, self.device) if out is None else _check_out(out, x.shape, torch.uint64)
         self._call(self._lib.mpc_encode, _ptr(x), _ptr(out), ctypes.c_int64(x.numel()))
         return out
 
-    def decode(self, v: torch.Tensor) -> torch.Tensor:
-        out = torch.empty(v.shape, dtype=torch.float64, device=self.device)
+    def decode(self, v: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty(v.shape, dtype=torch.float64, device=self.device)
+        else:
+            _check_out(out, v.shape, torch.float64)
         self._call(self._lib.mpc_decode, _ptr(v), _ptr(out), ctypes.c_int64(v.numel()))
         return out
 
     # ------------------------------------------------------------ share / reveal
-    def share(self, x: Optional[torch.Tensor], src: int, share_id: int, shape=None) -> torch.Tensor:
+    def share(self, x: Optional[torch.Tensor], src: int, share_id: int, shape=None,
+              out: Optional[torch.Tensor] = None) -> torch.Tensor:
         shape = tuple(x.shape) if x is not None else tuple(shape)
         n = 1
         for s in shape:
             n *= s
-        out = _u64(self._lead() + shape, self.device)
+        out = _u64(self._lead() + shape, self.device) if out is None else \
+            _check_out(out, self._lead() + shape, torch.uint64)
         self._call(self._lib.mpc_share, _ptr(x), src, ctypes.c_uint64(share_id), _ptr(out), ctypes.c_int64(n))
         return out
 
-    def reveal(self, shares: torch.Tensor) -> torch.Tensor:
+    def reveal(self, shares: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         shape = tuple(shares.shape[1:]) if self.all_parties else tuple(shares.shape)
-        out = _u64(shape, self.device)
+        out = _u64(shape, self.device) if out is None else _check_out(out, shape, torch.uint64)
         self._call(self._lib.mpc_reveal, _ptr(shares), _ptr(out), ctypes.c_int64(out.numel()))
         return out
 
     # ------------------------------------------------------------ offline TTP
-    def ttp_triples(self, triple_id: int, M: int, K: int, N: int):
-        a = _u64(self._lead() + (M, K), self.device)
-        b = _u64(self._lead() + (K, N), self.device)
-        c = _u64(self._lead() + (M, N), self.device)
+    def ttp_triples(self, triple_id: int, M: int, K: int, N: int, out=None):
+        if out is None:
+            a = _u64(self._lead() + (M, K), self.device)
+            b = _u64(self._lead() + (K, N), self.device)
+            c = _u64(self._lead() + (M, N), self.device)
+        else:
+            a, b, c = out
+            for t, shp in ((a, (M, K)), (b, (K, N)), (c, (M, N))):
+                _check_out(t, self._lead() + shp, torch.uint64)
         nb = self._lib.mpc_ttp_workspace_bytes(self._h, M, K, N)
         ws = self._workspace(nb)
         self._call(self._lib.mpc_ttp_triples, ctypes.c_uint64(triple_id), ctypes.c_int64(M), ctypes.c_int64(K),

@@ -1,9 +1,12 @@
 """Per-layer 2-party Beaver matmul timings for the paper's model workloads
-(configs[2]/[3]: ResNet-50 batch 1 im2col GEMMs, ViT-B/16 linear layers),
-both parties on one GPU, truncation fused.  Reports µs per private matmul,
-ring-TOPS and the share of the layer time spent in the tcgen05 GEMM.
+(configs[2]/[3]: ResNet-50 batch 1 im2col GEMMs, ViT-B/16 linear layers; also
+ResNet-18, the model the paper times, and Wav2Letter), both parties on one GPU,
+truncation fused.  Reports µs per private matmul, ring-TOPS and the share of
+the layer time spent in the tcgen05 GEMM.  --chain captures every layer of a
+model (each repeated `count` times, in order) in ONE CUDA graph and times the
+whole chain, as a private inference would run them back to back.
 
-  python scripts/bench_layers.py [--model resnet50|vit|all] [--reps 20] [--graph]
+  python scripts/bench_layers.py [--model resnet50|vit|resnet18|wav2letter|all] [--reps 20] [--graph] [--chain]
 """
 import argparse
 import json
@@ -59,18 +62,65 @@ def run_layer(ctx, M, K, N, reps, graph):
     return ms, (gemm_ms / reps if not graph else None)
 
 
+def run_chain(ctx, layers, reps):
+    """All layers of one model in one CUDA graph; returns ms per pass."""
+    dev = torch.device("cuda", 0)
+    bufs = []
+    for i, (_, M, K, N, count) in enumerate(layers):
+        X = synth.uniform_fixed((M, K), 100 + i)
+        Y = synth.uniform_fixed((K, N), 200 + i)
+        x = ctx.share(torch.from_numpy(X.view(np.int64)).to(dev).view(torch.uint64), 0, 1 + 2 * i)
+        y = ctx.share(torch.from_numpy(Y.view(np.int64)).to(dev).view(torch.uint64), 1, 2 + 2 * i)
+        a, b, c = ctx.ttp_triples(1 + i, M, K, N)
+        bufs.append((x, y, a, b, c, torch.empty_like(c), count))
+
+    def chain():
+        for x, y, a, b, c, z, count in bufs:
+            for _ in range(count):
+                ctx.beaver_matmul(x, y, a, b, c, truncate=True, out=z)
+
+    chain()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        chain()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            chain()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--model", default="all", choices=["resnet50", "vit", "all"])
+    ap.add_argument("--model", default="all", choices=list(synth.MODELS) + ["all"])
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--graph", action="store_true")
+    ap.add_argument("--chain", action="store_true")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     ctx = mpc.Context(2, mpc.ALL_PARTIES, device=0, master_seed=synth.MASTER_SEED)
-    models = {"resnet50": synth.RESNET50_B1, "vit": synth.VIT_B16}
     out = {}
-    for name, layers in models.items():
+    for name, layers in synth.MODELS.items():
         if args.model not in (name, "all"):
+            continue
+        if args.chain:
+            ms = run_chain(ctx, layers, args.reps)
+            ops = sum(2.0 * M * K * N * cnt for _, M, K, N, cnt in layers)
+            n = sum(cnt for *_, cnt in layers)
+            out[name] = {"chain_ms": ms, "private_matmuls": n, "ring_TOPS": ops / (ms * 1e-3) / 1e12,
+                         "graph": "one CUDA graph per model"}
+            print(f"{name}: chain of {n} private matmuls {ms:.3f} ms ({out[name]['ring_TOPS']:.2f} ring-TOPS)",
+                  flush=True)
             continue
         rows, total_ms, total_ops = [], 0.0, 0.0
         for lname, M, K, N, count in layers:

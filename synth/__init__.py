@@ -63,6 +63,26 @@ VIT_B16 = [
     ("head", 1, 768, 1000, 1),
 ]
 
+# ResNet-18 b1 im2col GEMMs (the model the paper benchmarks; SURVEY §8(d)
+# C3 extra row): 21 GEMMs, sum MNK = 1.81 G.
+RESNET18_B1 = [
+    ("conv1", 12544, 147, 64, 1),
+    ("l1.c", 3136, 576, 64, 4),
+    ("l2.c1", 784, 576, 128, 1), ("l2.c", 784, 1152, 128, 3), ("l2.ds", 784, 64, 128, 1),
+    ("l3.c1", 196, 1152, 256, 1), ("l3.c", 196, 2304, 256, 3), ("l3.ds", 196, 128, 256, 1),
+    ("l4.c1", 49, 2304, 512, 1), ("l4.c", 49, 4608, 512, 3), ("l4.ds", 49, 256, 512, 1),
+    ("fc", 1, 512, 1000, 1),
+]
+
+# Wav2Letter, 1 s of 16 kHz audio, batch 1 (SURVEY §8(d) optional row W,
+# torchaudio padding assumed): sum MNK = 1.33 G.
+WAV2LETTER_B1 = [
+    ("conv1", 100, 250, 250, 1), ("conv2", 50, 12000, 250, 1), ("conv3-9", 50, 1750, 250, 7),
+    ("conv10", 51, 8000, 2000, 1), ("conv11", 51, 2000, 2000, 1), ("conv12", 51, 2000, 29, 1),
+]
+
+MODELS = {"resnet50": RESNET50_B1, "vit": VIT_B16, "resnet18": RESNET18_B1, "wav2letter": WAV2LETTER_B1}
+
 CONFIGS = {
     "C1": dict(M=64, K=64, N=64, P=2, seed=1001),
     "C2": dict(M=4096, K=4096, N=4096, P=2, seed=1002),

@@ -51,6 +51,11 @@ def _layer_case(P, M, K, N, kind, seed):
     ("resnet.l4.c2", 49, 4608, 512, "resnet"),
     ("resnet.l3.c2", 196, 2304, 256, "resnet"),
     ("resnet.fc", 1, 2048, 1000, "resnet"),
+    ("resnet18.l2.c1", 784, 576, 128, "resnet"),
+    ("resnet18.fc", 1, 512, 1000, "resnet"),
+    ("wav2letter.conv2", 50, 12000, 250, "vit"),
+    ("wav2letter.conv10", 51, 8000, 2000, "vit"),
+    ("wav2letter.conv12", 51, 2000, 29, "vit"),
 ])
 def test_layer_gemm_parity(mpc, name, M, K, N, kind):
     P = 2

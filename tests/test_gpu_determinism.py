@@ -1,0 +1,71 @@
+"""Determinism across launch configurations (SURVEY.md §8(c) pin table,
+"Determinism": same seeds => identical shares across chunk counts and tile
+configs; ring addition is associative, so any order is exact).
+
+Each configuration runs in its own process because the GEMM's tuning knobs
+(K-chunk length MPC_GEMM_KC, split-K factor MPC_GEMM_SPLITS, programmatic
+dependent launch MPC_NO_PDL) are read once per process.  Every run must
+produce the oracle's shares bit for bit.
+"""
+import hashlib
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+M, K, N, P = 300, 3000, 700, 2        # 94 K-blocks, 2 x 6 output tiles: several units and a ragged tail
+
+SCRIPT = r"""
+import hashlib, sys
+import numpy as np, torch
+sys.path.insert(0, {root!r})
+import synth
+import paper_2109_00984_b200 as m
+M, K, N, P = {M}, {K}, {N}, {P}
+c = m.Context(P, m.ALL_PARTIES, device=0, master_seed=synth.MASTER_SEED)
+dev = lambda a: torch.from_numpy(a.view(np.int64)).cuda().view(torch.uint64)
+x = c.share(dev(synth.uniform_fixed((M, K), 31)), 0, 1)
+y = c.share(dev(synth.uniform_fixed((K, N), 32)), 1, 2)
+a, b, cc = c.ttp_triples(4, M, K, N)
+z = c.beaver_matmul(x, y, a, b, cc, truncate=True)
+print(hashlib.sha256(z.view(torch.int64).cpu().numpy().tobytes()).hexdigest())
+"""
+
+
+@pytest.fixture(scope="module")
+def expected():
+    from paper_2109_00984_b200 import build
+    build.build()
+    X = synth.uniform_fixed((M, K), 31)
+    Y = synth.uniform_fixed((K, N), 32)
+    a, b, c = oracle.ttp_triple(P, synth.MASTER_SEED, 4, M, K, N)
+    z = oracle.beaver_matmul(oracle.share(P, synth.MASTER_SEED, X, 0, 1), oracle.share(P, synth.MASTER_SEED, Y, 1, 2),
+                             a, b, c)
+    z = oracle.truncate(z, 16)
+    return hashlib.sha256(np.ascontiguousarray(z).view(np.int64).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("env", [
+    {},
+    {"MPC_GEMM_KC": "8"},
+    {"MPC_GEMM_KC": "33"},
+    {"MPC_GEMM_SPLITS": "3"},
+    {"MPC_GEMM_SPLITS": "7", "MPC_GEMM_KC": "5"},
+    {"MPC_NO_PDL": "1"},
+], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
+def test_same_shares_under_every_launch_config(expected, env):
+    full = dict(os.environ)
+    for k in ("MPC_GEMM_KC", "MPC_GEMM_SPLITS", "MPC_NO_PDL", "MPC_GEMM_DEBUG"):
+        full.pop(k, None)
+    full.update(env)
+    out = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, M=M, K=K, N=N, P=P)], env=full,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.strip().splitlines()[-1] == expected, env
