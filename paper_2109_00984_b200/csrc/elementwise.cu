@@ -126,7 +126,10 @@ __device__ __forceinline__ void load16(const uint64_t* __restrict__ src, bool fu
     }
 }
 
-// (bid, nblk): this block's index among the nblk blocks working on the left split
+// (bid, nblk): this block's index among the nblk blocks working on the left split.
+// LO: plane layout of the output (Layout::Left normally; Layout::Right when the
+// ring GEMM runs transposed, see RingGemmParams::transpose_out).
+template <Layout LO>
 __device__ __forceinline__ void split_left_body(const LeftSplitArgs& a, int64_t bid, int64_t nblk) {
     const int64_t KB = num_kb(a.K);
     const int64_t row_groups = (a.M + 7) / 8;
@@ -154,26 +157,28 @@ __device__ __forceinline__ void split_left_body(const LeftSplitArgs& a, int64_t 
                     load16(a.minus + p * a.party_stride + row * a.K + k0, full, vec, kleft, v);
 #pragma unroll
                     for (int m = 0; m < 16; ++m) acc[m] -= v[m];
-                    if (fused_copy) store_limbs16<Layout::Left>(a.cp_planes + p * a.cp_planes_stride, row, k0, KB, v);
+                    if (fused_copy) store_limbs16<LO>(a.cp_planes + p * a.cp_planes_stride, row, k0, KB, v);
                 }
             }
-            store_limbs16<Layout::Left>(a.sum_planes, row, k0, KB, acc);
+            store_limbs16<LO>(a.sum_planes, row, k0, KB, acc);
         }
         if (!fused_copy) {
             for (int q = 0; q < a.Pcopy; ++q) {
                 load16(a.cp_src + q * a.party_stride + row * a.K + k0, full, vec, kleft, v);
-                store_limbs16<Layout::Left>(a.cp_planes + q * a.cp_planes_stride, row, k0, KB, v);
+                store_limbs16<LO>(a.cp_planes + q * a.cp_planes_stride, row, k0, KB, v);
             }
         }
     }
 }
+template <Layout LO>
 __global__ void __launch_bounds__(256) split_left_kernel(LeftSplitArgs a) {
-    split_left_body(a, blockIdx.x, gridDim.x);
+    split_left_body<LO>(a, blockIdx.x, gridDim.x);
 }
 cudaError_t launch_split_left(const LeftSplitArgs& a, cudaStream_t st) {
     if (a.M == 0 || a.K == 0) return cudaSuccess;
     const int64_t warps = ((a.M + 7) / 8) * ((num_kb(a.K) * kKBlock + 63) / 64);
-    split_left_kernel<<<grid_for(warps * 32), 256, 0, st>>>(a);
+    if (a.swap) split_left_kernel<Layout::Right><<<grid_for(warps * 32), 256, 0, st>>>(a);
+    else split_left_kernel<Layout::Left><<<grid_for(warps * 32), 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -210,6 +215,7 @@ __device__ __forceinline__ void load_cols(const uint64_t* __restrict__ base, int
     }
 }
 
+template <Layout LO>
 __device__ __forceinline__ void split_right_body(const RightSplitArgs& a, int64_t bid, int64_t nblk) {
     const int64_t KB = num_kb(a.K);
     const int64_t ngroups = (a.N + 31) / 32;
@@ -238,14 +244,14 @@ __device__ __forceinline__ void split_right_body(const RightSplitArgs& a, int64_
                 for (int m = 0; m < 8; ++m) { d[0][m] -= v[0][m]; d[1][m] -= v[1][m]; }
                 if (fused_copy && !(p == 0 && a.add_delta_first)) {
                     uint8_t* pl = a.cp_planes + p * a.cp_planes_stride;
-                    store_limbs8<Layout::Right>(pl, n, k0, KB, v[0]);
-                    if (two) store_limbs8<Layout::Right>(pl, n + 1, k0, KB, v[1]);
+                    store_limbs8<LO>(pl, n, k0, KB, v[0]);
+                    if (two) store_limbs8<LO>(pl, n + 1, k0, KB, v[1]);
                 }
             }
         }
         if (a.sum_planes) {
-            store_limbs8<Layout::Right>(a.sum_planes, n, k0, KB, d[0]);
-            if (two) store_limbs8<Layout::Right>(a.sum_planes, n + 1, k0, KB, d[1]);
+            store_limbs8<LO>(a.sum_planes, n, k0, KB, d[0]);
+            if (two) store_limbs8<LO>(a.sum_planes, n + 1, k0, KB, d[1]);
         }
         for (int q = 0; q < a.Pcopy; ++q) {
             const bool addd = (q == 0) && a.add_delta_first;
@@ -256,26 +262,32 @@ __device__ __forceinline__ void split_right_body(const RightSplitArgs& a, int64_
                 for (int m = 0; m < 8; ++m) { v[0][m] += d[0][m]; v[1][m] += d[1][m]; }
             }
             uint8_t* pl = a.cp_planes + q * a.cp_planes_stride;
-            store_limbs8<Layout::Right>(pl, n, k0, KB, v[0]);
-            if (two) store_limbs8<Layout::Right>(pl, n + 1, k0, KB, v[1]);
+            store_limbs8<LO>(pl, n, k0, KB, v[0]);
+            if (two) store_limbs8<LO>(pl, n + 1, k0, KB, v[1]);
         }
     }
 }
+template <Layout LO>
 __global__ void __launch_bounds__(256, 2) split_right_kernel(RightSplitArgs a) {
-    split_right_body(a, blockIdx.x, gridDim.x);
+    split_right_body<LO>(a, blockIdx.x, gridDim.x);
 }
 cudaError_t launch_split_right(const RightSplitArgs& a, cudaStream_t st) {
     if (a.N == 0 || a.K == 0) return cudaSuccess;
     const int64_t warps = ((a.N + 31) / 32) * (num_kb(a.K) * 2);
-    split_right_kernel<<<grid_for(warps * 32), 256, 0, st>>>(a);
+    if (a.swap) split_right_kernel<Layout::Left><<<grid_for(warps * 32), 256, 0, st>>>(a);
+    else split_right_kernel<Layout::Right><<<grid_for(warps * 32), 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 
 // Both splits of one Beaver matmul in a single launch (they are independent):
 // blocks [0, nleft) run the left split, the rest the right split.
+template <Layout LL, Layout LR>
 __global__ void __launch_bounds__(256, 2) split_both_kernel(LeftSplitArgs l, RightSplitArgs r, int nleft) {
-    if ((int)blockIdx.x < nleft) split_left_body(l, blockIdx.x, nleft);
-    else split_right_body(r, blockIdx.x - nleft, gridDim.x - nleft);
+    // launched as a programmatic dependent of the previous kernel (e.g. the last
+    // layer's GEMM / finalize): nothing is read or written before it completes
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if ((int)blockIdx.x < nleft) split_left_body<LL>(l, blockIdx.x, nleft);
+    else split_right_body<LR>(r, blockIdx.x - nleft, gridDim.x - nleft);
     // each block is done: once all are, the ring GEMM (a programmatic dependent)
     // may launch and run its prologue while the last blocks drain — triggering
     // earlier would let GEMM CTAs take SMs from the split's tail
@@ -293,8 +305,12 @@ cudaError_t launch_split_both(const LeftSplitArgs& l, const RightSplitArgs& r, c
     const int64_t bytes_r = r.N * r.K * (int64_t)(2 * r.Psum + r.Pcopy + 1);
     int64_t nl = std::min<int64_t>(grid_for(wl), std::max<int64_t>(1, 148 * 16 * bytes_l / (bytes_l + bytes_r)));
     int64_t nr = std::min<int64_t>(grid_for(wr), std::max<int64_t>(1, 148 * 16 - nl));
-    split_both_kernel<<<(unsigned)(nl + nr), 256, 0, st>>>(l, r, (int)nl);
-    return cudaGetLastError();
+    if (l.swap != r.swap) return cudaErrorInvalidValue;
+    if (l.swap)
+        return launch_pdl(split_both_kernel<Layout::Right, Layout::Left>, dim3((unsigned)(nl + nr)), dim3(256), 0, st,
+                          l, r, (int)nl);
+    return launch_pdl(split_both_kernel<Layout::Left, Layout::Right>, dim3((unsigned)(nl + nr)), dim3(256), 0, st, l,
+                      r, (int)nl);
 }
 
 // ------------------------------------------------------------------ a3 TTP triples

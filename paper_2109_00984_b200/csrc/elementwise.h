@@ -19,6 +19,7 @@ struct LeftSplitArgs {
     int Pcopy;
     uint8_t* cp_planes;
     int64_t cp_planes_stride;        // bytes
+    int swap;                        // 1: planes in Layout::Right (transposed ring GEMM), else Layout::Left
 };
 
 struct RightSplitArgs {
@@ -33,6 +34,7 @@ struct RightSplitArgs {
     int add_delta_first;             // party 0's b' = b_0 + delta (R8)
     uint8_t* cp_planes;
     int64_t cp_planes_stride;
+    int swap;                        // 1: planes in Layout::Left (transposed ring GEMM), else Layout::Right
 };
 
 struct TtpGenArgs {

@@ -124,9 +124,23 @@ struct Carve {
     uint8_t* take(size_t n) { uint8_t* p = base ? base + off : nullptr; off += align256(n); return p; }
 };
 
+// The ring GEMM tiles its output in 256 x 128 blocks (rows x columns).  For a
+// small M it computes z^T = delta^T a_p^T + b'_p^T eps^T instead (x-side planes
+// in the right-operand layout, y-side planes in the left one, transposed
+// store) when that needs fewer padded tiles, e.g. M = 49: 256 x 512 -> 512 x 128.
+// Bit-identical either way (the same ring sums).  MPC_NO_SWAP=1 disables it.
+bool use_swap(int64_t M, int64_t N) {
+    static const bool off = getenv("MPC_NO_SWAP") != nullptr;
+    if (off) return false;
+    return pad_rows<Layout::Left>(N) * pad_rows<Layout::Right>(M) <
+           pad_rows<Layout::Left>(M) * pad_rows<Layout::Right>(N);
+}
+
 // workspace layout of beaver_matmul (see mpc_workspace_bytes)
 struct BeaverWs {
     uint8_t *eps_pl, *delta_pl, *a_pl, *b_pl;
+    int64_t a_stride, b_stride;   // bytes between parties' a_p / b'_p planes
+    bool swap;                    // transposed ring GEMM (use_swap)
     uint64_t* ed;        // one-party mode: [e | d] reveal buffer
     uint64_t* zbuf;      // one-party, P > 2, truncation: z reveal
     int8_t* hbuf;        // one-party, P > 2, truncation: top nibbles
@@ -138,21 +152,38 @@ BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N) {
     const int Pl = c->all ? c->P : 1;
     Carve cv(ws);
     BeaverWs w{};
-    w.eps_pl = cv.take(lp(M, K));
-    w.delta_pl = cv.take(rp(N, K));
-    w.a_pl = cv.take((size_t)Pl * lp(M, K));
-    w.b_pl = cv.take((size_t)Pl * rp(N, K));
+    w.swap = use_swap(M, N);
+    const int64_t xs = w.swap ? rp(M, K) : lp(M, K);     // eps, a_p planes (rows = M)
+    const int64_t ys = w.swap ? lp(N, K) : rp(N, K);     // delta, b'_p planes (rows = N)
+    const int64_t gM = w.swap ? N : M, gN = w.swap ? M : N;   // the GEMM's own output sizes
+    w.a_stride = xs;
+    w.b_stride = ys;
+    w.eps_pl = cv.take(xs);
+    w.delta_pl = cv.take(ys);
+    w.a_pl = cv.take((size_t)Pl * xs);
+    w.b_pl = cv.take((size_t)Pl * ys);
     w.ed = reinterpret_cast<uint64_t*>(c->all ? nullptr : cv.take(8 * (size_t)(M * K + K * N)));
     const bool alg1_one = !c->all && c->P > 2;
     w.zbuf = reinterpret_cast<uint64_t*>(alg1_one ? cv.take(8 * (size_t)(M * N)) : nullptr);
     w.hbuf = reinterpret_cast<int8_t*>(alg1_one ? cv.take((size_t)(M * N)) : nullptr);
-    size_t pb = ring_gemm_partials_bytes(Pl, M, N, 2 * (int)num_kb(K));
+    size_t pb = ring_gemm_partials_bytes(Pl, gM, gN, 2 * (int)num_kb(K));
     if (!c->all)   // the overlapped schedule runs two half-K GEMMs, the first on fewer SMs
-        pb = std::max({pb, ring_gemm_partials_bytes(1, M, N, (int)num_kb(K), kOverlapClusters),
-                       ring_gemm_partials_bytes(1, M, N, (int)num_kb(K))});
+        pb = std::max({pb, ring_gemm_partials_bytes(1, gM, gN, (int)num_kb(K), kOverlapClusters),
+                       ring_gemm_partials_bytes(1, gM, gN, (int)num_kb(K))});
     w.partials = reinterpret_cast<uint64_t*>(pb ? cv.take(pb) : nullptr);
     w.total = cv.off;
     return w;
+}
+
+// GEMM segment (x-side planes X, y-side planes Y): X @ Y^T normally, Y @ X^T when swapped.
+RingGemmSegment seg_of(const BeaverWs& w, const uint8_t* X, int64_t xstride, const uint8_t* Y, int64_t ystride,
+                       int kb) {
+    return w.swap ? RingGemmSegment{Y, X, kb, ystride, xstride} : RingGemmSegment{X, Y, kb, xstride, ystride};
+}
+void set_out(RingGemmParams& p, const BeaverWs& w, int64_t M, int64_t N) {
+    p.M = w.swap ? N : M;
+    p.N = w.swap ? M : N;
+    p.transpose_out = w.swap ? 1 : 0;
 }
 
 mpc_status beaver_local(mpc_ctx c, const BeaverWs& w, const uint64_t* ed, const uint64_t* a, const uint64_t* b,
@@ -177,26 +208,28 @@ mpc_status beaver_overlapped(mpc_ctx c, const BeaverWs& w, const uint64_t* x, co
     CHECK(nccl_allreduce(c, w.ed, w.ed, (size_t)sMK, ncclUint64, "eps reveal", c->comm_stream));
     cudaEventRecord(c->ev_eps, c->comm_stream);
     // a_p planes need no reveal
-    LeftSplitArgs La{M, K, 0, nullptr, nullptr, 0, nullptr, a, 1, w.a_pl, 0};
+    LeftSplitArgs La{M, K, 0, nullptr, nullptr, 0, nullptr, a, 1, w.a_pl, 0, w.swap};
     CHECK(run(c, kClsSplit, "split a", [&] { return launch_split_left(La, c->stream); }));
     cudaStreamWaitEvent(c->stream, c->ev_delta, 0);
-    RightSplitArgs R{K, N, 0, w.ed + sMK, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0};
+    RightSplitArgs R{K, N, 0, w.ed + sMK, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0, w.swap};
     CHECK(run(c, kClsSplit, "split delta", [&] { return launch_split_right(R, c->stream); }));
     RingGemmParams p1{};
-    p1.seg[0] = RingGemmSegment{w.a_pl, w.delta_pl, (int)num_kb(K), 0, 0};      // a_p @ delta
+    p1.seg[0] = seg_of(w, w.a_pl, 0, w.delta_pl, 0, (int)num_kb(K));           // a_p @ delta
     p1.nseg = 1;
-    p1.M = M; p1.N = N; p1.C = cc; p1.Z = z;
+    set_out(p1, w, M, N);
+    p1.C = cc; p1.Z = z;
     p1.trunc_bits = 0;
     p1.partials = w.partials;
     p1.max_clusters = kOverlapClusters;
     CHECK(gemm_run(c, p1, 1));
     cudaStreamWaitEvent(c->stream, c->ev_eps, 0);
-    LeftSplitArgs Le{M, K, 0, w.ed, nullptr, 1, w.eps_pl, nullptr, 0, nullptr, 0};
+    LeftSplitArgs Le{M, K, 0, w.ed, nullptr, 1, w.eps_pl, nullptr, 0, nullptr, 0, w.swap};
     CHECK(run(c, kClsSplit, "split eps", [&] { return launch_split_left(Le, c->stream); }));
     RingGemmParams p2{};
-    p2.seg[0] = RingGemmSegment{w.eps_pl, w.b_pl, (int)num_kb(K), 0, 0};       // eps @ b'_p
+    p2.seg[0] = seg_of(w, w.eps_pl, 0, w.b_pl, 0, (int)num_kb(K));             // eps @ b'_p
     p2.nseg = 1;
-    p2.M = M; p2.N = N; p2.C = z; p2.Z = z;                                     // z += ..., in place
+    set_out(p2, w, M, N);
+    p2.C = z; p2.Z = z;                                                         // z += ..., in place
     p2.trunc_bits = (truncate && c->P <= 2) ? c->frac : 0;
     p2.partials = w.partials;
     return gemm_run(c, p2, 1);
@@ -454,8 +487,8 @@ mpc_status mpc_beaver_matmul(mpc_ctx c, const uint64_t* x, const uint64_t* y, co
         return fail(c, MPC_ERR_ARG, "beaver_matmul: null pointer");
     const int64_t sMK = M * K, sKN = K * N, sMN = M * N;
     if (c->all) {
-        LeftSplitArgs L{M, K, sMK, x, a, c->P, w.eps_pl, a, c->P, w.a_pl, lp(M, K)};
-        RightSplitArgs R{K, N, sKN, y, b, c->P, w.delta_pl, b, c->P, 1, w.b_pl, rp(N, K)};
+        LeftSplitArgs L{M, K, sMK, x, a, c->P, w.eps_pl, a, c->P, w.a_pl, w.a_stride, w.swap};
+        RightSplitArgs R{K, N, sKN, y, b, c->P, w.delta_pl, b, c->P, 1, w.b_pl, w.b_stride, w.swap};
         CHECK(run(c, kClsSplit, "mask+reveal+split", [&] { return launch_split_both(L, R, c->stream); }));
     } else if (c->comm) {
         CHECK(beaver_overlapped(c, w, x, y, a, b, cc, z, M, K, N, truncate));
@@ -509,16 +542,17 @@ mpc_status beaver_local(mpc_ctx c, const BeaverWs& w, const uint64_t* ed, const 
     const int Pl = c->all ? c->P : 1;
     const int64_t sMK = M * K, sMN = M * N;
     if (!c->all) {
-        LeftSplitArgs L{M, K, 0, ed, nullptr, 1, w.eps_pl, a, 1, w.a_pl, 0};
-        RightSplitArgs R{K, N, 0, ed + sMK, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0};
+        LeftSplitArgs L{M, K, 0, ed, nullptr, 1, w.eps_pl, a, 1, w.a_pl, 0, w.swap};
+        RightSplitArgs R{K, N, 0, ed + sMK, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0, w.swap};
         CHECK(run(c, kClsSplit, "split eps/delta", [&] { return launch_split_both(L, R, c->stream); }));
     }
     RingGemmParams p{};
-    p.seg[0] = RingGemmSegment{w.a_pl, w.delta_pl, (int)num_kb(K), lp(M, K), 0};   // a_p @ delta
-    p.seg[1] = RingGemmSegment{w.eps_pl, w.b_pl, (int)num_kb(K), 0, rp(N, K)};     // eps @ b'_p
+    p.seg[0] = seg_of(w, w.a_pl, w.a_stride, w.delta_pl, 0, (int)num_kb(K));   // a_p @ delta
+    p.seg[1] = seg_of(w, w.eps_pl, 0, w.b_pl, w.b_stride, (int)num_kb(K));     // eps @ b'_p
     p.partials = w.partials;
     p.nseg = 2;
-    p.M = M; p.N = N; p.C = cc; p.Z = z;
+    set_out(p, w, M, N);
+    p.C = cc; p.Z = z;
     p.party_stride_c = p.party_stride_z = sMN;
     p.trunc_bits = (truncate && c->P <= 2) ? c->frac : 0;                                     // fused, 0 rounds
     return gemm_run(c, p, Pl);

@@ -29,7 +29,7 @@
 // 36 B/clk for 8192 MAC/clk.  Units (K chunk, super-pass) are ordered chunk
 // major so the second super-pass re-reads a K window still resident in L2.
 // The u64 running sum of a tile lives in the registers of 8 epilogue warps
-// (64 columns x 1 row per thread; setmaxnreg gives them 224 registers) and is
+// (64 columns x 1 row per thread; setmaxnreg gives them 216 registers) and is
 // written once, with the Beaver c_p addend and the fused truncation, at the
 // tile end.  The kernel is persistent: 74 clusters walk the tiles in a grouped
 // order (4 row tiles x all column tiles x parties per group).
@@ -445,44 +445,51 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Wor
                 }
             }
         }
-        // tile end: z = trunc(c + sum of all units) — one write per element
+        // tile end: z = trunc(c + sum of all units) — one write per element.
+        // Element (grow, gc) of the GEMM's output sits at base + gc * cs: row-major
+        // normally; column-major (i.e. the caller's row-major z, with the GEMM
+        // computing z^T) when transpose_out is set — then the 32 lanes of a warp
+        // (32 consecutive rows) touch 256 contiguous bytes per column.
         const int64_t grow = (int64_t)m * kTileM + rank * 128 + row;
+        const int64_t gc0 = (int64_t)n * kTileN + half * 64;
+        const bool tr = p.transpose_out != 0;
+        const int64_t cs = tr ? p.M : 1;
+        const int64_t off = (tr ? grow : grow * p.N) + gc0 * cs;
+        const bool full = !tr && vec && gc0 + 64 <= p.N;
         if (grow < p.M && wm.splits > 1) {
             // split-K: store this K range's partial sum in its own slab of the
-            // partials buffer; ring_gemm_finalize adds the slabs (ring addition
-            // commutes, any order is exact), c_p, and applies the truncation.
+            // partials buffer (same element layout as z); ring_gemm_finalize adds
+            // the slabs (ring addition commutes, any order is exact), c_p, and
+            // applies the truncation.
             const int s = w % wm.splits;
-            uint64_t* prow = p.partials + (int64_t)s * p.partial_stride + party * p.M * p.N + grow * p.N;
-            const int64_t gc0 = (int64_t)n * kTileN + half * 64;
-            if (vec && gc0 + 64 <= p.N) {
+            uint64_t* pb = p.partials + (int64_t)s * p.partial_stride + party * p.M * p.N + off;
+            if (full) {
 #pragma unroll
-                for (int j = 0; j < 64; j += 4) st_stream4(prow + gc0 + j, &run[j], pol);
+                for (int j = 0; j < 64; j += 4) st_stream4(pb + j, &run[j], pol);
             } else {
 #pragma unroll
                 for (int j = 0; j < 64; ++j)
-                    if (gc0 + j < p.N) prow[gc0 + j] = run[j];
+                    if (gc0 + j < p.N) pb[j * cs] = run[j];
             }
         } else if (grow < p.M) {
             // z = trunc(c + run).  z may alias c (in-place second phase): each
             // element is read before it is written by the same thread.  Batches of
             // 16 columns: all loads of a batch are issued before its stores, so a
             // row costs 4 memory round trips, not 32.
-            uint64_t* zrow = p.Z + party * p.party_stride_z + grow * p.N;
-            const uint64_t* crow = p.C ? p.C + party * p.party_stride_c + grow * p.N : nullptr;
-            const int64_t gc0 = (int64_t)n * kTileN + half * 64;
-            const bool full = vec && gc0 + 64 <= p.N;
+            uint64_t* zb = p.Z + party * p.party_stride_z + off;
+            const uint64_t* cb = p.C ? p.C + party * p.party_stride_c + off : nullptr;
 #pragma unroll
             for (int jb = 0; jb < 64; jb += 16) {
                 uint64_t v[16];
                 if (full) {
 #pragma unroll
                     for (int q = 0; q < 16; q += 4) {
-                        if (crow) ld_stream4(crow + gc0 + jb + q, pol, &v[q]);
+                        if (cb) ld_stream4(cb + jb + q, pol, &v[q]);
                         else v[q] = v[q + 1] = v[q + 2] = v[q + 3] = 0ull;
                     }
                 } else {
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = (crow && gc0 + jb + j < p.N) ? crow[gc0 + jb + j] : 0ull;
+                    for (int j = 0; j < 16; ++j) v[j] = (cb && gc0 + jb + j < p.N) ? cb[(jb + j) * cs] : 0ull;
                 }
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
@@ -491,11 +498,11 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Wor
                 }
                 if (full) {
 #pragma unroll
-                    for (int q = 0; q < 16; q += 4) st_stream4(zrow + gc0 + jb + q, &v[q], pol);
+                    for (int q = 0; q < 16; q += 4) st_stream4(zb + jb + q, &v[q], pol);
                 } else {
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
-                        if (gc0 + jb + j < p.N) zrow[gc0 + jb + j] = v[j];
+                        if (gc0 + jb + j < p.N) zb[(jb + j) * cs] = v[j];
                 }
             }
         }
@@ -684,6 +691,7 @@ namespace gemm {
 __global__ void finalize_kernel(uint64_t* __restrict__ z, const uint64_t* __restrict__ c,
                                 const uint64_t* __restrict__ part, int splits, int64_t n, int bits) {
     asm volatile("griddepcontrol.wait;" ::: "memory");     // programmatic dependent of the GEMM
+    asm volatile("griddepcontrol.launch_dependents;");      // the next split kernel may be scheduled
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         uint64_t v = c ? c[i] : 0ull;
         for (int s = 0; s < splits; ++s) v += part[(int64_t)s * n + i];

@@ -31,6 +31,9 @@ struct RingGemmParams {
     int64_t partial_stride;             // elements per slab (parties * M * N)
     int max_clusters;                   // 0: all SMs; else at most this many 2-CTA clusters (SMs left
                                         // to NCCL while a reveal overlaps the GEMM)
+    int transpose_out;                  // 1: the GEMM computes Z^T (M, N are its own sizes, i.e. the
+                                        // caller's N, M); element (m, n) is stored at Z[n * M + m] (and
+                                        // C is read there).  Used for small caller M (fewer padded rows).
 };
 
 // Largest unit length (32-K blocks) for which every s32 accumulator stays exact.

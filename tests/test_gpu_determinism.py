@@ -4,7 +4,8 @@ configs; ring addition is associative, so any order is exact).
 
 Each configuration runs in its own process because the GEMM's tuning knobs
 (K-chunk length MPC_GEMM_KC, split-K factor MPC_GEMM_SPLITS, programmatic
-dependent launch MPC_NO_PDL) are read once per process.  Every run must
+dependent launch MPC_NO_PDL, transposed GEMM for small M MPC_NO_SWAP) are
+read once per process.  Every run must
 produce the oracle's shares bit for bit.
 """
 import hashlib
@@ -20,7 +21,9 @@ import synth
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-M, K, N, P = 300, 3000, 700, 2        # 94 K-blocks, 2 x 6 output tiles: several units and a ragged tail
+P = 2
+SHAPES = [(300, 3000, 700),           # 94 K-blocks per segment, 2 x 6 output tiles, ragged tails
+          (49, 2000, 700)]            # small M: the ring GEMM runs transposed (unless MPC_NO_SWAP)
 
 SCRIPT = r"""
 import hashlib, sys
@@ -39,17 +42,18 @@ print(hashlib.sha256(z.view(torch.int64).cpu().numpy().tobytes()).hexdigest())
 """
 
 
-@pytest.fixture(scope="module")
-def expected():
+@pytest.fixture(scope="module", params=SHAPES, ids=lambda s: "x".join(map(str, s)))
+def case(request):
     from paper_2109_00984_b200 import build
     build.build()
+    M, K, N = request.param
     X = synth.uniform_fixed((M, K), 31)
     Y = synth.uniform_fixed((K, N), 32)
     a, b, c = oracle.ttp_triple(P, synth.MASTER_SEED, 4, M, K, N)
     z = oracle.beaver_matmul(oracle.share(P, synth.MASTER_SEED, X, 0, 1), oracle.share(P, synth.MASTER_SEED, Y, 1, 2),
                              a, b, c)
     z = oracle.truncate(z, 16)
-    return hashlib.sha256(np.ascontiguousarray(z).view(np.int64).tobytes()).hexdigest()
+    return (M, K, N), hashlib.sha256(np.ascontiguousarray(z).view(np.int64).tobytes()).hexdigest()
 
 
 @pytest.mark.parametrize("env", [
@@ -59,10 +63,12 @@ def expected():
     {"MPC_GEMM_SPLITS": "3"},
     {"MPC_GEMM_SPLITS": "7", "MPC_GEMM_KC": "5"},
     {"MPC_NO_PDL": "1"},
+    {"MPC_NO_SWAP": "1"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
-def test_same_shares_under_every_launch_config(expected, env):
+def test_same_shares_under_every_launch_config(case, env):
+    (M, K, N), expected = case
     full = dict(os.environ)
-    for k in ("MPC_GEMM_KC", "MPC_GEMM_SPLITS", "MPC_NO_PDL", "MPC_GEMM_DEBUG"):
+    for k in ("MPC_GEMM_KC", "MPC_GEMM_SPLITS", "MPC_NO_PDL", "MPC_NO_SWAP", "MPC_GEMM_DEBUG"):
         full.pop(k, None)
     full.update(env)
     out = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, M=M, K=K, N=N, P=P)], env=full,

@@ -149,7 +149,7 @@ def _beaver_case(P, M, K, N, seed, tid):
 
 @pytest.mark.parametrize("P", [1, 2, 3, 4])
 @pytest.mark.parametrize("M,K,N", [(64, 64, 64), (300, 100, 260), (129, 45, 1), (1, 1, 1), (200, 1, 130),
-                                   (130, 0, 70)])
+                                   (130, 0, 70), (49, 100, 700), (1, 45, 300)])   # last two: transposed GEMM
 def test_beaver_matmul_parity_untruncated(mpc, P, M, K, N):
     c = ctx(mpc, P)
     X, Y, xs, ys, a, b, cc = _beaver_case(P, M, K, N, seed=M + K + N, tid=P)
@@ -212,7 +212,7 @@ def test_truncate_parity(mpc, P):
 
 
 @pytest.mark.parametrize("P", [1, 2, 3])
-@pytest.mark.parametrize("M,K,N", [(64, 64, 64), (300, 100, 260), (1, 45, 3)])
+@pytest.mark.parametrize("M,K,N", [(64, 64, 64), (300, 100, 260), (1, 45, 3), (50, 90, 513)])
 def test_one_party_contexts_beaver(mpc, P, M, K, N):
     """The one-party-per-GPU kernels (mask, split of the revealed eps/delta, GEMM)
     on one device: P one-party contexts (no communicator), the eps||delta reveal
@@ -234,7 +234,8 @@ def test_one_party_contexts_beaver(mpc, P, M, K, N):
         assert np.array_equal(host(z1), oracle.truncate(oracle.beaver_matmul(xs, ys, a, b, cc), 16)[0])
 
 
-@pytest.mark.parametrize("M,K,N", [(64, 64, 64), (300, 100, 260), (197, 768, 300), (1024, 2048, 512)])
+@pytest.mark.parametrize("M,K,N", [(64, 64, 64), (300, 100, 260), (197, 768, 300), (1024, 2048, 512),
+                                   (49, 4608, 512)])
 def test_one_party_nccl_overlapped_schedule(mpc, M, K, N):
     """A one-party context WITH a (1-rank) NCCL communicator runs the production
     one-party-per-GPU schedule: mask, delta then eps reveals on the comm stream,
