@@ -100,6 +100,25 @@ def run_chain(ctx, layers, reps):
     return e0.elapsed_time(e1) / reps
 
 
+# Limb-GEMM roofline of one 2-party private matmul on one GPU:
+# 144*M*N*K int8 ops per party at the int8 peak bench.py uses (2 x measured
+# sustained bf16, MEASURED_PEAKS.json; 2 x 1407 TOPS if the file is absent).
+def int8_peak_tops():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        for k in ("bf16_tflops_sustained", "bf16_tflops"):
+            if k in d:
+                return 2.0 * float(d[k])
+    except (OSError, ValueError):
+        pass
+    return 2.0 * 1407.2
+
+
+def t_gemm_ms(M, K, N, parties=2):
+    return 144.0 * M * N * K * parties / (int8_peak_tops() * 1e12) * 1e3
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="all", choices=list(synth.MODELS) + ["all"])
@@ -117,10 +136,12 @@ def main():
             ms = run_chain(ctx, layers, args.reps)
             ops = sum(2.0 * M * K * N * cnt for _, M, K, N, cnt in layers)
             n = sum(cnt for *_, cnt in layers)
+            tg = sum(t_gemm_ms(M, K, N) * cnt for _, M, K, N, cnt in layers)
             out[name] = {"chain_ms": ms, "private_matmuls": n, "ring_TOPS": ops / (ms * 1e-3) / 1e12,
+                         "roofline_ms": tg, "roofline_frac": tg / ms,
                          "graph": "one CUDA graph per model"}
-            print(f"{name}: chain of {n} private matmuls {ms:.3f} ms ({out[name]['ring_TOPS']:.2f} ring-TOPS)",
-                  flush=True)
+            print(f"{name}: chain of {n} private matmuls {ms:.3f} ms ({out[name]['ring_TOPS']:.2f} ring-TOPS, "
+                  f"limb-GEMM roofline {tg:.3f} ms = {tg / ms:.3f})", flush=True)
             continue
         rows, total_ms, total_ops = [], 0.0, 0.0
         for lname, M, K, N, count in layers:
@@ -129,10 +150,11 @@ def main():
             total_ops += 2.0 * M * K * N * count
             rows.append({"layer": lname, "M": M, "K": K, "N": N, "count": count, "us": ms * 1e3,
                          "gemm_us": None if gms is None else gms * 1e3,
-                         "ring_TOPS": 2.0 * M * K * N / (ms * 1e-3) / 1e12})
+                         "ring_TOPS": 2.0 * M * K * N / (ms * 1e-3) / 1e12,
+                         "roofline_frac": t_gemm_ms(M, K, N) / ms})
             print(f"{name:9s} {lname:12s} {M:6d}x{K:5d}x{N:5d} x{count:2d}  {ms * 1e3:9.1f} us"
                   + ("" if gms is None else f"  (gemm {gms * 1e3:8.1f} us)")
-                  + f"  {rows[-1]['ring_TOPS']:7.2f} ring-TOPS", flush=True)
+                  + f"  {rows[-1]['ring_TOPS']:7.2f} ring-TOPS  roofline {rows[-1]['roofline_frac']:.3f}", flush=True)
         out[name] = {"layers": rows, "total_ms": total_ms, "ring_TOPS": total_ops / (total_ms * 1e-3) / 1e12,
                      "graph": args.graph}
         print(f"{name}: total {total_ms:.3f} ms per private inference's linear layers "
