@@ -274,3 +274,52 @@ def truncate(x, bits: int = 16, master: int | None = None, wrap_id: int = 0, dia
     r = r.reshape(x.shape)
     th = th.reshape(x.shape)
     return truncate_alg1(x, r, th, bits, diagnostics)
+
+
+# ---------------------------------------------------------------- O9 - O12
+def ttp_mul_triple(P: int, master: int, triple_id: int, shape):
+    """Elementwise Beaver triple (a, b, c), each (P, *shape), with Σc = Σa · Σb mod 2^64."""
+    _, kt = derive_keys(master, P)
+    shape = tuple(shape)
+    n = int(np.prod(shape, dtype=np.int64))
+    a, b, c = (np.zeros((P,) + shape, dtype=np.uint64) for _ in range(3))
+    lib().oracle_ttp_mul_triple(P, ctypes.c_uint64(kt), ctypes.c_uint64(triple_id), ctypes.c_int64(n),
+                                _p(a), _p(b), _p(c))
+    return a, b, c
+
+
+def ttp_square_pair(P: int, master: int, pair_id: int, shape):
+    """Beaver pair (a, b), each (P, *shape), with Σb = (Σa)^2 mod 2^64."""
+    _, kt = derive_keys(master, P)
+    shape = tuple(shape)
+    n = int(np.prod(shape, dtype=np.int64))
+    a, b = (np.zeros((P,) + shape, dtype=np.uint64) for _ in range(2))
+    lib().oracle_ttp_square_pair(P, ctypes.c_uint64(kt), ctypes.c_uint64(pair_id), ctypes.c_int64(n), _p(a), _p(b))
+    return a, b
+
+
+def beaver_mul(x, y, a, b, c, want_intermediates: bool = False):
+    """Un-truncated elementwise Beaver product shares z: (P, *shape) (scale 2^(2f))."""
+    x, y, a, b, c = (_u64(t) for t in (x, y, a, b, c))
+    P = x.shape[0]
+    n = x[0].size
+    z = np.zeros(x.shape, dtype=np.uint64)
+    eps = np.zeros(x.shape[1:], dtype=np.uint64)
+    delta = np.zeros(x.shape[1:], dtype=np.uint64)
+    lib().oracle_beaver_mul(P, _p(x), _p(y), _p(a), _p(b), _p(c), ctypes.c_int64(n), _p(eps), _p(delta), _p(z))
+    if want_intermediates:
+        return z, dict(eps=eps, delta=delta)
+    return z
+
+
+def beaver_square(x, a, b, want_intermediates: bool = False):
+    """Un-truncated Beaver square shares z: (P, *shape) (scale 2^(2f))."""
+    x, a, b = (_u64(t) for t in (x, a, b))
+    P = x.shape[0]
+    n = x[0].size
+    z = np.zeros(x.shape, dtype=np.uint64)
+    eps = np.zeros(x.shape[1:], dtype=np.uint64)
+    lib().oracle_beaver_square(P, _p(x), _p(a), _p(b), ctypes.c_int64(n), _p(eps), _p(z))
+    if want_intermediates:
+        return z, dict(eps=eps)
+    return z

@@ -19,7 +19,9 @@
  * Parity pins (tests/test_oracle_*.py): Philox KAT vectors, the frozen PRG
  * table, numpy uint64 matmul, Python big-int brute force, the paper's own
  * §4.3 float64 16-bit-block GEMM, the Beaver identity, the P=1 closed form,
- * the Alg. 1 identity against big-int recomputation.  "Parity unpinned": only
+ * the Alg. 1 identity against big-int recomputation; the elementwise product
+ * and square (O9-O12) against big-int identities and SPEC's examples
+ * (tests/test_oracle_elementwise.py).  "Parity unpinned": only
  * the *choice* of PRG layout (the paper allows any PRG); it is pinned
  * to the frozen table in SURVEY.md Appendix A.
  */
@@ -457,4 +459,117 @@ int oracle_truncate_alg1(int P, const uint64_t* x, const uint64_t* r, const uint
     }
     free(zs); free(beta); free(theta_z); free(z);
     return ORACLE_OK;
+}
+
+/* ========================================================================
+ * elementwise private multiplication and square.
+ * ======================================================================== */
+
+/* ------------------------------------------------------------------------
+ * O9  TTP Beaver triple for f = elementwise product (§4.2; P:576-580
+ * App. A.1.1 "A Beaver triple ... satisfies the property c = ab"):
+ *   a_p = G(k_ttp, A||p||id)[i], b_p = G(k_ttp, B||p||id)[i]
+ *   c   = (Σ_p a_p) · (Σ_p b_p)   elementwise, mod Q
+ *   c_p = G(k_ttp, C||p||id)[i] for p ≥ 1, c_0 = c − Σ_{p≥1} c_p
+ * (the same stream layout as the matmul triple, reading R6; triple ids are
+ * single-use, so a matmul and an elementwise triple never share an id).
+ * a, b, c: [P][n].
+ * ---------------------------------------------------------------------- */
+void oracle_ttp_mul_triple(int P, uint64_t k_ttp, uint64_t triple_id, int64_t n,
+                           uint64_t* a, uint64_t* b, uint64_t* c)
+{
+    for (int p = 0; p < P; p++) {
+        oracle_prg(k_ttp, oracle_stream_id(TAG_A, (uint32_t)p, triple_id), 0, n, a + (int64_t)p * n);
+        oracle_prg(k_ttp, oracle_stream_id(TAG_B, (uint32_t)p, triple_id), 0, n, b + (int64_t)p * n);
+    }
+    uint64_t* asum = (uint64_t*)calloc((size_t)(n > 0 ? n : 1), 8);
+    uint64_t* bsum = (uint64_t*)calloc((size_t)(n > 0 ? n : 1), 8);
+    oracle_reveal(P, a, n, asum);
+    oracle_reveal(P, b, n, bsum);
+    for (int64_t i = 0; i < n; i++) c[i] = asum[i] * bsum[i];
+    for (int p = 1; p < P; p++) {
+        uint64_t* cp = c + (int64_t)p * n;
+        oracle_prg(k_ttp, oracle_stream_id(TAG_C, (uint32_t)p, triple_id), 0, n, cp);
+        for (int64_t i = 0; i < n; i++) c[i] -= cp[i];                  /* c_0 −= c_p */
+    }
+    free(asum); free(bsum);
+}
+
+/* ------------------------------------------------------------------------
+ * O10 TTP Beaver pair for the square (App. A.1.1 "a Beaver pair
+ * ([a], [b]) such that b = a^2"):
+ *   a_p = G(k_ttp, A||p||id)[i];  b = (Σ_p a_p)^2 mod Q
+ *   b_p = G(k_ttp, C||p||id)[i] for p ≥ 1, b_0 = b − Σ_{p≥1} b_p
+ * (the correlated share uses the C tag, as c does in a triple — reading R20).
+ * a, b: [P][n].
+ * ---------------------------------------------------------------------- */
+void oracle_ttp_square_pair(int P, uint64_t k_ttp, uint64_t pair_id, int64_t n, uint64_t* a, uint64_t* b)
+{
+    for (int p = 0; p < P; p++)
+        oracle_prg(k_ttp, oracle_stream_id(TAG_A, (uint32_t)p, pair_id), 0, n, a + (int64_t)p * n);
+    uint64_t* asum = (uint64_t*)calloc((size_t)(n > 0 ? n : 1), 8);
+    oracle_reveal(P, a, n, asum);
+    for (int64_t i = 0; i < n; i++) b[i] = asum[i] * asum[i];
+    for (int p = 1; p < P; p++) {
+        uint64_t* bp = b + (int64_t)p * n;
+        oracle_prg(k_ttp, oracle_stream_id(TAG_C, (uint32_t)p, pair_id), 0, n, bp);
+        for (int64_t i = 0; i < n; i++) b[i] -= bp[i];                  /* b_0 −= b_p */
+    }
+    free(asum);
+}
+
+/* ------------------------------------------------------------------------
+ * O11 Beaver elementwise multiplication (§4.2):
+ *   [ε]_p = [x]_p − [a]_p,  [δ]_p = [y]_p − [b]_p;  ε, δ revealed (one round)
+ *   [z]_p = [c]_p + ε·[b]_p + [a]_p·δ + [p = 0]·ε·δ     (elementwise; R7)
+ * No truncation here (z at scale 2^(2f)).  All buffers [P][n]; eps_out and
+ * delta_out (n) may be NULL.
+ * ---------------------------------------------------------------------- */
+void oracle_beaver_mul(int P, const uint64_t* x, const uint64_t* y, const uint64_t* a, const uint64_t* b,
+                       const uint64_t* c, int64_t n, uint64_t* eps_out, uint64_t* delta_out, uint64_t* z)
+{
+    uint64_t* e = (uint64_t*)malloc((size_t)(P * (n > 0 ? n : 1)) * 8);
+    uint64_t* d = (uint64_t*)malloc((size_t)(P * (n > 0 ? n : 1)) * 8);
+    uint64_t* eps = (uint64_t*)malloc((size_t)(n > 0 ? n : 1) * 8);
+    uint64_t* delta = (uint64_t*)malloc((size_t)(n > 0 ? n : 1) * 8);
+    for (int64_t k = 0; k < (int64_t)P * n; k++) {
+        e[k] = x[k] - a[k];
+        d[k] = y[k] - b[k];
+    }
+    oracle_reveal(P, e, n, eps);
+    oracle_reveal(P, d, n, delta);
+    for (int p = 0; p < P; p++) {
+        for (int64_t i = 0; i < n; i++) {
+            int64_t k = (int64_t)p * n + i;
+            z[k] = c[k] + eps[i] * b[k] + a[k] * delta[i];
+            if (p == 0) z[k] += eps[i] * delta[i];
+        }
+    }
+    if (eps_out) memcpy(eps_out, eps, (size_t)n * 8);
+    if (delta_out) memcpy(delta_out, delta, (size_t)n * 8);
+    free(e); free(d); free(eps); free(delta);
+}
+
+/* ------------------------------------------------------------------------
+ * O12 Beaver square (App. A.1.1):
+ *   [ε]_p = [x]_p − [a]_p;  ε revealed (one round)
+ *   [x^2]_p = [b]_p + 2·ε·[a]_p + [p = 0]·ε^2          (party 0 adds the public ε², R7)
+ * All buffers [P][n]; eps_out (n) may be NULL.
+ * ---------------------------------------------------------------------- */
+void oracle_beaver_square(int P, const uint64_t* x, const uint64_t* a, const uint64_t* b, int64_t n,
+                          uint64_t* eps_out, uint64_t* z)
+{
+    uint64_t* e = (uint64_t*)malloc((size_t)(P * (n > 0 ? n : 1)) * 8);
+    uint64_t* eps = (uint64_t*)malloc((size_t)(n > 0 ? n : 1) * 8);
+    for (int64_t k = 0; k < (int64_t)P * n; k++) e[k] = x[k] - a[k];
+    oracle_reveal(P, e, n, eps);
+    for (int p = 0; p < P; p++) {
+        for (int64_t i = 0; i < n; i++) {
+            int64_t k = (int64_t)p * n + i;
+            z[k] = b[k] + 2u * eps[i] * a[k];
+            if (p == 0) z[k] += eps[i] * eps[i];
+        }
+    }
+    if (eps_out) memcpy(eps_out, eps, (size_t)n * 8);
+    free(e); free(eps);
 }

@@ -81,7 +81,13 @@ WAV2LETTER_B1 = [
     ("conv10", 51, 8000, 2000, 1), ("conv11", 51, 2000, 2000, 1), ("conv12", 51, 2000, 29, 1),
 ]
 
-MODELS = {"resnet50": RESNET50_B1, "vit": VIT_B16, "resnet18": RESNET18_B1, "wav2letter": WAV2LETTER_B1}
+# Text classification: the embedding applied as a
+# dense matmul of 32 one-hot tokens x vocabulary 519,820 x embedding 32 — a wide
+# reduction (K >> 16512, the per-unit exactness bound) at tiny M and N.
+TEXT_EMBED = [("embed", 32, 519820, 32, 1)]
+
+MODELS = {"resnet50": RESNET50_B1, "vit": VIT_B16, "resnet18": RESNET18_B1, "wav2letter": WAV2LETTER_B1,
+          "text": TEXT_EMBED}
 
 CONFIGS = {
     "C1": dict(M=64, K=64, N=64, P=2, seed=1001),

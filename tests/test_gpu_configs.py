@@ -76,6 +76,33 @@ def test_layer_gemm_parity(mpc, name, M, K, N, kind):
 
 
 @pytest.mark.slow
+def test_wide_k_text_embedding_full_parity(mpc):
+    """32 x 519,820 x 32 — K is 31x the
+    per-unit exactness bound, so the reduction runs as many drained K units
+    and split-K work items at a tiny output.  Every share is compared with the
+    oracle; the decoded product with float64 (exact: K*2^38 > 2^53 here, so
+    the float64 reference is computed in two exact halves)."""
+    P, (_, M, K, N, _) = 2, synth.TEXT_EMBED[0]
+    c = mpc.Context(P, mpc.ALL_PARTIES, device=0, master_seed=MASTER)
+    X = synth.gaussian_fixed((M, K), 1007, 1.0, -8, 8)
+    Y = synth.gaussian_fixed((K, N), 1008, 0.02, -8, 8)
+    gx, gy = c.share(dev(X), 0, 1), c.share(dev(Y), 1, 2)
+    ga, gb, gc = c.ttp_triples(9, M, K, N)
+    z = host(c.beaver_matmul(gx, gy, ga, gb, gc, truncate=True))
+    a, b, cc = oracle.ttp_triple(P, MASTER, 9, M, K, N)
+    ez, dg = oracle.truncate(oracle.beaver_matmul(oracle.share(P, MASTER, X, 0, 1), oracle.share(P, MASTER, Y, 1, 2),
+                                                  a, b, cc), 16, diagnostics=True)
+    assert np.array_equal(z, ez)
+    Xi, Yi = X.view(np.int64), Y.view(np.int64)
+    h = K // 2
+    exact = ((Xi[:, :h].astype(np.float64) @ Yi[:h].astype(np.float64)) +
+             (Xi[:, h:].astype(np.float64) @ Yi[h:].astype(np.float64))) / 2.0 ** 32
+    got = oracle.decode(oracle.reveal(z))
+    ok = dg["theta"] == 0
+    assert np.all(np.abs(got - exact)[ok] <= 2.0 ** -14)
+
+
+@pytest.mark.slow
 @pytest.mark.parametrize("P", [4, 8])
 def test_c5_8192_sampled(mpc, P):
     """configs[4]: P-party 8192^3 Beaver matmul + Alg. 1 truncation (all parties on
