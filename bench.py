@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--parties", type=int, default=2, help="P; one GPU: all P parties; N GPUs: N/P sessions")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-next-rows", action="store_true", help="skip the SURVEY §8(f) NEXT-row measurements")
     ap.add_argument("--sample-rows", type=int, default=16)
     return ap.parse_args()
 
@@ -443,6 +444,11 @@ def main():
     }
     if e2e:
         line["e2e"] = e2e
+    if world == 1 and not args.no_next_rows:
+        # elementwise private product / square (HBM-bound), same parties, n = M*N
+        sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "scripts"))
+        import bench_elementwise
+        line["next_rows"] = {"elementwise_mul_square": bench_elementwise.run(M * N, P, 20)}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = oracle_baseline(M, K, N)
     print(json.dumps(line), flush=True)

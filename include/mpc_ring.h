@@ -172,6 +172,48 @@ size_t mpc_ring_matmul_workspace_bytes(int64_t M, int64_t K, int64_t N);
 mpc_status mpc_ring_matmul(mpc_ctx ctx, const uint64_t* A, const uint64_t* B, uint64_t* C,
                            int64_t M, int64_t K, int64_t N, void* workspace, size_t workspace_bytes);
 
+/* ---- elementwise private multiplication and square --
+ * App. A.1.1 P:575-594 ("Multiplication", "Square").  All buffers n elements per
+ * party ([P][n] on an all-parties context), caller-owned device memory.
+ *
+ * mpc_ttp_mul_triples: a_p = G(k_ttp, A||p||id), b_p = G(k_ttp, B||p||id),
+ *   c = (sum a_p)(sum b_p) elementwise, c_p = G(k_ttp, C||p||id) for p >= 1,
+ *   c_0 = c - sum_{p>=1} c_p (R6, R21).  Offline; 0 rounds.
+ * mpc_ttp_square_pairs: the Beaver pair of P:592, b = a^2: a_p as above, b_p
+ *   (p >= 1) from the C stream, b_0 = a^2 - sum_{p>=1} b_p (R20).
+ * mpc_beaver_mul: e_p = x_p - a_p, d_p = y_p - b_p; [eps | delta] revealed in ONE
+ *   batched round; z_p = c_p + eps b_p + a_p delta + [p == 0] eps delta, then the
+ *   truncation of mpc_beaver_matmul (local for P <= 2, Alg. 1 with wrap_id for P > 2).
+ * mpc_beaver_square: e_p = x_p - a_p; eps revealed (one round);
+ *   z_p = b_p + 2 eps a_p + [p == 0] eps^2, then truncation as above.
+ * z must not alias an input.  One-party contexts use the context's scratch for
+ * the reveal buffer.  Errors: MPC_ERR_SHAPE (n < 0), MPC_ERR_ARG (null pointer),
+ * MPC_ERR_STATE (P > 1 one-party context without communicator), MPC_ERR_NCCL. */
+mpc_status mpc_ttp_mul_triples(mpc_ctx ctx, uint64_t triple_id, int64_t n, uint64_t* a, uint64_t* b, uint64_t* c);
+mpc_status mpc_ttp_square_pairs(mpc_ctx ctx, uint64_t pair_id, int64_t n, uint64_t* a, uint64_t* b);
+mpc_status mpc_beaver_mul(mpc_ctx ctx, const uint64_t* x, const uint64_t* y, const uint64_t* a,
+                          const uint64_t* b, const uint64_t* c, uint64_t* z, int64_t n,
+                          int truncate, uint64_t wrap_id);
+mpc_status mpc_beaver_square(mpc_ctx ctx, const uint64_t* x, const uint64_t* a, const uint64_t* b,
+                             uint64_t* z, int64_t n, int truncate, uint64_t wrap_id);
+/* The same with the round made explicit (one-party contexts, as mpc_beaver_finish):
+ * the caller forms [x - a | y - b] (mpc_beaver_mask with M = 1, K = n, N = 1; for the
+ * square N = 0), sums it over the parties (one round) and passes the revealed
+ * [eps | delta] (square: eps) here.  Local truncation only (P <= 2).
+ * MPC_ERR_UNSUPPORTED on an all-parties context. */
+mpc_status mpc_beaver_mul_finish(mpc_ctx ctx, const uint64_t* ed, const uint64_t* a, const uint64_t* b,
+                                 const uint64_t* c, uint64_t* z, int64_t n, int truncate);
+mpc_status mpc_beaver_square_finish(mpc_ctx ctx, const uint64_t* eps, const uint64_t* a, const uint64_t* b,
+                                    uint64_t* z, int64_t n, int truncate);
+
+/* ---- batched multi-tensor reveal (one round) --------------------------------
+ * out_t = sum over parties of share_t (mod 2^64) for t < count, counted as ONE
+ * round (collectives issued without a data-dependent wait): one NCCL
+ * group of allreduces on one-party contexts, local sums on all-parties contexts
+ * (share_t is then [P][n_t]).  shares / outs / ns: host arrays of count entries. */
+mpc_status mpc_reveal_batch(mpc_ctx ctx, int count, const uint64_t* const* shares, uint64_t* const* outs,
+                            const int64_t* ns);
+
 /* ---- measurement hooks (bench.py) ----------------------------------------
  * When enabled, the library brackets every launch of kernel class `cls` with CUDA
  * events on the launching stream and accumulates its device time.

@@ -33,7 +33,11 @@ TAG_PRZS, TAG_A, TAG_B, TAG_C, TAG_R, TAG_THETA = 1, 2, 3, 4, 5, 6
 def build(force: bool = False) -> str:
     """Compile oracle.c -> liboracle.so with plain gcc -O2 -fopenmp."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-o", _LIB, _SRC, "-lm"])
+        # compile to a private name, then rename: concurrent importers (spawned
+        # test workers) never load a half-written library
+        tmp = f"{_LIB}.{os.getpid()}.tmp"
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
     return _LIB
 
 

@@ -35,6 +35,13 @@ SIGNATURES = [
     ("mpc_truncate", _I, [_V, _V, _L, _I, _U]),
     ("mpc_ring_matmul_workspace_bytes", _S, [_L, _L, _L]),
     ("mpc_ring_matmul", _I, [_V, _V, _V, _V, _L, _L, _L, _V, _S]),
+    ("mpc_ttp_mul_triples", _I, [_V, _U, _L, _V, _V, _V]),
+    ("mpc_ttp_square_pairs", _I, [_V, _U, _L, _V, _V]),
+    ("mpc_beaver_mul", _I, [_V, _V, _V, _V, _V, _V, _V, _L, _I, _U]),
+    ("mpc_beaver_square", _I, [_V, _V, _V, _V, _V, _L, _I, _U]),
+    ("mpc_beaver_mul_finish", _I, [_V, _V, _V, _V, _V, _V, _L, _I]),
+    ("mpc_beaver_square_finish", _I, [_V, _V, _V, _V, _V, _L, _I]),
+    ("mpc_reveal_batch", _I, [_V, _I, ctypes.POINTER(_V), ctypes.POINTER(_V), ctypes.POINTER(_L)]),
     ("mpc_profile_enable", _I, [_V, _I]),
     ("mpc_profile_read", _I, [_V, _I, ctypes.POINTER(_D), ctypes.POINTER(_U)]),
     ("mpc_launch_count", _U, [_V]),

@@ -15,6 +15,7 @@
 
 #include "../../include/mpc_ring.h"
 #include "common.cuh"
+#include "beaver_elementwise.h"
 #include "elementwise.h"
 #include "ring_gemm.h"
 
@@ -602,6 +603,163 @@ mpc_status mpc_ring_matmul(mpc_ctx c, const uint64_t* A, const uint64_t* B, uint
     const size_t pb = ring_gemm_partials_bytes(1, M, N, (int)num_kb(K));
     p.partials = reinterpret_cast<uint64_t*>(pb ? cv.take(pb) : nullptr);
     return gemm_run(c, p, 1);
+}
+
+// ---------------------------------------------------------------- elementwise product / square
+// (App. A.1.1)
+mpc_status mpc_ttp_mul_triples(mpc_ctx c, uint64_t id, int64_t n, uint64_t* a, uint64_t* b, uint64_t* cc) {
+    CHECK(enter(c));
+    if (n < 0) return fail(c, MPC_ERR_SHAPE, "ttp_mul_triples: n < 0");
+    if (n == 0) return MPC_OK;
+    if (!a || !b || !cc) return fail(c, MPC_ERR_ARG, "ttp_mul_triples: null output");
+    const int lo = c->all ? 0 : c->rank, hi = c->all ? c->P : c->rank + 1;
+    return run(c, kClsPrg, "ttp_mul",
+               [&] { return launch_ttp_elementwise(false, c->kttp, id, c->P, lo, hi, a, b, cc, n, c->stream); });
+}
+
+mpc_status mpc_ttp_square_pairs(mpc_ctx c, uint64_t id, int64_t n, uint64_t* a, uint64_t* b) {
+    CHECK(enter(c));
+    if (n < 0) return fail(c, MPC_ERR_SHAPE, "ttp_square_pairs: n < 0");
+    if (n == 0) return MPC_OK;
+    if (!a || !b) return fail(c, MPC_ERR_ARG, "ttp_square_pairs: null output");
+    const int lo = c->all ? 0 : c->rank, hi = c->all ? c->P : c->rank + 1;
+    return run(c, kClsPrg, "ttp_square",
+               [&] { return launch_ttp_elementwise(true, c->kttp, id, c->P, lo, hi, a, b, nullptr, n, c->stream); });
+}
+
+}  // extern "C"
+
+namespace {
+// Shared body of mpc_beaver_mul (square = false) and mpc_beaver_square.
+mpc_status beaver_elementwise(mpc_ctx c, bool square, const uint64_t* x, const uint64_t* y, const uint64_t* a,
+                              const uint64_t* b, const uint64_t* cc, uint64_t* z, int64_t n, int truncate,
+                              uint64_t wrap_id) {
+    const char* what = square ? "beaver_square" : "beaver_mul";
+    CHECK(enter(c));
+    if (n < 0) return fail(c, MPC_ERR_SHAPE, "%s: n < 0", what);
+    const int Pl = c->all ? c->P : 1;
+    const int64_t nrev = square ? n : 2 * n;             // eps (|| delta): one batched reveal
+    c->rounds += 1;
+    c->bytes += 8ull * (uint64_t)nrev * Pl;
+    if (n == 0) return MPC_OK;
+    if (!x || !a || !b || !z || (!square && (!y || !cc))) return fail(c, MPC_ERR_ARG, "%s: null pointer", what);
+    const int bits = (truncate && c->P <= 2) ? c->frac : 0;               // fused local truncation
+    uint64_t* zb = nullptr;
+    int8_t* hb = nullptr;
+    if (c->all) {
+        CHECK(run(c, kClsSplit, what, [&] {
+            return launch_beaver_elementwise_all(square, x, y, a, b, cc, z, c->P, n, bits, c->stream);
+        }));
+    } else {
+        // one party: [x - a | y - b] -> reveal (one allreduce) -> z_p; scratch also holds Alg. 1's buffers
+        const size_t ed_bytes = align256(8 * (size_t)nrev);
+        const bool alg1 = truncate && c->P > 2;
+        CHECK(ensure_scratch(c, ed_bytes + (alg1 ? align256(8 * (size_t)n) + (size_t)n : 0)));
+        uint64_t* ed = static_cast<uint64_t*>(c->scratch);
+        if (alg1) {
+            zb = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(c->scratch) + ed_bytes);
+            hb = reinterpret_cast<int8_t*>(static_cast<uint8_t*>(c->scratch) + ed_bytes + align256(8 * (size_t)n));
+        }
+        CHECK(run(c, kClsSplit, "mask", [&] {
+            return launch_mask(x, a, n, square ? nullptr : y, square ? nullptr : b, square ? 0 : n, ed, c->stream);
+        }));
+        if (c->P > 1) CHECK(nccl_allreduce(c, ed, ed, (size_t)nrev, ncclUint64, "eps/delta reveal"));
+        CHECK(run(c, kClsSplit, what, [&] {
+            return launch_beaver_elementwise_finish(square, ed, a, b, cc, z, n, c->rank == 0, bits, c->stream);
+        }));
+    }
+    if (truncate && c->P > 2) CHECK(truncate_impl(c, z, n, c->frac, wrap_id, zb, hb));
+    return MPC_OK;
+}
+}  // namespace
+
+extern "C" {
+
+mpc_status mpc_beaver_mul(mpc_ctx c, const uint64_t* x, const uint64_t* y, const uint64_t* a, const uint64_t* b,
+                          const uint64_t* cc, uint64_t* z, int64_t n, int truncate, uint64_t wrap_id) {
+    return beaver_elementwise(c, false, x, y, a, b, cc, z, n, truncate, wrap_id);
+}
+
+mpc_status mpc_beaver_square(mpc_ctx c, const uint64_t* x, const uint64_t* a, const uint64_t* b, uint64_t* z,
+                             int64_t n, int truncate, uint64_t wrap_id) {
+    return beaver_elementwise(c, true, x, nullptr, a, b, nullptr, z, n, truncate, wrap_id);
+}
+
+// The elementwise product / square after the caller's reveal (one-party contexts;
+// the round made explicit, as mpc_beaver_finish for the matmul).
+mpc_status mpc_beaver_mul_finish(mpc_ctx c, const uint64_t* ed, const uint64_t* a, const uint64_t* b,
+                                 const uint64_t* cc, uint64_t* z, int64_t n, int truncate) {
+    CHECK(enter(c));
+    if (c->all) return fail(c, MPC_ERR_UNSUPPORTED, "beaver_mul_finish: one-party contexts only");
+    if (truncate && c->P > 2) return fail(c, MPC_ERR_UNSUPPORTED, "beaver_mul_finish: P > 2 truncation needs mpc_truncate");
+    if (n < 0) return fail(c, MPC_ERR_SHAPE, "beaver_mul_finish: n < 0");
+    c->rounds += 1;
+    c->bytes += 16ull * (uint64_t)n;
+    if (n == 0) return MPC_OK;
+    if (!ed || !a || !b || !cc || !z) return fail(c, MPC_ERR_ARG, "beaver_mul_finish: null pointer");
+    const int bits = truncate ? c->frac : 0;
+    return run(c, kClsSplit, "beaver_mul", [&] {
+        return launch_beaver_elementwise_finish(false, ed, a, b, cc, z, n, c->rank == 0, bits, c->stream);
+    });
+}
+
+mpc_status mpc_beaver_square_finish(mpc_ctx c, const uint64_t* e, const uint64_t* a, const uint64_t* b, uint64_t* z,
+                                    int64_t n, int truncate) {
+    CHECK(enter(c));
+    if (c->all) return fail(c, MPC_ERR_UNSUPPORTED, "beaver_square_finish: one-party contexts only");
+    if (truncate && c->P > 2) return fail(c, MPC_ERR_UNSUPPORTED, "beaver_square_finish: P > 2 truncation needs mpc_truncate");
+    if (n < 0) return fail(c, MPC_ERR_SHAPE, "beaver_square_finish: n < 0");
+    c->rounds += 1;
+    c->bytes += 8ull * (uint64_t)n;
+    if (n == 0) return MPC_OK;
+    if (!e || !a || !b || !z) return fail(c, MPC_ERR_ARG, "beaver_square_finish: null pointer");
+    const int bits = truncate ? c->frac : 0;
+    return run(c, kClsSplit, "beaver_square", [&] {
+        return launch_beaver_elementwise_finish(true, e, a, b, nullptr, z, n, c->rank == 0, bits, c->stream);
+    });
+}
+
+// Several reveals in one round: one NCCL group of allreduces (one-party
+// contexts), local sums (all parties on one device).
+mpc_status mpc_reveal_batch(mpc_ctx c, int count, const uint64_t* const* shares, uint64_t* const* outs,
+                            const int64_t* ns) {
+    CHECK(enter(c));
+    if (count < 0 || (count > 0 && (!shares || !outs || !ns))) return fail(c, MPC_ERR_ARG, "reveal_batch: bad arguments");
+    uint64_t total = 0;
+    for (int t = 0; t < count; ++t) {
+        if (ns[t] < 0) return fail(c, MPC_ERR_SHAPE, "reveal_batch: n[%d] < 0", t);
+        if (ns[t] > 0 && (!shares[t] || !outs[t])) return fail(c, MPC_ERR_ARG, "reveal_batch: null pointer %d", t);
+        total += (uint64_t)ns[t];
+    }
+    c->rounds += 1;
+    c->bytes += 8ull * total * (c->all ? c->P : 1);
+    if (c->all) {
+        for (int t = 0; t < count; ++t)
+            if (ns[t]) CHECK(run(c, kClsSplit, "reveal_sum",
+                                 [&] { return launch_sum_parties(shares[t], c->P, ns[t], outs[t], c->stream); }));
+        return MPC_OK;
+    }
+    if (c->P == 1 && !c->comm) {
+        for (int t = 0; t < count; ++t) {
+            if (!ns[t]) continue;
+            cudaError_t e = cudaMemcpyAsync(outs[t], shares[t], 8 * (size_t)ns[t], cudaMemcpyDeviceToDevice, c->stream);
+            if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "reveal_batch copy: %s", cudaGetErrorString(e));
+        }
+        return MPC_OK;
+    }
+    if (!c->comm) return fail(c, MPC_ERR_STATE, "reveal_batch: context has no communicator (created without nccl_id)");
+    ncclResult_t r = ncclGroupStart();
+    for (int t = 0; t < count && r == ncclSuccess; ++t)
+        if (ns[t]) r = ncclAllReduce(shares[t], outs[t], (size_t)ns[t], ncclUint64, ncclSum, c->comm, c->stream);
+    ncclResult_t r2 = ncclGroupEnd();
+    if (r == ncclSuccess) r = r2;
+    if (r != ncclSuccess) {
+        c->broken = true;
+        ncclCommAbort(c->comm);
+        c->comm = nullptr;
+        return fail(c, MPC_ERR_NCCL, "reveal_batch: %s", ncclGetErrorString(r));
+    }
+    return MPC_OK;
 }
 
 mpc_status mpc_profile_enable(mpc_ctx c, int enable) {

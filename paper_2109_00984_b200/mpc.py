@@ -201,6 +201,74 @@ class Context:
                    ctypes.c_int64(K), ctypes.c_int64(N), int(bool(truncate)), _ptr(ws), ctypes.c_size_t(ws.numel()))
         return z
 
+    # ------------------------------------------------------------ elementwise
+    def ttp_mul_triples(self, triple_id: int, shape, out=None):
+        """Elementwise Beaver triple (a, b, c), c = ab (App. A.1.1)."""
+        shp = self._lead() + tuple(shape)
+        a, b, c = out if out is not None else (_u64(shp, self.device) for _ in range(3))
+        for t in (a, b, c):
+            _check_out(t, shp, torch.uint64)
+        n = a[0].numel() if self.all_parties else a.numel()
+        self._call(self._lib.mpc_ttp_mul_triples, ctypes.c_uint64(triple_id), ctypes.c_int64(n), _ptr(a), _ptr(b),
+                   _ptr(c))
+        return a, b, c
+
+    def ttp_square_pairs(self, pair_id: int, shape, out=None):
+        """Beaver pair (a, b), b = a^2."""
+        shp = self._lead() + tuple(shape)
+        a, b = out if out is not None else (_u64(shp, self.device) for _ in range(2))
+        for t in (a, b):
+            _check_out(t, shp, torch.uint64)
+        n = a[0].numel() if self.all_parties else a.numel()
+        self._call(self._lib.mpc_ttp_square_pairs, ctypes.c_uint64(pair_id), ctypes.c_int64(n), _ptr(a), _ptr(b))
+        return a, b
+
+    def beaver_mul(self, x, y, a, b, c, truncate: bool = True, wrap_id: int = 0,
+                   out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Elementwise private product [x][y] (one round; + Alg. 1's round if P > 2 and truncate)."""
+        z = _u64(tuple(x.shape), self.device) if out is None else _check_out(out, tuple(x.shape), torch.uint64)
+        for t in (y, a, b, c):
+            _check_out(t, tuple(x.shape), torch.uint64)
+        n = x[0].numel() if self.all_parties else x.numel()
+        self._call(self._lib.mpc_beaver_mul, _ptr(x), _ptr(y), _ptr(a), _ptr(b), _ptr(c), _ptr(z),
+                   ctypes.c_int64(n), int(bool(truncate)), ctypes.c_uint64(wrap_id))
+        return z
+
+    def beaver_square(self, x, a, b, truncate: bool = True, wrap_id: int = 0,
+                      out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Private square [x^2] with a Beaver pair (one round; + Alg. 1's round if P > 2 and truncate)."""
+        z = _u64(tuple(x.shape), self.device) if out is None else _check_out(out, tuple(x.shape), torch.uint64)
+        for t in (a, b):
+            _check_out(t, tuple(x.shape), torch.uint64)
+        n = x[0].numel() if self.all_parties else x.numel()
+        self._call(self._lib.mpc_beaver_square, _ptr(x), _ptr(a), _ptr(b), _ptr(z), ctypes.c_int64(n),
+                   int(bool(truncate)), ctypes.c_uint64(wrap_id))
+        return z
+
+    def beaver_mul_finish(self, ed, a, b, c, truncate: bool = True) -> torch.Tensor:
+        """One-party context: z_p from the revealed [eps | delta] (see mpc_beaver_mul_finish)."""
+        z = _u64(tuple(a.shape), self.device)
+        self._call(self._lib.mpc_beaver_mul_finish, _ptr(ed), _ptr(a), _ptr(b), _ptr(c), _ptr(z),
+                   ctypes.c_int64(a.numel()), int(bool(truncate)))
+        return z
+
+    def beaver_square_finish(self, e, a, b, truncate: bool = True) -> torch.Tensor:
+        """One-party context: [x^2]_p from the revealed eps (see mpc_beaver_square_finish)."""
+        z = _u64(tuple(a.shape), self.device)
+        self._call(self._lib.mpc_beaver_square_finish, _ptr(e), _ptr(a), _ptr(b), _ptr(z),
+                   ctypes.c_int64(a.numel()), int(bool(truncate)))
+        return z
+
+    def reveal_batch(self, shares: list) -> list:
+        """Reveal several share tensors in one round."""
+        outs = [_u64(tuple(s.shape[1:]) if self.all_parties else tuple(s.shape), self.device) for s in shares]
+        cnt = len(shares)
+        sp = (ctypes.c_void_p * max(cnt, 1))(*[_ptr(s) for s in shares])
+        op = (ctypes.c_void_p * max(cnt, 1))(*[_ptr(o) for o in outs])
+        ns = (ctypes.c_int64 * max(cnt, 1))(*[o.numel() for o in outs])
+        self._call(self._lib.mpc_reveal_batch, cnt, sp, op, ns)
+        return outs
+
     def truncate(self, x: torch.Tensor, bits: Optional[int] = None, wrap_id: int = 0) -> torch.Tensor:
         """In place; returns x."""
         n = x[0].numel() if self.all_parties else x.numel()

@@ -33,6 +33,7 @@ def _free_port() -> int:
 
 
 def _run(world, fn, *args):
+    oracle.build()          # once, before the workers import it
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
