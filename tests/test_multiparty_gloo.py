@@ -170,3 +170,37 @@ def test_distributed_alg1_truncation_equals_oracle():
     exp = oracle.truncate_alg1(xs, r, th, 16)
     for p in range(world):
         assert np.array_equal(res[p], exp[p])
+
+
+# ---------------------------------------------------------------------------
+def _party_elementwise(rank, world, n):
+    """One party of the elementwise product and square:
+    mask, ONE reveal of [eps | delta] (mpc_beaver_mul's batched round), z_p with
+    the public term on party 0; the square reveals eps alone."""
+    P = world
+    X = synth.uniform_fixed((n,), 61)
+    Y = synth.uniform_fixed((n,), 62)
+    xs = oracle.share(P, MASTER, X, 0, 3)[rank]
+    ys = oracle.share(P, MASTER, Y, 1 % P, 4)[rank]
+    a, b, c = (t[rank] for t in oracle.ttp_mul_triple(P, MASTER, 5, (n,)))
+    ed = _ring_allreduce(np.concatenate([xs - a, ys - b]))
+    eps, delta = ed[:n], ed[n:]
+    z = c + eps * b + a * delta + (eps * delta if rank == 0 else np.uint64(0))
+    a2, b2 = (t[rank] for t in oracle.ttp_square_pair(P, MASTER, 6, (n,)))
+    e2 = _ring_allreduce(xs - a2)
+    z2 = b2 + np.uint64(2) * e2 * a2 + (e2 * e2 if rank == 0 else np.uint64(0))
+    return z, z2
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_distributed_elementwise_mul_square_equal_oracle(world):
+    n = 257
+    res = _run(world, _party_elementwise, n)
+    X = synth.uniform_fixed((n,), 61)
+    Y = synth.uniform_fixed((n,), 62)
+    xs = oracle.share(world, MASTER, X, 0, 3)
+    ys = oracle.share(world, MASTER, Y, 1 % world, 4)
+    ez = oracle.beaver_mul(xs, ys, *oracle.ttp_mul_triple(world, MASTER, 5, (n,)))
+    ez2 = oracle.beaver_square(xs, *oracle.ttp_square_pair(world, MASTER, 6, (n,)))
+    for r in range(world):
+        assert np.array_equal(res[r][0], ez[r]) and np.array_equal(res[r][1], ez2[r])
