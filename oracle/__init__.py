@@ -327,3 +327,50 @@ def beaver_square(x, a, b, want_intermediates: bool = False):
     if want_intermediates:
         return z, dict(eps=eps)
     return z
+
+
+# ---------------------------------------------------------------- O13 / O14
+class _ConvGeom(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int64) for f in ("B", "C", "H", "W", "Cout", "kh", "kw", "sh", "sw", "ph", "pw")]
+
+
+def conv_geom(B, C, H, W, Cout, kh, kw, stride=1, padding=0):
+    sh, sw = (stride, stride) if isinstance(stride, int) else stride
+    ph, pw = (padding, padding) if isinstance(padding, int) else padding
+    return _ConvGeom(B, C, H, W, Cout, kh, kw, sh, sw, ph, pw)
+
+
+def conv_out_shape(g):
+    return (g.B, g.Cout, (g.H + 2 * g.ph - g.kh) // g.sh + 1, (g.W + 2 * g.pw - g.kw) // g.sw + 1)
+
+
+def conv2d(x, w, g) -> np.ndarray:
+    """Ring convolution mod 2^64: x (B,C,H,W), w (Cout,C,kh,kw) -> (B,Cout,Ho,Wo)."""
+    x, w = _u64(x), _u64(w)
+    out = np.zeros(conv_out_shape(g), dtype=np.uint64)
+    lib().oracle_conv2d(_p(x), _p(w), ctypes.byref(g), _p(out))
+    return out
+
+
+def ttp_conv_triple(P: int, master: int, triple_id: int, g):
+    """Conv Beaver triple: a (P,B,C,H,W), b (P,Cout,C,kh,kw), c (P,B,Cout,Ho,Wo), Σc = conv(Σa, Σb)."""
+    _, kt = derive_keys(master, P)
+    a = np.zeros((P, g.B, g.C, g.H, g.W), dtype=np.uint64)
+    b = np.zeros((P, g.Cout, g.C, g.kh, g.kw), dtype=np.uint64)
+    c = np.zeros((P,) + conv_out_shape(g), dtype=np.uint64)
+    lib().oracle_ttp_conv_triple(P, ctypes.c_uint64(kt), ctypes.c_uint64(triple_id), ctypes.byref(g),
+                                 _p(a), _p(b), _p(c))
+    return a, b, c
+
+
+def beaver_conv2d(x, y, a, b, c, g, want_intermediates: bool = False):
+    """Un-truncated Beaver convolution shares z: (P,B,Cout,Ho,Wo) (scale 2^(2f))."""
+    x, y, a, b, c = (_u64(t) for t in (x, y, a, b, c))
+    P = x.shape[0]
+    z = np.zeros((P,) + conv_out_shape(g), dtype=np.uint64)
+    eps = np.zeros(x.shape[1:], dtype=np.uint64)
+    delta = np.zeros(y.shape[1:], dtype=np.uint64)
+    lib().oracle_beaver_conv2d(P, _p(x), _p(y), _p(a), _p(b), _p(c), ctypes.byref(g), _p(eps), _p(delta), _p(z))
+    if want_intermediates:
+        return z, dict(eps=eps, delta=delta)
+    return z

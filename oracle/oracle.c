@@ -573,3 +573,108 @@ void oracle_beaver_square(int P, const uint64_t* x, const uint64_t* a, const uin
     if (eps_out) memcpy(eps_out, eps, (size_t)n * 8);
     free(e); free(eps);
 }
+
+/* ========================================================================
+ * private 2-D convolution with true conv triples
+ * ("we use the same procedure to perform matrix multiplication and
+ * convolution"; §4.2 P:206 "convolutions").
+ * ======================================================================== */
+
+/* Convolution geometry: x (B, C, H, W), w (Cout, C, kh, kw), zero padding
+ * (ph, pw), stride (sh, sw), no dilation, one group; out (B, Cout, Ho, Wo)
+ * with Ho = (H + 2ph − kh)/sh + 1, Wo = (W + 2pw − kw)/sw + 1 (NCHW, the
+ * PyTorch layout CrypTen uses). */
+typedef struct { int64_t B, C, H, W, Cout, kh, kw, sh, sw, ph, pw; } oracle_conv_geom;
+
+static int64_t conv_ho(const oracle_conv_geom* g) { return (g->H + 2 * g->ph - g->kh) / g->sh + 1; }
+static int64_t conv_wo(const oracle_conv_geom* g) { return (g->W + 2 * g->pw - g->kw) / g->sw + 1; }
+
+/* out[b,co,oy,ox] = Σ_{ci,ky,kx} x[b,ci,oy·sh−ph+ky, ox·sw−pw+kx] · w[co,ci,ky,kx] mod Q
+ * (terms outside the input are the zero padding) — the definition, loop by loop. */
+void oracle_conv2d(const uint64_t* x, const uint64_t* w, const oracle_conv_geom* g, uint64_t* out)
+{
+    int64_t Ho = conv_ho(g), Wo = conv_wo(g);
+    for (int64_t b = 0; b < g->B; b++)
+        for (int64_t co = 0; co < g->Cout; co++)
+            for (int64_t oy = 0; oy < Ho; oy++)
+                for (int64_t ox = 0; ox < Wo; ox++) {
+                    uint64_t acc = 0;
+                    for (int64_t ci = 0; ci < g->C; ci++)
+                        for (int64_t ky = 0; ky < g->kh; ky++)
+                            for (int64_t kx = 0; kx < g->kw; kx++) {
+                                int64_t iy = oy * g->sh - g->ph + ky, ix = ox * g->sw - g->pw + kx;
+                                if (iy < 0 || iy >= g->H || ix < 0 || ix >= g->W) continue;
+                                acc += x[((b * g->C + ci) * g->H + iy) * g->W + ix]
+                                     * w[((co * g->C + ci) * g->kh + ky) * g->kw + kx];
+                            }
+                    out[((b * g->Cout + co) * Ho + oy) * Wo + ox] = acc;
+                }
+}
+
+/* ------------------------------------------------------------------------
+ * O13 TTP conv triple (P:589-590 with O4's construction, readings R6, R22):
+ *   a_p = G(k_ttp, A||p||id)[i] over the B·C·H·W input elements,
+ *   b_p = G(k_ttp, B||p||id)[i] over the Cout·C·kh·kw weight elements,
+ *   c = conv(Σ a_p, Σ b_p);  c_p = G(k_ttp, C||p||id)[i] (p ≥ 1), c_0 = c − Σ_{p≥1} c_p.
+ * a: [P][B·C·H·W], b: [P][Cout·C·kh·kw], c: [P][B·Cout·Ho·Wo].
+ * ---------------------------------------------------------------------- */
+void oracle_ttp_conv_triple(int P, uint64_t k_ttp, uint64_t triple_id, const oracle_conv_geom* g,
+                            uint64_t* a, uint64_t* b, uint64_t* c)
+{
+    int64_t na = g->B * g->C * g->H * g->W, nb = g->Cout * g->C * g->kh * g->kw;
+    int64_t nc = g->B * g->Cout * conv_ho(g) * conv_wo(g);
+    for (int p = 0; p < P; p++) {
+        oracle_prg(k_ttp, oracle_stream_id(TAG_A, (uint32_t)p, triple_id), 0, na, a + (int64_t)p * na);
+        oracle_prg(k_ttp, oracle_stream_id(TAG_B, (uint32_t)p, triple_id), 0, nb, b + (int64_t)p * nb);
+    }
+    uint64_t* asum = (uint64_t*)calloc((size_t)(na > 0 ? na : 1), 8);
+    uint64_t* bsum = (uint64_t*)calloc((size_t)(nb > 0 ? nb : 1), 8);
+    oracle_reveal(P, a, na, asum);
+    oracle_reveal(P, b, nb, bsum);
+    oracle_conv2d(asum, bsum, g, c);
+    for (int p = 1; p < P; p++) {
+        uint64_t* cp = c + (int64_t)p * nc;
+        oracle_prg(k_ttp, oracle_stream_id(TAG_C, (uint32_t)p, triple_id), 0, nc, cp);
+        for (int64_t i = 0; i < nc; i++) c[i] -= cp[i];
+    }
+    free(asum); free(bsum);
+}
+
+/* ------------------------------------------------------------------------
+ * O14 Beaver private convolution:
+ *   [ε]_p = [x]_p − [a]_p (input shape), [δ]_p = [y]_p − [b]_p (weight shape);
+ *   ε, δ revealed (one round, at the input / weight shapes — reading R22);
+ *   [z]_p = [c]_p + conv(ε, [b]_p) + conv([a]_p, δ) + [p = 0]·conv(ε, δ).
+ * No truncation (scale 2^(2f)).  eps_out / delta_out may be NULL.
+ * ---------------------------------------------------------------------- */
+void oracle_beaver_conv2d(int P, const uint64_t* x, const uint64_t* y, const uint64_t* a, const uint64_t* b,
+                          const uint64_t* c, const oracle_conv_geom* g, uint64_t* eps_out, uint64_t* delta_out,
+                          uint64_t* z)
+{
+    int64_t na = g->B * g->C * g->H * g->W, nb = g->Cout * g->C * g->kh * g->kw;
+    int64_t nc = g->B * g->Cout * conv_ho(g) * conv_wo(g);
+    uint64_t* e = (uint64_t*)malloc((size_t)(P * (na > 0 ? na : 1)) * 8);
+    uint64_t* d = (uint64_t*)malloc((size_t)(P * (nb > 0 ? nb : 1)) * 8);
+    uint64_t* eps = (uint64_t*)malloc((size_t)(na > 0 ? na : 1) * 8);
+    uint64_t* delta = (uint64_t*)malloc((size_t)(nb > 0 ? nb : 1) * 8);
+    uint64_t* t = (uint64_t*)malloc((size_t)(nc > 0 ? nc : 1) * 8);
+    for (int64_t k = 0; k < (int64_t)P * na; k++) e[k] = x[k] - a[k];
+    for (int64_t k = 0; k < (int64_t)P * nb; k++) d[k] = y[k] - b[k];
+    oracle_reveal(P, e, na, eps);
+    oracle_reveal(P, d, nb, delta);
+    for (int p = 0; p < P; p++) {
+        uint64_t* zp = z + (int64_t)p * nc;
+        for (int64_t i = 0; i < nc; i++) zp[i] = c[(int64_t)p * nc + i];
+        oracle_conv2d(eps, b + (int64_t)p * nb, g, t);                   /* conv(ε, [b]_p) */
+        for (int64_t i = 0; i < nc; i++) zp[i] += t[i];
+        oracle_conv2d(a + (int64_t)p * na, delta, g, t);                 /* conv([a]_p, δ) */
+        for (int64_t i = 0; i < nc; i++) zp[i] += t[i];
+        if (p == 0) {
+            oracle_conv2d(eps, delta, g, t);                             /* conv(ε, δ), party 0 */
+            for (int64_t i = 0; i < nc; i++) zp[i] += t[i];
+        }
+    }
+    if (eps_out) memcpy(eps_out, eps, (size_t)na * 8);
+    if (delta_out) memcpy(delta_out, delta, (size_t)nb * 8);
+    free(e); free(d); free(eps); free(delta); free(t);
+}
