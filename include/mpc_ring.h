@@ -214,6 +214,43 @@ mpc_status mpc_beaver_square_finish(mpc_ctx ctx, const uint64_t* eps, const uint
 mpc_status mpc_reveal_batch(mpc_ctx ctx, int count, const uint64_t* const* shares, uint64_t* const* outs,
                             const int64_t* ns);
 
+/* ---- private 2-D convolution with conv triples ------
+ * P:589-590 ("the same procedure to perform matrix multiplication and
+ * convolution"); R22.  Geometry: input x (B, C, H, W), weights
+ * y (Cout, C, kh, kw), zero padding (ph, pw), stride (sh, sw), no dilation, one
+ * group; output z (B, Cout, Ho, Wo), Ho = (H + 2ph - kh)/sh + 1 (NCHW, row-major).
+ * Per party (or [P][..] on an all-parties context).
+ *
+ * mpc_ttp_conv_triples: a_p = G(k_ttp, A||p||id) over the B*C*H*W input elements,
+ *   b_p = G(k_ttp, B||p||id) over the weight elements, c = conv(sum a_p, sum b_p),
+ *   c_p = G(k_ttp, C||p||id) (p >= 1), c_0 = c - sum_{p>=1} c_p.  Offline.  workspace:
+ *   mpc_ttp_conv_workspace_bytes (rank 0 / all-parties only).
+ * mpc_beaver_conv2d: e_p = x_p - a_p (input shape), d_p = y_p - b_p (weight shape),
+ *   [eps | delta] revealed in ONE round at those shapes (not at the im2col shape);
+ *   z_p = c_p + conv(a_p, delta) + conv(eps, b_p + [p == 0] delta) on the ring GEMM
+ *   with the implicit im2col written straight into limb planes; truncation as in
+ *   mpc_beaver_matmul.  workspace: mpc_conv2d_workspace_bytes.
+ * mpc_beaver_conv2d_finish: the same after the caller's reveal of
+ *   ed = [eps | delta] (na + nb u64, formed by mpc_mask); one-party contexts; local
+ *   truncation only.
+ * mpc_mask: ed = [x - a | y - b] for any n1, n2 (0 rounds).
+ * Errors: MPC_ERR_SHAPE (invalid geometry / workspace), MPC_ERR_ARG (null pointer). */
+typedef struct {
+    int64_t B, C, H, W, Cout, kh, kw, sh, sw, ph, pw;
+} mpc_conv2d_geom;
+size_t mpc_ttp_conv_workspace_bytes(mpc_ctx ctx, const mpc_conv2d_geom* geom);
+mpc_status mpc_ttp_conv_triples(mpc_ctx ctx, uint64_t triple_id, const mpc_conv2d_geom* geom,
+                                uint64_t* a, uint64_t* b, uint64_t* c, void* workspace, size_t workspace_bytes);
+size_t mpc_conv2d_workspace_bytes(mpc_ctx ctx, const mpc_conv2d_geom* geom);
+mpc_status mpc_beaver_conv2d(mpc_ctx ctx, const mpc_conv2d_geom* geom, const uint64_t* x, const uint64_t* y,
+                             const uint64_t* a, const uint64_t* b, const uint64_t* c, uint64_t* z,
+                             int truncate, uint64_t wrap_id, void* workspace, size_t workspace_bytes);
+mpc_status mpc_beaver_conv2d_finish(mpc_ctx ctx, const mpc_conv2d_geom* geom, const uint64_t* ed,
+                                    const uint64_t* a, const uint64_t* b, const uint64_t* c, uint64_t* z,
+                                    int truncate, void* workspace, size_t workspace_bytes);
+mpc_status mpc_mask(mpc_ctx ctx, const uint64_t* x, const uint64_t* a, int64_t n1, const uint64_t* y,
+                    const uint64_t* b, int64_t n2, uint64_t* ed);
+
 /* ---- measurement hooks (bench.py) ----------------------------------------
  * When enabled, the library brackets every launch of kernel class `cls` with CUDA
  * events on the launching stream and accumulates its device time.

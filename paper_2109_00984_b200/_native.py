@@ -10,6 +10,11 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmpc_ring.so")
 
+class ConvGeom(ctypes.Structure):
+    """mpc_conv2d_geom (include/mpc_ring.h)."""
+    _fields_ = [(f, ctypes.c_int64) for f in ("B", "C", "H", "W", "Cout", "kh", "kw", "sh", "sw", "ph", "pw")]
+
+
 # (name, restype, argtypes); P = void*, I = int, L = int64, U = uint64, S = size_t
 _V, _I, _L, _U, _S, _D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_size_t, ctypes.c_double
 SIGNATURES = [
@@ -42,6 +47,12 @@ SIGNATURES = [
     ("mpc_beaver_mul_finish", _I, [_V, _V, _V, _V, _V, _V, _L, _I]),
     ("mpc_beaver_square_finish", _I, [_V, _V, _V, _V, _V, _L, _I]),
     ("mpc_reveal_batch", _I, [_V, _I, ctypes.POINTER(_V), ctypes.POINTER(_V), ctypes.POINTER(_L)]),
+    ("mpc_mask", _I, [_V, _V, _V, _L, _V, _V, _L, _V]),
+    ("mpc_ttp_conv_workspace_bytes", _S, [_V, ctypes.POINTER(ConvGeom)]),
+    ("mpc_ttp_conv_triples", _I, [_V, _U, ctypes.POINTER(ConvGeom), _V, _V, _V, _V, _S]),
+    ("mpc_conv2d_workspace_bytes", _S, [_V, ctypes.POINTER(ConvGeom)]),
+    ("mpc_beaver_conv2d", _I, [_V, ctypes.POINTER(ConvGeom), _V, _V, _V, _V, _V, _V, _I, _U, _V, _S]),
+    ("mpc_beaver_conv2d_finish", _I, [_V, ctypes.POINTER(ConvGeom), _V, _V, _V, _V, _V, _I, _V, _S]),
     ("mpc_profile_enable", _I, [_V, _I]),
     ("mpc_profile_read", _I, [_V, _I, ctypes.POINTER(_D), ctypes.POINTER(_U)]),
     ("mpc_launch_count", _U, [_V]),

@@ -146,9 +146,9 @@ __device__ __forceinline__ void split_left_body(const LeftSplitArgs& a, int64_t 
         const int64_t kleft = a.K - k0;                     // <= 0: pure K padding
         const bool full = kleft >= 16;
         uint64_t acc[16], v[16];
-        if (a.Psum > 0) {
 #pragma unroll
-            for (int m = 0; m < 16; ++m) acc[m] = 0;
+        for (int m = 0; m < 16; ++m) acc[m] = 0;
+        if (a.Psum > 0) {
             for (int p = 0; p < a.Psum; ++p) {
                 load16(a.plus + p * a.party_stride + row * a.K + k0, full, vec, kleft, v);
 #pragma unroll
@@ -157,16 +157,22 @@ __device__ __forceinline__ void split_left_body(const LeftSplitArgs& a, int64_t 
                     load16(a.minus + p * a.party_stride + row * a.K + k0, full, vec, kleft, v);
 #pragma unroll
                     for (int m = 0; m < 16; ++m) acc[m] -= v[m];
-                    if (fused_copy) store_limbs16<LO>(a.cp_planes + p * a.cp_planes_stride, row, k0, KB, v);
+                    // party 0's copy needs the complete sum first (add_sum_first): written below
+                    if (fused_copy && !(p == 0 && a.add_sum_first))
+                        store_limbs16<LO>(a.cp_planes + p * a.cp_planes_stride, row, k0, KB, v);
                 }
             }
             store_limbs16<LO>(a.sum_planes, row, k0, KB, acc);
         }
-        if (!fused_copy) {
-            for (int q = 0; q < a.Pcopy; ++q) {
-                load16(a.cp_src + q * a.party_stride + row * a.K + k0, full, vec, kleft, v);
-                store_limbs16<LO>(a.cp_planes + q * a.cp_planes_stride, row, k0, KB, v);
+        for (int q = 0; q < a.Pcopy; ++q) {
+            const bool adds = q == 0 && a.add_sum_first;
+            if (fused_copy && !adds) continue;             // already written from registers
+            load16(a.cp_src + q * a.party_stride + row * a.K + k0, full, vec, kleft, v);
+            if (adds) {
+#pragma unroll
+                for (int m = 0; m < 16; ++m) v[m] += acc[m];
             }
+            store_limbs16<LO>(a.cp_planes + q * a.cp_planes_stride, row, k0, KB, v);
         }
     }
 }

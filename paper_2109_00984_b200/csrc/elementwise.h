@@ -20,6 +20,8 @@ struct LeftSplitArgs {
     uint8_t* cp_planes;
     int64_t cp_planes_stride;        // bytes
     int swap;                        // 1: planes in Layout::Right (transposed ring GEMM), else Layout::Left
+    int add_sum_first;               // copy of party 0 gets + the sum (b'_0 = b_0 + delta, R8), for weights
+                                     // given rows x K (conv: Cout x C*kh*kw)
 };
 
 struct RightSplitArgs {

@@ -16,6 +16,7 @@
 #include "../../include/mpc_ring.h"
 #include "common.cuh"
 #include "beaver_elementwise.h"
+#include "conv.h"
 #include "elementwise.h"
 #include "ring_gemm.h"
 
@@ -149,11 +150,16 @@ struct BeaverWs {
     size_t total;
 };
 
-BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N) {
+// ed_elems: size of the one-party [e | d] reveal buffer (default M*K + K*N; a
+// convolution reveals at the input / weight shapes instead).  allow_swap: the
+// transposed GEMM is possible for this output layout.
+BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N, int64_t ed_elems = -1,
+                      bool allow_swap = true) {
     const int Pl = c->all ? c->P : 1;
     Carve cv(ws);
     BeaverWs w{};
-    w.swap = use_swap(M, N);
+    w.swap = allow_swap && use_swap(M, N);
+    if (ed_elems < 0) ed_elems = M * K + K * N;
     const int64_t xs = w.swap ? rp(M, K) : lp(M, K);     // eps, a_p planes (rows = M)
     const int64_t ys = w.swap ? lp(N, K) : rp(N, K);     // delta, b'_p planes (rows = N)
     const int64_t gM = w.swap ? N : M, gN = w.swap ? M : N;   // the GEMM's own output sizes
@@ -163,7 +169,7 @@ BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N) {
     w.delta_pl = cv.take(ys);
     w.a_pl = cv.take((size_t)Pl * xs);
     w.b_pl = cv.take((size_t)Pl * ys);
-    w.ed = reinterpret_cast<uint64_t*>(c->all ? nullptr : cv.take(8 * (size_t)(M * K + K * N)));
+    w.ed = reinterpret_cast<uint64_t*>(c->all ? nullptr : cv.take(8 * (size_t)ed_elems));
     const bool alg1_one = !c->all && c->P > 2;
     w.zbuf = reinterpret_cast<uint64_t*>(alg1_one ? cv.take(8 * (size_t)(M * N)) : nullptr);
     w.hbuf = reinterpret_cast<int8_t*>(alg1_one ? cv.take((size_t)(M * N)) : nullptr);
@@ -760,6 +766,170 @@ mpc_status mpc_reveal_batch(mpc_ctx c, int count, const uint64_t* const* shares,
         return fail(c, MPC_ERR_NCCL, "reveal_batch: %s", ncclGetErrorString(r));
     }
     return MPC_OK;
+}
+
+// ---------------------------------------------------------------- private 2-D convolution
+// (R22)
+mpc_status mpc_mask(mpc_ctx c, const uint64_t* x, const uint64_t* a, int64_t n1, const uint64_t* y,
+                    const uint64_t* b, int64_t n2, uint64_t* ed) {
+    CHECK(enter(c));
+    if (n1 < 0 || n2 < 0) return fail(c, MPC_ERR_SHAPE, "mask: negative size");
+    if (n1 + n2 == 0) return MPC_OK;
+    if ((n1 && (!x || !a)) || (n2 && (!y || !b)) || !ed) return fail(c, MPC_ERR_ARG, "mask: null pointer");
+    return run(c, kClsSplit, "mask", [&] { return launch_mask(x, a, n1, y, b, n2, ed, c->stream); });
+}
+
+}  // extern "C"
+
+namespace {
+bool conv_geom_ok(const mpc_conv2d_geom* g) {
+    return g && g->B >= 0 && g->C >= 0 && g->H >= 0 && g->W >= 0 && g->Cout >= 0 && g->kh >= 1 && g->kw >= 1 &&
+           g->sh >= 1 && g->sw >= 1 && g->ph >= 0 && g->pw >= 0 && g->H + 2 * g->ph >= g->kh &&
+           g->W + 2 * g->pw >= g->kw && g->C * g->kh * g->kw < ((int64_t)1 << 30);
+}
+ConvGeom to_geom(const mpc_conv2d_geom* g) {
+    return ConvGeom{g->B, g->C, g->H, g->W, g->Cout, g->kh, g->kw, g->sh, g->sw, g->ph, g->pw};
+}
+// Transposed GEMM (Cout rows x pixel columns) only for one image: its row-major
+// output is then exactly NCHW.
+BeaverWs carve_conv(mpc_ctx c, void* ws, const ConvGeom& g) {
+    return carve_beaver(c, ws, g.M(), g.K(), g.Cout, g.in_elems() + g.w_elems(), g.B == 1);
+}
+// GEMM output mapping of a convolution: NCHW z from im2col rows (b, pixel).
+void conv_out(RingGemmParams& p, const BeaverWs& w, const ConvGeom& g) {
+    if (w.swap) { p.M = g.Cout; p.N = g.M(); }                 // (Cout x Ho*Wo) row-major = NCHW, B = 1
+    else { p.M = g.M(); p.N = g.Cout; p.out_hw = g.Ho() * g.Wo(); }
+    p.party_stride_c = p.party_stride_z = g.out_elems();
+}
+// x-side: implicit im2col of activation-shaped operands; y-side: weights (Cout x K rows)
+mpc_status conv_split(mpc_ctx c, const BeaverWs& w, const ConvGeom& g, const uint64_t* xp, const uint64_t* xm,
+                      int Psum, int64_t xstride, const uint64_t* acp, int Pcopy, const uint64_t* yp,
+                      const uint64_t* ym, int64_t ystride, const uint64_t* bcp, int add_first) {
+    Im2colSplitArgs I{g, xstride, xp, xm, Psum, w.eps_pl, acp, Pcopy, w.a_pl, w.a_stride, w.swap ? 1 : 0};
+    CHECK(run(c, kClsSplit, "split im2col", [&] { return launch_split_im2col(I, c->stream); }));
+    LeftSplitArgs Wt{g.Cout, g.K(), ystride, yp, ym, Psum, w.delta_pl, bcp, Pcopy, w.b_pl, w.b_stride,
+                     w.swap ? 0 : 1, add_first};
+    return run(c, kClsSplit, "split weights", [&] { return launch_split_left(Wt, c->stream); });
+}
+mpc_status conv_gemm(mpc_ctx c, const BeaverWs& w, const ConvGeom& g, const uint64_t* cc, uint64_t* z, int truncate,
+                     int parties) {
+    const int kb = (int)num_kb(g.K());
+    RingGemmParams p{};
+    p.seg[0] = seg_of(w, w.a_pl, w.a_stride, w.delta_pl, 0, kb);     // conv(a_p, delta)
+    p.seg[1] = seg_of(w, w.eps_pl, 0, w.b_pl, w.b_stride, kb);       // conv(eps, b_p + [p = 0] delta)
+    p.nseg = 2;
+    p.partials = w.partials;
+    conv_out(p, w, g);
+    p.C = cc; p.Z = z;
+    p.trunc_bits = (truncate && c->P <= 2) ? c->frac : 0;
+    return gemm_run(c, p, parties);
+}
+}  // namespace
+
+extern "C" {
+
+size_t mpc_conv2d_workspace_bytes(mpc_ctx c, const mpc_conv2d_geom* gg) {
+    if (!c || !conv_geom_ok(gg)) return 0;
+    return carve_conv(c, nullptr, to_geom(gg)).total;
+}
+
+mpc_status mpc_beaver_conv2d(mpc_ctx c, const mpc_conv2d_geom* gg, const uint64_t* x, const uint64_t* y,
+                             const uint64_t* a, const uint64_t* b, const uint64_t* cc, uint64_t* z, int truncate,
+                             uint64_t wrap_id, void* ws, size_t ws_bytes) {
+    CHECK(enter(c));
+    if (!conv_geom_ok(gg)) return fail(c, MPC_ERR_SHAPE, "beaver_conv2d: invalid geometry");
+    const ConvGeom g = to_geom(gg);
+    const BeaverWs w = carve_conv(c, ws, g);
+    if (ws_bytes < w.total) return fail(c, MPC_ERR_SHAPE, "beaver_conv2d: workspace %zu < %zu", ws_bytes, w.total);
+    const int Pl = c->all ? c->P : 1;
+    const int64_t na = g.in_elems(), nb = g.w_elems(), nz = g.out_elems();
+    c->rounds += 1;                                   // eps || delta at the input / weight shapes, one round
+    c->bytes += 8ull * (uint64_t)(na + nb) * Pl;
+    if (nz == 0) return MPC_OK;
+    if ((na && (!x || !a)) || (nb && (!y || !b)) || !cc || !z || (!ws && w.total))
+        return fail(c, MPC_ERR_ARG, "beaver_conv2d: null pointer");
+    if (c->all) {
+        CHECK(conv_split(c, w, g, x, a, c->P, na, a, c->P, y, b, nb, b, 1));
+    } else {
+        CHECK(run(c, kClsSplit, "mask", [&] { return launch_mask(x, a, na, y, b, nb, w.ed, c->stream); }));
+        if (c->P > 1) CHECK(nccl_allreduce(c, w.ed, w.ed, (size_t)(na + nb), ncclUint64, "eps/delta reveal"));
+        CHECK(conv_split(c, w, g, w.ed, nullptr, 1, 0, a, 1, w.ed + na, nullptr, 0, b, c->rank == 0));
+    }
+    CHECK(conv_gemm(c, w, g, cc, z, truncate, Pl));
+    if (truncate && c->P > 2) CHECK(truncate_impl(c, z, nz, c->frac, wrap_id, w.zbuf, w.hbuf));
+    return MPC_OK;
+}
+
+mpc_status mpc_beaver_conv2d_finish(mpc_ctx c, const mpc_conv2d_geom* gg, const uint64_t* ed, const uint64_t* a,
+                                    const uint64_t* b, const uint64_t* cc, uint64_t* z, int truncate, void* ws,
+                                    size_t ws_bytes) {
+    CHECK(enter(c));
+    if (c->all) return fail(c, MPC_ERR_UNSUPPORTED, "beaver_conv2d_finish: one-party contexts only");
+    if (truncate && c->P > 2) return fail(c, MPC_ERR_UNSUPPORTED, "beaver_conv2d_finish: P > 2 truncation needs mpc_truncate");
+    if (!conv_geom_ok(gg)) return fail(c, MPC_ERR_SHAPE, "beaver_conv2d_finish: invalid geometry");
+    const ConvGeom g = to_geom(gg);
+    const BeaverWs w = carve_conv(c, ws, g);
+    if (ws_bytes < w.total) return fail(c, MPC_ERR_SHAPE, "beaver_conv2d_finish: workspace %zu < %zu", ws_bytes, w.total);
+    const int64_t na = g.in_elems(), nb = g.w_elems();
+    c->rounds += 1;
+    c->bytes += 8ull * (uint64_t)(na + nb);
+    if (g.out_elems() == 0) return MPC_OK;
+    if (!ed || (na && !a) || (nb && !b) || !cc || !z || (!ws && w.total))
+        return fail(c, MPC_ERR_ARG, "beaver_conv2d_finish: null pointer");
+    CHECK(conv_split(c, w, g, ed, nullptr, 1, 0, a, 1, ed + na, nullptr, 0, b, c->rank == 0));
+    return conv_gemm(c, w, g, cc, z, truncate, 1);
+}
+
+size_t mpc_ttp_conv_workspace_bytes(mpc_ctx c, const mpc_conv2d_geom* gg) {
+    if (!c || !conv_geom_ok(gg)) return 0;
+    const ConvGeom g = to_geom(gg);
+    // the TTP's sums of a_p, b_p, their planes (normal GEMM orientation) and split-K slabs
+    return align256(8 * (size_t)g.in_elems()) + align256(8 * (size_t)g.w_elems()) + align256(lp(g.M(), g.K())) +
+           align256(rp(g.Cout, g.K())) + align256(ring_gemm_partials_bytes(1, g.M(), g.Cout, (int)num_kb(g.K())));
+}
+
+mpc_status mpc_ttp_conv_triples(mpc_ctx c, uint64_t id, const mpc_conv2d_geom* gg, uint64_t* a, uint64_t* b,
+                                uint64_t* cc, void* ws, size_t ws_bytes) {
+    CHECK(enter(c));
+    if (!conv_geom_ok(gg)) return fail(c, MPC_ERR_SHAPE, "ttp_conv_triples: invalid geometry");
+    const ConvGeom g = to_geom(gg);
+    const int64_t na = g.in_elems(), nb = g.w_elems(), nz = g.out_elems();
+    if ((na && !a) || (nb && !b) || (nz && !cc)) return fail(c, MPC_ERR_ARG, "ttp_conv_triples: null output");
+    const bool ttp = c->all || c->rank == 0;
+    if (ttp && ws_bytes < mpc_ttp_conv_workspace_bytes(c, gg)) return fail(c, MPC_ERR_SHAPE, "ttp_conv_triples: workspace too small");
+    if (ttp && !ws && nz) return fail(c, MPC_ERR_ARG, "ttp_conv_triples: null workspace");
+    const int lo = c->all ? 0 : c->rank, hi = c->all ? c->P : c->rank + 1;
+    Carve cv(ws);
+    uint64_t* asum = ttp ? reinterpret_cast<uint64_t*>(cv.take(8 * (size_t)na)) : nullptr;
+    uint64_t* bsum = ttp ? reinterpret_cast<uint64_t*>(cv.take(8 * (size_t)nb)) : nullptr;
+    uint8_t* a_pl = ttp ? cv.take(lp(g.M(), g.K())) : nullptr;
+    uint8_t* b_pl = ttp ? cv.take(rp(g.Cout, g.K())) : nullptr;
+    const size_t pb = ring_gemm_partials_bytes(1, g.M(), g.Cout, (int)num_kb(g.K()));
+    uint64_t* partials = reinterpret_cast<uint64_t*>(ttp && pb ? cv.take(pb) : nullptr);
+    CHECK(run(c, kClsPrg, "ttp_conv_a", [&] {
+        return launch_prg_parties(c->kttp, kTagA, id, c->P, lo, hi, a, asum, na, c->stream); }));
+    CHECK(run(c, kClsPrg, "ttp_conv_b", [&] {
+        return launch_prg_parties(c->kttp, kTagB, id, c->P, lo, hi, b, bsum, nb, c->stream); }));
+    if (nz == 0) return MPC_OK;
+    if (ttp) {
+        // c = conv(sum a, sum b) into party 0's c slot, on the tensor cores
+        Im2colSplitArgs I{g, 0, asum, nullptr, 1, a_pl, nullptr, 0, nullptr, 0, 0};
+        CHECK(run(c, kClsSplit, "ttp split im2col", [&] { return launch_split_im2col(I, c->stream); }));
+        LeftSplitArgs Wt{g.Cout, g.K(), 0, bsum, nullptr, 1, b_pl, nullptr, 0, nullptr, 0, 1, 0};
+        CHECK(run(c, kClsSplit, "ttp split weights", [&] { return launch_split_left(Wt, c->stream); }));
+        RingGemmParams p{};
+        p.seg[0] = RingGemmSegment{a_pl, b_pl, (int)num_kb(g.K()), 0, 0};
+        p.nseg = 1;
+        p.M = g.M(); p.N = g.Cout; p.out_hw = g.Ho() * g.Wo();
+        p.C = nullptr; p.Z = cc;
+        p.partials = partials;
+        CHECK(gemm_run(c, p, 1));
+    }
+    uint64_t* c_out = c->all ? cc + nz : cc;    // parties >= 1
+    const int out_lo = c->all ? 1 : c->rank, out_hi = c->all ? c->P : (c->rank == 0 ? 0 : c->rank + 1);
+    return run(c, kClsPrg, "ttp_c", [&] {
+        return launch_ttp_c(c->kttp, id, c->P, out_lo, out_hi, c_out, ttp ? cc : nullptr, nz, c->stream);
+    });
 }
 
 mpc_status mpc_profile_enable(mpc_ctx c, int enable) {

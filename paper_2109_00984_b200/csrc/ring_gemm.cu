@@ -448,13 +448,15 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Wor
         // tile end: z = trunc(c + sum of all units) — one write per element.
         // Element (grow, gc) of the GEMM's output sits at base + gc * cs: row-major
         // normally; column-major (i.e. the caller's row-major z, with the GEMM
-        // computing z^T) when transpose_out is set — then the 32 lanes of a warp
-        // (32 consecutive rows) touch 256 contiguous bytes per column.
+        // computing z^T) when transpose_out is set, and per-image column-major
+        // (NCHW conv output) with out_hw — then the 32 lanes of a warp (32
+        // consecutive rows) touch up to 256 contiguous bytes per column.
         const int64_t grow = (int64_t)m * kTileM + rank * 128 + row;
         const int64_t gc0 = (int64_t)n * kTileN + half * 64;
-        const bool tr = p.transpose_out != 0;
-        const int64_t cs = tr ? p.M : 1;
-        const int64_t off = (tr ? grow : grow * p.N) + gc0 * cs;
+        const int64_t hw = p.out_hw > 0 ? p.out_hw : (p.transpose_out ? p.M : 0);
+        const bool tr = hw > 0;
+        const int64_t cs = tr ? hw : 1;
+        const int64_t off = (tr ? (grow / hw) * p.N * hw + grow % hw : grow * p.N) + gc0 * cs;
         const bool full = !tr && vec && gc0 + 64 <= p.N;
         if (grow < p.M && wm.splits > 1) {
             // split-K: store this K range's partial sum in its own slab of the

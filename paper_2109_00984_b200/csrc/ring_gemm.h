@@ -34,6 +34,9 @@ struct RingGemmParams {
     int transpose_out;                  // 1: the GEMM computes Z^T (M, N are its own sizes, i.e. the
                                         // caller's N, M); element (m, n) is stored at Z[n * M + m] (and
                                         // C is read there).  Used for small caller M (fewer padded rows).
+    int64_t out_hw;                     // > 0 (overrides transpose_out): row m = b * out_hw + s of the GEMM
+                                        // goes to Z[(b * N + n) * out_hw + s] — the NCHW output of a
+                                        // convolution whose im2col rows are (b, pixel s).  C likewise.
 };
 
 // Largest unit length (32-K blocks) for which every s32 accumulator stays exact.

@@ -269,6 +269,56 @@ class Context:
         self._call(self._lib.mpc_reveal_batch, cnt, sp, op, ns)
         return outs
 
+    # ------------------------------------------------------------ conv2d
+    @staticmethod
+    def conv_geom(B, C, H, W, Cout, kh, kw, stride=1, padding=0):
+        """Geometry of x (B,C,H,W) * w (Cout,C,kh,kw), zero padding, stride; output (B,Cout,Ho,Wo)."""
+        sh, sw = (stride, stride) if isinstance(stride, int) else stride
+        ph, pw = (padding, padding) if isinstance(padding, int) else padding
+        return _native.ConvGeom(B, C, H, W, Cout, kh, kw, sh, sw, ph, pw)
+
+    @staticmethod
+    def conv_out_shape(g):
+        return (g.B, g.Cout, (g.H + 2 * g.ph - g.kh) // g.sh + 1, (g.W + 2 * g.pw - g.kw) // g.sw + 1)
+
+    def ttp_conv_triples(self, triple_id: int, g):
+        """Conv Beaver triple: a (input shape), b (weight shape), c = conv(a, b) (output shape)."""
+        a = _u64(self._lead() + (g.B, g.C, g.H, g.W), self.device)
+        b = _u64(self._lead() + (g.Cout, g.C, g.kh, g.kw), self.device)
+        c = _u64(self._lead() + self.conv_out_shape(g), self.device)
+        nb = self._lib.mpc_ttp_conv_workspace_bytes(self._h, ctypes.byref(g))
+        ws = self._workspace(nb)
+        self._call(self._lib.mpc_ttp_conv_triples, ctypes.c_uint64(triple_id), ctypes.byref(g), _ptr(a), _ptr(b),
+                   _ptr(c), _ptr(ws), ctypes.c_size_t(ws.numel()))
+        return a, b, c
+
+    def beaver_conv2d(self, g, x, y, a, b, c, truncate: bool = True, wrap_id: int = 0,
+                      out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Private convolution [conv(x, y)] (one round at the input/weight shapes; + Alg. 1's if P > 2)."""
+        shp = self._lead() + self.conv_out_shape(g)
+        z = _u64(shp, self.device) if out is None else _check_out(out, shp, torch.uint64)
+        ws = self._workspace(int(self._lib.mpc_conv2d_workspace_bytes(self._h, ctypes.byref(g))))
+        self._call(self._lib.mpc_beaver_conv2d, ctypes.byref(g), _ptr(x), _ptr(y), _ptr(a), _ptr(b), _ptr(c), _ptr(z),
+                   int(bool(truncate)), ctypes.c_uint64(wrap_id), _ptr(ws), ctypes.c_size_t(ws.numel()))
+        return z
+
+    def beaver_conv2d_finish(self, g, ed, a, b, c, truncate: bool = True) -> torch.Tensor:
+        """One-party context: z_p from the revealed [eps | delta] (see mpc_beaver_conv2d_finish)."""
+        z = _u64(self.conv_out_shape(g), self.device)
+        ws = self._workspace(int(self._lib.mpc_conv2d_workspace_bytes(self._h, ctypes.byref(g))))
+        self._call(self._lib.mpc_beaver_conv2d_finish, ctypes.byref(g), _ptr(ed), _ptr(a), _ptr(b), _ptr(c), _ptr(z),
+                   int(bool(truncate)), _ptr(ws), ctypes.c_size_t(ws.numel()))
+        return z
+
+    def mask(self, x, a, y=None, b=None) -> torch.Tensor:
+        """[x - a | y - b] as one flat buffer (0 rounds)."""
+        n1 = x.numel()
+        n2 = y.numel() if y is not None else 0
+        ed = _u64((n1 + n2,), self.device)
+        self._call(self._lib.mpc_mask, _ptr(x), _ptr(a), ctypes.c_int64(n1), _ptr(y), _ptr(b), ctypes.c_int64(n2),
+                   _ptr(ed))
+        return ed
+
     def truncate(self, x: torch.Tensor, bits: Optional[int] = None, wrap_id: int = 0) -> torch.Tensor:
         """In place; returns x."""
         n = x[0].numel() if self.all_parties else x.numel()
