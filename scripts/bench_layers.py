@@ -6,7 +6,8 @@ the layer time spent in the tcgen05 GEMM.  --chain captures every layer of a
 model (each repeated `count` times, in order) in ONE CUDA graph and times the
 whole chain, as a private inference would run them back to back.
 
-  python scripts/bench_layers.py [--model resnet50|vit|resnet18|wav2letter|all] [--reps 20] [--graph] [--chain]
+  python scripts/bench_layers.py [--model resnet50|vit|resnet18|wav2letter|text|all] [--reps 20]
+                                 [--graph] [--chain] [--conv]
 """
 import argparse
 import json
@@ -119,18 +120,75 @@ def t_gemm_ms(M, K, N, parties=2):
     return 144.0 * M * N * K * parties / (int8_peak_tops() * 1e12) * 1e3
 
 
+def run_conv_chain(ctx, layers, reps):
+    """All convolutions of one model as TRUE private convolutions (conv triples,
+    eps/delta revealed at the input/weight shapes) in one CUDA graph."""
+    dev = torch.device("cuda", 0)
+    bufs, reveal_bytes = [], 0
+    for i, (_, C, H, W, Co, k, st, pd, count) in enumerate(layers):
+        g = ctx.conv_geom(1, C, H, W, Co, k, k, st, pd)
+        X = synth.gaussian_fixed((1, C, H, W), 100 + i, 1.0, 0, 8, absval=True)
+        Y = synth.gaussian_fixed((Co, C, k, k), 200 + i, (2.0 / (C * k * k)) ** 0.5, -8, 8)
+        x = ctx.share(torch.from_numpy(X.view(np.int64)).to(dev).view(torch.uint64), 0, 1 + 2 * i)
+        y = ctx.share(torch.from_numpy(Y.view(np.int64)).to(dev).view(torch.uint64), 1, 2 + 2 * i)
+        a, b, c = ctx.ttp_conv_triples(1 + i, g)
+        bufs.append((g, x, y, a, b, c, torch.empty_like(c), count))
+        reveal_bytes += 8 * (X.size + Y.size) * count
+
+    def chain():
+        for g, x, y, a, b, c, z, count in bufs:
+            for _ in range(count):
+                ctx.beaver_conv2d(g, x, y, a, b, c, truncate=True, out=z)
+
+    chain()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        chain()
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=s):
+            chain()
+    for _ in range(3):
+        gr.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(reps):
+        gr.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps, reveal_bytes
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="all", choices=list(synth.MODELS) + ["all"])
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--graph", action="store_true")
     ap.add_argument("--chain", action="store_true")
+    ap.add_argument("--conv", action="store_true", help="true private convolutions (conv triples) for CNNs")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     ctx = mpc.Context(2, mpc.ALL_PARTIES, device=0, master_seed=synth.MASTER_SEED)
     out = {}
     for name, layers in synth.MODELS.items():
         if args.model not in (name, "all"):
+            continue
+        if args.conv:
+            if name not in synth.CONV_MODELS:
+                continue
+            ms, rb = run_conv_chain(ctx, synth.CONV_MODELS[name], args.reps)
+            ops = sum(2.0 * M * K * N * cnt for _, M, K, N, cnt in layers)
+            tg = sum(t_gemm_ms(M, K, N) * cnt for _, M, K, N, cnt in layers)
+            n = sum(cnt for *_, cnt in layers)
+            rb_im2col = sum(8 * (M * K + K * N) * cnt for _, M, K, N, cnt in layers)
+            out[name + "_conv"] = {"chain_ms": ms, "private_convs": n, "ring_TOPS": ops / (ms * 1e-3) / 1e12,
+                                   "roofline_ms": tg, "roofline_frac": tg / ms, "reveal_MB_per_party": rb / 1e6,
+                                   "reveal_MB_im2col_shape": rb_im2col / 1e6, "graph": "one CUDA graph per model"}
+            print(f"{name} (true convs): chain of {n} private convolutions {ms:.3f} ms "
+                  f"({out[name + '_conv']['ring_TOPS']:.2f} ring-TOPS), reveal {rb / 1e6:.0f} MB/party "
+                  f"(im2col-shape reveal would be {rb_im2col / 1e6:.0f} MB)", flush=True)
             continue
         if args.chain:
             ms = run_chain(ctx, layers, args.reps)

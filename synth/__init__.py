@@ -81,6 +81,38 @@ WAV2LETTER_B1 = [
     ("conv10", 51, 8000, 2000, 1), ("conv11", 51, 2000, 2000, 1), ("conv12", 51, 2000, 29, 1),
 ]
 
+# The same networks as true convolutions: (name, C, H, W, Cout,
+# k, stride, pad, count), batch 1, torchvision ResNet v1.5 (stride in the 3x3 conv);
+# the fc layer is a 1x1 convolution on a 1x1 map.  Same GEMM shapes as the lists above.
+RESNET50_CONV_B1 = [
+    ("conv1", 3, 224, 224, 64, 7, 2, 3, 1),
+    ("l1.b1.c1", 64, 56, 56, 64, 1, 1, 0, 1), ("l1.c2", 64, 56, 56, 64, 3, 1, 1, 3),
+    ("l1.c3", 64, 56, 56, 256, 1, 1, 0, 3), ("l1.ds", 64, 56, 56, 256, 1, 1, 0, 1),
+    ("l1.c1", 256, 56, 56, 64, 1, 1, 0, 2),
+    ("l2.b1.c1", 256, 56, 56, 128, 1, 1, 0, 1), ("l2.b1.c2", 128, 56, 56, 128, 3, 2, 1, 1),
+    ("l2.c3", 128, 28, 28, 512, 1, 1, 0, 4), ("l2.ds", 256, 56, 56, 512, 1, 2, 0, 1),
+    ("l2.c1", 512, 28, 28, 128, 1, 1, 0, 3), ("l2.c2", 128, 28, 28, 128, 3, 1, 1, 3),
+    ("l3.b1.c1", 512, 28, 28, 256, 1, 1, 0, 1), ("l3.b1.c2", 256, 28, 28, 256, 3, 2, 1, 1),
+    ("l3.c3", 256, 14, 14, 1024, 1, 1, 0, 6), ("l3.ds", 512, 28, 28, 1024, 1, 2, 0, 1),
+    ("l3.c1", 1024, 14, 14, 256, 1, 1, 0, 5), ("l3.c2", 256, 14, 14, 256, 3, 1, 1, 5),
+    ("l4.b1.c1", 1024, 14, 14, 512, 1, 1, 0, 1), ("l4.b1.c2", 512, 14, 14, 512, 3, 2, 1, 1),
+    ("l4.c3", 512, 7, 7, 2048, 1, 1, 0, 3), ("l4.ds", 1024, 14, 14, 2048, 1, 2, 0, 1),
+    ("l4.c1", 2048, 7, 7, 512, 1, 1, 0, 2), ("l4.c2", 512, 7, 7, 512, 3, 1, 1, 2),
+    ("fc", 2048, 1, 1, 1000, 1, 1, 0, 1),
+]
+RESNET18_CONV_B1 = [
+    ("conv1", 3, 224, 224, 64, 7, 2, 3, 1),
+    ("l1.c", 64, 56, 56, 64, 3, 1, 1, 4),
+    ("l2.b1.c1", 64, 56, 56, 128, 3, 2, 1, 1), ("l2.c", 128, 28, 28, 128, 3, 1, 1, 3),
+    ("l2.ds", 64, 56, 56, 128, 1, 2, 0, 1),
+    ("l3.b1.c1", 128, 28, 28, 256, 3, 2, 1, 1), ("l3.c", 256, 14, 14, 256, 3, 1, 1, 3),
+    ("l3.ds", 128, 28, 28, 256, 1, 2, 0, 1),
+    ("l4.b1.c1", 256, 14, 14, 512, 3, 2, 1, 1), ("l4.c", 512, 7, 7, 512, 3, 1, 1, 3),
+    ("l4.ds", 256, 14, 14, 512, 1, 2, 0, 1),
+    ("fc", 512, 1, 1, 1000, 1, 1, 0, 1),
+]
+CONV_MODELS = {"resnet50": RESNET50_CONV_B1, "resnet18": RESNET18_CONV_B1}
+
 # Text classification: the embedding applied as a
 # dense matmul of 32 one-hot tokens x vocabulary 519,820 x embedding 32 — a wide
 # reduction (K >> 16512, the per-unit exactness bound) at tiny M and N.
