@@ -34,6 +34,10 @@ struct Im2colSplitArgs {
     int layout_right;                // planes in Layout::Right (transposed GEMM) instead of Layout::Left
 };
 cudaError_t launch_split_im2col(const Im2colSplitArgs& a, cudaStream_t st);
+// im2col split of the activation side and the weights split (elementwise.h LeftSplitArgs) in one
+// launch; they must target opposite plane layouts (one left, one right GEMM operand).
+struct LeftSplitArgs;
+cudaError_t launch_split_conv(const Im2colSplitArgs& im, const LeftSplitArgs& wt, cudaStream_t st);
 
 // out_sum[i] = sum_{p<P} G(key, tag||p||id)[i]; parties [lo, hi) also written to out ([hi-lo][n]).
 // Either output may be null.

@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "common.cuh"
+#include "conv.h"
 #include "elementwise.h"
 
 namespace mpc {
@@ -317,6 +318,109 @@ cudaError_t launch_split_both(const LeftSplitArgs& l, const RightSplitArgs& r, c
                           l, r, (int)nl);
     return launch_pdl(split_both_kernel<Layout::Left, Layout::Right>, dim3((unsigned)(nl + nr)), dim3(256), 0, st, l,
                       r, (int)nl);
+}
+
+// ------------------------------------------------------------------ conv: implicit im2col split
+// A warp covers 32 consecutive im2col rows (lane = row, i.e. 32 neighbouring
+// output pixels: the gathers of one K index are nearly contiguous) and one
+// 16-K chunk; each lane gathers its 16 (ci, ky, kx) values per party and
+// writes 16 bytes per limb plane.  The K padding (K .. 32*KB) is written as 0.
+template <Layout LO>
+__device__ __forceinline__ void split_im2col_body(const Im2colSplitArgs& a, int64_t bid, int64_t nblk) {
+    const ConvGeom& g = a.g;
+    const int64_t Ho = g.Ho(), Wo = g.Wo(), M = g.M(), K = g.K(), KB = num_kb(K);
+    const int64_t khw = g.kh * g.kw;
+    const int64_t rgroups = (M + 31) / 32, kchunks = KB * 2;
+    const int lane = threadIdx.x & 31;
+    const bool fused_copy = a.cp_src == a.minus && a.Pcopy == a.Psum && a.Psum > 0;
+    for (int64_t w = (bid * blockDim.x + threadIdx.x) >> 5; w < rgroups * kchunks; w += (nblk * blockDim.x) >> 5) {
+        const int64_t kc = w / rgroups, rg = w % rgroups;     // neighbouring warps: neighbouring rows
+        const int64_t row = rg * 32 + lane;
+        if (row >= M) continue;
+        const int64_t k0 = kc * 16;
+        const int64_t b = row / (Ho * Wo), s = row % (Ho * Wo);
+        const int64_t oy = s / Wo, ox = s % Wo;
+        int64_t off[16];                                        // element offset in one party's tensor, or -1
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const int64_t k = k0 + m;
+            off[m] = -1;
+            if (k < K) {
+                const int64_t ci = k / khw, r = k % khw;
+                const int64_t iy = oy * g.sh - g.ph + r / g.kw, ix = ox * g.sw - g.pw + r % g.kw;
+                if (iy >= 0 && iy < g.H && ix >= 0 && ix < g.W) off[m] = ((b * g.C + ci) * g.H + iy) * g.W + ix;
+            }
+        }
+        uint64_t acc[16], v[16];
+#pragma unroll
+        for (int m = 0; m < 16; ++m) acc[m] = 0;
+        for (int p = 0; p < a.Psum; ++p) {
+            const uint64_t* src = a.plus + p * a.party_stride;
+#pragma unroll
+            for (int m = 0; m < 16; ++m) v[m] = off[m] >= 0 ? __ldg(src + off[m]) : 0ull;
+#pragma unroll
+            for (int m = 0; m < 16; ++m) acc[m] += v[m];
+            if (a.minus) {
+                const uint64_t* sm = a.minus + p * a.party_stride;
+#pragma unroll
+                for (int m = 0; m < 16; ++m) v[m] = off[m] >= 0 ? __ldg(sm + off[m]) : 0ull;
+#pragma unroll
+                for (int m = 0; m < 16; ++m) acc[m] -= v[m];
+                if (fused_copy) store_limbs16<LO>(a.cp_planes + p * a.cp_planes_stride, row, k0, KB, v);
+            }
+        }
+        if (a.Psum > 0) store_limbs16<LO>(a.sum_planes, row, k0, KB, acc);
+        if (!fused_copy) {
+            for (int q = 0; q < a.Pcopy; ++q) {
+                const uint64_t* src = a.cp_src + q * a.party_stride;
+#pragma unroll
+                for (int m = 0; m < 16; ++m) v[m] = off[m] >= 0 ? __ldg(src + off[m]) : 0ull;
+                store_limbs16<LO>(a.cp_planes + q * a.cp_planes_stride, row, k0, KB, v);
+            }
+        }
+    }
+}
+
+template <Layout LO>
+__global__ void __launch_bounds__(256) split_im2col_kernel(Im2colSplitArgs a) {
+    split_im2col_body<LO>(a, blockIdx.x, gridDim.x);
+}
+cudaError_t launch_split_im2col(const Im2colSplitArgs& a, cudaStream_t st) {
+    const int64_t M = a.g.M(), K = a.g.K();
+    if (M == 0 || K == 0) return cudaSuccess;
+    const int64_t warps = ((M + 31) / 32) * num_kb(K) * 2;
+    if (a.layout_right) split_im2col_kernel<Layout::Right><<<grid_for(warps * 32), 256, 0, st>>>(a);
+    else split_im2col_kernel<Layout::Left><<<grid_for(warps * 32), 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+// Both splits of one private convolution in one launch (a programmatic
+// dependent, like split_both_kernel): blocks [0, nim) split the implicit
+// im2col of eps / a_p, the rest the weights' delta / b'_p.
+template <Layout LI, Layout LW>
+__global__ void __launch_bounds__(256, 2) split_conv_kernel(Im2colSplitArgs im, LeftSplitArgs wt, int nim) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if ((int)blockIdx.x < nim) split_im2col_body<LI>(im, blockIdx.x, nim);
+    else split_left_body<LW>(wt, blockIdx.x - nim, gridDim.x - nim);
+    asm volatile("griddepcontrol.launch_dependents;");
+}
+cudaError_t launch_split_conv(const Im2colSplitArgs& im, const LeftSplitArgs& wt, cudaStream_t st) {
+    const bool di = im.g.M() > 0 && im.g.K() > 0, dw = wt.M > 0 && wt.K > 0;
+    if (!dw) return launch_split_im2col(im, st);
+    if (!di) return launch_split_left(wt, st);
+    if ((im.layout_right != 0) == (wt.swap != 0)) return cudaErrorInvalidValue;   // one left, one right operand
+    const int64_t wi = ((im.g.M() + 31) / 32) * num_kb(im.g.K()) * 2 * 32;
+    const int64_t ww = ((wt.M + 7) / 8) * ((num_kb(wt.K) * kKBlock + 63) / 64) * 32;
+    // blocks in proportion to the bytes each side moves (the im2col side re-reads each input kh*kw times)
+    const int64_t bytes_i = im.g.M() * im.g.K() * (int64_t)(2 * im.Psum + im.Pcopy + 1);
+    const int64_t bytes_w = wt.M * wt.K * (int64_t)(2 * wt.Psum + wt.Pcopy + 1);
+    int64_t ni = std::min<int64_t>(grid_for(wi), std::max<int64_t>(1, 148 * 16 * bytes_i / (bytes_i + bytes_w)));
+    int64_t nw = std::min<int64_t>(grid_for(ww), std::max<int64_t>(1, 148 * 16 - ni));
+    if (im.layout_right)
+        return launch_pdl(split_conv_kernel<Layout::Right, Layout::Left>, dim3((unsigned)(ni + nw)), dim3(256), 0, st,
+                          im, wt, (int)ni);
+    return launch_pdl(split_conv_kernel<Layout::Left, Layout::Right>, dim3((unsigned)(ni + nw)), dim3(256), 0, st, im,
+                      wt, (int)ni);
 }
 
 // ------------------------------------------------------------------ a3 TTP triples

@@ -806,10 +806,9 @@ mpc_status conv_split(mpc_ctx c, const BeaverWs& w, const ConvGeom& g, const uin
                       int Psum, int64_t xstride, const uint64_t* acp, int Pcopy, const uint64_t* yp,
                       const uint64_t* ym, int64_t ystride, const uint64_t* bcp, int add_first) {
     Im2colSplitArgs I{g, xstride, xp, xm, Psum, w.eps_pl, acp, Pcopy, w.a_pl, w.a_stride, w.swap ? 1 : 0};
-    CHECK(run(c, kClsSplit, "split im2col", [&] { return launch_split_im2col(I, c->stream); }));
     LeftSplitArgs Wt{g.Cout, g.K(), ystride, yp, ym, Psum, w.delta_pl, bcp, Pcopy, w.b_pl, w.b_stride,
                      w.swap ? 0 : 1, add_first};
-    return run(c, kClsSplit, "split weights", [&] { return launch_split_left(Wt, c->stream); });
+    return run(c, kClsSplit, "split conv", [&] { return launch_split_conv(I, Wt, c->stream); });
 }
 mpc_status conv_gemm(mpc_ctx c, const BeaverWs& w, const ConvGeom& g, const uint64_t* cc, uint64_t* z, int truncate,
                      int parties) {
