@@ -339,17 +339,19 @@ __device__ __forceinline__ void split_im2col_body(const Im2colSplitArgs& a, int6
         if (row >= M) continue;
         const int64_t k0 = kc * 16;
         const int64_t b = row / (Ho * Wo), s = row % (Ho * Wo);
-        const int64_t oy = s / Wo, ox = s % Wo;
+        // (ci, ky, kx) of k0 once, then stepped: 32-bit index math inside one image
+        // (C*H*W < 2^31, checked by the host), one 64-bit image base
+        const int iy0 = (int)(s / Wo) * (int)g.sh - (int)g.ph, ix0 = (int)(s % Wo) * (int)g.sw - (int)g.pw;
+        const int H = (int)g.H, W = (int)g.W, kw = (int)g.kw, kh = (int)g.kh;
+        int ci = (int)(k0 / khw), r = (int)(k0 % khw);
+        int ky = r / kw, kx = r - ky * kw;
+        const int64_t base = b * g.C * g.H * g.W;
         int64_t off[16];                                        // element offset in one party's tensor, or -1
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
-            const int64_t k = k0 + m;
-            off[m] = -1;
-            if (k < K) {
-                const int64_t ci = k / khw, r = k % khw;
-                const int64_t iy = oy * g.sh - g.ph + r / g.kw, ix = ox * g.sw - g.pw + r % g.kw;
-                if (iy >= 0 && iy < g.H && ix >= 0 && ix < g.W) off[m] = ((b * g.C + ci) * g.H + iy) * g.W + ix;
-            }
+            const int iy = iy0 + ky, ix = ix0 + kx;
+            off[m] = (k0 + m < K && iy >= 0 && iy < H && ix >= 0 && ix < W) ? base + (ci * H + iy) * W + ix : -1;
+            if (++kx == kw) { kx = 0; if (++ky == kh) { ky = 0; ++ci; } }
         }
         uint64_t acc[16], v[16];
 #pragma unroll

@@ -785,7 +785,8 @@ namespace {
 bool conv_geom_ok(const mpc_conv2d_geom* g) {
     return g && g->B >= 0 && g->C >= 0 && g->H >= 0 && g->W >= 0 && g->Cout >= 0 && g->kh >= 1 && g->kw >= 1 &&
            g->sh >= 1 && g->sw >= 1 && g->ph >= 0 && g->pw >= 0 && g->H + 2 * g->ph >= g->kh &&
-           g->W + 2 * g->pw >= g->kw && g->C * g->kh * g->kw < ((int64_t)1 << 30);
+           g->W + 2 * g->pw >= g->kw && g->C * g->kh * g->kw < ((int64_t)1 << 30) &&
+           g->C * g->H * g->W < ((int64_t)1 << 31) && g->H < ((int64_t)1 << 30) && g->W < ((int64_t)1 << 30);
 }
 ConvGeom to_geom(const mpc_conv2d_geom* g) {
     return ConvGeom{g->B, g->C, g->H, g->W, g->Cout, g->kh, g->kw, g->sh, g->sw, g->ph, g->pw};
