@@ -374,3 +374,95 @@ def beaver_conv2d(x, y, a, b, c, g, want_intermediates: bool = False):
     if want_intermediates:
         return z, dict(eps=eps, delta=delta)
     return z
+
+
+# ---------------------------------------------------------------- O15 - O19
+def bshare(P: int, master: int, x, src: int, share_id: int, shape=None) -> np.ndarray:
+    """Binary (XOR) PRZS shares of the src party's words x: (P, *x.shape); x None -> zero-share of `shape`."""
+    kp, _ = derive_keys(master, P)
+    kp = np.ascontiguousarray(kp)
+    if x is None:
+        out = np.zeros((P,) + tuple(shape), dtype=np.uint64)
+        lib().oracle_bshare(P, _p(kp), None, src, ctypes.c_uint64(share_id), ctypes.c_int64(out[0].size), _p(out))
+        return out
+    x = _u64(x)
+    out = np.zeros((P,) + x.shape, dtype=np.uint64)
+    lib().oracle_bshare(P, _p(kp), _p(x), src, ctypes.c_uint64(share_id), ctypes.c_int64(x.size), _p(out))
+    return out
+
+
+def breveal(shares) -> np.ndarray:
+    shares = _u64(shares)
+    out = np.zeros(shares.shape[1:], dtype=np.uint64)
+    lib().oracle_breveal(shares.shape[0], _p(shares), ctypes.c_int64(out.size), _p(out))
+    return out
+
+
+def ttp_binary_triple(P: int, master: int, triple_id: int, shape):
+    _, kt = derive_keys(master, P)
+    n = int(np.prod(shape, dtype=np.int64))
+    a, b, c = (np.zeros((P,) + tuple(shape), dtype=np.uint64) for _ in range(3))
+    lib().oracle_ttp_binary_triple(P, ctypes.c_uint64(kt), ctypes.c_uint64(triple_id), ctypes.c_int64(n),
+                                   _p(a), _p(b), _p(c))
+    return a, b, c
+
+
+def binary_and(x, y, a, b, c) -> np.ndarray:
+    x, y, a, b, c = (_u64(t) for t in (x, y, a, b, c))
+    z = np.zeros(x.shape, dtype=np.uint64)
+    lib().oracle_binary_and(x.shape[0], _p(x), _p(y), _p(a), _p(b), _p(c), ctypes.c_int64(x[0].size), _p(z))
+    return z
+
+
+def add_ring(P: int, master: int, add_id: int, x, y) -> np.ndarray:
+    """Binary shares of (x + y) mod 2^64 from binary shares x, y (Kogge-Stone, triples dealt by add_id)."""
+    _, kt = derive_keys(master, P)
+    x, y = _u64(x), _u64(y)
+    out = np.zeros(x.shape, dtype=np.uint64)
+    lib().oracle_add_ring(P, ctypes.c_uint64(kt), ctypes.c_uint64(add_id), _p(x), _p(y), ctypes.c_int64(x[0].size),
+                          _p(out))
+    return out
+
+
+def a2b(master: int, a2b_id: int, x) -> np.ndarray:
+    """Binary shares (P, *shape) of the value arithmetically shared by x (P, *shape)."""
+    x = _u64(x)
+    P = x.shape[0]
+    kp, kt = derive_keys(master, P)
+    kp = np.ascontiguousarray(kp)
+    out = np.zeros(x.shape, dtype=np.uint64)
+    lib().oracle_a2b(P, _p(kp), ctypes.c_uint64(kt), ctypes.c_uint64(a2b_id), _p(x), ctypes.c_int64(x[0].size),
+                     _p(out))
+    return out
+
+
+def ttp_bit_pair(P: int, master: int, pair_id: int, shape):
+    _, kt = derive_keys(master, P)
+    n = int(np.prod(shape, dtype=np.int64))
+    rA, rB = (np.zeros((P,) + tuple(shape), dtype=np.uint64) for _ in range(2))
+    lib().oracle_ttp_bit_pair(P, ctypes.c_uint64(kt), ctypes.c_uint64(pair_id), ctypes.c_int64(n), _p(rA), _p(rB))
+    return rA, rB
+
+
+def b2a_bit(b, rA, rB, want_z: bool = False):
+    b, rA, rB = (_u64(t) for t in (b, rA, rB))
+    out = np.zeros(b.shape, dtype=np.uint64)
+    z = np.zeros(b.shape[1:], dtype=np.uint64)
+    lib().oracle_b2a_bit(b.shape[0], _p(b), _p(rA), _p(rB), ctypes.c_int64(b[0].size), _p(out), _p(z))
+    return (out, z) if want_z else out
+
+
+def relu(master: int, relu_id: int, x, diagnostics: bool = False):
+    """ReLU([x]) = [x][x >= 0] for arithmetic shares x (P, *shape); relu_id < 2^32."""
+    x = _u64(x)
+    P = x.shape[0]
+    kp, kt = derive_keys(master, P)
+    kp = np.ascontiguousarray(kp)
+    out = np.zeros(x.shape, dtype=np.uint64)
+    sign = np.zeros(x.shape, dtype=np.uint64)
+    rounds = ctypes.c_int(0)
+    lib().oracle_relu(P, _p(kp), ctypes.c_uint64(kt), ctypes.c_uint64(relu_id), _p(x), ctypes.c_int64(x[0].size),
+                      _p(out), _p(sign), ctypes.byref(rounds))
+    if diagnostics:
+        return out, dict(sign=sign, rounds=rounds.value)
+    return out

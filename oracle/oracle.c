@@ -678,3 +678,240 @@ void oracle_beaver_conv2d(int P, const uint64_t* x, const uint64_t* y, const uin
     if (delta_out) memcpy(delta_out, delta, (size_t)nb * 8);
     free(e); free(d); free(eps); free(delta); free(t);
 }
+
+/* ========================================================================
+ * the ReLU path — binary secret sharing (P:180-182,
+ * App. A.1.2), A2B by a carry-lookahead adder,
+ * the sign bit, single-bit B2A (Alg. 2) and the final
+ * multiplication ReLU([x]) = [x][x >= 0].
+ * Stream tags of this path (reading R23): BPRZS = 7 (binary zero-shares),
+ * BA/BB/BC = 8/9/10 (binary AND triples), RBIT/RB/RA = 11/12/13 (bit pairs),
+ * MA/MB/MC = 14/15/16 (the final arithmetic multiplication triple).
+ * ======================================================================== */
+enum { TAG_BPRZS = 7, TAG_BA = 8, TAG_BB = 9, TAG_BC = 10, TAG_RBIT = 11, TAG_RB = 12, TAG_RA = 13,
+       TAG_MA = 14, TAG_MB = 15, TAG_MC = 16 };
+
+/* Binary sharing by pseudorandom zero-share (XOR version of O3, reading R23):
+ * ⟨x⟩_p = G(k_p, BPRZS||0||id)[i] ⊕ G(k_{p−1}, BPRZS||0||id)[i] ⊕ [p = src]·x[i]. */
+void oracle_bshare(int P, const uint64_t* k_party, const uint64_t* x, int src, uint64_t share_id, int64_t n,
+                   uint64_t* shares)
+{
+    uint64_t stream = oracle_stream_id(TAG_BPRZS, 0, share_id);
+    for (int p = 0; p < P; p++) {
+        int prev = (p + P - 1) % P;
+        for (int64_t i = 0; i < n; i++) {
+            uint64_t v = oracle_prg_at(k_party[p], stream, (uint64_t)i) ^ oracle_prg_at(k_party[prev], stream, (uint64_t)i);
+            if (p == src && x != NULL) v ^= x[i];
+            shares[(int64_t)p * n + i] = v;
+        }
+    }
+}
+
+/* x = ⊕_p ⟨x⟩_p */
+void oracle_breveal(int P, const uint64_t* shares, int64_t n, uint64_t* out)
+{
+    for (int64_t i = 0; i < n; i++) {
+        uint64_t s = 0;
+        for (int p = 0; p < P; p++) s ^= shares[(int64_t)p * n + i];
+        out[i] = s;
+    }
+}
+
+/* Binary Beaver triple ("c = a ⊗ b", bitwise, packed 64 per word):
+ * a_p = G(k_ttp, BA||p||id), b_p = G(k_ttp, BB||p||id), c = (⊕a) & (⊕b),
+ * c_p = G(k_ttp, BC||p||id) for p ≥ 1, c_0 = c ⊕ ⊕_{p≥1} c_p. */
+void oracle_ttp_binary_triple(int P, uint64_t k_ttp, uint64_t id, int64_t n, uint64_t* a, uint64_t* b, uint64_t* c)
+{
+    for (int p = 0; p < P; p++) {
+        oracle_prg(k_ttp, oracle_stream_id(TAG_BA, (uint32_t)p, id), 0, n, a + (int64_t)p * n);
+        oracle_prg(k_ttp, oracle_stream_id(TAG_BB, (uint32_t)p, id), 0, n, b + (int64_t)p * n);
+    }
+    uint64_t* as = (uint64_t*)calloc((size_t)(n > 0 ? n : 1), 8);
+    uint64_t* bs = (uint64_t*)calloc((size_t)(n > 0 ? n : 1), 8);
+    oracle_breveal(P, a, n, as);
+    oracle_breveal(P, b, n, bs);
+    for (int64_t i = 0; i < n; i++) c[i] = as[i] & bs[i];
+    for (int p = 1; p < P; p++) {
+        uint64_t* cp = c + (int64_t)p * n;
+        oracle_prg(k_ttp, oracle_stream_id(TAG_BC, (uint32_t)p, id), 0, n, cp);
+        for (int64_t i = 0; i < n; i++) c[i] ^= cp[i];
+    }
+    free(as); free(bs);
+}
+
+/* O15 Bitwise AND: ⟨ε⟩ = ⟨x⟩ ⊕ ⟨a⟩, ⟨δ⟩ = ⟨y⟩ ⊕ ⟨b⟩, ε, δ revealed
+ * (one round); ⟨z⟩_p = ⟨c⟩_p ⊕ (ε & ⟨b⟩_p) ⊕ (⟨a⟩_p & δ) ⊕ [p = 0](ε & δ). */
+void oracle_binary_and(int P, const uint64_t* x, const uint64_t* y, const uint64_t* a, const uint64_t* b,
+                       const uint64_t* c, int64_t n, uint64_t* z)
+{
+    for (int64_t i = 0; i < n; i++) {
+        uint64_t eps = 0, delta = 0;
+        for (int p = 0; p < P; p++) {
+            eps ^= x[(int64_t)p * n + i] ^ a[(int64_t)p * n + i];
+            delta ^= y[(int64_t)p * n + i] ^ b[(int64_t)p * n + i];
+        }
+        for (int p = 0; p < P; p++) {
+            int64_t k = (int64_t)p * n + i;
+            z[k] = c[k] ^ (eps & b[k]) ^ (a[k] & delta);
+            if (p == 0) z[k] ^= eps & delta;
+        }
+    }
+}
+
+/* AND of two binary-shared tensors with the triple of AND gate `gate_id` (dealt here by the TTP). */
+static void and_gate(int P, uint64_t k_ttp, uint64_t gate_id, const uint64_t* x, const uint64_t* y, int64_t n,
+                     uint64_t* z)
+{
+    size_t sz = (size_t)(P * (n > 0 ? n : 1)) * 8;
+    uint64_t *a = (uint64_t*)malloc(sz), *b = (uint64_t*)malloc(sz), *c = (uint64_t*)malloc(sz);
+    oracle_ttp_binary_triple(P, k_ttp, gate_id, n, a, b, c);
+    oracle_binary_and(P, x, y, a, b, c, n, z);
+    free(a); free(b); free(c);
+}
+
+/* AND gate ids of one ring addition (reading R24): adder `add_id`, Kogge-Stone
+ * level l (0 = the generate bits x & y, 1..6 = prefix levels), operand w
+ * (0: P & (G << k), 1: P & (P << k)):  gate = (add_id << 4) | (l << 1) | w. */
+static uint64_t gate_id(uint64_t add_id, int l, int w) { return (add_id << 4) | ((uint64_t)l << 1) | (uint64_t)w; }
+
+/* O16 ring addition ⟨x + y mod 2^64⟩ as a carry-lookahead (Kogge-Stone) adder
+ * on binary shares (SPEC add_ring): generate G = x & y, propagate
+ * Pr = x ⊕ y; for k = 1, 2, 4, ..., 32: G ← G ⊕ (Pr & (G << k)),
+ * Pr ← Pr & (Pr << k) (the two ANDs of a level share one round; G and
+ * Pr & (G << k) are disjoint, so OR = XOR); sum = x ⊕ y ⊕ (G << 1).
+ * 1 + 6 AND rounds (the first generate AND is batched with nothing; 7 rounds). */
+void oracle_add_ring(int P, uint64_t k_ttp, uint64_t add_id, const uint64_t* x, const uint64_t* y, int64_t n,
+                     uint64_t* out)
+{
+    size_t sz = (size_t)(P * (n > 0 ? n : 1)) * 8;
+    uint64_t *G = (uint64_t*)malloc(sz), *Pr = (uint64_t*)malloc(sz), *t = (uint64_t*)malloc(sz),
+             *u = (uint64_t*)malloc(sz);
+    int64_t Pn = (int64_t)P * n;
+    and_gate(P, k_ttp, gate_id(add_id, 0, 0), x, y, n, G);
+    for (int64_t k = 0; k < Pn; k++) Pr[k] = x[k] ^ y[k];
+    for (int l = 1; l <= 6; l++) {
+        int s = 1 << (l - 1);
+        for (int64_t k = 0; k < Pn; k++) t[k] = G[k] << s;       /* local logical shift */
+        and_gate(P, k_ttp, gate_id(add_id, l, 0), Pr, t, n, u);
+        for (int64_t k = 0; k < Pn; k++) G[k] ^= u[k];
+        for (int64_t k = 0; k < Pn; k++) t[k] = Pr[k] << s;
+        and_gate(P, k_ttp, gate_id(add_id, l, 1), Pr, t, n, u);
+        memcpy(Pr, u, (size_t)Pn * 8);
+    }
+    for (int64_t k = 0; k < Pn; k++) out[k] = x[k] ^ y[k] ^ (G[k] << 1);
+    free(G); free(Pr); free(t); free(u);
+}
+
+/* O17 A2B: party q binary-shares its arithmetic share
+ * [x]_q (binary PRZS, share id (a2b_id << 8) | q); the P binary values are
+ * summed by a tree of ring adders, adjacent pairs level by level (level h,
+ * pair i has adder id (a2b_id << 12) | (h << 6) | i; an odd last element
+ * passes up).  Rounds: ceil(log2 P) adder levels of 7 AND rounds.
+ * x: [P][n] arithmetic shares -> out: [P][n] binary shares of x. */
+void oracle_a2b(int P, const uint64_t* k_party, uint64_t k_ttp, uint64_t a2b_id, const uint64_t* x, int64_t n,
+                uint64_t* out)
+{
+    size_t one = (size_t)(P * (n > 0 ? n : 1)) * 8;
+    uint64_t** items = (uint64_t**)malloc(sizeof(uint64_t*) * (size_t)P);
+    for (int q = 0; q < P; q++) {
+        items[q] = (uint64_t*)malloc(one);
+        oracle_bshare(P, k_party, x + (int64_t)q * n, q, (a2b_id << 8) | (uint64_t)q, n, items[q]);
+    }
+    int cnt = P, h = 1;
+    while (cnt > 1) {
+        int nc = 0;
+        for (int i = 0; i + 1 < cnt; i += 2) {
+            uint64_t* s = (uint64_t*)malloc(one);
+            oracle_add_ring(P, k_ttp, (a2b_id << 12) | ((uint64_t)h << 6) | (uint64_t)(i / 2), items[i], items[i + 1], n, s);
+            free(items[i]); free(items[i + 1]);
+            items[nc++] = s;
+        }
+        if (cnt & 1) items[nc++] = items[cnt - 1];
+        cnt = nc;
+        h++;
+    }
+    memcpy(out, items[0], (size_t)P * (size_t)n * 8);
+    free(items[0]);
+    free(items);
+}
+
+/* Bit pair ([r], ⟨r⟩) from the TTP (Alg. 2 input): r = G(k_ttp, RBIT||0||id)[i] & 1;
+ * ⟨r⟩_p = G(k_ttp, RB||p||id)[i] & 1 (p ≥ 1), ⟨r⟩_0 = r ⊕ ⊕_{p≥1}⟨r⟩_p;
+ * [r]_p = G(k_ttp, RA||p||id)[i] (p ≥ 1), [r]_0 = r − Σ_{p≥1} [r]_p. */
+void oracle_ttp_bit_pair(int P, uint64_t k_ttp, uint64_t id, int64_t n, uint64_t* rA, uint64_t* rB)
+{
+    for (int64_t i = 0; i < n; i++) {
+        uint64_t r = oracle_prg_at(k_ttp, oracle_stream_id(TAG_RBIT, 0, id), (uint64_t)i) & 1u;
+        uint64_t rb0 = r, ra0 = r;
+        for (int p = 1; p < P; p++) {
+            uint64_t vb = oracle_prg_at(k_ttp, oracle_stream_id(TAG_RB, (uint32_t)p, id), (uint64_t)i) & 1u;
+            uint64_t va = oracle_prg_at(k_ttp, oracle_stream_id(TAG_RA, (uint32_t)p, id), (uint64_t)i);
+            rB[(int64_t)p * n + i] = vb;
+            rA[(int64_t)p * n + i] = va;
+            rb0 ^= vb;
+            ra0 -= va;
+        }
+        rB[i] = rb0;
+        rA[i] = ra0;
+    }
+}
+
+/* O18 single-bit B2A (Alg. 2): ⟨z⟩ = ⟨b⟩ ⊕ ⟨r⟩; z = reveal(⟨z⟩) (one
+ * round); [b] = [r] + z − 2[r]z (party 0 adds the public z).  b: [P][n] binary
+ * shares whose bit 0 is the shared bit (higher bits ignored).  z_out may be NULL. */
+void oracle_b2a_bit(int P, const uint64_t* b, const uint64_t* rA, const uint64_t* rB, int64_t n, uint64_t* out,
+                    uint64_t* z_out)
+{
+    for (int64_t i = 0; i < n; i++) {
+        uint64_t z = 0;
+        for (int p = 0; p < P; p++) z ^= (b[(int64_t)p * n + i] ^ rB[(int64_t)p * n + i]) & 1u;
+        for (int p = 0; p < P; p++) {
+            int64_t k = (int64_t)p * n + i;
+            out[k] = rA[k] - 2u * z * rA[k] + (p == 0 ? z : 0u);
+        }
+        if (z_out) z_out[i] = z;
+    }
+}
+
+/* O19 ReLU([x]) = [x] · [x >= 0] (reading R25):
+ *   ⟨x⟩ = A2B([x]) (a2b id relu_id);  ⟨s⟩ = ⟨x⟩ >> 63 (sign bit);
+ *   [s] = B2A_bit(⟨s⟩) with bit pair relu_id;  [x >= 0] = 1 − [s] (party 0 adds 1);
+ *   out = BeaverMul([x], [x >= 0]) with the MA/MB/MC triple relu_id (one round).
+ * The indicator carries scale 1, so out keeps x's scale (no truncation).
+ * x, out: [P][n]; sign_out ([P][n] arithmetic shares of [x < 0]) and rounds may be NULL. */
+void oracle_relu(int P, const uint64_t* k_party, uint64_t k_ttp, uint64_t relu_id, const uint64_t* x, int64_t n,
+                 uint64_t* out, uint64_t* sign_out, int* rounds)
+{
+    size_t sz = (size_t)(P * (n > 0 ? n : 1)) * 8;
+    uint64_t *xb = (uint64_t*)malloc(sz), *rA = (uint64_t*)malloc(sz), *rB = (uint64_t*)malloc(sz),
+             *s = (uint64_t*)malloc(sz), *ind = (uint64_t*)malloc(sz), *a = (uint64_t*)malloc(sz),
+             *b = (uint64_t*)malloc(sz), *c = (uint64_t*)malloc(sz);
+    int64_t Pn = (int64_t)P * n;
+    oracle_a2b(P, k_party, k_ttp, relu_id, x, n, xb);
+    for (int64_t k = 0; k < Pn; k++) xb[k] >>= 63;                      /* sign bit, local */
+    oracle_ttp_bit_pair(P, k_ttp, relu_id, n, rA, rB);
+    oracle_b2a_bit(P, xb, rA, rB, n, s, NULL);                          /* [x < 0] */
+    for (int p = 0; p < P; p++)
+        for (int64_t i = 0; i < n; i++) ind[(int64_t)p * n + i] = (p == 0 ? 1u : 0u) - s[(int64_t)p * n + i];
+    for (int p = 0; p < P; p++) {                                       /* triple c = a·b (O9's construction) */
+        oracle_prg(k_ttp, oracle_stream_id(TAG_MA, (uint32_t)p, relu_id), 0, n, a + (int64_t)p * n);
+        oracle_prg(k_ttp, oracle_stream_id(TAG_MB, (uint32_t)p, relu_id), 0, n, b + (int64_t)p * n);
+    }
+    for (int64_t i = 0; i < n; i++) {
+        uint64_t as = 0, bs = 0;
+        for (int p = 0; p < P; p++) { as += a[(int64_t)p * n + i]; bs += b[(int64_t)p * n + i]; }
+        c[i] = as * bs;
+    }
+    for (int p = 1; p < P; p++) {
+        oracle_prg(k_ttp, oracle_stream_id(TAG_MC, (uint32_t)p, relu_id), 0, n, c + (int64_t)p * n);
+        for (int64_t i = 0; i < n; i++) c[i] -= c[(int64_t)p * n + i];
+    }
+    oracle_beaver_mul(P, x, ind, a, b, c, n, NULL, NULL, out);
+    if (sign_out) memcpy(sign_out, s, (size_t)Pn * 8);
+    if (rounds) {
+        int levels = 0;
+        for (int q = 1; q < P; q *= 2) levels++;
+        *rounds = levels * 7 + 1 + 1;                                   /* A2B, B2A, multiplication */
+    }
+    free(xb); free(rA); free(rB); free(s); free(ind); free(a); free(b); free(c);
+}
