@@ -251,6 +251,20 @@ mpc_status mpc_beaver_conv2d_finish(mpc_ctx ctx, const mpc_conv2d_geom* geom, co
 mpc_status mpc_mask(mpc_ctx ctx, const uint64_t* x, const uint64_t* a, int64_t n1, const uint64_t* y,
                     const uint64_t* b, int64_t n2, uint64_t* ed);
 
+/* ---- ReLU ----------------------
+ * out = shares of ReLU(x) = [x] * [x >= 0] for x, out: n per party ([P][n]).
+ * A2B: every party's arithmetic share is binary-shared (binary PRZS) and the P
+ * values summed by a tree of Kogge-Stone adders with binary Beaver ANDs
+ * (App. A.1.2-A.1.3; R23, R24); the sign bit <x> >> 63
+ * goes through Alg. 2 (bit pair from the TTP) to [x < 0], and
+ * out = BeaverMul([x], 1 - [x < 0]) (R25) — exact, x's scale, no truncation.
+ * Rounds: ceil(log2 P)*7 + 2.  relu_id (< 2^32) selects every stream (binary
+ * zero-shares, binary triples, bit pair, multiplication triple); single-use.
+ * sign_out (optional, same shape) receives the shares of [x < 0].
+ * All-parties contexts with P <= 8 (one fused kernel); one-party contexts:
+ * MPC_ERR_UNSUPPORTED. */
+mpc_status mpc_relu(mpc_ctx ctx, const uint64_t* x, uint64_t* out, int64_t n, uint64_t relu_id, uint64_t* sign_out);
+
 /* ---- measurement hooks (bench.py) ----------------------------------------
  * When enabled, the library brackets every launch of kernel class `cls` with CUDA
  * events on the launching stream and accumulates its device time.

@@ -53,6 +53,7 @@ SIGNATURES = [
     ("mpc_conv2d_workspace_bytes", _S, [_V, ctypes.POINTER(ConvGeom)]),
     ("mpc_beaver_conv2d", _I, [_V, ctypes.POINTER(ConvGeom), _V, _V, _V, _V, _V, _V, _I, _U, _V, _S]),
     ("mpc_beaver_conv2d_finish", _I, [_V, ctypes.POINTER(ConvGeom), _V, _V, _V, _V, _V, _I, _V, _S]),
+    ("mpc_relu", _I, [_V, _V, _V, _L, _U, _V]),
     ("mpc_profile_enable", _I, [_V, _I]),
     ("mpc_profile_read", _I, [_V, _I, ctypes.POINTER(_D), ctypes.POINTER(_U)]),
     ("mpc_launch_count", _U, [_V]),

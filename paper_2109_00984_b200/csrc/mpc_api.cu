@@ -18,6 +18,7 @@
 #include "beaver_elementwise.h"
 #include "conv.h"
 #include "elementwise.h"
+#include "relu.h"
 #include "ring_gemm.h"
 
 using namespace mpc;
@@ -930,6 +931,22 @@ mpc_status mpc_ttp_conv_triples(mpc_ctx c, uint64_t id, const mpc_conv2d_geom* g
     return run(c, kClsPrg, "ttp_c", [&] {
         return launch_ttp_c(c->kttp, id, c->P, out_lo, out_hi, c_out, ttp ? cc : nullptr, nz, c->stream);
     });
+}
+
+// ---------------------------------------------------------------- ReLU
+mpc_status mpc_relu(mpc_ctx c, const uint64_t* x, uint64_t* out, int64_t n, uint64_t relu_id, uint64_t* sign_out) {
+    CHECK(enter(c));
+    if (n < 0) return fail(c, MPC_ERR_SHAPE, "relu: n < 0");
+    if (relu_id >> 32) return fail(c, MPC_ERR_ARG, "relu: relu_id must be < 2^32 (R24 gate ids)");
+    if (!c->all) return fail(c, MPC_ERR_UNSUPPORTED, "relu: one-party contexts are not supported yet");
+    if (c->P > 8) return fail(c, MPC_ERR_UNSUPPORTED, "relu: at most 8 parties");
+    int levels = 0;
+    for (int q = 1; q < c->P; q *= 2) levels++;
+    c->rounds += (uint64_t)(7 * levels + 2);       // A2B adders, B2A, multiplication (R25)
+    if (n == 0) return MPC_OK;
+    if (!x || !out) return fail(c, MPC_ERR_ARG, "relu: null pointer");
+    return run(c, kClsSplit, "relu",
+               [&] { return launch_relu_all(c->kp, c->kttp, relu_id, c->P, x, out, sign_out, n, c->stream); });
 }
 
 mpc_status mpc_profile_enable(mpc_ctx c, int enable) {

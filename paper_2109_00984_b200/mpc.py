@@ -319,6 +319,15 @@ class Context:
                    _ptr(ed))
         return ed
 
+    # ------------------------------------------------------------ ReLU
+    def relu(self, x: torch.Tensor, relu_id: int, out: Optional[torch.Tensor] = None, want_sign: bool = False):
+        """ReLU([x]) = [x][x >= 0] (A2B -> sign bit -> B2A -> Beaver multiplication)."""
+        z = _u64(tuple(x.shape), self.device) if out is None else _check_out(out, tuple(x.shape), torch.uint64)
+        sign = _u64(tuple(x.shape), self.device) if want_sign else None
+        n = x[0].numel() if self.all_parties else x.numel()
+        self._call(self._lib.mpc_relu, _ptr(x), _ptr(z), ctypes.c_int64(n), ctypes.c_uint64(relu_id), _ptr(sign))
+        return (z, sign) if want_sign else z
+
     def truncate(self, x: torch.Tensor, bits: Optional[int] = None, wrap_id: int = 0) -> torch.Tensor:
         """In place; returns x."""
         n = x[0].numel() if self.all_parties else x.numel()
