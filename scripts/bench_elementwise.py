@@ -7,6 +7,8 @@ Algorithmic bytes per element (P parties, u64 shares):
   square: read x_p, a_p, b_p,           write z_p  -> 32 P B
   TTP triple: write a_p, b_p, c_p -> 24 P B;  TTP pair: 16 P B
   Alg. 1 truncation (P > 2): read + write x_p -> 16 P B (plus Philox for r_p, theta_r)
+  ReLU (fused A2B + B2A + multiplication): read x_p, write out_p -> 16 P B; bound by the
+    Philox expansions of its triples (relu_philox_per_elem)
 
   python scripts/bench_elementwise.py [--n 16777216] [--parties 2] [--reps 50]
 """
@@ -66,11 +68,23 @@ def run(n, P, reps):
     }
     if P > 2:
         cases["trunc_alg1"] = (lambda: ctx.truncate(z, 16, wrap_id=5), 16 * P)
+    if P <= 8:   # the fused ReLU path (Philox / ALU bound; bytes = x_p in, out_p out)
+        cases["relu"] = (lambda: ctx.relu(x, relu_id=9, out=z), 16 * P)
     for name, (fn, bpe) in cases.items():
         ms = timed(fn, reps)
         gbs = bpe * n / (ms * 1e-3) / 1e9
         out[name] = {"ms": ms, "bytes_per_elem": bpe, "achieved_gbs": gbs, "frac_of_hbm": gbs / peak,
                      "Gelem_per_s": n / (ms * 1e-3) / 1e9}
+    if "relu" in out:
+        # Philox4x32-10 blocks per element (each block serves an element pair): binary zero-shares
+        # P per leaf, per AND gate 3P - 1, ceil(log2 P) * 12 gates per adder path... counted exactly:
+        levels, q = 0, 1
+        while q < P:
+            q, levels = q * 2, levels + 1
+        adders = P - 1                               # a tree over P leaves has P - 1 adders
+        blocks = P * P + adders * 12 * (3 * P - 1) + (1 + 2 * (P - 1)) + (3 * P - 1)
+        out["relu"]["philox_blocks_per_elem"] = blocks / 2.0
+        out["relu"]["philox_blocks_per_s"] = blocks / 2.0 * n / (out["relu"]["ms"] * 1e-3)
     return out
 
 
