@@ -87,6 +87,28 @@ int mpc_rank(mpc_ctx ctx);
  * the other parties before mpc_create).  MPC_ERR_NCCL on failure. */
 mpc_status mpc_nccl_unique_id(void* out128);
 
+/* ---- in-process party group (one-party contexts without NCCL) ------------
+ * A group joins P one-party contexts of ONE process on one device: their
+ * reveals are the same collectives as over NCCL (sum, int8 sum, XOR), done by a
+ * host rendezvous plus one reduction kernel launched by the last party to
+ * arrive, ordered with CUDA events on each party's stream.  Each party must be
+ * driven by its own host thread (a collective blocks its caller until all P
+ * parties have entered it; after 300 s without them the context fails with
+ * MPC_ERR_STATE), and every party must call the same sequence of collective
+ * entry points with the same sizes (a mismatch returns MPC_ERR_SHAPE and
+ * breaks the group).  Purpose: running the one-party-per-GPU schedule — same
+ * kernels, streams and events — for P > 1 parties on a single GPU (tests;
+ * the paper's parties are separate processes).
+ * mpc_group_create: P in [1, 16].  mpc_create_local: like mpc_create with
+ * rank in [0, P) and the group instead of an NCCL id; MPC_ERR_ARG if the rank
+ * is already attached.  The group must outlive its contexts (destroy the
+ * contexts first). */
+typedef struct mpc_group_s* mpc_group;           /* opaque, library-owned */
+mpc_status mpc_group_create(mpc_group* out, int world_size);
+mpc_status mpc_group_destroy(mpc_group group);
+mpc_status mpc_create_local(mpc_ctx* out, mpc_group group, int rank, int device,
+                            uint64_t master_seed, int frac_bits);
+
 /* ---- fixed point (§4.1; App. A.1.1) ----------------
  * encode: out[i] = round_half_away(x[i] * 2^f) as two's complement u64;
  *   MPC_ERR_OVERFLOW if any |x[i]| * 2^f >= 2^63 or NaN (checked on the device;
@@ -261,8 +283,13 @@ mpc_status mpc_mask(mpc_ctx ctx, const uint64_t* x, const uint64_t* a, int64_t n
  * Rounds: ceil(log2 P)*7 + 2.  relu_id (< 2^32) selects every stream (binary
  * zero-shares, binary triples, bit pair, multiplication triple); single-use.
  * sign_out (optional, same shape) receives the shares of [x < 0].
- * All-parties contexts with P <= 8 (one fused kernel); one-party contexts:
- * MPC_ERR_UNSUPPORTED. */
+ * All-parties contexts, P <= 8: one fused kernel, every reveal a local XOR / sum.
+ * One-party contexts, P <= 16: round by round over the transport — per height of
+ * the adder tree 7 XOR reveals (NCCL: all-gather + local XOR), the B2A bit
+ * reveal (1 bit per element, packed) and the multiplication's sum reveal;
+ * rank 0 also generates the TTP's correction words.  Work buffers come from
+ * the context (8n(P + 6 floor(P/2)) bytes at most).  Both modes give
+ * bit-identical shares. */
 mpc_status mpc_relu(mpc_ctx ctx, const uint64_t* x, uint64_t* out, int64_t n, uint64_t relu_id, uint64_t* sign_out);
 
 /* ---- measurement hooks (bench.py) ----------------------------------------

@@ -26,6 +26,9 @@ SIGNATURES = [
     ("mpc_world_size", _I, [_V]),
     ("mpc_rank", _I, [_V]),
     ("mpc_nccl_unique_id", _I, [_V]),
+    ("mpc_group_create", _I, [ctypes.POINTER(_V), _I]),
+    ("mpc_group_destroy", _I, [_V]),
+    ("mpc_create_local", _I, [ctypes.POINTER(_V), _V, _I, _I, _U, _I]),
     ("mpc_encode", _I, [_V, _V, _V, _L]),
     ("mpc_decode", _I, [_V, _V, _V, _L]),
     ("mpc_share", _I, [_V, _V, _I, _U, _V, _L]),

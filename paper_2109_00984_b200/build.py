@@ -36,16 +36,30 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every csrc/*.cu to an object in parallel (build/), then link the
+    shared library; the .so is replaced atomically."""
     if not force and not needs_build():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     inc, libdir = _nccl_dirs()
-    cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(ROOT, "include"), "-I", inc,
-           *sources(), "-o", LIB + ".tmp",
-           "-L", libdir, "-l:libnccl.so.2", f"-Xlinker=-rpath={libdir}"]
-    subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
+    import shutil
+    objdir = os.path.join(ROOT, "build", f"mpc_ring_obj.{os.getpid()}")   # per process: concurrent builds
+    os.makedirs(objdir, exist_ok=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+             "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"), "-I", inc]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        subprocess.check_call(["nvcc", *flags, "-c", src, "-o", obj])
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(compile_one, sources()))
+    tmp = f"{LIB}.{os.getpid()}.tmp"
+    subprocess.check_call(["nvcc", *ARCH, "-shared", *objs, "-o", tmp,
+                           "-L", libdir, "-l:libnccl.so.2", f"-Xlinker=-rpath={libdir}"])
+    os.replace(tmp, LIB)
+    shutil.rmtree(objdir, ignore_errors=True)
     return LIB
 
 

@@ -20,6 +20,7 @@
 #include "elementwise.h"
 #include "relu.h"
 #include "ring_gemm.h"
+#include "transport.h"
 
 using namespace mpc;
 
@@ -33,6 +34,9 @@ struct mpc_ctx_s {
     uint64_t kttp = 0;
     cudaStream_t stream = nullptr;
     ncclComm_t comm = nullptr;
+    LocalGroup* lg = nullptr;               // in-process transport (mpc_create_local), instead of NCCL
+    uint64_t* xbuf = nullptr;               // NCCL XOR reveal: all-gathered binary shares
+    size_t xbuf_bytes = 0;
     cudaStream_t comm_stream = nullptr;     // reveals of the overlapped Beaver schedule
     cudaEvent_t ev_mask = nullptr, ev_delta = nullptr, ev_eps = nullptr;
     bool broken = false;
@@ -81,13 +85,56 @@ mpc_status run(mpc_ctx c, int cls, const char* what, F&& f) {
     return MPC_OK;
 }
 
-mpc_status nccl_allreduce(mpc_ctx c, const void* send, void* recv, size_t count, ncclDataType_t dt, const char* what,
+inline bool has_comm(mpc_ctx c) { return c->comm != nullptr || c->lg != nullptr; }
+
+// One reveal collective of this party on `st` (default: the context stream):
+// recv = op over the parties' send buffers (transport.h).  Any failure leaves
+// the context broken (MPC_ERR_STATE afterwards), as the collective contract
+// can no longer be kept.
+mpc_status comm_allreduce(mpc_ctx c, const void* send, void* recv, size_t count, RedOp op, const char* what,
                           cudaStream_t st = nullptr) {
-    if (!c->comm) return fail(c, MPC_ERR_STATE, "%s: context has no communicator (created without nccl_id)", what);
     if (!st) st = c->stream;
+    if (c->P == 1 && !has_comm(c)) {            // one party: the reveal is the share itself
+        if (send == recv || count == 0) return MPC_OK;
+        const size_t bytes = count * (op == RedOp::SumI8 ? 1 : 8);
+        cudaError_t e = cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, st);
+        return e == cudaSuccess ? MPC_OK : fail(c, MPC_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    }
+    if (!has_comm(c)) return fail(c, MPC_ERR_STATE, "%s: context has no communicator (created without nccl_id)", what);
     ProfEvent ev{nullptr, nullptr, kClsComm};
     if (c->prof) { ev.a = take_event(c); ev.b = take_event(c); cudaEventRecord(ev.a, st); }
-    ncclResult_t r = count ? ncclAllReduce(send, recv, count, dt, ncclSum, c->comm, st) : ncclSuccess;
+    if (c->lg) {
+        const int r = local_group_allreduce(c->lg, c->rank, send, recv, count, op, st);
+        if (c->prof) { cudaEventRecord(ev.b, st); c->pending.push_back(ev); }
+        if (r != 0) {
+            c->broken = true;
+            static const char* why[] = {"", "parties called different collectives (count / op mismatch)",
+                                        "timed out waiting for the other parties", "CUDA error", "group broken"};
+            return fail(c, r == 1 ? MPC_ERR_SHAPE : MPC_ERR_STATE, "%s: local group: %s", what, why[r < 5 ? r : 4]);
+        }
+        return MPC_OK;
+    }
+    ncclResult_t r = ncclSuccess;
+    if (count == 0) {
+    } else if (op == RedOp::XorU64) {
+        // NCCL has no XOR reduction: all-gather the P binary shares, XOR them locally
+        const size_t need = 8 * count * (size_t)c->P;
+        if (c->xbuf_bytes < need) {
+            cudaStreamSynchronize(st);
+            if (c->xbuf) cudaFree(c->xbuf);
+            c->xbuf = nullptr; c->xbuf_bytes = 0;
+            if (cudaMalloc(&c->xbuf, need) != cudaSuccess) return fail(c, MPC_ERR_CUDA, "%s: xor buffer alloc", what);
+            c->xbuf_bytes = need;
+        }
+        r = ncclAllGather(send, c->xbuf, count, ncclUint64, c->comm, st);
+        if (r == ncclSuccess) {
+            cudaError_t e = launch_xor_gathered(c->xbuf, c->P, (int64_t)count, static_cast<uint64_t*>(recv), st);
+            c->launches++;
+            if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "%s: xor: %s", what, cudaGetErrorString(e));
+        }
+    } else {
+        r = ncclAllReduce(send, recv, count, op == RedOp::SumI8 ? ncclInt8 : ncclUint64, ncclSum, c->comm, st);
+    }
     if (c->prof) { cudaEventRecord(ev.b, st); c->pending.push_back(ev); }
     if (r != ncclSuccess) {
         c->broken = true;
@@ -211,9 +258,9 @@ mpc_status beaver_overlapped(mpc_ctx c, const BeaverWs& w, const uint64_t* x, co
     CHECK(run(c, kClsSplit, "mask", [&] { return launch_mask(x, a, sMK, y, b, sKN, w.ed, c->stream); }));
     cudaEventRecord(c->ev_mask, c->stream);
     cudaStreamWaitEvent(c->comm_stream, c->ev_mask, 0);
-    CHECK(nccl_allreduce(c, w.ed + sMK, w.ed + sMK, (size_t)sKN, ncclUint64, "delta reveal", c->comm_stream));
+    CHECK(comm_allreduce(c, w.ed + sMK, w.ed + sMK, (size_t)sKN, RedOp::SumU64, "delta reveal", c->comm_stream));
     cudaEventRecord(c->ev_delta, c->comm_stream);
-    CHECK(nccl_allreduce(c, w.ed, w.ed, (size_t)sMK, ncclUint64, "eps reveal", c->comm_stream));
+    CHECK(comm_allreduce(c, w.ed, w.ed, (size_t)sMK, RedOp::SumU64, "eps reveal", c->comm_stream));
     cudaEventRecord(c->ev_eps, c->comm_stream);
     // a_p planes need no reveal
     LeftSplitArgs La{M, K, 0, nullptr, nullptr, 0, nullptr, a, 1, w.a_pl, 0, w.swap};
@@ -272,8 +319,8 @@ mpc_status truncate_impl(mpc_ctx c, uint64_t* x, int64_t n, int bits, uint64_t w
     c->bytes += 9ull * (uint64_t)n;
     CHECK(run(c, kClsTrunc, "trunc_alg1_a",
               [&] { return launch_trunc_alg1_a(x, n, c->kttp, wrap_id, c->rank, zbuf, hbuf, c->stream); }));
-    CHECK(nccl_allreduce(c, zbuf, zbuf, (size_t)n, ncclUint64, "truncate z reveal"));
-    CHECK(nccl_allreduce(c, hbuf, hbuf, (size_t)n, ncclInt8, "truncate top-bit reveal"));
+    CHECK(comm_allreduce(c, zbuf, zbuf, (size_t)n, RedOp::SumU64, "truncate z reveal"));
+    CHECK(comm_allreduce(c, hbuf, hbuf, (size_t)n, RedOp::SumI8, "truncate top-bit reveal"));
     return run(c, kClsTrunc, "trunc_alg1_b", [&] {
         return launch_trunc_alg1_b(x, n, bits, c->kttp, wrap_id, c->P, c->rank, zbuf, hbuf, c->stream);
     });
@@ -328,11 +375,55 @@ mpc_status mpc_create(mpc_ctx* out, int world_size, int rank, int device, const 
     return MPC_OK;
 }
 
+struct mpc_group_s { LocalGroup* g; };
+
+mpc_status mpc_group_create(mpc_group* out, int world_size) {
+    if (!out) return MPC_ERR_ARG;
+    *out = nullptr;
+    if (world_size < 1 || world_size > kMaxParties) return MPC_ERR_ARG;
+    LocalGroup* g = local_group_create(world_size);
+    if (!g) return MPC_ERR_CUDA;
+    *out = new mpc_group_s{g};
+    return MPC_OK;
+}
+
+mpc_status mpc_group_destroy(mpc_group g) {
+    if (!g) return MPC_ERR_ARG;
+    local_group_destroy(g->g);
+    delete g;
+    return MPC_OK;
+}
+
+mpc_status mpc_create_local(mpc_ctx* out, mpc_group group, int rank, int device, uint64_t master_seed,
+                            int frac_bits) {
+    if (!out) return MPC_ERR_ARG;
+    *out = nullptr;
+    if (!group) return MPC_ERR_ARG;
+    const int P = local_group_size(group->g);
+    if (rank < 0 || rank >= P) return MPC_ERR_ARG;
+    mpc_ctx c = nullptr;
+    mpc_status s = mpc_create(&c, P, rank, device, nullptr, master_seed, frac_bits);
+    if (s != MPC_OK) return s;
+    if (!local_group_attach(group->g, rank)) { mpc_destroy(c); return MPC_ERR_ARG; }
+    c->lg = group->g;
+    if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_mask, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_delta, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_eps, cudaEventDisableTiming) != cudaSuccess) {
+        mpc_destroy(c);
+        return MPC_ERR_CUDA;
+    }
+    *out = c;
+    return MPC_OK;
+}
+
 mpc_status mpc_destroy(mpc_ctx c) {
     if (!c) return MPC_ERR_ARG;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream); else cudaDeviceSynchronize();
     if (c->comm) ncclCommDestroy(c->comm);
+    if (c->lg) local_group_detach(c->lg, c->rank);
+    if (c->xbuf) cudaFree(c->xbuf);
     if (c->comm_stream) { cudaStreamSynchronize(c->comm_stream); cudaStreamDestroy(c->comm_stream); }
     for (cudaEvent_t e : {c->ev_mask, c->ev_delta, c->ev_eps}) if (e) cudaEventDestroy(e);
     for (auto& e : c->pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
@@ -415,11 +506,11 @@ mpc_status mpc_reveal(mpc_ctx c, const uint64_t* share, uint64_t* out, int64_t n
     if (n == 0) return MPC_OK;
     if (!share || !out) return fail(c, MPC_ERR_ARG, "reveal: null pointer");
     if (c->all) return run(c, kClsSplit, "reveal_sum", [&] { return launch_sum_parties(share, c->P, n, out, c->stream); });
-    if (c->P == 1 && !c->comm) {
+    if (c->P == 1 && !has_comm(c)) {
         cudaError_t e = cudaMemcpyAsync(out, share, 8 * (size_t)n, cudaMemcpyDeviceToDevice, c->stream);
         return e == cudaSuccess ? MPC_OK : fail(c, MPC_ERR_CUDA, "reveal copy: %s", cudaGetErrorString(e));
     }
-    return nccl_allreduce(c, share, out, (size_t)n, ncclUint64, "reveal");
+    return comm_allreduce(c, share, out, (size_t)n, RedOp::SumU64, "reveal");
 }
 
 size_t mpc_ttp_workspace_bytes(mpc_ctx c, int64_t M, int64_t K, int64_t N) {
@@ -498,13 +589,13 @@ mpc_status mpc_beaver_matmul(mpc_ctx c, const uint64_t* x, const uint64_t* y, co
         LeftSplitArgs L{M, K, sMK, x, a, c->P, w.eps_pl, a, c->P, w.a_pl, w.a_stride, w.swap};
         RightSplitArgs R{K, N, sKN, y, b, c->P, w.delta_pl, b, c->P, 1, w.b_pl, w.b_stride, w.swap};
         CHECK(run(c, kClsSplit, "mask+reveal+split", [&] { return launch_split_both(L, R, c->stream); }));
-    } else if (c->comm) {
+    } else if (has_comm(c)) {
         CHECK(beaver_overlapped(c, w, x, y, a, b, cc, z, M, K, N, truncate));
         if (truncate && c->P > 2) CHECK(truncate_impl(c, z, sMN, c->frac, wrap_id, w.zbuf, w.hbuf));
         return MPC_OK;
     } else {
         CHECK(run(c, kClsSplit, "mask", [&] { return launch_mask(x, a, sMK, y, b, sKN, w.ed, c->stream); }));
-        if (c->P > 1) CHECK(nccl_allreduce(c, w.ed, w.ed, (size_t)(sMK + sKN), ncclUint64, "eps/delta reveal"));
+        if (c->P > 1) CHECK(comm_allreduce(c, w.ed, w.ed, (size_t)(sMK + sKN), RedOp::SumU64, "eps/delta reveal"));
     }
     CHECK(beaver_local(c, w, w.ed, a, b, cc, z, M, K, N, truncate));
     if (truncate && c->P > 2) CHECK(truncate_impl(c, z, sMN, c->frac, wrap_id, w.zbuf, w.hbuf));
@@ -670,7 +761,7 @@ mpc_status beaver_elementwise(mpc_ctx c, bool square, const uint64_t* x, const u
         CHECK(run(c, kClsSplit, "mask", [&] {
             return launch_mask(x, a, n, square ? nullptr : y, square ? nullptr : b, square ? 0 : n, ed, c->stream);
         }));
-        if (c->P > 1) CHECK(nccl_allreduce(c, ed, ed, (size_t)nrev, ncclUint64, "eps/delta reveal"));
+        if (c->P > 1) CHECK(comm_allreduce(c, ed, ed, (size_t)nrev, RedOp::SumU64, "eps/delta reveal"));
         CHECK(run(c, kClsSplit, what, [&] {
             return launch_beaver_elementwise_finish(square, ed, a, b, cc, z, n, c->rank == 0, bits, c->stream);
         }));
@@ -746,7 +837,7 @@ mpc_status mpc_reveal_batch(mpc_ctx c, int count, const uint64_t* const* shares,
                                  [&] { return launch_sum_parties(shares[t], c->P, ns[t], outs[t], c->stream); }));
         return MPC_OK;
     }
-    if (c->P == 1 && !c->comm) {
+    if (c->P == 1 && !has_comm(c)) {
         for (int t = 0; t < count; ++t) {
             if (!ns[t]) continue;
             cudaError_t e = cudaMemcpyAsync(outs[t], shares[t], 8 * (size_t)ns[t], cudaMemcpyDeviceToDevice, c->stream);
@@ -754,7 +845,12 @@ mpc_status mpc_reveal_batch(mpc_ctx c, int count, const uint64_t* const* shares,
         }
         return MPC_OK;
     }
-    if (!c->comm) return fail(c, MPC_ERR_STATE, "reveal_batch: context has no communicator (created without nccl_id)");
+    if (!has_comm(c)) return fail(c, MPC_ERR_STATE, "reveal_batch: context has no communicator (created without nccl_id)");
+    if (c->lg) {
+        for (int t = 0; t < count; ++t)
+            if (ns[t]) CHECK(comm_allreduce(c, shares[t], outs[t], (size_t)ns[t], RedOp::SumU64, "reveal_batch"));
+        return MPC_OK;
+    }
     ncclResult_t r = ncclGroupStart();
     for (int t = 0; t < count && r == ncclSuccess; ++t)
         if (ns[t]) r = ncclAllReduce(shares[t], outs[t], (size_t)ns[t], ncclUint64, ncclSum, c->comm, c->stream);
@@ -853,7 +949,7 @@ mpc_status mpc_beaver_conv2d(mpc_ctx c, const mpc_conv2d_geom* gg, const uint64_
         CHECK(conv_split(c, w, g, x, a, c->P, na, a, c->P, y, b, nb, b, 1));
     } else {
         CHECK(run(c, kClsSplit, "mask", [&] { return launch_mask(x, a, na, y, b, nb, w.ed, c->stream); }));
-        if (c->P > 1) CHECK(nccl_allreduce(c, w.ed, w.ed, (size_t)(na + nb), ncclUint64, "eps/delta reveal"));
+        if (c->P > 1) CHECK(comm_allreduce(c, w.ed, w.ed, (size_t)(na + nb), RedOp::SumU64, "eps/delta reveal"));
         CHECK(conv_split(c, w, g, w.ed, nullptr, 1, 0, a, 1, w.ed + na, nullptr, 0, b, c->rank == 0));
     }
     CHECK(conv_gemm(c, w, g, cc, z, truncate, Pl));
@@ -934,19 +1030,71 @@ mpc_status mpc_ttp_conv_triples(mpc_ctx c, uint64_t id, const mpc_conv2d_geom* g
 }
 
 // ---------------------------------------------------------------- ReLU
+}  // extern "C"
+namespace {
+// One party per context: leaf binary sharing (0 rounds), then for every height
+// of the adder tree 7 XOR reveals between the 8 adder steps, the B2A bit reveal
+// (packed, 1 bit per element) and the multiplication's sum reveal.  Work
+// buffers live in the context scratch: V [P][n], G and Pr [nodes][n], the
+// reveal buffer [4][nodes][n] (>= [2][n]) and the packed bits.
+mpc_status relu_one_party(mpc_ctx c, const uint64_t* x, uint64_t* out, int64_t n, uint64_t id, uint64_t* sign_out) {
+    std::vector<std::vector<ReluNode>> H;
+    relu_tree_nodes(c->P, id, H);
+    size_t kmax = 0;
+    for (auto& h : H) kmax = std::max(kmax, h.size());
+    const size_t un = 8 * (size_t)n;
+    const size_t nV = align256(un * c->P), nGP = align256(un * kmax), nED = align256(un * std::max<size_t>(4 * kmax, 2));
+    const int64_t nw = relu_zbits_words(n);
+    CHECK(ensure_scratch(c, nV + 2 * nGP + nED + align256(8 * (size_t)nw)));
+    Carve cv(c->scratch);
+    uint64_t* V = reinterpret_cast<uint64_t*>(cv.take(un * c->P));
+    uint64_t* G = reinterpret_cast<uint64_t*>(cv.take(un * kmax));
+    uint64_t* Pr = reinterpret_cast<uint64_t*>(cv.take(un * kmax));
+    uint64_t* ED = reinterpret_cast<uint64_t*>(cv.take(un * std::max<size_t>(4 * kmax, 2)));
+    uint64_t* zb = reinterpret_cast<uint64_t*>(cv.take(8 * (size_t)nw));
+    const int P = c->P, p = c->rank;
+    CHECK(run(c, kClsSplit, "relu_leaf", [&] { return launch_relu_leaf(c->kp, P, p, id, x, V, n, c->stream); }));
+    for (auto& nodes : H) {
+        ReluAdderArgs a{};
+        a.kttp = c->kttp; a.P = P; a.p = p; a.nnodes = (int)nodes.size();
+        for (int k = 0; k < a.nnodes; ++k) a.node[k] = nodes[k];
+        a.V = V; a.G = G; a.Pr = Pr; a.ED = ED; a.n = n;
+        for (int l = 0; l <= 7; ++l) {
+            CHECK(run(c, kClsSplit, "relu_adder", [&] { return launch_relu_adder_step(a, l, c->stream); }));
+            if (l == 7) break;
+            const size_t words = (size_t)n * a.nnodes * ((l == 0 || l == 6) ? 2 : 4);
+            c->bytes += 8ull * words;
+            CHECK(comm_allreduce(c, ED, ED, words, RedOp::XorU64, "relu AND reveal"));
+        }
+    }
+    CHECK(run(c, kClsSplit, "relu_b2a",
+              [&] { return launch_relu_b2a_mask(c->kttp, P, p, id, V, zb, n, c->stream); }));
+    c->bytes += 8ull * (uint64_t)nw;
+    CHECK(comm_allreduce(c, zb, zb, (size_t)nw, RedOp::XorU64, "relu B2A reveal"));
+    CHECK(run(c, kClsSplit, "relu_b2a_mul",
+              [&] { return launch_relu_b2a_mul_mask(c->kttp, P, p, id, zb, x, ED, sign_out, n, c->stream); }));
+    c->bytes += 16ull * (uint64_t)n;
+    CHECK(comm_allreduce(c, ED, ED, 2 * (size_t)n, RedOp::SumU64, "relu multiplication reveal"));
+    return run(c, kClsSplit, "relu_mul",
+               [&] { return launch_relu_mul_finish(c->kttp, P, p, id, ED, out, n, c->stream); });
+}
+}  // namespace
+extern "C" {
+
 mpc_status mpc_relu(mpc_ctx c, const uint64_t* x, uint64_t* out, int64_t n, uint64_t relu_id, uint64_t* sign_out) {
     CHECK(enter(c));
     if (n < 0) return fail(c, MPC_ERR_SHAPE, "relu: n < 0");
     if (relu_id >> 32) return fail(c, MPC_ERR_ARG, "relu: relu_id must be < 2^32 (R24 gate ids)");
-    if (!c->all) return fail(c, MPC_ERR_UNSUPPORTED, "relu: one-party contexts are not supported yet");
-    if (c->P > 8) return fail(c, MPC_ERR_UNSUPPORTED, "relu: at most 8 parties");
+    if (c->all && c->P > 8) return fail(c, MPC_ERR_UNSUPPORTED, "relu: at most 8 parties on one device");
     int levels = 0;
     for (int q = 1; q < c->P; q *= 2) levels++;
     c->rounds += (uint64_t)(7 * levels + 2);       // A2B adders, B2A, multiplication (R25)
     if (n == 0) return MPC_OK;
     if (!x || !out) return fail(c, MPC_ERR_ARG, "relu: null pointer");
-    return run(c, kClsSplit, "relu",
-               [&] { return launch_relu_all(c->kp, c->kttp, relu_id, c->P, x, out, sign_out, n, c->stream); });
+    if (c->all)
+        return run(c, kClsSplit, "relu",
+                   [&] { return launch_relu_all(c->kp, c->kttp, relu_id, c->P, x, out, sign_out, n, c->stream); });
+    return relu_one_party(c, x, out, n, relu_id, sign_out);
 }
 
 mpc_status mpc_profile_enable(mpc_ctx c, int enable) {

@@ -63,12 +63,38 @@ def nccl_unique_id() -> bytes:
     return _native.nccl_unique_id()
 
 
+class Group:
+    """An mpc_group: P one-party contexts of this process whose reveals meet in
+    a host rendezvous instead of NCCL (mpc_create_local).  Drive each party's
+    Context from its own thread; destroy the contexts before the group."""
+
+    def __init__(self, world_size: int):
+        self._lib = _native.lib()
+        self.P = world_size
+        h = ctypes.c_void_p()
+        st = self._lib.mpc_group_create(ctypes.byref(h), world_size)
+        if st != 0:
+            raise MpcError(st, "mpc_group_create failed")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.mpc_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Context:
     """An mpc_ctx: one party of P (rank >= 0) or all P parties (rank = ALL_PARTIES) on `device`."""
 
     def __init__(self, world_size: int, rank: int = ALL_PARTIES, device: int = 0,
                  master_seed: int = 210900984, frac_bits: int = DEFAULT_FRAC_BITS,
-                 nccl_id: Optional[bytes] = None):
+                 nccl_id: Optional[bytes] = None, group: Optional["Group"] = None):
         self._lib = _native.lib()
         self.P = world_size
         self.rank = rank
@@ -79,8 +105,15 @@ class Context:
         idbuf = None
         if nccl_id is not None:
             idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
-        st = self._lib.mpc_create(ctypes.byref(h), world_size, rank, device, idbuf,
-                                  ctypes.c_uint64(master_seed), frac_bits)
+        self._group = group               # keeps the group alive while this party is attached
+        if group is not None:
+            if group.P != world_size:
+                raise ValueError(f"group of {group.P} parties, world_size {world_size}")
+            st = self._lib.mpc_create_local(ctypes.byref(h), group._h, rank, device, ctypes.c_uint64(master_seed),
+                                            frac_bits)
+        else:
+            st = self._lib.mpc_create(ctypes.byref(h), world_size, rank, device, idbuf,
+                                      ctypes.c_uint64(master_seed), frac_bits)
         if st != 0:
             raise MpcError(st, "mpc_create failed (needs an sm_100 GPU; nccl_id for one party per GPU)")
         self._h = h
