@@ -181,6 +181,27 @@ mpc_status mpc_beaver_finish(mpc_ctx ctx, const uint64_t* ed, const uint64_t* a,
                              const uint64_t* c, uint64_t* z, int64_t M, int64_t K, int64_t N,
                              int truncate, void* workspace, size_t workspace_bytes);
 
+/* ---- the Beaver matmul in two halves: weights known ahead ------
+ * mpc_beaver_prepare is the input-independent y side: d_p = y_p - b_p, delta =
+ * reveal(d) (1 round, 8KN bytes), and the limb planes of delta and of
+ * b'_p = b_p + [p = 0] delta, kept in `workspace`.  mpc_beaver_matmul_prepared is
+ * the x side on the SAME workspace: eps = reveal(x - a) (1 round, 8MK bytes),
+ * the split of eps and a_p, the ring GEMM z_p = c_p + a_p @ delta + eps @ b'_p and
+ * the truncation (+ Alg. 1's round when P > 2 and truncate).  Together they give
+ * exactly mpc_beaver_matmul's shares for the same inputs and triple.  delta
+ * depends only on y and the triple, so a model's weight-side prepares can run
+ * ahead of the activations — e.g. on another stream beside the previous
+ * layer's GEMM; one workspace per prepared operand (mpc_workspace_bytes(M, K, N)
+ * bytes; M, K, N must be the same in both calls — M fixes the GEMM orientation),
+ * not reused before the prepared matmul has run.  One-party contexts: delta is
+ * revealed in prepare; the prepared matmul reveals eps on the comm stream while
+ * a_p @ delta already runs.  Errors as mpc_beaver_matmul. */
+mpc_status mpc_beaver_prepare(mpc_ctx ctx, const uint64_t* y, const uint64_t* b, int64_t M, int64_t K, int64_t N,
+                              void* workspace, size_t workspace_bytes);
+mpc_status mpc_beaver_matmul_prepared(mpc_ctx ctx, const uint64_t* x, const uint64_t* a, const uint64_t* c,
+                                      uint64_t* z, int64_t M, int64_t K, int64_t N, int truncate,
+                                      uint64_t wrap_id, void* workspace, size_t workspace_bytes);
+
 /* ---- truncation by 2^bits (App. A.1.1 "Truncation") ----------
  * In place on x (n or [P][n]).  bits in [1, 62].  P <= 2: out_p =
  * (signed(x_p) >> bits) + bit_{bits-1}(x_p) (0 rounds).  P > 2: Alg. 1 with the wrap

@@ -244,6 +244,8 @@ void set_out(RingGemmParams& p, const BeaverWs& w, int64_t M, int64_t N) {
 mpc_status beaver_local(mpc_ctx c, const BeaverWs& w, const uint64_t* ed, const uint64_t* a, const uint64_t* b,
                         const uint64_t* cc, uint64_t* z, int64_t M, int64_t K, int64_t N, int truncate);
 mpc_status gemm_run(mpc_ctx c, RingGemmParams& p, int parties);
+mpc_status beaver_gemm(mpc_ctx c, const BeaverWs& w, const uint64_t* cc, uint64_t* z, int64_t M, int64_t K,
+                       int64_t N, int truncate);
 
 // One party per GPU with a communicator: the reveal overlaps the GEMM terms
 // that do not need it.  Comm stream: delta is revealed first,
@@ -628,6 +630,88 @@ mpc_status mpc_beaver_finish(mpc_ctx c, const uint64_t* ed, const uint64_t* a, c
     return beaver_local(c, w, ed, a, b, cc, z, M, K, N, truncate);
 }
 
+// ---- the input-independent y side (weights known ahead), then the x side ----
+mpc_status mpc_beaver_prepare(mpc_ctx c, const uint64_t* y, const uint64_t* b, int64_t M, int64_t K, int64_t N,
+                              void* ws, size_t ws_bytes) {
+    CHECK(enter(c));
+    if (M < 0 || K < 0 || N < 0) return fail(c, MPC_ERR_SHAPE, "beaver_prepare: negative size");
+    if (K > (int64_t)1 << 30 || M > (int64_t)1 << 31 || N > (int64_t)1 << 31) return fail(c, MPC_ERR_SHAPE, "beaver_prepare: too large");
+    const BeaverWs w = carve_beaver(c, ws, M, K, N);
+    if (ws_bytes < w.total) return fail(c, MPC_ERR_SHAPE, "beaver_prepare: workspace %zu < %zu", ws_bytes, w.total);
+    const int Pl = c->all ? c->P : 1;
+    const int64_t sMK = M * K, sKN = K * N;
+    c->rounds += 1;                                   // the delta reveal (input-independent)
+    c->bytes += 8ull * (uint64_t)sKN * Pl;
+    if (M == 0 || N == 0) return MPC_OK;
+    if ((sKN && (!y || !b)) || (!ws && w.total)) return fail(c, MPC_ERR_ARG, "beaver_prepare: null pointer");
+    if (c->all) {
+        RightSplitArgs R{K, N, sKN, y, b, c->P, w.delta_pl, b, c->P, 1, w.b_pl, w.b_stride, w.swap};
+        return run(c, kClsSplit, "prepare: mask+reveal+split delta", [&] { return launch_split_right(R, c->stream); });
+    }
+    uint64_t* d = w.ed + sMK;
+    CHECK(run(c, kClsSplit, "prepare: mask", [&] { return launch_mask(nullptr, nullptr, 0, y, b, sKN, d, c->stream); }));
+    if (c->P > 1) CHECK(comm_allreduce(c, d, d, (size_t)sKN, RedOp::SumU64, "delta reveal"));
+    RightSplitArgs R{K, N, 0, d, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0, w.swap};
+    return run(c, kClsSplit, "prepare: split delta", [&] { return launch_split_right(R, c->stream); });
+}
+
+mpc_status mpc_beaver_matmul_prepared(mpc_ctx c, const uint64_t* x, const uint64_t* a, const uint64_t* cc, uint64_t* z,
+                                      int64_t M, int64_t K, int64_t N, int truncate, uint64_t wrap_id, void* ws,
+                                      size_t ws_bytes) {
+    CHECK(enter(c));
+    if (M < 0 || K < 0 || N < 0) return fail(c, MPC_ERR_SHAPE, "beaver_matmul_prepared: negative size");
+    if (K > (int64_t)1 << 30 || M > (int64_t)1 << 31 || N > (int64_t)1 << 31) return fail(c, MPC_ERR_SHAPE, "beaver_matmul_prepared: too large");
+    const BeaverWs w = carve_beaver(c, ws, M, K, N);
+    if (ws_bytes < w.total) return fail(c, MPC_ERR_SHAPE, "beaver_matmul_prepared: workspace %zu < %zu", ws_bytes, w.total);
+    const int Pl = c->all ? c->P : 1;
+    const int64_t sMK = M * K, sMN = M * N;
+    c->rounds += 1;                                   // the eps reveal
+    c->bytes += 8ull * (uint64_t)sMK * Pl;
+    if (M == 0 || N == 0) return MPC_OK;
+    if ((sMK && (!x || !a)) || !cc || !z || (!ws && w.total)) return fail(c, MPC_ERR_ARG, "beaver_matmul_prepared: null pointer");
+    if (c->all) {
+        LeftSplitArgs L{M, K, sMK, x, a, c->P, w.eps_pl, a, c->P, w.a_pl, w.a_stride, w.swap};
+        CHECK(run(c, kClsSplit, "mask+reveal+split eps", [&] { return launch_split_left(L, c->stream); }));
+        CHECK(beaver_gemm(c, w, cc, z, M, K, N, truncate));
+    } else if (!has_comm(c)) {
+        if (c->P > 1) return fail(c, MPC_ERR_STATE, "beaver_matmul_prepared: context has no communicator");
+        LeftSplitArgs L{M, K, 0, x, a, 1, w.eps_pl, a, 1, w.a_pl, 0, w.swap};
+        CHECK(run(c, kClsSplit, "mask+split eps", [&] { return launch_split_left(L, c->stream); }));
+        CHECK(beaver_gemm(c, w, cc, z, M, K, N, truncate));
+    } else {
+        // eps revealed on the comm stream while a_p is split and z = c_p + a_p @ delta
+        // runs on the SMs the reveal leaves free; then eps @ b'_p (as beaver_overlapped)
+        CHECK(run(c, kClsSplit, "mask", [&] { return launch_mask(x, a, sMK, nullptr, nullptr, 0, w.ed, c->stream); }));
+        cudaEventRecord(c->ev_mask, c->stream);
+        cudaStreamWaitEvent(c->comm_stream, c->ev_mask, 0);
+        CHECK(comm_allreduce(c, w.ed, w.ed, (size_t)sMK, RedOp::SumU64, "eps reveal", c->comm_stream));
+        cudaEventRecord(c->ev_eps, c->comm_stream);
+        LeftSplitArgs La{M, K, 0, nullptr, nullptr, 0, nullptr, a, 1, w.a_pl, 0, w.swap};
+        CHECK(run(c, kClsSplit, "split a", [&] { return launch_split_left(La, c->stream); }));
+        RingGemmParams p1{};
+        p1.seg[0] = seg_of(w, w.a_pl, 0, w.delta_pl, 0, (int)num_kb(K));
+        p1.nseg = 1;
+        set_out(p1, w, M, N);
+        p1.C = cc; p1.Z = z;
+        p1.partials = w.partials;
+        p1.max_clusters = kOverlapClusters;
+        CHECK(gemm_run(c, p1, 1));
+        cudaStreamWaitEvent(c->stream, c->ev_eps, 0);
+        LeftSplitArgs Le{M, K, 0, w.ed, nullptr, 1, w.eps_pl, nullptr, 0, nullptr, 0, w.swap};
+        CHECK(run(c, kClsSplit, "split eps", [&] { return launch_split_left(Le, c->stream); }));
+        RingGemmParams p2{};
+        p2.seg[0] = seg_of(w, w.eps_pl, 0, w.b_pl, 0, (int)num_kb(K));
+        p2.nseg = 1;
+        set_out(p2, w, M, N);
+        p2.C = z; p2.Z = z;
+        p2.trunc_bits = (truncate && c->P <= 2) ? c->frac : 0;
+        p2.partials = w.partials;
+        CHECK(gemm_run(c, p2, 1));
+    }
+    if (truncate && c->P > 2) CHECK(truncate_impl(c, z, sMN, c->frac, wrap_id, w.zbuf, w.hbuf));
+    return MPC_OK;
+}
+
 }  // extern "C"
 
 namespace {
@@ -638,13 +722,21 @@ namespace {
 // already produced the planes).
 mpc_status beaver_local(mpc_ctx c, const BeaverWs& w, const uint64_t* ed, const uint64_t* a, const uint64_t* b,
                         const uint64_t* cc, uint64_t* z, int64_t M, int64_t K, int64_t N, int truncate) {
-    const int Pl = c->all ? c->P : 1;
-    const int64_t sMK = M * K, sMN = M * N;
+    const int64_t sMK = M * K;
     if (!c->all) {
         LeftSplitArgs L{M, K, 0, ed, nullptr, 1, w.eps_pl, a, 1, w.a_pl, 0, w.swap};
         RightSplitArgs R{K, N, 0, ed + sMK, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0, w.swap};
         CHECK(run(c, kClsSplit, "split eps/delta", [&] { return launch_split_both(L, R, c->stream); }));
     }
+    return beaver_gemm(c, w, cc, z, M, K, N, truncate);
+}
+
+// The ring GEMM of the Beaver step from the limb planes in the workspace:
+// z_p = c_p + a_p @ delta + eps @ b'_p (all parties of the context), truncated if P <= 2.
+mpc_status beaver_gemm(mpc_ctx c, const BeaverWs& w, const uint64_t* cc, uint64_t* z, int64_t M, int64_t K,
+                       int64_t N, int truncate) {
+    const int Pl = c->all ? c->P : 1;
+    const int64_t sMN = M * N;
     RingGemmParams p{};
     p.seg[0] = seg_of(w, w.a_pl, w.a_stride, w.delta_pl, 0, (int)num_kb(K));   // a_p @ delta
     p.seg[1] = seg_of(w, w.eps_pl, 0, w.b_pl, w.b_stride, (int)num_kb(K));     // eps @ b'_p

@@ -63,6 +63,13 @@ def nccl_unique_id() -> bytes:
     return _native.nccl_unique_id()
 
 
+class Prepared:
+    """A prepared y operand (delta and b'_p limb planes) of an M x K x N Beaver matmul."""
+
+    def __init__(self, M: int, K: int, N: int, ws: torch.Tensor):
+        self.M, self.K, self.N, self.ws = M, K, N, ws
+
+
 class Group:
     """An mpc_group: P one-party contexts of this process whose reveals meet in
     a host rendezvous instead of NCCL (mpc_create_local).  Drive each party's
@@ -213,6 +220,33 @@ class Context:
         self._call(self._lib.mpc_beaver_matmul, _ptr(x), _ptr(y), _ptr(a), _ptr(b), _ptr(c), _ptr(z),
                    ctypes.c_int64(M), ctypes.c_int64(K), ctypes.c_int64(N), int(bool(truncate)),
                    ctypes.c_uint64(wrap_id), _ptr(ws), ctypes.c_size_t(ws.numel()))
+        return z
+
+    def beaver_prepare(self, y, b, M: int, out: Optional["Prepared"] = None) -> "Prepared":
+        """The input-independent y side of a Beaver matmul with M x-rows (delta
+        reveal + splits, mpc_beaver_prepare); returns the prepared operand, whose
+        own workspace feeds beaver_matmul_prepared (`out`: reuse its workspace)."""
+        K, N = y.shape[-2], y.shape[-1]
+        if out is not None:
+            if (out.M, out.K, out.N) != (M, K, N):
+                raise ValueError("prepared operand of another shape")
+            ws = out.ws
+        else:
+            ws = torch.empty(max(self.workspace_bytes(M, K, N), 256), dtype=torch.uint8, device=self.device)
+        self._call(self._lib.mpc_beaver_prepare, _ptr(y), _ptr(b), ctypes.c_int64(M), ctypes.c_int64(K),
+                   ctypes.c_int64(N), _ptr(ws), ctypes.c_size_t(ws.numel()))
+        return out if out is not None else Prepared(M, K, N, ws)
+
+    def beaver_matmul_prepared(self, x, a, c, prep: "Prepared", truncate: bool = True, wrap_id: int = 0,
+                               out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """The x side on a prepared y operand (mpc_beaver_matmul_prepared)."""
+        M, K, N = prep.M, prep.K, prep.N
+        if x.shape[-2:] != (M, K):
+            raise ValueError(f"x {tuple(x.shape)} does not match the prepared {M} x {K}")
+        z = out if out is not None else _u64(self._lead() + (M, N), self.device)
+        self._call(self._lib.mpc_beaver_matmul_prepared, _ptr(x), _ptr(a), _ptr(c), _ptr(z), ctypes.c_int64(M),
+                   ctypes.c_int64(K), ctypes.c_int64(N), int(bool(truncate)), ctypes.c_uint64(wrap_id),
+                   _ptr(prep.ws), ctypes.c_size_t(prep.ws.numel()))
         return z
 
     def beaver_mask(self, x, y, a, b) -> torch.Tensor:

@@ -63,8 +63,13 @@ def run_layer(ctx, M, K, N, reps, graph):
     return ms, (gemm_ms / reps if not graph else None)
 
 
-def run_chain(ctx, layers, reps):
-    """All layers of one model in one CUDA graph; returns ms per pass."""
+def run_chain(ctx, layers, reps, prepared=False):
+    """All layers of one model in one CUDA graph; returns ms per pass.
+
+    prepared: the weight side of every private matmul (delta reveal, delta and
+    b'_p splits: mpc_beaver_prepare) runs on a second stream, in layer order,
+    beside the activation chain (mpc_beaver_matmul_prepared, which waits for its
+    layer's prepare) — all inside the same graph and timed region."""
     dev = torch.device("cuda", 0)
     bufs = []
     for i, (_, M, K, N, count) in enumerate(layers):
@@ -73,16 +78,38 @@ def run_chain(ctx, layers, reps):
         x = ctx.share(torch.from_numpy(X.view(np.int64)).to(dev).view(torch.uint64), 0, 1 + 2 * i)
         y = ctx.share(torch.from_numpy(Y.view(np.int64)).to(dev).view(torch.uint64), 1, 2 + 2 * i)
         a, b, c = ctx.ttp_triples(1 + i, M, K, N)
-        bufs.append((x, y, a, b, c, torch.empty_like(c), count))
+        preps = [ctx.beaver_prepare(y, b, M) for _ in range(count)] if prepared else None
+        bufs.append((x, y, a, b, c, torch.empty_like(c), count, preps))
+
+    side = torch.cuda.Stream(priority=0) if prepared else None
 
     def chain():
-        for x, y, a, b, c, z, count in bufs:
-            for _ in range(count):
-                ctx.beaver_matmul(x, y, a, b, c, truncate=True, out=z)
+        if not prepared:
+            for x, y, a, b, c, z, count, _ in bufs:
+                for _ in range(count):
+                    ctx.beaver_matmul(x, y, a, b, c, truncate=True, out=z)
+            return
+        main = torch.cuda.current_stream()
+        side.wait_stream(main)
+        evs = []
+        with torch.cuda.stream(side):
+            for x, y, a, b, c, z, count, preps in bufs:
+                for r in range(count):
+                    ctx.beaver_prepare(y, b, x.shape[-2], out=preps[r])
+                    e = torch.cuda.Event()
+                    e.record(side)
+                    evs.append(e)
+        k = 0
+        for x, y, a, b, c, z, count, preps in bufs:
+            for r in range(count):
+                main.wait_event(evs[k])
+                k += 1
+                ctx.beaver_matmul_prepared(x, a, c, preps[r], truncate=True, out=z)
+        main.wait_stream(side)
 
     chain()
     torch.cuda.synchronize()
-    s = torch.cuda.Stream()
+    s = torch.cuda.Stream(priority=-1) if prepared else torch.cuda.Stream()
     with torch.cuda.stream(s):
         chain()
         torch.cuda.synchronize()
@@ -168,6 +195,8 @@ def main():
     ap.add_argument("--graph", action="store_true")
     ap.add_argument("--chain", action="store_true")
     ap.add_argument("--conv", action="store_true", help="true private convolutions (conv triples) for CNNs")
+    ap.add_argument("--prepared", action="store_true",
+                    help="chain: weight sides prepared on a second stream beside the activation chain")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     ctx = mpc.Context(2, mpc.ALL_PARTIES, device=0, master_seed=synth.MASTER_SEED)
@@ -191,14 +220,16 @@ def main():
                   f"(im2col-shape reveal would be {rb_im2col / 1e6:.0f} MB)", flush=True)
             continue
         if args.chain:
-            ms = run_chain(ctx, layers, args.reps)
+            ms = run_chain(ctx, layers, args.reps, prepared=args.prepared)
             ops = sum(2.0 * M * K * N * cnt for _, M, K, N, cnt in layers)
             n = sum(cnt for *_, cnt in layers)
             tg = sum(t_gemm_ms(M, K, N) * cnt for _, M, K, N, cnt in layers)
-            out[name] = {"chain_ms": ms, "private_matmuls": n, "ring_TOPS": ops / (ms * 1e-3) / 1e12,
-                         "roofline_ms": tg, "roofline_frac": tg / ms,
-                         "graph": "one CUDA graph per model"}
-            print(f"{name}: chain of {n} private matmuls {ms:.3f} ms ({out[name]['ring_TOPS']:.2f} ring-TOPS, "
+            key = name + ("_prepared" if args.prepared else "")
+            out[key] = {"chain_ms": ms, "private_matmuls": n, "ring_TOPS": ops / (ms * 1e-3) / 1e12,
+                        "roofline_ms": tg, "roofline_frac": tg / ms,
+                        "graph": "one CUDA graph per model" + (
+                            "; weight sides (delta reveal + splits) on a second stream" if args.prepared else "")}
+            print(f"{key}: chain of {n} private matmuls {ms:.3f} ms ({out[key]['ring_TOPS']:.2f} ring-TOPS, "
                   f"limb-GEMM roofline {tg:.3f} ms = {tg / ms:.3f})", flush=True)
             continue
         rows, total_ms, total_ops = [], 0.0, 0.0

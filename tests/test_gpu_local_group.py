@@ -222,3 +222,22 @@ def test_collective_contract_mismatch_fails_everywhere(mpc):
         return 0
 
     assert run_parties(mpc, P, body) == [2, 2]                 # MPC_ERR_SHAPE on both parties
+
+
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("M,K,N", [(64, 64, 64), (300, 100, 260), (49, 700, 300)])
+def test_beaver_prepared_one_party(mpc, P, M, K, N):
+    """Weight side prepared (delta reveal) ahead, then eps revealed on the comm
+    stream overlapping a_p @ delta: the one-call shares bit for bit."""
+    X = synth.uniform_fixed((M, K), M + 5)
+    Y = synth.uniform_fixed((K, N), N + 6)
+    xs, ys = oracle.share(P, MASTER, X, 0, 11), oracle.share(P, MASTER, Y, 1, 12)
+    a, b, cc = oracle.ttp_triple(P, MASTER, 13, M, K, N)
+
+    def body(c, r):
+        prep = c.beaver_prepare(dev(ys[r]), dev(b[r]), M)
+        z = c.beaver_matmul_prepared(dev(xs[r]), dev(a[r]), dev(cc[r]), prep, truncate=True, wrap_id=4)
+        return host(z)
+
+    z = np.stack(run_parties(mpc, P, body))
+    assert np.array_equal(z, oracle.truncate(oracle.beaver_matmul(xs, ys, a, b, cc), 16, MASTER, wrap_id=4))
