@@ -174,16 +174,20 @@ struct Carve {
     uint8_t* take(size_t n) { uint8_t* p = base ? base + off : nullptr; off += align256(n); return p; }
 };
 
-// The ring GEMM tiles its output in 256 x 128 blocks (rows x columns).  For a
-// small M it computes z^T = delta^T a_p^T + b'_p^T eps^T instead (x-side planes
-// in the right-operand layout, y-side planes in the left one, transposed
-// store) when that needs fewer padded tiles, e.g. M = 49: 256 x 512 -> 512 x 128.
+// The ring GEMM tiles its output in 256 x 128 blocks (rows x columns), or, for
+// at most 32 rows, in stacked-plane 32 x 32 blocks (ring_gemm_small.cu).  It can
+// compute z^T = delta^T a_p^T + b'_p^T eps^T instead (x-side planes in the
+// right-operand layout, y-side planes in the left one, transposed store): the
+// orientation whose GEMM the tensor-time model (ring_gemm_plan) rates cheaper
+// is used, e.g. M = 49, N = 512: 256 x 512 -> 512 x 128 padded tiles.
 // Bit-identical either way (the same ring sums).  MPC_NO_SWAP=1 disables it.
-bool use_swap(int64_t M, int64_t N) {
+bool use_swap(int64_t M, int64_t N, int64_t K, int parties) {
     static const bool off = getenv("MPC_NO_SWAP") != nullptr;
-    if (off) return false;
-    return pad_rows<Layout::Left>(N) * pad_rows<Layout::Right>(M) <
-           pad_rows<Layout::Left>(M) * pad_rows<Layout::Right>(N);
+    if (off || M == N) return false;
+    const int tkb = (int)(2 * num_kb(K));
+    const double straight = ring_gemm_plan(parties, M, N, tkb, 74, true).cycles;
+    const double swapped = ring_gemm_plan(parties, N, M, tkb, 74, true).cycles;
+    return swapped < straight;
 }
 
 // workspace layout of beaver_matmul (see mpc_workspace_bytes)
@@ -206,7 +210,7 @@ BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N, int6
     const int Pl = c->all ? c->P : 1;
     Carve cv(ws);
     BeaverWs w{};
-    w.swap = allow_swap && use_swap(M, N);
+    w.swap = allow_swap && use_swap(M, N, K, Pl);
     if (ed_elems < 0) ed_elems = M * K + K * N;
     const int64_t xs = w.swap ? rp(M, K) : lp(M, K);     // eps, a_p planes (rows = M)
     const int64_t ys = w.swap ? lp(N, K) : rp(N, K);     // delta, b'_p planes (rows = N)

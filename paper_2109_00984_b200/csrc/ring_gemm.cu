@@ -43,6 +43,7 @@
 #include <cuda_runtime.h>
 #include "common.cuh"
 #include "ring_gemm.h"
+#include "tcgen05.cuh"
 
 namespace mpc {
 namespace gemm {
@@ -66,91 +67,8 @@ constexpr uint32_t kIdesc = (2u << 4)             // D format: S32
                           | ((uint32_t)(kTileN >> 3) << 17)
                           | ((uint32_t)(kTileM >> 4) << 24);
 
-// ----------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t cluster_id() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t nclusters() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
-    return r;
-}
-// shared::cluster address of the same smem offset in CTA `rank` of the cluster
-__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-// arrive on the barrier at cluster address `caddr` (possibly in the peer CTA)
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(caddr) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}"
-        :: "r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAITC_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAITC_%=;\n\t}"
-        :: "r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ unsigned long long globaltimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-// The role loops run on whole warps (warp-uniform control flow, so descriptor
-// arithmetic stays in uniform registers); single-thread operations are issued
-// by one lane chosen with elect.sync inside the same asm block.
-__device__ __forceinline__ bool elect_one() {
-    uint32_t e;
-    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(e));
-    return e != 0;
-}
-// commit all prior MMAs of the warp's elected lane; arrive on `bar` (same offset) in both CTAs
-__device__ __forceinline__ void tc_commit_both(uint64_t* bar) {
-    asm volatile(
-        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
-        :: "r"(smem_u32(bar)), "h"((uint16_t)0x3) : "memory");
-}
-// SWIZZLE_NONE K-major descriptor: LBO = 128 B (K halves), SBO = 256 B (8-row groups), version 1
-__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
-    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(128u >> 4) << 16) | ((uint64_t)(256u >> 4) << 32)
-         | (1ull << 46);
-}
+// ----------------------------------------------------------------- PTX helpers (tcgen05.cuh)
+using namespace tc;
 __device__ __forceinline__ void mma_u8_2cta(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p, e;\n\t"
@@ -158,41 +76,6 @@ __device__ __forceinline__ void mma_u8_2cta(uint32_t tmem_d, uint64_t adesc, uin
         "setp.ne.b32 p, %4, 0;\n\t"
         "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}"
         :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate) : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-// c_p reads and z writes stream through L2 once: mark them evict-first so they
-// do not push the K window of limb planes (re-read by the second super-pass) out.
-__device__ __forceinline__ uint64_t evict_first_policy() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ ulonglong2 ld_stream(const uint64_t* p, uint64_t pol) {
-    ulonglong2 v;
-    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
-                 : "=l"(v.x), "=l"(v.y) : "l"(p), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ void st_stream(uint64_t* p, ulonglong2 v, uint64_t pol) {
-    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;"
-                 :: "l"(p), "l"(v.x), "l"(v.y), "l"(pol) : "memory");
-}
-// 32-byte (one full sector) variants; p must be 32-byte aligned
-__device__ __forceinline__ void ld_stream4(const uint64_t* p, uint64_t pol, uint64_t* v) {
-    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u64 {%0, %1, %2, %3}, [%4], %5;"
-                 : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(p), "l"(pol));
-}
-__device__ __forceinline__ void st_stream4(uint64_t* p, const uint64_t* v, uint64_t pol) {
-    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u64 [%0], {%1, %2, %3, %4}, %5;"
-                 :: "l"(p), "l"(v[0]), "l"(v[1]), "l"(v[2]), "l"(v[3]), "l"(pol) : "memory");
 }
 
 // Tile t -> (party, m tile, n tile) in the grouped order: groups of kGroupM row
@@ -616,7 +499,14 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     if (prm.max_clusters > 0 && prm.max_clusters < max_clusters) max_clusters = prm.max_clusters;
     const int tkb = prm.seg[0].kb + (prm.nseg > 1 ? prm.seg[1].kb : 0);
     RingGemmParams q = prm;
-    q.splits = prm.partials ? ring_gemm_choose_splits(tiles, tkb, max_clusters) : 1;
+    const RingGemmPlan plan = ring_gemm_plan(parties, prm.M, prm.N, tkb, max_clusters, prm.partials != nullptr);
+    q.splits = plan.splits;
+    if (plan.small) {
+        if (q.splits > 1) q.partial_stride = ring_gemm_out_elems(q, parties);
+        cudaError_t e = ring_gemm_small_launch(q, parties, 2 * max_clusters, stream);
+        if (e != cudaSuccess || q.splits <= 1) return e;
+        return ring_gemm_finalize(q, parties, stream);
+    }
     if (q.splits > 1) {
         // split-K: partial sums go to per-split slabs, then finalize adds them, c_p, truncates
         q.partial_stride = ring_gemm_out_elems(q, parties);
@@ -685,7 +575,8 @@ size_t ring_gemm_partials_bytes(int parties, int64_t M, int64_t N, int total_kb,
                           (pad_rows<Layout::Right>(N) / gemm::kTileN);
     int64_t clusters = sms / 2;
     if (max_clusters > 0 && max_clusters < clusters) clusters = max_clusters;
-    const int s = ring_gemm_choose_splits(tiles, total_kb, clusters);
+    (void)tiles;
+    const int s = ring_gemm_plan(parties, M, N, total_kb, clusters, true).splits;
     return s > 1 ? (size_t)s * parties * M * N * sizeof(uint64_t) : 0;
 }
 

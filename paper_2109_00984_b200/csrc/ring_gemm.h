@@ -39,6 +39,14 @@ struct RingGemmParams {
                                         // convolution whose im2col rows are (b, pixel s).  C likewise.
 };
 
+// Which kernel runs an M x N x (tkb 32-K blocks) GEMM and its split-K factor:
+// the 2-CTA 256 x 128 kernel, or (M <= 32, when its tensor-time model is lower)
+// the stacked-plane kernel of ring_gemm_small.cu.  split_ok: a partials buffer exists.
+struct RingGemmPlan { bool small; int splits; double cycles; /* tensor-time model, SM-cycles */ };
+RingGemmPlan ring_gemm_plan(int parties, int64_t M, int64_t N, int tkb, int64_t max_clusters, bool split_ok);
+size_t ring_gemm_small_smem_bytes();
+cudaError_t ring_gemm_small_launch(const RingGemmParams& q, int parties, int64_t max_ctas, cudaStream_t stream);
+
 // Largest unit length (32-K blocks) for which every s32 accumulator stays exact.
 int ring_gemm_max_kc();
 // Unit length used for a fused reduction of `total_kb` blocks (L2-window sized).

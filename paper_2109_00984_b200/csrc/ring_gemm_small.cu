@@ -1,0 +1,314 @@
+// ring_gemm_small.cu — the ring GEMM for outputs with at most 32 rows
+// (tcgen05, sm_100a): the limb planes of the left operand are STACKED along
+// the UMMA M dimension instead of padding 32 rows to a 256-row tile.
+//
+// Same product as ring_gemm.cu (Z_p = [C_p] + sum_seg L @ R^T mod 2^64 from
+// u8 limb planes, L = sum_i 2^(8i) L_i, R = sum_j 2^(8j) R_j), computed as
+//     L @ R^T = sum_i sum_{j <= 7-i} 2^(8(i+j)) L_i @ R_j^T      (mod 2^64)
+// with the 32 rows of the 8 planes L_0..L_7 stacked into two 128-row MMA
+// operands: A_lo = [L_0; L_1; L_2; L_3] and A_hi = [L_4; L_5; L_6; L_7]
+// (rows 32 i' + r).  One tcgen05.mma.cta_group::1.kind::i8 (M = 128, N = 32,
+// K = 32) with right plane R_j gives L_i @ R_j^T for four planes i at once, in
+// TMEM lanes 32 i' + r:
+//     D_lo,j = A_lo @ R_j^T  (j = 0..7)     D_hi,j = A_hi @ R_j^T  (j = 0..3)
+// — 12 MMAs per 32-K block (j <= 3 for A_hi: pairs with i + j >= 8 vanish),
+// 12 accumulators of 32 columns in TMEM.  Each epilogue thread owns TMEM lane
+// 32 i' + r (plane i = i' or 4 + i', output row r) and adds
+//     run[c] += D_j[lane][c] << 8(i + j)        (read as u32, i + j <= 7)
+// into u64 running sums; at the tile end the four planes of a row are summed
+// through shared memory and c_p / the truncation applied (the store mapping,
+// split-K slabs and finalize are those of ring_gemm.cu).
+//
+// Exactness: every D entry is a single limb product sum, D <= K_r * 255^2, so
+// the s32 accumulator read as u32 is exact for K_r <= 66052 (2064 32-K
+// blocks, the unit length cap); for i + j >= 4 only D mod 2^(64-8(i+j)) matters.
+//
+// Why: a 256 x 128 tile holding 32 x 32 useful outputs (the 32 x 519,820 x 32
+// text matmul) wastes 31/32 of the tensor work; stacking wastes
+// only the plane pairs with i + j >= 8 that share an MMA with needed ones
+// (12 of the 48 plane products issued per 32-K block).
+//
+// Warp roles (384 threads): warp 0 producer (16 bulk copies of 1 KiB per
+// 32-K block: 8 left-plane row blocks, 8 right-plane row blocks), warp 1 MMA
+// issuer, warp 2 TMEM allocator, warps 4..11 epilogue (two per TMEM lane
+// quadrant, 16 columns each).
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "ring_gemm.h"
+#include "tcgen05.cuh"
+
+namespace mpc {
+namespace gemm_small {
+using namespace tc;
+
+constexpr int kRows = 32;                         // output rows per tile (stacked per plane)
+constexpr int kTileN = 32;                        // output columns per tile (UMMA N)
+constexpr int kChunk = 1024;                      // 32 rows x 32 K bytes of one plane (4 core-matrix row groups)
+constexpr int kStageBytes = 16 * kChunk;          // A: 8 planes, B: 8 planes
+constexpr int kStages = 8;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 128 + 32 * kEpiWarps;
+constexpr int kTmemCols = 512;                    // 12 accumulators x 32 columns used
+constexpr int kMaxUnit = 2048;                    // 32-K blocks per accumulation unit (<= 2064)
+constexpr uint32_t kIdesc = (2u << 4)             // D: S32; A, B: unsigned 8-bit
+                          | ((uint32_t)(kTileN >> 3) << 17)
+                          | ((uint32_t)(128 >> 4) << 24);
+
+__device__ __forceinline__ void mma_u8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+        :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate) : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
+        :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void epi_sync() {           // the 8 epilogue warps only
+    asm volatile("bar.sync 1, %0;" :: "n"(32 * kEpiWarps) : "memory");
+}
+
+// work item w -> (party, column tile, K block range) — all warps compute the same values
+struct Items {
+    int parties, nt, tkb, splits;
+    __device__ int count() const { return parties * nt * splits; }
+    __device__ void decode(int w, int& party, int& n, int& klo, int& khi) const {
+        const int t = w / splits, s = w % splits;
+        party = t % parties;
+        n = t / parties;
+        klo = (int)((int64_t)tkb * s / splits);
+        khi = (int)((int64_t)tkb * (s + 1) / splits);
+    }
+};
+
+__global__ void __launch_bounds__(kThreads, 1) ring_gemm_small_kernel(const __grid_constant__ RingGemmParams p,
+                                                                     int parties) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");
+    uint64_t* red = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);      // [4][32][32] u64 = 32 KiB
+    uint64_t* full = red + 4 * kRows * kTileN;
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    Items it{parties, (int)((p.N + kTileN - 1) / kTileN), p.seg[0].kb + (p.nseg > 1 ? p.seg[1].kb : 0),
+             p.splits < 1 ? 1 : p.splits};
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, kEpiWarps);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(smem_u32(tmem_slot)), "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------ producer
+        asm volatile("griddepcontrol.wait;" ::: "memory");        // planes written by the split kernel
+        int s = 0; uint32_t ph = 0;
+        for (int w = blockIdx.x; w < it.count(); w += gridDim.x) {
+            int party, n, klo, khi;
+            it.decode(w, party, n, klo, khi);
+            const int64_t rbB = n >> 1;                            // 64-row right block
+            const int64_t offB = (int64_t)(n & 1) * kChunk;        // rows 32(n&1)..+31 of that block
+            for (int kt = klo; kt < khi; ++kt) {
+                const int sg = (kt < p.seg[0].kb) ? 0 : 1;
+                const RingGemmSegment& S = p.seg[sg];
+                const int64_t kb = kt - (sg ? p.seg[0].kb : 0);
+                const uint8_t* srcA = S.A + party * S.party_stride_A + kb * (8 * PlaneGeom<Layout::Left>::kBlock);
+                const uint8_t* srcB = S.B + party * S.party_stride_B +
+                                      (rbB * S.kb + kb) * (8 * PlaneGeom<Layout::Right>::kBlock) + offB;
+                mbar_wait(&empty[s], ph ^ 1);
+                uint8_t* st = smem + s * kStageBytes;
+                if (lane == 0) mbar_expect_tx(&full[s], kStageBytes);
+                __syncwarp();
+                if (lane < 8)
+                    bulk_g2s(st + lane * kChunk, srcA + (int64_t)lane * PlaneGeom<Layout::Left>::kBlock, kChunk,
+                             &full[s]);
+                else if (lane < 16)
+                    bulk_g2s(st + lane * kChunk, srcB + (int64_t)(lane - 8) * PlaneGeom<Layout::Right>::kBlock,
+                             kChunk, &full[s]);
+                __syncwarp();
+                if (++s == kStages) { s = 0; ph ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        int s = 0; uint32_t ph = 0; uint32_t u = 0;
+        for (int w = blockIdx.x; w < it.count(); w += gridDim.x) {
+            int party, n, klo, khi;
+            it.decode(w, party, n, klo, khi);
+            for (int k0 = klo; k0 < khi; k0 += kMaxUnit, ++u) {
+                const int k1 = min(khi, k0 + kMaxUnit);
+                mbar_wait(tempty, (u & 1) ^ 1);                     // the epilogue drained the last unit
+                tc_fence_after();
+                for (int kt = k0; kt < k1; ++kt) {
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint64_t da = smem_desc(smem_u32(smem + s * kStageBytes));
+                    const uint64_t db = da + ((8 * kChunk) >> 4);
+                    const uint32_t acc = kt == k0 ? 0u : 1u;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        mma_u8(tmem_base + j * kTileN, da, db + (uint64_t)(j * (kChunk >> 4)), acc);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        mma_u8(tmem_base + (8 + j) * kTileN, da + (uint64_t)((4 * kChunk) >> 4),
+                               db + (uint64_t)(j * (kChunk >> 4)), acc);
+                    tc_commit(&empty[s]);
+                    if (++s == kStages) { s = 0; ph ^= 1; }
+                }
+                tc_commit(tfull);
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------ epilogue
+        const int q = warp & 3;                                    // TMEM lane quadrant = plane i' (i = i' or 4 + i')
+        const int h = (warp - 4) >> 2;                             // column half
+        const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + h * 16;
+        const int et = threadIdx.x - 128;                          // 0..255
+        uint32_t u = 0;
+        for (int w = blockIdx.x; w < it.count(); w += gridDim.x) {
+            int party, n, klo, khi;
+            it.decode(w, party, n, klo, khi);
+            uint64_t run[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) run[c] = 0;
+            for (int k0 = klo; k0 < khi; k0 += kMaxUnit, ++u) {
+                mbar_wait(tfull, u & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int a = 0; a < 12; ++a) {
+                    const int i = a < 8 ? q : 4 + q;                // plane of this lane in accumulator a
+                    const int j = a < 8 ? a : a - 8;
+                    const int sh = i + j;
+                    if (sh > 7) continue;                           // warp-uniform (q is per warp)
+                    uint32_t v[16];
+                    tmem_ld16(tq + a * kTileN, v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) run[c] += (uint64_t)v[c] << (8 * sh);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty);
+            }
+            // sum the four planes of each row (TMEM quadrants) through shared memory
+            uint64_t* mine = red + ((int64_t)q * kRows + lane) * kTileN + h * 16;
+#pragma unroll
+            for (int c = 0; c < 16; c += 2) *reinterpret_cast<ulonglong2*>(mine + c) = make_ulonglong2(run[c], run[c + 1]);
+            epi_sync();
+            const int M = (int)p.M;
+            const int64_t hw = p.out_hw > 0 ? p.out_hw : (p.transpose_out ? p.M : 0);
+            const bool tr = hw > 0;
+            const bool split = it.splits > 1;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int idx = e * 256 + et;                        // consecutive threads: consecutive columns
+                const int r = idx / kTileN, col = idx % kTileN;
+                const int64_t gc = (int64_t)n * kTileN + col;
+                if (r >= M || gc >= p.N) continue;
+                uint64_t v = 0;
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) v += red[((int64_t)qq * kRows + r) * kTileN + col];
+                const int64_t off = tr ? ((int64_t)r / hw) * p.N * hw + r % hw + gc * hw : (int64_t)r * p.N + gc;
+                if (split) {
+                    const int sidx = w % it.splits;
+                    p.partials[(int64_t)sidx * p.partial_stride + party * p.M * p.N + off] = v;
+                } else {
+                    if (p.C) v += p.C[party * p.party_stride_c + off];
+                    if (p.trunc_bits) v = div_pow2_round(v, p.trunc_bits);
+                    p.Z[party * p.party_stride_z + off] = v;
+                }
+            }
+            epi_sync();                                              // red is reused by the next item
+        }
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem_base), "r"(kTmemCols));
+    }
+}
+
+}  // namespace gemm_small
+
+size_t ring_gemm_small_smem_bytes() {
+    return (size_t)gemm_small::kStages * gemm_small::kStageBytes + 4 * 32 * 32 * 8 + 1024 /*align*/ + 256;
+}
+
+// Tensor-time model (cycles, all SMs) of both kernels for an M x N output with
+// tkb 32-K blocks: the 2-CTA kernel runs 36 MMAs of 64 cycles per 256 x 128
+// tile and block on a CTA pair; the stacked one 12 MMAs of ~48 cycles (N = 32
+// MMAs are shared-memory bound) per 32 x 32 tile and block on one SM.
+namespace {
+int64_t waves(int64_t items, int64_t slots) { return (items + slots - 1) / slots; }
+}  // namespace
+
+RingGemmPlan ring_gemm_plan(int parties, int64_t M, int64_t N, int tkb, int64_t max_clusters, bool split_ok) {
+    RingGemmPlan pl{};
+    const int64_t tiles_n = (int64_t)parties * (pad_rows<Layout::Left>(M) / 256) * (pad_rows<Layout::Right>(N) / 128);
+    pl.splits = split_ok ? ring_gemm_choose_splits(tiles_n, tkb, max_clusters) : 1;
+    pl.cycles = (double)waves(tiles_n * pl.splits, max_clusters) * ((tkb + pl.splits - 1) / pl.splits) * 2304.0;
+    static const int env = getenv("MPC_GEMM_SMALL") ? atoi(getenv("MPC_GEMM_SMALL")) : -1;   // 0: off, 1: force
+    if (M > gemm_small::kRows || M < 1 || N < 1 || tkb < 1 || env == 0) return pl;
+    const int64_t ctas = 2 * max_clusters;
+    const int64_t tiles_s = (int64_t)parties * ((N + gemm_small::kTileN - 1) / gemm_small::kTileN);
+    int s_s = 1;
+    if (split_ok && tiles_s < ctas) {
+        s_s = (int)(ctas / tiles_s);
+        if (s_s > 64) s_s = 64;
+        if (s_s > tkb / 8) s_s = tkb / 8;
+        if (s_s < 1) s_s = 1;
+    }
+    const double t_n = pl.cycles;
+    const double t_s = (double)waves(tiles_s * s_s, ctas) * ((tkb + s_s - 1) / s_s) * 12.0 * 48.0;
+    if (env == 1 || t_s < t_n) {
+        pl.small = true;
+        pl.splits = s_s;
+        pl.cycles = t_s;
+    }
+    return pl;
+}
+
+cudaError_t ring_gemm_small_launch(const RingGemmParams& q, int parties, int64_t max_ctas, cudaStream_t stream) {
+    static int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t smem = ring_gemm_small_smem_bytes();
+    if (attr_dev != dev) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_small::ring_gemm_small_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_dev = dev;
+    }
+    if (q.M > gemm_small::kRows) return cudaErrorInvalidValue;
+    const int64_t items = (int64_t)parties * ((q.N + gemm_small::kTileN - 1) / gemm_small::kTileN) *
+                          (q.splits < 1 ? 1 : q.splits);
+    int64_t ctas = items < max_ctas ? items : max_ctas;
+    if (ctas < 1) ctas = 1;
+    return launch_pdl(gemm_small::ring_gemm_small_kernel, dim3((unsigned)ctas), dim3(gemm_small::kThreads), smem,
+                      stream, q, parties);
+}
+
+}  // namespace mpc

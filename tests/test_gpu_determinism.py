@@ -23,7 +23,9 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 P = 2
 SHAPES = [(300, 3000, 700),           # 94 K-blocks per segment, 2 x 6 output tiles, ragged tails
-          (49, 2000, 700)]            # small M: the ring GEMM runs transposed (unless MPC_NO_SWAP)
+          (49, 2000, 700),            # small M: the ring GEMM runs transposed (unless MPC_NO_SWAP)
+          (20, 3000, 300),            # M <= 32: the stacked-plane kernel (unless MPC_GEMM_SMALL=0)
+          (300, 2000, 24)]            # N <= 32: transposed onto the stacked-plane kernel
 
 SCRIPT = r"""
 import hashlib, sys
@@ -64,11 +66,13 @@ def case(request):
     {"MPC_GEMM_SPLITS": "7", "MPC_GEMM_KC": "5"},
     {"MPC_NO_PDL": "1"},
     {"MPC_NO_SWAP": "1"},
+    {"MPC_GEMM_SMALL": "0"},
+    {"MPC_GEMM_SMALL": "1"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 def test_same_shares_under_every_launch_config(case, env):
     (M, K, N), expected = case
     full = dict(os.environ)
-    for k in ("MPC_GEMM_KC", "MPC_GEMM_SPLITS", "MPC_NO_PDL", "MPC_NO_SWAP", "MPC_GEMM_DEBUG"):
+    for k in ("MPC_GEMM_KC", "MPC_GEMM_SPLITS", "MPC_NO_PDL", "MPC_NO_SWAP", "MPC_GEMM_DEBUG", "MPC_GEMM_SMALL"):
         full.pop(k, None)
     full.update(env)
     out = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, M=M, K=K, N=N, P=P)], env=full,

@@ -338,3 +338,36 @@ def test_beaver_prepared_parity(mpc, P, M, K, N):
     z2 = c.beaver_matmul_prepared(dev(xs), dev(a), dev(cc), c.beaver_prepare(dev(ys), dev(b), M), truncate=True,
                                   wrap_id=8)
     assert np.array_equal(host(z2), ez)
+
+
+# ------------------------------------------------------------------ stacked-plane GEMM (M <= 32)
+@pytest.mark.parametrize("M,K,N", [(32, 64, 32), (1, 2048, 1000), (17, 300, 45), (32, 5000, 33), (3, 33, 1),
+                                   (31, 1, 65)])
+def test_small_m_ring_matmul_parity(mpc, M, K, N):
+    """Outputs with <= 32 rows run on the stacked-plane kernel (ring_gemm_small.cu)."""
+    c = ctx(mpc, 1)
+    A = synth.uniform_ring((M, K), 5 + M)
+    B = synth.uniform_ring((K, N), 6 + N)
+    assert np.array_equal(host(c.ring_matmul(dev(A), dev(B))), oracle.ring_matmul(A, B))
+
+
+@pytest.mark.parametrize("K", [2047 * 32, 2048 * 32 + 5, 70000])
+def test_small_m_accumulator_bounds(mpc, K):
+    """All-0xFF limbs: every D entry is K * 255^2; units of 2048 32-K blocks keep
+    the u32 reads exact (C = K since (2^64 - 1)^2 = 1 mod 2^64)."""
+    c = ctx(mpc, 1)
+    A = np.full((32, K), 2 ** 64 - 1, dtype=np.uint64)
+    B = np.full((K, 40), 2 ** 64 - 1, dtype=np.uint64)
+    assert np.all(host(c.ring_matmul(dev(A), dev(B))) == np.uint64(K))
+
+
+@pytest.mark.parametrize("P", [1, 2, 3])
+@pytest.mark.parametrize("M,K,N", [(32, 3000, 32), (1, 768, 1000), (100, 300, 20), (8, 70000, 8)])
+def test_small_m_beaver_parity(mpc, P, M, K, N):
+    c = ctx(mpc, P)
+    X, Y, xs, ys, a, b, cc = _beaver_case(P, M, K, N, seed=M + 2 * N, tid=90 + P)
+    z = c.beaver_matmul(dev(xs), dev(ys), dev(a), dev(b), dev(cc), truncate=True, wrap_id=6)
+    ez = oracle.truncate(oracle.beaver_matmul(xs, ys, a, b, cc), 16, MASTER, wrap_id=6)
+    assert np.array_equal(host(z), ez)
+    ga, gb, gc = c.ttp_triples(90 + P, M, K, N)            # the TTP's c = a @ b on the same kernel
+    assert np.array_equal(host(gc), cc)
