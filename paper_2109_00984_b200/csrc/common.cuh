@@ -68,10 +68,13 @@ __host__ __device__ __forceinline__ uint64_t philox_at(uint64_t key, uint64_t st
 // to 32; the K padding is written as zeros, the row padding is never read
 // into a stored output.
 constexpr int kKBlock = 32;
-enum class Layout : int { Left = 0, Right = 1 };
+enum class Layout : int { Left = 0, Right = 1, Small = 2 };
 template <Layout L> struct PlaneGeom;
 template <> struct PlaneGeom<Layout::Left>  { static constexpr int kRows = 128, kBlock = 128 * 32, kPad = 256; };
 template <> struct PlaneGeom<Layout::Right> { static constexpr int kRows = 64, kBlock = 64 * 32, kPad = 128; };
+// both operands of the stacked-plane GEMM for <= 32 output rows (ring_gemm_small.cu):
+// 32-row blocks, so one (row block, 32-K block) of all 8 planes is 8 KiB contiguous
+template <> struct PlaneGeom<Layout::Small> { static constexpr int kRows = 32, kBlock = 32 * 32, kPad = 32; };
 
 __host__ __device__ __forceinline__ int64_t num_kb(int64_t k) { return (k + kKBlock - 1) / kKBlock; }
 template <Layout L>

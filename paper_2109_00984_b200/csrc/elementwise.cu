@@ -184,7 +184,8 @@ __global__ void __launch_bounds__(256) split_left_kernel(LeftSplitArgs a) {
 cudaError_t launch_split_left(const LeftSplitArgs& a, cudaStream_t st) {
     if (a.M == 0 || a.K == 0) return cudaSuccess;
     const int64_t warps = ((a.M + 7) / 8) * ((num_kb(a.K) * kKBlock + 63) / 64);
-    if (a.swap) split_left_kernel<Layout::Right><<<grid_for(warps * 32), 256, 0, st>>>(a);
+    if (a.swap == 2) split_left_kernel<Layout::Small><<<grid_for(warps * 32), 256, 0, st>>>(a);
+    else if (a.swap) split_left_kernel<Layout::Right><<<grid_for(warps * 32), 256, 0, st>>>(a);
     else split_left_kernel<Layout::Left><<<grid_for(warps * 32), 256, 0, st>>>(a);
     return cudaGetLastError();
 }
@@ -281,7 +282,8 @@ __global__ void __launch_bounds__(256, 2) split_right_kernel(RightSplitArgs a) {
 cudaError_t launch_split_right(const RightSplitArgs& a, cudaStream_t st) {
     if (a.N == 0 || a.K == 0) return cudaSuccess;
     const int64_t warps = ((a.N + 31) / 32) * (num_kb(a.K) * 2);
-    if (a.swap) split_right_kernel<Layout::Left><<<grid_for(warps * 32), 256, 0, st>>>(a);
+    if (a.swap == 2) split_right_kernel<Layout::Small><<<grid_for(warps * 32), 256, 0, st>>>(a);
+    else if (a.swap) split_right_kernel<Layout::Left><<<grid_for(warps * 32), 256, 0, st>>>(a);
     else split_right_kernel<Layout::Right><<<grid_for(warps * 32), 256, 0, st>>>(a);
     return cudaGetLastError();
 }
@@ -313,6 +315,9 @@ cudaError_t launch_split_both(const LeftSplitArgs& l, const RightSplitArgs& r, c
     int64_t nl = std::min<int64_t>(grid_for(wl), std::max<int64_t>(1, 148 * 16 * bytes_l / (bytes_l + bytes_r)));
     int64_t nr = std::min<int64_t>(grid_for(wr), std::max<int64_t>(1, 148 * 16 - nl));
     if (l.swap != r.swap) return cudaErrorInvalidValue;
+    if (l.swap == 2)
+        return launch_pdl(split_both_kernel<Layout::Small, Layout::Small>, dim3((unsigned)(nl + nr)), dim3(256), 0, st,
+                          l, r, (int)nl);
     if (l.swap)
         return launch_pdl(split_both_kernel<Layout::Right, Layout::Left>, dim3((unsigned)(nl + nr)), dim3(256), 0, st,
                           l, r, (int)nl);
@@ -463,7 +468,10 @@ __global__ void ttp_left_kernel(TtpGenArgs g) {
                 }
             }
         }
-        if (g.sum_planes) store_limbs16<Layout::Left>(g.sum_planes, row, k0, KB, sum);
+        if (g.sum_planes) {
+            if (g.small) store_limbs16<Layout::Small>(g.sum_planes, row, k0, KB, sum);
+            else store_limbs16<Layout::Left>(g.sum_planes, row, k0, KB, sum);
+        }
     }
 }
 // Right factor b (K x N row-major): b_q = G(k_ttp, B||q||id)[k*N + n];
@@ -499,7 +507,10 @@ __global__ void ttp_right_kernel(TtpGenArgs g) {
                 }
             }
         }
-        if (g.sum_planes) store_limbs16<Layout::Right>(g.sum_planes, n, k0, KB, sum);
+        if (g.sum_planes) {
+            if (g.small) store_limbs16<Layout::Small>(g.sum_planes, n, k0, KB, sum);
+            else store_limbs16<Layout::Right>(g.sum_planes, n, k0, KB, sum);
+        }
     }
 }
 cudaError_t launch_ttp_left(const TtpGenArgs& g, cudaStream_t st) {

@@ -19,7 +19,8 @@ struct LeftSplitArgs {
     int Pcopy;
     uint8_t* cp_planes;
     int64_t cp_planes_stride;        // bytes
-    int swap;                        // 1: planes in Layout::Right (transposed ring GEMM), else Layout::Left
+    int swap;                        // plane layout: 0 Layout::Left, 1 Layout::Right (transposed ring GEMM),
+                                     // 2 Layout::Small (stacked-plane GEMM)
     int add_sum_first;               // copy of party 0 gets + the sum (b'_0 = b_0 + delta, R8), for weights
                                      // given rows x K (conv: Cout x C*kh*kw)
 };
@@ -36,7 +37,8 @@ struct RightSplitArgs {
     int add_delta_first;             // party 0's b' = b_0 + delta (R8)
     uint8_t* cp_planes;
     int64_t cp_planes_stride;
-    int swap;                        // 1: planes in Layout::Left (transposed ring GEMM), else Layout::Right
+    int swap;                        // plane layout: 0 Layout::Right, 1 Layout::Left (transposed ring GEMM),
+                                     // 2 Layout::Small (stacked-plane GEMM)
 };
 
 struct TtpGenArgs {
@@ -47,6 +49,7 @@ struct TtpGenArgs {
     int out_lo, out_hi;              // parties whose u64 shares are written
     uint64_t* out;                   // [out_hi - out_lo][rows*K]
     uint8_t* sum_planes;             // planes of sum_q over all P parties (TTP), or null
+    int small;                       // 1: sum planes in Layout::Small (stacked-plane GEMM)
 };
 
 cudaError_t launch_encode(const double* x, uint64_t* out, int64_t n, int frac_bits, int* err, cudaStream_t st);

@@ -174,27 +174,63 @@ struct Carve {
     uint8_t* take(size_t n) { uint8_t* p = base ? base + off : nullptr; off += align256(n); return p; }
 };
 
-// The ring GEMM tiles its output in 256 x 128 blocks (rows x columns), or, for
-// at most 32 rows, in stacked-plane 32 x 32 blocks (ring_gemm_small.cu).  It can
-// compute z^T = delta^T a_p^T + b'_p^T eps^T instead (x-side planes in the
-// right-operand layout, y-side planes in the left one, transposed store): the
-// orientation whose GEMM the tensor-time model (ring_gemm_plan) rates cheaper
-// is used, e.g. M = 49, N = 512: 256 x 512 -> 512 x 128 padded tiles.
-// Bit-identical either way (the same ring sums).  MPC_NO_SWAP=1 disables it.
-bool use_swap(int64_t M, int64_t N, int64_t K, int parties) {
-    static const bool off = getenv("MPC_NO_SWAP") != nullptr;
-    if (off || M == N) return false;
+// GEMM orientation and kernel of a Beaver step.  The ring GEMM tiles its output
+// in 256 x 128 blocks, or — for at most 32 rows — in stacked-plane 32 x 32 blocks
+// (ring_gemm_small.cu, planes in Layout::Small).  It can also compute
+// z^T = delta^T a_p^T + b'_p^T eps^T (x-side planes in the right-operand layout,
+// y-side planes in the left one, transposed store).  Of the (orientation,
+// kernel) options the tensor-time model (ring_gemm_model_cycles) rates
+// cheapest is used: e.g. M = 49, N = 512 runs transposed (256 x 512 -> 512 x 128
+// padded tiles), M = 32 or N <= 32 on the stacked-plane kernel.  Bit-identical
+// either way (the same ring sums).  MPC_NO_SWAP=1 disables the transposition,
+// MPC_GEMM_SMALL=0/1 disables / forces (where possible) the stacked kernel.
+struct GemmChoice { bool swap, small; };
+GemmChoice choose_gemm(int parties, int64_t M, int64_t N, int64_t K, bool allow_swap, bool allow_small) {
+    static const bool no_swap = getenv("MPC_NO_SWAP") != nullptr;
+    static const int small_env = getenv("MPC_GEMM_SMALL") ? atoi(getenv("MPC_GEMM_SMALL")) : -1;
+    allow_swap = allow_swap && !no_swap;
+    allow_small = allow_small && small_env != 0;
     const int tkb = (int)(2 * num_kb(K));
-    const double straight = ring_gemm_plan(parties, M, N, tkb, 74, true).cycles;
-    const double swapped = ring_gemm_plan(parties, N, M, tkb, 74, true).cycles;
-    return swapped < straight;
+    GemmChoice best{false, false};
+    if (M == 0 || N == 0) return best;
+    double cost = ring_gemm_model_cycles(parties, M, N, tkb, 74, false);
+    auto consider = [&](bool sw, bool sm) {
+        const int64_t gm = sw ? N : M, gn = sw ? M : N;
+        if (sm && gm > kSmallRows) return;
+        const double t = ring_gemm_model_cycles(parties, gm, gn, tkb, 74, sm);
+        if (t < cost) { cost = t; best = GemmChoice{sw, sm}; }
+    };
+    if (allow_swap) consider(true, false);
+    if (allow_small) consider(false, true);
+    if (allow_small && allow_swap) consider(true, true);
+    if (small_env == 1 && allow_small && !best.small) {
+        if (M <= kSmallRows) best = GemmChoice{false, true};
+        else if (allow_swap && N <= kSmallRows) best = GemmChoice{true, true};
+    }
+    return best;
+}
+
+// workspace of a plain one-party ring GEMM C = A @ B (the TTP's c = a @ b, mpc_ring_matmul):
+// limb planes of A and B in the layout of the kernel choose_gemm picks (no transposition), partials
+struct PlainGemmWs { uint8_t *a_pl, *b_pl; uint64_t* partials; bool small; size_t total; };
+PlainGemmWs plain_gemm_ws(int64_t M, int64_t K, int64_t N, void* ws = nullptr) {
+    PlainGemmWs w{};
+    w.small = choose_gemm(1, M, N, (K + 1) / 2, false, true).small;     // model of one K-long segment
+    Carve cv(ws);
+    w.a_pl = cv.take(w.small ? planes_bytes<Layout::Small>(M, K) : lp(M, K));
+    w.b_pl = cv.take(w.small ? planes_bytes<Layout::Small>(N, K) : rp(N, K));
+    const size_t pb = ring_gemm_partials_bytes(1, M, N, (int)num_kb(K), 0, w.small);
+    w.partials = reinterpret_cast<uint64_t*>(pb ? cv.take(pb) : nullptr);
+    w.total = cv.off;
+    return w;
 }
 
 // workspace layout of beaver_matmul (see mpc_workspace_bytes)
 struct BeaverWs {
     uint8_t *eps_pl, *delta_pl, *a_pl, *b_pl;
     int64_t a_stride, b_stride;   // bytes between parties' a_p / b'_p planes
-    bool swap;                    // transposed ring GEMM (use_swap)
+    bool swap;                    // transposed ring GEMM (choose_gemm)
+    bool small;                   // stacked-plane GEMM, planes in Layout::Small (choose_gemm)
     uint64_t* ed;        // one-party mode: [e | d] reveal buffer
     uint64_t* zbuf;      // one-party, P > 2, truncation: z reveal
     int8_t* hbuf;        // one-party, P > 2, truncation: top nibbles
@@ -206,14 +242,16 @@ struct BeaverWs {
 // convolution reveals at the input / weight shapes instead).  allow_swap: the
 // transposed GEMM is possible for this output layout.
 BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N, int64_t ed_elems = -1,
-                      bool allow_swap = true) {
+                      bool allow_swap = true, bool allow_small = true) {
     const int Pl = c->all ? c->P : 1;
     Carve cv(ws);
     BeaverWs w{};
-    w.swap = allow_swap && use_swap(M, N, K, Pl);
+    const GemmChoice gc = choose_gemm(Pl, M, N, K, allow_swap, allow_small);
+    w.swap = gc.swap;
+    w.small = gc.small;
     if (ed_elems < 0) ed_elems = M * K + K * N;
-    const int64_t xs = w.swap ? rp(M, K) : lp(M, K);     // eps, a_p planes (rows = M)
-    const int64_t ys = w.swap ? lp(N, K) : rp(N, K);     // delta, b'_p planes (rows = N)
+    const int64_t xs = w.small ? planes_bytes<Layout::Small>(M, K) : (w.swap ? rp(M, K) : lp(M, K));   // eps, a_p
+    const int64_t ys = w.small ? planes_bytes<Layout::Small>(N, K) : (w.swap ? lp(N, K) : rp(N, K));   // delta, b'_p
     const int64_t gM = w.swap ? N : M, gN = w.swap ? M : N;   // the GEMM's own output sizes
     w.a_stride = xs;
     w.b_stride = ys;
@@ -225,16 +263,18 @@ BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N, int6
     const bool alg1_one = !c->all && c->P > 2;
     w.zbuf = reinterpret_cast<uint64_t*>(alg1_one ? cv.take(8 * (size_t)(M * N)) : nullptr);
     w.hbuf = reinterpret_cast<int8_t*>(alg1_one ? cv.take((size_t)(M * N)) : nullptr);
-    size_t pb = ring_gemm_partials_bytes(Pl, gM, gN, 2 * (int)num_kb(K));
+    size_t pb = ring_gemm_partials_bytes(Pl, gM, gN, 2 * (int)num_kb(K), 0, w.small);
     if (!c->all)   // the overlapped schedule runs two half-K GEMMs, the first on fewer SMs
-        pb = std::max({pb, ring_gemm_partials_bytes(1, gM, gN, (int)num_kb(K), kOverlapClusters),
-                       ring_gemm_partials_bytes(1, gM, gN, (int)num_kb(K))});
+        pb = std::max({pb, ring_gemm_partials_bytes(1, gM, gN, (int)num_kb(K), kOverlapClusters, w.small),
+                       ring_gemm_partials_bytes(1, gM, gN, (int)num_kb(K), 0, w.small)});
     w.partials = reinterpret_cast<uint64_t*>(pb ? cv.take(pb) : nullptr);
     w.total = cv.off;
     return w;
 }
 
 // GEMM segment (x-side planes X, y-side planes Y): X @ Y^T normally, Y @ X^T when swapped.
+// plane-layout code of the split kernels (LeftSplitArgs / RightSplitArgs::swap)
+inline int lay(const BeaverWs& w) { return w.small ? 2 : (w.swap ? 1 : 0); }
 RingGemmSegment seg_of(const BeaverWs& w, const uint8_t* X, int64_t xstride, const uint8_t* Y, int64_t ystride,
                        int kb) {
     return w.swap ? RingGemmSegment{Y, X, kb, ystride, xstride} : RingGemmSegment{X, Y, kb, xstride, ystride};
@@ -243,6 +283,7 @@ void set_out(RingGemmParams& p, const BeaverWs& w, int64_t M, int64_t N) {
     p.M = w.swap ? N : M;
     p.N = w.swap ? M : N;
     p.transpose_out = w.swap ? 1 : 0;
+    p.small = w.small ? 1 : 0;
 }
 
 mpc_status beaver_local(mpc_ctx c, const BeaverWs& w, const uint64_t* ed, const uint64_t* a, const uint64_t* b,
@@ -269,10 +310,10 @@ mpc_status beaver_overlapped(mpc_ctx c, const BeaverWs& w, const uint64_t* x, co
     CHECK(comm_allreduce(c, w.ed, w.ed, (size_t)sMK, RedOp::SumU64, "eps reveal", c->comm_stream));
     cudaEventRecord(c->ev_eps, c->comm_stream);
     // a_p planes need no reveal
-    LeftSplitArgs La{M, K, 0, nullptr, nullptr, 0, nullptr, a, 1, w.a_pl, 0, w.swap};
+    LeftSplitArgs La{M, K, 0, nullptr, nullptr, 0, nullptr, a, 1, w.a_pl, 0, lay(w)};
     CHECK(run(c, kClsSplit, "split a", [&] { return launch_split_left(La, c->stream); }));
     cudaStreamWaitEvent(c->stream, c->ev_delta, 0);
-    RightSplitArgs R{K, N, 0, w.ed + sMK, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0, w.swap};
+    RightSplitArgs R{K, N, 0, w.ed + sMK, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0, lay(w)};
     CHECK(run(c, kClsSplit, "split delta", [&] { return launch_split_right(R, c->stream); }));
     RingGemmParams p1{};
     p1.seg[0] = seg_of(w, w.a_pl, 0, w.delta_pl, 0, (int)num_kb(K));           // a_p @ delta
@@ -284,7 +325,7 @@ mpc_status beaver_overlapped(mpc_ctx c, const BeaverWs& w, const uint64_t* x, co
     p1.max_clusters = kOverlapClusters;
     CHECK(gemm_run(c, p1, 1));
     cudaStreamWaitEvent(c->stream, c->ev_eps, 0);
-    LeftSplitArgs Le{M, K, 0, w.ed, nullptr, 1, w.eps_pl, nullptr, 0, nullptr, 0, w.swap};
+    LeftSplitArgs Le{M, K, 0, w.ed, nullptr, 1, w.eps_pl, nullptr, 0, nullptr, 0, lay(w)};
     CHECK(run(c, kClsSplit, "split eps", [&] { return launch_split_left(Le, c->stream); }));
     RingGemmParams p2{};
     p2.seg[0] = seg_of(w, w.eps_pl, 0, w.b_pl, 0, (int)num_kb(K));             // eps @ b'_p
@@ -522,7 +563,7 @@ mpc_status mpc_reveal(mpc_ctx c, const uint64_t* share, uint64_t* out, int64_t n
 size_t mpc_ttp_workspace_bytes(mpc_ctx c, int64_t M, int64_t K, int64_t N) {
     (void)c;
     if (M < 0 || K < 0 || N < 0) return 0;
-    return align256(lp(M, K)) + align256(rp(N, K)) + align256(ring_gemm_partials_bytes(1, M, N, (int)num_kb(K)));
+    return plain_gemm_ws(M, K, N).total;
 }
 
 mpc_status mpc_ttp_triples(mpc_ctx c, uint64_t id, int64_t M, int64_t K, int64_t N, uint64_t* a, uint64_t* b,
@@ -534,14 +575,13 @@ mpc_status mpc_ttp_triples(mpc_ctx c, uint64_t id, int64_t M, int64_t K, int64_t
     if (ttp && ws_bytes < mpc_ttp_workspace_bytes(c, M, K, N)) return fail(c, MPC_ERR_SHAPE, "ttp_triples: workspace too small");
     if (ttp && !ws && (M * K + K * N) > 0) return fail(c, MPC_ERR_ARG, "ttp_triples: null workspace");
     const int lo = c->all ? 0 : c->rank, hi = c->all ? c->P : c->rank + 1;
-    Carve cv(ws);
-    uint8_t* a_pl = ttp ? cv.take(lp(M, K)) : nullptr;
-    uint8_t* b_pl = ttp ? cv.take(rp(N, K)) : nullptr;
-    const size_t pb = ring_gemm_partials_bytes(1, M, N, (int)num_kb(K));
-    uint64_t* partials = reinterpret_cast<uint64_t*>(ttp && pb ? cv.take(pb) : nullptr);
-    TtpGenArgs ga{c->kttp, id, kTagA, c->P, M, K, lo, hi, a, a_pl};
+    const PlainGemmWs pw = plain_gemm_ws(M, K, N, ttp ? ws : nullptr);
+    uint8_t* a_pl = ttp ? pw.a_pl : nullptr;
+    uint8_t* b_pl = ttp ? pw.b_pl : nullptr;
+    uint64_t* partials = ttp ? pw.partials : nullptr;
+    TtpGenArgs ga{c->kttp, id, kTagA, c->P, M, K, lo, hi, a, a_pl, pw.small ? 1 : 0};
     CHECK(run(c, kClsPrg, "ttp_a", [&] { return launch_ttp_left(ga, c->stream); }));
-    TtpGenArgs gb{c->kttp, id, kTagB, c->P, N, K, lo, hi, b, b_pl};
+    TtpGenArgs gb{c->kttp, id, kTagB, c->P, N, K, lo, hi, b, b_pl, pw.small ? 1 : 0};
     CHECK(run(c, kClsPrg, "ttp_b", [&] { return launch_ttp_right(gb, c->stream); }));
     if (M == 0 || N == 0) return MPC_OK;
     if (ttp) {
@@ -553,6 +593,7 @@ mpc_status mpc_ttp_triples(mpc_ctx c, uint64_t id, int64_t M, int64_t K, int64_t
         p.party_stride_c = p.party_stride_z = 0;
         p.trunc_bits = 0;
         p.partials = partials;
+        p.small = pw.small ? 1 : 0;
         CHECK(gemm_run(c, p, 1));
     }
     uint64_t* c_out = c->all ? cc + M * N : cc;    // parties >= 1
@@ -592,8 +633,8 @@ mpc_status mpc_beaver_matmul(mpc_ctx c, const uint64_t* x, const uint64_t* y, co
         return fail(c, MPC_ERR_ARG, "beaver_matmul: null pointer");
     const int64_t sMK = M * K, sKN = K * N, sMN = M * N;
     if (c->all) {
-        LeftSplitArgs L{M, K, sMK, x, a, c->P, w.eps_pl, a, c->P, w.a_pl, w.a_stride, w.swap};
-        RightSplitArgs R{K, N, sKN, y, b, c->P, w.delta_pl, b, c->P, 1, w.b_pl, w.b_stride, w.swap};
+        LeftSplitArgs L{M, K, sMK, x, a, c->P, w.eps_pl, a, c->P, w.a_pl, w.a_stride, lay(w)};
+        RightSplitArgs R{K, N, sKN, y, b, c->P, w.delta_pl, b, c->P, 1, w.b_pl, w.b_stride, lay(w)};
         CHECK(run(c, kClsSplit, "mask+reveal+split", [&] { return launch_split_both(L, R, c->stream); }));
     } else if (has_comm(c)) {
         CHECK(beaver_overlapped(c, w, x, y, a, b, cc, z, M, K, N, truncate));
@@ -649,13 +690,13 @@ mpc_status mpc_beaver_prepare(mpc_ctx c, const uint64_t* y, const uint64_t* b, i
     if (M == 0 || N == 0) return MPC_OK;
     if ((sKN && (!y || !b)) || (!ws && w.total)) return fail(c, MPC_ERR_ARG, "beaver_prepare: null pointer");
     if (c->all) {
-        RightSplitArgs R{K, N, sKN, y, b, c->P, w.delta_pl, b, c->P, 1, w.b_pl, w.b_stride, w.swap};
+        RightSplitArgs R{K, N, sKN, y, b, c->P, w.delta_pl, b, c->P, 1, w.b_pl, w.b_stride, lay(w)};
         return run(c, kClsSplit, "prepare: mask+reveal+split delta", [&] { return launch_split_right(R, c->stream); });
     }
     uint64_t* d = w.ed + sMK;
     CHECK(run(c, kClsSplit, "prepare: mask", [&] { return launch_mask(nullptr, nullptr, 0, y, b, sKN, d, c->stream); }));
     if (c->P > 1) CHECK(comm_allreduce(c, d, d, (size_t)sKN, RedOp::SumU64, "delta reveal"));
-    RightSplitArgs R{K, N, 0, d, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0, w.swap};
+    RightSplitArgs R{K, N, 0, d, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0, lay(w)};
     return run(c, kClsSplit, "prepare: split delta", [&] { return launch_split_right(R, c->stream); });
 }
 
@@ -674,12 +715,12 @@ mpc_status mpc_beaver_matmul_prepared(mpc_ctx c, const uint64_t* x, const uint64
     if (M == 0 || N == 0) return MPC_OK;
     if ((sMK && (!x || !a)) || !cc || !z || (!ws && w.total)) return fail(c, MPC_ERR_ARG, "beaver_matmul_prepared: null pointer");
     if (c->all) {
-        LeftSplitArgs L{M, K, sMK, x, a, c->P, w.eps_pl, a, c->P, w.a_pl, w.a_stride, w.swap};
+        LeftSplitArgs L{M, K, sMK, x, a, c->P, w.eps_pl, a, c->P, w.a_pl, w.a_stride, lay(w)};
         CHECK(run(c, kClsSplit, "mask+reveal+split eps", [&] { return launch_split_left(L, c->stream); }));
         CHECK(beaver_gemm(c, w, cc, z, M, K, N, truncate));
     } else if (!has_comm(c)) {
         if (c->P > 1) return fail(c, MPC_ERR_STATE, "beaver_matmul_prepared: context has no communicator");
-        LeftSplitArgs L{M, K, 0, x, a, 1, w.eps_pl, a, 1, w.a_pl, 0, w.swap};
+        LeftSplitArgs L{M, K, 0, x, a, 1, w.eps_pl, a, 1, w.a_pl, 0, lay(w)};
         CHECK(run(c, kClsSplit, "mask+split eps", [&] { return launch_split_left(L, c->stream); }));
         CHECK(beaver_gemm(c, w, cc, z, M, K, N, truncate));
     } else {
@@ -690,7 +731,7 @@ mpc_status mpc_beaver_matmul_prepared(mpc_ctx c, const uint64_t* x, const uint64
         cudaStreamWaitEvent(c->comm_stream, c->ev_mask, 0);
         CHECK(comm_allreduce(c, w.ed, w.ed, (size_t)sMK, RedOp::SumU64, "eps reveal", c->comm_stream));
         cudaEventRecord(c->ev_eps, c->comm_stream);
-        LeftSplitArgs La{M, K, 0, nullptr, nullptr, 0, nullptr, a, 1, w.a_pl, 0, w.swap};
+        LeftSplitArgs La{M, K, 0, nullptr, nullptr, 0, nullptr, a, 1, w.a_pl, 0, lay(w)};
         CHECK(run(c, kClsSplit, "split a", [&] { return launch_split_left(La, c->stream); }));
         RingGemmParams p1{};
         p1.seg[0] = seg_of(w, w.a_pl, 0, w.delta_pl, 0, (int)num_kb(K));
@@ -701,7 +742,7 @@ mpc_status mpc_beaver_matmul_prepared(mpc_ctx c, const uint64_t* x, const uint64
         p1.max_clusters = kOverlapClusters;
         CHECK(gemm_run(c, p1, 1));
         cudaStreamWaitEvent(c->stream, c->ev_eps, 0);
-        LeftSplitArgs Le{M, K, 0, w.ed, nullptr, 1, w.eps_pl, nullptr, 0, nullptr, 0, w.swap};
+        LeftSplitArgs Le{M, K, 0, w.ed, nullptr, 1, w.eps_pl, nullptr, 0, nullptr, 0, lay(w)};
         CHECK(run(c, kClsSplit, "split eps", [&] { return launch_split_left(Le, c->stream); }));
         RingGemmParams p2{};
         p2.seg[0] = seg_of(w, w.eps_pl, 0, w.b_pl, 0, (int)num_kb(K));
@@ -728,8 +769,8 @@ mpc_status beaver_local(mpc_ctx c, const BeaverWs& w, const uint64_t* ed, const 
                         const uint64_t* cc, uint64_t* z, int64_t M, int64_t K, int64_t N, int truncate) {
     const int64_t sMK = M * K;
     if (!c->all) {
-        LeftSplitArgs L{M, K, 0, ed, nullptr, 1, w.eps_pl, a, 1, w.a_pl, 0, w.swap};
-        RightSplitArgs R{K, N, 0, ed + sMK, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0, w.swap};
+        LeftSplitArgs L{M, K, 0, ed, nullptr, 1, w.eps_pl, a, 1, w.a_pl, 0, lay(w)};
+        RightSplitArgs R{K, N, 0, ed + sMK, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0, lay(w)};
         CHECK(run(c, kClsSplit, "split eps/delta", [&] { return launch_split_both(L, R, c->stream); }));
     }
     return beaver_gemm(c, w, cc, z, M, K, N, truncate);
@@ -774,7 +815,7 @@ mpc_status mpc_truncate(mpc_ctx c, uint64_t* x, int64_t n, int bits, uint64_t wr
 
 size_t mpc_ring_matmul_workspace_bytes(int64_t M, int64_t K, int64_t N) {
     if (M < 0 || K < 0 || N < 0) return 0;
-    return align256(lp(M, K)) + align256(rp(N, K)) + align256(ring_gemm_partials_bytes(1, M, N, (int)num_kb(K)));
+    return plain_gemm_ws(M, K, N).total;
 }
 
 mpc_status mpc_ring_matmul(mpc_ctx c, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t M, int64_t K,
@@ -784,18 +825,17 @@ mpc_status mpc_ring_matmul(mpc_ctx c, const uint64_t* A, const uint64_t* B, uint
     if (ws_bytes < mpc_ring_matmul_workspace_bytes(M, K, N)) return fail(c, MPC_ERR_SHAPE, "ring_matmul: workspace too small");
     if (M == 0 || N == 0) return MPC_OK;
     if (!C || (K && (!A || !B || !ws))) return fail(c, MPC_ERR_ARG, "ring_matmul: null pointer");
-    Carve cv(ws);
-    uint8_t* a_pl = cv.take(lp(M, K));
-    uint8_t* b_pl = cv.take(rp(N, K));
-    LeftSplitArgs L{M, K, 0, A, nullptr, 1, a_pl, nullptr, 0, nullptr, 0};
-    RightSplitArgs R{K, N, 0, B, nullptr, 1, b_pl, nullptr, 0, 0, nullptr, 0};
+    const PlainGemmWs pw = plain_gemm_ws(M, K, N, ws);
+    const int code = pw.small ? 2 : 0;
+    LeftSplitArgs L{M, K, 0, A, nullptr, 1, pw.a_pl, nullptr, 0, nullptr, 0, code};
+    RightSplitArgs R{K, N, 0, B, nullptr, 1, pw.b_pl, nullptr, 0, 0, nullptr, 0, code};
     CHECK(run(c, kClsSplit, "split A/B", [&] { return launch_split_both(L, R, c->stream); }));
     RingGemmParams p{};
-    p.seg[0] = RingGemmSegment{a_pl, b_pl, (int)num_kb(K), 0, 0};
+    p.seg[0] = RingGemmSegment{pw.a_pl, pw.b_pl, (int)num_kb(K), 0, 0};
     p.nseg = 1;
     p.M = M; p.N = N; p.C = nullptr; p.Z = C;
-    const size_t pb = ring_gemm_partials_bytes(1, M, N, (int)num_kb(K));
-    p.partials = reinterpret_cast<uint64_t*>(pb ? cv.take(pb) : nullptr);
+    p.partials = pw.partials;
+    p.small = pw.small ? 1 : 0;
     return gemm_run(c, p, 1);
 }
 
@@ -987,7 +1027,7 @@ ConvGeom to_geom(const mpc_conv2d_geom* g) {
 // Transposed GEMM (Cout rows x pixel columns) only for one image: its row-major
 // output is then exactly NCHW.
 BeaverWs carve_conv(mpc_ctx c, void* ws, const ConvGeom& g) {
-    return carve_beaver(c, ws, g.M(), g.K(), g.Cout, g.in_elems() + g.w_elems(), g.B == 1);
+    return carve_beaver(c, ws, g.M(), g.K(), g.Cout, g.in_elems() + g.w_elems(), g.B == 1, false);
 }
 // GEMM output mapping of a convolution: NCHW z from im2col rows (b, pixel).
 void conv_out(RingGemmParams& p, const BeaverWs& w, const ConvGeom& g) {

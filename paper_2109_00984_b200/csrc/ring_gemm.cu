@@ -499,9 +499,8 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     if (prm.max_clusters > 0 && prm.max_clusters < max_clusters) max_clusters = prm.max_clusters;
     const int tkb = prm.seg[0].kb + (prm.nseg > 1 ? prm.seg[1].kb : 0);
     RingGemmParams q = prm;
-    const RingGemmPlan plan = ring_gemm_plan(parties, prm.M, prm.N, tkb, max_clusters, prm.partials != nullptr);
-    q.splits = plan.splits;
-    if (plan.small) {
+    q.splits = prm.partials ? ring_gemm_splits(parties, prm.M, prm.N, tkb, max_clusters, prm.small != 0) : 1;
+    if (prm.small) {
         if (q.splits > 1) q.partial_stride = ring_gemm_out_elems(q, parties);
         cudaError_t e = ring_gemm_small_launch(q, parties, 2 * max_clusters, stream);
         if (e != cudaSuccess || q.splits <= 1) return e;
@@ -567,7 +566,7 @@ int ring_gemm_choose_splits(int64_t tiles, int tkb, int64_t clusters) {
     return best;
 }
 
-size_t ring_gemm_partials_bytes(int parties, int64_t M, int64_t N, int total_kb, int max_clusters) {
+size_t ring_gemm_partials_bytes(int parties, int64_t M, int64_t N, int total_kb, int max_clusters, bool small) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -576,7 +575,7 @@ size_t ring_gemm_partials_bytes(int parties, int64_t M, int64_t N, int total_kb,
     int64_t clusters = sms / 2;
     if (max_clusters > 0 && max_clusters < clusters) clusters = max_clusters;
     (void)tiles;
-    const int s = ring_gemm_plan(parties, M, N, total_kb, clusters, true).splits;
+    const int s = ring_gemm_splits(parties, M, N, total_kb, clusters, small);
     return s > 1 ? (size_t)s * parties * M * N * sizeof(uint64_t) : 0;
 }
 

@@ -37,15 +37,20 @@ struct RingGemmParams {
     int64_t out_hw;                     // > 0 (overrides transpose_out): row m = b * out_hw + s of the GEMM
                                         // goes to Z[(b * N + n) * out_hw + s] — the NCHW output of a
                                         // convolution whose im2col rows are (b, pixel s).  C likewise.
+    int small;                          // 1: stacked-plane kernel (M <= 32, planes in Layout::Small)
 };
 
-// Which kernel runs an M x N x (tkb 32-K blocks) GEMM and its split-K factor:
-// the 2-CTA 256 x 128 kernel, or (M <= 32, when its tensor-time model is lower)
-// the stacked-plane kernel of ring_gemm_small.cu.  split_ok: a partials buffer exists.
-struct RingGemmPlan { bool small; int splits; double cycles; /* tensor-time model, SM-cycles */ };
-RingGemmPlan ring_gemm_plan(int parties, int64_t M, int64_t N, int tkb, int64_t max_clusters, bool split_ok);
+// Two kernels: the 2-CTA 256 x 128 kernel (planes in Layout::Left / Right) and,
+// for at most 32 output rows, the stacked-plane kernel of ring_gemm_small.cu
+// (both operands in Layout::Small) — RingGemmParams::small picks it; the caller
+// wrote the planes in the matching layout.  Tensor-time model (SM-cycles, both
+// kernels as launched, split-K included) used to choose kernel and orientation:
+double ring_gemm_model_cycles(int parties, int64_t M, int64_t N, int tkb, int64_t max_clusters, bool small);
+// split-K factor the launcher uses (1 without a partials buffer)
+int ring_gemm_splits(int parties, int64_t M, int64_t N, int tkb, int64_t max_clusters, bool small);
 size_t ring_gemm_small_smem_bytes();
 cudaError_t ring_gemm_small_launch(const RingGemmParams& q, int parties, int64_t max_ctas, cudaStream_t stream);
+constexpr int kSmallRows = 32;                     // output rows the stacked-plane kernel handles
 
 // Largest unit length (32-K blocks) for which every s32 accumulator stays exact.
 int ring_gemm_max_kc();
@@ -54,7 +59,8 @@ int ring_gemm_default_kc(int total_kb);
 size_t ring_gemm_smem_bytes();
 int ring_gemm_choose_splits(int64_t tiles, int tkb, int64_t clusters);
 // workspace for the split-K partial sums of a GEMM with these sizes (0 if no split)
-size_t ring_gemm_partials_bytes(int parties, int64_t M, int64_t N, int total_kb, int max_clusters = 0);
+size_t ring_gemm_partials_bytes(int parties, int64_t M, int64_t N, int total_kb, int max_clusters = 0,
+                                bool small = false);
 int64_t ring_gemm_out_elems(const RingGemmParams& q, int parties);
 cudaError_t ring_gemm_finalize(const RingGemmParams& q, int parties, cudaStream_t stream);
 cudaError_t ring_gemm_launch(const RingGemmParams& p, int parties, cudaStream_t stream);

@@ -28,8 +28,13 @@
 // only the plane pairs with i + j >= 8 that share an MMA with needed ones
 // (12 of the 48 plane products issued per 32-K block).
 //
-// Warp roles (384 threads): warp 0 producer (16 bulk copies of 1 KiB per
-// 32-K block: 8 left-plane row blocks, 8 right-plane row blocks), warp 1 MMA
+// Operands in Layout::Small (common.cuh): one 32-K block of the 32 rows of all
+// 8 planes is 8 KiB contiguous, so a stage is two bulk copies (16 x 1 KiB
+// copies from the 128/64-row layouts ran at a third of this speed: the copy
+// engine is message-rate bound for small copies).
+//
+// Warp roles (384 threads): warp 0 producer (two 8 KiB bulk copies per
+// 32-K block), warp 1 MMA
 // issuer, warp 2 TMEM allocator, warps 4..11 epilogue (two per TMEM lane
 // quadrant, 16 columns each).
 #include <cstdint>
@@ -127,25 +132,20 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_small_kernel(const __gr
         for (int w = blockIdx.x; w < it.count(); w += gridDim.x) {
             int party, n, klo, khi;
             it.decode(w, party, n, klo, khi);
-            const int64_t rbB = n >> 1;                            // 64-row right block
-            const int64_t offB = (int64_t)(n & 1) * kChunk;        // rows 32(n&1)..+31 of that block
             for (int kt = klo; kt < khi; ++kt) {
                 const int sg = (kt < p.seg[0].kb) ? 0 : 1;
                 const RingGemmSegment& S = p.seg[sg];
                 const int64_t kb = kt - (sg ? p.seg[0].kb : 0);
-                const uint8_t* srcA = S.A + party * S.party_stride_A + kb * (8 * PlaneGeom<Layout::Left>::kBlock);
-                const uint8_t* srcB = S.B + party * S.party_stride_B +
-                                      (rbB * S.kb + kb) * (8 * PlaneGeom<Layout::Right>::kBlock) + offB;
+                // Layout::Small: (32-row block, 32-K block) of all 8 planes = 8 KiB contiguous
+                const uint8_t* srcA = S.A + party * S.party_stride_A + kb * (8 * kChunk);
+                const uint8_t* srcB = S.B + party * S.party_stride_B + ((int64_t)n * S.kb + kb) * (8 * kChunk);
                 mbar_wait(&empty[s], ph ^ 1);
                 uint8_t* st = smem + s * kStageBytes;
-                if (lane == 0) mbar_expect_tx(&full[s], kStageBytes);
-                __syncwarp();
-                if (lane < 8)
-                    bulk_g2s(st + lane * kChunk, srcA + (int64_t)lane * PlaneGeom<Layout::Left>::kBlock, kChunk,
-                             &full[s]);
-                else if (lane < 16)
-                    bulk_g2s(st + lane * kChunk, srcB + (int64_t)(lane - 8) * PlaneGeom<Layout::Right>::kBlock,
-                             kChunk, &full[s]);
+                if (elect_one()) {
+                    mbar_expect_tx(&full[s], kStageBytes);
+                    bulk_g2s(st, srcA, 8 * kChunk, &full[s]);
+                    bulk_g2s(st + 8 * kChunk, srcB, 8 * kChunk, &full[s]);
+                }
                 __syncwarp();
                 if (++s == kStages) { s = 0; ph ^= 1; }
             }
@@ -257,38 +257,36 @@ size_t ring_gemm_small_smem_bytes() {
     return (size_t)gemm_small::kStages * gemm_small::kStageBytes + 4 * 32 * 32 * 8 + 1024 /*align*/ + 256;
 }
 
-// Tensor-time model (cycles, all SMs) of both kernels for an M x N output with
-// tkb 32-K blocks: the 2-CTA kernel runs 36 MMAs of 64 cycles per 256 x 128
-// tile and block on a CTA pair; the stacked one 12 MMAs of ~48 cycles (N = 32
-// MMAs are shared-memory bound) per 32 x 32 tile and block on one SM.
 namespace {
 int64_t waves(int64_t items, int64_t slots) { return (items + slots - 1) / slots; }
+int small_splits(int64_t tiles, int tkb, int64_t ctas) {
+    if (tiles <= 0 || tiles >= ctas) return 1;
+    int64_t s = ctas / tiles;
+    if (s > 64) s = 64;
+    if (s > tkb / 8) s = tkb / 8;
+    return s < 1 ? 1 : (int)s;
+}
 }  // namespace
 
-RingGemmPlan ring_gemm_plan(int parties, int64_t M, int64_t N, int tkb, int64_t max_clusters, bool split_ok) {
-    RingGemmPlan pl{};
-    const int64_t tiles_n = (int64_t)parties * (pad_rows<Layout::Left>(M) / 256) * (pad_rows<Layout::Right>(N) / 128);
-    pl.splits = split_ok ? ring_gemm_choose_splits(tiles_n, tkb, max_clusters) : 1;
-    pl.cycles = (double)waves(tiles_n * pl.splits, max_clusters) * ((tkb + pl.splits - 1) / pl.splits) * 2304.0;
-    static const int env = getenv("MPC_GEMM_SMALL") ? atoi(getenv("MPC_GEMM_SMALL")) : -1;   // 0: off, 1: force
-    if (M > gemm_small::kRows || M < 1 || N < 1 || tkb < 1 || env == 0) return pl;
-    const int64_t ctas = 2 * max_clusters;
-    const int64_t tiles_s = (int64_t)parties * ((N + gemm_small::kTileN - 1) / gemm_small::kTileN);
-    int s_s = 1;
-    if (split_ok && tiles_s < ctas) {
-        s_s = (int)(ctas / tiles_s);
-        if (s_s > 64) s_s = 64;
-        if (s_s > tkb / 8) s_s = tkb / 8;
-        if (s_s < 1) s_s = 1;
+int ring_gemm_splits(int parties, int64_t M, int64_t N, int tkb, int64_t max_clusters, bool small) {
+    if (small) return small_splits((int64_t)parties * ((N + gemm_small::kTileN - 1) / gemm_small::kTileN), tkb,
+                                   2 * max_clusters);
+    const int64_t tiles = (int64_t)parties * (pad_rows<Layout::Left>(M) / 256) * (pad_rows<Layout::Right>(N) / 128);
+    return ring_gemm_choose_splits(tiles, tkb, max_clusters);
+}
+
+// The 2-CTA kernel issues 36 MMAs of 64 cycles per 256 x 128 tile and 32-K
+// block on a CTA pair; the stacked one 12 MMAs of ~48 cycles (N = 32 MMAs are
+// shared-memory bound) per 32 x 32 tile and block on one SM.
+double ring_gemm_model_cycles(int parties, int64_t M, int64_t N, int tkb, int64_t max_clusters, bool small) {
+    const int s = ring_gemm_splits(parties, M, N, tkb, max_clusters, small);
+    if (small) {
+        if (M > gemm_small::kRows) return 1e30;
+        const int64_t tiles = (int64_t)parties * ((N + gemm_small::kTileN - 1) / gemm_small::kTileN);
+        return (double)waves(tiles * s, 2 * max_clusters) * ((tkb + s - 1) / s) * 12.0 * 48.0;
     }
-    const double t_n = pl.cycles;
-    const double t_s = (double)waves(tiles_s * s_s, ctas) * ((tkb + s_s - 1) / s_s) * 12.0 * 48.0;
-    if (env == 1 || t_s < t_n) {
-        pl.small = true;
-        pl.splits = s_s;
-        pl.cycles = t_s;
-    }
-    return pl;
+    const int64_t tiles = (int64_t)parties * (pad_rows<Layout::Left>(M) / 256) * (pad_rows<Layout::Right>(N) / 128);
+    return (double)waves(tiles * s, max_clusters) * ((tkb + s - 1) / s) * 2304.0;
 }
 
 cudaError_t ring_gemm_small_launch(const RingGemmParams& q, int parties, int64_t max_ctas, cudaStream_t stream) {
