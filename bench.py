@@ -449,6 +449,10 @@ def main():
         sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "scripts"))
         import bench_elementwise
         line["next_rows"] = {"elementwise_mul_square": bench_elementwise.run(M * N, P, 20)}
+        # the other BASELINE.json configs (C1, C3, C4, C5) and NEXT-4, same run, all parties on this GPU
+        import bench_configs
+        torch.cuda.empty_cache()
+        line["configs_measured"] = bench_configs.run()
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = oracle_baseline(M, K, N)
     print(json.dumps(line), flush=True)

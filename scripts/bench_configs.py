@@ -1,0 +1,118 @@
+"""The other BASELINE.json configs, measured in the same run as bench.py's
+headline (configs[1]), all parties on one GPU:
+
+  C1  configs[0]: 2-party Beaver 64x64x64 (latency: us per private matmul, one CUDA graph)
+  C3  configs[2]: 2-party ResNet-50 b1 linear/conv layers as im2col ring GEMMs + truncation
+                  (54 private matmuls in one CUDA graph)
+  C4  configs[3]: 2-party ViT-B/16 linear layers (50 private matmuls in one CUDA graph)
+  C5  configs[4]: 4- and 8-party Beaver 8192^3 (Alg. 1 truncation), all parties on one GPU
+  NEXT-4:         the 32 x 519,820 x 32 text-embedding matmul (stacked-plane GEMM)
+
+Each line gives ms, ring-TOPS (2*M*N*K per private matmul) and the fraction of
+the limb-GEMM roofline (144*M*N*K int8 ops per party at bench.py's int8 peak).
+
+  python scripts/bench_configs.py [--skip-c5]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "scripts"))
+
+import synth  # noqa: E402
+import paper_2109_00984_b200 as mpc  # noqa: E402
+import bench_layers  # noqa: E402
+
+
+def _events_ms(fn, reps, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def c1_latency(reps=200):
+    P, M, K, N = 2, 64, 64, 64
+    ctx = mpc.Context(P, mpc.ALL_PARTIES, device=0, master_seed=synth.MASTER_SEED)
+    dev = lambda a: torch.from_numpy(a.view(np.int64)).cuda().view(torch.uint64)  # noqa: E731
+    x = ctx.share(dev(synth.uniform_fixed((M, K), 1001)), 0, 1)
+    y = ctx.share(dev(synth.uniform_fixed((K, N), 1002)), 1, 2)
+    a, b, c = ctx.ttp_triples(1, M, K, N)
+    z = torch.empty_like(c)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ctx.beaver_matmul(x, y, a, b, c, truncate=True, out=z)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(10):
+                ctx.beaver_matmul(x, y, a, b, c, truncate=True, out=z)
+    ms = _events_ms(g.replay, reps // 10) / 10
+    return {"workload": "configs[0] 2-party 64^3 Beaver + truncation", "us_per_private_matmul": ms * 1e3,
+            "graph": "10 matmuls per CUDA graph replay"}
+
+
+def chain(name, reps=10):
+    ctx = mpc.Context(2, mpc.ALL_PARTIES, device=0, master_seed=synth.MASTER_SEED)
+    layers = synth.MODELS[name]
+    ms = bench_layers.run_chain(ctx, layers, reps)
+    ops = sum(2.0 * M * K * N * cnt for _, M, K, N, cnt in layers)
+    tg = sum(bench_layers.t_gemm_ms(M, K, N) * cnt for _, M, K, N, cnt in layers)
+    n = sum(cnt for *_, cnt in layers)
+    return {"private_matmuls": n, "chain_ms": ms, "ring_TOPS": ops / (ms * 1e-3) / 1e12,
+            "roofline_ms": tg, "roofline_frac": tg / ms}
+
+
+def c5(P, n=8192, steps=3):
+    ctx = mpc.Context(P, mpc.ALL_PARTIES, device=0, master_seed=synth.MASTER_SEED)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randint(-8 << 16, 8 << 16, (P, n, n), device="cuda", generator=gen).view(torch.uint64)
+    y = torch.randint(-8 << 16, 8 << 16, (P, n, n), device="cuda", generator=gen).view(torch.uint64)
+    a, b, c = ctx.ttp_triples(1, n, n, n)
+    z = torch.empty_like(c)
+    ctx.profile_enable(True)
+    ms = _events_ms(lambda: ctx.beaver_matmul(x, y, a, b, c, truncate=True, wrap_id=1, out=z), steps, warm=1)
+    gemm_ms, gl = ctx.profile_read("gemm")
+    trunc_ms, _ = ctx.profile_read("trunc")
+    split_ms, _ = ctx.profile_read("split")
+    ctx.profile_enable(False)
+    k = steps + 1
+    tg = bench_layers.t_gemm_ms(n, n, n, parties=P)
+    out = {"ms_per_private_matmul": ms, "ring_TOPS": 2.0 * n ** 3 / (ms * 1e-3) / 1e12,
+           "gemm_ms": gemm_ms / k, "alg1_truncation_ms": trunc_ms / k, "split_ms": split_ms / k,
+           "roofline_ms": tg, "roofline_frac": tg / ms,
+           "note": f"all {P} parties on one GPU (the GEMM work is P x 144 n^3); one party per GPU is the NCCL path"}
+    del x, y, a, b, c, z
+    torch.cuda.empty_cache()
+    return out
+
+
+def run(skip_c5=False):
+    out = {"C1": c1_latency()}
+    for key, name in (("C3_resnet50", "resnet50"), ("C4_vit_b16", "vit"), ("NEXT4_text", "text")):
+        out[key] = chain(name)
+        torch.cuda.empty_cache()
+    if not skip_c5:
+        out["C5_p4_8192"] = c5(4)
+        out["C5_p8_8192"] = c5(8)
+    return out
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--skip-c5", action="store_true")
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    print(json.dumps(run(args.skip_c5), indent=1))
