@@ -194,10 +194,14 @@ GemmChoice choose_gemm(int parties, int64_t M, int64_t N, int64_t K, bool allow_
     GemmChoice best{false, false};
     if (M == 0 || N == 0) return best;
     double cost = ring_gemm_model_cycles(parties, M, N, tkb, 74, false);
+    // The stacked-plane kernel's per-launch overhead is lower (one CTA per work
+    // item, a 32 x 32 epilogue): measured faster than the 2-CTA kernel for every
+    // M <= 32 shape tried (scripts/gemm_kernel_compare.py) even where the
+    // tensor-time model rates it up to ~1.2x slower, so it is preferred within 1.3x.
     auto consider = [&](bool sw, bool sm) {
         const int64_t gm = sw ? N : M, gn = sw ? M : N;
         if (sm && gm > kSmallRows) return;
-        const double t = ring_gemm_model_cycles(parties, gm, gn, tkb, 74, sm);
+        const double t = ring_gemm_model_cycles(parties, gm, gn, tkb, 74, sm) / (sm ? 1.3 : 1.0);
         if (t < cost) { cost = t; best = GemmChoice{sw, sm}; }
     };
     if (allow_swap) consider(true, false);
