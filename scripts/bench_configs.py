@@ -99,8 +99,32 @@ def c5(P, n=8192, steps=3):
     return out
 
 
+def one_party_schedule(n=4096, steps=10):
+    """One party per GPU, as the N-GPU bench runs it, on this GPU: a 1-rank NCCL
+    communicator (its allreduces are copies, so no NVLink time is measured) runs
+    the overlapped schedule — mask, delta then eps reveal on the comm stream, a_p
+    split + phase-1 GEMM on 132 SMs, eps split + phase-2 GEMM — against the fused
+    single-GEMM schedule of a context without communicator (P = 1 both).  The
+    difference is what the overlap structure itself costs (two GEMM launches,
+    16 SMs left to NCCL during phase 1)."""
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.randint(-8 << 16, 8 << 16, (n, n), device="cuda", generator=gen).view(torch.uint64)
+    y = torch.randint(-8 << 16, 8 << 16, (n, n), device="cuda", generator=gen).view(torch.uint64)
+    out = {}
+    for label, uid in (("fused_no_comm", None), ("overlapped_nccl_1rank", mpc.nccl_unique_id())):
+        ctx = mpc.Context(1, 0, device=0, master_seed=synth.MASTER_SEED, nccl_id=uid)
+        a, b, c = ctx.ttp_triples(1, n, n, n)
+        z = torch.empty_like(c)
+        out[label + "_ms"] = _events_ms(lambda: ctx.beaver_matmul(x, y, a, b, c, truncate=True, out=z), steps)
+        del ctx, a, b, c, z
+    out["schedule_overhead_frac"] = out["overlapped_nccl_1rank_ms"] / out["fused_no_comm_ms"] - 1.0
+    out["workload"] = f"1 party {n}^3 Beaver + truncation"
+    torch.cuda.empty_cache()
+    return out
+
+
 def run(skip_c5=False):
-    out = {"C1": c1_latency()}
+    out = {"C1": c1_latency(), "one_party_schedule": one_party_schedule()}
     for key, name in (("C3_resnet50", "resnet50"), ("C4_vit_b16", "vit"), ("NEXT4_text", "text")):
         out[key] = chain(name)
         torch.cuda.empty_cache()
