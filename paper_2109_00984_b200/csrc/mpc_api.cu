@@ -401,7 +401,9 @@ mpc_status mpc_create(mpc_ctx* out, int world_size, int rank, int device, const 
     c->master = master_seed;
     for (int p = 0; p < world_size; ++p) c->kp.k[p] = philox_at(master_seed, stream_word(kTagKeyParty, p, 0), 0);
     c->kttp = philox_at(master_seed, stream_word(kTagKeyTTP, 0, 0), 0);
-    if (cudaMalloc(&c->d_err, sizeof(int)) != cudaSuccess) { delete c; return MPC_ERR_CUDA; }
+    // d_err[0]: the synchronous encode check; d_err[1]: the sticky flag of mpc_encode_async
+    if (cudaMalloc(&c->d_err, 2 * sizeof(int)) != cudaSuccess) { delete c; return MPC_ERR_CUDA; }
+    if (cudaMemset(c->d_err, 0, 2 * sizeof(int)) != cudaSuccess) { cudaFree(c->d_err); delete c; return MPC_ERR_CUDA; }
     if (!c->all && nccl_id) {
         // One party per process: own communicator (also for P = 1, where the
         // reveals are 1-rank allreduces).  NCCL gets a bounded CTA count so its
@@ -524,6 +526,25 @@ mpc_status mpc_encode(mpc_ctx c, const double* x, uint64_t* out, int64_t n) {
     cudaError_t e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "encode: %s", cudaGetErrorString(e));
     if (h) return fail(c, MPC_ERR_OVERFLOW, "encode: |x| * 2^%d >= 2^63 or NaN", c->frac);
+    return MPC_OK;
+}
+
+mpc_status mpc_encode_async(mpc_ctx c, const double* x, uint64_t* out, int64_t n) {
+    CHECK(enter(c));
+    if (n < 0) return fail(c, MPC_ERR_SHAPE, "encode: n < 0");
+    if (n == 0) return MPC_OK;
+    if (!x || !out) return fail(c, MPC_ERR_ARG, "encode: null pointer");
+    return run(c, kClsCodec, "encode", [&] { return launch_encode(x, out, n, c->frac, c->d_err + 1, c->stream); });
+}
+
+mpc_status mpc_check_overflow(mpc_ctx c) {
+    CHECK(enter(c));
+    int h = 0;
+    cudaMemcpyAsync(&h, c->d_err + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+    cudaMemsetAsync(c->d_err + 1, 0, sizeof(int), c->stream);
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "check_overflow: %s", cudaGetErrorString(e));
+    if (h) return fail(c, MPC_ERR_OVERFLOW, "encode_async: |x| * 2^%d >= 2^63 or NaN since the last check", c->frac);
     return MPC_OK;
 }
 

@@ -153,11 +153,17 @@ class Context:
         return (self.P,) if self.all_parties else ()
 
     # ------------------------------------------------------------ fixed point
-    def encode(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    def encode(self, x: torch.Tensor, out: Optional[torch.Tensor] = None, check: bool = True) -> torch.Tensor:
+        """check=False: no stream synchronisation; overflows are reported by check_overflow()."""
         x = x.to(device=self.device, dtype=torch.float64).contiguous()
         out = _u64(x.shape, self.device) if out is None else _check_out(out, x.shape, torch.uint64)
-        self._call(self._lib.mpc_encode, _ptr(x), _ptr(out), ctypes.c_int64(x.numel()))
+        fn = self._lib.mpc_encode if check else self._lib.mpc_encode_async
+        self._call(fn, _ptr(x), _ptr(out), ctypes.c_int64(x.numel()))
         return out
+
+    def check_overflow(self) -> None:
+        """Raises MpcError(MPC_ERR_OVERFLOW) if an encode(check=False) overflowed since the last check."""
+        self._call(self._lib.mpc_check_overflow)
 
     def decode(self, v: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         if out is None:

@@ -48,6 +48,15 @@ def test_encode_decode_parity(mpc):
     assert np.array_equal(d, oracle.decode(oracle.encode(x)))
     with pytest.raises(mpc.MpcError):
         c.encode(torch.tensor([2.0 ** 47], dtype=torch.float64, device="cuda"))
+    # the unsynchronised form: same codes, overflow reported by check_overflow (sticky until checked)
+    assert np.array_equal(host(c.encode(torch.from_numpy(x).cuda(), check=False)), oracle.encode(x))
+    c.check_overflow()
+    c.encode(torch.tensor([1.0, float("nan")], dtype=torch.float64, device="cuda"), check=False)
+    c.encode(torch.tensor([1.0], dtype=torch.float64, device="cuda"), check=False)
+    with pytest.raises(mpc.MpcError) as e:
+        c.check_overflow()
+    assert e.value.status == 3
+    c.check_overflow()                                   # cleared
 
 
 # ------------------------------------------------------------------ share / reveal
