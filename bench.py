@@ -68,6 +68,20 @@ class ClockSampler:
         self.rows = []
         self._proc = None
         self._t = None
+        self.nvml = []               # SM clock every ~2 ms through NVML (finer than nvidia-smi's -lms 50)
+        self._stop = threading.Event()
+        self._nt = None
+
+    def _nvml_reader(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            while not self._stop.is_set():
+                self.nvml.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                time.sleep(0.002)
+        except Exception:
+            pass
 
     def _reader(self):
         for line in self._proc.stdout:
@@ -82,12 +96,17 @@ class ClockSampler:
                                           stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._reader, daemon=True)
             self._t.start()
+            self._nt = threading.Thread(target=self._nvml_reader, daemon=True)
+            self._nt.start()
             time.sleep(0.3)          # first sample lands before the timed region starts
         except Exception:
             self._proc = None
         return self
 
     def __exit__(self, *a):
+        self._stop.set()
+        if self._nt is not None:
+            self._nt.join(timeout=5)
         if self._proc is not None:
             self._proc.terminate()
             try:
@@ -98,6 +117,7 @@ class ClockSampler:
 
     def mark(self):
         self._mark = len(self.rows)
+        self._nmark = len(self.nvml)
 
     def summary(self):
         rows = self.rows[getattr(self, "_mark", 0):] or self.rows[-1:]
@@ -109,8 +129,11 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and "Active" in r[5 + i]
                           and "Not" not in r[5 + i]})
+        nv = self.nvml[getattr(self, "_nmark", 0):]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows),
+                "sm_mhz_nvml_median": statistics.median(nv) if nv else None,
+                "sm_mhz_nvml_mean": statistics.fmean(nv) if nv else None, "nvml_samples": len(nv)}
 
 
 def load_peaks():
@@ -425,7 +448,8 @@ def main():
     clocks = sampler.summary()
     # tcgen05 kind::i8 issues 8192 MAC/clk/SM (scripts/mma_probe): the tensor peak at the SM clock
     # actually sustained during the timed region (the GEMM runs under the 1 kW power cap)
-    clk_peak = 2.0 * 8192 * 148 * clocks["sm_mhz"] * 1e6 / 1e12 if clocks.get("sm_mhz") else None
+    clk = clocks.get("sm_mhz_nvml_mean") or clocks.get("sm_mhz")
+    clk_peak = 2.0 * 8192 * 148 * clk * 1e6 / 1e12 if clk else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
