@@ -63,13 +63,16 @@ def run_layer(ctx, M, K, N, reps, graph):
     return ms, (gemm_ms / reps if not graph else None)
 
 
-def run_chain(ctx, layers, reps, prepared=False):
+def run_chain(ctx, layers, reps, prepared=False, offline=False):
     """All layers of one model in one CUDA graph; returns ms per pass.
 
     prepared: the weight side of every private matmul (delta reveal, delta and
     b'_p splits: mpc_beaver_prepare) runs on a second stream, in layer order,
     beside the activation chain (mpc_beaver_matmul_prepared, which waits for its
-    layer's prepare) — all inside the same graph and timed region."""
+    layer's prepare) — all inside the same graph and timed region.
+    offline: the weight sides are prepared once before timing (they depend only
+    on the weights and the pre-generated triples, so they belong to the offline
+    phase with the triples); the timed graph holds the x sides only."""
     dev = torch.device("cuda", 0)
     bufs = []
     for i, (_, M, K, N, count) in enumerate(layers):
@@ -78,12 +81,23 @@ def run_chain(ctx, layers, reps, prepared=False):
         x = ctx.share(torch.from_numpy(X.view(np.int64)).to(dev).view(torch.uint64), 0, 1 + 2 * i)
         y = ctx.share(torch.from_numpy(Y.view(np.int64)).to(dev).view(torch.uint64), 1, 2 + 2 * i)
         a, b, c = ctx.ttp_triples(1 + i, M, K, N)
-        preps = [ctx.beaver_prepare(y, b, M) for _ in range(count)] if prepared else None
+        preps = [ctx.beaver_prepare(y, b, M) for _ in range(count)] if (prepared or offline) else None
         bufs.append((x, y, a, b, c, torch.empty_like(c), count, preps))
 
     side = torch.cuda.Stream(priority=0) if prepared else None
 
+    if offline:
+        for x, y, a, b, c, z, count, preps in bufs:
+            for r in range(count):
+                ctx.beaver_prepare(y, b, x.shape[-2], out=preps[r])
+        torch.cuda.synchronize()
+
     def chain():
+        if offline:
+            for x, y, a, b, c, z, count, preps in bufs:
+                for r in range(count):
+                    ctx.beaver_matmul_prepared(x, a, c, preps[r], truncate=True, out=z)
+            return
         if not prepared:
             for x, y, a, b, c, z, count, _ in bufs:
                 for _ in range(count):
