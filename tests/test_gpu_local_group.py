@@ -241,3 +241,27 @@ def test_beaver_prepared_one_party(mpc, P, M, K, N):
 
     z = np.stack(run_parties(mpc, P, body))
     assert np.array_equal(z, oracle.truncate(oracle.beaver_matmul(xs, ys, a, b, cc), 16, MASTER, wrap_id=4))
+
+
+def test_relu_one_party_sixteen_parties(mpc):
+    """P = 16 (the context maximum): four adder-tree heights, 8 adders at the first."""
+    P, n = 16, 4099
+    X = synth.uniform_ring((n,), 16)
+    xs = oracle.share(P, MASTER, X, 3, 5)
+    res = run_parties(mpc, P, lambda c, r: (host(c.relu(dev(xs[r]), relu_id=21)), c.stats()[0]))
+    ez, dg = oracle.relu(MASTER, 21, xs, diagnostics=True)
+    assert np.array_equal(np.stack([r[0] for r in res]), ez)
+    assert all(r[1] == dg["rounds"] == 7 * 4 + 2 for r in res)
+
+
+def test_beaver_eight_parties_alg1(mpc):
+    """Eight one-party contexts: overlapped schedule + Alg. 1 (u64 and int8 reveals)."""
+    P, M, K, N = 8, 70, 90, 50
+    X = synth.uniform_fixed((M, K), 81)
+    Y = synth.uniform_fixed((K, N), 82)
+    xs, ys = oracle.share(P, MASTER, X, 0, 1), oracle.share(P, MASTER, Y, 7, 2)
+    a, b, cc = oracle.ttp_triple(P, MASTER, 8, M, K, N)
+    res = run_parties(mpc, P, lambda c, r: host(c.beaver_matmul(dev(xs[r]), dev(ys[r]), dev(a[r]), dev(b[r]),
+                                                                 dev(cc[r]), truncate=True, wrap_id=9)))
+    assert np.array_equal(np.stack(res), oracle.truncate(oracle.beaver_matmul(xs, ys, a, b, cc), 16, MASTER,
+                                                         wrap_id=9))
