@@ -59,7 +59,7 @@ constexpr int kStages = 4;
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 128 + 32 * kEpiWarps;    // 384
 constexpr int kTmemCols = 512;
-constexpr int kGroupM = 4;                        // row tiles per scheduling group
+constexpr int kGroupM = 4;                        // row tiles per scheduling group (MPC_GEMM_GROUPM overrides)
 constexpr int kPasses = 2;                        // super-passes of 4 shifts each
 constexpr uint32_t kIdesc = (2u << 4)             // D format: S32
                           | (0u << 7)             // A: unsigned 8-bit
@@ -81,16 +81,16 @@ __device__ __forceinline__ void mma_u8_2cta(uint32_t tmem_d, uint64_t adesc, uin
 // Tile t -> (party, m tile, n tile) in the grouped order: groups of kGroupM row
 // tiles; inside a group, n tiles outer, then row tiles, then parties.
 struct TileMap {
-    int parties, mt, nt;
+    int parties, mt, nt, gmax;                       // gmax: row tiles per group
     __device__ void decode(int t, int& party, int& m, int& n) const {
-        const int per_group_full = kGroupM * nt * parties;
+        const int per_group_full = gmax * nt * parties;
         const int g = t / per_group_full;
         const int r = t % per_group_full;
-        const int gm = min(kGroupM, mt - g * kGroupM);        // row tiles in this group
+        const int gm = min(gmax, mt - g * gmax);              // row tiles in this group
         const int per_n = gm * parties;
         n = r / per_n;
         const int r2 = r % per_n;
-        m = g * kGroupM + r2 / parties;
+        m = g * gmax + r2 / parties;
         party = r2 % parties;
     }
 };
@@ -412,7 +412,8 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     const uint32_t rank = cluster_rank();
     const bool leader = (rank == 0);
     WorkMap wm;
-    wm.tm = TileMap{parties, (int)(pad_rows<Layout::Left>(p.M) / kTileM), (int)(pad_rows<Layout::Right>(p.N) / kTileN)};
+    wm.tm = TileMap{parties, (int)(pad_rows<Layout::Left>(p.M) / kTileM), (int)(pad_rows<Layout::Right>(p.N) / kTileN),
+                    p.group_m > 0 ? p.group_m : kGroupM};
     wm.tkb = p.seg[0].kb + (p.nseg > 1 ? p.seg[1].kb : 0);
     wm.kc = p.kc;
     wm.splits = p.splits < 1 ? 1 : p.splits;
@@ -499,6 +500,8 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     if (prm.max_clusters > 0 && prm.max_clusters < max_clusters) max_clusters = prm.max_clusters;
     const int tkb = prm.seg[0].kb + (prm.nseg > 1 ? prm.seg[1].kb : 0);
     RingGemmParams q = prm;
+    static const int env_group = getenv("MPC_GEMM_GROUPM") ? atoi(getenv("MPC_GEMM_GROUPM")) : 0;
+    if (q.group_m <= 0) q.group_m = env_group;
     q.splits = prm.partials ? ring_gemm_splits(parties, prm.M, prm.N, tkb, max_clusters, prm.small != 0) : 1;
     if (prm.small) {
         if (q.splits > 1) q.partial_stride = ring_gemm_out_elems(q, parties);

@@ -38,6 +38,7 @@ struct RingGemmParams {
                                         // goes to Z[(b * N + n) * out_hw + s] — the NCHW output of a
                                         // convolution whose im2col rows are (b, pixel s).  C likewise.
     int small;                          // 1: stacked-plane kernel (M <= 32, planes in Layout::Small)
+    int group_m;                        // row tiles per scheduling group of the 2-CTA kernel (0: default 4)
 };
 
 // Two kernels: the 2-CTA 256 x 128 kernel (planes in Layout::Left / Right) and,
