@@ -32,6 +32,12 @@
  *           MPC_ERR_CUDA / MPC_ERR_NCCL; the message is in mpc_last_error().  After
  *           a failed collective the context is in MPC_ERR_STATE: only
  *           mpc_destroy is allowed.
+ * Contract. Every party calls the same sequence of collective entry points with
+ *           the same sizes ("synchronization point").  With the environment
+ *           variable MPC_CHECK_COLLECTIVES=1 at mpc_create, each NCCL collective is
+ *           preceded by a min/max allreduce of a (sequence, op, size) word and a
+ *           mismatch returns MPC_ERR_SHAPE (debug aid: it synchronises the stream);
+ *           the in-process party group always checks.
  * Rounds.   mpc_stats counts communication rounds (Table 3): reveal = 1,
  *           beaver_matmul = 1, truncation = 0 for P <= 2 and 1 for P > 2.
  * Ids.      share_id / triple_id / wrap_id are caller-chosen 48-bit ids that select

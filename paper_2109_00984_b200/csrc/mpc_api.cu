@@ -37,6 +37,9 @@ struct mpc_ctx_s {
     LocalGroup* lg = nullptr;               // in-process transport (mpc_create_local), instead of NCCL
     uint64_t* xbuf = nullptr;               // NCCL XOR reveal: all-gathered binary shares
     size_t xbuf_bytes = 0;
+    bool check_collectives = false;         // MPC_CHECK_COLLECTIVES=1: verify the collective contract (NCCL)
+    uint64_t coll_seq = 0;
+    uint64_t* check_buf = nullptr;          // 2 words
     cudaStream_t comm_stream = nullptr;     // reveals of the overlapped Beaver schedule
     cudaEvent_t ev_mask = nullptr, ev_delta = nullptr, ev_eps = nullptr;
     bool broken = false;
@@ -115,13 +118,30 @@ mpc_status comm_allreduce(mpc_ctx c, const void* send, void* recv, size_t count,
         return MPC_OK;
     }
     ncclResult_t r = ncclSuccess;
-    if (count == 0) {
+    if (c->check_collectives) {
+        // collective contract: every party enters the same collective with the same size.
+        // Word = (sequence number, op, count) folded into a u64; min == max across parties iff all agree.
+        const uint64_t word = (c->coll_seq++ << 40) ^ ((uint64_t)op << 36) ^ (uint64_t)count;
+        uint64_t h[2] = {word, ~word};
+        cudaMemcpyAsync(c->check_buf, h, sizeof(h), cudaMemcpyHostToDevice, st);
+        r = ncclAllReduce(c->check_buf, c->check_buf, 1, ncclUint64, ncclMin, c->comm, st);     // min(word)
+        if (r == ncclSuccess)
+            r = ncclAllReduce(c->check_buf + 1, c->check_buf + 1, 1, ncclUint64, ncclMin, c->comm, st);  // min(~word) = ~max
+        cudaMemcpyAsync(h, c->check_buf, sizeof(h), cudaMemcpyDeviceToHost, st);
+        if (r == ncclSuccess && cudaStreamSynchronize(st) == cudaSuccess && h[0] != ~h[1]) {
+            c->broken = true;
+            return fail(c, MPC_ERR_SHAPE, "%s: parties entered different collectives (collective contract broken)", what);
+        }
+    }
+    if (r != ncclSuccess) {
+    } else if (count == 0) {
     } else if (op == RedOp::XorU64) {
         // NCCL has no XOR reduction: all-gather the P binary shares, XOR them locally
         const size_t need = 8 * count * (size_t)c->P;
         if (c->xbuf_bytes < need) {
             cudaStreamSynchronize(st);
             if (c->xbuf) cudaFree(c->xbuf);
+    if (c->check_buf) cudaFree(c->check_buf);
             c->xbuf = nullptr; c->xbuf_bytes = 0;
             if (cudaMalloc(&c->xbuf, need) != cudaSuccess) return fail(c, MPC_ERR_CUDA, "%s: xor buffer alloc", what);
             c->xbuf_bytes = need;
@@ -423,6 +443,13 @@ mpc_status mpc_create(mpc_ctx* out, int world_size, int rank, int device, const 
             cudaEventCreateWithFlags(&c->ev_eps, cudaEventDisableTiming) != cudaSuccess) {
             ncclCommDestroy(c->comm); cudaFree(c->d_err); delete c; return MPC_ERR_CUDA;
         }
+        const char* chk = getenv("MPC_CHECK_COLLECTIVES");
+        if (chk && atoi(chk) != 0) {
+            if (cudaMalloc(&c->check_buf, 2 * sizeof(uint64_t)) != cudaSuccess) {
+                ncclCommDestroy(c->comm); cudaFree(c->d_err); delete c; return MPC_ERR_CUDA;
+            }
+            c->check_collectives = true;
+        }
     }
     *out = c;
     return MPC_OK;
@@ -477,6 +504,7 @@ mpc_status mpc_destroy(mpc_ctx c) {
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->lg) local_group_detach(c->lg, c->rank);
     if (c->xbuf) cudaFree(c->xbuf);
+    if (c->check_buf) cudaFree(c->check_buf);
     if (c->comm_stream) { cudaStreamSynchronize(c->comm_stream); cudaStreamDestroy(c->comm_stream); }
     for (cudaEvent_t e : {c->ev_mask, c->ev_delta, c->ev_eps}) if (e) cudaEventDestroy(e);
     for (auto& e : c->pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }

@@ -380,3 +380,31 @@ def test_small_m_beaver_parity(mpc, P, M, K, N):
     assert np.array_equal(host(z), ez)
     ga, gb, gc = c.ttp_triples(90 + P, M, K, N)            # the TTP's c = a @ b on the same kernel
     assert np.array_equal(host(gc), cc)
+
+
+def test_collective_contract_check_nccl():
+    """MPC_CHECK_COLLECTIVES=1: every NCCL collective is preceded by the (sequence,
+    op, size) agreement check; a 1-rank communicator always agrees, so the
+    overlapped Beaver schedule and the reveal still give the oracle's shares."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = r"""
+import sys; sys.path.insert(0, {root!r})
+import numpy as np, torch, oracle, synth
+import paper_2109_00984_b200 as m
+M, K, N = 130, 70, 90
+c = m.Context(1, 0, device=0, master_seed=synth.MASTER_SEED, nccl_id=m.nccl_unique_id())
+X, Y = synth.uniform_fixed((M, K), 1), synth.uniform_fixed((K, N), 2)
+a, b, cc = oracle.ttp_triple(1, synth.MASTER_SEED, 3, M, K, N)
+dev = lambda t: torch.from_numpy(np.ascontiguousarray(t).view(np.int64)).cuda().view(torch.uint64)
+z = c.beaver_matmul(dev(X), dev(Y), dev(a[0]), dev(b[0]), dev(cc[0]), truncate=True)
+r = c.reveal(z).view(torch.int64).cpu().numpy().view(np.uint64)
+ez = oracle.truncate(oracle.beaver_matmul(X[None], Y[None], a, b, cc), 16)[0]
+assert np.array_equal(r, ez)
+print("OK")
+""".format(root=root)
+    env = dict(os.environ, MPC_CHECK_COLLECTIVES="1")
+    out = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and out.stdout.strip().endswith("OK"), out.stderr[-2000:]
