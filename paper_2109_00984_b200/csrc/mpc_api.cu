@@ -220,7 +220,7 @@ GemmChoice choose_gemm(int parties, int64_t M, int64_t N, int64_t K, bool allow_
     // tensor-time model rates it up to ~1.2x slower, so it is preferred within 1.3x.
     auto consider = [&](bool sw, bool sm) {
         const int64_t gm = sw ? N : M, gn = sw ? M : N;
-        if (sm && gm > kSmallRows) return;
+        if (sm && gm > kSmallMaxRows) return;
         const double t = ring_gemm_model_cycles(parties, gm, gn, tkb, 74, sm) / (sm ? 1.3 : 1.0);
         if (t < cost) { cost = t; best = GemmChoice{sw, sm}; }
     };

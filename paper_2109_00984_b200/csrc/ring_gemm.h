@@ -41,8 +41,8 @@ struct RingGemmParams {
     int group_m;                        // row tiles per scheduling group of the 2-CTA kernel (0: default 4)
 };
 
-// Two kernels: the 2-CTA 256 x 128 kernel (planes in Layout::Left / Right) and,
-// for at most 32 output rows, the stacked-plane kernel of ring_gemm_small.cu
+// Two kernels: the 2-CTA 256 x 128 kernel (planes in Layout::Left / Right) and
+// the stacked-plane kernel of ring_gemm_small.cu (32 x 32 tiles, for few rows)
 // (both operands in Layout::Small) — RingGemmParams::small picks it; the caller
 // wrote the planes in the matching layout.  Tensor-time model (SM-cycles, both
 // kernels as launched, split-K included) used to choose kernel and orientation:
@@ -51,7 +51,8 @@ double ring_gemm_model_cycles(int parties, int64_t M, int64_t N, int tkb, int64_
 int ring_gemm_splits(int parties, int64_t M, int64_t N, int tkb, int64_t max_clusters, bool small);
 size_t ring_gemm_small_smem_bytes();
 cudaError_t ring_gemm_small_launch(const RingGemmParams& q, int parties, int64_t max_ctas, cudaStream_t stream);
-constexpr int kSmallRows = 32;                     // output rows the stacked-plane kernel handles
+constexpr int kSmallRows = 32;                     // output rows of one stacked-plane tile
+constexpr int kSmallMaxRows = 256;                 // GEMM rows up to which the stacked kernel is considered
 
 // Largest unit length (32-K blocks) for which every s32 accumulator stays exact.
 int ring_gemm_max_kc();

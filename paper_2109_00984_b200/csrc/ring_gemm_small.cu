@@ -1,6 +1,7 @@
-// ring_gemm_small.cu — the ring GEMM for outputs with at most 32 rows
-// (tcgen05, sm_100a): the limb planes of the left operand are STACKED along
-// the UMMA M dimension instead of padding 32 rows to a 256-row tile.
+// ring_gemm_small.cu — the stacked-plane ring GEMM (tcgen05, sm_100a), for
+// outputs with few rows: in 32 x 32 output tiles, the limb planes of the left
+// operand's 32 rows are STACKED along the UMMA M dimension instead of padding
+// the rows to a 256-row tile.
 //
 // Same product as ring_gemm.cu (Z_p = [C_p] + sum_seg L @ R^T mod 2^64 from
 // u8 limb planes, L = sum_i 2^(8i) L_i, R = sum_j 2^(8j) R_j), computed as
@@ -82,14 +83,16 @@ __device__ __forceinline__ void epi_sync() {           // the 8 epilogue warps o
     asm volatile("bar.sync 1, %0;" :: "n"(32 * kEpiWarps) : "memory");
 }
 
-// work item w -> (party, column tile, K block range) — all warps compute the same values
+// work item w -> (party, 32-row tile, 32-column tile, K block range) — all warps
+// compute the same values; the split-K ranges of one tile are consecutive items
 struct Items {
-    int parties, nt, tkb, splits;
-    __device__ int count() const { return parties * nt * splits; }
-    __device__ void decode(int w, int& party, int& n, int& klo, int& khi) const {
+    int parties, mt, nt, tkb, splits;
+    __device__ int count() const { return parties * mt * nt * splits; }
+    __device__ void decode(int w, int& party, int& m, int& n, int& klo, int& khi) const {
         const int t = w / splits, s = w % splits;
         party = t % parties;
-        n = t / parties;
+        m = (t / parties) % mt;
+        n = t / (parties * mt);
         klo = (int)((int64_t)tkb * s / splits);
         khi = (int)((int64_t)tkb * (s + 1) / splits);
     }
@@ -107,8 +110,8 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_small_kernel(const __gr
     uint64_t* tempty = tfull + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    Items it{parties, (int)((p.N + kTileN - 1) / kTileN), p.seg[0].kb + (p.nseg > 1 ? p.seg[1].kb : 0),
-             p.splits < 1 ? 1 : p.splits};
+    Items it{parties, (int)((p.M + kRows - 1) / kRows), (int)((p.N + kTileN - 1) / kTileN),
+             p.seg[0].kb + (p.nseg > 1 ? p.seg[1].kb : 0), p.splits < 1 ? 1 : p.splits};
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         mbar_init(tfull, 1);
@@ -130,14 +133,14 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_small_kernel(const __gr
         asm volatile("griddepcontrol.wait;" ::: "memory");        // planes written by the split kernel
         int s = 0; uint32_t ph = 0;
         for (int w = blockIdx.x; w < it.count(); w += gridDim.x) {
-            int party, n, klo, khi;
-            it.decode(w, party, n, klo, khi);
+            int party, m, n, klo, khi;
+            it.decode(w, party, m, n, klo, khi);
             for (int kt = klo; kt < khi; ++kt) {
                 const int sg = (kt < p.seg[0].kb) ? 0 : 1;
                 const RingGemmSegment& S = p.seg[sg];
                 const int64_t kb = kt - (sg ? p.seg[0].kb : 0);
                 // Layout::Small: (32-row block, 32-K block) of all 8 planes = 8 KiB contiguous
-                const uint8_t* srcA = S.A + party * S.party_stride_A + kb * (8 * kChunk);
+                const uint8_t* srcA = S.A + party * S.party_stride_A + ((int64_t)m * S.kb + kb) * (8 * kChunk);
                 const uint8_t* srcB = S.B + party * S.party_stride_B + ((int64_t)n * S.kb + kb) * (8 * kChunk);
                 mbar_wait(&empty[s], ph ^ 1);
                 uint8_t* st = smem + s * kStageBytes;
@@ -154,8 +157,8 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_small_kernel(const __gr
         // ------------------------------------------------ MMA issuer
         int s = 0; uint32_t ph = 0; uint32_t u = 0;
         for (int w = blockIdx.x; w < it.count(); w += gridDim.x) {
-            int party, n, klo, khi;
-            it.decode(w, party, n, klo, khi);
+            int party, m, n, klo, khi;
+            it.decode(w, party, m, n, klo, khi);
             for (int k0 = klo; k0 < khi; k0 += kMaxUnit, ++u) {
                 const int k1 = min(khi, k0 + kMaxUnit);
                 mbar_wait(tempty, (u & 1) ^ 1);                     // the epilogue drained the last unit
@@ -187,8 +190,8 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_small_kernel(const __gr
         const int et = threadIdx.x - 128;                          // 0..255
         uint32_t u = 0;
         for (int w = blockIdx.x; w < it.count(); w += gridDim.x) {
-            int party, n, klo, khi;
-            it.decode(w, party, n, klo, khi);
+            int party, m, n, klo, khi;
+            it.decode(w, party, m, n, klo, khi);
             uint64_t run[16];
 #pragma unroll
             for (int c = 0; c < 16; ++c) run[c] = 0;
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_small_kernel(const __gr
 #pragma unroll
             for (int c = 0; c < 16; c += 2) *reinterpret_cast<ulonglong2*>(mine + c) = make_ulonglong2(run[c], run[c + 1]);
             epi_sync();
-            const int M = (int)p.M;
+            const int64_t row0 = (int64_t)m * kRows;
             const int64_t hw = p.out_hw > 0 ? p.out_hw : (p.transpose_out ? p.M : 0);
             const bool tr = hw > 0;
             const bool split = it.splits > 1;
@@ -225,11 +228,12 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_small_kernel(const __gr
                 const int idx = e * 256 + et;                        // consecutive threads: consecutive columns
                 const int r = idx / kTileN, col = idx % kTileN;
                 const int64_t gc = (int64_t)n * kTileN + col;
-                if (r >= M || gc >= p.N) continue;
+                const int64_t gr = row0 + r;
+                if (gr >= p.M || gc >= p.N) continue;
                 uint64_t v = 0;
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq) v += red[((int64_t)qq * kRows + r) * kTileN + col];
-                const int64_t off = tr ? ((int64_t)r / hw) * p.N * hw + r % hw + gc * hw : (int64_t)r * p.N + gc;
+                const int64_t off = tr ? (gr / hw) * p.N * hw + gr % hw + gc * hw : gr * p.N + gc;
                 if (split) {
                     const int sidx = w % it.splits;
                     p.partials[(int64_t)sidx * p.partial_stride + party * p.M * p.N + off] = v;
@@ -268,9 +272,13 @@ int small_splits(int64_t tiles, int tkb, int64_t ctas) {
 }
 }  // namespace
 
+int64_t small_tiles(int parties, int64_t M, int64_t N) {
+    return (int64_t)parties * ((M + gemm_small::kRows - 1) / gemm_small::kRows) *
+           ((N + gemm_small::kTileN - 1) / gemm_small::kTileN);
+}
+
 int ring_gemm_splits(int parties, int64_t M, int64_t N, int tkb, int64_t max_clusters, bool small) {
-    if (small) return small_splits((int64_t)parties * ((N + gemm_small::kTileN - 1) / gemm_small::kTileN), tkb,
-                                   2 * max_clusters);
+    if (small) return small_splits(small_tiles(parties, M, N), tkb, 2 * max_clusters);
     const int64_t tiles = (int64_t)parties * (pad_rows<Layout::Left>(M) / 256) * (pad_rows<Layout::Right>(N) / 128);
     return ring_gemm_choose_splits(tiles, tkb, max_clusters);
 }
@@ -280,11 +288,8 @@ int ring_gemm_splits(int parties, int64_t M, int64_t N, int tkb, int64_t max_clu
 // shared-memory bound) per 32 x 32 tile and block on one SM.
 double ring_gemm_model_cycles(int parties, int64_t M, int64_t N, int tkb, int64_t max_clusters, bool small) {
     const int s = ring_gemm_splits(parties, M, N, tkb, max_clusters, small);
-    if (small) {
-        if (M > gemm_small::kRows) return 1e30;
-        const int64_t tiles = (int64_t)parties * ((N + gemm_small::kTileN - 1) / gemm_small::kTileN);
-        return (double)waves(tiles * s, 2 * max_clusters) * ((tkb + s - 1) / s) * 12.0 * 48.0;
-    }
+    if (small)
+        return (double)waves(small_tiles(parties, M, N) * s, 2 * max_clusters) * ((tkb + s - 1) / s) * 12.0 * 48.0;
     const int64_t tiles = (int64_t)parties * (pad_rows<Layout::Left>(M) / 256) * (pad_rows<Layout::Right>(N) / 128);
     return (double)waves(tiles * s, max_clusters) * ((tkb + s - 1) / s) * 2304.0;
 }
@@ -300,9 +305,8 @@ cudaError_t ring_gemm_small_launch(const RingGemmParams& q, int parties, int64_t
         if (e != cudaSuccess) return e;
         attr_dev = dev;
     }
-    if (q.M > gemm_small::kRows) return cudaErrorInvalidValue;
-    const int64_t items = (int64_t)parties * ((q.N + gemm_small::kTileN - 1) / gemm_small::kTileN) *
-                          (q.splits < 1 ? 1 : q.splits);
+    const int64_t items = small_tiles(parties, q.M, q.N) * (q.splits < 1 ? 1 : q.splits);
+    if (items >= (int64_t)1 << 31) return cudaErrorInvalidValue;
     int64_t ctas = items < max_ctas ? items : max_ctas;
     if (ctas < 1) ctas = 1;
     return launch_pdl(gemm_small::ring_gemm_small_kernel, dim3((unsigned)ctas), dim3(gemm_small::kThreads), smem,

@@ -351,7 +351,7 @@ def test_beaver_prepared_parity(mpc, P, M, K, N):
 
 # ------------------------------------------------------------------ stacked-plane GEMM (M <= 32)
 @pytest.mark.parametrize("M,K,N", [(32, 64, 32), (1, 2048, 1000), (17, 300, 45), (32, 5000, 33), (3, 33, 1),
-                                   (31, 1, 65)])
+                                   (31, 1, 65), (64, 64, 64), (49, 4608, 200), (100, 300, 70), (200, 129, 40)])
 def test_small_m_ring_matmul_parity(mpc, M, K, N):
     """Outputs with <= 32 rows run on the stacked-plane kernel (ring_gemm_small.cu)."""
     c = ctx(mpc, 1)
@@ -371,7 +371,8 @@ def test_small_m_accumulator_bounds(mpc, K):
 
 
 @pytest.mark.parametrize("P", [1, 2, 3])
-@pytest.mark.parametrize("M,K,N", [(32, 3000, 32), (1, 768, 1000), (100, 300, 20), (8, 70000, 8)])
+@pytest.mark.parametrize("M,K,N", [(32, 3000, 32), (1, 768, 1000), (100, 300, 20), (8, 70000, 8), (64, 64, 64),
+                                   (49, 1000, 130)])
 def test_small_m_beaver_parity(mpc, P, M, K, N):
     c = ctx(mpc, P)
     X, Y, xs, ys, a, b, cc = _beaver_case(P, M, K, N, seed=M + 2 * N, tid=90 + P)
