@@ -228,8 +228,9 @@ GemmChoice choose_gemm(int parties, int64_t M, int64_t N, int64_t K, bool allow_
     if (allow_small) consider(false, true);
     if (allow_small && allow_swap) consider(true, true);
     if (small_env == 1 && allow_small && !best.small) {
-        if (M <= kSmallRows) best = GemmChoice{false, true};
-        else if (allow_swap && N <= kSmallRows) best = GemmChoice{true, true};
+        if (M <= kSmallMaxRows && (M <= N || !allow_swap)) best = GemmChoice{false, true};
+        else if (allow_swap && N <= kSmallMaxRows) best = GemmChoice{true, true};
+        else if (M <= kSmallMaxRows) best = GemmChoice{false, true};
     }
     return best;
 }

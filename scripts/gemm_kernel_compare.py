@@ -18,6 +18,11 @@ import paper_2109_00984_b200 as mpc  # noqa: E402
 
 SHAPES = [(1, 2048, 1000), (1, 768, 1000), (32, 519820, 32), (16, 4096, 256), (32, 1024, 2048), (8, 8192, 8192),
           (32, 4096, 4096), (2048, 1024, 24)]
+MID = [(64, 64, 64), (49, 4608, 512), (49, 512, 2048), (49, 1024, 2048), (49, 2048, 512), (196, 2304, 256),
+       (196, 256, 1024), (100, 250, 250), (50, 12000, 250), (50, 1750, 250), (51, 8000, 2000), (51, 2000, 2000),
+       (51, 2000, 29), (197, 768, 768), (128, 1024, 1024)]
+if os.environ.get("SHAPES") == "mid":
+    SHAPES = MID
 
 
 def main():
