@@ -30,8 +30,17 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# stdout carries exactly one JSON line: NCCL's own log lines (e.g. its version banner) go to stderr
-os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+# stdout carries exactly one JSON line: file descriptor 1 is pointed at stderr for the whole run (NCCL
+# prints its version banner straight to stdout under NCCL_DEBUG=VERSION), and the line is written to a
+# duplicate of the original stdout
+_JSON_OUT = os.fdopen(os.dup(1), "w")
+os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    _JSON_OUT.write(json.dumps(line) + "\n")
+    _JSON_OUT.flush()
+
 
 import synth  # noqa: E402
 
@@ -235,7 +244,7 @@ def run_reference(args):
                              "sample": times[0]["sample"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "vs_baseline": None}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------- GPU leg
@@ -252,6 +261,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one GPU per rank; ranks beyond the visible devices share them (only for exercising the
+    # multi-process path on a 1-GPU box with --parties 1, where no NCCL communicator spans processes)
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     M, K, N = args.M, args.K, args.N
     P = args.parties
@@ -285,15 +297,16 @@ def main():
     Y = synth.uniform_fixed((K, N), 1003)
     Xd = torch.from_numpy(X.view(np.int64)).to(dev).view(torch.uint64)
     Yd = torch.from_numpy(Y.view(np.int64)).to(dev).view(torch.uint64)
+    src_y = 1 % P                      # y's data owner (party 0 when P = 1)
     holds_x = world == 1 or party == 0
-    holds_y = world == 1 or party == 1
+    holds_y = world == 1 or party == src_y
     pipeline = {}
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for rep in range(2):        # the first pass also pays the caching allocator's cudaMallocs
         sync_all()
         e0.record(stream)
         x = ctx.share(Xd if holds_x else None, 0, 1, shape=(M, K))
-        y = ctx.share(Yd if holds_y else None, 1, 2, shape=(K, N))
+        y = ctx.share(Yd if holds_y else None, src_y, 2, shape=(K, N))
         e1.record(stream)
         torch.cuda.synchronize(dev)
         pipeline["a2_share_ms"] = e0.elapsed_time(e1)
@@ -341,6 +354,40 @@ def main():
         t = torch.tensor([ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+
+    # ---- exposed communication: the same one-party schedule and kernels with the
+    # collectives on a 1-rank communicator (local copies) on this GPU; exposed = (t - t_no_comm) / t
+    exposed = None
+    if world > 1:
+        ms_local = -1.0
+        try:
+            c1 = mpc.Context(1, 0, device=local, master_seed=synth.MASTER_SEED, nccl_id=mpc.nccl_unique_id())
+            x1 = c1.share(Xd, 0, 1)
+            y1 = c1.share(Yd, 0, 2)
+            a1, b1, cc1 = c1.ttp_triples(1, M, K, N)
+            z1 = torch.empty_like(cc1)
+            for _ in range(max(args.warmup, 1)):
+                c1.beaver_matmul(x1, y1, a1, b1, cc1, truncate=True, out=z1)
+            torch.cuda.synchronize(dev)
+            t0.record(stream)
+            for _ in range(args.steps):
+                c1.beaver_matmul(x1, y1, a1, b1, cc1, truncate=True, out=z1)
+            t1.record(stream)
+            torch.cuda.synchronize(dev)
+            ms_local = t0.elapsed_time(t1) / args.steps
+            del x1, y1, a1, b1, cc1, z1
+            c1.close()
+        except Exception as e:  # noqa: BLE001 — report, never hang the other ranks
+            print(f"[bench] exposed-communication probe failed on rank {rank}: {e}", file=sys.stderr)
+        tl = torch.tensor([ms_local], dtype=torch.float64)
+        tmin = tl.clone()
+        dist.all_reduce(tl, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tmin, op=dist.ReduceOp.MIN)
+        if float(tmin.item()) > 0:
+            exposed = {"ms_per_step": ms, "ms_per_step_no_comm": float(tl.item()),
+                       "frac": (ms - float(tl.item())) / ms,
+                       "how": "same one-party kernels and streams with the reveals on a 1-rank NCCL communicator "
+                              "(local copies), max over ranks; SURVEY 8(d) exposed communication"}
 
     # ---- a10: reveal + decode of the result (correctness only, off the timed path)
     e0.record(stream)
@@ -396,7 +443,7 @@ def main():
                 # encode without a per-step host sync; overflow is checked once after the timed region
                 ctx.share(ctx.encode(dX[s], out=xe, check=False) if holds_x else None, 0, 2 * sid, shape=(M, K),
                           out=x)
-                ctx.share(ctx.encode(dY[s], out=ye, check=False) if holds_y else None, 1, 2 * sid + 1,
+                ctx.share(ctx.encode(dY[s], out=ye, check=False) if holds_y else None, src_y, 2 * sid + 1,
                           shape=(K, N), out=y)
                 done[s].record(stream)
                 ctx.beaver_matmul(x, y, a, b, c, truncate=True, out=z)
@@ -480,6 +527,8 @@ def main():
     }
     if e2e:
         line["e2e"] = e2e
+    if exposed:
+        line["exposed_comm"] = exposed
     if world == 1 and not args.no_next_rows:
         # elementwise private product / square (HBM-bound), same parties, n = M*N
         sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "scripts"))
@@ -491,7 +540,7 @@ def main():
         line["configs_measured"] = bench_configs.run()
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = oracle_baseline(M, K, N)
-    print(json.dumps(line), flush=True)
+    emit(line)
     if world > 1:
         dist.barrier()
 
