@@ -192,11 +192,14 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
                         const uint8_t* srcB = S.B + party * S.party_stride_B + (rbB * S.kb + kb) * (8 * GR::kBlock);
                         if (p.dbg) { const long long w0 = clock64(); mbar_wait(&B.empty[s], ph ^ 1); st_empty += clock64() - w0; }
                         else mbar_wait(&B.empty[s], ph ^ 1);
+                        const bool drop = p.fault_inject && kt == klo && w == (int)cluster_id();
                         if (elect_one()) {
                             mbar_expect_tx(&B.full[s], bytesA + bytesB);
                             uint8_t* st = B.stage_base + s * kStageBytes;
-                            bulk_g2s(st, srcA, bytesA, &B.full[s]);
-                            bulk_g2s(st + kAStage, srcB, bytesB, &B.full[s]);
+                            if (!drop) {
+                                bulk_g2s(st, srcA, bytesA, &B.full[s]);
+                                bulk_g2s(st + kAStage, srcB, bytesB, &B.full[s]);
+                            }
                         }
                         __syncwarp();
                         if (++s == kStages) { s = 0; ph ^= 1; }
@@ -502,6 +505,8 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     RingGemmParams q = prm;
     static const int env_group = getenv("MPC_GEMM_GROUPM") ? atoi(getenv("MPC_GEMM_GROUPM")) : 0;
     if (q.group_m <= 0) q.group_m = env_group;
+    static const int env_fault = getenv("MPC_GEMM_FAULT_INJECT") ? atoi(getenv("MPC_GEMM_FAULT_INJECT")) : 0;
+    q.fault_inject = env_fault;
     q.splits = prm.partials ? ring_gemm_splits(parties, prm.M, prm.N, tkb, max_clusters, prm.small != 0) : 1;
     if (prm.small) {
         if (q.splits > 1) q.partial_stride = ring_gemm_out_elems(q, parties);

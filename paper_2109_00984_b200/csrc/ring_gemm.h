@@ -39,6 +39,8 @@ struct RingGemmParams {
                                         // convolution whose im2col rows are (b, pixel s).  C likewise.
     int small;                          // 1: stacked-plane kernel (M <= 32, planes in Layout::Small)
     int group_m;                        // row tiles per scheduling group of the 2-CTA kernel (0: default 4)
+    int fault_inject;                   // test hook (MPC_GEMM_FAULT_INJECT=1): drop one stage's copies, so the
+                                        // pipeline stalls and the mbarrier watchdog must trap
 };
 
 // Two kernels: the 2-CTA 256 x 128 kernel (planes in Layout::Left / Right) and

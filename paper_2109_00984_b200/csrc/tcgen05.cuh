@@ -45,20 +45,43 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(caddr) : "memory");
 }
+// Waits with a watchdog: the first try_wait is the fast path; a wait that has
+// not completed after 2^34 cycles (~9 s; every legitimate wait in these kernels
+// is a pipeline hand-off of microseconds) traps, so a protocol error (a lost
+// arrive, a TMEM / mbarrier misuse) fails the launch with an error instead of
+// hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred p, q;\n\t.reg .b64 t0, t1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@p bra DONE_%=;\n\t"
+        "mov.u64 t0, %%clock64;\n\t"
         "WAIT_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}"
+        "@p bra DONE_%=;\n\t"
+        "mov.u64 t1, %%clock64;\n\t"
+        "sub.s64 t1, t1, t0;\n\t"
+        "setp.gt.s64 q, t1, 17179869184;\n\t"
+        "@q trap;\n\t"
+        "bra WAIT_%=;\n\t"
+        "DONE_%=:\n\t}"
         :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred p, q;\n\t.reg .b64 t0, t1;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@p bra DONEC_%=;\n\t"
+        "mov.u64 t0, %%clock64;\n\t"
         "WAITC_%=:\n\t"
         "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAITC_%=;\n\t}"
+        "@p bra DONEC_%=;\n\t"
+        "mov.u64 t1, %%clock64;\n\t"
+        "sub.s64 t1, t1, t0;\n\t"
+        "setp.gt.s64 q, t1, 17179869184;\n\t"
+        "@q trap;\n\t"
+        "bra WAITC_%=;\n\t"
+        "DONEC_%=:\n\t}"
         :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {

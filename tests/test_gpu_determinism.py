@@ -79,3 +79,26 @@ def test_same_shares_under_every_launch_config(case, env):
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     assert out.stdout.strip().splitlines()[-1] == expected, env
+
+
+def test_mbarrier_watchdog_traps_instead_of_hanging():
+    """A stage whose bulk copies are dropped (MPC_GEMM_FAULT_INJECT=1) never
+    completes its mbarrier; the wait watchdog (2^34 cycles) traps, so the call
+    fails with a CUDA error in seconds instead of hanging the GPU."""
+    script = r"""
+import sys; sys.path.insert(0, {root!r})
+import torch, synth
+import paper_2109_00984_b200 as m
+c = m.Context(1, m.ALL_PARTIES, device=0)
+A = torch.zeros((300, 300), dtype=torch.uint64, device="cuda")
+try:
+    C = c.ring_matmul(A, A)
+    torch.cuda.synchronize()
+except Exception as e:
+    print("FAILED:", type(e).__name__)
+    sys.exit(3)
+print("NO-TRAP")
+""".format(root=ROOT)
+    env = dict(os.environ, MPC_GEMM_FAULT_INJECT="1")
+    out = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=180)
+    assert out.returncode != 0 and "NO-TRAP" not in out.stdout, (out.stdout, out.stderr[-2000:])
