@@ -193,6 +193,21 @@ mpc_status mpc_beaver_finish(mpc_ctx ctx, const uint64_t* ed, const uint64_t* a,
                              const uint64_t* c, uint64_t* z, int64_t M, int64_t K, int64_t N,
                              int truncate, void* workspace, size_t workspace_bytes);
 
+/* ---- a batch of independent Beaver matmuls of one shape -------
+ * z[i] = x[i] @ y[i] for i < batch (e.g. the heads of an attention layer), as
+ * mpc_beaver_matmul on each i with triple (a[i], b[i], c[i]) — bit-identical — but
+ * every eps || delta of the batch in ONE reveal round and one split + one ring
+ * GEMM launch for the whole batch (the GEMM walks batch x parties instances).
+ * Layout: x [P][batch][M][K], y [P][batch][K][N], a like x, b like y, c and z
+ * [P][batch][M][N] for all-parties contexts; without the leading P for one party.
+ * workspace: mpc_workspace_bytes_batched(ctx, batch, M, K, N).  Rounds: 1 (+1 for
+ * Alg. 1 when P > 2 and truncate).  batch <= 65536; errors as mpc_beaver_matmul. */
+size_t mpc_workspace_bytes_batched(mpc_ctx ctx, int64_t batch, int64_t M, int64_t K, int64_t N);
+mpc_status mpc_beaver_matmul_batched(mpc_ctx ctx, int64_t batch, const uint64_t* x, const uint64_t* y,
+                                     const uint64_t* a, const uint64_t* b, const uint64_t* c, uint64_t* z,
+                                     int64_t M, int64_t K, int64_t N, int truncate, uint64_t wrap_id,
+                                     void* workspace, size_t workspace_bytes);
+
 /* ---- the Beaver matmul in two halves: weights known ahead ------
  * mpc_beaver_prepare is the input-independent y side: d_p = y_p - b_p, delta =
  * reveal(d) (1 round, 8KN bytes), and the limb planes of delta and of

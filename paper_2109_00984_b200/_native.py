@@ -42,6 +42,8 @@ SIGNATURES = [
     ("mpc_beaver_matmul", _I, [_V, _V, _V, _V, _V, _V, _V, _L, _L, _L, _I, _U, _V, _S]),
     ("mpc_beaver_mask", _I, [_V, _V, _V, _V, _V, _V, _L, _L, _L]),
     ("mpc_beaver_finish", _I, [_V, _V, _V, _V, _V, _V, _L, _L, _L, _I, _V, _S]),
+    ("mpc_workspace_bytes_batched", _S, [_V, _L, _L, _L, _L]),
+    ("mpc_beaver_matmul_batched", _I, [_V, _L, _V, _V, _V, _V, _V, _V, _L, _L, _L, _I, _U, _V, _S]),
     ("mpc_beaver_prepare", _I, [_V, _V, _V, _L, _L, _L, _V, _S]),
     ("mpc_beaver_matmul_prepared", _I, [_V, _V, _V, _V, _V, _L, _L, _L, _I, _U, _V, _S]),
     ("mpc_truncate", _I, [_V, _V, _L, _I, _U]),

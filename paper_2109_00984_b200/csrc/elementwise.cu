@@ -136,10 +136,17 @@ __device__ __forceinline__ void split_left_body(const LeftSplitArgs& a, int64_t 
     const int64_t row_groups = (a.M + 7) / 8;
     const int64_t kgroups = (KB * kKBlock + 63) / 64;      // whole padded K: pad limbs must be 0
     const int64_t warps_total = row_groups * kgroups;
+    const int64_t nb = a.batch > 1 ? a.batch : 1;
     const int lane = threadIdx.x & 31;
-    const bool vec = (a.K & 1) == 0 && (a.party_stride & 1) == 0;
+    const bool vec = (a.K & 1) == 0 && (a.party_stride & 1) == 0 && (a.in_bstride & 1) == 0;
     const bool fused_copy = a.cp_src == a.minus && a.Pcopy == a.Psum && a.Psum > 0;
-    for (int64_t w = (bid * blockDim.x + threadIdx.x) >> 5; w < warps_total; w += (nblk * blockDim.x) >> 5) {
+    for (int64_t bw = (bid * blockDim.x + threadIdx.x) >> 5; bw < warps_total * nb; bw += (nblk * blockDim.x) >> 5) {
+        const int64_t bi = bw / warps_total, w = bw - bi * warps_total;      // batch element, warp task
+        const uint64_t* plus = a.plus ? a.plus + bi * a.in_bstride : nullptr;
+        const uint64_t* minus = a.minus ? a.minus + bi * a.in_bstride : nullptr;
+        const uint64_t* cp_src = a.cp_src ? a.cp_src + bi * a.in_bstride : nullptr;
+        uint8_t* sum_planes = a.sum_planes ? a.sum_planes + bi * a.sum_bstride : nullptr;
+        uint8_t* cp_planes = a.cp_planes ? a.cp_planes + bi * a.cp_bstride : nullptr;
         const int64_t rg = w / kgroups, kg = w % kgroups;
         const int64_t row = rg * 8 + (lane & 7);
         const int64_t k0 = kg * 64 + (lane >> 3) * 16;
@@ -151,29 +158,29 @@ __device__ __forceinline__ void split_left_body(const LeftSplitArgs& a, int64_t 
         for (int m = 0; m < 16; ++m) acc[m] = 0;
         if (a.Psum > 0) {
             for (int p = 0; p < a.Psum; ++p) {
-                load16(a.plus + p * a.party_stride + row * a.K + k0, full, vec, kleft, v);
+                load16(plus + p * a.party_stride + row * a.K + k0, full, vec, kleft, v);
 #pragma unroll
                 for (int m = 0; m < 16; ++m) acc[m] += v[m];
-                if (a.minus) {
-                    load16(a.minus + p * a.party_stride + row * a.K + k0, full, vec, kleft, v);
+                if (minus) {
+                    load16(minus + p * a.party_stride + row * a.K + k0, full, vec, kleft, v);
 #pragma unroll
                     for (int m = 0; m < 16; ++m) acc[m] -= v[m];
                     // party 0's copy needs the complete sum first (add_sum_first): written below
                     if (fused_copy && !(p == 0 && a.add_sum_first))
-                        store_limbs16<LO>(a.cp_planes + p * a.cp_planes_stride, row, k0, KB, v);
+                        store_limbs16<LO>(cp_planes + p * a.cp_planes_stride, row, k0, KB, v);
                 }
             }
-            store_limbs16<LO>(a.sum_planes, row, k0, KB, acc);
+            store_limbs16<LO>(sum_planes, row, k0, KB, acc);
         }
         for (int q = 0; q < a.Pcopy; ++q) {
             const bool adds = q == 0 && a.add_sum_first;
             if (fused_copy && !adds) continue;             // already written from registers
-            load16(a.cp_src + q * a.party_stride + row * a.K + k0, full, vec, kleft, v);
+            load16(cp_src + q * a.party_stride + row * a.K + k0, full, vec, kleft, v);
             if (adds) {
 #pragma unroll
                 for (int m = 0; m < 16; ++m) v[m] += acc[m];
             }
-            store_limbs16<LO>(a.cp_planes + q * a.cp_planes_stride, row, k0, KB, v);
+            store_limbs16<LO>(cp_planes + q * a.cp_planes_stride, row, k0, KB, v);
         }
     }
 }
@@ -183,7 +190,7 @@ __global__ void __launch_bounds__(256) split_left_kernel(LeftSplitArgs a) {
 }
 cudaError_t launch_split_left(const LeftSplitArgs& a, cudaStream_t st) {
     if (a.M == 0 || a.K == 0) return cudaSuccess;
-    const int64_t warps = ((a.M + 7) / 8) * ((num_kb(a.K) * kKBlock + 63) / 64);
+    const int64_t warps = ((a.M + 7) / 8) * ((num_kb(a.K) * kKBlock + 63) / 64) * (a.batch > 1 ? a.batch : 1);
     if (a.swap == 2) split_left_kernel<Layout::Small><<<grid_for(warps * 32), 256, 0, st>>>(a);
     else if (a.swap) split_left_kernel<Layout::Right><<<grid_for(warps * 32), 256, 0, st>>>(a);
     else split_left_kernel<Layout::Left><<<grid_for(warps * 32), 256, 0, st>>>(a);
@@ -229,10 +236,17 @@ __device__ __forceinline__ void split_right_body(const RightSplitArgs& a, int64_
     const int64_t ngroups = (a.N + 31) / 32;
     const int64_t kchunks = KB * 2;                         // whole padded K, 16 per chunk
     const int64_t warps_total = ngroups * kchunks;
+    const int64_t nb = a.batch > 1 ? a.batch : 1;
     const int lane = threadIdx.x & 31;
     const bool fused_copy = a.cp_src == a.minus && a.Pcopy == a.Psum && a.Psum > 0;
-    const bool even = (a.N & 1) == 0 && (a.party_stride & 1) == 0;
-    for (int64_t w = (bid * blockDim.x + threadIdx.x) >> 5; w < warps_total; w += (nblk * blockDim.x) >> 5) {
+    const bool even = (a.N & 1) == 0 && (a.party_stride & 1) == 0 && (a.in_bstride & 1) == 0;
+    for (int64_t bw = (bid * blockDim.x + threadIdx.x) >> 5; bw < warps_total * nb; bw += (nblk * blockDim.x) >> 5) {
+        const int64_t bi = bw / warps_total, w = bw - bi * warps_total;      // batch element, warp task
+        const uint64_t* plus = a.plus ? a.plus + bi * a.in_bstride : nullptr;
+        const uint64_t* minus = a.minus ? a.minus + bi * a.in_bstride : nullptr;
+        const uint64_t* cp_src = a.cp_src ? a.cp_src + bi * a.in_bstride : nullptr;
+        uint8_t* sum_planes = a.sum_planes ? a.sum_planes + bi * a.sum_bstride : nullptr;
+        uint8_t* cp_planes = a.cp_planes ? a.cp_planes + bi * a.cp_bstride : nullptr;
         const int64_t kc = w / ngroups, ng = w % ngroups;
         const int64_t n = ng * 32 + 2 * (lane & 15);
         const int64_t k0 = kc * 16 + (lane >> 4) * 8;
@@ -243,33 +257,33 @@ __device__ __forceinline__ void split_right_body(const RightSplitArgs& a, int64_
 #pragma unroll
         for (int m = 0; m < 8; ++m) { d[0][m] = 0; d[1][m] = 0; }
         for (int p = 0; p < a.Psum; ++p) {
-            load_cols(a.plus + p * a.party_stride, a.N, n, k0, a.K, vec, two, v);
+            load_cols(plus + p * a.party_stride, a.N, n, k0, a.K, vec, two, v);
 #pragma unroll
             for (int m = 0; m < 8; ++m) { d[0][m] += v[0][m]; d[1][m] += v[1][m]; }
-            if (a.minus) {
-                load_cols(a.minus + p * a.party_stride, a.N, n, k0, a.K, vec, two, v);
+            if (minus) {
+                load_cols(minus + p * a.party_stride, a.N, n, k0, a.K, vec, two, v);
 #pragma unroll
                 for (int m = 0; m < 8; ++m) { d[0][m] -= v[0][m]; d[1][m] -= v[1][m]; }
                 if (fused_copy && !(p == 0 && a.add_delta_first)) {
-                    uint8_t* pl = a.cp_planes + p * a.cp_planes_stride;
+                    uint8_t* pl = cp_planes + p * a.cp_planes_stride;
                     store_limbs8<LO>(pl, n, k0, KB, v[0]);
                     if (two) store_limbs8<LO>(pl, n + 1, k0, KB, v[1]);
                 }
             }
         }
-        if (a.sum_planes) {
-            store_limbs8<LO>(a.sum_planes, n, k0, KB, d[0]);
-            if (two) store_limbs8<LO>(a.sum_planes, n + 1, k0, KB, d[1]);
+        if (sum_planes) {
+            store_limbs8<LO>(sum_planes, n, k0, KB, d[0]);
+            if (two) store_limbs8<LO>(sum_planes, n + 1, k0, KB, d[1]);
         }
         for (int q = 0; q < a.Pcopy; ++q) {
             const bool addd = (q == 0) && a.add_delta_first;
             if (fused_copy && !addd) continue;               // already written from registers
-            load_cols(a.cp_src + q * a.party_stride, a.N, n, k0, a.K, vec, two, v);
+            load_cols(cp_src + q * a.party_stride, a.N, n, k0, a.K, vec, two, v);
             if (addd) {
 #pragma unroll
                 for (int m = 0; m < 8; ++m) { v[0][m] += d[0][m]; v[1][m] += d[1][m]; }
             }
-            uint8_t* pl = a.cp_planes + q * a.cp_planes_stride;
+            uint8_t* pl = cp_planes + q * a.cp_planes_stride;
             store_limbs8<LO>(pl, n, k0, KB, v[0]);
             if (two) store_limbs8<LO>(pl, n + 1, k0, KB, v[1]);
         }
@@ -281,7 +295,7 @@ __global__ void __launch_bounds__(256, 2) split_right_kernel(RightSplitArgs a) {
 }
 cudaError_t launch_split_right(const RightSplitArgs& a, cudaStream_t st) {
     if (a.N == 0 || a.K == 0) return cudaSuccess;
-    const int64_t warps = ((a.N + 31) / 32) * (num_kb(a.K) * 2);
+    const int64_t warps = ((a.N + 31) / 32) * (num_kb(a.K) * 2) * (a.batch > 1 ? a.batch : 1);
     if (a.swap == 2) split_right_kernel<Layout::Small><<<grid_for(warps * 32), 256, 0, st>>>(a);
     else if (a.swap) split_right_kernel<Layout::Left><<<grid_for(warps * 32), 256, 0, st>>>(a);
     else split_right_kernel<Layout::Right><<<grid_for(warps * 32), 256, 0, st>>>(a);
@@ -307,11 +321,12 @@ cudaError_t launch_split_both(const LeftSplitArgs& l, const RightSplitArgs& r, c
     if (!dl && !dr) return cudaSuccess;
     if (!dr) return launch_split_left(l, st);
     if (!dl) return launch_split_right(r, st);
-    const int64_t wl = ((l.M + 7) / 8) * ((num_kb(l.K) * kKBlock + 63) / 64) * 32;
-    const int64_t wr = ((r.N + 31) / 32) * (num_kb(r.K) * 2) * 32;
+    const int64_t bl = l.batch > 1 ? l.batch : 1, br = r.batch > 1 ? r.batch : 1;
+    const int64_t wl = ((l.M + 7) / 8) * ((num_kb(l.K) * kKBlock + 63) / 64) * 32 * bl;
+    const int64_t wr = ((r.N + 31) / 32) * (num_kb(r.K) * 2) * 32 * br;
     // share the block budget in proportion to the bytes each side moves
-    const int64_t bytes_l = l.M * l.K * (int64_t)(2 * l.Psum + l.Pcopy + 1);
-    const int64_t bytes_r = r.N * r.K * (int64_t)(2 * r.Psum + r.Pcopy + 1);
+    const int64_t bytes_l = l.M * l.K * (int64_t)(2 * l.Psum + l.Pcopy + 1) * bl;
+    const int64_t bytes_r = r.N * r.K * (int64_t)(2 * r.Psum + r.Pcopy + 1) * br;
     int64_t nl = std::min<int64_t>(grid_for(wl), std::max<int64_t>(1, 148 * 16 * bytes_l / (bytes_l + bytes_r)));
     int64_t nr = std::min<int64_t>(grid_for(wr), std::max<int64_t>(1, 148 * 16 - nl));
     if (l.swap != r.swap) return cudaErrorInvalidValue;

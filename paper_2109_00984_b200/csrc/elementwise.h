@@ -23,6 +23,9 @@ struct LeftSplitArgs {
                                      // 2 Layout::Small (stacked-plane GEMM)
     int add_sum_first;               // copy of party 0 gets + the sum (b'_0 = b_0 + delta, R8), for weights
                                      // given rows x K (conv: Cout x C*kh*kw)
+    int batch;                       // independent matrices (0/1 = one): element b reads its inputs at
+    int64_t in_bstride;              //   + b * in_bstride (elements) and writes planes at
+    int64_t sum_bstride, cp_bstride; //   + b * sum_bstride / cp_bstride (bytes)
 };
 
 struct RightSplitArgs {
@@ -39,6 +42,9 @@ struct RightSplitArgs {
     int64_t cp_planes_stride;
     int swap;                        // plane layout: 0 Layout::Right, 1 Layout::Left (transposed ring GEMM),
                                      // 2 Layout::Small (stacked-plane GEMM)
+    int batch;                       // as LeftSplitArgs
+    int64_t in_bstride;
+    int64_t sum_bstride, cp_bstride;
 };
 
 struct TtpGenArgs {

@@ -260,6 +260,8 @@ struct BeaverWs {
     uint64_t* zbuf;      // one-party, P > 2, truncation: z reveal
     int8_t* hbuf;        // one-party, P > 2, truncation: top nibbles
     uint64_t* partials;  // ring GEMM split-K slabs (small shapes only)
+    int64_t batch;       // independent matmuls (mpc_beaver_matmul_batched; 1 otherwise)
+    int64_t xs, ys;      // bytes of one matrix's x-side / y-side planes (the batch strides)
     size_t total;
 };
 
@@ -267,28 +269,33 @@ struct BeaverWs {
 // convolution reveals at the input / weight shapes instead).  allow_swap: the
 // transposed GEMM is possible for this output layout.
 BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N, int64_t ed_elems = -1,
-                      bool allow_swap = true, bool allow_small = true) {
+                      bool allow_swap = true, bool allow_small = true, int64_t batch = 1) {
     const int Pl = c->all ? c->P : 1;
     Carve cv(ws);
     BeaverWs w{};
-    const GemmChoice gc = choose_gemm(Pl, M, N, K, allow_swap, allow_small);
+    w.batch = batch < 1 ? 1 : batch;
+    const int inst = (int)(Pl * w.batch);                     // GEMM instances
+    const GemmChoice gc = choose_gemm(inst, M, N, K, allow_swap, allow_small);
     w.swap = gc.swap;
     w.small = gc.small;
     if (ed_elems < 0) ed_elems = M * K + K * N;
     const int64_t xs = w.small ? planes_bytes<Layout::Small>(M, K) : (w.swap ? rp(M, K) : lp(M, K));   // eps, a_p
     const int64_t ys = w.small ? planes_bytes<Layout::Small>(N, K) : (w.swap ? lp(N, K) : rp(N, K));   // delta, b'_p
     const int64_t gM = w.swap ? N : M, gN = w.swap ? M : N;   // the GEMM's own output sizes
-    w.a_stride = xs;
-    w.b_stride = ys;
-    w.eps_pl = cv.take(xs);
-    w.delta_pl = cv.take(ys);
-    w.a_pl = cv.take((size_t)Pl * xs);
-    w.b_pl = cv.take((size_t)Pl * ys);
-    w.ed = reinterpret_cast<uint64_t*>(c->all ? nullptr : cv.take(8 * (size_t)ed_elems));
+    const int64_t B = w.batch;
+    w.xs = xs;
+    w.ys = ys;
+    w.a_stride = B * xs;                                      // party strides; batch stride xs / ys
+    w.b_stride = B * ys;
+    w.eps_pl = cv.take(B * xs);
+    w.delta_pl = cv.take(B * ys);
+    w.a_pl = cv.take((size_t)Pl * B * xs);
+    w.b_pl = cv.take((size_t)Pl * B * ys);
+    w.ed = reinterpret_cast<uint64_t*>(c->all ? nullptr : cv.take(8 * (size_t)(B * ed_elems)));
     const bool alg1_one = !c->all && c->P > 2;
-    w.zbuf = reinterpret_cast<uint64_t*>(alg1_one ? cv.take(8 * (size_t)(M * N)) : nullptr);
-    w.hbuf = reinterpret_cast<int8_t*>(alg1_one ? cv.take((size_t)(M * N)) : nullptr);
-    size_t pb = ring_gemm_partials_bytes(Pl, gM, gN, 2 * (int)num_kb(K), 0, w.small);
+    w.zbuf = reinterpret_cast<uint64_t*>(alg1_one ? cv.take(8 * (size_t)(B * M * N)) : nullptr);
+    w.hbuf = reinterpret_cast<int8_t*>(alg1_one ? cv.take((size_t)(B * M * N)) : nullptr);
+    size_t pb = ring_gemm_partials_bytes(inst, gM, gN, 2 * (int)num_kb(K), 0, w.small);
     if (!c->all)   // the overlapped schedule runs two half-K GEMMs, the first on fewer SMs
         pb = std::max({pb, ring_gemm_partials_bytes(1, gM, gN, (int)num_kb(K), kOverlapClusters, w.small),
                        ring_gemm_partials_bytes(1, gM, gN, (int)num_kb(K), 0, w.small)});
@@ -302,13 +309,16 @@ BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N, int6
 inline int lay(const BeaverWs& w) { return w.small ? 2 : (w.swap ? 1 : 0); }
 RingGemmSegment seg_of(const BeaverWs& w, const uint8_t* X, int64_t xstride, const uint8_t* Y, int64_t ystride,
                        int kb) {
-    return w.swap ? RingGemmSegment{Y, X, kb, ystride, xstride} : RingGemmSegment{X, Y, kb, xstride, ystride};
+    return w.swap ? RingGemmSegment{Y, X, kb, ystride, xstride, w.ys, w.xs}
+                  : RingGemmSegment{X, Y, kb, xstride, ystride, w.xs, w.ys};
 }
 void set_out(RingGemmParams& p, const BeaverWs& w, int64_t M, int64_t N) {
     p.M = w.swap ? N : M;
     p.N = w.swap ? M : N;
     p.transpose_out = w.swap ? 1 : 0;
     p.small = w.small ? 1 : 0;
+    p.batch = (int)w.batch;
+    p.batch_stride_c = p.batch_stride_z = M * N;
 }
 
 mpc_status beaver_local(mpc_ctx c, const BeaverWs& w, const uint64_t* ed, const uint64_t* a, const uint64_t* b,
@@ -729,6 +739,51 @@ mpc_status mpc_beaver_finish(mpc_ctx c, const uint64_t* ed, const uint64_t* a, c
     return beaver_local(c, w, ed, a, b, cc, z, M, K, N, truncate);
 }
 
+// ---- a batch of independent Beaver matmuls of one shape (e.g. attention heads) ----
+mpc_status mpc_beaver_matmul_batched(mpc_ctx c, int64_t batch, const uint64_t* x, const uint64_t* y,
+                                     const uint64_t* a, const uint64_t* b, const uint64_t* cc, uint64_t* z, int64_t M,
+                                     int64_t K, int64_t N, int truncate, uint64_t wrap_id, void* ws, size_t ws_bytes) {
+    CHECK(enter(c));
+    if (batch < 0 || M < 0 || K < 0 || N < 0) return fail(c, MPC_ERR_SHAPE, "beaver_matmul_batched: negative size");
+    if (batch > 65536 || K > (int64_t)1 << 30 || M > (int64_t)1 << 31 || N > (int64_t)1 << 31)
+        return fail(c, MPC_ERR_SHAPE, "beaver_matmul_batched: too large");
+    const BeaverWs w = carve_beaver(c, ws, M, K, N, -1, true, true, batch < 1 ? 1 : batch);
+    if (ws_bytes < w.total) return fail(c, MPC_ERR_SHAPE, "beaver_matmul_batched: workspace %zu < %zu", ws_bytes, w.total);
+    const int Pl = c->all ? c->P : 1;
+    const int64_t sMK = M * K, sKN = K * N, sMN = M * N;
+    c->rounds += 1;                                   // every eps || delta of the batch: one reveal
+    c->bytes += 8ull * (uint64_t)(batch * (sMK + sKN)) * Pl;
+    if (batch == 0 || M == 0 || N == 0) return MPC_OK;
+    if ((sMK && (!x || !a)) || (sKN && (!y || !b)) || !cc || !z || (!ws && w.total))
+        return fail(c, MPC_ERR_ARG, "beaver_matmul_batched: null pointer");
+    const int code = lay(w);
+    if (c->all) {
+        LeftSplitArgs L{M, K, batch * sMK, x, a, c->P, w.eps_pl, a, c->P, w.a_pl, w.a_stride, code, 0,
+                        batch, sMK, w.xs, w.xs};
+        RightSplitArgs R{K, N, batch * sKN, y, b, c->P, w.delta_pl, b, c->P, 1, w.b_pl, w.b_stride, code,
+                         batch, sKN, w.ys, w.ys};
+        CHECK(run(c, kClsSplit, "mask+reveal+split (batched)", [&] { return launch_split_both(L, R, c->stream); }));
+    } else {
+        // one party: [e (batch x M x K) | d (batch x K x N)] -> one reveal -> splits
+        uint64_t* e = w.ed;
+        uint64_t* d = w.ed + batch * sMK;
+        CHECK(run(c, kClsSplit, "mask", [&] { return launch_mask(x, a, batch * sMK, y, b, batch * sKN, e, c->stream); }));
+        if (c->P > 1) CHECK(comm_allreduce(c, e, e, (size_t)(batch * (sMK + sKN)), RedOp::SumU64, "eps/delta reveal"));
+        LeftSplitArgs L{M, K, 0, e, nullptr, 1, w.eps_pl, a, 1, w.a_pl, 0, code, 0, batch, sMK, w.xs, w.xs};
+        RightSplitArgs R{K, N, 0, d, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0, code,
+                         batch, sKN, w.ys, w.ys};
+        CHECK(run(c, kClsSplit, "split eps/delta (batched)", [&] { return launch_split_both(L, R, c->stream); }));
+    }
+    CHECK(beaver_gemm(c, w, cc, z, M, K, N, truncate));
+    if (truncate && c->P > 2) CHECK(truncate_impl(c, z, batch * sMN, c->frac, wrap_id, w.zbuf, w.hbuf));
+    return MPC_OK;
+}
+
+size_t mpc_workspace_bytes_batched(mpc_ctx c, int64_t batch, int64_t M, int64_t K, int64_t N) {
+    if (!c || batch < 0 || M < 0 || K < 0 || N < 0) return 0;
+    return carve_beaver(c, nullptr, M, K, N, -1, true, true, batch < 1 ? 1 : batch).total;
+}
+
 // ---- the input-independent y side (weights known ahead), then the x side ----
 mpc_status mpc_beaver_prepare(mpc_ctx c, const uint64_t* y, const uint64_t* b, int64_t M, int64_t K, int64_t N,
                               void* ws, size_t ws_bytes) {
@@ -843,7 +898,7 @@ mpc_status beaver_gemm(mpc_ctx c, const BeaverWs& w, const uint64_t* cc, uint64_
     p.nseg = 2;
     set_out(p, w, M, N);
     p.C = cc; p.Z = z;
-    p.party_stride_c = p.party_stride_z = sMN;
+    p.party_stride_c = p.party_stride_z = w.batch * sMN;
     p.trunc_bits = (truncate && c->P <= 2) ? c->frac : 0;                                     // fused, 0 rounds
     return gemm_run(c, p, Pl);
 }

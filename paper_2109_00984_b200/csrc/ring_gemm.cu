@@ -99,8 +99,9 @@ struct TileMap {
 // 32-K block sequence per tile (split-K for shapes with few tiles); the
 // ranges of one tile are consecutive items, so they run concurrently.
 struct WorkMap {
-    TileMap tm;
+    TileMap tm;                                      // tm.parties = instances = parties x batch
     int tkb, kc, splits;
+    int nparties;                                    // parties per batch element
     __device__ int items() const { return tm.parties * tm.mt * tm.nt * splits; }
     // 32-bit arithmetic only (the launcher uses splits > 1 only for tkb < 2^24),
     // and results broadcast from lane 0: the role loops must stay provably
@@ -177,6 +178,8 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
         for (int w = cluster_id(); w < wm.items(); w += nclusters()) {
             int party, m, n, klo, khi;
             wm.decode(w, party, m, n, klo, khi);
+            const int bi = party / wm.nparties;              // instance -> (batch element, party)
+            party -= bi * wm.nparties;
             const int64_t rbA = (int64_t)m * 2 + rank;       // 128-row left block
             const int64_t rbB = (int64_t)n * 2 + rank;       // 64-row right block
             for (int k0 = klo; k0 < khi; k0 += kc) {
@@ -188,8 +191,10 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
                         const int sg = (kt < p.seg[0].kb) ? 0 : 1;
                         const RingGemmSegment& S = p.seg[sg];
                         const int kb = kt - (sg ? p.seg[0].kb : 0);
-                        const uint8_t* srcA = S.A + party * S.party_stride_A + (rbA * S.kb + kb) * (8 * GL::kBlock);
-                        const uint8_t* srcB = S.B + party * S.party_stride_B + (rbB * S.kb + kb) * (8 * GR::kBlock);
+                        const uint8_t* srcA = S.A + party * S.party_stride_A + bi * S.batch_stride_A +
+                                              (rbA * S.kb + kb) * (8 * GL::kBlock);
+                        const uint8_t* srcB = S.B + party * S.party_stride_B + bi * S.batch_stride_B +
+                                              (rbB * S.kb + kb) * (8 * GR::kBlock);
                         if (p.dbg) { const long long w0 = clock64(); mbar_wait(&B.empty[s], ph ^ 1); st_empty += clock64() - w0; }
                         else mbar_wait(&B.empty[s], ph ^ 1);
                         const bool drop = p.fault_inject && kt == klo && w == (int)cluster_id();
@@ -308,6 +313,8 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Wor
     for (int w = cluster_id(); w < wm.items(); w += nclusters()) {
         int party, m, n, klo, khi;
         wm.decode(w, party, m, n, klo, khi);
+        const int bi = party / wm.nparties;                  // instance -> (batch element, party)
+        party -= bi * wm.nparties;
         uint64_t run[64];
 #pragma unroll
         for (int j = 0; j < 64; ++j) run[j] = 0;
@@ -350,7 +357,8 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Wor
             // the slabs (ring addition commutes, any order is exact), c_p, and
             // applies the truncation.
             const int s = w % wm.splits;
-            uint64_t* pb = p.partials + (int64_t)s * p.partial_stride + party * p.M * p.N + off;
+            uint64_t* pb = p.partials + (int64_t)s * p.partial_stride + party * p.party_stride_z +
+                           bi * p.batch_stride_z + off;
             if (full) {
 #pragma unroll
                 for (int j = 0; j < 64; j += 4) st_stream4(pb + j, &run[j], pol);
@@ -364,8 +372,8 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Wor
             // element is read before it is written by the same thread.  Batches of
             // 16 columns: all loads of a batch are issued before its stores, so a
             // row costs 4 memory round trips, not 32.
-            uint64_t* zb = p.Z + party * p.party_stride_z + off;
-            const uint64_t* cb = p.C ? p.C + party * p.party_stride_c + off : nullptr;
+            uint64_t* zb = p.Z + party * p.party_stride_z + bi * p.batch_stride_z + off;
+            const uint64_t* cb = p.C ? p.C + party * p.party_stride_c + bi * p.batch_stride_c + off : nullptr;
 #pragma unroll
             for (int jb = 0; jb < 64; jb += 16) {
                 uint64_t v[16];
@@ -415,8 +423,9 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     const uint32_t rank = cluster_rank();
     const bool leader = (rank == 0);
     WorkMap wm;
-    wm.tm = TileMap{parties, (int)(pad_rows<Layout::Left>(p.M) / kTileM), (int)(pad_rows<Layout::Right>(p.N) / kTileN),
-                    p.group_m > 0 ? p.group_m : kGroupM};
+    wm.tm = TileMap{parties * (p.batch > 1 ? p.batch : 1), (int)(pad_rows<Layout::Left>(p.M) / kTileM),
+                    (int)(pad_rows<Layout::Right>(p.N) / kTileN), p.group_m > 0 ? p.group_m : kGroupM};
+    wm.nparties = parties;
     wm.tkb = p.seg[0].kb + (p.nseg > 1 ? p.seg[1].kb : 0);
     wm.kc = p.kc;
     wm.splits = p.splits < 1 ? 1 : p.splits;
@@ -497,7 +506,8 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     if (prm.kc < 1 || prm.kc > ring_gemm_max_kc()) return cudaErrorInvalidValue;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t tiles = (int64_t)parties * (pad_rows<Layout::Left>(prm.M) / gemm::kTileM) *
+    const int inst = parties * (prm.batch > 1 ? prm.batch : 1);       // GEMM instances (batch x parties)
+    const int64_t tiles = (int64_t)inst * (pad_rows<Layout::Left>(prm.M) / gemm::kTileM) *
                           (pad_rows<Layout::Right>(prm.N) / gemm::kTileN);
     int64_t max_clusters = sms / 2;
     if (prm.max_clusters > 0 && prm.max_clusters < max_clusters) max_clusters = prm.max_clusters;
@@ -507,7 +517,7 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     if (q.group_m <= 0) q.group_m = env_group;
     static const int env_fault = getenv("MPC_GEMM_FAULT_INJECT") ? atoi(getenv("MPC_GEMM_FAULT_INJECT")) : 0;
     q.fault_inject = env_fault;
-    q.splits = prm.partials ? ring_gemm_splits(parties, prm.M, prm.N, tkb, max_clusters, prm.small != 0) : 1;
+    q.splits = prm.partials ? ring_gemm_splits(inst, prm.M, prm.N, tkb, max_clusters, prm.small != 0) : 1;
     if (prm.small) {
         if (q.splits > 1) q.partial_stride = ring_gemm_out_elems(q, parties);
         cudaError_t e = ring_gemm_small_launch(q, parties, 2 * max_clusters, stream);
@@ -602,13 +612,16 @@ __global__ void finalize_kernel(uint64_t* __restrict__ z, const uint64_t* __rest
 
 // z = trunc(z + c) over all parties after a split-K GEMM (party buffers contiguous).
 int64_t ring_gemm_out_elems(const RingGemmParams& q, int parties) {
-    return parties > 1 ? (int64_t)parties * q.party_stride_z : q.M * q.N;
+    const int64_t per_party = (q.batch > 1 ? q.batch : 1) * q.M * q.N;
+    return parties > 1 ? (int64_t)parties * q.party_stride_z : per_party;
 }
 
 cudaError_t ring_gemm_finalize(const RingGemmParams& q, int parties, cudaStream_t stream) {
     const int64_t n = ring_gemm_out_elems(q, parties);
-    if (parties > 1 && (q.party_stride_z != q.M * q.N || (q.C && q.party_stride_c != q.party_stride_z)))
-        return cudaErrorInvalidValue;
+    const int64_t per_party = (q.batch > 1 ? q.batch : 1) * q.M * q.N;
+    if ((parties > 1 && (q.party_stride_z != per_party || (q.C && q.party_stride_c != q.party_stride_z))) ||
+        (q.batch > 1 && (q.batch_stride_z != q.M * q.N || (q.C && q.batch_stride_c != q.batch_stride_z))))
+        return cudaErrorInvalidValue;                   // the finalize pass needs z (and c) contiguous
     int64_t blocks = (n + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;

@@ -11,6 +11,8 @@ struct RingGemmSegment {
     int kb;                  // number of 32-K blocks of this segment (both operands)
     int64_t party_stride_A;  // bytes between parties' A planes (0 = shared, e.g. eps)
     int64_t party_stride_B;
+    int64_t batch_stride_A;  // bytes between batch elements' planes (batched GEMM; 0 when batch = 1)
+    int64_t batch_stride_B;
 };
 
 struct RingGemmParams {
@@ -39,6 +41,9 @@ struct RingGemmParams {
                                         // convolution whose im2col rows are (b, pixel s).  C likewise.
     int small;                          // 1: stacked-plane kernel (M <= 32, planes in Layout::Small)
     int group_m;                        // row tiles per scheduling group of the 2-CTA kernel (0: default 4)
+    int batch;                          // independent GEMMs of the same shape (0/1 = one); instance
+                                        // (b, p) reads planes at b * batch_stride_A/B + p * party_stride_A/B
+    int64_t batch_stride_c, batch_stride_z;  // elements between batch elements of C / Z (and the partials)
     int fault_inject;                   // test hook (MPC_GEMM_FAULT_INJECT=1): drop one stage's copies, so the
                                         // pipeline stalls and the mbarrier watchdog must trap
 };

@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_small_kernel(const __gr
     uint64_t* tempty = tfull + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    Items it{parties, (int)((p.M + kRows - 1) / kRows), (int)((p.N + kTileN - 1) / kTileN),
+    Items it{parties * (p.batch > 1 ? p.batch : 1), (int)((p.M + kRows - 1) / kRows), (int)((p.N + kTileN - 1) / kTileN),
              p.seg[0].kb + (p.nseg > 1 ? p.seg[1].kb : 0), p.splits < 1 ? 1 : p.splits};
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -135,13 +135,17 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_small_kernel(const __gr
         for (int w = blockIdx.x; w < it.count(); w += gridDim.x) {
             int party, m, n, klo, khi;
             it.decode(w, party, m, n, klo, khi);
+            const int bi = party / parties;                        // instance -> (batch element, party)
+            party -= bi * parties;
             for (int kt = klo; kt < khi; ++kt) {
                 const int sg = (kt < p.seg[0].kb) ? 0 : 1;
                 const RingGemmSegment& S = p.seg[sg];
                 const int64_t kb = kt - (sg ? p.seg[0].kb : 0);
                 // Layout::Small: (32-row block, 32-K block) of all 8 planes = 8 KiB contiguous
-                const uint8_t* srcA = S.A + party * S.party_stride_A + ((int64_t)m * S.kb + kb) * (8 * kChunk);
-                const uint8_t* srcB = S.B + party * S.party_stride_B + ((int64_t)n * S.kb + kb) * (8 * kChunk);
+                const uint8_t* srcA = S.A + party * S.party_stride_A + bi * S.batch_stride_A +
+                                      ((int64_t)m * S.kb + kb) * (8 * kChunk);
+                const uint8_t* srcB = S.B + party * S.party_stride_B + bi * S.batch_stride_B +
+                                      ((int64_t)n * S.kb + kb) * (8 * kChunk);
                 mbar_wait(&empty[s], ph ^ 1);
                 uint8_t* st = smem + s * kStageBytes;
                 if (elect_one()) {
@@ -159,6 +163,8 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_small_kernel(const __gr
         for (int w = blockIdx.x; w < it.count(); w += gridDim.x) {
             int party, m, n, klo, khi;
             it.decode(w, party, m, n, klo, khi);
+            const int bi = party / parties;                        // instance -> (batch element, party)
+            party -= bi * parties;
             for (int k0 = klo; k0 < khi; k0 += kMaxUnit, ++u) {
                 const int k1 = min(khi, k0 + kMaxUnit);
                 mbar_wait(tempty, (u & 1) ^ 1);                     // the epilogue drained the last unit
@@ -192,6 +198,8 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_small_kernel(const __gr
         for (int w = blockIdx.x; w < it.count(); w += gridDim.x) {
             int party, m, n, klo, khi;
             it.decode(w, party, m, n, klo, khi);
+            const int bi = party / parties;                        // instance -> (batch element, party)
+            party -= bi * parties;
             uint64_t run[16];
 #pragma unroll
             for (int c = 0; c < 16; ++c) run[c] = 0;
@@ -236,11 +244,12 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_small_kernel(const __gr
                 const int64_t off = tr ? (gr / hw) * p.N * hw + gr % hw + gc * hw : gr * p.N + gc;
                 if (split) {
                     const int sidx = w % it.splits;
-                    p.partials[(int64_t)sidx * p.partial_stride + party * p.M * p.N + off] = v;
+                    p.partials[(int64_t)sidx * p.partial_stride + party * p.party_stride_z + bi * p.batch_stride_z +
+                               off] = v;
                 } else {
-                    if (p.C) v += p.C[party * p.party_stride_c + off];
+                    if (p.C) v += p.C[party * p.party_stride_c + bi * p.batch_stride_c + off];
                     if (p.trunc_bits) v = div_pow2_round(v, p.trunc_bits);
-                    p.Z[party * p.party_stride_z + off] = v;
+                    p.Z[party * p.party_stride_z + bi * p.batch_stride_z + off] = v;
                 }
             }
             epi_sync();                                              // red is reused by the next item
@@ -305,7 +314,7 @@ cudaError_t ring_gemm_small_launch(const RingGemmParams& q, int parties, int64_t
         if (e != cudaSuccess) return e;
         attr_dev = dev;
     }
-    const int64_t items = small_tiles(parties, q.M, q.N) * (q.splits < 1 ? 1 : q.splits);
+    const int64_t items = small_tiles(parties * (q.batch > 1 ? q.batch : 1), q.M, q.N) * (q.splits < 1 ? 1 : q.splits);
     if (items >= (int64_t)1 << 31) return cudaErrorInvalidValue;
     int64_t ctas = items < max_ctas ? items : max_ctas;
     if (ctas < 1) ctas = 1;

@@ -228,6 +228,20 @@ class Context:
                    ctypes.c_uint64(wrap_id), _ptr(ws), ctypes.c_size_t(ws.numel()))
         return z
 
+    def beaver_matmul_batched(self, x, y, a, b, c, truncate: bool = True, wrap_id: int = 0,
+                              out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """z[i] = x[i] @ y[i] for a batch of one shape: x [(P,) batch, M, K], y [(P,) batch, K, N]
+        (mpc_beaver_matmul_batched: one reveal round, one split and one GEMM launch)."""
+        B, M, K = x.shape[-3], x.shape[-2], x.shape[-1]
+        N = y.shape[-1]
+        z = out if out is not None else _u64(self._lead() + (B, M, N), self.device)
+        nb = int(self._lib.mpc_workspace_bytes_batched(self._h, B, M, K, N))
+        ws = self._workspace(nb)
+        self._call(self._lib.mpc_beaver_matmul_batched, ctypes.c_int64(B), _ptr(x), _ptr(y), _ptr(a), _ptr(b),
+                   _ptr(c), _ptr(z), ctypes.c_int64(M), ctypes.c_int64(K), ctypes.c_int64(N), int(bool(truncate)),
+                   ctypes.c_uint64(wrap_id), _ptr(ws), ctypes.c_size_t(ws.numel()))
+        return z
+
     def beaver_prepare(self, y, b, M: int, out: Optional["Prepared"] = None) -> "Prepared":
         """The input-independent y side of a Beaver matmul with M x-rows (delta
         reveal + splits, mpc_beaver_prepare); returns the prepared operand, whose

@@ -68,9 +68,7 @@ def chain(name, reps=10, offline_variant=False):
     ctx = mpc.Context(2, mpc.ALL_PARTIES, device=0, master_seed=synth.MASTER_SEED)
     layers = synth.MODELS[name]
     ms = bench_layers.run_chain(ctx, layers, reps)
-    ops = sum(2.0 * M * K * N * cnt for _, M, K, N, cnt in layers)
-    tg = sum(bench_layers.t_gemm_ms(M, K, N) * cnt for _, M, K, N, cnt in layers)
-    n = sum(cnt for *_, cnt in layers)
+    ops, tg, n = bench_layers.layer_totals(layers)
     out = {"private_matmuls": n, "chain_ms": ms, "ring_TOPS": ops / (ms * 1e-3) / 1e12,
            "roofline_ms": tg, "roofline_frac": tg / ms}
     if offline_variant:
@@ -133,8 +131,9 @@ def one_party_schedule(n=4096, steps=10):
 
 def run(skip_c5=False):
     out = {"C1": c1_latency(), "one_party_schedule": one_party_schedule()}
-    for key, name in (("C3_resnet50", "resnet50"), ("C4_vit_b16", "vit"), ("NEXT4_text", "text")):
-        out[key] = chain(name, offline_variant=name != "text")
+    for key, name in (("C3_resnet50", "resnet50"), ("C4_vit_b16", "vit"), ("C4_vit_b16_with_attention", "vit_attn"),
+                      ("NEXT4_text", "text")):
+        out[key] = chain(name, offline_variant=name in ("resnet50", "vit"))
         torch.cuda.empty_cache()
     if not skip_c5:
         out["C5_p4_8192"] = c5(4)

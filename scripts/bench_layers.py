@@ -75,7 +75,19 @@ def run_chain(ctx, layers, reps, prepared=False, offline=False):
     phase with the triples); the timed graph holds the x sides only."""
     dev = torch.device("cuda", 0)
     bufs = []
-    for i, (_, M, K, N, count) in enumerate(layers):
+    batched = []                      # (x, y, a, b, c, z, count) of batched entries (attention heads)
+    for i, layer in enumerate(layers):
+        _, M, K, N, count = layer[:5]
+        if len(layer) > 5:            # a batch of independent matmuls (6th field), one batched call
+            B = layer[5]
+            X = synth.uniform_fixed((B, M, K), 100 + i)
+            Y = synth.uniform_fixed((B, K, N), 200 + i)
+            x = ctx.share(torch.from_numpy(X.view(np.int64)).to(dev).view(torch.uint64), 0, 1 + 2 * i)
+            y = ctx.share(torch.from_numpy(Y.view(np.int64)).to(dev).view(torch.uint64), 1, 2 + 2 * i)
+            tr = [ctx.ttp_triples(1000 * (i + 1) + h, M, K, N) for h in range(B)]
+            a, b, c = (torch.stack([t[j] for t in tr], dim=1).contiguous() for j in range(3))
+            batched.append((x, y, a, b, c, torch.empty_like(c), count))
+            continue
         X = synth.uniform_fixed((M, K), 100 + i)
         Y = synth.uniform_fixed((K, N), 200 + i)
         x = ctx.share(torch.from_numpy(X.view(np.int64)).to(dev).view(torch.uint64), 0, 1 + 2 * i)
@@ -83,6 +95,11 @@ def run_chain(ctx, layers, reps, prepared=False, offline=False):
         a, b, c = ctx.ttp_triples(1 + i, M, K, N)
         preps = [ctx.beaver_prepare(y, b, M) for _ in range(count)] if (prepared or offline) else None
         bufs.append((x, y, a, b, c, torch.empty_like(c), count, preps))
+
+    def run_batched():
+        for x, y, a, b, c, z, count in batched:
+            for _ in range(count):
+                ctx.beaver_matmul_batched(x, y, a, b, c, truncate=True, out=z)
 
     side = torch.cuda.Stream(priority=0) if prepared else None
 
@@ -93,6 +110,7 @@ def run_chain(ctx, layers, reps, prepared=False, offline=False):
         torch.cuda.synchronize()
 
     def chain():
+        run_batched()
         if offline:
             for x, y, a, b, c, z, count, preps in bufs:
                 for r in range(count):
@@ -159,6 +177,19 @@ def int8_peak_tops():
 
 def t_gemm_ms(M, K, N, parties=2):
     return 144.0 * M * N * K * parties / (int8_peak_tops() * 1e12) * 1e3
+
+
+def layer_totals(layers):
+    """(ring ops 2*M*N*K, limb-GEMM roofline ms, private matmuls) of a layer list
+    whose entries are (name, M, K, N, count[, batch])."""
+    ops = tg = n = 0.0
+    for layer in layers:
+        _, M, K, N, cnt = layer[:5]
+        B = layer[5] if len(layer) > 5 else 1
+        ops += 2.0 * M * K * N * cnt * B
+        tg += t_gemm_ms(M, K, N) * cnt * B
+        n += cnt * B
+    return ops, tg, int(n)
 
 
 def run_conv_chain(ctx, layers, reps):
@@ -235,9 +266,7 @@ def main():
             continue
         if args.chain:
             ms = run_chain(ctx, layers, args.reps, prepared=args.prepared)
-            ops = sum(2.0 * M * K * N * cnt for _, M, K, N, cnt in layers)
-            n = sum(cnt for *_, cnt in layers)
-            tg = sum(t_gemm_ms(M, K, N) * cnt for _, M, K, N, cnt in layers)
+            ops, tg, n = layer_totals(layers)
             key = name + ("_prepared" if args.prepared else "")
             out[key] = {"chain_ms": ms, "private_matmuls": n, "ring_TOPS": ops / (ms * 1e-3) / 1e12,
                         "roofline_ms": tg, "roofline_frac": tg / ms,

@@ -63,6 +63,11 @@ VIT_B16 = [
     ("head", 1, 768, 1000, 1),
 ]
 
+# ViT-B/16 with the attention matmuls (SURVEY §8(d) C4 "optional attention"): per
+# block the 12 heads' Q @ K^T (197 x 64 x 197) and A @ V (197 x 197 x 64) as one
+# batched private matmul each (6th field = batch).  Softmax is out of scope.
+VIT_B16_ATTN = VIT_B16[:2] + [("qk^T", 197, 64, 197, 12, 12), ("attn@v", 197, 197, 64, 12, 12)] + VIT_B16[2:]
+
 # ResNet-18 b1 im2col GEMMs (the model the paper benchmarks; SURVEY §8(d)
 # C3 extra row): 21 GEMMs, sum MNK = 1.81 G.
 RESNET18_B1 = [
@@ -119,7 +124,7 @@ CONV_MODELS = {"resnet50": RESNET50_CONV_B1, "resnet18": RESNET18_CONV_B1}
 TEXT_EMBED = [("embed", 32, 519820, 32, 1)]
 
 MODELS = {"resnet50": RESNET50_B1, "vit": VIT_B16, "resnet18": RESNET18_B1, "wav2letter": WAV2LETTER_B1,
-          "text": TEXT_EMBED}
+          "text": TEXT_EMBED, "vit_attn": VIT_B16_ATTN}
 
 CONFIGS = {
     "C1": dict(M=64, K=64, N=64, P=2, seed=1001),

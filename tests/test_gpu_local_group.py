@@ -265,3 +265,22 @@ def test_beaver_eight_parties_alg1(mpc):
                                                                  dev(cc[r]), truncate=True, wrap_id=9)))
     assert np.array_equal(np.stack(res), oracle.truncate(oracle.beaver_matmul(xs, ys, a, b, cc), 16, MASTER,
                                                          wrap_id=9))
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_beaver_matmul_batched_one_party(mpc, P):
+    B, M, K, N = 6, 70, 64, 90
+    X = np.stack([synth.uniform_fixed((M, K), 10 + i) for i in range(B)])
+    Y = np.stack([synth.uniform_fixed((K, N), 20 + i) for i in range(B)])
+    xs, ys = oracle.share(P, MASTER, X, 0, 31), oracle.share(P, MASTER, Y, 1, 32)
+    tr = [oracle.ttp_triple(P, MASTER, 40 + i, M, K, N) for i in range(B)]
+    a, b, cc = (np.ascontiguousarray(np.stack([t[j] for t in tr], axis=1)) for j in range(3))
+
+    def body(c, r):
+        return host(c.beaver_matmul_batched(dev(xs[r]), dev(ys[r]), dev(a[r]), dev(b[r]), dev(cc[r]),
+                                            truncate=True, wrap_id=3)), c.stats()[0]
+
+    res = run_parties(mpc, P, body)
+    ez = np.stack([oracle.beaver_matmul(xs[:, i], ys[:, i], a[:, i], b[:, i], cc[:, i]) for i in range(B)], axis=1)
+    assert np.array_equal(np.stack([r[0] for r in res]), oracle.truncate(ez, 16, MASTER, wrap_id=3))
+    assert all(r[1] == 1 + (P > 2) for r in res)

@@ -409,3 +409,30 @@ print("OK")
     env = dict(os.environ, MPC_CHECK_COLLECTIVES="1")
     out = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and out.stdout.strip().endswith("OK"), out.stderr[-2000:]
+
+
+# ------------------------------------------------------------------ batched (attention heads)
+def _batched_case(P, B, M, K, N, seed):
+    X = np.stack([synth.uniform_fixed((M, K), seed + 2 * i) for i in range(B)])
+    Y = np.stack([synth.uniform_fixed((K, N), seed + 2 * i + 1) for i in range(B)])
+    xs = oracle.share(P, MASTER, X, 0, 500 + seed)                     # (P, B, M, K)
+    ys = oracle.share(P, MASTER, Y, 1 % P, 600 + seed)
+    tr = [oracle.ttp_triple(P, MASTER, 700 + seed + i, M, K, N) for i in range(B)]
+    a, b, c = (np.ascontiguousarray(np.stack([t[j] for t in tr], axis=1)) for j in range(3))
+    return X, Y, xs, ys, a, b, c
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4])
+@pytest.mark.parametrize("B,M,K,N", [(12, 197, 64, 197), (12, 197, 197, 64), (3, 33, 100, 50), (5, 5, 7, 300),
+                                     (2, 300, 130, 260)])
+def test_beaver_matmul_batched_parity(mpc, P, B, M, K, N):
+    """A batch of independent private matmuls in one reveal, one split and one GEMM
+    launch (mpc_beaver_matmul_batched) equals the oracle's Beaver matmul of each."""
+    c = ctx(mpc, P)
+    X, Y, xs, ys, a, b, cc = _batched_case(P, B, M, K, N, seed=B + M)
+    r0, _ = c.stats()
+    z = host(c.beaver_matmul_batched(dev(xs), dev(ys), dev(a), dev(b), dev(cc), truncate=True, wrap_id=17))
+    assert c.stats()[0] - r0 == 1 + (P > 2)
+    ez = np.stack([oracle.beaver_matmul(xs[:, i], ys[:, i], a[:, i], b[:, i], cc[:, i]) for i in range(B)], axis=1)
+    assert np.array_equal(oracle.reveal(ez), np.stack([X[i] @ Y[i] for i in range(B)]))   # Beaver identity
+    assert np.array_equal(z, oracle.truncate(ez, 16, MASTER, wrap_id=17))
