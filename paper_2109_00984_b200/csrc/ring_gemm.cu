@@ -360,8 +360,9 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Wor
             uint64_t* pb = p.partials + (int64_t)s * p.partial_stride + party * p.party_stride_z +
                            bi * p.batch_stride_z + off;
             if (full) {
+                const uint64_t ppol = p.partials_evict_first ? pol : evict_last_policy();
 #pragma unroll
-                for (int j = 0; j < 64; j += 4) st_stream4(pb + j, &run[j], pol);
+                for (int j = 0; j < 64; j += 4) st_stream4(pb + j, &run[j], ppol);
             } else {
 #pragma unroll
                 for (int j = 0; j < 64; ++j)
@@ -517,6 +518,8 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     if (q.group_m <= 0) q.group_m = env_group;
     static const int env_fault = getenv("MPC_GEMM_FAULT_INJECT") ? atoi(getenv("MPC_GEMM_FAULT_INJECT")) : 0;
     q.fault_inject = env_fault;
+    static const int env_pef = getenv("MPC_PARTIALS_EVICT_FIRST") ? atoi(getenv("MPC_PARTIALS_EVICT_FIRST")) : 0;
+    q.partials_evict_first = env_pef;
     q.splits = prm.partials ? ring_gemm_splits(inst, prm.M, prm.N, tkb, max_clusters, prm.small != 0) : 1;
     if (prm.small) {
         if (q.splits > 1) q.partial_stride = ring_gemm_out_elems(q, parties);
@@ -573,10 +576,12 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
 int ring_gemm_choose_splits(int64_t tiles, int tkb, int64_t clusters) {
     static const int env = getenv("MPC_GEMM_SPLITS") ? atoi(getenv("MPC_GEMM_SPLITS")) : 0;
     if (env > 0) return tkb >= env ? env : (tkb > 0 ? tkb : 1);
-    if (tiles <= 0 || tkb < 16 || tiles >= clusters) return 1;
+    static const int env_minkb = getenv("MPC_GEMM_MINKB") ? atoi(getenv("MPC_GEMM_MINKB")) : 0;
+    const int minkb = env_minkb > 0 ? env_minkb : 8;
+    if (tiles <= 0 || tkb < 2 * minkb || tiles >= clusters) return 1;
     int best = 1;
     double best_cost = 1e30;
-    for (int s = 1; s <= tkb / 8 && s <= 64; ++s) {
+    for (int s = 1; s <= tkb / minkb && s <= 64; ++s) {
         const int64_t waves = (tiles * s + clusters - 1) / clusters;
         const double cost = (double)waves * ((tkb + s - 1) / s) * 1.0 + (s > 1 ? 2.0 : 0.0);
         if (cost < best_cost - 1e-9) { best_cost = cost; best = s; }

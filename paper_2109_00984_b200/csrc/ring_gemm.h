@@ -44,6 +44,8 @@ struct RingGemmParams {
     int batch;                          // independent GEMMs of the same shape (0/1 = one); instance
                                         // (b, p) reads planes at b * batch_stride_A/B + p * party_stride_A/B
     int64_t batch_stride_c, batch_stride_z;  // elements between batch elements of C / Z (and the partials)
+    int partials_evict_first;           // experiment (MPC_PARTIALS_EVICT_FIRST=1): split-K partials stored
+                                        // evict-first like z; default evict-last, so finalize reads them from L2
     int fault_inject;                   // test hook (MPC_GEMM_FAULT_INJECT=1): drop one stage's copies, so the
                                         // pipeline stalls and the mbarrier watchdog must trap
 };

@@ -9,7 +9,9 @@ headline (configs[1]), all parties on one GPU:
   NEXT-4:         the 32 x 519,820 x 32 text-embedding matmul (stacked-plane GEMM)
 
 Each line gives ms, ring-TOPS (2*M*N*K per private matmul) and the fraction of
-the limb-GEMM roofline (144*M*N*K int8 ops per party at bench.py's int8 peak).
+the limb-GEMM roofline (144*M*N*K int8 ops per party at bench.py's int8 peak);
+chains also give the fraction of the per-layer max(tensor time, HBM floor)
+(bench_layers.t_hbm_ms: the x, a, y, b, c reads and z write of every party).
 
   python scripts/bench_configs.py [--skip-c5]
 """
@@ -69,13 +71,15 @@ def chain(name, reps=10, offline_variant=False):
     layers = synth.MODELS[name]
     ms = bench_layers.run_chain(ctx, layers, reps)
     ops, tg, n = bench_layers.layer_totals(layers)
+    rl = bench_layers.layer_rooflines(layers)
     out = {"private_matmuls": n, "chain_ms": ms, "ring_TOPS": ops / (ms * 1e-3) / 1e12,
-           "roofline_ms": tg, "roofline_frac": tg / ms}
+           "roofline_ms": tg, "roofline_frac": tg / ms,
+           "roofline_tensor_or_hbm_ms": rl, "roofline_tensor_or_hbm_frac": rl / ms}
     if offline_variant:
         # weight sides (delta reveal + splits) prepared with the triples, before the input arrives
         mo = bench_layers.run_chain(ctx, layers, reps, offline=True)
         out["weights_prepared_offline"] = {"chain_ms": mo, "ring_TOPS": ops / (mo * 1e-3) / 1e12,
-                                           "roofline_frac": tg / mo,
+                                           "roofline_frac": tg / mo, "roofline_tensor_or_hbm_frac": rl / mo,
                                            "note": "delta = w - b revealed in the offline phase (mpc_beaver_prepare); "
                                                    "the timed chain holds the eps reveal, x-side split and GEMM"}
     return out

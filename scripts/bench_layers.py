@@ -192,6 +192,34 @@ def layer_totals(layers):
     return ops, tg, int(n)
 
 
+def hbm_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return 6650.0
+
+
+def t_hbm_ms(M, K, N, parties=2):
+    """HBM floor of one private matmul with all parties on one GPU: the bytes the
+    protocol cannot avoid — read x_p, a_p (M x K), y_p, b_p (K x N), c_p (M x N)
+    and write z_p, 8 B each, for every party (limb planes excluded: they are this
+    design's intermediate, not the method's)."""
+    return parties * 8.0 * (2 * M * K + 2 * K * N + 2 * M * N) / (hbm_gbs() * 1e9) * 1e3
+
+
+def layer_rooflines(layers):
+    """Per-layer max(limb-GEMM tensor time, HBM floor), summed over the chain:
+    the roofline of a chain whose small layers are HBM-bound rather than
+    tensor-bound (reported beside the tensor-only figure)."""
+    tot = 0.0
+    for layer in layers:
+        _, M, K, N, cnt = layer[:5]
+        B = layer[5] if len(layer) > 5 else 1
+        tot += max(t_gemm_ms(M, K, N), t_hbm_ms(M, K, N)) * cnt * B
+    return tot
+
+
 def run_conv_chain(ctx, layers, reps):
     """All convolutions of one model as TRUE private convolutions (conv triples,
     eps/delta revealed at the input/weight shapes) in one CUDA graph."""
@@ -268,12 +296,15 @@ def main():
             ms = run_chain(ctx, layers, args.reps, prepared=args.prepared)
             ops, tg, n = layer_totals(layers)
             key = name + ("_prepared" if args.prepared else "")
+            rl = layer_rooflines(layers)
             out[key] = {"chain_ms": ms, "private_matmuls": n, "ring_TOPS": ops / (ms * 1e-3) / 1e12,
                         "roofline_ms": tg, "roofline_frac": tg / ms,
+                        "roofline_tensor_or_hbm_ms": rl, "roofline_tensor_or_hbm_frac": rl / ms,
                         "graph": "one CUDA graph per model" + (
                             "; weight sides (delta reveal + splits) on a second stream" if args.prepared else "")}
             print(f"{key}: chain of {n} private matmuls {ms:.3f} ms ({out[key]['ring_TOPS']:.2f} ring-TOPS, "
-                  f"limb-GEMM roofline {tg:.3f} ms = {tg / ms:.3f})", flush=True)
+                  f"limb-GEMM roofline {tg:.3f} ms = {tg / ms:.3f}; per-layer max(tensor, HBM) {rl:.3f} ms "
+                  f"= {rl / ms:.3f})", flush=True)
             continue
         rows, total_ms, total_ops = [], 0.0, 0.0
         for lname, M, K, N, count in layers:
