@@ -62,7 +62,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-next-rows", action="store_true", help="skip the SURVEY §8(f) NEXT-row measurements")
-    ap.add_argument("--sample-rows", type=int, default=16)
+    ap.add_argument("--sample-rows", type=int, default=0,
+                    help="--impl reference: 4x the output rows the oracle computes per step "
+                         "(0: sized for ~90 s of oracle work over the whole run)")
     return ap.parse_args()
 
 
@@ -227,7 +229,18 @@ def run_reference(args):
     if rank != 0:
         return
     M, K, N = args.M, args.K, args.N
-    rows_n = max(1, args.sample_rows // 4)
+    if args.sample_rows > 0:
+        rows_n = max(1, args.sample_rows // 4)
+    else:
+        # size the row sample so the whole run takes ~90 s of oracle work: the
+        # time is affine in the rows (the full K x N delta reveal is a fixed
+        # cost), so two short calibration runs give both terms
+        budget = min(15.0, max(1.0, 90.0 / max(1, args.warmup + args.steps)))
+        t4 = OracleSample(M, K, N, 4).run()["seconds"]
+        t16 = OracleSample(M, K, N, 16).run()["seconds"]
+        per_row = max((t16 - t4) / 12.0, 1e-6)
+        fixed = max(t4 - 4 * per_row, 0.0)
+        rows_n = int(max(4, min(M, (budget - fixed) / per_row)))
     sample = OracleSample(M, K, N, rows_n)
     times = []
     for i in range(args.warmup + args.steps):
