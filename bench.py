@@ -203,24 +203,40 @@ class OracleSample:
         z = self.oracle.beaver_matmul(self.xs, self.ys, self.a, self.b, self.c)
         self.oracle.truncate(z, 16)
         t = time.perf_counter() - t0
-        cores = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
+        cores = self.oracle.get_threads()
         ops = 2.0 * self.rows_n * self.K * self.N
         return {"value": ops / t / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle", "seconds": t,
                 "sample": f"{self.rows_n} of {self.M} output rows of both parties' shares (full {self.K}x{self.N} "
                           f"delta reveal), online Beaver + truncation, {t:.2f} s"}
 
 
-def oracle_baseline(M, K, N, target_s=12.0):
+def oracle_baseline(M, K, N, target_s=12.0, one_thread_s=5.0):
     """cpu_baseline: grow the row sample (time is affine in the rows: the full
-    delta reveal is a fixed cost) until the timed oracle work is ~target_s."""
-    rows_n = 8
-    r = OracleSample(M, K, N, rows_n).run()
-    for _ in range(3):
-        if r["seconds"] >= target_s / 2 or rows_n >= M:
-            break
-        rows_n = int(min(M, rows_n * min(16.0, max(2.0, target_s / max(r["seconds"], 1e-3)))))
+    delta reveal is a fixed cost) until the timed oracle work is ~target_s, on
+    every host core; then the same with ONE OpenMP thread, the paper's CPU
+    setting, on a ~one_thread_s sample (timed twice)."""
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+
+    def grow(target):
+        rows_n = 8
         r = OracleSample(M, K, N, rows_n).run()
-    r.pop("seconds")
+        for _ in range(3):
+            if r["seconds"] >= target / 2 or rows_n >= M:
+                break
+            rows_n = int(min(M, rows_n * min(16.0, max(2.0, target / max(r["seconds"], 1e-3)))))
+            r = OracleSample(M, K, N, rows_n).run()
+        r.pop("seconds")
+        return r
+
+    oracle.set_threads(cores)
+    r = grow(target_s)
+    oracle.set_threads(1)
+    try:
+        r1 = grow(one_thread_s)
+    finally:
+        oracle.set_threads(cores)
+    r["one_thread"] = {"value": r1["value"], "cores": r1["cores"], "sample": r1["sample"]}
     return r
 
 

@@ -60,8 +60,19 @@ def lib():
         L.oracle_encode.restype = ctypes.c_int
         L.oracle_truncate_local.restype = ctypes.c_int
         L.oracle_truncate_alg1.restype = ctypes.c_int
+        L.oracle_set_threads.argtypes = [ctypes.c_int]
+        L.oracle_get_threads.restype = ctypes.c_int
         _lib = L
     return _lib
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of the oracle's loops (timing only; results are independent of it)."""
+    lib().oracle_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(lib().oracle_get_threads())
 
 
 def _p(a: np.ndarray):

@@ -29,6 +29,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <math.h>
+#include <omp.h>
 
 typedef __int128 i128;
 
@@ -164,6 +165,12 @@ void oracle_reveal(int P, const uint64_t* shares, int64_t n, uint64_t* out)
         out[i] = s;
     }
 }
+
+/* Thread count of the OpenMP loops (timing only: results do not depend on it).
+ * bench.py times the oracle with one thread, the paper's CPU setting,
+ * and with every host core. */
+void oracle_set_threads(int n) { if (n > 0) omp_set_num_threads(n); }
+int oracle_get_threads(void) { return omp_get_max_threads(); }
 
 /* ------------------------------------------------------------------------
  * Ring GEMM: C = A @ B mod 2^64, A: M×K, B: K×N, row-major.  The textbook
