@@ -747,6 +747,7 @@ mpc_status mpc_beaver_matmul_batched(mpc_ctx c, int64_t batch, const uint64_t* x
     if (batch < 0 || M < 0 || K < 0 || N < 0) return fail(c, MPC_ERR_SHAPE, "beaver_matmul_batched: negative size");
     if (batch > 65536 || K > (int64_t)1 << 30 || M > (int64_t)1 << 31 || N > (int64_t)1 << 31)
         return fail(c, MPC_ERR_SHAPE, "beaver_matmul_batched: too large");
+    const int nb = (int)batch;                        // <= 65536 (checked above)
     const BeaverWs w = carve_beaver(c, ws, M, K, N, -1, true, true, batch < 1 ? 1 : batch);
     if (ws_bytes < w.total) return fail(c, MPC_ERR_SHAPE, "beaver_matmul_batched: workspace %zu < %zu", ws_bytes, w.total);
     const int Pl = c->all ? c->P : 1;
@@ -759,9 +760,9 @@ mpc_status mpc_beaver_matmul_batched(mpc_ctx c, int64_t batch, const uint64_t* x
     const int code = lay(w);
     if (c->all) {
         LeftSplitArgs L{M, K, batch * sMK, x, a, c->P, w.eps_pl, a, c->P, w.a_pl, w.a_stride, code, 0,
-                        batch, sMK, w.xs, w.xs};
+                        nb, sMK, w.xs, w.xs};
         RightSplitArgs R{K, N, batch * sKN, y, b, c->P, w.delta_pl, b, c->P, 1, w.b_pl, w.b_stride, code,
-                         batch, sKN, w.ys, w.ys};
+                         nb, sKN, w.ys, w.ys};
         CHECK(run(c, kClsSplit, "mask+reveal+split (batched)", [&] { return launch_split_both(L, R, c->stream); }));
     } else {
         // one party: [e (batch x M x K) | d (batch x K x N)] -> one reveal -> splits
@@ -769,9 +770,9 @@ mpc_status mpc_beaver_matmul_batched(mpc_ctx c, int64_t batch, const uint64_t* x
         uint64_t* d = w.ed + batch * sMK;
         CHECK(run(c, kClsSplit, "mask", [&] { return launch_mask(x, a, batch * sMK, y, b, batch * sKN, e, c->stream); }));
         if (c->P > 1) CHECK(comm_allreduce(c, e, e, (size_t)(batch * (sMK + sKN)), RedOp::SumU64, "eps/delta reveal"));
-        LeftSplitArgs L{M, K, 0, e, nullptr, 1, w.eps_pl, a, 1, w.a_pl, 0, code, 0, batch, sMK, w.xs, w.xs};
+        LeftSplitArgs L{M, K, 0, e, nullptr, 1, w.eps_pl, a, 1, w.a_pl, 0, code, 0, nb, sMK, w.xs, w.xs};
         RightSplitArgs R{K, N, 0, d, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0, code,
-                         batch, sKN, w.ys, w.ys};
+                         nb, sKN, w.ys, w.ys};
         CHECK(run(c, kClsSplit, "split eps/delta (batched)", [&] { return launch_split_both(L, R, c->stream); }));
     }
     CHECK(beaver_gemm(c, w, cc, z, M, K, N, truncate));
