@@ -210,6 +210,21 @@ class OracleSample:
                           f"delta reveal), online Beaver + truncation, {t:.2f} s"}
 
 
+def sample_rows_for(M, K, N, target_s):
+    """Rows of an oracle sample that takes about target_s: the time is affine in
+    the rows (the full K x N delta reveal is a fixed cost), so grow the sample
+    geometrically (x2..x16 per probe, each probe about the target at most) until
+    one run takes at least half the target — robust to a fixed cost that
+    dwarfs the per-row cost (a two-point fit there divides noise by noise)."""
+    rows_n = 8
+    for _ in range(5):
+        t = OracleSample(M, K, N, rows_n).run()["seconds"]
+        if t >= target_s / 2 or rows_n >= M:
+            break
+        rows_n = int(min(M, rows_n * min(16.0, max(2.0, target_s / max(t, 1e-3)))))
+    return rows_n
+
+
 def oracle_baseline(M, K, N, target_s=12.0, one_thread_s=5.0):
     """cpu_baseline: grow the row sample (time is affine in the rows: the full
     delta reveal is a fixed cost) until the timed oracle work is ~target_s, on
@@ -248,15 +263,9 @@ def run_reference(args):
     if args.sample_rows > 0:
         rows_n = max(1, args.sample_rows // 4)
     else:
-        # size the row sample so the whole run takes ~90 s of oracle work: the
-        # time is affine in the rows (the full K x N delta reveal is a fixed
-        # cost), so two short calibration runs give both terms
+        # size the row sample so the whole run takes ~90 s of oracle work
         budget = min(15.0, max(1.0, 90.0 / max(1, args.warmup + args.steps)))
-        t4 = OracleSample(M, K, N, 4).run()["seconds"]
-        t16 = OracleSample(M, K, N, 16).run()["seconds"]
-        per_row = max((t16 - t4) / 12.0, 1e-6)
-        fixed = max(t4 - 4 * per_row, 0.0)
-        rows_n = int(max(4, min(M, (budget - fixed) / per_row)))
+        rows_n = sample_rows_for(M, K, N, budget)
     sample = OracleSample(M, K, N, rows_n)
     times = []
     for i in range(args.warmup + args.steps):
