@@ -186,19 +186,26 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
             party -= bi * wm.nparties;
             const int64_t rbA = (int64_t)m * 2 + rank;       // 128-row left block
             const int64_t rbB = (int64_t)n * 2 + rank;       // 64-row right block
+            // this item's block-0 addresses of both segments (the copy loop is latency-critical:
+            // per block only a select and one add remain)
+            const int kb0 = p.seg[0].kb;
+            const RingGemmSegment& S0 = p.seg[0];
+            const RingGemmSegment& S1 = p.seg[p.nseg > 1 ? 1 : 0];
+            const uint8_t* a0 = S0.A + party * S0.party_stride_A + bi * S0.batch_stride_A + rbA * S0.kb * (8 * GL::kBlock);
+            const uint8_t* b0 = S0.B + party * S0.party_stride_B + bi * S0.batch_stride_B + rbB * S0.kb * (8 * GR::kBlock);
+            const uint8_t* a1 = S1.A + party * S1.party_stride_A + bi * S1.batch_stride_A + rbA * S1.kb * (8 * GL::kBlock) -
+                                (int64_t)kb0 * (8 * GL::kBlock);
+            const uint8_t* b1 = S1.B + party * S1.party_stride_B + bi * S1.batch_stride_B + rbB * S1.kb * (8 * GR::kBlock) -
+                                (int64_t)kb0 * (8 * GR::kBlock);
             for (int k0 = klo; k0 < khi; k0 += kc) {
                 const int k1 = min(khi, k0 + kc);
                 for (int g = 0; g < kPasses; ++g) {
                     const uint32_t bytesA = (uint32_t)pass_planes(g) * GL::kBlock;
                     const uint32_t bytesB = (uint32_t)pass_planes(g) * GR::kBlock;
                     for (int kt = k0; kt < k1; ++kt) {
-                        const int sg = (kt < p.seg[0].kb) ? 0 : 1;
-                        const RingGemmSegment& S = p.seg[sg];
-                        const int kb = kt - (sg ? p.seg[0].kb : 0);
-                        const uint8_t* srcA = S.A + party * S.party_stride_A + bi * S.batch_stride_A +
-                                              (rbA * S.kb + kb) * (8 * GL::kBlock);
-                        const uint8_t* srcB = S.B + party * S.party_stride_B + bi * S.batch_stride_B +
-                                              (rbB * S.kb + kb) * (8 * GR::kBlock);
+                        const bool second = kt >= kb0;
+                        const uint8_t* srcA = (second ? a1 : a0) + (int64_t)kt * (8 * GL::kBlock);
+                        const uint8_t* srcB = (second ? b1 : b0) + (int64_t)kt * (8 * GR::kBlock);
                         if (p.dbg) { const long long w0 = clock64(); mbar_wait(&B.empty[s], ph ^ 1); st_empty += clock64() - w0; }
                         else mbar_wait(&B.empty[s], ph ^ 1);
                         const bool drop = FAULT && kt == klo && w == (int)cluster_id();
