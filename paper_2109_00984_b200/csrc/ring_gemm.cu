@@ -41,6 +41,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include "common.cuh"
 #include "ring_gemm.h"
 #include "tcgen05.cuh"
@@ -167,7 +168,7 @@ __device__ __forceinline__ void issue_kblock(uint64_t da, uint64_t db, uint32_t 
 // FAULT: the fault-injection instantiation (MPC_GEMM_FAULT_INJECT, watchdog test).  A
 // compile-time switch: a runtime check in the producer's copy loop cost the
 // 8192^3 GEMMs 8-10% (measured: 108 vs 117-121 ms for 4-party 8192^3).
-template <bool FAULT>
+template <bool FAULT, bool TMA>
 __device__ __forceinline__ void control_roles(const RingGemmParams& p, const WorkMap& wm, int warp, int lane,
                                               uint32_t rank, uint32_t tmem_base, const Bars& B) {
     const bool leader = rank == 0;
@@ -208,6 +209,24 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
                         const uint8_t* srcB = (second ? b1 : b0) + (int64_t)kt * (8 * GR::kBlock);
                         if (p.dbg) { const long long w0 = clock64(); mbar_wait(&B.empty[s], ph ^ 1); st_empty += clock64() - w0; }
                         else mbar_wait(&B.empty[s], ph ^ 1);
+                        if (TMA) {
+                            // both CTAs: own half by 2-CTA tensor TMA, completing the LEADER's
+                            // barrier, which expects both halves' bytes (rows of 2 KiB; the maps
+                            // start at the segment's plane buffer)
+                            if (elect_one()) {
+                                if (leader) mbar_expect_tx(&B.full[s], 2 * (bytesA + bytesB));
+                                const uint32_t fb = mapa(smem_u32(&B.full[s]), 0);
+                                const uint8_t* st = B.stage_base + s * kStageBytes;
+                                const RingGemmSegment& Sx = second ? S1 : S0;
+                                tma_load_2d_2sm(smem_u32(st), &p.tma.a[second ? 1 : 0][g], 0,
+                                                (int)((srcA - Sx.A) >> 11), fb);
+                                tma_load_2d_2sm(smem_u32(st + kAStage), &p.tma.b[second ? 1 : 0][g], 0,
+                                                (int)((srcB - Sx.B) >> 11), fb);
+                            }
+                            __syncwarp();
+                            if (++s == kStages) { s = 0; ph ^= 1; }
+                            continue;
+                        }
                         const bool drop = FAULT && kt == klo && w == (int)cluster_id();
                         if (elect_one()) {
                             mbar_expect_tx(&B.full[s], bytesA + bytesB);
@@ -226,15 +245,18 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
         if (p.dbg && lane == 0) atomicAdd(&p.dbg[0], (unsigned long long)st_empty);
     } else if (warp == 1 && !leader) {
         // ------------------------------------------------ peer: relay "stage full" to the leader
-        int s = 0; uint32_t ph = 0;
-        const uint32_t leader_full0 = mapa(smem_u32(&B.full[0]), 0);
-        for (int w = cluster_id(); w < wm.items(); w += nclusters())
-            for (int i = 0; i < kPasses * wm.item_kb(w); ++i) {
-                mbar_wait(&B.full[s], ph);
-                if (elect_one()) mbar_arrive_cluster(leader_full0 + s * 8);
-                __syncwarp();
-                if (++s == kStages) { s = 0; ph ^= 1; }
-            }
+        // (bulk-copy producer only; 2-CTA TMA completes the leader's barrier directly)
+        if (!TMA) {
+            int s = 0; uint32_t ph = 0;
+            const uint32_t leader_full0 = mapa(smem_u32(&B.full[0]), 0);
+            for (int w = cluster_id(); w < wm.items(); w += nclusters())
+                for (int i = 0; i < kPasses * wm.item_kb(w); ++i) {
+                    mbar_wait(&B.full[s], ph);
+                    if (elect_one()) mbar_arrive_cluster(leader_full0 + s * 8);
+                    __syncwarp();
+                    if (++s == kStages) { s = 0; ph ^= 1; }
+                }
+        }
     } else if (warp == 1) {
         // ------------------------------------------------ leader: MMA issuer (one elected lane)
         int s = 0; uint32_t ph = 0; uint32_t u = 0;
@@ -417,7 +439,7 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Wor
     }
 }
 
-template <bool FAULT>
+template <bool FAULT, bool TMA>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -444,7 +466,9 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     wm.splits = p.splits < 1 ? 1 : p.splits;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) { mbar_init(&B.full[s], leader ? 2 : 1); mbar_init(&B.empty[s], 1); }
+        // full: the leader's own copies (+ the peer's relay without TMA; with 2-CTA TMA the
+        // peer's bytes complete the leader's barrier directly)
+        for (int s = 0; s < kStages; ++s) { mbar_init(&B.full[s], (leader && !TMA) ? 2 : 1); mbar_init(&B.empty[s], 1); }
         mbar_init(B.tfull, 1);
         for (int h = 0; h < 2; ++h) mbar_init(&B.tempty[h], 2 * kEpiWarps);   // both CTAs' epilogue warps (leader's copy)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -462,7 +486,7 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     // register budget: the control warpgroup needs few, the epilogue holds 64 u64 sums per thread
     if (warp < 4) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
-        control_roles<FAULT>(p, wm, warp, lane, rank, tmem_base, B);
+        control_roles<FAULT, TMA>(p, wm, warp, lane, rank, tmem_base, B);
         if (p.dbg && warp == 1 && lane == 0 && rank == 0) atomicMax(&p.dbg[6], globaltimer());
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
@@ -506,16 +530,62 @@ size_t ring_gemm_smem_bytes() {
     return (size_t)gemm::kStages * gemm::kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 }
 
+// Tensor maps of the 2-CTA kernel's operands: each segment's plane buffer as a 2-D
+// tensor of 256-byte rows (every block offset, party and batch stride is a multiple
+// of 256 B), boxes of one super-pass's planes (8 or 6) of one 32-K block.
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr) != cudaSuccess ||
+            qr != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+constexpr int kTmaRow = 2048;                     // bytes per tensor-map row: 256 x 8-byte elements
+static bool encode_rows(CUtensorMap* m, const void* base, uint64_t bytes, uint32_t box_rows) {
+    const PFN_cuTensorMapEncodeTiled_v12000 enc = tmap_encoder();
+    if (!enc || !base || bytes < kTmaRow || (bytes % kTmaRow) || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+    const cuuint64_t dims[2] = {kTmaRow / 8, bytes / kTmaRow};
+    const cuuint64_t strides[1] = {kTmaRow};
+    const cuuint32_t box[2] = {kTmaRow / 8, box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+static bool fill_tma(RingGemmParams& q, int parties) {
+    const int64_t nb = q.batch > 1 ? q.batch : 1;
+    const int64_t rbA = pad_rows<Layout::Left>(q.M) / gemm::GL::kRows, rbB = pad_rows<Layout::Right>(q.N) / gemm::GR::kRows;
+    for (int sg = 0; sg < q.nseg && sg < 2; ++sg) {
+        const RingGemmSegment& S = q.seg[sg];
+        const uint64_t instA = (uint64_t)rbA * S.kb * 8 * gemm::GL::kBlock;
+        const uint64_t instB = (uint64_t)rbB * S.kb * 8 * gemm::GR::kBlock;
+        const uint64_t extA = instA + (uint64_t)(parties - 1) * S.party_stride_A + (uint64_t)(nb - 1) * S.batch_stride_A;
+        const uint64_t extB = instB + (uint64_t)(parties - 1) * S.party_stride_B + (uint64_t)(nb - 1) * S.batch_stride_B;
+        if ((S.party_stride_A | S.party_stride_B | S.batch_stride_A | S.batch_stride_B) % kTmaRow) return false;
+        for (int g = 0; g < gemm::kPasses; ++g) {
+            const int planes = g == 0 ? 8 : 6;
+            if (!encode_rows(&q.tma.a[sg][g], S.A, extA, planes * gemm::GL::kBlock / kTmaRow) ||
+                !encode_rows(&q.tma.b[sg][g], S.B, extB, planes * gemm::GR::kBlock / kTmaRow))
+                return false;
+        }
+    }
+    return true;
+}
+
 cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_t stream) {
     static int attr_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
     const size_t smem = ring_gemm_smem_bytes();
     if (attr_dev != dev) {
-        cudaError_t e = cudaFuncSetAttribute(gemm::ring_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(gemm::ring_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaSuccess;
+        for (auto k : {gemm::ring_gemm_kernel<false, true>, gemm::ring_gemm_kernel<false, false>,
+                       gemm::ring_gemm_kernel<true, false>})
+            if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr_dev = dev;
     }
@@ -552,11 +622,14 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     if (clusters < 1) clusters = 1;
     static const bool debug = getenv("MPC_GEMM_DEBUG") != nullptr;
     if (!debug) {
-        cudaError_t e = q.fault_inject
-            ? launch_pdl(gemm::ring_gemm_kernel<true>, dim3((unsigned)(clusters * 2)), dim3(gemm::kThreads), smem,
-                         stream, q, parties)
-            : launch_pdl(gemm::ring_gemm_kernel<false>, dim3((unsigned)(clusters * 2)), dim3(gemm::kThreads), smem,
-                         stream, q, parties);
+        // 2-CTA tensor TMA producer unless disabled (MPC_GEMM_TMA=0), under fault injection, or
+        // when a map cannot be encoded; then the bulk-copy producer with the peer relay
+        static const bool env_tma = !(getenv("MPC_GEMM_TMA") && atoi(getenv("MPC_GEMM_TMA")) == 0);
+        const bool tma = env_tma && !q.fault_inject && fill_tma(q, parties);
+        auto kern = q.fault_inject ? gemm::ring_gemm_kernel<true, false>
+                  : tma            ? gemm::ring_gemm_kernel<false, true>
+                                   : gemm::ring_gemm_kernel<false, false>;
+        cudaError_t e = launch_pdl(kern, dim3((unsigned)(clusters * 2)), dim3(gemm::kThreads), smem, stream, q, parties);
         if (e != cudaSuccess || q.splits <= 1) return e;
         return ring_gemm_finalize(q, parties, stream);
     }
@@ -567,7 +640,7 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0, stream);
-    gemm::ring_gemm_kernel<false><<<(unsigned)(clusters * 2), gemm::kThreads, smem, stream>>>(q, parties);
+    gemm::ring_gemm_kernel<false, false><<<(unsigned)(clusters * 2), gemm::kThreads, smem, stream>>>(q, parties);
     cudaEventRecord(e1, stream);
     cudaError_t e = cudaGetLastError();
     cudaMemcpyAsync(h, q.dbg, sizeof(h), cudaMemcpyDeviceToHost, stream);

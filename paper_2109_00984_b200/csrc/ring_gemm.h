@@ -1,6 +1,7 @@
 // ring_gemm.h — host interface of the tcgen05 limb-plane ring GEMM (internal).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace mpc {
@@ -13,6 +14,14 @@ struct RingGemmSegment {
     int64_t party_stride_B;
     int64_t batch_stride_A;  // bytes between batch elements' planes (batched GEMM; 0 when batch = 1)
     int64_t batch_stride_B;
+};
+
+// 2-D tensor maps (rows of 256 B over a whole plane buffer) of the two segments' left /
+// right planes, one per super-pass width (8 or 6 planes per 32-K block); filled by
+// ring_gemm_launch for the 2-CTA kernel's tensor-TMA producer.
+struct RingGemmTma {
+    CUtensorMap a[2][2];                // [segment][pass]
+    CUtensorMap b[2][2];
 };
 
 struct RingGemmParams {
@@ -48,6 +57,7 @@ struct RingGemmParams {
                                         // evict-first like z; default evict-last, so finalize reads them from L2
     int fault_inject;                   // test hook (MPC_GEMM_FAULT_INJECT=1): drop one stage's copies, so the
                                         // pipeline stalls and the mbarrier watchdog must trap
+    RingGemmTma tma;                    // set by the launcher (2-CTA kernel, MPC_GEMM_TMA != 0)
 };
 
 // Two kernels: the 2-CTA 256 x 128 kernel (planes in Layout::Left / Right) and
