@@ -34,8 +34,10 @@
 // tile end.  The kernel is persistent: 74 clusters walk the tiles in a grouped
 // order (4 row tiles x all column tiles x parties per group).
 //
-// Warp roles (384 threads per CTA): warp 0 = bulk-copy producer (both CTAs),
-// warp 1 = MMA issuer (leader CTA) / stage relay (peer CTA), warp 2 = TMEM
+// Warp roles (384 threads per CTA): warp 0 = producer (both CTAs: 2-CTA tensor
+// TMA completing the leader's stage barrier, or — MPC_GEMM_TMA=0 / fault
+// injection — bulk copies), warp 1 = MMA issuer (leader CTA) / stage relay
+// (peer CTA, bulk-copy producer only), warp 2 = TMEM
 // allocator, warps 4..11 = epilogue.
 #include <cstdint>
 #include <cstdio>
@@ -544,6 +546,11 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     }();
     return fn;
 }
+static CUtensorMapL2promotion tma_promotion() {
+    static const int v = getenv("MPC_GEMM_TMA_PROMO") ? atoi(getenv("MPC_GEMM_TMA_PROMO")) : 3;   // tuning knob
+    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+         : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
 constexpr int kTmaRow = 2048;                     // bytes per tensor-map row: 256 x 8-byte elements
 static bool encode_rows(CUtensorMap* m, const void* base, uint64_t bytes, uint32_t box_rows) {
     const PFN_cuTensorMapEncodeTiled_v12000 enc = tmap_encoder();
@@ -553,7 +560,7 @@ static bool encode_rows(CUtensorMap* m, const void* base, uint64_t bytes, uint32
     const cuuint32_t box[2] = {kTmaRow / 8, box_rows};
     const cuuint32_t es[2] = {1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(base), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, tma_promotion(),
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 static bool fill_tma(RingGemmParams& q, int parties) {
