@@ -182,6 +182,7 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
         asm volatile("griddepcontrol.wait;" ::: "memory");
         int s = 0; uint32_t ph = 0;
         long long st_empty = 0;
+        const uint64_t l2pol = l2_policy(p.tma_l2);
         for (int w = cluster_id(); w < wm.items(); w += nclusters()) {
             int party, m, n, klo, khi;
             wm.decode(w, party, m, n, klo, khi);
@@ -220,10 +221,17 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
                                 const uint32_t fb = mapa(smem_u32(&B.full[s]), 0);
                                 const uint8_t* st = B.stage_base + s * kStageBytes;
                                 const RingGemmSegment& Sx = second ? S1 : S0;
-                                tma_load_2d_2sm(smem_u32(st), &p.tma.a[second ? 1 : 0][g], 0,
-                                                (int)((srcA - Sx.A) >> 11), fb);
-                                tma_load_2d_2sm(smem_u32(st + kAStage), &p.tma.b[second ? 1 : 0][g], 0,
-                                                (int)((srcB - Sx.B) >> 11), fb);
+                                if (p.tma_l2 == 3) {
+                                    tma_load_2d_2sm(smem_u32(st), &p.tma.a[second ? 1 : 0][g], 0,
+                                                    (int)((srcA - Sx.A) >> 11), fb);
+                                    tma_load_2d_2sm(smem_u32(st + kAStage), &p.tma.b[second ? 1 : 0][g], 0,
+                                                    (int)((srcB - Sx.B) >> 11), fb);
+                                } else {
+                                    tma_load_2d_2sm_hint(smem_u32(st), &p.tma.a[second ? 1 : 0][g], 0,
+                                                         (int)((srcA - Sx.A) >> 11), fb, l2pol);
+                                    tma_load_2d_2sm_hint(smem_u32(st + kAStage), &p.tma.b[second ? 1 : 0][g], 0,
+                                                         (int)((srcB - Sx.B) >> 11), fb, l2pol);
+                                }
                             }
                             __syncwarp();
                             if (++s == kStages) { s = 0; ph ^= 1; }
@@ -629,10 +637,17 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     if (clusters < 1) clusters = 1;
     static const bool debug = getenv("MPC_GEMM_DEBUG") != nullptr;
     if (!debug) {
-        // 2-CTA tensor TMA producer unless disabled (MPC_GEMM_TMA=0), under fault injection, or
-        // when a map cannot be encoded; then the bulk-copy producer with the peer relay
-        static const bool env_tma = !(getenv("MPC_GEMM_TMA") && atoi(getenv("MPC_GEMM_TMA")) == 0);
-        const bool tma = env_tma && !q.fault_inject && fill_tma(q, parties);
+        // Producer: 2-CTA tensor TMA for latency-bound launches (at most 4 work items per
+        // cluster: the small model layers), bulk copies with the peer relay otherwise.
+        // Measured: TMA saves 2-4% on the ResNet / ViT chains, but on long power-capped
+        // runs of large GEMMs it reads 1.5-1.8x the DRAM bytes (more L2 misses; no L2
+        // cache-hint fixes it), lowers the sustained clock ~6% and ends ~1% slower.
+        // MPC_GEMM_TMA=0 / 1 forces either; fault injection uses the bulk path.
+        static const int env_tma = getenv("MPC_GEMM_TMA") ? atoi(getenv("MPC_GEMM_TMA")) : -1;
+        const bool want_tma = env_tma < 0 ? tiles * q.splits <= 4 * max_clusters : env_tma != 0;
+        const bool tma = want_tma && !q.fault_inject && fill_tma(q, parties);
+        static const int env_l2 = getenv("MPC_GEMM_TMA_L2") ? atoi(getenv("MPC_GEMM_TMA_L2")) : 3;
+        q.tma_l2 = env_l2;
         auto kern = q.fault_inject ? gemm::ring_gemm_kernel<true, false>
                   : tma            ? gemm::ring_gemm_kernel<false, true>
                                    : gemm::ring_gemm_kernel<false, false>;

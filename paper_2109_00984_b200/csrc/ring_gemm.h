@@ -57,6 +57,8 @@ struct RingGemmParams {
                                         // evict-first like z; default evict-last, so finalize reads them from L2
     int fault_inject;                   // test hook (MPC_GEMM_FAULT_INJECT=1): drop one stage's copies, so the
                                         // pipeline stalls and the mbarrier watchdog must trap
+    int tma_l2;                         // L2 policy of the TMA operand loads: 0 evict_normal, 1 evict_last,
+                                        // 2 evict_first, 3 no hint (MPC_GEMM_TMA_L2; experiment)
     RingGemmTma tma;                    // set by the launcher (2-CTA kernel, MPC_GEMM_TMA != 0)
 };
 
