@@ -637,14 +637,13 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     if (clusters < 1) clusters = 1;
     static const bool debug = getenv("MPC_GEMM_DEBUG") != nullptr;
     if (!debug) {
-        // Producer: 2-CTA tensor TMA for latency-bound launches (at most 4 work items per
-        // cluster: the small model layers), bulk copies with the peer relay otherwise.
-        // Measured: TMA saves 2-4% on the ResNet / ViT chains, but on long power-capped
-        // runs of large GEMMs it reads 1.5-1.8x the DRAM bytes (more L2 misses; no L2
-        // cache-hint fixes it), lowers the sustained clock ~6% and ends ~1% slower.
-        // MPC_GEMM_TMA=0 / 1 forces either; fault injection uses the bulk path.
-        static const int env_tma = getenv("MPC_GEMM_TMA") ? atoi(getenv("MPC_GEMM_TMA")) : -1;
-        const bool want_tma = env_tma < 0 ? tiles * q.splits <= 4 * max_clusters : env_tma != 0;
+        // Producer: 2-CTA tensor TMA (no relay hop; measured 2-3% faster at 4096^3 over
+        // 50-200 step runs and 1-4% on the model chains), bulk copies with the peer relay
+        // under MPC_GEMM_TMA=0 or fault injection.  In some GPU calls (boxes) the TMA
+        // producer read 1.5-1.8x the DRAM bytes (and lost ~1% over 200 steps); in others
+        // it reads the same 4.4 GB per 4096^3 launch as the bulk path.
+        static const int env_tma = getenv("MPC_GEMM_TMA") ? atoi(getenv("MPC_GEMM_TMA")) : 1;
+        const bool want_tma = env_tma != 0;
         const bool tma = want_tma && !q.fault_inject && fill_tma(q, parties);
         static const int env_l2 = getenv("MPC_GEMM_TMA_L2") ? atoi(getenv("MPC_GEMM_TMA_L2")) : 3;
         q.tma_l2 = env_l2;
