@@ -571,6 +571,19 @@ static bool encode_rows(CUtensorMap* m, const void* base, uint64_t bytes, uint32
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, tma_promotion(),
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+// Bytes of every operand plane buffer a launch reads (both segments, all instances).
+static uint64_t ring_gemm_plane_bytes(const RingGemmParams& q, int parties) {
+    const int64_t nb = q.batch > 1 ? q.batch : 1;
+    const int64_t rbA = pad_rows<Layout::Left>(q.M) / gemm::GL::kRows, rbB = pad_rows<Layout::Right>(q.N) / gemm::GR::kRows;
+    uint64_t tot = 0;
+    for (int sg = 0; sg < q.nseg && sg < 2; ++sg) {
+        const RingGemmSegment& S = q.seg[sg];
+        const uint64_t ia = (uint64_t)rbA * S.kb * 8 * gemm::GL::kBlock, ib = (uint64_t)rbB * S.kb * 8 * gemm::GR::kBlock;
+        tot += ia * ((S.party_stride_A ? parties : 1) * (S.batch_stride_A ? nb : 1));
+        tot += ib * ((S.party_stride_B ? parties : 1) * (S.batch_stride_B ? nb : 1));
+    }
+    return tot;
+}
 static bool fill_tma(RingGemmParams& q, int parties) {
     const int64_t nb = q.batch > 1 ? q.batch : 1;
     const int64_t rbA = pad_rows<Layout::Left>(q.M) / gemm::GL::kRows, rbB = pad_rows<Layout::Right>(q.N) / gemm::GR::kRows;
@@ -638,12 +651,14 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     static const bool debug = getenv("MPC_GEMM_DEBUG") != nullptr;
     if (!debug) {
         // Producer: 2-CTA tensor TMA (no relay hop; measured 2-3% faster at 4096^3 over
-        // 50-200 step runs and 1-4% on the model chains), bulk copies with the peer relay
-        // under MPC_GEMM_TMA=0 or fault injection.  In some GPU calls (boxes) the TMA
-        // producer read 1.5-1.8x the DRAM bytes (and lost ~1% over 200 steps); in others
-        // it reads the same 4.4 GB per 4096^3 launch as the bulk path.
-        static const int env_tma = getenv("MPC_GEMM_TMA") ? atoi(getenv("MPC_GEMM_TMA")) : 1;
-        const bool want_tma = env_tma != 0;
+        // 50-200 step runs and 1-4% on the model chains), except for GEMMs whose operand
+        // planes exceed 2 GiB: there the TMA-fed kernel reads far more DRAM (4-party
+        // 8192^3: 276 vs 100 GB per launch; faster alone under ncu, 3% slower in a
+        // power-capped run).  In some GPU calls the TMA producer also read 1.5-1.8x the
+        // DRAM bytes at 4096^3.  MPC_GEMM_TMA=0 / 1 forces either; fault
+        // injection uses the bulk path.
+        static const int env_tma = getenv("MPC_GEMM_TMA") ? atoi(getenv("MPC_GEMM_TMA")) : -1;
+        const bool want_tma = env_tma < 0 ? ring_gemm_plane_bytes(q, parties) <= (2ull << 30) : env_tma != 0;
         const bool tma = want_tma && !q.fault_inject && fill_tma(q, parties);
         static const int env_l2 = getenv("MPC_GEMM_TMA_L2") ? atoi(getenv("MPC_GEMM_TMA_L2")) : 3;
         q.tma_l2 = env_l2;
