@@ -81,6 +81,34 @@ typedef enum {
  * MPC_ERR_UNSUPPORTED if `device` is not a compute-capability 10.0 GPU. */
 mpc_status mpc_create(mpc_ctx* out, int world_size, int rank, int device,
                       const void* nccl_id, uint64_t master_seed, int frac_bits);
+
+/* ---- explicit keys (one party per process) ---------------------------------
+ * SECURITY NOTE.  mpc_create derives EVERY party's PRZS key and the TTP key from
+ * master_seed (the reproducibility convention of DESIGN.md R5, which lets the
+ * oracle and the GPU agree bit for bit).  A party holding the master seed can
+ * therefore regenerate a = sum a_p and b = sum b_p and unmask x = eps + a,
+ * y = delta + b: mpc_create is for benchmarks and tests, NOT a private
+ * deployment.  A deployment agrees keys at set-up ("sync random seeds"):
+ *   przs_self  k_p, shared by party p and party p+1 (mod P),
+ *   przs_prev  k_{p-1}, shared by party p-1 and party p (P = 1: equal to przs_self),
+ *   ttp        k_ttp, held by the dealer only (has_ttp = 0 on a computing party).
+ * mpc_create_with_keys creates one party (rank in [0, P), never MPC_ALL_PARTIES)
+ * that knows only these keys.  Without k_ttp the context cannot generate TTP
+ * material: mpc_ttp_* , mpc_truncate (wrap pair from an id) and mpc_relu return
+ * MPC_ERR_STATE; the triples are passed in as arguments, and the P > 2 truncation
+ * takes its wrap pair with mpc_truncate_pairs.  Shares are bit-identical to an
+ * mpc_create context whose master seed derives the same keys (mpc_derive_keys
+ * returns rank's keys under the R5 convention).  MPC_ERR_ARG for a bad rank,
+ * NULL keys, or P = 1 with przs_self != przs_prev. */
+typedef struct {
+    uint64_t przs_self;
+    uint64_t przs_prev;
+    uint64_t ttp;
+    int has_ttp;
+} mpc_keys;
+mpc_status mpc_derive_keys(uint64_t master_seed, int world_size, int rank, mpc_keys* out);
+mpc_status mpc_create_with_keys(mpc_ctx* out, int world_size, int rank, int device,
+                                const void* nccl_id, const mpc_keys* keys, int frac_bits);
 mpc_status mpc_destroy(mpc_ctx ctx);
 mpc_status mpc_set_stream(mpc_ctx ctx, void* cuda_stream);
 const char* mpc_last_error(mpc_ctx ctx);      /* never NULL; valid until the next call on ctx */
@@ -157,7 +185,7 @@ mpc_status mpc_ttp_triples(mpc_ctx ctx, uint64_t triple_id, int64_t M, int64_t K
  * r_p = G(k_ttp, R||p||id); theta_r = (sum signed(r_p) - signed(sum r_p)) / 2^64;
  * [theta_r]_p = G(k_ttp, THETA||p||id) for p >= 1, [theta_r]_0 = theta_r - sum_{p>=1}.
  * mpc_truncate regenerates exactly these values from wrap_id; this entry point
- * materialises them (tests, inspection). */
+ * materialises them for mpc_truncate_pairs (the offline phase). */
 mpc_status mpc_ttp_wrap_pairs(mpc_ctx ctx, uint64_t wrap_id, int64_t n,
                               uint64_t* r, uint64_t* theta_r);
 
@@ -234,6 +262,14 @@ mpc_status mpc_beaver_matmul_prepared(mpc_ctx ctx, const uint64_t* x, const uint
  * (signed(x_p) >> bits) + bit_{bits-1}(x_p) (0 rounds).  P > 2: Alg. 1 with the wrap
  * pair wrap_id, eta skipped (1 round). */
 mpc_status mpc_truncate(mpc_ctx ctx, uint64_t* x_inout, int64_t n, int bits, uint64_t wrap_id);
+/* The same truncation with the wrap pair passed in (Alg. 1's inputs [r], [theta_r],
+ * P:606-612), as materialised offline by mpc_ttp_wrap_pairs: r and theta_r hold this
+ * party's shares (n) or every party's ([P][n]).  The online step then reads the pair
+ * instead of regenerating it from k_ttp (no TTP work on party 0's critical path; works
+ * on a context without k_ttp).  Result bit-identical to mpc_truncate with the pair's
+ * wrap_id.  P <= 2 ignores r / theta_r (local truncation).  Each pair is single-use. */
+mpc_status mpc_truncate_pairs(mpc_ctx ctx, uint64_t* x_inout, int64_t n, int bits, const uint64_t* r,
+                              const uint64_t* theta_r);
 
 /* ---- plain ring GEMM C = A @ B mod 2^64 (building block of ttp_triples) ---
  * A: M x K, B: K x N, C: M x N, device buffers; not a protocol step (no shares).

@@ -3,6 +3,6 @@
 The hot path is the C-ABI library ``libmpc_ring.so`` (include/mpc_ring.h);
 ``mpc.Context`` is its thin Python binding.
 """
-from .mpc import ALL_PARTIES, Context, Group, MpcError, create, nccl_unique_id  # noqa: F401
+from .mpc import ALL_PARTIES, Context, Group, Keys, MpcError, create, derive_keys, nccl_unique_id  # noqa: F401
 
-__all__ = ["ALL_PARTIES", "Context", "Group", "MpcError", "create", "nccl_unique_id"]
+__all__ = ["ALL_PARTIES", "Context", "Group", "Keys", "MpcError", "create", "derive_keys", "nccl_unique_id"]

@@ -15,10 +15,18 @@ class ConvGeom(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int64) for f in ("B", "C", "H", "W", "Cout", "kh", "kw", "sh", "sw", "ph", "pw")]
 
 
+class Keys(ctypes.Structure):
+    """mpc_keys (include/mpc_ring.h): one party's PRZS key pair and, for the dealer, k_ttp."""
+    _fields_ = [("przs_self", ctypes.c_uint64), ("przs_prev", ctypes.c_uint64), ("ttp", ctypes.c_uint64),
+                ("has_ttp", ctypes.c_int)]
+
+
 # (name, restype, argtypes); P = void*, I = int, L = int64, U = uint64, S = size_t
 _V, _I, _L, _U, _S, _D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_size_t, ctypes.c_double
 SIGNATURES = [
     ("mpc_create", _I, [ctypes.POINTER(_V), _I, _I, _I, _V, _U, _I]),
+    ("mpc_derive_keys", _I, [_U, _I, _I, ctypes.POINTER(Keys)]),
+    ("mpc_create_with_keys", _I, [ctypes.POINTER(_V), _I, _I, _I, _V, ctypes.POINTER(Keys), _I]),
     ("mpc_destroy", _I, [_V]),
     ("mpc_set_stream", _I, [_V, _V]),
     ("mpc_last_error", ctypes.c_char_p, [_V]),
@@ -47,6 +55,7 @@ SIGNATURES = [
     ("mpc_beaver_prepare", _I, [_V, _V, _V, _L, _L, _L, _V, _S]),
     ("mpc_beaver_matmul_prepared", _I, [_V, _V, _V, _V, _V, _L, _L, _L, _I, _U, _V, _S]),
     ("mpc_truncate", _I, [_V, _V, _L, _I, _U]),
+    ("mpc_truncate_pairs", _I, [_V, _V, _L, _I, _V, _V]),
     ("mpc_ring_matmul_workspace_bytes", _S, [_L, _L, _L]),
     ("mpc_ring_matmul", _I, [_V, _V, _V, _V, _L, _L, _L, _V, _S]),
     ("mpc_ttp_mul_triples", _I, [_V, _U, _L, _V, _V, _V]),
@@ -96,3 +105,12 @@ def nccl_unique_id() -> bytes:
     if st != 0:
         raise RuntimeError(f"mpc_nccl_unique_id failed ({st})")
     return buf.raw
+
+
+def derive_keys(master_seed: int, world_size: int, rank: int) -> Keys:
+    """Party `rank`'s keys under the reproducibility convention (mpc_derive_keys; host only)."""
+    k = Keys()
+    st = lib().mpc_derive_keys(ctypes.c_uint64(master_seed), world_size, rank, ctypes.byref(k))
+    if st != 0:
+        raise ValueError(f"mpc_derive_keys failed ({st})")
+    return k

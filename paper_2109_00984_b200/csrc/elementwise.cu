@@ -566,36 +566,67 @@ cudaError_t launch_ttp_c(uint64_t key, uint64_t id, int P, int out_lo, int out_h
 }
 
 // ------------------------------------------------------------------ a9 wrap pairs
-// theta_r of the r shares, exactly: (sum signed(r_q) - signed(sum r_q)) / 2^64
-__device__ __forceinline__ int64_t theta_r_at(uint64_t key, uint64_t id, int P, int64_t i) {
-    __int128 s = 0;
-    uint64_t u = 0;
-    for (int q = 0; q < P; ++q) {
-        const uint64_t r = philox_at(key, stream_word(kTagR, (uint32_t)q, id), (uint64_t)i);
-        s += (__int128)(int64_t)r;
-        u += r;
-    }
-    return (int64_t)((s - (__int128)(int64_t)u) >> 64);
+// Element pairs: one Philox4x32-10 block yields both elements of a pair, so
+// every per-element helper below works on pair j = elements (2j, 2j + 1).
+// Pair loads / stores are 16-byte vectors when n is even and the base is
+// 16-byte aligned (then every party's row of [P][n] is too).
+__device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+__device__ __forceinline__ void ld_pair(const uint64_t* __restrict__ p, int64_t i0, bool vec, bool has1, uint64_t (&o)[2]) {
+    if (vec) { const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(p + i0); o[0] = t.x; o[1] = t.y; }
+    else { o[0] = p[i0]; o[1] = has1 ? p[i0 + 1] : 0ull; }
 }
-// [theta_r]_q: q >= 1 -> G(THETA||q||id), q = 0 -> theta_r - sum_{q>=1}
-__device__ __forceinline__ uint64_t theta_share_at(uint64_t key, uint64_t id, int P, int q, int64_t i) {
-    if (q > 0) return philox_at(key, stream_word(kTagTheta, (uint32_t)q, id), (uint64_t)i);
-    uint64_t t = (uint64_t)theta_r_at(key, id, P, i);
-    for (int s = 1; s < P; ++s) t -= philox_at(key, stream_word(kTagTheta, (uint32_t)s, id), (uint64_t)i);
-    return t;
+__device__ __forceinline__ void st_pair(uint64_t* __restrict__ p, int64_t i0, bool vec, bool has1, const uint64_t (&v)[2]) {
+    if (vec) *reinterpret_cast<ulonglong2*>(p + i0) = make_ulonglong2(v[0], v[1]);
+    else { p[i0] = v[0]; if (has1) p[i0 + 1] = v[1]; }
+}
+// wrap count of two terms: (signed(u) + signed(v) - signed(u + v)) / 2^64 in {-1, 0, 1}
+__device__ __forceinline__ uint64_t wrap2(uint64_t u, uint64_t v) {
+    const __int128 s = (__int128)(int64_t)u + (__int128)(int64_t)v - (__int128)(int64_t)(u + v);
+    return (uint64_t)(int64_t)(s >> 64);
+}
+// theta_r of pair j, exactly: (sum signed(r_q) - signed(sum r_q)) / 2^64 (the TTP's view)
+__device__ __forceinline__ void theta_r_pair(uint64_t key, uint64_t id, int P, uint64_t j, uint64_t (&t)[2]) {
+    __int128 s[2] = {0, 0};
+    uint64_t u[2] = {0, 0};
+    for (int q = 0; q < P; ++q) {
+        uint64_t r[2];
+        philox_pair(key, stream_word(kTagR, (uint32_t)q, id), j, r[0], r[1]);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) { s[e] += (__int128)(int64_t)r[e]; u[e] += r[e]; }
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) t[e] = (uint64_t)(int64_t)((s[e] - (__int128)(int64_t)u[e]) >> 64);
+}
+// [theta_r]_q of pair j: q >= 1 -> G(THETA||q||id), q = 0 -> theta_r - sum_{q>=1} (TTP view)
+__device__ __forceinline__ void theta_share_pair(uint64_t key, uint64_t id, int P, int q, uint64_t j, uint64_t (&t)[2]) {
+    if (q > 0) { philox_pair(key, stream_word(kTagTheta, (uint32_t)q, id), j, t[0], t[1]); return; }
+    theta_r_pair(key, id, P, j, t);
+    for (int s = 1; s < P; ++s) {
+        uint64_t v[2];
+        philox_pair(key, stream_word(kTagTheta, (uint32_t)s, id), j, v[0], v[1]);
+        t[0] -= v[0]; t[1] -= v[1];
+    }
 }
 __global__ void wrap_pair_kernel(uint64_t key, uint64_t id, int P, int lo, int hi, uint64_t* __restrict__ r,
                                  uint64_t* __restrict__ th, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    const int64_t npairs = (n + 1) / 2;
+    const bool vec = (n & 1) == 0 && aligned16(r) && aligned16(th);
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npairs; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i0 = 2 * j;
+        const bool has1 = i0 + 1 < n;
         for (int q = lo; q < hi; ++q) {
-            r[(int64_t)(q - lo) * n + i] = philox_at(key, stream_word(kTagR, (uint32_t)q, id), (uint64_t)i);
-            th[(int64_t)(q - lo) * n + i] = theta_share_at(key, id, P, q, i);
+            uint64_t v[2], t[2];
+            philox_pair(key, stream_word(kTagR, (uint32_t)q, id), (uint64_t)j, v[0], v[1]);
+            theta_share_pair(key, id, P, q, (uint64_t)j, t);
+            st_pair(r + (int64_t)(q - lo) * n, i0, vec, has1, v);
+            st_pair(th + (int64_t)(q - lo) * n, i0, vec, has1, t);
         }
+    }
 }
 cudaError_t launch_wrap_pair(uint64_t key, uint64_t id, int P, int lo, int hi, uint64_t* r, uint64_t* th, int64_t n,
                              cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    wrap_pair_kernel<<<grid_for(n), 256, 0, st>>>(key, id, P, lo, hi, r, th, n);
+    wrap_pair_kernel<<<grid_for((n + 1) / 2), 256, 0, st>>>(key, id, P, lo, hi, r, th, n);
     return cudaGetLastError();
 }
 
@@ -612,118 +643,170 @@ cudaError_t launch_trunc_local(uint64_t* x, int64_t n, int bits, cudaStream_t st
 
 // ------------------------------------------------------------------ a9 truncation, P > 2, all parties
 // Alg. 1 + correction, eta skipped, for
-// every party of element i in one thread (local reveal of z).
-// One thread per element pair (one Philox block yields both elements' r_q and
-// [theta_r]_q); the parties' r_q stay in registers (P <= 16, unrolled).
-__global__ void __launch_bounds__(128) trunc_alg1_all_kernel(uint64_t* __restrict__ x, int P, int64_t n, int bits,
-                                                            uint64_t key, uint64_t id) {
+// every party of an element pair in one thread (the reveal of z is local).
+// P is a template constant, so each party's r_q pair stays in registers
+// between the two passes, and x_q too for P <= 4; above that the second pass
+// re-reads x_q (an L1 hit: the block's 256 x P x 16 B were just loaded), which
+// keeps the kernel under 128 registers (2 blocks per SM).  The wrap pair
+// ([r], [theta_r]) is either regenerated from its Philox streams
+// (PAIRS = false: wrap_id, the seeded TTP; one block per element pair and
+// stream) or read from memory (PAIRS = true: materialised offline by
+// mpc_ttp_wrap_pairs).
+template <int P, bool PAIRS>
+__global__ void __launch_bounds__(256, (P <= 8 ? 2 : 1)) trunc_alg1_all_kernel(uint64_t* __restrict__ x, int64_t n, int bits,
+                                                            uint64_t key, uint64_t id, const uint64_t* __restrict__ rin,
+                                                            const uint64_t* __restrict__ thin) {
     const int64_t npairs = (n + 1) / 2;
+    const bool vec = (n & 1) == 0 && aligned16(x) && (!PAIRS || (aligned16(rin) && aligned16(thin)));
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npairs; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i0 = 2 * j;
         const bool has1 = i0 + 1 < n;
-        uint64_t r[kMaxParties][2];
+        uint64_t xv[P][2], r[P][2];
         uint64_t zsum[2] = {0, 0}, rsum[2] = {0, 0};
         __int128 zs[2] = {0, 0}, rs[2] = {0, 0};
 #pragma unroll
-        for (int q = 0; q < kMaxParties; ++q) {
-            if (q < P) {
-                philox_pair(key, stream_word(kTagR, (uint32_t)q, id), (uint64_t)j, r[q][0], r[q][1]);
-                const uint64_t* xq = x + (int64_t)q * n + i0;
+        for (int q = 0; q < P; ++q) {
+            ld_pair(x + (int64_t)q * n, i0, vec, has1, xv[q]);
+            if (PAIRS) ld_pair(rin + (int64_t)q * n, i0, vec, has1, r[q]);
+            else philox_pair(key, stream_word(kTagR, (uint32_t)q, id), (uint64_t)j, r[q][0], r[q][1]);
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const uint64_t xv = (e == 0 || has1) ? xq[e] : 0ull;
-                    const uint64_t z = xv + r[q][e];
-                    zsum[e] += z;
-                    zs[e] += (__int128)(int64_t)z;
-                    rsum[e] += r[q][e];
-                    rs[e] += (__int128)(int64_t)r[q][e];
-                }
+            for (int e = 0; e < 2; ++e) {
+                const uint64_t z = xv[q][e] + r[q][e];                  // z_q = x_q + r_q
+                zsum[e] += z;
+                zs[e] += (__int128)(int64_t)z;
+                if (!PAIRS) { rsum[e] += r[q][e]; rs[e] += (__int128)(int64_t)r[q][e]; }
             }
         }
-        uint64_t theta_z[2], theta_r[2];
+        uint64_t theta_z[2], theta_r[2] = {0, 0};
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-            theta_z[e] = (uint64_t)(int64_t)((zs[e] - (__int128)(int64_t)zsum[e]) >> 64);   // wraps of z's shares
-            theta_r[e] = (uint64_t)(int64_t)((rs[e] - (__int128)(int64_t)rsum[e]) >> 64);   // wraps of r's shares
+            theta_z[e] = (uint64_t)(int64_t)((zs[e] - (__int128)(int64_t)zsum[e]) >> 64);      // wraps of z
+            if (!PAIRS) theta_r[e] = (uint64_t)(int64_t)((rs[e] - (__int128)(int64_t)rsum[e]) >> 64);
         }
-        uint64_t th_sum[2] = {0, 0};                                                        // sum_{q>=1} [theta_r]_q
+        uint64_t th_sum[2] = {0, 0};                                   // sum_{q>=1} [theta_r]_q (seeded TTP)
 #pragma unroll
-        for (int q = kMaxParties - 1; q >= 0; --q) {
-            if (q < P) {
-                uint64_t th[2];
-                if (q > 0) {
-                    philox_pair(key, stream_word(kTagTheta, (uint32_t)q, id), (uint64_t)j, th[0], th[1]);
-                    th_sum[0] += th[0];
-                    th_sum[1] += th[1];
-                } else {
-                    th[0] = theta_r[0] - th_sum[0];
-                    th[1] = theta_r[1] - th_sum[1];
-                }
-                uint64_t* xq = x + (int64_t)q * n + i0;
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    if (e == 1 && !has1) break;
-                    const uint64_t xv = xq[e];
-                    const uint64_t z = xv + r[q][e];
-                    const __int128 bs = (__int128)(int64_t)xv + (__int128)(int64_t)r[q][e] - (__int128)(int64_t)z;
-                    const uint64_t beta = (uint64_t)(int64_t)(bs >> 64);
-                    const uint64_t theta_x = beta - th[e] + (q == 0 ? theta_z[e] : 0ull);
-                    xq[e] = div_pow2_round(xv, bits) - theta_x * (1ull << (64 - bits));
-                }
+        for (int q = P - 1; q >= 0; --q) {
+            uint64_t th[2];
+            if (PAIRS) {
+                ld_pair(thin + (int64_t)q * n, i0, vec, has1, th);
+            } else if (q > 0) {
+                philox_pair(key, stream_word(kTagTheta, (uint32_t)q, id), (uint64_t)j, th[0], th[1]);
+                th_sum[0] += th[0];
+                th_sum[1] += th[1];
+            } else {
+                th[0] = theta_r[0] - th_sum[0];
+                th[1] = theta_r[1] - th_sum[1];
             }
+            if (P > 4) ld_pair(x + (int64_t)q * n, i0, vec, has1, xv[q]);     // L1 hit (see above)
+            uint64_t o[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const uint64_t beta = wrap2(xv[q][e], r[q][e]);
+                const uint64_t theta_x = beta - th[e] + (q == 0 ? theta_z[e] : 0ull);
+                o[e] = div_pow2_round(xv[q][e], bits) - theta_x * (1ull << (64 - bits));
+            }
+            st_pair(x + (int64_t)q * n, i0, vec, has1, o);
         }
     }
 }
-cudaError_t launch_trunc_alg1_all(uint64_t* x, int P, int64_t n, int bits, uint64_t key, uint64_t id, cudaStream_t st) {
-    if (n == 0) return cudaSuccess;
-    trunc_alg1_all_kernel<<<grid_for((n + 1) / 2, 128), 128, 0, st>>>(x, P, n, bits, key, id);
+template <bool PAIRS>
+static cudaError_t launch_alg1_all_t(uint64_t* x, int P, int64_t n, int bits, uint64_t key, uint64_t id,
+                                     const uint64_t* r, const uint64_t* th, cudaStream_t st) {
+    const unsigned g = grid_for((n + 1) / 2, 256);
+    switch (P) {
+#define MPC_ALG1_CASE(Q) case Q: trunc_alg1_all_kernel<Q, PAIRS><<<g, 256, 0, st>>>(x, n, bits, key, id, r, th); break;
+        MPC_ALG1_CASE(3) MPC_ALG1_CASE(4) MPC_ALG1_CASE(5) MPC_ALG1_CASE(6) MPC_ALG1_CASE(7) MPC_ALG1_CASE(8)
+        MPC_ALG1_CASE(9) MPC_ALG1_CASE(10) MPC_ALG1_CASE(11) MPC_ALG1_CASE(12) MPC_ALG1_CASE(13) MPC_ALG1_CASE(14)
+        MPC_ALG1_CASE(15) MPC_ALG1_CASE(16)
+#undef MPC_ALG1_CASE
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
+}
+cudaError_t launch_trunc_alg1_all(uint64_t* x, int P, int64_t n, int bits, uint64_t key, uint64_t id,
+                                  const uint64_t* r, const uint64_t* th, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    return r ? launch_alg1_all_t<true>(x, P, n, bits, key, id, r, th, st)
+             : launch_alg1_all_t<false>(x, P, n, bits, key, id, nullptr, nullptr, st);
 }
 
 // ------------------------------------------------------------------ a9 truncation, P > 2, one party
 // Phase A: z_p = x_p + r_p -> zbuf (u64, to be sum-allreduced) and the top
-// nibble h_p = signed(z_p) >> 60 -> hbuf (int8, sum-allreduced; exact for P <= 16).
+// nibble h_p = signed(z_p) >> 60 -> hbuf (int8, sum-allreduced; exact for
+// P <= 16).  r_p from memory (rin) or from its Philox stream.
 __global__ void trunc_alg1_a_kernel(const uint64_t* __restrict__ x, int64_t n, uint64_t key, uint64_t id, int party,
-                                    uint64_t* __restrict__ zbuf, int8_t* __restrict__ hbuf) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t z = x[i] + philox_at(key, stream_word(kTagR, (uint32_t)party, id), (uint64_t)i);
-        zbuf[i] = z;
-        hbuf[i] = (int8_t)((int64_t)z >> 60);
+                                    const uint64_t* __restrict__ rin, uint64_t* __restrict__ zbuf,
+                                    int8_t* __restrict__ hbuf) {
+    const int64_t npairs = (n + 1) / 2;
+    const bool vec = (n & 1) == 0 && aligned16(x) && aligned16(zbuf) && (!rin || aligned16(rin));
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npairs; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i0 = 2 * j;
+        const bool has1 = i0 + 1 < n;
+        uint64_t xv[2], r[2], z[2];
+        ld_pair(x, i0, vec, has1, xv);
+        if (rin) ld_pair(rin, i0, vec, has1, r);
+        else philox_pair(key, stream_word(kTagR, (uint32_t)party, id), (uint64_t)j, r[0], r[1]);
+        z[0] = xv[0] + r[0];
+        z[1] = xv[1] + r[1];
+        st_pair(zbuf, i0, vec, has1, z);
+        hbuf[i0] = (int8_t)((int64_t)z[0] >> 60);
+        if (has1) hbuf[i0 + 1] = (int8_t)((int64_t)z[1] >> 60);
     }
 }
 // Phase B: with z = sum z_q and H = sum h_q: S = sum signed(z_q) = (H + kappa) 2^60
-// + (z mod 2^60), kappa = ((z >> 60) - H) mod 16; theta_z = (S - signed(z)) / 2^64.
+// + (z mod 2^60), kappa = ((z >> 60) - H) mod 16; theta_z = (S - signed(z)) / 2^64
+// (party 0 only).  [theta_r]_p from memory (thin) or regenerated (seeded TTP: for
+// party 0 that is the TTP's theta_r over all P r streams).
 __global__ void trunc_alg1_b_kernel(uint64_t* __restrict__ x, int64_t n, int bits, uint64_t key, uint64_t id, int P,
-                                    int party, const uint64_t* __restrict__ zsum, const int8_t* __restrict__ hsum) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t xq = x[i];
-        const uint64_t r = philox_at(key, stream_word(kTagR, (uint32_t)party, id), (uint64_t)i);
-        const uint64_t zq = xq + r;
-        const __int128 bs = (__int128)(int64_t)xq + (__int128)(int64_t)r - (__int128)(int64_t)zq;
-        const uint64_t beta = (uint64_t)(int64_t)(bs >> 64);
-        uint64_t theta_z = 0;
-        if (party == 0) {
-            const uint64_t z = zsum[i];
-            const int64_t H = hsum[i];
-            const int64_t kappa = (((int64_t)(z >> 60) - H) % 16 + 16) % 16;
-            const __int128 S = (__int128)(H + kappa) * ((__int128)1 << 60) + (__int128)(z & ((1ull << 60) - 1));
-            theta_z = (uint64_t)(int64_t)((S - (__int128)(int64_t)z) >> 64);
+                                    int party, const uint64_t* __restrict__ rin, const uint64_t* __restrict__ thin,
+                                    const uint64_t* __restrict__ zsum, const int8_t* __restrict__ hsum) {
+    const int64_t npairs = (n + 1) / 2;
+    const bool vec = (n & 1) == 0 && aligned16(x) && (!rin || (aligned16(rin) && aligned16(thin))) &&
+                     (party != 0 || aligned16(zsum));
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npairs; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i0 = 2 * j;
+        const bool has1 = i0 + 1 < n;
+        uint64_t xv[2], r[2], th[2], theta_z[2] = {0, 0};
+        ld_pair(x, i0, vec, has1, xv);
+        if (rin) {
+            ld_pair(rin, i0, vec, has1, r);
+            ld_pair(thin, i0, vec, has1, th);
+        } else {
+            philox_pair(key, stream_word(kTagR, (uint32_t)party, id), (uint64_t)j, r[0], r[1]);
+            theta_share_pair(key, id, P, party, (uint64_t)j, th);
         }
-        const uint64_t thq = theta_share_at(key, id, P, party, i);
-        const uint64_t theta_x = beta - thq + theta_z;
-        x[i] = div_pow2_round(xq, bits) - theta_x * (1ull << (64 - bits));
+        if (party == 0) {
+            uint64_t zv[2];
+            ld_pair(zsum, i0, vec, has1, zv);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                if (e == 1 && !has1) break;
+                const int64_t H = hsum[i0 + e];
+                const int64_t kappa = (((int64_t)(zv[e] >> 60) - H) % 16 + 16) % 16;
+                const __int128 S = (__int128)(H + kappa) * ((__int128)1 << 60) + (__int128)(zv[e] & ((1ull << 60) - 1));
+                theta_z[e] = (uint64_t)(int64_t)((S - (__int128)(int64_t)zv[e]) >> 64);
+            }
+        }
+        uint64_t o[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const uint64_t theta_x = wrap2(xv[e], r[e]) - th[e] + theta_z[e];
+            o[e] = div_pow2_round(xv[e], bits) - theta_x * (1ull << (64 - bits));
+        }
+        st_pair(x, i0, vec, has1, o);
     }
 }
-cudaError_t launch_trunc_alg1_a(const uint64_t* x, int64_t n, uint64_t key, uint64_t id, int party, uint64_t* zbuf,
-                                int8_t* hbuf, cudaStream_t st) {
+cudaError_t launch_trunc_alg1_a(const uint64_t* x, int64_t n, uint64_t key, uint64_t id, int party, const uint64_t* r,
+                                uint64_t* zbuf, int8_t* hbuf, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    trunc_alg1_a_kernel<<<grid_for(n), 256, 0, st>>>(x, n, key, id, party, zbuf, hbuf);
+    trunc_alg1_a_kernel<<<grid_for((n + 1) / 2), 256, 0, st>>>(x, n, key, id, party, r, zbuf, hbuf);
     return cudaGetLastError();
 }
 cudaError_t launch_trunc_alg1_b(uint64_t* x, int64_t n, int bits, uint64_t key, uint64_t id, int P, int party,
-                                const uint64_t* zsum, const int8_t* hsum, cudaStream_t st) {
+                                const uint64_t* r, const uint64_t* th, const uint64_t* zsum, const int8_t* hsum,
+                                cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    trunc_alg1_b_kernel<<<grid_for(n), 256, 0, st>>>(x, n, bits, key, id, P, party, zsum, hsum);
+    trunc_alg1_b_kernel<<<grid_for((n + 1) / 2), 256, 0, st>>>(x, n, bits, key, id, P, party, r, th, zsum, hsum);
     return cudaGetLastError();
 }
 

@@ -75,10 +75,14 @@ cudaError_t launch_ttp_c(uint64_t key, uint64_t id, int P, int out_lo, int out_h
 cudaError_t launch_wrap_pair(uint64_t key, uint64_t id, int P, int lo, int hi, uint64_t* r, uint64_t* th, int64_t n,
                              cudaStream_t st);
 cudaError_t launch_trunc_local(uint64_t* x, int64_t n, int bits, cudaStream_t st);
-cudaError_t launch_trunc_alg1_all(uint64_t* x, int P, int64_t n, int bits, uint64_t key, uint64_t id, cudaStream_t st);
-cudaError_t launch_trunc_alg1_a(const uint64_t* x, int64_t n, uint64_t key, uint64_t id, int party, uint64_t* zbuf,
-                                int8_t* hbuf, cudaStream_t st);
+// Alg. 1 (P > 2).  r, th: the wrap pair in memory ([P][n] for all parties, n for one
+// party), or both null to regenerate it from wrap id `id` under k_ttp `key`.
+cudaError_t launch_trunc_alg1_all(uint64_t* x, int P, int64_t n, int bits, uint64_t key, uint64_t id,
+                                  const uint64_t* r, const uint64_t* th, cudaStream_t st);
+cudaError_t launch_trunc_alg1_a(const uint64_t* x, int64_t n, uint64_t key, uint64_t id, int party, const uint64_t* r,
+                                uint64_t* zbuf, int8_t* hbuf, cudaStream_t st);
 cudaError_t launch_trunc_alg1_b(uint64_t* x, int64_t n, int bits, uint64_t key, uint64_t id, int P, int party,
-                                const uint64_t* zsum, const int8_t* hsum, cudaStream_t st);
+                                const uint64_t* r, const uint64_t* th, const uint64_t* zsum, const int8_t* hsum,
+                                cudaStream_t st);
 
 }  // namespace mpc

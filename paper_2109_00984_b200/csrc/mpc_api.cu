@@ -32,6 +32,7 @@ struct mpc_ctx_s {
     uint64_t master = 0;
     KeySet kp{};
     uint64_t kttp = 0;
+    bool has_ttp = true;                 // holds k_ttp (mpc_create; mpc_create_with_keys only if given)
     cudaStream_t stream = nullptr;
     ncclComm_t comm = nullptr;
     LocalGroup* lg = nullptr;               // in-process transport (mpc_create_local), instead of NCCL
@@ -53,6 +54,8 @@ struct mpc_ctx_s {
     int* d_err = nullptr;
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
+    cudaStream_t scratch_stream = nullptr;  // last stream that used the scratch
+    cudaEvent_t scratch_ev = nullptr;
 };
 
 namespace {
@@ -141,7 +144,6 @@ mpc_status comm_allreduce(mpc_ctx c, const void* send, void* recv, size_t count,
         if (c->xbuf_bytes < need) {
             cudaStreamSynchronize(st);
             if (c->xbuf) cudaFree(c->xbuf);
-    if (c->check_buf) cudaFree(c->check_buf);
             c->xbuf = nullptr; c->xbuf_bytes = 0;
             if (cudaMalloc(&c->xbuf, need) != cudaSuccess) return fail(c, MPC_ERR_CUDA, "%s: xor buffer alloc", what);
             c->xbuf_bytes = need;
@@ -178,6 +180,12 @@ mpc_status enter(mpc_ctx c) {
     cudaError_t e = cudaSetDevice(c->device);
     if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
     return MPC_OK;
+}
+
+// TTP material (triples, wrap pairs, the ReLU path's binary triples) needs k_ttp
+// (a context from mpc_create_with_keys without it must be handed that material)
+mpc_status need_ttp(mpc_ctx c, const char* what) {
+    return c->has_ttp ? MPC_OK : fail(c, MPC_ERR_STATE, "%s: context holds no TTP key (mpc_create_with_keys)", what);
 }
 
 constexpr int kCommSms = 16;     // SMs (NCCL CTAs) reserved for a reveal overlapped with the GEMM
@@ -377,7 +385,17 @@ mpc_status gemm_run(mpc_ctx c, RingGemmParams& p, int parties) {
     return run(c, kClsGemm, "ring_gemm", [&] { return ring_gemm_launch(p, parties, c->stream); });
 }
 
+// The context scratch (elementwise mul / square, truncate, relu buffers) is
+// stream-ordered: a call on another stream than the scratch's last user first
+// waits for that stream's work, and a reallocation waits for both streams.
 mpc_status ensure_scratch(mpc_ctx c, size_t bytes) {
+    if (c->scratch_stream != c->stream && c->scratch) {
+        if (!c->scratch_ev && cudaEventCreateWithFlags(&c->scratch_ev, cudaEventDisableTiming) != cudaSuccess)
+            return fail(c, MPC_ERR_CUDA, "scratch event");
+        cudaEventRecord(c->scratch_ev, c->scratch_stream);
+        cudaStreamWaitEvent(c->stream, c->scratch_ev, 0);
+    }
+    c->scratch_stream = c->stream;
     if (c->scratch_bytes >= bytes) return MPC_OK;
     if (c->scratch) { cudaStreamSynchronize(c->stream); cudaFree(c->scratch); c->scratch = nullptr; c->scratch_bytes = 0; }
     cudaError_t e = cudaMalloc(&c->scratch, bytes);
@@ -386,25 +404,30 @@ mpc_status ensure_scratch(mpc_ctx c, size_t bytes) {
     return MPC_OK;
 }
 
-// Truncation of x ([P][n] or n) by `bits` with wrap pair `wrap_id`.
-mpc_status truncate_impl(mpc_ctx c, uint64_t* x, int64_t n, int bits, uint64_t wrap_id, uint64_t* zbuf, int8_t* hbuf) {
+// Truncation of x ([P][n] or n) by `bits` with the wrap pair `wrap_id` (seeded
+// TTP: regenerated from k_ttp) or, when r / th are given, the wrap pair in memory
+// (materialised offline by mpc_ttp_wrap_pairs; Alg. 1 takes [r], [theta_r] as
+// inputs).
+mpc_status truncate_impl(mpc_ctx c, uint64_t* x, int64_t n, int bits, uint64_t wrap_id, uint64_t* zbuf, int8_t* hbuf,
+                         const uint64_t* r = nullptr, const uint64_t* th = nullptr) {
     if (c->P <= 2) {
         const int64_t tot = n * (c->all ? c->P : 1);
         return run(c, kClsTrunc, "trunc_local", [&] { return launch_trunc_local(x, tot, bits, c->stream); });
     }
+    if (!r) CHECK(need_ttp(c, "truncate (wrap pair from wrap_id)"));
     c->rounds += 1;
     if (c->all) {
         c->bytes += 8ull * (uint64_t)n * c->P + (uint64_t)n * c->P;
         return run(c, kClsTrunc, "trunc_alg1_all",
-                   [&] { return launch_trunc_alg1_all(x, c->P, n, bits, c->kttp, wrap_id, c->stream); });
+                   [&] { return launch_trunc_alg1_all(x, c->P, n, bits, c->kttp, wrap_id, r, th, c->stream); });
     }
     c->bytes += 9ull * (uint64_t)n;
     CHECK(run(c, kClsTrunc, "trunc_alg1_a",
-              [&] { return launch_trunc_alg1_a(x, n, c->kttp, wrap_id, c->rank, zbuf, hbuf, c->stream); }));
+              [&] { return launch_trunc_alg1_a(x, n, c->kttp, wrap_id, c->rank, r, zbuf, hbuf, c->stream); }));
     CHECK(comm_allreduce(c, zbuf, zbuf, (size_t)n, RedOp::SumU64, "truncate z reveal"));
     CHECK(comm_allreduce(c, hbuf, hbuf, (size_t)n, RedOp::SumI8, "truncate top-bit reveal"));
     return run(c, kClsTrunc, "trunc_alg1_b", [&] {
-        return launch_trunc_alg1_b(x, n, bits, c->kttp, wrap_id, c->P, c->rank, zbuf, hbuf, c->stream);
+        return launch_trunc_alg1_b(x, n, bits, c->kttp, wrap_id, c->P, c->rank, r, th, zbuf, hbuf, c->stream);
     });
 }
 
@@ -412,8 +435,10 @@ mpc_status truncate_impl(mpc_ctx c, uint64_t* x, int64_t n, int bits, uint64_t w
 
 extern "C" {
 
-mpc_status mpc_create(mpc_ctx* out, int world_size, int rank, int device, const void* nccl_id,
-                      uint64_t master_seed, int frac_bits) {
+}  // extern "C"
+namespace {
+mpc_status create_impl(mpc_ctx* out, int world_size, int rank, int device, const void* nccl_id, const KeySet& kp,
+                       uint64_t kttp, bool has_ttp, int frac_bits) {
     if (!out) return MPC_ERR_ARG;
     *out = nullptr;
     if (world_size < 1 || world_size > kMaxParties) return MPC_ERR_ARG;
@@ -429,9 +454,9 @@ mpc_status mpc_create(mpc_ctx* out, int world_size, int rank, int device, const 
     c->all = (rank == MPC_ALL_PARTIES);
     c->device = device;
     c->frac = frac_bits;
-    c->master = master_seed;
-    for (int p = 0; p < world_size; ++p) c->kp.k[p] = philox_at(master_seed, stream_word(kTagKeyParty, p, 0), 0);
-    c->kttp = philox_at(master_seed, stream_word(kTagKeyTTP, 0, 0), 0);
+    c->kp = kp;
+    c->kttp = kttp;
+    c->has_ttp = has_ttp;
     // d_err[0]: the synchronous encode check; d_err[1]: the sticky flag of mpc_encode_async
     if (cudaMalloc(&c->d_err, 2 * sizeof(int)) != cudaSuccess) { delete c; return MPC_ERR_CUDA; }
     if (cudaMemset(c->d_err, 0, 2 * sizeof(int)) != cudaSuccess) { cudaFree(c->d_err); delete c; return MPC_ERR_CUDA; }
@@ -464,6 +489,48 @@ mpc_status mpc_create(mpc_ctx* out, int world_size, int rank, int device, const 
     }
     *out = c;
     return MPC_OK;
+}
+
+// The reproducibility convention (R5): every key from one master seed.
+KeySet derive_party_keys(uint64_t master_seed, int world_size) {
+    KeySet kp{};
+    for (int p = 0; p < world_size && p < kMaxParties; ++p)
+        kp.k[p] = philox_at(master_seed, stream_word(kTagKeyParty, p, 0), 0);
+    return kp;
+}
+uint64_t derive_ttp_key(uint64_t master_seed) { return philox_at(master_seed, stream_word(kTagKeyTTP, 0, 0), 0); }
+}  // namespace
+extern "C" {
+
+mpc_status mpc_create(mpc_ctx* out, int world_size, int rank, int device, const void* nccl_id,
+                      uint64_t master_seed, int frac_bits) {
+    return create_impl(out, world_size, rank, device, nccl_id, derive_party_keys(master_seed, world_size),
+                       derive_ttp_key(master_seed), true, frac_bits);
+}
+
+mpc_status mpc_derive_keys(uint64_t master_seed, int world_size, int rank, mpc_keys* out) {
+    if (!out || world_size < 1 || world_size > kMaxParties || rank < 0 || rank >= world_size) return MPC_ERR_ARG;
+    const KeySet kp = derive_party_keys(master_seed, world_size);
+    out->przs_self = kp.k[rank];
+    out->przs_prev = kp.k[(rank + world_size - 1) % world_size];
+    out->ttp = derive_ttp_key(master_seed);
+    out->has_ttp = 1;
+    return MPC_OK;
+}
+
+mpc_status mpc_create_with_keys(mpc_ctx* out, int world_size, int rank, int device, const void* nccl_id,
+                                const mpc_keys* keys, int frac_bits) {
+    if (!out) return MPC_ERR_ARG;
+    *out = nullptr;
+    if (!keys || rank == MPC_ALL_PARTIES || world_size < 1 || world_size > kMaxParties || rank < 0 ||
+        rank >= world_size)
+        return MPC_ERR_ARG;
+    if (world_size == 1 && keys->przs_self != keys->przs_prev) return MPC_ERR_ARG;   // one party is its own neighbour
+    KeySet kp{};                                 // only this party's two PRZS keys; the others stay 0
+    kp.k[(rank + world_size - 1) % world_size] = keys->przs_prev;
+    kp.k[rank] = keys->przs_self;
+    return create_impl(out, world_size, rank, device, nccl_id, kp, keys->has_ttp ? keys->ttp : 0,
+                       keys->has_ttp != 0, frac_bits);
 }
 
 struct mpc_group_s { LocalGroup* g; };
@@ -522,6 +589,7 @@ mpc_status mpc_destroy(mpc_ctx c) {
     for (auto e : c->pool) cudaEventDestroy(e);
     if (c->d_err) cudaFree(c->d_err);
     if (c->scratch) cudaFree(c->scratch);
+    if (c->scratch_ev) cudaEventDestroy(c->scratch_ev);
     delete c;
     return MPC_OK;
 }
@@ -633,6 +701,7 @@ size_t mpc_ttp_workspace_bytes(mpc_ctx c, int64_t M, int64_t K, int64_t N) {
 mpc_status mpc_ttp_triples(mpc_ctx c, uint64_t id, int64_t M, int64_t K, int64_t N, uint64_t* a, uint64_t* b,
                            uint64_t* cc, void* ws, size_t ws_bytes) {
     CHECK(enter(c));
+    CHECK(need_ttp(c, "ttp_triples"));
     if (M < 0 || K < 0 || N < 0) return fail(c, MPC_ERR_SHAPE, "ttp_triples: negative size");
     if ((M * K && !a) || (K * N && !b) || (M * N && !cc)) return fail(c, MPC_ERR_ARG, "ttp_triples: null output");
     const bool ttp = c->all || c->rank == 0;       // holds the TTP view: needs a, b sums and c
@@ -669,6 +738,7 @@ mpc_status mpc_ttp_triples(mpc_ctx c, uint64_t id, int64_t M, int64_t K, int64_t
 
 mpc_status mpc_ttp_wrap_pairs(mpc_ctx c, uint64_t id, int64_t n, uint64_t* r, uint64_t* th) {
     CHECK(enter(c));
+    CHECK(need_ttp(c, "ttp_wrap_pairs"));
     if (n < 0) return fail(c, MPC_ERR_SHAPE, "wrap_pairs: n < 0");
     if (n == 0) return MPC_OK;
     if (!r || !th) return fail(c, MPC_ERR_ARG, "wrap_pairs: null output");
@@ -923,6 +993,22 @@ mpc_status mpc_truncate(mpc_ctx c, uint64_t* x, int64_t n, int bits, uint64_t wr
     return truncate_impl(c, x, n, bits, wrap_id, zb, hb);
 }
 
+mpc_status mpc_truncate_pairs(mpc_ctx c, uint64_t* x, int64_t n, int bits, const uint64_t* r, const uint64_t* theta_r) {
+    CHECK(enter(c));
+    if (n < 0) return fail(c, MPC_ERR_SHAPE, "truncate_pairs: n < 0");
+    if (bits < 1 || bits > 62) return fail(c, MPC_ERR_ARG, "truncate_pairs: bits %d out of [1, 62]", bits);
+    if (n == 0) return MPC_OK;
+    if (!x || (c->P > 2 && (!r || !theta_r))) return fail(c, MPC_ERR_ARG, "truncate_pairs: null pointer");
+    uint64_t* zb = nullptr;
+    int8_t* hb = nullptr;
+    if (!c->all && c->P > 2) {
+        CHECK(ensure_scratch(c, align256(8 * (size_t)n) + (size_t)n));
+        zb = static_cast<uint64_t*>(c->scratch);
+        hb = reinterpret_cast<int8_t*>(static_cast<uint8_t*>(c->scratch) + align256(8 * (size_t)n));
+    }
+    return truncate_impl(c, x, n, bits, 0, zb, hb, r, theta_r);
+}
+
 size_t mpc_ring_matmul_workspace_bytes(int64_t M, int64_t K, int64_t N) {
     if (M < 0 || K < 0 || N < 0) return 0;
     return plain_gemm_ws(M, K, N).total;
@@ -953,6 +1039,7 @@ mpc_status mpc_ring_matmul(mpc_ctx c, const uint64_t* A, const uint64_t* B, uint
 // (App. A.1.1)
 mpc_status mpc_ttp_mul_triples(mpc_ctx c, uint64_t id, int64_t n, uint64_t* a, uint64_t* b, uint64_t* cc) {
     CHECK(enter(c));
+    CHECK(need_ttp(c, "ttp_mul_triples"));
     if (n < 0) return fail(c, MPC_ERR_SHAPE, "ttp_mul_triples: n < 0");
     if (n == 0) return MPC_OK;
     if (!a || !b || !cc) return fail(c, MPC_ERR_ARG, "ttp_mul_triples: null output");
@@ -963,6 +1050,7 @@ mpc_status mpc_ttp_mul_triples(mpc_ctx c, uint64_t id, int64_t n, uint64_t* a, u
 
 mpc_status mpc_ttp_square_pairs(mpc_ctx c, uint64_t id, int64_t n, uint64_t* a, uint64_t* b) {
     CHECK(enter(c));
+    CHECK(need_ttp(c, "ttp_square_pairs"));
     if (n < 0) return fail(c, MPC_ERR_SHAPE, "ttp_square_pairs: n < 0");
     if (n == 0) return MPC_OK;
     if (!a || !b) return fail(c, MPC_ERR_ARG, "ttp_square_pairs: null output");
@@ -1234,6 +1322,7 @@ size_t mpc_ttp_conv_workspace_bytes(mpc_ctx c, const mpc_conv2d_geom* gg) {
 mpc_status mpc_ttp_conv_triples(mpc_ctx c, uint64_t id, const mpc_conv2d_geom* gg, uint64_t* a, uint64_t* b,
                                 uint64_t* cc, void* ws, size_t ws_bytes) {
     CHECK(enter(c));
+    CHECK(need_ttp(c, "ttp_conv_triples"));
     if (!conv_geom_ok(gg)) return fail(c, MPC_ERR_SHAPE, "ttp_conv_triples: invalid geometry");
     const ConvGeom g = to_geom(gg);
     const int64_t na = g.in_elems(), nb = g.w_elems(), nz = g.out_elems();
@@ -1329,6 +1418,7 @@ extern "C" {
 
 mpc_status mpc_relu(mpc_ctx c, const uint64_t* x, uint64_t* out, int64_t n, uint64_t relu_id, uint64_t* sign_out) {
     CHECK(enter(c));
+    CHECK(need_ttp(c, "relu"));
     if (n < 0) return fail(c, MPC_ERR_SHAPE, "relu: n < 0");
     if (relu_id >> 32) return fail(c, MPC_ERR_ARG, "relu: relu_id must be < 2^32 (R24 gate ids)");
     if (c->all && c->P > 8) return fail(c, MPC_ERR_UNSUPPORTED, "relu: at most 8 parties on one device");

@@ -352,6 +352,9 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Wor
                      (reinterpret_cast<uintptr_t>(p.C) & 31) == 0 && (reinterpret_cast<uintptr_t>(p.partials) & 31) == 0;
     const uint64_t pol = evict_first_policy();
     const uint32_t tbase = tmem_base + ((uint32_t)(wq * 32) << 16) + half * 64;
+    // the epilogue reads C and writes Z: order it after the previous kernel (PDL) itself,
+    // not only through the producer -> MMA chain, which is empty when K == 0
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     uint32_t u = 0;
     for (int w = cluster_id(); w < wm.items(); w += nclusters()) {
         int party, m, n, klo, khi;

@@ -190,6 +190,9 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_small_kernel(const __gr
         }
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue
+        // reads C / writes Z: ordered after the previous kernel even when no K block
+        // (and so no producer wait) precedes the first tile end (K == 0)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         const int q = warp & 3;                                    // TMEM lane quadrant = plane i' (i = i' or 4 + i')
         const int h = (warp - 4) >> 2;                             // column half
         const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + h * 16;

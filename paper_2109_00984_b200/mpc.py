@@ -58,6 +58,14 @@ def _check_out(t: torch.Tensor, shape, dtype) -> torch.Tensor:
     return t
 
 
+def derive_keys(master_seed: int, world_size: int, rank: int) -> "_native.Keys":
+    """Party `rank`'s keys as mpc_create derives them from master_seed (mpc_derive_keys)."""
+    return _native.derive_keys(master_seed, world_size, rank)
+
+
+Keys = _native.Keys
+
+
 def nccl_unique_id() -> bytes:
     """128-byte ncclUniqueId from the native library's NCCL (rank 0 calls this)."""
     return _native.nccl_unique_id()
@@ -101,7 +109,10 @@ class Context:
 
     def __init__(self, world_size: int, rank: int = ALL_PARTIES, device: int = 0,
                  master_seed: int = 210900984, frac_bits: int = DEFAULT_FRAC_BITS,
-                 nccl_id: Optional[bytes] = None, group: Optional["Group"] = None):
+                 nccl_id: Optional[bytes] = None, group: Optional["Group"] = None,
+                 keys: Optional["_native.Keys"] = None):
+        """keys: explicit party keys (mpc_create_with_keys; one party per process) instead
+        of deriving every key from master_seed (mpc_create)."""
         self._lib = _native.lib()
         self.P = world_size
         self.rank = rank
@@ -113,7 +124,12 @@ class Context:
         if nccl_id is not None:
             idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
         self._group = group               # keeps the group alive while this party is attached
-        if group is not None:
+        if keys is not None:
+            if group is not None or rank == ALL_PARTIES:
+                raise ValueError("explicit keys: one party per process (no group, no ALL_PARTIES)")
+            st = self._lib.mpc_create_with_keys(ctypes.byref(h), world_size, rank, device, idbuf,
+                                                ctypes.byref(keys), frac_bits)
+        elif group is not None:
             if group.P != world_size:
                 raise ValueError(f"group of {group.P} parties, world_size {world_size}")
             st = self._lib.mpc_create_local(ctypes.byref(h), group._h, rank, device, ctypes.c_uint64(master_seed),
@@ -125,6 +141,7 @@ class Context:
             raise MpcError(st, "mpc_create failed (needs an sm_100 GPU; nccl_id for one party per GPU)")
         self._h = h
         self._ws = None
+        self._last_stream = None
 
     # ------------------------------------------------------------ plumbing
     def close(self):
@@ -139,7 +156,12 @@ class Context:
             pass
 
     def _call(self, fn, *args):
-        self._lib.mpc_set_stream(self._h, ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
+        cur = torch.cuda.current_stream(self.device)
+        if self._last_stream is not None and self._last_stream != cur:
+            # the workspace (and the library's scratch) were last used on another stream
+            cur.wait_stream(self._last_stream)
+        self._last_stream = cur
+        self._lib.mpc_set_stream(self._h, ctypes.c_void_p(cur.cuda_stream))
         st = fn(self._h, *args)
         if st != 0:
             raise MpcError(st, self._lib.mpc_last_error(self._h).decode())
@@ -217,11 +239,19 @@ class Context:
     def workspace_bytes(self, M: int, K: int, N: int) -> int:
         return int(self._lib.mpc_workspace_bytes(self._h, M, K, N))
 
+    def _check_operands(self, lead, M, K, N, x=None, y=None, a=None, b=None, c=None, z=None):
+        """Every operand of an M x K x N Beaver step has exactly its shape (the
+        library reads and writes through raw pointers)."""
+        for t, shp in ((x, (M, K)), (a, (M, K)), (y, (K, N)), (b, (K, N)), (c, (M, N)), (z, (M, N))):
+            if t is not None:
+                _check_out(t, lead + shp, t.dtype if t.dtype in (torch.uint64, torch.int64) else torch.uint64)
+
     def beaver_matmul(self, x, y, a, b, c, truncate: bool = True, wrap_id: int = 0,
                       out: Optional[torch.Tensor] = None) -> torch.Tensor:
         M, K = x.shape[-2], x.shape[-1]
         N = y.shape[-1]
         z = out if out is not None else _u64(self._lead() + (M, N), self.device)
+        self._check_operands(self._lead(), M, K, N, x, y, a, b, c, z)
         ws = self._workspace(self.workspace_bytes(M, K, N))
         self._call(self._lib.mpc_beaver_matmul, _ptr(x), _ptr(y), _ptr(a), _ptr(b), _ptr(c), _ptr(z),
                    ctypes.c_int64(M), ctypes.c_int64(K), ctypes.c_int64(N), int(bool(truncate)),
@@ -235,6 +265,7 @@ class Context:
         B, M, K = x.shape[-3], x.shape[-2], x.shape[-1]
         N = y.shape[-1]
         z = out if out is not None else _u64(self._lead() + (B, M, N), self.device)
+        self._check_operands(self._lead() + (B,), M, K, N, x, y, a, b, c, z)
         nb = int(self._lib.mpc_workspace_bytes_batched(self._h, B, M, K, N))
         ws = self._workspace(nb)
         self._call(self._lib.mpc_beaver_matmul_batched, ctypes.c_int64(B), _ptr(x), _ptr(y), _ptr(a), _ptr(b),
@@ -247,6 +278,7 @@ class Context:
         reveal + splits, mpc_beaver_prepare); returns the prepared operand, whose
         own workspace feeds beaver_matmul_prepared (`out`: reuse its workspace)."""
         K, N = y.shape[-2], y.shape[-1]
+        self._check_operands(self._lead(), M, K, N, y=y, b=b)
         if out is not None:
             if (out.M, out.K, out.N) != (M, K, N):
                 raise ValueError("prepared operand of another shape")
@@ -264,6 +296,7 @@ class Context:
         if x.shape[-2:] != (M, K):
             raise ValueError(f"x {tuple(x.shape)} does not match the prepared {M} x {K}")
         z = out if out is not None else _u64(self._lead() + (M, N), self.device)
+        self._check_operands(self._lead(), M, K, N, x=x, a=a, c=c, z=z)
         self._call(self._lib.mpc_beaver_matmul_prepared, _ptr(x), _ptr(a), _ptr(c), _ptr(z), ctypes.c_int64(M),
                    ctypes.c_int64(K), ctypes.c_int64(N), int(bool(truncate)), ctypes.c_uint64(wrap_id),
                    _ptr(prep.ws), ctypes.c_size_t(prep.ws.numel()))
@@ -273,6 +306,7 @@ class Context:
         """One-party context: [x - a | y - b] (to be revealed by the caller, one round)."""
         M, K = x.shape[-2], x.shape[-1]
         N = y.shape[-1]
+        self._check_operands((), M, K, N, x, y, a, b)
         ed = _u64((M * K + K * N,), self.device)
         self._call(self._lib.mpc_beaver_mask, _ptr(x), _ptr(y), _ptr(a), _ptr(b), _ptr(ed),
                    ctypes.c_int64(M), ctypes.c_int64(K), ctypes.c_int64(N))
@@ -283,6 +317,8 @@ class Context:
         M, K = a.shape[-2], a.shape[-1]
         N = b.shape[-1]
         z = out if out is not None else _u64((M, N), self.device)
+        self._check_operands((), M, K, N, a=a, b=b, c=c, z=z)
+        _check_out(ed, (M * K + K * N,), ed.dtype)
         ws = self._workspace(self.workspace_bytes(M, K, N))
         self._call(self._lib.mpc_beaver_finish, _ptr(ed), _ptr(a), _ptr(b), _ptr(c), _ptr(z), ctypes.c_int64(M),
                    ctypes.c_int64(K), ctypes.c_int64(N), int(bool(truncate)), _ptr(ws), ctypes.c_size_t(ws.numel()))
@@ -420,6 +456,16 @@ class Context:
         n = x[0].numel() if self.all_parties else x.numel()
         self._call(self._lib.mpc_truncate, _ptr(x), ctypes.c_int64(n), int(bits or self.frac_bits),
                    ctypes.c_uint64(wrap_id))
+        return x
+
+    def truncate_pairs(self, x: torch.Tensor, r: torch.Tensor, theta_r: torch.Tensor,
+                       bits: Optional[int] = None) -> torch.Tensor:
+        """In place with a wrap pair from ttp_wrap_pairs (mpc_truncate_pairs); returns x."""
+        n = x[0].numel() if self.all_parties else x.numel()
+        for t in (r, theta_r):
+            _check_out(t, self._lead() + (n,), torch.uint64)
+        self._call(self._lib.mpc_truncate_pairs, _ptr(x), ctypes.c_int64(n), int(bits or self.frac_bits),
+                   _ptr(r), _ptr(theta_r))
         return x
 
     def ring_matmul(self, A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:

@@ -68,3 +68,29 @@ def test_null_context_is_rejected(libpath):
     assert L.mpc_share(None, None, 0, 0, None, 0) == 1
     assert L.mpc_beaver_matmul(None, None, None, None, None, None, None, 1, 1, 1, 0, 0, None, 0) == 1
     assert L.mpc_last_error(None) == b"null context"
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_derive_keys_matches_the_convention(libpath, P):
+    """mpc_derive_keys (host only) returns party p's PRZS pair (k_p, k_{p-1}) and
+    k_ttp exactly as the frozen R5 convention (pinned in tests/golden/prg_frozen.txt
+    through the oracle's derivation)."""
+    import oracle
+    from paper_2109_00984_b200 import _native
+    kp, kt = oracle.derive_keys(210900984, P)
+    for r in range(P):
+        k = _native.derive_keys(210900984, P, r)
+        assert (k.przs_self, k.przs_prev, k.ttp, k.has_ttp) == (int(kp[r]), int(kp[(r - 1) % P]), int(kt), 1)
+    with pytest.raises(ValueError):
+        _native.derive_keys(1, P, P)
+
+
+def test_create_with_keys_rejects_bad_arguments(libpath):
+    from paper_2109_00984_b200 import _native
+    L = _native.lib()
+    h = ctypes.c_void_p()
+    k = _native.Keys(1, 2, 3, 1)
+    assert L.mpc_create_with_keys(ctypes.byref(h), 2, -1, 0, None, ctypes.byref(k), 16) == 1   # ALL_PARTIES
+    assert L.mpc_create_with_keys(ctypes.byref(h), 2, 0, 0, None, None, 16) == 1               # no keys
+    assert L.mpc_create_with_keys(ctypes.byref(h), 1, 0, 0, None, ctypes.byref(k), 16) == 1    # P=1, self != prev
+    assert not h.value

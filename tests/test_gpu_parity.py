@@ -324,6 +324,23 @@ def test_c2_4096_sampled_rows_and_identity(mpc):
             Bj = ((Yt >> (16 * j)) & 0xFFFF).double()
             ref += (Ai @ Bj).long() << (16 * (i + j))
     assert torch.equal(zsum, ref)
+    # truncation on the whole matrix: the GPU's fused epilogue truncation equals the
+    # oracle's local truncation of the identity-checked raw shares, and its
+    # failure events (theta_x != 0) number as the paper predicts
+    ez_all, dg = oracle.truncate(z_raw, 16, diagnostics=True)
+    assert np.array_equal(z, ez_all)
+    ev = dg["theta"] != 0
+    zabs = np.abs(oracle.reveal(z_raw).view(np.int64).astype(np.float64))
+    p = zabs / 2.0 ** 64
+    mean, sd = p.sum(), (p * (1 - p)).sum() ** 0.5
+    cnt = int(ev.sum())
+    assert abs(cnt - mean) <= 6 * sd + 1, (cnt, mean)
+    exact = (Xt.double() @ Yt.double()).cpu().numpy() / 2.0 ** 32      # exact: K * 2^38 < 2^53
+    got = oracle.decode(oracle.reveal(z))
+    err = np.abs(got - exact)
+    assert np.all(err[~ev] <= 2.0 ** -14)
+    assert np.all(err[ev] > 1.0)
+    print(f"4096^3 P=2: {cnt} truncation failure events, expected {mean:.2f} +- {sd:.2f}")
 
 
 # ------------------------------------------------------------------ prepared (y side ahead)
