@@ -143,8 +143,8 @@ def test_c5_8192_rows_identity_and_events(mpc, P):
     rows = np.sort(rng.choice(np.arange(1, M - 1), 1, replace=False))
     rows = np.concatenate([[0], rows, [M - 1]]).astype(np.int64)
     ridx = torch.from_numpy(rows).cuda()
-    zr_rows = host(z_raw[:, ridx].contiguous())
-    z_rows = host(z[:, ridx].contiguous())
+    zr_rows = host(z_raw.view(torch.int64)[:, ridx].contiguous().view(torch.uint64))
+    z_rows = host(z.view(torch.int64)[:, ridx].contiguous().view(torch.uint64))
     # oracle: full rows from the rows of x, a and all of y, b
     xs = np.stack([oracle.share(P, MASTER, X[r], 0, 1, start=int(r) * K) for r in rows], axis=1)
     ys = oracle.share(P, MASTER, Y, 1, 2)
