@@ -111,6 +111,13 @@ mpc_status mpc_create_with_keys(mpc_ctx* out, int world_size, int rank, int devi
                                 const void* nccl_id, const mpc_keys* keys, int frac_bits);
 mpc_status mpc_destroy(mpc_ctx ctx);
 mpc_status mpc_set_stream(mpc_ctx ctx, void* cuda_stream);
+/* One party per GPU: the eps reveal of mpc_beaver_matmul runs in `chunks` row chunks
+ * (whole 256-row GEMM tiles), each followed by its share of the GEMM terms that need
+ * no delta, while the later chunks and delta are still in flight.
+ * chunks in [1, 8], 0 = the default policy (min(4, M / 1024)); capped by the number of
+ * row tiles; ignored (1) for the transposed / stacked-plane GEMM orientations and
+ * batches.  Shares are bit-identical for every chunk count.  MPC_ERR_ARG outside [0, 8]. */
+mpc_status mpc_set_reveal_chunks(mpc_ctx ctx, int chunks);
 const char* mpc_last_error(mpc_ctx ctx);      /* never NULL; valid until the next call on ctx */
 /* rounds and bytes SENT by this process's party/parties since creation (R19) */
 mpc_status mpc_stats(mpc_ctx ctx, uint64_t* rounds, uint64_t* bytes_sent);

@@ -29,6 +29,7 @@ SIGNATURES = [
     ("mpc_create_with_keys", _I, [ctypes.POINTER(_V), _I, _I, _I, _V, ctypes.POINTER(Keys), _I]),
     ("mpc_destroy", _I, [_V]),
     ("mpc_set_stream", _I, [_V, _V]),
+    ("mpc_set_reveal_chunks", _I, [_V, _I]),
     ("mpc_last_error", ctypes.c_char_p, [_V]),
     ("mpc_stats", _I, [_V, ctypes.POINTER(_U), ctypes.POINTER(_U)]),
     ("mpc_world_size", _I, [_V]),

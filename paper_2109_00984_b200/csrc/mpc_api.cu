@@ -43,6 +43,8 @@ struct mpc_ctx_s {
     uint64_t* check_buf = nullptr;          // 2 words
     cudaStream_t comm_stream = nullptr;     // reveals of the overlapped Beaver schedule
     cudaEvent_t ev_mask = nullptr, ev_delta = nullptr, ev_eps = nullptr;
+    cudaEvent_t ev_chunk[8] = {};           // eps row chunks of the overlapped schedule (created on first use)
+    int reveal_chunks = 0;                  // mpc_set_reveal_chunks (0: default policy)
     bool broken = false;
     std::string err;
     uint64_t rounds = 0, bytes = 0, launches = 0;
@@ -273,6 +275,29 @@ struct BeaverWs {
     size_t total;
 };
 
+// Row chunks of the eps reveal in the overlapped schedule: eps is
+// M x K row-major, so a chunk of rows is contiguous in the reveal buffer, its
+// limb planes are a contiguous run of 128-row blocks and its GEMM output rows a
+// contiguous run of z.  Chunks are whole 256-row GEMM tiles with at least 1024
+// rows (enough tiles per chunk GEMM to fill the SMs the reveal leaves); not for
+// the transposed / stacked-plane GEMMs (small M: the eps reveal is small too).
+// mpc_set_reveal_chunks / MPC_REVEAL_CHUNKS=c force c chunks where the shape allows.
+constexpr int kMaxRevealChunks = 8;
+int reveal_chunks(mpc_ctx ctx, const BeaverWs& w, int64_t M) {
+    if (w.swap || w.small || w.batch > 1) return 1;
+    static const int env = getenv("MPC_REVEAL_CHUNKS") ? atoi(getenv("MPC_REVEAL_CHUNKS")) : 0;
+    const int64_t tiles = (M + 255) / 256;
+    int c = ctx->reveal_chunks > 0 ? ctx->reveal_chunks : env > 0 ? env : (int)std::min<int64_t>(4, M / 1024);
+    c = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)c, (int64_t)kMaxRevealChunks, tiles}));
+    return c;
+}
+// rows [m0, m1) of chunk i of c: whole 256-row tiles, spread evenly
+inline void chunk_rows(int64_t M, int i, int c, int64_t& m0, int64_t& m1) {
+    const int64_t tiles = (M + 255) / 256;
+    m0 = std::min<int64_t>(M, tiles * i / c * 256);
+    m1 = std::min<int64_t>(M, tiles * (i + 1) / c * 256);
+}
+
 // ed_elems: size of the one-party [e | d] reveal buffer (default M*K + K*N; a
 // convolution reveals at the input / weight shapes instead).  allow_swap: the
 // transposed GEMM is possible for this output layout.
@@ -304,9 +329,16 @@ BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N, int6
     w.zbuf = reinterpret_cast<uint64_t*>(alg1_one ? cv.take(8 * (size_t)(B * M * N)) : nullptr);
     w.hbuf = reinterpret_cast<int8_t*>(alg1_one ? cv.take((size_t)(B * M * N)) : nullptr);
     size_t pb = ring_gemm_partials_bytes(inst, gM, gN, 2 * (int)num_kb(K), 0, w.small);
-    if (!c->all)   // the overlapped schedule runs two half-K GEMMs, the first on fewer SMs
+    if (!c->all) {   // the overlapped schedule runs half-K GEMMs: phase 1 per eps row chunk on fewer SMs
         pb = std::max({pb, ring_gemm_partials_bytes(1, gM, gN, (int)num_kb(K), kOverlapClusters, w.small),
                        ring_gemm_partials_bytes(1, gM, gN, (int)num_kb(K), 0, w.small)});
+        const int nch = reveal_chunks(c, w, M);
+        for (int i = 0; i < nch && nch > 1; ++i) {
+            int64_t m0, m1;
+            chunk_rows(M, i, nch, m0, m1);
+            pb = std::max(pb, ring_gemm_partials_bytes(1, m1 - m0, N, (int)num_kb(K), kOverlapClusters, false));
+        }
+    }
     w.partials = reinterpret_cast<uint64_t*>(pb ? cv.take(pb) : nullptr);
     w.total = cv.off;
     return w;
@@ -336,42 +368,67 @@ mpc_status beaver_gemm(mpc_ctx c, const BeaverWs& w, const uint64_t* cc, uint64_
                        int64_t N, int truncate);
 
 // One party per GPU with a communicator: the reveal overlaps the GEMM terms
-// that do not need it.  Comm stream: delta is revealed first,
-// then eps.  Compute stream: a_p's limb planes are split while delta is in
-// flight; phase 1, z = c_p + a_p @ delta, runs on the SMs NCCL leaves free
-// while eps is revealed; phase 2 adds eps @ (b_p + [p = 0] delta) and
-// truncates.  Bit-identical to the fused single-GEMM schedule (ring addition).
+// that do not need all of it.  Comm stream: eps is revealed
+// first, in row chunks, then delta.  Compute stream: b_p's limb planes (and a_p's,
+// p != 0) are split while eps chunk 0 is in flight; for each eps chunk, its planes
+// (and, for party 0, those of a'_0 = a_0 + eps on the same rows: the public
+// eps@delta folded into party 0's left operand, R7/R8) are split and phase 1,
+// z[rows] = c_p[rows] + eps[rows] @ b_p, runs on the SMs NCCL leaves free while
+// the next chunks and delta are revealed; then delta is split and phase 2 adds
+// a'_p @ delta and truncates.  Exposed communication: the first eps chunk.
+// Bit-identical to the fused single-GEMM schedule (ring addition commutes).
 mpc_status beaver_overlapped(mpc_ctx c, const BeaverWs& w, const uint64_t* x, const uint64_t* y, const uint64_t* a,
                              const uint64_t* b, const uint64_t* cc, uint64_t* z, int64_t M, int64_t K, int64_t N,
                              int truncate) {
     const int64_t sMK = M * K, sKN = K * N;
+    const int nch = reveal_chunks(c, w, M);
+    for (int i = 0; i < nch; ++i)
+        if (!c->ev_chunk[i] && cudaEventCreateWithFlags(&c->ev_chunk[i], cudaEventDisableTiming) != cudaSuccess)
+            return fail(c, MPC_ERR_CUDA, "beaver: chunk event");
     CHECK(run(c, kClsSplit, "mask", [&] { return launch_mask(x, a, sMK, y, b, sKN, w.ed, c->stream); }));
     cudaEventRecord(c->ev_mask, c->stream);
     cudaStreamWaitEvent(c->comm_stream, c->ev_mask, 0);
+    for (int i = 0; i < nch; ++i) {
+        int64_t m0, m1;
+        chunk_rows(M, i, nch, m0, m1);
+        CHECK(comm_allreduce(c, w.ed + m0 * K, w.ed + m0 * K, (size_t)((m1 - m0) * K), RedOp::SumU64, "eps reveal",
+                             c->comm_stream));
+        cudaEventRecord(c->ev_chunk[i], c->comm_stream);
+    }
     CHECK(comm_allreduce(c, w.ed + sMK, w.ed + sMK, (size_t)sKN, RedOp::SumU64, "delta reveal", c->comm_stream));
     cudaEventRecord(c->ev_delta, c->comm_stream);
-    CHECK(comm_allreduce(c, w.ed, w.ed, (size_t)sMK, RedOp::SumU64, "eps reveal", c->comm_stream));
-    cudaEventRecord(c->ev_eps, c->comm_stream);
-    // a_p planes need no reveal
+    // planes that need no reveal: b_p (all parties), a_p (p != 0)
+    RightSplitArgs Rb{K, N, 0, nullptr, nullptr, 0, nullptr, b, 1, 0, w.b_pl, 0, lay(w)};
     LeftSplitArgs La{M, K, 0, nullptr, nullptr, 0, nullptr, a, 1, w.a_pl, 0, lay(w)};
-    CHECK(run(c, kClsSplit, "split a", [&] { return launch_split_left(La, c->stream); }));
+    if (c->rank != 0) CHECK(run(c, kClsSplit, "split a/b", [&] { return launch_split_both(La, Rb, c->stream); }));
+    else CHECK(run(c, kClsSplit, "split b", [&] { return launch_split_right(Rb, c->stream); }));
+    // per eps chunk of rows of a 256-row-tile grid: Layout::Left blocks of 128 rows
+    const int64_t lblk = (int64_t)num_kb(K) * 8 * PlaneGeom<Layout::Left>::kBlock;     // bytes per 128-row block
+    for (int i = 0; i < nch; ++i) {
+        int64_t m0, m1;
+        chunk_rows(M, i, nch, m0, m1);
+        const int64_t mc = m1 - m0;
+        const int64_t pl_off = nch > 1 ? (m0 / 128) * lblk : 0;
+        cudaStreamWaitEvent(c->stream, c->ev_chunk[i], 0);
+        LeftSplitArgs Le{mc, K, 0, w.ed + m0 * K, nullptr, 1, w.eps_pl + pl_off,
+                         c->rank == 0 ? a + m0 * K : nullptr, c->rank == 0 ? 1 : 0,
+                         c->rank == 0 ? w.a_pl + pl_off : nullptr, 0, lay(w), c->rank == 0 ? 1 : 0};
+        CHECK(run(c, kClsSplit, "split eps", [&] { return launch_split_left(Le, c->stream); }));
+        RingGemmParams p1{};
+        p1.seg[0] = seg_of(w, w.eps_pl + pl_off, 0, w.b_pl, 0, (int)num_kb(K));        // eps @ b_p
+        p1.nseg = 1;
+        set_out(p1, w, mc, N);
+        p1.C = cc + m0 * N; p1.Z = z + m0 * N;
+        p1.trunc_bits = 0;
+        p1.partials = w.partials;
+        p1.max_clusters = kOverlapClusters;
+        CHECK(gemm_run(c, p1, 1));
+    }
     cudaStreamWaitEvent(c->stream, c->ev_delta, 0);
-    RightSplitArgs R{K, N, 0, w.ed + sMK, nullptr, 1, w.delta_pl, b, 1, c->rank == 0, w.b_pl, 0, lay(w)};
-    CHECK(run(c, kClsSplit, "split delta", [&] { return launch_split_right(R, c->stream); }));
-    RingGemmParams p1{};
-    p1.seg[0] = seg_of(w, w.a_pl, 0, w.delta_pl, 0, (int)num_kb(K));           // a_p @ delta
-    p1.nseg = 1;
-    set_out(p1, w, M, N);
-    p1.C = cc; p1.Z = z;
-    p1.trunc_bits = 0;
-    p1.partials = w.partials;
-    p1.max_clusters = kOverlapClusters;
-    CHECK(gemm_run(c, p1, 1));
-    cudaStreamWaitEvent(c->stream, c->ev_eps, 0);
-    LeftSplitArgs Le{M, K, 0, w.ed, nullptr, 1, w.eps_pl, nullptr, 0, nullptr, 0, lay(w)};
-    CHECK(run(c, kClsSplit, "split eps", [&] { return launch_split_left(Le, c->stream); }));
+    RightSplitArgs Rd{K, N, 0, w.ed + sMK, nullptr, 1, w.delta_pl, nullptr, 0, 0, nullptr, 0, lay(w)};
+    CHECK(run(c, kClsSplit, "split delta", [&] { return launch_split_right(Rd, c->stream); }));
     RingGemmParams p2{};
-    p2.seg[0] = seg_of(w, w.eps_pl, 0, w.b_pl, 0, (int)num_kb(K));             // eps @ b'_p
+    p2.seg[0] = seg_of(w, w.a_pl, 0, w.delta_pl, 0, (int)num_kb(K));              // a'_p @ delta
     p2.nseg = 1;
     set_out(p2, w, M, N);
     p2.C = z; p2.Z = z;                                                         // z += ..., in place
@@ -585,12 +642,19 @@ mpc_status mpc_destroy(mpc_ctx c) {
     if (c->check_buf) cudaFree(c->check_buf);
     if (c->comm_stream) { cudaStreamSynchronize(c->comm_stream); cudaStreamDestroy(c->comm_stream); }
     for (cudaEvent_t e : {c->ev_mask, c->ev_delta, c->ev_eps}) if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ev_chunk) if (e) cudaEventDestroy(e);
     for (auto& e : c->pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     for (auto e : c->pool) cudaEventDestroy(e);
     if (c->d_err) cudaFree(c->d_err);
     if (c->scratch) cudaFree(c->scratch);
     if (c->scratch_ev) cudaEventDestroy(c->scratch_ev);
     delete c;
+    return MPC_OK;
+}
+
+mpc_status mpc_set_reveal_chunks(mpc_ctx c, int chunks) {
+    if (!c || chunks < 0 || chunks > 8) return MPC_ERR_ARG;
+    c->reveal_chunks = chunks;
     return MPC_OK;
 }
 

@@ -236,6 +236,10 @@ class Context:
         return r, th
 
     # ------------------------------------------------------------ online
+    def set_reveal_chunks(self, chunks: int) -> None:
+        """Row chunks of the overlapped eps reveal (one party per GPU; 0 = default policy)."""
+        self._call(self._lib.mpc_set_reveal_chunks, int(chunks))
+
     def workspace_bytes(self, M: int, K: int, N: int) -> int:
         return int(self._lib.mpc_workspace_bytes(self._h, M, K, N))
 

@@ -29,3 +29,19 @@ def test_torchrun_two_ranks_one_json_line():
     assert d["check"]["max_abs_err_sampled_rows"] <= 2.0 ** -14
     assert d["e2e"]["max_abs_err_sampled_rows"] <= 2.0 ** -14
     assert d["gpu_launches"] > 0 and "exposed_comm" in d
+    chk = d["check"]["bit_exact_vs_oracle"]          # the timed shares of session 0, gathered to rank 0
+    assert chk["bit_exact"] and chk["outputs_per_party"] == 2 * 128
+
+
+def test_multiparty_emulation_matches_oracle():
+    """bench_multiparty's per-party code (the N-GPU schedule: chunked eps reveal,
+    offline wrap pairs, Alg. 1 over u64 + int8 reveals) for P parties as threads on
+    one GPU, at a small size, bit-exact on its seeded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "scripts"))
+    import bench_multiparty as bmp
+    for P, n in ((2, 1024), (3, 1100), (5, 640)):
+        out = bmp.run_local_group(P, n, n // 2, n + 64, steps=2, warmup=1, chunks=3)
+        assert out["check"]["bit_exact"], (P, n)
+        assert out["rounds_per_step"] == (2 if P > 2 else 1)
+    base = bmp.per_gpu_baseline(512, 512, 512, steps=2)
+    assert base["ms_per_private_matmul"] > 0
