@@ -347,6 +347,9 @@ mpc_status mpc_reveal_batch(mpc_ctx ctx, int count, const uint64_t* const* share
  *   ed = [eps | delta] (na + nb u64, formed by mpc_mask); one-party contexts; local
  *   truncation only.
  * mpc_mask: ed = [x - a | y - b] for any n1, n2 (0 rounds).
+ * 1-D convolutions (Wav2Letter): the H = kh = 1 case, ph = 0, sh = 1 —
+ * x (B, C, L) and w (Cout, C, k) have exactly the memory layout of (B, C, 1, L) and
+ * (Cout, C, 1, k), so every entry point below serves them unchanged.
  * Errors: MPC_ERR_SHAPE (invalid geometry / workspace), MPC_ERR_ARG (null pointer). */
 typedef struct {
     int64_t B, C, H, W, Cout, kh, kw, sh, sw, ph, pw;

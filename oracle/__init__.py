@@ -351,6 +351,12 @@ def conv_geom(B, C, H, W, Cout, kh, kw, stride=1, padding=0):
     return _ConvGeom(B, C, H, W, Cout, kh, kw, sh, sw, ph, pw)
 
 
+def conv1d_geom(B, C, L, Cout, k, stride=1, padding=0):
+    """A 1-D convolution (Wav2Letter) as the H = kh = 1 case of the 2-D
+    geometry: x (B, C, L) = (B, C, 1, L), w (Cout, C, k) = (Cout, C, 1, k)."""
+    return conv_geom(B, C, 1, L, Cout, 1, k, (1, stride), (0, padding))
+
+
 def conv_out_shape(g):
     return (g.B, g.Cout, (g.H + 2 * g.ph - g.kh) // g.sh + 1, (g.W + 2 * g.pw - g.kw) // g.sw + 1)
 

@@ -47,6 +47,32 @@ __host__ __device__ __forceinline__ void philox_pair(uint64_t key, uint64_t stre
     e1 = ((uint64_t)c3 << 32) | c2;
 }
 
+// The same generator with its 10 round keys precomputed on the host and passed by
+// value as a kernel parameter: the rounds then read them straight from the
+// constant bank (LOP3 operands), so a Philox block costs its 20 multiplies and 20
+// three-input XORs and no key-schedule adds — for kernels that expand many
+// streams under one key (Alg. 1, the wrap pairs, sharing).
+struct PhiloxRK { uint32_t k[20]; };
+inline PhiloxRK philox_round_keys(uint64_t key) {
+    PhiloxRK rk;
+    uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+    for (int r = 0; r < 10; ++r) { rk.k[2 * r] = k0; rk.k[2 * r + 1] = k1; k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    return rk;
+}
+__device__ __forceinline__ void philox_pair_rk(const PhiloxRK& rk, uint64_t stream, uint64_t j, uint64_t& e0,
+                                               uint64_t& e1) {
+    uint32_t c0 = (uint32_t)j, c1 = (uint32_t)(j >> 32), c2 = (uint32_t)stream, c3 = (uint32_t)(stream >> 32);
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+        const uint32_t n0 = hi1 ^ c1 ^ rk.k[2 * r], n2 = hi0 ^ c3 ^ rk.k[2 * r + 1];
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    }
+    e0 = ((uint64_t)c1 << 32) | c0;
+    e1 = ((uint64_t)c3 << 32) | c2;
+}
+
 __host__ __device__ __forceinline__ uint64_t philox_at(uint64_t key, uint64_t stream, uint64_t i) {
     uint64_t e0, e1;
     philox_pair(key, stream, i >> 1, e0, e1);

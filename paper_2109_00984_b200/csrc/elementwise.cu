@@ -46,31 +46,89 @@ cudaError_t launch_decode(const uint64_t* v, double* out, int64_t n, int frac_bi
 
 // ------------------------------------------------------------------ a2 share
 // [x]_p = G(k_p, s)[i] - G(k_{p-1}, s)[i] + [p == src] x[i]   (R4)
-// One thread per element pair (one Philox call yields two elements).
-__global__ void share_kernel(KeySet keys, int P, int party_lo, int party_hi, const uint64_t* __restrict__ x, int src,
-                             uint64_t stream, uint64_t* __restrict__ out, int64_t n) {
+// One thread per element pair (one Philox block yields two elements), round keys
+// precomputed on the host (philox_pair_rk).  All parties: every stream G(k_q) is
+// expanded ONCE — party q's own block is party q+1's neighbour block, and party 0's
+// neighbour k_{P-1} closes the ring (P blocks for P parties); P is a template
+// constant so each party's round keys are constant-bank operands.  One party:
+// its own and its neighbour's stream.  16-byte loads / stores when n is even and
+// the buffers are aligned.
+struct ShareRK { PhiloxRK k[kMaxParties]; };
+__device__ __forceinline__ void ld2(const uint64_t* __restrict__ p, int64_t i0, bool vec, bool has1, uint64_t (&o)[2]) {
+    if (vec) { const ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(p + i0)); o[0] = t.x; o[1] = t.y; }
+    else { o[0] = p[i0]; o[1] = has1 ? p[i0 + 1] : 0ull; }
+}
+__device__ __forceinline__ void st2(uint64_t* __restrict__ p, int64_t i0, bool vec, bool has1, uint64_t v0, uint64_t v1) {
+    if (vec) *reinterpret_cast<ulonglong2*>(p + i0) = make_ulonglong2(v0, v1);
+    else { p[i0] = v0; if (has1) p[i0 + 1] = v1; }
+}
+template <int P>
+__global__ void __launch_bounds__(256) share_all_kernel(const ShareRK rk, const uint64_t* __restrict__ x, int src,
+                                                        uint64_t stream, uint64_t* __restrict__ out, int64_t n) {
     const int64_t npairs = (n + 1) / 2;
+    const bool vec = (n & 1) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+                     (!x || (reinterpret_cast<uintptr_t>(x) & 15) == 0);
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npairs; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i0 = 2 * j;
         const bool has1 = i0 + 1 < n;
-        uint64_t g0, g1, h0, h1;
-        // previous neighbour of the first party computed
-        philox_pair(keys.k[(party_lo + P - 1) % P], stream, (uint64_t)j, h0, h1);
-        for (int p = party_lo; p < party_hi; ++p) {
-            philox_pair(keys.k[p], stream, (uint64_t)j, g0, g1);
-            uint64_t v0 = g0 - h0, v1 = g1 - h1;
-            if (p == src && x) { v0 += x[i0]; if (has1) v1 += x[i0 + 1]; }
-            uint64_t* o = out + (int64_t)(p - party_lo) * n;
-            o[i0] = v0;
-            if (has1) o[i0 + 1] = v1;
-            h0 = g0; h1 = g1;
+        uint64_t xv[2] = {0, 0};
+        if (x) ld2(x, i0, vec, has1, xv);
+        uint64_t g[2], first[2], prev[2];
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            philox_pair_rk(rk.k[q], stream, (uint64_t)j, g[0], g[1]);
+            if (q == 0) { first[0] = g[0]; first[1] = g[1]; }
+            else {
+                const uint64_t add = q == src ? 1ull : 0ull;
+                st2(out + (int64_t)q * n, i0, vec, has1, g[0] - prev[0] + add * xv[0], g[1] - prev[1] + add * xv[1]);
+            }
+            prev[0] = g[0]; prev[1] = g[1];
         }
+        const uint64_t add0 = src == 0 ? 1ull : 0ull;            // party 0: G(k_0) - G(k_{P-1})
+        st2(out, i0, vec, has1, first[0] - prev[0] + add0 * xv[0], first[1] - prev[1] + add0 * xv[1]);
+    }
+}
+__global__ void __launch_bounds__(256) share_one_kernel(const PhiloxRK self, const PhiloxRK prev, int is_src,
+                                                        const uint64_t* __restrict__ x, uint64_t stream,
+                                                        uint64_t* __restrict__ out, int64_t n) {
+    const int64_t npairs = (n + 1) / 2;
+    const bool vec = (n & 1) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+                     (!x || (reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npairs; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i0 = 2 * j;
+        const bool has1 = i0 + 1 < n;
+        uint64_t xv[2] = {0, 0}, g[2], h[2];
+        if (is_src && x) ld2(x, i0, vec, has1, xv);
+        philox_pair_rk(self, stream, (uint64_t)j, g[0], g[1]);
+        philox_pair_rk(prev, stream, (uint64_t)j, h[0], h[1]);
+        st2(out, i0, vec, has1, g[0] - h[0] + xv[0], g[1] - h[1] + xv[1]);
     }
 }
 cudaError_t launch_share(const KeySet& keys, int P, int party_lo, int party_hi, const uint64_t* x, int src,
                          uint64_t stream, uint64_t* out, int64_t n, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    share_kernel<<<grid_for((n + 1) / 2), 256, 0, st>>>(keys, P, party_lo, party_hi, x, src, stream, out, n);
+    const unsigned g = grid_for((n + 1) / 2);
+    if (party_hi - party_lo == 1 || P == 1) {
+        // one party (or P = 1, where [x]_0 = G(k_0) - G(k_0) + x = x)
+        for (int p = party_lo; p < party_hi; ++p) {
+            share_one_kernel<<<g, 256, 0, st>>>(philox_round_keys(keys.k[p]),
+                                                philox_round_keys(keys.k[(p + P - 1) % P]), p == src ? 1 : 0,
+                                                p == src ? x : nullptr, stream, out + (int64_t)(p - party_lo) * n, n);
+        }
+        return cudaGetLastError();
+    }
+    if (party_lo != 0 || party_hi != P) return cudaErrorInvalidValue;
+    ShareRK rk;
+    for (int q = 0; q < P; ++q) rk.k[q] = philox_round_keys(keys.k[q]);
+    const uint64_t* xs = (src >= 0 && src < P) ? x : nullptr;
+    switch (P) {
+#define MPC_SHARE_CASE(Q) case Q: share_all_kernel<Q><<<g, 256, 0, st>>>(rk, xs, src, stream, out, n); break;
+        MPC_SHARE_CASE(2) MPC_SHARE_CASE(3) MPC_SHARE_CASE(4) MPC_SHARE_CASE(5) MPC_SHARE_CASE(6) MPC_SHARE_CASE(7)
+        MPC_SHARE_CASE(8) MPC_SHARE_CASE(9) MPC_SHARE_CASE(10) MPC_SHARE_CASE(11) MPC_SHARE_CASE(12)
+        MPC_SHARE_CASE(13) MPC_SHARE_CASE(14) MPC_SHARE_CASE(15) MPC_SHARE_CASE(16)
+#undef MPC_SHARE_CASE
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 
@@ -585,12 +643,12 @@ __device__ __forceinline__ uint64_t wrap2(uint64_t u, uint64_t v) {
     return (uint64_t)(int64_t)(s >> 64);
 }
 // theta_r of pair j, exactly: (sum signed(r_q) - signed(sum r_q)) / 2^64 (the TTP's view)
-__device__ __forceinline__ void theta_r_pair(uint64_t key, uint64_t id, int P, uint64_t j, uint64_t (&t)[2]) {
+__device__ __forceinline__ void theta_r_pair(const PhiloxRK& rk, uint64_t id, int P, uint64_t j, uint64_t (&t)[2]) {
     __int128 s[2] = {0, 0};
     uint64_t u[2] = {0, 0};
     for (int q = 0; q < P; ++q) {
         uint64_t r[2];
-        philox_pair(key, stream_word(kTagR, (uint32_t)q, id), j, r[0], r[1]);
+        philox_pair_rk(rk, stream_word(kTagR, (uint32_t)q, id), j, r[0], r[1]);
 #pragma unroll
         for (int e = 0; e < 2; ++e) { s[e] += (__int128)(int64_t)r[e]; u[e] += r[e]; }
     }
@@ -598,16 +656,17 @@ __device__ __forceinline__ void theta_r_pair(uint64_t key, uint64_t id, int P, u
     for (int e = 0; e < 2; ++e) t[e] = (uint64_t)(int64_t)((s[e] - (__int128)(int64_t)u[e]) >> 64);
 }
 // [theta_r]_q of pair j: q >= 1 -> G(THETA||q||id), q = 0 -> theta_r - sum_{q>=1} (TTP view)
-__device__ __forceinline__ void theta_share_pair(uint64_t key, uint64_t id, int P, int q, uint64_t j, uint64_t (&t)[2]) {
-    if (q > 0) { philox_pair(key, stream_word(kTagTheta, (uint32_t)q, id), j, t[0], t[1]); return; }
-    theta_r_pair(key, id, P, j, t);
+__device__ __forceinline__ void theta_share_pair(const PhiloxRK& rk, uint64_t id, int P, int q, uint64_t j,
+                                                 uint64_t (&t)[2]) {
+    if (q > 0) { philox_pair_rk(rk, stream_word(kTagTheta, (uint32_t)q, id), j, t[0], t[1]); return; }
+    theta_r_pair(rk, id, P, j, t);
     for (int s = 1; s < P; ++s) {
         uint64_t v[2];
-        philox_pair(key, stream_word(kTagTheta, (uint32_t)s, id), j, v[0], v[1]);
+        philox_pair_rk(rk, stream_word(kTagTheta, (uint32_t)s, id), j, v[0], v[1]);
         t[0] -= v[0]; t[1] -= v[1];
     }
 }
-__global__ void wrap_pair_kernel(uint64_t key, uint64_t id, int P, int lo, int hi, uint64_t* __restrict__ r,
+__global__ void wrap_pair_kernel(const PhiloxRK rk, uint64_t id, int P, int lo, int hi, uint64_t* __restrict__ r,
                                  uint64_t* __restrict__ th, int64_t n) {
     const int64_t npairs = (n + 1) / 2;
     const bool vec = (n & 1) == 0 && aligned16(r) && aligned16(th);
@@ -616,8 +675,8 @@ __global__ void wrap_pair_kernel(uint64_t key, uint64_t id, int P, int lo, int h
         const bool has1 = i0 + 1 < n;
         for (int q = lo; q < hi; ++q) {
             uint64_t v[2], t[2];
-            philox_pair(key, stream_word(kTagR, (uint32_t)q, id), (uint64_t)j, v[0], v[1]);
-            theta_share_pair(key, id, P, q, (uint64_t)j, t);
+            philox_pair_rk(rk, stream_word(kTagR, (uint32_t)q, id), (uint64_t)j, v[0], v[1]);
+            theta_share_pair(rk, id, P, q, (uint64_t)j, t);
             st_pair(r + (int64_t)(q - lo) * n, i0, vec, has1, v);
             st_pair(th + (int64_t)(q - lo) * n, i0, vec, has1, t);
         }
@@ -626,7 +685,7 @@ __global__ void wrap_pair_kernel(uint64_t key, uint64_t id, int P, int lo, int h
 cudaError_t launch_wrap_pair(uint64_t key, uint64_t id, int P, int lo, int hi, uint64_t* r, uint64_t* th, int64_t n,
                              cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    wrap_pair_kernel<<<grid_for((n + 1) / 2), 256, 0, st>>>(key, id, P, lo, hi, r, th, n);
+    wrap_pair_kernel<<<grid_for((n + 1) / 2), 256, 0, st>>>(philox_round_keys(key), id, P, lo, hi, r, th, n);
     return cudaGetLastError();
 }
 
@@ -654,7 +713,7 @@ cudaError_t launch_trunc_local(uint64_t* x, int64_t n, int bits, cudaStream_t st
 // mpc_ttp_wrap_pairs).
 template <int P, bool PAIRS>
 __global__ void __launch_bounds__(256, (P <= 8 ? 2 : 1)) trunc_alg1_all_kernel(uint64_t* __restrict__ x, int64_t n, int bits,
-                                                            uint64_t key, uint64_t id, const uint64_t* __restrict__ rin,
+                                                            const PhiloxRK rk, uint64_t id, const uint64_t* __restrict__ rin,
                                                             const uint64_t* __restrict__ thin) {
     const int64_t npairs = (n + 1) / 2;
     const bool vec = (n & 1) == 0 && aligned16(x) && (!PAIRS || (aligned16(rin) && aligned16(thin)));
@@ -668,7 +727,7 @@ __global__ void __launch_bounds__(256, (P <= 8 ? 2 : 1)) trunc_alg1_all_kernel(u
         for (int q = 0; q < P; ++q) {
             ld_pair(x + (int64_t)q * n, i0, vec, has1, xv[q]);
             if (PAIRS) ld_pair(rin + (int64_t)q * n, i0, vec, has1, r[q]);
-            else philox_pair(key, stream_word(kTagR, (uint32_t)q, id), (uint64_t)j, r[q][0], r[q][1]);
+            else philox_pair_rk(rk, stream_word(kTagR, (uint32_t)q, id), (uint64_t)j, r[q][0], r[q][1]);
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const uint64_t z = xv[q][e] + r[q][e];                  // z_q = x_q + r_q
@@ -690,7 +749,7 @@ __global__ void __launch_bounds__(256, (P <= 8 ? 2 : 1)) trunc_alg1_all_kernel(u
             if (PAIRS) {
                 ld_pair(thin + (int64_t)q * n, i0, vec, has1, th);
             } else if (q > 0) {
-                philox_pair(key, stream_word(kTagTheta, (uint32_t)q, id), (uint64_t)j, th[0], th[1]);
+                philox_pair_rk(rk, stream_word(kTagTheta, (uint32_t)q, id), (uint64_t)j, th[0], th[1]);
                 th_sum[0] += th[0];
                 th_sum[1] += th[1];
             } else {
@@ -709,12 +768,106 @@ __global__ void __launch_bounds__(256, (P <= 8 ? 2 : 1)) trunc_alg1_all_kernel(u
         }
     }
 }
+// The same computation for bits <= 32 (the fixed-point truncation, f = 16) with
+// every wrap count in 32-bit arithmetic: theta_x * 2^(64 - bits) mod 2^64 depends
+// only on theta_x mod 2^bits, so theta_x, beta, theta_z, theta_r and the
+// [theta_r] shares are needed mod 2^32.  With m(v) = v >> 63 and C the carries of a
+// running unsigned sum, the wrap count of sum_q v_q is C - sum_q m(v_q) + m(sum), and
+// beta_q = carry(x_q + r_q) - m(x_q) - m(r_q) + m(z_q) — the exact integer identities
+// the int128 form evaluates, at a third of its ALU instructions (the kernel is
+// ALU-pipe bound: ncu, P = 8).  Pass 1 keeps only beta_q per party; pass 2 re-reads
+// x_q (L1) and needs no r_q.
+__device__ __forceinline__ uint32_t add_carry(uint64_t a, uint64_t b, uint64_t& s) {
+    uint32_t lo, hi, c;
+    asm("add.cc.u32 %0, %3, %5;\n\taddc.cc.u32 %1, %4, %6;\n\taddc.u32 %2, 0, 0;"
+        : "=r"(lo), "=r"(hi), "=r"(c)
+        : "r"((uint32_t)a), "r"((uint32_t)(a >> 32)), "r"((uint32_t)b), "r"((uint32_t)(b >> 32)));
+    s = ((uint64_t)hi << 32) | lo;
+    return c;
+}
+__device__ __forceinline__ void acc_carry(uint64_t& s, uint64_t v, uint32_t& cnt) {
+    uint32_t lo = (uint32_t)s, hi = (uint32_t)(s >> 32);
+    asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, 0;"
+        : "+r"(lo), "+r"(hi), "+r"(cnt) : "r"((uint32_t)v), "r"((uint32_t)(v >> 32)));
+    s = ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint32_t msb(uint64_t v) { return (uint32_t)(v >> 63); }
+
+template <int P, bool PAIRS>
+__global__ void __launch_bounds__(256, (P <= 8 ? 2 : 1)) trunc_alg1_all_w32_kernel(
+        uint64_t* __restrict__ x, int64_t n, int bits, const PhiloxRK rk, uint64_t id, const uint64_t* __restrict__ rin,
+        const uint64_t* __restrict__ thin) {
+    const int64_t npairs = (n + 1) / 2;
+    const bool vec = (n & 1) == 0 && aligned16(x) && (!PAIRS || (aligned16(rin) && aligned16(thin)));
+    const uint32_t hshift = 32 - bits;                                  // theta_x lands in the high word
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npairs; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i0 = 2 * j;
+        const bool has1 = i0 + 1 < n;
+        uint32_t beta[P][2];
+        uint64_t zsum[2] = {0, 0}, rsum[2] = {0, 0};
+        uint32_t cz[2] = {0, 0}, cr[2] = {0, 0};                        // carries minus msb counts
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            uint64_t xv[2], r[2];
+            ld_pair(x + (int64_t)q * n, i0, vec, has1, xv);
+            if (PAIRS) ld_pair(rin + (int64_t)q * n, i0, vec, has1, r);
+            else philox_pair_rk(rk, stream_word(kTagR, (uint32_t)q, id), (uint64_t)j, r[0], r[1]);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                uint64_t z;
+                const uint32_t c = add_carry(xv[e], r[e], z);                 // z_q = x_q + r_q
+                beta[q][e] = c - msb(xv[e]) - msb(r[e]) + msb(z);
+                acc_carry(zsum[e], z, cz[e]);
+                cz[e] -= msb(z);
+                if (!PAIRS) { acc_carry(rsum[e], r[e], cr[e]); cr[e] -= msb(r[e]); }
+            }
+        }
+        uint32_t theta_z[2], theta_r[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            theta_z[e] = cz[e] + msb(zsum[e]);                                // wraps of z
+            theta_r[e] = cr[e] + msb(rsum[e]);                                // wraps of r (seeded TTP)
+        }
+        uint32_t th_sum[2] = {0, 0};
+#pragma unroll
+        for (int q = P - 1; q >= 0; --q) {
+            uint32_t th[2];
+            if (PAIRS) {
+                uint64_t t[2];
+                ld_pair(thin + (int64_t)q * n, i0, vec, has1, t);
+                th[0] = (uint32_t)t[0]; th[1] = (uint32_t)t[1];
+            } else if (q > 0) {
+                uint64_t t[2];
+                philox_pair_rk(rk, stream_word(kTagTheta, (uint32_t)q, id), (uint64_t)j, t[0], t[1]);
+                th[0] = (uint32_t)t[0]; th[1] = (uint32_t)t[1];
+                th_sum[0] += th[0]; th_sum[1] += th[1];
+            } else {
+                th[0] = theta_r[0] - th_sum[0];
+                th[1] = theta_r[1] - th_sum[1];
+            }
+            uint64_t xv[2], o[2];
+            ld_pair(x + (int64_t)q * n, i0, vec, has1, xv);                   // L1 hit: loaded in pass 1
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const uint32_t theta_x = beta[q][e] - th[e] + (q == 0 ? theta_z[e] : 0u);
+                o[e] = div_pow2_round(xv[e], bits) - ((uint64_t)(theta_x << hshift) << 32);
+            }
+            st_pair(x + (int64_t)q * n, i0, vec, has1, o);
+        }
+    }
+}
+
 template <bool PAIRS>
 static cudaError_t launch_alg1_all_t(uint64_t* x, int P, int64_t n, int bits, uint64_t key, uint64_t id,
                                      const uint64_t* r, const uint64_t* th, cudaStream_t st) {
     const unsigned g = grid_for((n + 1) / 2, 256);
+    const PhiloxRK rk = philox_round_keys(key);
+    const bool w32 = bits <= 32 && !getenv("MPC_ALG1_INT128");        // A/B switch for measurements
     switch (P) {
-#define MPC_ALG1_CASE(Q) case Q: trunc_alg1_all_kernel<Q, PAIRS><<<g, 256, 0, st>>>(x, n, bits, key, id, r, th); break;
+#define MPC_ALG1_CASE(Q) case Q:                                                                         \
+        if (w32) trunc_alg1_all_w32_kernel<Q, PAIRS><<<g, 256, 0, st>>>(x, n, bits, rk, id, r, th);        \
+        else trunc_alg1_all_kernel<Q, PAIRS><<<g, 256, 0, st>>>(x, n, bits, rk, id, r, th);                \
+        break;
         MPC_ALG1_CASE(3) MPC_ALG1_CASE(4) MPC_ALG1_CASE(5) MPC_ALG1_CASE(6) MPC_ALG1_CASE(7) MPC_ALG1_CASE(8)
         MPC_ALG1_CASE(9) MPC_ALG1_CASE(10) MPC_ALG1_CASE(11) MPC_ALG1_CASE(12) MPC_ALG1_CASE(13) MPC_ALG1_CASE(14)
         MPC_ALG1_CASE(15) MPC_ALG1_CASE(16)
@@ -734,7 +887,7 @@ cudaError_t launch_trunc_alg1_all(uint64_t* x, int P, int64_t n, int bits, uint6
 // Phase A: z_p = x_p + r_p -> zbuf (u64, to be sum-allreduced) and the top
 // nibble h_p = signed(z_p) >> 60 -> hbuf (int8, sum-allreduced; exact for
 // P <= 16).  r_p from memory (rin) or from its Philox stream.
-__global__ void trunc_alg1_a_kernel(const uint64_t* __restrict__ x, int64_t n, uint64_t key, uint64_t id, int party,
+__global__ void trunc_alg1_a_kernel(const uint64_t* __restrict__ x, int64_t n, const PhiloxRK rk, uint64_t id, int party,
                                     const uint64_t* __restrict__ rin, uint64_t* __restrict__ zbuf,
                                     int8_t* __restrict__ hbuf) {
     const int64_t npairs = (n + 1) / 2;
@@ -745,7 +898,7 @@ __global__ void trunc_alg1_a_kernel(const uint64_t* __restrict__ x, int64_t n, u
         uint64_t xv[2], r[2], z[2];
         ld_pair(x, i0, vec, has1, xv);
         if (rin) ld_pair(rin, i0, vec, has1, r);
-        else philox_pair(key, stream_word(kTagR, (uint32_t)party, id), (uint64_t)j, r[0], r[1]);
+        else philox_pair_rk(rk, stream_word(kTagR, (uint32_t)party, id), (uint64_t)j, r[0], r[1]);
         z[0] = xv[0] + r[0];
         z[1] = xv[1] + r[1];
         st_pair(zbuf, i0, vec, has1, z);
@@ -757,7 +910,7 @@ __global__ void trunc_alg1_a_kernel(const uint64_t* __restrict__ x, int64_t n, u
 // + (z mod 2^60), kappa = ((z >> 60) - H) mod 16; theta_z = (S - signed(z)) / 2^64
 // (party 0 only).  [theta_r]_p from memory (thin) or regenerated (seeded TTP: for
 // party 0 that is the TTP's theta_r over all P r streams).
-__global__ void trunc_alg1_b_kernel(uint64_t* __restrict__ x, int64_t n, int bits, uint64_t key, uint64_t id, int P,
+__global__ void trunc_alg1_b_kernel(uint64_t* __restrict__ x, int64_t n, int bits, const PhiloxRK rk, uint64_t id, int P,
                                     int party, const uint64_t* __restrict__ rin, const uint64_t* __restrict__ thin,
                                     const uint64_t* __restrict__ zsum, const int8_t* __restrict__ hsum) {
     const int64_t npairs = (n + 1) / 2;
@@ -772,8 +925,8 @@ __global__ void trunc_alg1_b_kernel(uint64_t* __restrict__ x, int64_t n, int bit
             ld_pair(rin, i0, vec, has1, r);
             ld_pair(thin, i0, vec, has1, th);
         } else {
-            philox_pair(key, stream_word(kTagR, (uint32_t)party, id), (uint64_t)j, r[0], r[1]);
-            theta_share_pair(key, id, P, party, (uint64_t)j, th);
+            philox_pair_rk(rk, stream_word(kTagR, (uint32_t)party, id), (uint64_t)j, r[0], r[1]);
+            theta_share_pair(rk, id, P, party, (uint64_t)j, th);
         }
         if (party == 0) {
             uint64_t zv[2];
@@ -799,14 +952,15 @@ __global__ void trunc_alg1_b_kernel(uint64_t* __restrict__ x, int64_t n, int bit
 cudaError_t launch_trunc_alg1_a(const uint64_t* x, int64_t n, uint64_t key, uint64_t id, int party, const uint64_t* r,
                                 uint64_t* zbuf, int8_t* hbuf, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    trunc_alg1_a_kernel<<<grid_for((n + 1) / 2), 256, 0, st>>>(x, n, key, id, party, r, zbuf, hbuf);
+    trunc_alg1_a_kernel<<<grid_for((n + 1) / 2), 256, 0, st>>>(x, n, philox_round_keys(key), id, party, r, zbuf, hbuf);
     return cudaGetLastError();
 }
 cudaError_t launch_trunc_alg1_b(uint64_t* x, int64_t n, int bits, uint64_t key, uint64_t id, int P, int party,
                                 const uint64_t* r, const uint64_t* th, const uint64_t* zsum, const int8_t* hsum,
                                 cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    trunc_alg1_b_kernel<<<grid_for((n + 1) / 2), 256, 0, st>>>(x, n, bits, key, id, P, party, r, th, zsum, hsum);
+    trunc_alg1_b_kernel<<<grid_for((n + 1) / 2), 256, 0, st>>>(x, n, bits, philox_round_keys(key), id, P, party, r, th,
+                                                               zsum, hsum);
     return cudaGetLastError();
 }
 

@@ -408,6 +408,33 @@ class Context:
     def conv_out_shape(g):
         return (g.B, g.Cout, (g.H + 2 * g.ph - g.kh) // g.sh + 1, (g.W + 2 * g.pw - g.kw) // g.sw + 1)
 
+    @staticmethod
+    def conv1d_geom(B, C, L, Cout, k, stride=1, padding=0):
+        """A 1-D convolution x (B, C, L) * w (Cout, C, k) as the H = kh = 1 case of
+        mpc_conv2d_geom (same memory layout: (B, C, 1, L) and (Cout, C, 1, k))."""
+        return _native.ConvGeom(B, C, 1, L, Cout, 1, k, 1, stride, 0, padding)
+
+    def ttp_conv1d_triples(self, triple_id: int, g):
+        """Conv triple of a 1-D geometry, shaped a (B, C, L), b (Cout, C, k), c (B, Cout, L_out)."""
+        a, b, c = self.ttp_conv_triples(triple_id, g)
+        lead = self._lead()
+        return (a.view(lead + (g.B, g.C, g.W)), b.view(lead + (g.Cout, g.C, g.kw)),
+                c.view(lead + (g.B, g.Cout, self.conv_out_shape(g)[3])))
+
+    def beaver_conv1d(self, g, x, y, a, b, c, truncate: bool = True, wrap_id: int = 0,
+                      out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Private 1-D convolution: mpc_beaver_conv2d on the (B, C, 1, L) views."""
+        if g.H != 1 or g.kh != 1:
+            raise ValueError("not a 1-D geometry (conv1d_geom)")
+        lead = self._lead()
+        v4 = lambda t, shp: t.reshape(lead + shp)  # noqa: E731  (views of contiguous tensors)
+        Lo = self.conv_out_shape(g)[3]
+        z = self.beaver_conv2d(g, v4(x, (g.B, g.C, 1, g.W)), v4(y, (g.Cout, g.C, 1, g.kw)),
+                               v4(a, (g.B, g.C, 1, g.W)), v4(b, (g.Cout, g.C, 1, g.kw)),
+                               v4(c, (g.B, g.Cout, 1, Lo)), truncate, wrap_id,
+                               None if out is None else v4(out, (g.B, g.Cout, 1, Lo)))
+        return z.view(lead + (g.B, g.Cout, Lo))
+
     def ttp_conv_triples(self, triple_id: int, g):
         """Conv Beaver triple: a (input shape), b (weight shape), c = conv(a, b) (output shape)."""
         a = _u64(self._lead() + (g.B, g.C, g.H, g.W), self.device)

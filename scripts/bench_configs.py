@@ -139,6 +139,16 @@ def run(skip_c5=False):
                       ("NEXT4_text", "text")):
         out[key] = chain(name, offline_variant=name in ("resnet50", "vit"))
         torch.cuda.empty_cache()
+    # the convolutional models as true private convolutions (conv triples, reveal at the
+    # activation / weight shapes): ResNet-50 b1 (2-D) and Wav2Letter b1 / b32 (1-D)
+    ctx = mpc.Context(2, mpc.ALL_PARTIES, device=0, master_seed=synth.MASTER_SEED)
+    ms, rb = bench_layers.run_conv_chain(ctx, synth.CONV_MODELS["resnet50"], 20)
+    out["NEXT2_resnet50_conv2d"] = {"chain_ms": ms, "reveal_MB_per_party": rb / 1e6,
+                                    "reveal_MB_im2col_shape": sum(8 * (M * K + K * N) * c
+                                                                  for _, M, K, N, c in synth.RESNET50_B1) / 1e6}
+    out["NEXT2_wav2letter_conv1d"] = bench_layers.wav2letter_conv1d_report(ctx)
+    del ctx
+    torch.cuda.empty_cache()
     if not skip_c5:
         out["C5_p4_8192"] = c5(4)
         out["C5_p8_8192"] = c5(8)

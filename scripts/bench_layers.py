@@ -261,6 +261,68 @@ def run_conv_chain(ctx, layers, reps):
     return e0.elapsed_time(e1) / reps, reveal_bytes
 
 
+def run_conv1d_chain(ctx, layers, B, reps):
+    """Wav2Letter's convolutions as TRUE private 1-D convolutions (eps / delta revealed at
+    the activation / weight shapes) in one CUDA graph; returns (ms, reveal bytes per party,
+    im2col-shape reveal bytes per party, ring ops)."""
+    dev = torch.device("cuda", 0)
+    bufs, rb, rb_im2col, ops = [], 0, 0, 0.0
+    for i, (_, C, L, Co, k, st, pd, count) in enumerate(layers):
+        g = ctx.conv1d_geom(B, C, L, Co, k, st, pd)
+        Lo = (L + 2 * pd - k) // st + 1
+        X = synth.gaussian_fixed((B, C, L), 300 + i, 1.0, -8, 8)
+        Y = synth.gaussian_fixed((Co, C, k), 400 + i, (2.0 / (C * k)) ** 0.5, -8, 8)
+        x = ctx.share(torch.from_numpy(X.view(np.int64)).to(dev).view(torch.uint64), 0, 1 + 2 * i)
+        y = ctx.share(torch.from_numpy(Y.view(np.int64)).to(dev).view(torch.uint64), 1, 2 + 2 * i)
+        a, b, c = ctx.ttp_conv1d_triples(1 + i, g)
+        bufs.append((g, x, y, a, b, c, torch.empty_like(c), count))
+        rb += 8 * (X.size + Y.size) * count
+        M, K = B * Lo, C * k
+        rb_im2col += 8 * (M * K + K * Co) * count
+        ops += 2.0 * M * K * Co * count
+
+    def chain():
+        for g, x, y, a, b, c, z, count in bufs:
+            for _ in range(count):
+                ctx.beaver_conv1d(g, x, y, a, b, c, truncate=True, out=z)
+
+    chain()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        chain()
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=s):
+            chain()
+    for _ in range(3):
+        gr.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(reps):
+        gr.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps, rb, rb_im2col, ops
+
+
+def wav2letter_conv1d_report(ctx, reps=20):
+    out = {}
+    for B in (1, 32):
+        ms, rb, rbi, ops = run_conv1d_chain(ctx, synth.WAV2LETTER_CONV1D, B, reps)
+        layers = [(n, B * ((L + 2 * pd - k) // st + 1), C * k, Co, cnt)
+                  for n, C, L, Co, k, st, pd, cnt in synth.WAV2LETTER_CONV1D]
+        tg = sum(t_gemm_ms(M, K, N) * cnt for _, M, K, N, cnt in layers)
+        rl = layer_rooflines(layers)
+        out[f"b{B}"] = {"chain_ms": ms, "private_convs": sum(l[-1] for l in synth.WAV2LETTER_CONV1D),
+                        "ring_TOPS": ops / (ms * 1e-3) / 1e12, "roofline_ms": tg, "roofline_frac": tg / ms,
+                        "roofline_tensor_or_hbm_frac": rl / ms,
+                        "reveal_MB_per_party": rb / 1e6, "reveal_MB_im2col_shape": rbi / 1e6,
+                        "graph": "one CUDA graph per model; true 1-D convolutions (conv triples)"}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="all", choices=list(synth.MODELS) + ["all"])
@@ -278,6 +340,13 @@ def main():
         if args.model not in (name, "all"):
             continue
         if args.conv:
+            if name == "wav2letter":
+                out["wav2letter_conv1d"] = r = wav2letter_conv1d_report(ctx, args.reps)
+                for bk, v in r.items():
+                    print(f"wav2letter {bk} (true 1-D convs): {v['chain_ms']:.3f} ms ({v['ring_TOPS']:.2f} ring-TOPS), "
+                          f"reveal {v['reveal_MB_per_party']:.0f} MB/party (im2col shape "
+                          f"{v['reveal_MB_im2col_shape']:.0f} MB)", flush=True)
+                continue
             if name not in synth.CONV_MODELS:
                 continue
             ms, rb = run_conv_chain(ctx, synth.CONV_MODELS[name], args.reps)

@@ -118,6 +118,18 @@ RESNET18_CONV_B1 = [
 ]
 CONV_MODELS = {"resnet50": RESNET50_CONV_B1, "resnet18": RESNET18_CONV_B1}
 
+# Wav2Letter as true 1-D convolutions: torchaudio's
+# waveform model, 1 s of 16 kHz audio, 29 classes: (name, C, L, Cout, k, stride, pad,
+# count).  Same im2col GEMM shapes as WAV2LETTER_B1 (M = B * L_out, K = C * k, N = Cout).
+WAV2LETTER_CONV1D = [
+    ("conv1", 1, 16000, 250, 250, 160, 45, 1),
+    ("conv2", 250, 100, 250, 48, 2, 23, 1),
+    ("conv3-9", 250, 50, 250, 7, 1, 3, 7),
+    ("conv10", 250, 50, 2000, 32, 1, 16, 1),
+    ("conv11", 2000, 51, 2000, 1, 1, 0, 1),
+    ("conv12", 2000, 51, 29, 1, 1, 0, 1),
+]
+
 # Text classification: the embedding applied as a
 # dense matmul of 32 one-hot tokens x vocabulary 519,820 x embedding 32 — a wide
 # reduction (K >> 16512, the per-unit exactness bound) at tiny M and N.

@@ -21,6 +21,7 @@ GEOMS = [  # (B, C, H, W, Cout, kh, kw, stride, padding)
     (1, 16, 14, 14, 40, 1, 1, 2, 0),
     (1, 6, 7, 12, 300, 2, 4, (1, 2), (0, 1)),       # Cout >> pixels: transposed GEMM
     (3, 4, 5, 5, 3, 5, 5, 1, 2),
+    (2, 6, 1, 30, 4, 1, 8, (1, 2), (0, 3)),         # a 1-D convolution (H = kh = 1): Wav2Letter's conv2 family
 ]
 
 
@@ -138,3 +139,67 @@ def test_resnet_layers_full_parity(mpc, name, t):
                                      stride=(og.sh, og.sw), padding=(og.ph, og.pw)).numpy()
     ok = dg["theta"] == 0
     assert np.all(np.abs(got - ref)[ok] <= 2.0 ** -14)
+
+
+# ---------------------------------------------------------------- 1-D convolutions (Wav2Letter)
+def _inputs1d(g, seed):
+    X = synth.gaussian_fixed((g.B, g.C, g.W), seed, 1.0, -8, 8)
+    Y = synth.gaussian_fixed((g.Cout, g.C, g.kw), seed + 1, (2.0 / (g.C * g.kw)) ** 0.5, -8, 8)
+    return X, Y
+
+
+@pytest.mark.parametrize("B", [1, 4])
+@pytest.mark.parametrize("layer", synth.WAV2LETTER_CONV1D, ids=[l[0] for l in synth.WAV2LETTER_CONV1D])
+def test_wav2letter_conv1d_full_parity(mpc, layer, B):
+    """Every Wav2Letter layer as a true private 1-D convolution at full
+    size (batch 1 and 4), 2 parties, truncated: every share equals the oracle's
+    (eps, delta revealed at the activation / weight shapes), and the decoded output
+    is within 2^-14 of torch's float64 conv1d except the flagged wraps."""
+    name, C, L, Co, k, st, pd, _ = layer
+    if B > 1 and C * k > 2000:
+        pytest.skip("oracle time: batch 4 only for K <= 2000")
+    P = 2
+    c = mpc.Context(P, mpc.ALL_PARTIES, device=0, master_seed=MASTER)
+    g, og = c.conv1d_geom(B, C, L, Co, k, st, pd), oracle.conv1d_geom(B, C, L, Co, k, st, pd)
+    X, Y = _inputs1d(g, 31 + k)
+    gx, gy = c.share(dev(X), 0, 1), c.share(dev(Y), 1, 2)
+    ga, gb, gc = c.ttp_conv1d_triples(9, g)
+    assert tuple(ga.shape) == (P, B, C, L) and tuple(gb.shape) == (P, Co, C, k)
+    z = host(c.beaver_conv1d(g, gx, gy, ga, gb, gc, truncate=True))
+    Lo = (L + 2 * pd - k) // st + 1
+    assert z.shape == (P, B, Co, Lo)
+    X4, Y4 = X.reshape(B, C, 1, L), Y.reshape(Co, C, 1, k)
+    xs, ys = oracle.share(P, MASTER, X4, 0, 1), oracle.share(P, MASTER, Y4, 1, 2)
+    ez, dg = oracle.truncate(oracle.beaver_conv2d(xs, ys, *oracle.ttp_conv_triple(P, MASTER, 9, og), og), 16,
+                             diagnostics=True)
+    assert np.array_equal(z, ez.reshape(z.shape)), name
+    got = oracle.decode(oracle.reveal(z))
+    ref = torch.nn.functional.conv1d(torch.tensor(X.view(np.int64) / 65536.0), torch.tensor(Y.view(np.int64) / 65536.0),
+                                     stride=st, padding=pd).numpy()
+    ok = (dg["theta"] == 0).reshape(got.shape)
+    assert np.all(np.abs(got - ref)[ok] <= 2.0 ** -14)
+
+
+def test_conv1d_one_party_group_alg1(mpc):
+    """A 1-D convolution through the one-party schedule (3 parties as threads,
+    reveals through the in-process group) with Alg. 1 truncation."""
+    from test_gpu_local_group import run_parties
+    P, t = 3, (2, 250, 50, 250, 7, 1, 3)
+    og = oracle.conv1d_geom(*t)
+    X, Y = _inputs1d(og, 41)
+    X4, Y4 = X.reshape(t[0], t[1], 1, t[2]), Y.reshape(t[3], t[1], 1, t[4])
+    xs, ys = oracle.share(P, MASTER, X4, 0, 1), oracle.share(P, MASTER, Y4, 1, 2)
+    a, b, cc = oracle.ttp_conv_triple(P, MASTER, 10, og)
+
+    def body(ctx, r):
+        g = ctx.conv1d_geom(*t)
+        lead = (t[0], t[1], t[2])
+        z = ctx.beaver_conv1d(g, dev(xs[r]).view(lead), dev(ys[r]).view(t[3], t[1], t[4]), dev(a[r]).view(lead),
+                              dev(b[r]).view(t[3], t[1], t[4]), dev(cc[r]).view(t[0], t[3], -1), truncate=True,
+                              wrap_id=12)
+        return host(z)
+
+    got = np.stack([z.reshape(cc.shape[1:]) for z in run_parties(mpc, P, body)])
+    ez = oracle.truncate(oracle.beaver_conv2d(xs, ys, a, b, cc, og), 16, MASTER, wrap_id=12)
+    assert np.array_equal(got, ez)
+

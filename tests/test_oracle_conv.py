@@ -123,3 +123,64 @@ def test_decoded_accuracy_vs_float64(P):
     fail = (dg["theta"] != 0) if P <= 2 else (dg["eta"] != 0)
     assert np.all(np.abs(got - ref)[~fail] <= 2.0 ** -14)
     assert fail.sum() <= 1
+
+
+# ---------------------------------------------------------------- 1-D (Wav2Letter)
+CONV1D = [  # (B, C, L, Cout, k, stride, padding)
+    (1, 1, 400, 5, 25, 16, 4),            # Wav2Letter conv1 family (waveform front end, 250 / 160 / 45)
+    (2, 6, 30, 4, 8, 2, 3),               # conv2 family (k 48, stride 2, pad 23)
+    (1, 5, 12, 7, 7, 1, 3),               # conv3-9 (k 7, same padding)
+    (3, 9, 11, 6, 1, 1, 0),               # 1x1 layers
+]
+
+
+def _conv1d_loops(x, w, stride, pad):
+    """1-D ring convolution written out here (explicit loops, wrapping via Python ints)."""
+    B, C, L = x.shape
+    Cout, _, k = w.shape
+    Lo = (L + 2 * pad - k) // stride + 1
+    out = np.zeros((B, Cout, Lo), dtype=np.uint64)
+    for bi in range(B):
+        for co in range(Cout):
+            for o in range(Lo):
+                acc = 0
+                for ci in range(C):
+                    for t in range(k):
+                        pos = o * stride - pad + t
+                        if 0 <= pos < L:
+                            acc += int(x[bi, ci, pos]) * int(w[co, ci, t])
+                out[bi, co, o] = acc % 2 ** 64
+    return out
+
+
+@pytest.mark.parametrize("t", CONV1D)
+def test_conv1d_as_h1_conv2d(t):
+    """The 1-D geometry (H = kh = 1) of the oracle's conv2d equals a 1-D convolution
+    written out with loops on full-range ring elements, and PyTorch's float64 conv1d
+    on small integers."""
+    B, C, L, Cout, k, st, pd = t
+    g = oracle.conv1d_geom(*t)
+    rng = np.random.default_rng(sum(t))
+    x = synth.uniform_ring((B, C, L), 11 + L)
+    w = synth.uniform_ring((Cout, C, k), 12 + k)
+    got = oracle.conv2d(x.reshape(B, C, 1, L), w.reshape(Cout, C, 1, k), g)
+    Lo = (L + 2 * pd - k) // st + 1
+    assert got.shape == (B, Cout, 1, Lo)
+    assert np.array_equal(got.reshape(B, Cout, Lo), _conv1d_loops(x, w, st, pd))
+    xs = rng.integers(-300, 300, (B, C, L))
+    ws = rng.integers(-300, 300, (Cout, C, k))
+    ref = torch.nn.functional.conv1d(torch.from_numpy(xs).double(), torch.from_numpy(ws).double(), stride=st,
+                                     padding=pd).numpy().astype(np.int64)
+    got2 = oracle.conv2d(synth.to_ring(xs).reshape(B, C, 1, L), synth.to_ring(ws).reshape(Cout, C, 1, k), g)
+    assert np.array_equal(got2.view(np.int64).reshape(B, Cout, Lo), ref)
+
+
+def test_wav2letter_geometry_matches_the_gemm_shapes():
+    """synth.WAV2LETTER_CONV1D reproduces the im2col GEMM shapes of WAV2LETTER_B1
+    (M = L_out, K = C * k, N = Cout), i.e. torchaudio's waveform Wav2Letter on 1 s
+    of 16 kHz audio."""
+    shapes = []
+    for name, C, L, Co, k, st, pd, cnt in synth.WAV2LETTER_CONV1D:
+        Lo = (L + 2 * pd - k) // st + 1
+        shapes.append((name, Lo, C * k, Co, cnt))
+    assert shapes == [tuple(s) for s in synth.WAV2LETTER_B1]
