@@ -775,8 +775,8 @@ __global__ void __launch_bounds__(256, (P <= 8 ? 2 : 1)) trunc_alg1_all_kernel(u
 // running unsigned sum, the wrap count of sum_q v_q is C - sum_q m(v_q) + m(sum), and
 // beta_q = carry(x_q + r_q) - m(x_q) - m(r_q) + m(z_q) — the exact integer identities
 // the int128 form evaluates, at a third of its ALU instructions (the kernel is
-// ALU-pipe bound: ncu, P = 8).  Pass 1 keeps only beta_q per party; pass 2 re-reads
-// x_q (L1) and needs no r_q.
+// ALU-pipe bound: ncu, P = 8).  Pass 1 keeps beta_q and x_q per party; pass 2 needs
+// no r_q.
 __device__ __forceinline__ uint32_t add_carry(uint64_t a, uint64_t b, uint64_t& s) {
     uint32_t lo, hi, c;
     asm("add.cc.u32 %0, %3, %5;\n\taddc.cc.u32 %1, %4, %6;\n\taddc.u32 %2, 0, 0;"
@@ -804,19 +804,24 @@ __global__ void __launch_bounds__(256, (P <= 8 ? 2 : 1)) trunc_alg1_all_w32_kern
         const int64_t i0 = 2 * j;
         const bool has1 = i0 + 1 < n;
         uint32_t beta[P][2];
+        uint64_t xv[P][2];
         uint64_t zsum[2] = {0, 0}, rsum[2] = {0, 0};
         uint32_t cz[2] = {0, 0}, cr[2] = {0, 0};                        // carries minus msb counts
+        // every party's x pair is requested before any Philox block is expanded (the
+        // loads' latency hides under the arithmetic; ncu: long-scoreboard stalls
+        // dominated when each load was consumed right after its own block)
+#pragma unroll
+        for (int q = 0; q < P; ++q) ld_pair(x + (int64_t)q * n, i0, vec, has1, xv[q]);
 #pragma unroll
         for (int q = 0; q < P; ++q) {
-            uint64_t xv[2], r[2];
-            ld_pair(x + (int64_t)q * n, i0, vec, has1, xv);
+            uint64_t r[2];
             if (PAIRS) ld_pair(rin + (int64_t)q * n, i0, vec, has1, r);
             else philox_pair_rk(rk, stream_word(kTagR, (uint32_t)q, id), (uint64_t)j, r[0], r[1]);
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 uint64_t z;
-                const uint32_t c = add_carry(xv[e], r[e], z);                 // z_q = x_q + r_q
-                beta[q][e] = c - msb(xv[e]) - msb(r[e]) + msb(z);
+                const uint32_t c = add_carry(xv[q][e], r[e], z);              // z_q = x_q + r_q
+                beta[q][e] = c - msb(xv[q][e]) - msb(r[e]) + msb(z);
                 acc_carry(zsum[e], z, cz[e]);
                 cz[e] -= msb(z);
                 if (!PAIRS) { acc_carry(rsum[e], r[e], cr[e]); cr[e] -= msb(r[e]); }
@@ -845,12 +850,11 @@ __global__ void __launch_bounds__(256, (P <= 8 ? 2 : 1)) trunc_alg1_all_w32_kern
                 th[0] = theta_r[0] - th_sum[0];
                 th[1] = theta_r[1] - th_sum[1];
             }
-            uint64_t xv[2], o[2];
-            ld_pair(x + (int64_t)q * n, i0, vec, has1, xv);                   // L1 hit: loaded in pass 1
+            uint64_t o[2];
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const uint32_t theta_x = beta[q][e] - th[e] + (q == 0 ? theta_z[e] : 0u);
-                o[e] = div_pow2_round(xv[e], bits) - ((uint64_t)(theta_x << hshift) << 32);
+                o[e] = div_pow2_round(xv[q][e], bits) - ((uint64_t)(theta_x << hshift) << 32);
             }
             st_pair(x + (int64_t)q * n, i0, vec, has1, o);
         }
