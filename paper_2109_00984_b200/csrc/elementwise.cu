@@ -810,12 +810,17 @@ __global__ void __launch_bounds__(256, (P <= 8 ? 2 : 1)) trunc_alg1_all_w32_kern
         // every party's x pair is requested before any Philox block is expanded (the
         // loads' latency hides under the arithmetic; ncu: long-scoreboard stalls
         // dominated when each load was consumed right after its own block)
+        uint64_t rv[PAIRS ? P : 1][2];                                  // the wrap pair's r_q (PAIRS)
 #pragma unroll
         for (int q = 0; q < P; ++q) ld_pair(x + (int64_t)q * n, i0, vec, has1, xv[q]);
+        if (PAIRS) {
+#pragma unroll
+            for (int q = 0; q < P; ++q) ld_pair(rin + (int64_t)q * n, i0, vec, has1, rv[PAIRS ? q : 0]);
+        }
 #pragma unroll
         for (int q = 0; q < P; ++q) {
             uint64_t r[2];
-            if (PAIRS) ld_pair(rin + (int64_t)q * n, i0, vec, has1, r);
+            if (PAIRS) { r[0] = rv[PAIRS ? q : 0][0]; r[1] = rv[PAIRS ? q : 0][1]; }
             else philox_pair_rk(rk, stream_word(kTagR, (uint32_t)q, id), (uint64_t)j, r[0], r[1]);
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
@@ -834,13 +839,15 @@ __global__ void __launch_bounds__(256, (P <= 8 ? 2 : 1)) trunc_alg1_all_w32_kern
             theta_r[e] = cr[e] + msb(rsum[e]);                                // wraps of r (seeded TTP)
         }
         uint32_t th_sum[2] = {0, 0};
+        if (PAIRS) {                                                    // every [theta_r]_q requested up front
+#pragma unroll
+            for (int q = 0; q < P; ++q) ld_pair(thin + (int64_t)q * n, i0, vec, has1, rv[PAIRS ? q : 0]);
+        }
 #pragma unroll
         for (int q = P - 1; q >= 0; --q) {
             uint32_t th[2];
             if (PAIRS) {
-                uint64_t t[2];
-                ld_pair(thin + (int64_t)q * n, i0, vec, has1, t);
-                th[0] = (uint32_t)t[0]; th[1] = (uint32_t)t[1];
+                th[0] = (uint32_t)rv[PAIRS ? q : 0][0]; th[1] = (uint32_t)rv[PAIRS ? q : 0][1];
             } else if (q > 0) {
                 uint64_t t[2];
                 philox_pair_rk(rk, stream_word(kTagTheta, (uint32_t)q, id), (uint64_t)j, t[0], t[1]);

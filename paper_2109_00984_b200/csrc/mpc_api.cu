@@ -56,8 +56,6 @@ struct mpc_ctx_s {
     int* d_err = nullptr;
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
-    uint32_t* counters = nullptr;           // split-K arrival counters of the ring GEMM (all 0 between launches)
-    int64_t counter_slots = 0;
     cudaStream_t scratch_stream = nullptr;  // last stream that used the scratch
     cudaEvent_t scratch_ev = nullptr;
 };
@@ -439,25 +437,8 @@ mpc_status beaver_overlapped(mpc_ctx c, const BeaverWs& w, const uint64_t* x, co
     return gemm_run(c, p2, 1);
 }
 
-// Zero-initialised split-K arrival counters of the context (grown on demand; every
-// launch leaves them 0), so the ring GEMM reduces split-K partials itself.
-mpc_status ensure_counters(mpc_ctx c, int64_t slots) {
-    if (c->counter_slots >= slots) return MPC_OK;
-    if (c->counters) { cudaStreamSynchronize(c->stream); cudaFree(c->counters); c->counters = nullptr; c->counter_slots = 0; }
-    const int64_t n = std::max<int64_t>(slots, 4096);
-    if (cudaMalloc(&c->counters, n * sizeof(uint32_t)) != cudaSuccess ||
-        cudaMemset(c->counters, 0, n * sizeof(uint32_t)) != cudaSuccess)
-        return fail(c, MPC_ERR_CUDA, "split-K counters alloc");
-    c->counter_slots = n;
-    return MPC_OK;
-}
-
 mpc_status gemm_run(mpc_ctx c, RingGemmParams& p, int parties) {
     p.kc = ring_gemm_default_kc(p.seg[0].kb + (p.nseg > 1 ? p.seg[1].kb : 0));
-    if (p.partials && !p.small) {
-        CHECK(ensure_counters(c, ring_gemm_counter_slots(p, parties)));
-        p.counters = c->counters;
-    }
     return run(c, kClsGemm, "ring_gemm", [&] { return ring_gemm_launch(p, parties, c->stream); });
 }
 
@@ -667,7 +648,6 @@ mpc_status mpc_destroy(mpc_ctx c) {
     if (c->d_err) cudaFree(c->d_err);
     if (c->scratch) cudaFree(c->scratch);
     if (c->scratch_ev) cudaEventDestroy(c->scratch_ev);
-    if (c->counters) cudaFree(c->counters);
     delete c;
     return MPC_OK;
 }

@@ -131,7 +131,6 @@ struct WorkMap {
 struct Bars {
     uint8_t* stage_base;
     uint64_t *full, *empty, *tfull, *tempty;
-    uint32_t* arrivals;              // split-K arrival count read back by the epilogue warps
 };
 
 // Super-pass g accumulates 4 shifts into TMEM slots 0..3 (128 columns each):
@@ -398,60 +397,24 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Wor
         const int64_t cs = tr ? hw : 1;
         const int64_t off = (tr ? (grow / hw) * p.N * hw + grow % hw : grow * p.N) + gc0 * cs;
         const bool full = !tr && vec && gc0 + 64 <= p.N;
-        bool store_z = wm.splits <= 1;
-        if (wm.splits > 1) {
+        if (grow < p.M && wm.splits > 1) {
             // split-K: store this K range's partial sum in its own slab of the
-            // partials buffer (same element layout as z).  Ring addition commutes, so
-            // any order of the slabs is exact.  With arrival counters the last K range
-            // of this tile half to finish adds the other slabs (read from L2) to its
-            // own sum in registers, then takes the z path below (c_p, truncation);
-            // without, ring_gemm_finalize does that in a second launch.
+            // partials buffer (same element layout as z); ring_gemm_finalize adds
+            // the slabs (ring addition commutes, any order is exact), c_p, and
+            // applies the truncation.
             const int s = w % wm.splits;
-            const int64_t pbase = party * p.party_stride_z + bi * p.batch_stride_z + off;
-            if (grow < p.M) {
-                uint64_t* pb = p.partials + (int64_t)s * p.partial_stride + pbase;
-                if (full) {
-                    const uint64_t ppol = p.partials_evict_first ? pol : evict_last_policy();
+            uint64_t* pb = p.partials + (int64_t)s * p.partial_stride + party * p.party_stride_z +
+                           bi * p.batch_stride_z + off;
+            if (full) {
+                const uint64_t ppol = p.partials_evict_first ? pol : evict_last_policy();
 #pragma unroll
-                    for (int j = 0; j < 64; j += 4) st_stream4(pb + j, &run[j], ppol);
-                } else {
+                for (int j = 0; j < 64; j += 4) st_stream4(pb + j, &run[j], ppol);
+            } else {
 #pragma unroll
-                    for (int j = 0; j < 64; ++j)
-                        if (gc0 + j < p.N) pb[j * cs] = run[j];
-                }
+                for (int j = 0; j < 64; ++j)
+                    if (gc0 + j < p.N) pb[j * cs] = run[j];
             }
-            if (p.counters) {
-                __threadfence();                                   // this thread's slab rows, device-wide
-                epi_bar();
-                uint32_t* cnt = p.counters + (int64_t)(w / wm.splits) * 2 + rank;
-                if (threadIdx.x == 128) *B.arrivals = atomicAdd(cnt, 1u);
-                epi_bar();
-                if (*B.arrivals == (uint32_t)(wm.splits - 1)) {
-                    __threadfence();
-                    if (grow < p.M) {
-                        for (int s2 = 0; s2 < wm.splits; ++s2) {
-                            if (s2 == s) continue;
-                            const uint64_t* pb = p.partials + (int64_t)s2 * p.partial_stride + pbase;
-                            if (full) {
-#pragma unroll
-                                for (int j = 0; j < 64; j += 4) {
-                                    uint64_t v[4];
-                                    ld_cg4(pb + j, v);
-                                    run[j] += v[0]; run[j + 1] += v[1]; run[j + 2] += v[2]; run[j + 3] += v[3];
-                                }
-                            } else {
-#pragma unroll
-                                for (int j = 0; j < 64; ++j)
-                                    if (gc0 + j < p.N) run[j] += __ldcg(pb + j * cs);
-                            }
-                        }
-                    }
-                    if (threadIdx.x == 128) *cnt = 0;                  // left 0 for the next launch
-                    store_z = true;
-                }
-            }
-        }
-        if (store_z && grow < p.M) {
+        } else if (grow < p.M) {
             // z = trunc(c + run).  z may alias c (in-place second phase): each
             // element is read before it is written by the same thread.  Batches of
             // 16 columns: all loads of a batch are issued before its stores, so a
@@ -503,7 +466,6 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     B.tfull = B.empty + kStages;
     B.tempty = B.tfull + 1;           // [2]: TMEM slots 0-1 / 2-3 drained
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(B.tempty + 2);
-    B.arrivals = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
@@ -676,7 +638,6 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     q.partials_evict_first = env_pef;
     q.splits = prm.partials ? ring_gemm_splits(inst, prm.M, prm.N, tkb, max_clusters, prm.small != 0) : 1;
     if (prm.small) {
-        q.counters = nullptr;                     // the stacked-plane kernel reduces split-K in ring_gemm_finalize
         if (q.splits > 1) q.partial_stride = ring_gemm_out_elems(q, parties);
         cudaError_t e = ring_gemm_small_launch(q, parties, 2 * max_clusters, stream);
         if (e != cudaSuccess || q.splits <= 1) return e;
@@ -700,21 +661,24 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
         // DRAM bytes at 4096^3.  MPC_GEMM_TMA=0 / 1 forces either; fault
         // injection uses the bulk path.
         static const int env_tma = getenv("MPC_GEMM_TMA") ? atoi(getenv("MPC_GEMM_TMA")) : -1;
-        const bool want_tma = env_tma < 0 ? ring_gemm_plane_bytes(q, parties) <= (2ull << 30) : env_tma != 0;
+        const uint64_t plane_bytes = ring_gemm_plane_bytes(q, parties);
+        const bool want_tma = env_tma < 0 ? plane_bytes <= (2ull << 30) : env_tma != 0;
+        // Launches over more than 2 GiB of operand planes (configs[4]) use 32-block units:
+        // the concurrent clusters' K window then stays in L2 (4-party 8192^3: DRAM reads
+        // 106 -> 68 GB per launch, ncu 101.7 -> 95.3 ms; 16 / 24 blocks no better), while
+        // 4096^3 keeps 64 (32: 5.90 -> 6.01 ms, the drain between units costs more).
+        if (plane_bytes > (2ull << 30) && !getenv("MPC_GEMM_KC") && q.kc > 32) q.kc = 32;
         const bool tma = want_tma && !q.fault_inject && fill_tma(q, parties);
         static const int env_l2 = getenv("MPC_GEMM_TMA_L2") ? atoi(getenv("MPC_GEMM_TMA_L2")) : 3;
         q.tma_l2 = env_l2;
         auto kern = q.fault_inject ? gemm::ring_gemm_kernel<true, false>
                   : tma            ? gemm::ring_gemm_kernel<false, true>
                                    : gemm::ring_gemm_kernel<false, false>;
-        static const bool fused_off = getenv("MPC_GEMM_FUSED_SPLITK") && atoi(getenv("MPC_GEMM_FUSED_SPLITK")) == 0;
-        if (fused_off) q.counters = nullptr;
         cudaError_t e = launch_pdl(kern, dim3((unsigned)(clusters * 2)), dim3(gemm::kThreads), smem, stream, q, parties);
-        if (e != cudaSuccess || q.splits <= 1 || q.counters) return e;
+        if (e != cudaSuccess || q.splits <= 1) return e;
         return ring_gemm_finalize(q, parties, stream);
     }
     // diagnostic mode: stall-cycle attribution of the producer and MMA threads
-    q.counters = nullptr;
     unsigned long long h[8] = {0, 0, 0, 0, ~0ull, 0, 0, 0};
     cudaMalloc(&q.dbg, sizeof(h));
     cudaMemcpyAsync(q.dbg, h, sizeof(h), cudaMemcpyHostToDevice, stream);
@@ -786,11 +750,6 @@ __global__ void finalize_kernel(uint64_t* __restrict__ z, const uint64_t* __rest
     }
 }
 }  // namespace gemm
-
-int64_t ring_gemm_counter_slots(const RingGemmParams& q, int parties) {
-    const int64_t inst = (int64_t)parties * (q.batch > 1 ? q.batch : 1);
-    return 2 * inst * (pad_rows<Layout::Left>(q.M) / gemm::kTileM) * (pad_rows<Layout::Right>(q.N) / gemm::kTileN);
-}
 
 // z = trunc(z + c) over all parties after a split-K GEMM (party buffers contiguous).
 int64_t ring_gemm_out_elems(const RingGemmParams& q, int parties) {

@@ -60,13 +60,7 @@ struct RingGemmParams {
     int tma_l2;                         // L2 policy of the TMA operand loads: 0 evict_normal, 1 evict_last,
                                         // 2 evict_first, 3 no hint (MPC_GEMM_TMA_L2; experiment)
     RingGemmTma tma;                    // set by the launcher (2-CTA kernel, MPC_GEMM_TMA != 0)
-    uint32_t* counters;                 // split-K in the kernel: one arrival counter per (instance, m tile,
-                                        // n tile, CTA half), all 0 on entry and left 0 (ring_gemm_counter_slots);
-                                        // the last K range of a tile to finish adds the others' partials, c_p,
-                                        // truncates and writes z — no finalize launch.  Null: finalize kernel.
 };
-// arrival counters the 2-CTA kernel needs for an in-kernel split-K reduction of this launch
-int64_t ring_gemm_counter_slots(const RingGemmParams& q, int parties);
 
 // Two kernels: the 2-CTA 256 x 128 kernel (planes in Layout::Left / Right) and
 // the stacked-plane kernel of ring_gemm_small.cu (32 x 32 tiles, for few rows)

@@ -181,13 +181,5 @@ __device__ __forceinline__ void st_stream4(uint64_t* p, const uint64_t* v, uint6
                  :: "l"(p), "l"(v[0]), "l"(v[1]), "l"(v[2]), "l"(v[3]), "l"(pol) : "memory");
 }
 
-// L2-coherent 32-byte load (another SM's split-K partial, written in this launch)
-__device__ __forceinline__ void ld_cg4(const uint64_t* p, uint64_t* v) {
-    asm volatile("ld.global.cg.v4.u64 {%0, %1, %2, %3}, [%4];"
-                 : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(p) : "memory");
-}
-// the 8 epilogue warps of a CTA (threads 128..383)
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-
 }  // namespace tc
 }  // namespace mpc
