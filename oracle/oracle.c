@@ -922,3 +922,152 @@ void oracle_relu(int P, const uint64_t* k_party, uint64_t k_ttp, uint64_t relu_i
     }
     free(xb); free(rA); free(rB); free(s); free(ind); free(a); free(b); free(c);
 }
+
+/* ========================================================================
+ * The boundary's calls with the C-ABI's shape (SURVEY §8(b) "the oracle
+ * library exports the same functions as oracle_mpc_* with host pointers and
+ * identical semantics"): include/mpc_ring.h's north-star entry points, for an
+ * all-parties context (rank = -1; every share argument is [P][n] in HOST
+ * memory).  Each one only composes the steps above (O1-O8); status codes are
+ * mpc_status's numbers.  A parity harness can run one protocol script against
+ * either library (tests/test_oracle_boundary.py, tests/test_gpu_boundary_swap.py).
+ * ======================================================================== */
+#define ORACLE_MPC_OK 0
+#define ORACLE_MPC_ERR_ARG 1
+#define ORACLE_MPC_ERR_SHAPE 2
+#define ORACLE_MPC_ERR_OVERFLOW 3
+#define ORACLE_MPC_ERR_UNSUPPORTED 7
+
+typedef struct oracle_mpc_ctx_s {
+    int P, frac;
+    uint64_t k_party[16], k_ttp;
+    uint64_t rounds, bytes;
+} oracle_mpc_ctx_s;
+typedef oracle_mpc_ctx_s* oracle_mpc_ctx;
+
+int oracle_mpc_create(oracle_mpc_ctx* out, int world_size, int rank, int device, const void* nccl_id,
+                      uint64_t master_seed, int frac_bits)
+{
+    (void)device; (void)nccl_id;
+    if (!out) return ORACLE_MPC_ERR_ARG;
+    *out = NULL;
+    if (world_size < 1 || world_size > 16 || frac_bits < 1 || frac_bits > 30) return ORACLE_MPC_ERR_ARG;
+    if (rank != -1) return ORACLE_MPC_ERR_UNSUPPORTED;       /* the oracle simulates every party */
+    oracle_mpc_ctx c = (oracle_mpc_ctx)calloc(1, sizeof(oracle_mpc_ctx_s));
+    if (!c) return ORACLE_MPC_ERR_ARG;
+    c->P = world_size;
+    c->frac = frac_bits;
+    oracle_derive_keys(master_seed, world_size, c->k_party, &c->k_ttp);
+    *out = c;
+    return ORACLE_MPC_OK;
+}
+
+int oracle_mpc_destroy(oracle_mpc_ctx c) { if (!c) return ORACLE_MPC_ERR_ARG; free(c); return ORACLE_MPC_OK; }
+
+int oracle_mpc_stats(oracle_mpc_ctx c, uint64_t* rounds, uint64_t* bytes_sent)
+{
+    if (!c) return ORACLE_MPC_ERR_ARG;
+    if (rounds) *rounds = c->rounds;
+    if (bytes_sent) *bytes_sent = c->bytes;
+    return ORACLE_MPC_OK;
+}
+
+int oracle_mpc_encode(oracle_mpc_ctx c, const double* x, uint64_t* out, int64_t n)
+{
+    if (!c || n < 0) return ORACLE_MPC_ERR_ARG;
+    return oracle_encode(x, out, n, c->frac) == ORACLE_OK ? ORACLE_MPC_OK : ORACLE_MPC_ERR_OVERFLOW;
+}
+
+int oracle_mpc_decode(oracle_mpc_ctx c, const uint64_t* v, double* out, int64_t n)
+{
+    if (!c || n < 0) return ORACLE_MPC_ERR_ARG;
+    oracle_decode(v, out, n, c->frac);
+    return ORACLE_MPC_OK;
+}
+
+int oracle_mpc_share(oracle_mpc_ctx c, const uint64_t* x, int src, uint64_t share_id, uint64_t* share_out, int64_t n)
+{
+    if (!c || n < 0 || src < 0 || src >= c->P || (n > 0 && (!x || !share_out))) return ORACLE_MPC_ERR_ARG;
+    oracle_share(c->P, c->k_party, x, src, share_id, n, share_out);
+    return ORACLE_MPC_OK;
+}
+
+int oracle_mpc_reveal(oracle_mpc_ctx c, const uint64_t* share, uint64_t* out, int64_t n)
+{
+    if (!c || n < 0 || (n > 0 && (!share || !out))) return ORACLE_MPC_ERR_ARG;
+    c->rounds += 1;
+    c->bytes += 8ull * (uint64_t)n * (uint64_t)c->P;
+    oracle_reveal(c->P, share, n, out);
+    return ORACLE_MPC_OK;
+}
+
+int oracle_mpc_ttp_triples(oracle_mpc_ctx c, uint64_t triple_id, int64_t M, int64_t K, int64_t N,
+                           uint64_t* a, uint64_t* b, uint64_t* cc, void* workspace, size_t workspace_bytes)
+{
+    (void)workspace; (void)workspace_bytes;
+    if (!c || M < 0 || K < 0 || N < 0) return ORACLE_MPC_ERR_SHAPE;
+    oracle_ttp_triple(c->P, c->k_ttp, triple_id, M, K, N, NULL, 0, a, b, cc);
+    return ORACLE_MPC_OK;
+}
+
+int oracle_mpc_ttp_wrap_pairs(oracle_mpc_ctx c, uint64_t wrap_id, int64_t n, uint64_t* r, uint64_t* theta_r)
+{
+    if (!c || n < 0) return ORACLE_MPC_ERR_ARG;
+    oracle_wrap_pair(c->P, c->k_ttp, wrap_id, n, r, theta_r);
+    return ORACLE_MPC_OK;
+}
+
+/* O6 (P <= 2) or O7 (P > 2) in place, the wrap pair regenerated from wrap_id (r, th NULL) or given */
+static int oracle_mpc_truncate_impl(oracle_mpc_ctx c, uint64_t* x, int64_t n, int bits, uint64_t wrap_id,
+                                    const uint64_t* r_in, const uint64_t* th_in)
+{
+    if (bits < 1 || bits > 62) return ORACLE_MPC_ERR_ARG;
+    int64_t Pn = (int64_t)c->P * n;
+    uint64_t* out = (uint64_t*)malloc((size_t)(Pn > 0 ? Pn : 1) * 8);
+    int rc;
+    if (c->P <= 2) {
+        rc = oracle_truncate_local(c->P, x, n, bits, out);
+    } else {
+        uint64_t* r = (uint64_t*)r_in;
+        uint64_t* th = (uint64_t*)th_in;
+        if (!r_in) {
+            r = (uint64_t*)malloc((size_t)(Pn > 0 ? Pn : 1) * 8);
+            th = (uint64_t*)malloc((size_t)(Pn > 0 ? Pn : 1) * 8);
+            oracle_wrap_pair(c->P, c->k_ttp, wrap_id, n, r, th);
+        }
+        rc = oracle_truncate_alg1(c->P, x, r, th, n, bits, out, NULL, NULL);
+        if (!r_in) { free(r); free(th); }
+        c->rounds += 1;
+        c->bytes += 9ull * (uint64_t)n * (uint64_t)c->P;
+    }
+    if (rc == ORACLE_OK) memcpy(x, out, (size_t)Pn * 8);
+    free(out);
+    return rc == ORACLE_OK ? ORACLE_MPC_OK : ORACLE_MPC_ERR_ARG;
+}
+
+int oracle_mpc_truncate(oracle_mpc_ctx c, uint64_t* x, int64_t n, int bits, uint64_t wrap_id)
+{
+    if (!c || n < 0 || (n > 0 && !x)) return ORACLE_MPC_ERR_ARG;
+    return oracle_mpc_truncate_impl(c, x, n, bits, wrap_id, NULL, NULL);
+}
+
+int oracle_mpc_truncate_pairs(oracle_mpc_ctx c, uint64_t* x, int64_t n, int bits, const uint64_t* r,
+                              const uint64_t* theta_r)
+{
+    if (!c || n < 0 || (n > 0 && (!x || (c->P > 2 && (!r || !theta_r))))) return ORACLE_MPC_ERR_ARG;
+    return oracle_mpc_truncate_impl(c, x, n, bits, 0, r, theta_r);
+}
+
+int oracle_mpc_beaver_matmul(oracle_mpc_ctx c, const uint64_t* x, const uint64_t* y, const uint64_t* a,
+                             const uint64_t* b, const uint64_t* cc, uint64_t* z, int64_t M, int64_t K, int64_t N,
+                             int truncate, uint64_t wrap_id, void* workspace, size_t workspace_bytes)
+{
+    (void)workspace; (void)workspace_bytes;
+    if (!c || M < 0 || K < 0 || N < 0) return ORACLE_MPC_ERR_SHAPE;
+    c->rounds += 1;                                            /* eps || delta */
+    c->bytes += 8ull * (uint64_t)(M * K + K * N) * (uint64_t)c->P;
+    if (M == 0 || N == 0) return ORACLE_MPC_OK;
+    oracle_beaver_matmul(c->P, x, y, a, b, cc, M, K, N, NULL, NULL, NULL, NULL, z);
+    if (truncate) return oracle_mpc_truncate_impl(c, z, M * N, c->frac, wrap_id, NULL, NULL);
+    return ORACLE_MPC_OK;
+}
