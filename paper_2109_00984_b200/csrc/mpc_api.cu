@@ -34,7 +34,9 @@ struct mpc_ctx_s {
     uint64_t kttp = 0;
     bool has_ttp = true;                 // holds k_ttp (mpc_create; mpc_create_with_keys only if given)
     cudaStream_t stream = nullptr;
-    ncclComm_t comm = nullptr;
+    ncclComm_t comm = nullptr;              // maxCTAs = kCommSms: reveals overlapped with the GEMM (comm stream)
+    ncclComm_t comm_fast = nullptr;         // no CTA cap: reveals nothing overlaps (context stream; Alg. 1's
+                                            // z / top-nibble reveals, output reveals, ReLU rounds)
     LocalGroup* lg = nullptr;               // in-process transport (mpc_create_local), instead of NCCL
     uint64_t* xbuf = nullptr;               // NCCL XOR reveal: all-gathered binary shares
     size_t xbuf_bytes = 0;
@@ -94,6 +96,20 @@ mpc_status run(mpc_ctx c, int cls, const char* what, F&& f) {
 }
 
 inline bool has_comm(mpc_ctx c) { return c->comm != nullptr || c->lg != nullptr; }
+// A collective on the comm stream overlaps a GEMM: the CTA-capped communicator
+// leaves it SMs.  Anything else (on the context stream, nothing beside it) gets all
+// the CTAs NCCL wants.  Every party issues its collectives in the same program
+// order, and the two communicators' operations never overlap in time (the comm
+// stream's reveals complete before the compute stream's next collective).
+inline ncclComm_t pick_comm(mpc_ctx c, cudaStream_t st) {
+    return (st == c->comm_stream || !c->comm_fast) ? c->comm : c->comm_fast;
+}
+void abort_comms(mpc_ctx c) {
+    if (c->comm_fast) ncclCommAbort(c->comm_fast);
+    if (c->comm) ncclCommAbort(c->comm);
+    c->comm_fast = nullptr;
+    c->comm = nullptr;
+}
 
 // One reveal collective of this party on `st` (default: the context stream):
 // recv = op over the parties' send buffers (transport.h).  Any failure leaves
@@ -150,20 +166,19 @@ mpc_status comm_allreduce(mpc_ctx c, const void* send, void* recv, size_t count,
             if (cudaMalloc(&c->xbuf, need) != cudaSuccess) return fail(c, MPC_ERR_CUDA, "%s: xor buffer alloc", what);
             c->xbuf_bytes = need;
         }
-        r = ncclAllGather(send, c->xbuf, count, ncclUint64, c->comm, st);
+        r = ncclAllGather(send, c->xbuf, count, ncclUint64, pick_comm(c, st), st);
         if (r == ncclSuccess) {
             cudaError_t e = launch_xor_gathered(c->xbuf, c->P, (int64_t)count, static_cast<uint64_t*>(recv), st);
             c->launches++;
             if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "%s: xor: %s", what, cudaGetErrorString(e));
         }
     } else {
-        r = ncclAllReduce(send, recv, count, op == RedOp::SumI8 ? ncclInt8 : ncclUint64, ncclSum, c->comm, st);
+        r = ncclAllReduce(send, recv, count, op == RedOp::SumI8 ? ncclInt8 : ncclUint64, ncclSum, pick_comm(c, st), st);
     }
     if (c->prof) { cudaEventRecord(ev.b, st); c->pending.push_back(ev); }
     if (r != ncclSuccess) {
         c->broken = true;
-        ncclCommAbort(c->comm);
-        c->comm = nullptr;
+        abort_comms(c);
         return fail(c, MPC_ERR_NCCL, "%s: %s", what, ncclGetErrorString(r));
     }
     return MPC_OK;
@@ -530,16 +545,23 @@ mpc_status create_impl(mpc_ctx* out, int world_size, int rank, int device, const
         if (ncclCommInitRankConfig(&c->comm, world_size, id, rank, &cfg) != ncclSuccess) {
             cudaFree(c->d_err); delete c; return MPC_ERR_NCCL;
         }
+        // the same ranks again without the CTA cap, for the collectives nothing overlaps
+        // (collective: every party splits at creation, so all or none have it)
+        ncclConfig_t cfg_fast = NCCL_CONFIG_INITIALIZER;
+        cfg_fast.blocking = 1;
+        if (ncclCommSplit(c->comm, 0, rank, &c->comm_fast, &cfg_fast) != ncclSuccess) {
+            ncclCommDestroy(c->comm); cudaFree(c->d_err); delete c; return MPC_ERR_NCCL;
+        }
         if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&c->ev_mask, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&c->ev_delta, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&c->ev_eps, cudaEventDisableTiming) != cudaSuccess) {
-            ncclCommDestroy(c->comm); cudaFree(c->d_err); delete c; return MPC_ERR_CUDA;
+            ncclCommDestroy(c->comm_fast); ncclCommDestroy(c->comm); cudaFree(c->d_err); delete c; return MPC_ERR_CUDA;
         }
         const char* chk = getenv("MPC_CHECK_COLLECTIVES");
         if (chk && atoi(chk) != 0) {
             if (cudaMalloc(&c->check_buf, 2 * sizeof(uint64_t)) != cudaSuccess) {
-                ncclCommDestroy(c->comm); cudaFree(c->d_err); delete c; return MPC_ERR_CUDA;
+                ncclCommDestroy(c->comm_fast); ncclCommDestroy(c->comm); cudaFree(c->d_err); delete c; return MPC_ERR_CUDA;
             }
             c->check_collectives = true;
         }
@@ -636,6 +658,7 @@ mpc_status mpc_destroy(mpc_ctx c) {
     if (!c) return MPC_ERR_ARG;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream); else cudaDeviceSynchronize();
+    if (c->comm_fast) ncclCommDestroy(c->comm_fast);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->lg) local_group_detach(c->lg, c->rank);
     if (c->xbuf) cudaFree(c->xbuf);
@@ -1251,13 +1274,13 @@ mpc_status mpc_reveal_batch(mpc_ctx c, int count, const uint64_t* const* shares,
     }
     ncclResult_t r = ncclGroupStart();
     for (int t = 0; t < count && r == ncclSuccess; ++t)
-        if (ns[t]) r = ncclAllReduce(shares[t], outs[t], (size_t)ns[t], ncclUint64, ncclSum, c->comm, c->stream);
+        if (ns[t]) r = ncclAllReduce(shares[t], outs[t], (size_t)ns[t], ncclUint64, ncclSum, pick_comm(c, c->stream),
+                                     c->stream);
     ncclResult_t r2 = ncclGroupEnd();
     if (r == ncclSuccess) r = r2;
     if (r != ncclSuccess) {
         c->broken = true;
-        ncclCommAbort(c->comm);
-        c->comm = nullptr;
+        abort_comms(c);
         return fail(c, MPC_ERR_NCCL, "reveal_batch: %s", ncclGetErrorString(r));
     }
     return MPC_OK;
