@@ -357,7 +357,10 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "dtype": "u64", "data": "synthetic",
             "config": {"workload": WORKLOAD + f" — oracle on a {rows_n}-row sample", "M": M, "K": K, "N": N,
-                       "parties": 2},
+                       "parties": 2, "same_config": False,
+                       "sample_note": f"the CPU oracle computes {rows_n} of the {M} output rows of both parties per "
+                                      "step (the full K x N delta reveal included) and the value is scaled to "
+                                      "ring-TOPS of that sample; a full 4096^3 oracle step takes minutes"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": times[0]["cores"], "kind": "oracle",
                              "sample": times[0]["sample"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
