@@ -673,7 +673,31 @@ def main():
             rs = [0, M // 2, M - 1]
             Xf = X[rs].view(np.int64).astype(np.float64) / 65536
             e2e_err = float(np.max(np.abs(hout[(ke - 1) % 2][rs].numpy() - Xf @ (Y.view(np.int64) / 65536.0))))
+        # the e2e leg's own floor, measured here (outside the timed region): this step's H2D / D2H
+        # alone over PCIe from pinned memory, against the device step time of the value line
+        def copy_ms(fn, reps=3):
+            fn()
+            torch.cuda.synchronize(dev)
+            t0.record(stream)
+            for _ in range(reps):
+                fn()
+            t1.record(stream)
+            torch.cuda.synchronize(dev)
+            return t0.elapsed_time(t1) / reps
+
+        def h2d_once():
+            if holds_x:
+                dX[0].copy_(hX, non_blocking=True)
+            if holds_y:
+                dY[0].copy_(hY, non_blocking=True)
+        h2d_ms = copy_ms(h2d_once) if h2d else 0.0
+        d2h_ms = copy_ms(lambda: hout[0].copy_(dout[0], non_blocking=True))
+        floor = max(ms, h2d_ms, d2h_ms)
         e2e = {"value": sessions * 2.0 * M * N * K / (ems * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ems,
+               "floor": {"h2d_ms": h2d_ms, "d2h_ms": d2h_ms, "device_step_ms": ms, "floor_ms": floor,
+                         "frac": floor / ems,
+                         "what": "max(the value line's device step, this step's H2D alone, its D2H alone): "
+                                 "copies and compute overlap, so the e2e step cannot be shorter"},
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "per_step": "H2D plaintext X,Y (f64, pinned) + encode + share + beaver_matmul (truncated) with a "
                            "fresh triple + reveal + decode + D2H of the f64 product",
