@@ -30,7 +30,7 @@
 // (K chunk, super-pass) are ordered chunk major so the second super-pass
 // re-reads a K window still resident in L2.
 // The u64 running sum of a tile lives in the registers of 8 epilogue warps
-// (64 columns x 1 row per thread; setmaxnreg gives them 208 registers) and is
+// (64 columns x 1 row per thread; setmaxnreg gives them 216 registers) and is
 // written once, with the Beaver c_p addend and the fused truncation, at the
 // tile end.  The kernel is persistent: 74 clusters walk the tiles in a grouped
 // order (4 row tiles x all column tiles x parties per group).
@@ -534,15 +534,12 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     const uint32_t tmem_base = *tmem_slot;
     if (p.dbg && threadIdx.x == 0) atomicMax(&p.dbg[5], globaltimer());
     // register budget: the control warpgroup needs few, the epilogue holds 64 u64 sums per thread
-    // setmaxnreg budget (launch: 168 x 384 of the SM's 64 Ki registers): the control
-    // warpgroup gives back (168 - 80) x 128 = 11264, the epilogue takes (208 - 168) x 256
-    // = 10240 — an increase the freed pool cannot cover blocks in setmaxnreg.inc forever
     if (warp < 4) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
         control_roles<FAULT, TMA>(p, wm, warp, lane, rank, tmem_base, B);
         if (p.dbg && warp == 1 && lane == 0 && rank == 0) atomicMax(&p.dbg[6], globaltimer());
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
         epilogue_role(p, wm, warp, lane, rank, tmem_base, B);
         if (p.dbg && lane == 0) atomicMax(&p.dbg[7], globaltimer());
     }
