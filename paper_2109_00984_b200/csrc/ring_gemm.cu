@@ -23,12 +23,11 @@
 // rows 64r..64r+63 of the right planes (2 KiB) in shared memory, and its
 // 128-lane half of the accumulators.  TMEM (512 columns) holds 4 accumulators
 // of 128 columns, so the 8 shifts run as 2 super-passes per K chunk:
-// {4, 5, 6, 7} (26 MMAs per 32-K block, limb planes 0..7) and {0, 1, 2, 3}
-// (10 MMAs, planes 0..3, two 32-K blocks per pipeline stage) — 12 plane loads
-// per operand and 32-K block instead of the 26 a 2-accumulator schedule needs,
-// which keeps the per-SM L2->SM feed at about 31 B/clk for 8192 MAC/clk.  Units
-// (K chunk, super-pass) are ordered chunk major so the second super-pass
-// re-reads a K window still resident in L2.
+// {0, 7, 1, 6} (18 MMAs per 32-K block, limb planes 0..7) and {2, 5, 3, 4}
+// (18 MMAs, planes 0..5) — 14 plane loads per 32-K block instead of the 26 a
+// 2-accumulator schedule needs, which keeps the per-SM L2->SM feed at about
+// 36 B/clk for 8192 MAC/clk.  Units (K chunk, super-pass) are ordered chunk
+// major so the second super-pass re-reads a K window still resident in L2.
 // The u64 running sum of a tile lives in the registers of 8 epilogue warps
 // (64 columns x 1 row per thread; setmaxnreg gives them 216 registers) and is
 // written once, with the Beaver c_p addend and the fused truncation, at the
@@ -135,20 +134,15 @@ struct Bars {
 };
 
 // Super-pass g accumulates 4 shifts into TMEM slots 0..3 (128 columns each):
-// g = 0: shifts {4, 5, 6, 7} (5+6+7+8 = 26 MMAs per 32-K block, limb planes 0..7)
-// g = 1: shifts {0, 1, 2, 3} (1+2+3+4 = 10 MMAs per 32-K block, limb planes 0..3)
-// — 12 plane loads per operand and 32-K block (8 + 4; the round-1 grouping
-// {0,7,1,6} / {2,5,3,4} needed 8 + 6 = 14): 72 instead of 84 KB of L2 -> SMEM
-// traffic per CTA and block, the feed that bounds the kernel.  A
-// pass-1 stage holds TWO 32-K blocks (2 x 24 KB of planes 0..3), so its 20 MMAs
-// take about as long as a pass-0 stage's 26 and the 4-stage ring still looks
-// ahead ~3 stages of MMA time.
-__host__ __device__ constexpr int slot_shift(int g, int a) { return g == 0 ? 4 + a : a; }
-__host__ __device__ constexpr int pass_planes(int g) { return g == 0 ? 8 : 4; }
-__host__ __device__ constexpr int pass_bps(int g) { return g == 0 ? 1 : 2; }   // 32-K blocks per stage
+// g = 0: shifts {0, 7, 1, 6} (1+8+2+7 = 18 MMAs per 32-K block, planes 0..7)
+// g = 1: shifts {2, 5, 3, 4} (3+6+4+5 = 18 MMAs per 32-K block, planes 0..5)
+__host__ __device__ constexpr int slot_shift(int g, int a) {
+    return g == 0 ? ((a & 1) ? 7 - (a >> 1) : (a >> 1)) : ((a & 1) ? 5 - (a >> 1) : 2 + (a >> 1));
+}
+__device__ __forceinline__ int pass_planes(int g) { return g == 0 ? 8 : 6; }
 
 // The limb MMAs of TMEM slots A0 and A0+1 (one release group) for one 32-K
-// block of super-pass G, fully unrolled: every descriptor is the
+// block of super-pass G, fully unrolled (9 MMAs): every descriptor is the
 // stage's base descriptor plus a compile-time offset (A plane i at +4 KiB * i,
 // B plane j at +2 KiB * j; the 14-bit address field never carries for smem
 // addresses < 256 KiB).  FIRST: the block starts a unit, so the first product
@@ -210,11 +204,12 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
             for (int k0 = klo; k0 < khi; k0 += kc) {
                 const int k1 = min(khi, k0 + kc);
                 for (int g = 0; g < kPasses; ++g) {
-                    const uint32_t bytesA = (uint32_t)pass_planes(g) * GL::kBlock;     // per 32-K block
+                    const uint32_t bytesA = (uint32_t)pass_planes(g) * GL::kBlock;
                     const uint32_t bytesB = (uint32_t)pass_planes(g) * GR::kBlock;
-                    const int bps = pass_bps(g);
-                    for (int kt = k0; kt < k1; kt += bps) {
-                        const int nb = min(bps, k1 - kt);                            // blocks in this stage
+                    for (int kt = k0; kt < k1; ++kt) {
+                        const bool second = kt >= kb0;
+                        const uint8_t* srcA = (second ? a1 : a0) + (int64_t)kt * (8 * GL::kBlock);
+                        const uint8_t* srcB = (second ? b1 : b0) + (int64_t)kt * (8 * GR::kBlock);
                         if (p.dbg) { const long long w0 = clock64(); mbar_wait(&B.empty[s], ph ^ 1); st_empty += clock64() - w0; }
                         else mbar_wait(&B.empty[s], ph ^ 1);
                         if (TMA) {
@@ -222,26 +217,20 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
                             // barrier, which expects both halves' bytes (rows of 2 KiB; the maps
                             // start at the segment's plane buffer)
                             if (elect_one()) {
-                                if (leader) mbar_expect_tx(&B.full[s], 2 * (uint32_t)nb * (bytesA + bytesB));
+                                if (leader) mbar_expect_tx(&B.full[s], 2 * (bytesA + bytesB));
                                 const uint32_t fb = mapa(smem_u32(&B.full[s]), 0);
                                 const uint8_t* st = B.stage_base + s * kStageBytes;
-                                for (int bb = 0; bb < nb; ++bb) {
-                                    const int ktb = kt + bb;
-                                    const bool second = ktb >= kb0;
-                                    const uint8_t* srcA = (second ? a1 : a0) + (int64_t)ktb * (8 * GL::kBlock);
-                                    const uint8_t* srcB = (second ? b1 : b0) + (int64_t)ktb * (8 * GR::kBlock);
-                                    const RingGemmSegment& Sx = second ? S1 : S0;
-                                    const uint32_t dA = smem_u32(st + bb * bytesA);
-                                    const uint32_t dB = smem_u32(st + kAStage + bb * bytesB);
-                                    if (p.tma_l2 == 3) {
-                                        tma_load_2d_2sm(dA, &p.tma.a[second ? 1 : 0][g], 0, (int)((srcA - Sx.A) >> 11), fb);
-                                        tma_load_2d_2sm(dB, &p.tma.b[second ? 1 : 0][g], 0, (int)((srcB - Sx.B) >> 11), fb);
-                                    } else {
-                                        tma_load_2d_2sm_hint(dA, &p.tma.a[second ? 1 : 0][g], 0,
-                                                             (int)((srcA - Sx.A) >> 11), fb, l2pol);
-                                        tma_load_2d_2sm_hint(dB, &p.tma.b[second ? 1 : 0][g], 0,
-                                                             (int)((srcB - Sx.B) >> 11), fb, l2pol);
-                                    }
+                                const RingGemmSegment& Sx = second ? S1 : S0;
+                                if (p.tma_l2 == 3) {
+                                    tma_load_2d_2sm(smem_u32(st), &p.tma.a[second ? 1 : 0][g], 0,
+                                                    (int)((srcA - Sx.A) >> 11), fb);
+                                    tma_load_2d_2sm(smem_u32(st + kAStage), &p.tma.b[second ? 1 : 0][g], 0,
+                                                    (int)((srcB - Sx.B) >> 11), fb);
+                                } else {
+                                    tma_load_2d_2sm_hint(smem_u32(st), &p.tma.a[second ? 1 : 0][g], 0,
+                                                         (int)((srcA - Sx.A) >> 11), fb, l2pol);
+                                    tma_load_2d_2sm_hint(smem_u32(st + kAStage), &p.tma.b[second ? 1 : 0][g], 0,
+                                                         (int)((srcB - Sx.B) >> 11), fb, l2pol);
                                 }
                             }
                             __syncwarp();
@@ -250,17 +239,11 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
                         }
                         const bool drop = FAULT && kt == klo && w == (int)cluster_id();
                         if (elect_one()) {
-                            mbar_expect_tx(&B.full[s], (uint32_t)nb * (bytesA + bytesB));
+                            mbar_expect_tx(&B.full[s], bytesA + bytesB);
                             uint8_t* st = B.stage_base + s * kStageBytes;
                             if (!drop) {
-                                for (int bb = 0; bb < nb; ++bb) {
-                                    const int ktb = kt + bb;
-                                    const bool second = ktb >= kb0;
-                                    const uint8_t* srcA = (second ? a1 : a0) + (int64_t)ktb * (8 * GL::kBlock);
-                                    const uint8_t* srcB = (second ? b1 : b0) + (int64_t)ktb * (8 * GR::kBlock);
-                                    bulk_g2s(st + bb * bytesA, srcA, bytesA, &B.full[s]);
-                                    bulk_g2s(st + kAStage + bb * bytesB, srcB, bytesB, &B.full[s]);
-                                }
+                                bulk_g2s(st, srcA, bytesA, &B.full[s]);
+                                bulk_g2s(st + kAStage, srcB, bytesB, &B.full[s]);
                             }
                         }
                         __syncwarp();
@@ -276,20 +259,13 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
         if (!TMA) {
             int s = 0; uint32_t ph = 0;
             const uint32_t leader_full0 = mapa(smem_u32(&B.full[0]), 0);
-            for (int w = cluster_id(); w < wm.items(); w += nclusters()) {
-                int party, m, n, klo, khi;
-                wm.decode(w, party, m, n, klo, khi);
-                for (int k0 = klo; k0 < khi; k0 += kc) {
-                    const int nk = min(khi, k0 + kc) - k0;
-                    const int stages = nk + (nk + pass_bps(1) - 1) / pass_bps(1);     // pass 0 + pass 1
-                    for (int i = 0; i < stages; ++i) {
-                        mbar_wait(&B.full[s], ph);
-                        if (elect_one()) mbar_arrive_cluster(leader_full0 + s * 8);
-                        __syncwarp();
-                        if (++s == kStages) { s = 0; ph ^= 1; }
-                    }
+            for (int w = cluster_id(); w < wm.items(); w += nclusters())
+                for (int i = 0; i < kPasses * wm.item_kb(w); ++i) {
+                    mbar_wait(&B.full[s], ph);
+                    if (elect_one()) mbar_arrive_cluster(leader_full0 + s * 8);
+                    __syncwarp();
+                    if (++s == kStages) { s = 0; ph ^= 1; }
                 }
-            }
         }
     } else if (warp == 1) {
         // ------------------------------------------------ leader: MMA issuer (one elected lane)
@@ -302,37 +278,30 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
             for (int k0 = klo; k0 < khi; k0 += kc) {
                 const int k1 = min(khi, k0 + kc);
                 for (int g = 0; g < kPasses; ++g, ++u) {
-                    const int bps = pass_bps(g);
-                    for (int kt = k0; kt < k1; kt += bps) {
+                    for (int kt = k0; kt < k1; ++kt) {
                         {
                             const long long w0 = p.dbg ? clock64() : 0;
                             mbar_wait_cluster(&B.full[s], ph);
                             if (p.dbg) st_full += clock64() - w0;
                         }
                         tc_fence_after();
-                        const uint64_t da0 = smem_desc(smem_u32(B.stage_base + s * kStageBytes));
-                        const uint64_t db0 = da0 + (kAStage >> 4);
-                        const int nb = min(bps, k1 - kt);
-                        for (int bb = 0; bb < nb; ++bb) {
-                            // block bb of the stage: planes at bb x (planes x block) in each operand region
-                            const uint64_t da = da0 + (uint64_t)(bb * ((pass_planes(1) * GL::kBlock) >> 4));
-                            const uint64_t db = db0 + (uint64_t)(bb * ((pass_planes(1) * GR::kBlock) >> 4));
-                            if (kt + bb == k0) {
-                                // first block of the unit: each slot pair may be overwritten once both
-                                // epilogues have drained it (the pair-1 drain overlaps pair-0 MMAs)
-                                const long long w0 = p.dbg ? clock64() : 0;
-                                mbar_wait_cluster(&B.tempty[0], (u & 1) ^ 1);
-                                if (p.dbg) st_tempty += clock64() - w0;
-                                tc_fence_after();
-                                if (g == 0) issue_slots<0, true, 0>(da, db, tmem_base); else issue_slots<1, true, 0>(da, db, tmem_base);
-                                const long long w1 = p.dbg ? clock64() : 0;
-                                mbar_wait_cluster(&B.tempty[1], (u & 1) ^ 1);
-                                if (p.dbg) st_tempty += clock64() - w1;
-                                tc_fence_after();
-                                if (g == 0) issue_slots<0, true, 2>(da, db, tmem_base); else issue_slots<1, true, 2>(da, db, tmem_base);
-                            } else {
-                                if (g == 0) issue_kblock<0>(da, db, tmem_base); else issue_kblock<1>(da, db, tmem_base);
-                            }
+                        const uint64_t da = smem_desc(smem_u32(B.stage_base + s * kStageBytes));
+                        const uint64_t db = da + (kAStage >> 4);
+                        if (kt == k0) {
+                            // first block of the unit: each slot pair may be overwritten once both
+                            // epilogues have drained it (the pair-1 drain overlaps pair-0 MMAs)
+                            const long long w0 = p.dbg ? clock64() : 0;
+                            mbar_wait_cluster(&B.tempty[0], (u & 1) ^ 1);
+                            if (p.dbg) st_tempty += clock64() - w0;
+                            tc_fence_after();
+                            if (g == 0) issue_slots<0, true, 0>(da, db, tmem_base); else issue_slots<1, true, 0>(da, db, tmem_base);
+                            const long long w1 = p.dbg ? clock64() : 0;
+                            mbar_wait_cluster(&B.tempty[1], (u & 1) ^ 1);
+                            if (p.dbg) st_tempty += clock64() - w1;
+                            tc_fence_after();
+                            if (g == 0) issue_slots<0, true, 2>(da, db, tmem_base); else issue_slots<1, true, 2>(da, db, tmem_base);
+                        } else {
+                            if (g == 0) issue_kblock<0>(da, db, tmem_base); else issue_kblock<1>(da, db, tmem_base);
                         }
                         tc_commit_both(&B.empty[s]);
                         if (++s == kStages) { s = 0; ph ^= 1; }
@@ -350,29 +319,23 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
 }
 
 // ---------------------------------------------------------------- epilogue warpgroups
-// run[j] += acc_S0[j] * 2^(8 S0) + acc_S1[j] * 2^(8 S1)  (mod 2^64) for the 64
-// columns of this thread, with acc read as u32 (exact for S <= 3; for S >= 4 only
-// acc mod 2^(64-8S) matters, so the 32-bit wrap is harmless).  Shifts >= 4 only
-// touch the high word: their sum is formed in 32 bits and added once.
+// run[j] += acc_S[j] * 2^(8S) + acc_{7-S}[j] * 2^(8(7-S))  (mod 2^64) for the 64
+// columns of this thread, with acc read as u32.  Compile-time S: the two 32-bit
+// halves of the contribution are built with constant shifts (the 7-S term only
+// touches the high word), then one 64-bit add.
 template <int S>
-__device__ __forceinline__ uint64_t shifted(uint32_t v) {
-    if constexpr (S >= 4) return (uint64_t)(v << (8 * S - 32)) << 32;
-    else return (uint64_t)v << (8 * S);
-}
-template <int S0, int S1>
-__device__ __forceinline__ void drain2(uint64_t (&run)[64], uint32_t t0, uint32_t t1) {
+__device__ __forceinline__ void drain_pair(uint64_t (&run)[64], uint32_t t_lo, uint32_t t_hi) {
 #pragma unroll
     for (int cc = 0; cc < 64; cc += 16) {
         uint32_t a[16], b[16];
-        tmem_ld16(t0 + cc, a);
-        tmem_ld16(t1 + cc, b);
+        tmem_ld16(t_lo + cc, a);
+        tmem_ld16(t_hi + cc, b);
         tmem_wait_ld();
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-            if constexpr (S0 >= 4 && S1 >= 4)
-                run[cc + j] += (uint64_t)((a[j] << (8 * S0 - 32)) + (b[j] << (8 * S1 - 32))) << 32;
-            else
-                run[cc + j] += shifted<S0>(a[j]) + shifted<S1>(b[j]);
+            const uint32_t lo32 = a[j] << (8 * S);
+            const uint32_t hi32 = (S == 0 ? 0u : (a[j] >> (32 - 8 * S))) + (b[j] << (24 - 8 * S));
+            run[cc + j] += ((uint64_t)hi32 << 32) | lo32;
         }
     }
 }
@@ -407,13 +370,13 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Wor
                 tc_fence_after();
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    // slot pair h of super-pass g holds shifts slot_shift(g, 2h), slot_shift(g, 2h + 1)
+                    // slot pair h of super-pass g holds shifts (S, 7-S) with S = 2g + h
                     const uint32_t tl = tbase + (2 * h) * 128, th = tl + 128;
                     switch (2 * g + h) {
-                        case 0: drain2<slot_shift(0, 0), slot_shift(0, 1)>(run, tl, th); break;
-                        case 1: drain2<slot_shift(0, 2), slot_shift(0, 3)>(run, tl, th); break;
-                        case 2: drain2<slot_shift(1, 0), slot_shift(1, 1)>(run, tl, th); break;
-                        default: drain2<slot_shift(1, 2), slot_shift(1, 3)>(run, tl, th); break;
+                        case 0: drain_pair<0>(run, tl, th); break;
+                        case 1: drain_pair<1>(run, tl, th); break;
+                        case 2: drain_pair<2>(run, tl, th); break;
+                        default: drain_pair<3>(run, tl, th); break;
                     }
                     tc_fence_before();
                     __syncwarp();
@@ -535,7 +498,7 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     if (p.dbg && threadIdx.x == 0) atomicMax(&p.dbg[5], globaltimer());
     // register budget: the control warpgroup needs few, the epilogue holds 64 u64 sums per thread
     if (warp < 4) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
         control_roles<FAULT, TMA>(p, wm, warp, lane, rank, tmem_base, B);
         if (p.dbg && warp == 1 && lane == 0 && rank == 0) atomicMax(&p.dbg[6], globaltimer());
     } else {
@@ -635,7 +598,7 @@ static bool fill_tma(RingGemmParams& q, int parties) {
         const uint64_t extB = instB + (uint64_t)(parties - 1) * S.party_stride_B + (uint64_t)(nb - 1) * S.batch_stride_B;
         if ((S.party_stride_A | S.party_stride_B | S.batch_stride_A | S.batch_stride_B) % kTmaRow) return false;
         for (int g = 0; g < gemm::kPasses; ++g) {
-            const int planes = gemm::pass_planes(g);
+            const int planes = g == 0 ? 8 : 6;
             if (!encode_rows(&q.tma.a[sg][g], S.A, extA, planes * gemm::GL::kBlock / kTmaRow) ||
                 !encode_rows(&q.tma.b[sg][g], S.B, extB, planes * gemm::GR::kBlock / kTmaRow))
                 return false;
