@@ -100,8 +100,14 @@ def c5(P, n=8192, steps=3):
     ctx.profile_enable(False)
     k = steps + 1
     tg = bench_layers.t_gemm_ms(n, n, n, parties=P)
+    hbm = bench_layers.hbm_gbs()
+    t_ms, s_ms = trunc_ms / k, split_ms / k
     out = {"ms_per_private_matmul": ms, "ring_TOPS": 2.0 * n ** 3 / (ms * 1e-3) / 1e12,
-           "gemm_ms": gemm_ms / k, "alg1_truncation_ms": trunc_ms / k, "split_ms": split_ms / k,
+           "gemm_ms": gemm_ms / k, "alg1_truncation_ms": t_ms, "split_ms": s_ms,
+           # Alg. 1 (seeded TTP): reads and writes every party's share, 16 P B per element
+           "alg1_hbm_frac": 16.0 * P * n * n / (t_ms * 1e-3) / (hbm * 1e9) if t_ms > 0 else None,
+           # mask + local reveal + split: (3P + 1) x 8 B per element of both operands
+           "split_hbm_frac": 2 * (3 * P + 1) * 8.0 * n * n / (s_ms * 1e-3) / (hbm * 1e9) if s_ms > 0 else None,
            "roofline_ms": tg, "roofline_frac": tg / ms,
            "note": f"all {P} parties on one GPU (the GEMM work is P x 144 n^3); one party per GPU is the NCCL path"}
     del x, y, a, b, c, z
@@ -112,11 +118,12 @@ def c5(P, n=8192, steps=3):
 def one_party_schedule(n=4096, steps=10):
     """One party per GPU, as the N-GPU bench runs it, on this GPU: a 1-rank NCCL
     communicator (its allreduces are copies, so no NVLink time is measured) runs
-    the overlapped schedule — mask, delta then eps reveal on the comm stream, a_p
-    split + phase-1 GEMM on 132 SMs, eps split + phase-2 GEMM — against the fused
-    single-GEMM schedule of a context without communicator (P = 1 both).  The
-    difference is what the overlap structure itself costs (two GEMM launches,
-    16 SMs left to NCCL during phase 1)."""
+    the overlapped schedule — mask, eps (row chunks) then delta reveal on the comm
+    stream, b_p split + per-chunk eps split and phase-1 GEMM (eps @ b_p) on 132 SMs,
+    delta split + phase-2 GEMM (a'_p @ delta) — against the fused single-GEMM
+    schedule of a context without communicator (P = 1 both).  The difference is
+    what the overlap structure itself costs (chunked phase-1 launches, 16 SMs left
+    to NCCL during phase 1)."""
     gen = torch.Generator(device="cuda").manual_seed(7)
     x = torch.randint(-8 << 16, 8 << 16, (n, n), device="cuda", generator=gen).view(torch.uint64)
     y = torch.randint(-8 << 16, 8 << 16, (n, n), device="cuda", generator=gen).view(torch.uint64)
