@@ -63,7 +63,7 @@ def run_layer(ctx, M, K, N, reps, graph):
     return ms, (gemm_ms / reps if not graph else None)
 
 
-def run_chain(ctx, layers, reps, prepared=False, offline=False):
+def run_chain(ctx, layers, reps, prepared=False, offline=False, hook=None):
     """All layers of one model in one CUDA graph; returns ms per pass.
 
     prepared: the weight side of every private matmul (delta reveal, delta and
@@ -151,6 +151,8 @@ def run_chain(ctx, layers, reps, prepared=False, offline=False):
     for _ in range(3):
         g.replay()
     torch.cuda.synchronize()
+    if hook is not None:              # e.g. a kernel timeline of one replay (scripts/chain_timeline.py)
+        hook(g)
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
     for _ in range(reps):

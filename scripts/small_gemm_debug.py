@@ -11,7 +11,7 @@ import synth  # noqa: E402
 import paper_2109_00984_b200 as m  # noqa: E402
 
 c = m.Context(2, m.ALL_PARTIES, device=0, master_seed=synth.MASTER_SEED)
-shapes = [(3136, 64, 64), (3136, 576, 64), (784, 1152, 128), (196, 2304, 256), (49, 4608, 512),
+shapes = [(3136, 64, 256), (784, 128, 512), (196, 256, 1024), (3136, 64, 64), (3136, 576, 64), (784, 1152, 128), (196, 2304, 256), (49, 4608, 512),
           (197, 768, 768), (197, 768, 3072), (197, 3072, 768), (12544, 147, 64), (1, 2048, 1000)]
 for (M, K, N) in shapes:
     dev = lambda a: torch.from_numpy(a.view(np.int64)).cuda().view(torch.uint64)  # noqa: E731
