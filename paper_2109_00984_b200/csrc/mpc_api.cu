@@ -281,6 +281,7 @@ struct BeaverWs {
     int64_t a_stride, b_stride;   // bytes between parties' a_p / b'_p planes
     bool swap;                    // transposed ring GEMM (choose_gemm)
     bool small;                   // stacked-plane GEMM, planes in Layout::Small (choose_gemm)
+    bool fused;                   // the fused 2-party small-output kernel (no planes; use_fused_small)
     uint64_t* ed;        // one-party mode: [e | d] reveal buffer
     uint64_t* zbuf;      // one-party, P > 2, truncation: z reveal
     int8_t* hbuf;        // one-party, P > 2, truncation: top nibbles
@@ -316,12 +317,27 @@ inline void chunk_rows(int64_t M, int i, int c, int64_t& m0, int64_t& m1) {
 // ed_elems: size of the one-party [e | d] reveal buffer (default M*K + K*N; a
 // convolution reveals at the input / weight shapes instead).  allow_swap: the
 // transposed GEMM is possible for this output layout.
+// The fused small-output kernel (ring_gemm_fused.cu) serves mpc_beaver_matmul when both
+// parties of a 2-party context are on this GPU, M, N <= 32 and K is long enough for its
+// split-K grid (>= 64 32-K blocks); MPC_FUSED_SMALL=0 keeps the planes-based path.
+bool use_fused_small(mpc_ctx c, int64_t M, int64_t K, int64_t N) {
+    static const int env = getenv("MPC_FUSED_SMALL") ? atoi(getenv("MPC_FUSED_SMALL")) : 1;
+    return env != 0 && c->all && c->P == 2 && M >= 1 && M <= 32 && N >= 1 && N <= 32 && num_kb(K) >= 64;
+}
+
 BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N, int64_t ed_elems = -1,
-                      bool allow_swap = true, bool allow_small = true, int64_t batch = 1) {
+                      bool allow_swap = true, bool allow_small = true, int64_t batch = 1, bool allow_fused = false) {
     const int Pl = c->all ? c->P : 1;
     Carve cv(ws);
     BeaverWs w{};
     w.batch = batch < 1 ? 1 : batch;
+    if (allow_fused && w.batch == 1 && use_fused_small(c, M, K, N)) {
+        w.fused = true;
+        const size_t pb = fused_small_partials_bytes(M, K, N);
+        w.partials = reinterpret_cast<uint64_t*>(pb ? cv.take(pb) : nullptr);
+        w.total = cv.off;
+        return w;
+    }
     const int inst = (int)(Pl * w.batch);                     // GEMM instances
     const GemmChoice gc = choose_gemm(inst, M, N, K, allow_swap, allow_small);
     w.swap = gc.swap;
@@ -835,7 +851,10 @@ mpc_status mpc_ttp_wrap_pairs(mpc_ctx c, uint64_t id, int64_t n, uint64_t* r, ui
 
 size_t mpc_workspace_bytes(mpc_ctx c, int64_t M, int64_t K, int64_t N) {
     if (!c || M < 0 || K < 0 || N < 0) return 0;
-    return carve_beaver(c, nullptr, M, K, N).total;
+    // the planes-based layout (mpc_beaver_prepare / _matmul_prepared / _finish use it) covers
+    // the fused small-output kernel's partials too
+    return std::max(carve_beaver(c, nullptr, M, K, N).total,
+                    carve_beaver(c, nullptr, M, K, N, -1, true, true, 1, true).total);
 }
 
 mpc_status mpc_beaver_matmul(mpc_ctx c, const uint64_t* x, const uint64_t* y, const uint64_t* a, const uint64_t* b,
@@ -844,7 +863,7 @@ mpc_status mpc_beaver_matmul(mpc_ctx c, const uint64_t* x, const uint64_t* y, co
     CHECK(enter(c));
     if (M < 0 || K < 0 || N < 0) return fail(c, MPC_ERR_SHAPE, "beaver_matmul: negative size");
     if (K > (int64_t)1 << 30 || M > (int64_t)1 << 31 || N > (int64_t)1 << 31) return fail(c, MPC_ERR_SHAPE, "beaver_matmul: too large");
-    const BeaverWs w = carve_beaver(c, ws, M, K, N);
+    const BeaverWs w = carve_beaver(c, ws, M, K, N, -1, true, true, 1, true);
     if (ws_bytes < w.total) return fail(c, MPC_ERR_SHAPE, "beaver_matmul: workspace %zu < %zu", ws_bytes, w.total);
     const int Pl = c->all ? c->P : 1;
     c->rounds += 1;                                   // eps || delta: one batched reveal
@@ -853,6 +872,10 @@ mpc_status mpc_beaver_matmul(mpc_ctx c, const uint64_t* x, const uint64_t* y, co
     if ((M * K && (!x || !a)) || (K * N && (!y || !b)) || !cc || !z || (!ws && w.total))
         return fail(c, MPC_ERR_ARG, "beaver_matmul: null pointer");
     const int64_t sMK = M * K, sKN = K * N, sMN = M * N;
+    if (w.fused) {
+        FusedSmallParams f{x, a, y, b, cc, z, M, K, N, truncate ? c->frac : 0, w.partials};
+        return run(c, kClsGemm, "fused beaver (small)", [&] { return fused_small_launch(f, c->stream); });
+    }
     if (c->all) {
         LeftSplitArgs L{M, K, sMK, x, a, c->P, w.eps_pl, a, c->P, w.a_pl, w.a_stride, lay(w)};
         RightSplitArgs R{K, N, sKN, y, b, c->P, w.delta_pl, b, c->P, 1, w.b_pl, w.b_stride, lay(w)};

@@ -88,4 +88,28 @@ int64_t ring_gemm_out_elems(const RingGemmParams& q, int parties);
 cudaError_t ring_gemm_finalize(const RingGemmParams& q, int parties, cudaStream_t stream);
 cudaError_t ring_gemm_launch(const RingGemmParams& p, int parties, cudaStream_t stream);
 
+// The fused 2-party Beaver matmul for M <= 32, N <= 32 with both parties on this GPU
+// (ring_gemm_fused.cu): mask, local reveal, limb split and limb GEMM in one kernel,
+// reading the u64 shares once; split-K slabs added by ring_gemm_finalize.
+struct FusedSmallParams {
+    const uint64_t *x, *a;              // [2][M][K] row-major (party stride M*K)
+    const uint64_t *y, *b;              // [2][K][N] row-major (party stride K*N)
+    const uint64_t* C;                  // [2][M][N] Beaver c_p (may be null)
+    uint64_t* Z;                        // [2][M][N]
+    int64_t M, K, N;
+    int trunc_bits;                     // 0 or the per-share truncation (P <= 2, R10)
+    uint64_t* partials;                 // fused_small_partials_bytes (null when 0)
+    int unit;                           // set by the launcher: 32-K blocks per drained TMEM unit
+    int pf_mode;                        // set by the launcher: L2 prefetch of the x / a rows (0 none,
+                                        // 1 line prefetches, 2 one bulk prefetch per row; MPC_FUSED_PF)
+    int pf_dist;                        // set by the launcher: blocks the L2 prefetch runs ahead
+    int cyclic;                         // set by the launcher: 32-K blocks dealt to the CTAs round-robin
+    unsigned long long* dbg;            // MPC_FUSED_DEBUG: [0] MMA full-wait, [1] MMA total, [2] converter
+                                        // empty-wait, [3] converter total cycles (summed over CTAs / warps)
+};
+size_t fused_small_smem_bytes();
+int fused_small_ctas(int64_t K, int sms);
+size_t fused_small_partials_bytes(int64_t M, int64_t K, int64_t N);
+cudaError_t fused_small_launch(const FusedSmallParams& p, cudaStream_t stream);
+
 }  // namespace mpc

@@ -1,0 +1,498 @@
+// ring_gemm_fused.cu — the whole 2-party Beaver private matmul of a small output
+// (M <= 32, N <= 32, both parties on this GPU) in one tcgen05 kernel: mask, local
+// reveal, limb split and the limb GEMM, with the u64 shares read from HBM once.
+//
+// The planes-based path (split kernel -> limb planes in HBM -> ring GEMM) reads
+// the four u64 share inputs, writes six plane sets (eps, a_0, a_1, delta, b'_0,
+// b'_1) and reads them back: for the wide-K text matmul (32 x 519,820 x 32, P:397-
+// 410) that is 1.9 GB + 0.8 GB against the 1.06 GB the protocol
+// must read.  Here each CTA takes a K range of the one 32 x 32 output tile and,
+// per 32-K block, its converter warps load x_p, a_p (32 x 32 each) and y_p, b_p
+// (32 x 32 each) straight into registers, form (R7/R8)
+//     eps = sum_p (x_p - a_p),   delta = sum_p (y_p - b_p),   b'_0 = b_0 + delta,
+// and write the u8 limb planes of eps, a_0, a_1, delta, b'_0, b'_1 into a shared-
+// memory stage in the UMMA canonical K-major layout; one elected thread issues
+//     z_p = c_p + a_p @ delta + eps @ b'_p          (mod 2^64, p = 0, 1)
+// as stacked-plane MMAs (ring_gemm_small.cu): A = 4 left planes stacked along M
+// (M = 128: lanes 32 i' + r), B = one right plane.  Both parties accumulate into
+// the SAME 8 TMEM accumulators D_0..D_7 of 64 columns (party p: columns 32p..):
+//   eps @ b'_p : one N = 64 MMA covers both parties (b'_0 / b'_1 plane j stored
+//                as one 64-row operand), A_lo = eps planes 0-3 -> D_j (j = 0..7),
+//                A_hi = eps planes 4-7 -> D_{j+4} (j = 0..3);
+//   a_p @ delta: N = 32 per party, A_lo(a_p) -> D_j, A_hi(a_p) -> D_{j+4}.
+// Lane group i' of D_j then holds shift i' + j for both A_lo (plane i', right
+// plane j) and A_hi (plane 4 + i', right plane j - 4), so 8 accumulators x 64
+// columns = all 512 TMEM columns hold both parties (the stacked kernel needs 12
+// per party).  Exactness: an entry sums at most 2 products per K for shifts
+// <= 3 (no A_hi term), so reading it as u32 is exact for units of <= 1032 32-K
+// blocks; shifts >= 4 only need the entry mod 2^(64 - 8s) (<= 2^32).
+//
+// Split-K over the CTAs (one per SM), the 32-K blocks dealt round-robin so the
+// CTAs stream neighbouring 256-byte row pieces of x / a through DRAM together;
+// slab g of the partials buffer holds CTA g's [2][M][N] sum, and
+// ring_gemm_finalize adds the slabs, c_p and the per-share truncation (P <= 2,
+// R10).  Bit-identical to the planes-based path: the same ring sums, and
+// unsigned addition commutes.
+//
+// Warps: 0 = TMEM allocator and MMA issuer (one thread), 1..3 idle, 4..7 = left
+// converters (8 rows each), 8..11 = right converters (8 output columns each),
+// which also prefetch their inputs kPrefetch blocks ahead into L2, drain TMEM at
+// unit ends into shared-memory output sums (a warp reads the TMEM lane quadrant
+// warp % 4; warps 4..7 hold party 0, 8..11 party 1) and write the slab.
+//
+// Measured (text 32 x 519,820 x 32, one B200; scripts/gpu/fused*.sh): 0.49 ms for
+// the planes-based path -> 0.30 ms.  MPC_FUSED_DEBUG stall attribution: the
+// converter warps are busy 94% of the kernel (load latency: long-scoreboard), the
+// MMA thread 58% (36 MMAs of N = 32/64 per 32-K block, shared-memory bound at
+// ~70 cycles each).  Kept as tuning knobs, all slower here: two blocks of loads
+// in flight per thread (MPC_FUSED_DEPTH=2, registers moved by setmaxnreg: 0.32-
+// 0.37 ms), longer prefetch distances (MPC_FUSED_PFD 4..12: 0.34-0.41 ms), bulk
+// prefetches of the row pieces (MPC_FUSED_PF=2: 0.37-0.40 ms, message-rate
+// bound), contiguous K ranges per CTA (MPC_FUSED_CYCLIC=0: +2-4%).
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "ring_gemm.h"
+#include "tcgen05.cuh"
+
+namespace mpc {
+namespace gemm_fused {
+using namespace tc;
+
+constexpr int kRows = 32;                         // output rows and columns of the tile
+constexpr int kPlane = 1024;                      // one limb plane of 32 rows x 32 K
+constexpr int kSet = 8 * kPlane;                  // the 8 planes of one operand
+// stage: [eps][a_0][a_1][delta] sets, then the b' pair set (plane j of b'_0 at
+// j * 2 KiB, of b'_1 1 KiB after it: the 64-row B operand of the eps @ b' MMA)
+constexpr int kOffEps = 0, kOffA0 = kSet, kOffA1 = 2 * kSet, kOffDelta = 3 * kSet, kOffPair = 4 * kSet;
+constexpr int kStageBytes = 6 * kSet;             // 48 KiB
+constexpr int kStages = 4;
+constexpr int kThreads = 384;                     // warp 0: TMEM allocator + MMA issuer; 4..11: converters
+constexpr int kConvWarps = 8;
+constexpr int kTmemCols = 512;
+constexpr int kMaxUnit = 1032;                    // 32-K blocks per accumulation unit (exact, see above)
+constexpr int kPrefetch = 2;                      // 32-K blocks the L2 prefetch runs ahead (2 measured best of 0-12)
+__host__ __device__ constexpr uint32_t idesc(int n) {
+    return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);   // S32 <- u8 x u8, M = 128
+}
+
+__device__ __forceinline__ void mma_u8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t id, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+        :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(id), "r"(acc) : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void conv_sync() {            // the 8 converter / epilogue warps
+    asm volatile("bar.sync 1, %0;" :: "n"(32 * kConvWarps) : "memory");
+}
+// bulk L2 prefetch of [p, p + bytes): the instruction takes a 16-byte aligned start and size
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p), a0 = a & ~uintptr_t(15);
+    const uint32_t n = (uint32_t)((a + bytes - a0 + 15) & ~uintptr_t(15));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(a0), "r"(n) : "memory");
+}
+__device__ __forceinline__ void prefetch_l2_line(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" :: "l"(p));
+}
+
+// 8 consecutive-k values of one row -> byte l of each into plane l (8 bytes at
+// `off` inside every plane of the set; planes `pstride` bytes apart)
+__device__ __forceinline__ void st_planes8(uint8_t* set, uint32_t off, int pstride, const uint64_t (&v)[8]) {
+    uint32_t w[8][2];
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        uint32_t lo[4], hi[4];
+        transpose4x4((uint32_t)v[4 * g], (uint32_t)v[4 * g + 1], (uint32_t)v[4 * g + 2], (uint32_t)v[4 * g + 3], lo);
+        transpose4x4((uint32_t)(v[4 * g] >> 32), (uint32_t)(v[4 * g + 1] >> 32), (uint32_t)(v[4 * g + 2] >> 32),
+                     (uint32_t)(v[4 * g + 3] >> 32), hi);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) { w[l][g] = lo[l]; w[4 + l][g] = hi[l]; }
+    }
+#pragma unroll
+    for (int l = 0; l < 8; ++l)
+        *reinterpret_cast<uint2*>(set + off + l * pstride) = make_uint2(w[l][0], w[l][1]);
+}
+
+// (row, 8-K quarter kq) -> byte offset of its 8-byte run inside a 32-row plane
+__device__ __forceinline__ uint32_t plane_off(int row, int kq) {
+    return (uint32_t)((row >> 3) * 256 + (kq >> 1) * 128 + (row & 7) * 16 + (kq & 1) * 8);
+}
+
+// 8 consecutive u64 of one row of a row-major matrix (0 past `left` valid values)
+__device__ __forceinline__ void load_row8(const uint64_t* __restrict__ src, int64_t left, bool vec, uint64_t (&v)[8]) {
+    if (vec && left >= 8) {
+        const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(src);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) { const ulonglong2 t = __ldg(s2 + m); v[2 * m] = t.x; v[2 * m + 1] = t.y; }
+    } else {
+#pragma unroll
+        for (int m = 0; m < 8; ++m) v[m] = m < left ? __ldg(src + m) : 0ull;
+    }
+}
+
+template <int DEPTH>
+__global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const __grid_constant__ FusedSmallParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");   // the finalize may launch
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes + 2 * kRows * kRows * 8);
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t M = p.M, K = p.K, N = p.N;
+    const int KB = (int)num_kb(K);
+    const int g = blockIdx.x, G = gridDim.x;
+    // this CTA's 32-K blocks: i -> g + i * G (block-cyclic: at any moment the CTAs read neighbouring
+    // blocks of the same rows, so the 256-byte row pieces of x / a stream through DRAM pages in order),
+    // or a contiguous range (MPC_FUSED_CYCLIC=0)
+    const int kb0 = (int)((int64_t)KB * g / G);
+    const int nblk = p.cyclic ? (KB > g ? (KB - g + G - 1) / G : 0) : (int)((int64_t)KB * (g + 1) / G) - kb0;
+    auto kt_of = [&](int i) { return p.cyclic ? g + i * G : kb0 + i; };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], kConvWarps); mbar_init(&empty[s], 1); }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, kConvWarps);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(smem_u32(tmem_slot)), "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int64_t sMK = M * K, sKN = K * N;
+
+    if (warp < 4) {
+        // ------------------------------------------------ MMA issuer (one thread of warp 0)
+        if (DEPTH == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+      if (warp == 0) {
+        if (lane == 0) {
+            int s = 0; uint32_t ph = 0; uint32_t u = 0;
+            long long dbg_full = 0;
+            const long long t_mma0 = clock64();
+            for (int k0 = 0; k0 < nblk; k0 += p.unit, ++u) {
+                const int k1 = min(nblk, k0 + p.unit);
+                mbar_wait(tempty, (u & 1) ^ 1);                               // last unit drained
+                tc_fence_after();
+                for (int kt = k0; kt < k1; ++kt) {
+                    const long long w0 = p.dbg ? clock64() : 0;
+                    mbar_wait(&full[s], ph);
+                    if (p.dbg) dbg_full += clock64() - w0;
+                    tc_fence_after();
+                    const uint32_t st = smem_u32(smem + s * kStageBytes);
+                    const uint64_t dE = smem_desc(st + kOffEps), dP = smem_desc(st + kOffPair);
+                    const uint64_t dD = smem_desc(st + kOffDelta);
+                    const uint32_t first = kt == k0 ? 0u : 1u;
+                    // eps @ b'_p, both parties in one N = 64 MMA; the lo MMAs open every accumulator
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        mma_u8(tmem_base + j * 64, dE, dP + (uint64_t)(j * (2 * kPlane) >> 4), idesc(64), first);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        mma_u8(tmem_base + (j + 4) * 64, dE + (uint64_t)((4 * kPlane) >> 4),
+                               dP + (uint64_t)(j * (2 * kPlane) >> 4), idesc(64), 1u);
+                    // a_p @ delta, per party (N = 32, the party's 32 columns)
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const uint64_t dA = smem_desc(st + (q ? kOffA1 : kOffA0));
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            mma_u8(tmem_base + j * 64 + q * 32, dA, dD + (uint64_t)((j * kPlane) >> 4), idesc(32), 1u);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            mma_u8(tmem_base + (j + 4) * 64 + q * 32, dA + (uint64_t)((4 * kPlane) >> 4),
+                                   dD + (uint64_t)((j * kPlane) >> 4), idesc(32), 1u);
+                    }
+                    tc_commit(&empty[s]);
+                    if (++s == kStages) { s = 0; ph ^= 1; }
+                }
+                tc_commit(tfull);
+            }
+            if (p.dbg) {
+                atomicAdd(&p.dbg[0], (unsigned long long)dbg_full);
+                atomicAdd(&p.dbg[1], (unsigned long long)(clock64() - t_mma0));
+            }
+        }
+        __syncwarp();
+      }
+    } else {
+        // ------------------------------------------------ converters, then the TMEM drain
+        // registers: the control warpgroup frees 112 per thread (168 -> 56), the converters take
+        // 48 more (168 -> 216; the increase must fit in what was freed, or setmaxnreg.inc never
+        // returns); the converters keep two 32-K blocks of loads in flight
+        if (DEPTH == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
+        asm volatile("griddepcontrol.wait;" ::: "memory");                  // shares written by earlier kernels
+        const bool left = warp < 8;
+        const int grp = warp & 3;                                      // 8-row (left) / 8-column (right) group
+        const int idx = grp * 8 + (lane & 7);                                // row of x / a, or column of y / b
+        const int kq = lane >> 3;                                            // 8-K quarter of the 32-K block
+        const bool vec = ((K & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.x) | reinterpret_cast<uintptr_t>(p.a)) & 15) == 0;
+        const uint32_t poff = plane_off(idx, kq);
+        const int q4 = warp & 3;                                             // TMEM lane quadrant = plane group i'
+        const int party = (warp - 4) >> 2;                                   // drain: this warp's party
+        // L2 prefetch of a later block: a left lane's own 64-byte runs of x_p, a_p; one lane of each
+        // right warp the whole 32 x N run of one of y_0, b_0, y_1, b_1 (contiguous)
+        auto prefetch = [&](int i) {
+            if (i >= nblk) return;
+            const int kt = kt_of(i);
+            const int64_t kbase = (int64_t)kt * 32 + kq * 8;
+            if (p.pf_mode == 0) return;
+            if (left) {
+                if (idx < M && kbase < K) {
+                    const int64_t o = idx * K + kbase;
+                    if (p.pf_mode == 1) {
+                        prefetch_l2_line(p.x + o); prefetch_l2_line(p.a + o);
+                        prefetch_l2_line(p.x + sMK + o); prefetch_l2_line(p.a + sMK + o);
+                    } else if (kq == 0) {                                    // one bulk prefetch per row
+                        const uint32_t nb = (uint32_t)(8 * (K - kbase < 32 ? K - kbase : 32));
+                        prefetch_l2(p.x + o, nb); prefetch_l2(p.a + o, nb);
+                        prefetch_l2(p.x + sMK + o, nb); prefetch_l2(p.a + sMK + o, nb);
+                    }
+                }
+            } else if (lane == 0) {
+                const int64_t k0 = (int64_t)kt * 32, kl = K - k0 < 32 ? K - k0 : 32;
+                const uint64_t* base = ((grp & 1) ? p.b : p.y) + (grp >> 1) * sKN + k0 * N;
+                prefetch_l2(base, (uint32_t)(kl * N * 8));
+            }
+        };
+        // this thread's 8 K values of its row / column from the four share inputs
+        auto load = [&](int kt, uint64_t (&v0)[8], uint64_t (&v1)[8], uint64_t (&v2)[8], uint64_t (&v3)[8]) {
+            const int64_t kbase = (int64_t)kt * 32 + kq * 8;
+            if (left) {
+                if (idx < M) {
+                    const int64_t o = idx * K + kbase, lft = K - kbase;
+                    load_row8(p.x + o, lft, vec, v0);
+                    load_row8(p.a + o, lft, vec, v1);
+                    load_row8(p.x + sMK + o, lft, vec, v2);
+                    load_row8(p.a + sMK + o, lft, vec, v3);
+                } else {
+#pragma unroll
+                    for (int m = 0; m < 8; ++m) v0[m] = v1[m] = v2[m] = v3[m] = 0ull;
+                }
+            } else {
+                const uint64_t* py = p.y + kbase * N + idx;
+                const uint64_t* pb = p.b + kbase * N + idx;
+                const int lim = idx < N ? (int)(K - kbase < 8 ? K - kbase : 8) : 0;   // valid K rows
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    const bool ok = m < lim;
+                    v0[m] = ok ? __ldg(py + m * N) : 0ull;
+                    v1[m] = ok ? __ldg(pb + m * N) : 0ull;
+                    v2[m] = ok ? __ldg(py + sKN + m * N) : 0ull;
+                    v3[m] = ok ? __ldg(pb + sKN + m * N) : 0ull;
+                }
+            }
+        };
+        // TMEM drain target: the output sums [party][row][32] in shared memory, added to by the four
+        // lane-group warps of each party (shared-memory atomics; once per unit), so no registers
+        // stay live across the conversion loop
+        unsigned long long* runb = reinterpret_cast<unsigned long long*>(smem + kStages * kStageBytes);
+        unsigned long long* mine = runb + ((int64_t)party * kRows + lane) * kRows;
+        for (int i = threadIdx.x - 128; i < 2 * kRows * kRows; i += 32 * kConvWarps) runb[i] = 0ull;
+        conv_sync();
+        int s = 0; uint32_t ph = 0; uint32_t u = 0;
+        long long dbg_empty = 0;
+        const long long t_conv0 = clock64();
+        // convert the CTA's i-th block into stage s, hand it to the MMA issuer; at a unit end drain TMEM
+        auto convert = [&](int i, uint64_t (&v0)[8], uint64_t (&v1)[8], uint64_t (&v2)[8], uint64_t (&v3)[8]) {
+            // mask + local reveal: v0 <- sum_p (plus_p - minus_p)
+#pragma unroll
+            for (int m = 0; m < 8; ++m) v0[m] = v0[m] - v1[m] + v2[m] - v3[m];
+            const long long w0 = p.dbg ? clock64() : 0;
+            mbar_wait(&empty[s], ph ^ 1);
+            if (p.dbg) dbg_empty += clock64() - w0;
+            uint8_t* st = smem + s * kStageBytes;
+            if (left) {
+                st_planes8(st + kOffEps, poff, kPlane, v0);                 // eps
+                st_planes8(st + kOffA0, poff, kPlane, v1);                  // a_0
+                st_planes8(st + kOffA1, poff, kPlane, v3);                  // a_1
+            } else {
+#pragma unroll
+                for (int m = 0; m < 8; ++m) v1[m] += v0[m];                 // b'_0 = b_0 + delta (R8)
+                st_planes8(st + kOffDelta, poff, kPlane, v0);               // delta
+                st_planes8(st + kOffPair, poff, 2 * kPlane, v1);            // b'_0 plane j at j * 2 KiB
+                st_planes8(st + kOffPair + kPlane, poff, 2 * kPlane, v3);   // b'_1 1 KiB after it
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[s]);
+            if (++s == kStages) { s = 0; ph ^= 1; }
+            if ((i + 1) % p.unit != 0 && i + 1 != nblk) return;
+            // drain the unit: lane group i' = q4 of D_j holds shift q4 + j (> 7 vanishes mod 2^64)
+            mbar_wait(tfull, u & 1);
+            tc_fence_after();
+            const uint32_t tq = tmem_base + ((uint32_t)(q4 * 32) << 16) + party * 32;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                uint64_t run[16];
+#pragma unroll
+                for (int c = 0; c < 16; ++c) run[c] = 0ull;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (q4 + j > 7) continue;                                // warp-uniform
+                    uint32_t a[16];
+                    tmem_ld16(tq + j * 64 + 16 * h, a);
+                    tmem_wait_ld();
+                    const int sh = 8 * (q4 + j);
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) run[c] += (uint64_t)a[c] << sh;
+                }
+#pragma unroll
+                for (int c = 0; c < 16; ++c) atomicAdd(mine + 16 * h + c, (unsigned long long)run[c]);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty);
+            ++u;
+        };
+        for (int i = 0; i < p.pf_dist; ++i) prefetch(i);
+        // two blocks in flight per thread: the loads of block kt + 1 are issued before block kt is
+        // converted (the converters are latency-bound: one block's loads alone leave HBM half idle)
+        uint64_t a0[8], a1[8], a2[8], a3[8], b0[8], b1[8], b2[8], b3[8];
+        if (DEPTH == 1) {
+            for (int i = 0; i < nblk; ++i) {
+                prefetch(i + p.pf_dist);
+                load(kt_of(i), a0, a1, a2, a3);
+                convert(i, a0, a1, a2, a3);
+            }
+        } else {
+            if (nblk > 0) load(kt_of(0), a0, a1, a2, a3);
+            for (int i = 0; i < nblk; i += 2) {
+                if (i + 1 < nblk) load(kt_of(i + 1), b0, b1, b2, b3);
+                prefetch(i + p.pf_dist);
+                convert(i, a0, a1, a2, a3);
+                if (i + 1 >= nblk) break;
+                if (i + 2 < nblk) load(kt_of(i + 2), a0, a1, a2, a3);
+                prefetch(i + 1 + p.pf_dist);
+                convert(i + 1, b0, b1, b2, b3);
+            }
+        }
+        if (p.dbg && lane == 0) {
+            atomicAdd(&p.dbg[2], (unsigned long long)dbg_empty);
+            atomicAdd(&p.dbg[3], (unsigned long long)(clock64() - t_conv0));
+        }
+        conv_sync();                                                         // every drain has added
+        const int et = threadIdx.x - 128;
+        const bool split = G > 1;
+        for (int e = et; e < 2 * kRows * kRows; e += 32 * kConvWarps) {
+            const int pq = e >> 10, r = (e >> 5) & 31, col = e & 31;
+            if (r >= M || col >= N) continue;
+            uint64_t v = runb[((int64_t)pq * kRows + r) * kRows + col];
+            const int64_t o = (int64_t)pq * M * N + r * N + col;
+            if (split) {
+                p.partials[(int64_t)g * 2 * M * N + o] = v;
+            } else {
+                if (p.C) v += p.C[o];
+                p.Z[o] = p.trunc_bits ? div_pow2_round(v, p.trunc_bits) : v;
+            }
+        }
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem_base), "r"(kTmemCols));
+    }
+}
+
+}  // namespace gemm_fused
+
+size_t fused_small_smem_bytes() {
+    return (size_t)gemm_fused::kStages * gemm_fused::kStageBytes + 2 * 32 * 32 * 8 /*output sums*/ +
+           1024 /*align*/ + 256 /*barriers*/;
+}
+
+int fused_small_ctas(int64_t K, int sms) {
+    const int64_t kb = num_kb(K);
+    static const int env = getenv("MPC_FUSED_CTAS") ? atoi(getenv("MPC_FUSED_CTAS")) : 0;   // test knob
+    if (env > 0) return (int)std::min<int64_t>(std::max<int64_t>(kb, 1), std::min(env, sms));
+    // at least 16 blocks per CTA: shorter ranges pay the pipeline fill and the slab
+    // write / finalize read for little work
+    int64_t g = kb / 16;
+    if (g > sms) g = sms;
+    return g < 1 ? 1 : (int)g;
+}
+
+size_t fused_small_partials_bytes(int64_t M, int64_t K, int64_t N) {
+    const int g = fused_small_ctas(K, 148);
+    return g > 1 ? (size_t)g * 2 * M * N * sizeof(uint64_t) : 0;
+}
+
+cudaError_t fused_small_launch(const FusedSmallParams& p, cudaStream_t stream) {
+    if (p.M < 1 || p.M > 32 || p.N < 1 || p.N > 32 || p.K < 0) return cudaErrorInvalidValue;
+    static int attr_dev = -1;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = fused_small_smem_bytes();
+    if (attr_dev != dev) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_fused::fused_small_kernel<1>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(gemm_fused::fused_small_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(gemm_fused::fused_small_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_dev = dev;
+    }
+    const int G = fused_small_ctas(p.K, sms < 148 ? sms : 148);
+    if (G > 1 && !p.partials) return cudaErrorInvalidValue;
+    FusedSmallParams q0 = p;
+    static const int env_unit = getenv("MPC_FUSED_UNIT") ? atoi(getenv("MPC_FUSED_UNIT")) : 0;   // test knob
+    q0.unit = env_unit > 0 && env_unit < gemm_fused::kMaxUnit ? env_unit : gemm_fused::kMaxUnit;
+    static const int env_pf = getenv("MPC_FUSED_PF") ? atoi(getenv("MPC_FUSED_PF")) : 1;         // tuning knob
+    q0.pf_mode = env_pf;
+    static const int env_pfd = getenv("MPC_FUSED_PFD") ? atoi(getenv("MPC_FUSED_PFD")) : gemm_fused::kPrefetch;
+    q0.pf_dist = env_pfd;
+    static const int env_cyc = getenv("MPC_FUSED_CYCLIC") ? atoi(getenv("MPC_FUSED_CYCLIC")) : 1;
+    q0.cyclic = env_cyc;
+    static const int env_depth = getenv("MPC_FUSED_DEPTH") ? atoi(getenv("MPC_FUSED_DEPTH")) : 1;  // tuning knob
+    static const bool debug = getenv("MPC_FUSED_DEBUG") != nullptr;      // stall attribution (synchronises)
+    unsigned long long h[4] = {0, 0, 0, 0};
+    if (debug) {
+        cudaMalloc(&q0.dbg, sizeof(h));
+        cudaMemsetAsync(q0.dbg, 0, sizeof(h), stream);
+    }
+    cudaError_t e = launch_pdl(env_depth == 3 ? gemm_fused::fused_small_kernel<3>
+                               : env_depth == 2 ? gemm_fused::fused_small_kernel<2> : gemm_fused::fused_small_kernel<1>,
+                               dim3((unsigned)G), dim3(gemm_fused::kThreads), smem, stream, q0);
+    if (debug) {
+        cudaMemcpyAsync(h, q0.dbg, sizeof(h), cudaMemcpyDeviceToHost, stream);
+        cudaStreamSynchronize(stream);
+        cudaFree(q0.dbg);
+        fprintf(stderr, "[fused_small] G=%d: MMA thread %.0f cyc (waiting for stages %.1f%%); converter warps %.0f cyc "
+                "(waiting for free stages %.1f%%)\n", G, (double)h[1] / G, 100.0 * h[0] / (h[1] ? h[1] : 1),
+                (double)h[3] / (8.0 * G), 100.0 * h[2] / (h[3] ? h[3] : 1));
+    }
+    if (e != cudaSuccess || G <= 1) return e;
+    RingGemmParams q{};
+    q.M = p.M; q.N = p.N; q.C = p.C; q.Z = p.Z;
+    q.party_stride_c = q.party_stride_z = p.M * p.N;
+    q.trunc_bits = p.trunc_bits;
+    q.splits = G;
+    q.partials = p.partials;
+    q.partial_stride = 2 * p.M * p.N;
+    return ring_gemm_finalize(q, 2, stream);
+}
+
+}  // namespace mpc

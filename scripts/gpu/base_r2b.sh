@@ -1,0 +1,7 @@
+# round-2 re-entry baseline: build, smoke, GPU suite, bench
+python -c "import __graft_entry__ as g; g.build()"
+python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1
+timeout 2400 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/gpu_suite.log 2>&1
+tail -5 gpurun_out/gpu_suite.log
+python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+tail -c 600 gpurun_out/bench.json
