@@ -85,7 +85,22 @@ __device__ __forceinline__ void mma_u8_2cta(uint32_t tmem_d, uint64_t adesc, uin
 // tiles; inside a group, n tiles outer, then row tiles, then parties.
 struct TileMap {
     int parties, mt, nt, gmax;                       // gmax: row tiles per group
+    int party_major;                                 // 1: instance outermost, then the grouped (m, n) order
     __device__ void decode(int t, int& party, int& m, int& n) const {
+        if (party_major) {
+            // one instance's tiles at a time: a wave then shares its party-specific operand strips
+            // (a_p, b'_p) across more tiles (R-less L2 traffic when the party operands dominate)
+            const int per_inst = mt * nt;
+            party = t / per_inst;
+            const int r0 = t - party * per_inst;
+            const int per_group_full = gmax * nt;
+            const int g = r0 / per_group_full;
+            const int r = r0 % per_group_full;
+            const int gm = min(gmax, mt - g * gmax);
+            n = r / gm;
+            m = g * gmax + r % gm;
+            return;
+        }
         const int per_group_full = gmax * nt * parties;
         const int g = t / per_group_full;
         const int r = t % per_group_full;
@@ -472,7 +487,8 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     const bool leader = (rank == 0);
     WorkMap wm;
     wm.tm = TileMap{parties * (p.batch > 1 ? p.batch : 1), (int)(pad_rows<Layout::Left>(p.M) / kTileM),
-                    (int)(pad_rows<Layout::Right>(p.N) / kTileN), p.group_m > 0 ? p.group_m : kGroupM};
+                    (int)(pad_rows<Layout::Right>(p.N) / kTileN), p.group_m > 0 ? p.group_m : kGroupM,
+                    p.party_major};
     wm.nparties = parties;
     wm.tkb = p.seg[0].kb + (p.nseg > 1 ? p.seg[1].kb : 0);
     wm.kc = p.kc;
@@ -632,6 +648,8 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     RingGemmParams q = prm;
     static const int env_group = getenv("MPC_GEMM_GROUPM") ? atoi(getenv("MPC_GEMM_GROUPM")) : 0;
     if (q.group_m <= 0) q.group_m = env_group;
+    static const int env_pm = getenv("MPC_GEMM_PARTY_MAJOR") ? atoi(getenv("MPC_GEMM_PARTY_MAJOR")) : -1;
+    q.party_major = env_pm > 0 ? 1 : 0;
     static const int env_fault = getenv("MPC_GEMM_FAULT_INJECT") ? atoi(getenv("MPC_GEMM_FAULT_INJECT")) : 0;
     q.fault_inject = env_fault;
     static const int env_pef = getenv("MPC_PARTIALS_EVICT_FIRST") ? atoi(getenv("MPC_PARTIALS_EVICT_FIRST")) : 0;
@@ -668,6 +686,14 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
         // 106 -> 68 GB per launch, ncu 101.7 -> 95.3 ms; 16 / 24 blocks no better), while
         // 4096^3 keeps 64 (32: 5.90 -> 6.01 ms, the drain between units costs more).
         if (plane_bytes > (2ull << 30) && !getenv("MPC_GEMM_KC") && q.kc > 32) q.kc = 32;
+        // ... and take the tiles one instance (party) at a time in groups of 8 row tiles: a wave of 74
+        // tiles then reads 8 row strips of (a_p, eps) and ~9 column strips of (delta, b'_p) instead of
+        // 4 x (4 a_p + eps) and ~5 x (delta + 4 b'_p) — 4-party 8192^3 DRAM reads 68.5 -> 55.3 GB per
+        // launch, GEMM 102.4 -> 101.3 ms (profiles/r02/tile_order.txt); 4096^3 unchanged either way
+        if (plane_bytes > (2ull << 30) && env_pm < 0) {
+            q.party_major = 1;
+            if (prm.group_m <= 0 && env_group <= 0) q.group_m = 8;
+        }
         const bool tma = want_tma && !q.fault_inject && fill_tma(q, parties);
         static const int env_l2 = getenv("MPC_GEMM_TMA_L2") ? atoi(getenv("MPC_GEMM_TMA_L2")) : 3;
         q.tma_l2 = env_l2;

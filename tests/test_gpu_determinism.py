@@ -5,7 +5,8 @@ configs; ring addition is associative, so any order is exact).
 Each configuration runs in its own process because the GEMM's tuning knobs
 (K-chunk length MPC_GEMM_KC, split-K factor MPC_GEMM_SPLITS, programmatic
 dependent launch MPC_NO_PDL, transposed GEMM for small M MPC_NO_SWAP, the
-2-CTA GEMM's operand producer MPC_GEMM_TMA) are
+2-CTA GEMM's operand producer MPC_GEMM_TMA, its tile order MPC_GEMM_PARTY_MAJOR /
+MPC_GEMM_GROUPM) are
 read once per process.  Every run must
 produce the oracle's shares bit for bit.
 """
@@ -72,12 +73,14 @@ def case(request):
     {"MPC_GEMM_TMA": "0"},                  # bulk-copy producer with the peer relay everywhere
     {"MPC_GEMM_TMA": "1"},                  # 2-CTA tensor-TMA producer everywhere
     {"MPC_GEMM_TMA": "1", "MPC_GEMM_TMA_L2": "1"},
+    {"MPC_GEMM_PARTY_MAJOR": "1"},          # instance-major tile order (the > 2 GiB default)
+    {"MPC_GEMM_PARTY_MAJOR": "1", "MPC_GEMM_GROUPM": "3"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 def test_same_shares_under_every_launch_config(case, env):
     (M, K, N), expected = case
     full = dict(os.environ)
     for k in ("MPC_GEMM_KC", "MPC_GEMM_SPLITS", "MPC_NO_PDL", "MPC_NO_SWAP", "MPC_GEMM_DEBUG", "MPC_GEMM_SMALL",
-              "MPC_GEMM_TMA", "MPC_GEMM_TMA_L2"):
+              "MPC_GEMM_TMA", "MPC_GEMM_TMA_L2", "MPC_GEMM_PARTY_MAJOR", "MPC_GEMM_GROUPM"):
         full.pop(k, None)
     full.update(env)
     out = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, M=M, K=K, N=N, P=P)], env=full,
