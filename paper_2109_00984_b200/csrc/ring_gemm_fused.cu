@@ -367,10 +367,24 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const __grid_c
         // converted (the converters are latency-bound: one block's loads alone leave HBM half idle)
         uint64_t a0[8], a1[8], a2[8], a3[8], b0[8], b1[8], b2[8], b3[8];
         if (DEPTH == 1) {
+            long long t_ld = 0, t_cv = 0;
             for (int i = 0; i < nblk; ++i) {
                 prefetch(i + p.pf_dist);
+                const long long c0 = p.dbg ? clock64() : 0;
                 load(kt_of(i), a0, a1, a2, a3);
+                long long c1 = 0;
+                if (p.dbg) {                                                  // after every load has landed
+                    uint64_t chk = 0;
+#pragma unroll
+                    for (int m = 0; m < 8; ++m) chk += a0[m] ^ a1[m] ^ a2[m] ^ a3[m];
+                    c1 = chk == 0x123456789abcdefull ? 0 : clock64();
+                }
                 convert(i, a0, a1, a2, a3);
+                if (p.dbg) { t_ld += c1 - c0; t_cv += clock64() - c1; }
+            }
+            if (p.dbg && lane == 0) {
+                atomicAdd(&p.dbg[left ? 4 : 6], (unsigned long long)t_ld);
+                atomicAdd(&p.dbg[left ? 5 : 7], (unsigned long long)t_cv);
             }
         } else {
             if (nblk > 0) load(kt_of(0), a0, a1, a2, a3);
@@ -468,7 +482,7 @@ cudaError_t fused_small_launch(const FusedSmallParams& p, cudaStream_t stream) {
     q0.cyclic = env_cyc;
     static const int env_depth = getenv("MPC_FUSED_DEPTH") ? atoi(getenv("MPC_FUSED_DEPTH")) : 1;  // tuning knob
     static const bool debug = getenv("MPC_FUSED_DEBUG") != nullptr;      // stall attribution (synchronises)
-    unsigned long long h[4] = {0, 0, 0, 0};
+    unsigned long long h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (debug) {
         cudaMalloc(&q0.dbg, sizeof(h));
         cudaMemsetAsync(q0.dbg, 0, sizeof(h), stream);
@@ -483,6 +497,9 @@ cudaError_t fused_small_launch(const FusedSmallParams& p, cudaStream_t stream) {
         fprintf(stderr, "[fused_small] G=%d: MMA thread %.0f cyc (waiting for stages %.1f%%); converter warps %.0f cyc "
                 "(waiting for free stages %.1f%%)\n", G, (double)h[1] / G, 100.0 * h[0] / (h[1] ? h[1] : 1),
                 (double)h[3] / (8.0 * G), 100.0 * h[2] / (h[3] ? h[3] : 1));
+        fprintf(stderr, "[fused_small] per warp: left loads %.0f cyc, left convert %.0f; right loads %.0f, right "
+                "convert %.0f (convert includes the free-stage wait)\n", h[4] / (4.0 * G), h[5] / (4.0 * G),
+                h[6] / (4.0 * G), h[7] / (4.0 * G));
     }
     if (e != cudaSuccess || G <= 1) return e;
     RingGemmParams q{};
