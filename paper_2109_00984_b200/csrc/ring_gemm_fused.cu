@@ -34,21 +34,27 @@
 // R10).  Bit-identical to the planes-based path: the same ring sums, and
 // unsigned addition commutes.
 //
-// Warps: 0 = TMEM allocator and MMA issuer (one thread), 1..3 idle, 4..7 = left
-// converters (8 rows each), 8..11 = right converters (8 output columns each),
-// which also prefetch their inputs kPrefetch blocks ahead into L2, drain TMEM at
-// unit ends into shared-memory output sums (a warp reads the TMEM lane quadrant
-// warp % 4; warps 4..7 hold party 0, 8..11 party 1) and write the slab.
+// Warps: 0 = TMEM allocator and MMA issuer (one thread), 1..3 idle, then NG = 2
+// groups of 8 converter warps taking alternate blocks (so one group's loads are in
+// flight while the other converts): in each group 4 warps for x / a rows (8 rows
+// each) and 4 for y / b columns (8 columns each).  A converter prefetches its next
+// block into L2; group 0 also drains TMEM at unit ends into shared-memory output
+// sums (a warp reads the TMEM lane quadrant warp % 4; its warps 4..7 hold party 0,
+// 8..11 party 1) and writes the slab.
 //
 // Measured (text 32 x 519,820 x 32, one B200; scripts/gpu/fused*.sh): 0.49 ms for
-// the planes-based path -> 0.30 ms.  MPC_FUSED_DEBUG stall attribution: the
-// converter warps are busy 94% of the kernel (load latency: long-scoreboard), the
-// MMA thread 58% (36 MMAs of N = 32/64 per 32-K block, shared-memory bound at
-// ~70 cycles each).  Kept as tuning knobs, all slower here: two blocks of loads
-// in flight per thread (MPC_FUSED_DEPTH=2, registers moved by setmaxnreg: 0.32-
-// 0.37 ms), longer prefetch distances (MPC_FUSED_PFD 4..12: 0.34-0.41 ms), bulk
-// prefetches of the row pieces (MPC_FUSED_PF=2: 0.37-0.40 ms, message-rate
-// bound), contiguous K ranges per CTA (MPC_FUSED_CYCLIC=0: +2-4%).
+// the planes-based path -> 0.29-0.31 ms.  A read-only probe of the same access
+// pattern (scripts/fused_read_probe.cu) streams the 1.06 GB at 6.5 TB/s (164 us),
+// so the pattern is not the limit; MPC_FUSED_DEBUG stall attribution puts the
+// converter warps busy ~90% (load latency) and the MMA thread ~55% (36 MMAs per
+// block, the N = 32 ones shared-memory bound at ~70 cycles each), and neither two
+// blocks of loads in flight per thread (setmaxnreg-moved registers) nor the second
+// converter group shortens a block (per-group block time doubles): the shared
+// L1TEX / shared-memory data path (load fills, plane stores, the tensor core's
+// operand reads) is the suspected co-bottleneck.  Kept as knobs: MPC_FUSED_GROUPS
+// (1: 0.30 ms), MPC_FUSED_PFD (prefetch distance; 4+ blocks: 0.35-0.40 ms),
+// MPC_FUSED_PF (2: bulk row prefetches, message-rate bound, slower),
+// MPC_FUSED_CYCLIC=0 (contiguous K ranges, +2-4%); L1::no_allocate loads: 0.55 ms.
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
@@ -71,11 +77,11 @@ constexpr int kSet = 8 * kPlane;                  // the 8 planes of one operand
 constexpr int kOffEps = 0, kOffA0 = kSet, kOffA1 = 2 * kSet, kOffDelta = 3 * kSet, kOffPair = 4 * kSet;
 constexpr int kStageBytes = 6 * kSet;             // 48 KiB
 constexpr int kStages = 4;
-constexpr int kThreads = 384;                     // warp 0: TMEM allocator + MMA issuer; 4..11: converters
-constexpr int kConvWarps = 8;
+// warp 0: TMEM allocator + MMA issuer; 1..3 idle; 4..: NG groups of 8 converter warps
+__host__ __device__ constexpr int kThreadsOf(int ng) { return 128 + 256 * ng; }
 constexpr int kTmemCols = 512;
 constexpr int kMaxUnit = 1032;                    // 32-K blocks per accumulation unit (exact, see above)
-constexpr int kPrefetch = 2;                      // 32-K blocks the L2 prefetch runs ahead (2 measured best of 0-12)
+constexpr int kPrefetch = 1;                      // blocks (of a converter group) the L2 prefetch runs ahead
 __host__ __device__ constexpr uint32_t idesc(int n) {
     return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);   // S32 <- u8 x u8, M = 128
 }
@@ -94,8 +100,8 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void conv_sync() {            // the 8 converter / epilogue warps
-    asm volatile("bar.sync 1, %0;" :: "n"(32 * kConvWarps) : "memory");
+__device__ __forceinline__ void conv_sync() {            // the 8 warps of converter group 0
+    asm volatile("bar.sync 1, 256;" ::: "memory");
 }
 // bulk L2 prefetch of [p, p + bytes): the instruction takes a 16-byte aligned start and size
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
@@ -142,8 +148,8 @@ __device__ __forceinline__ void load_row8(const uint64_t* __restrict__ src, int6
     }
 }
 
-template <int DEPTH>
-__global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const __grid_constant__ FusedSmallParams p) {
+template <int NG>
+__global__ void __launch_bounds__(kThreadsOf(NG), 1) fused_small_kernel(const __grid_constant__ FusedSmallParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");   // the finalize may launch
@@ -162,10 +168,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const __grid_c
     const int kb0 = (int)((int64_t)KB * g / G);
     const int nblk = p.cyclic ? (KB > g ? (KB - g + G - 1) / G : 0) : (int)((int64_t)KB * (g + 1) / G) - kb0;
     auto kt_of = [&](int i) { return p.cyclic ? g + i * G : kb0 + i; };
+    const int U = p.unit;                                                    // even when NG == 2 (launcher)
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], kConvWarps); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 8); mbar_init(&empty[s], 1); }
         mbar_init(tfull, 1);
-        mbar_init(tempty, kConvWarps);
+        mbar_init(tempty, 8);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -179,16 +186,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const __grid_c
     const uint32_t tmem_base = *tmem_slot;
     const int64_t sMK = M * K, sKN = K * N;
 
-    if (warp < 4) {
-        // ------------------------------------------------ MMA issuer (one thread of warp 0)
-        if (DEPTH == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
-      if (warp == 0) {
+    if (warp == 0) {
+        // ------------------------------------------------ MMA issuer (one thread)
         if (lane == 0) {
             int s = 0; uint32_t ph = 0; uint32_t u = 0;
             long long dbg_full = 0;
             const long long t_mma0 = clock64();
-            for (int k0 = 0; k0 < nblk; k0 += p.unit, ++u) {
-                const int k1 = min(nblk, k0 + p.unit);
+            for (int k0 = 0; k0 < nblk; k0 += U, ++u) {
+                const int k1 = min(nblk, k0 + U);
                 mbar_wait(tempty, (u & 1) ^ 1);                               // last unit drained
                 tc_fence_after();
                 for (int kt = k0; kt < k1; ++kt) {
@@ -196,29 +201,33 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const __grid_c
                     mbar_wait(&full[s], ph);
                     if (p.dbg) dbg_full += clock64() - w0;
                     tc_fence_after();
-                    const uint32_t st = smem_u32(smem + s * kStageBytes);
-                    const uint64_t dE = smem_desc(st + kOffEps), dP = smem_desc(st + kOffPair);
-                    const uint64_t dD = smem_desc(st + kOffDelta);
+                    // every operand address from two per-block base values, re-read through an opaque
+                    // move so the compiler does not hoist 36 addresses out of the loop
+                    uint32_t st = smem_u32(smem + s * kStageBytes), tb = tmem_base;
+                    asm volatile("mov.b32 %0, %0;" : "+r"(st));
+                    asm volatile("mov.b32 %0, %0;" : "+r"(tb));
+                    const uint64_t d0 = smem_desc(st);                       // eps set; +offset>>4 for the rest
                     const uint32_t first = kt == k0 ? 0u : 1u;
                     // eps @ b'_p, both parties in one N = 64 MMA; the lo MMAs open every accumulator
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
-                        mma_u8(tmem_base + j * 64, dE, dP + (uint64_t)(j * (2 * kPlane) >> 4), idesc(64), first);
+                        mma_u8(tb + j * 64, d0, d0 + (uint64_t)((kOffPair + j * 2 * kPlane) >> 4), idesc(64), first);
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
-                        mma_u8(tmem_base + (j + 4) * 64, dE + (uint64_t)((4 * kPlane) >> 4),
-                               dP + (uint64_t)(j * (2 * kPlane) >> 4), idesc(64), 1u);
+                        mma_u8(tb + (j + 4) * 64, d0 + (uint64_t)((4 * kPlane) >> 4),
+                               d0 + (uint64_t)((kOffPair + j * 2 * kPlane) >> 4), idesc(64), 1u);
                     // a_p @ delta, per party (N = 32, the party's 32 columns)
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
-                        const uint64_t dA = smem_desc(st + (q ? kOffA1 : kOffA0));
+                        const int offA = q ? kOffA1 : kOffA0;
 #pragma unroll
                         for (int j = 0; j < 8; ++j)
-                            mma_u8(tmem_base + j * 64 + q * 32, dA, dD + (uint64_t)((j * kPlane) >> 4), idesc(32), 1u);
+                            mma_u8(tb + j * 64 + q * 32, d0 + (uint64_t)(offA >> 4),
+                                   d0 + (uint64_t)((kOffDelta + j * kPlane) >> 4), idesc(32), 1u);
 #pragma unroll
                         for (int j = 0; j < 4; ++j)
-                            mma_u8(tmem_base + (j + 4) * 64 + q * 32, dA + (uint64_t)((4 * kPlane) >> 4),
-                                   dD + (uint64_t)((j * kPlane) >> 4), idesc(32), 1u);
+                            mma_u8(tb + (j + 4) * 64 + q * 32, d0 + (uint64_t)((offA + 4 * kPlane) >> 4),
+                                   d0 + (uint64_t)((kOffDelta + j * kPlane) >> 4), idesc(32), 1u);
                     }
                     tc_commit(&empty[s]);
                     if (++s == kStages) { s = 0; ph ^= 1; }
@@ -231,29 +240,25 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const __grid_c
             }
         }
         __syncwarp();
-      }
-    } else {
-        // ------------------------------------------------ converters, then the TMEM drain
-        // registers: the control warpgroup frees 112 per thread (168 -> 56), the converters take
-        // 48 more (168 -> 216; the increase must fit in what was freed, or setmaxnreg.inc never
-        // returns); the converters keep two 32-K blocks of loads in flight
-        if (DEPTH == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
+    } else if (warp >= 4) {
+        // ------------------------------------------------ converters (NG groups of 8 warps on alternate
+        // blocks, so one group's loads are in flight while the other converts), then the TMEM drain
         asm volatile("griddepcontrol.wait;" ::: "memory");                  // shares written by earlier kernels
-        const bool left = warp < 8;
-        const int grp = warp & 3;                                      // 8-row (left) / 8-column (right) group
+        const int cw = warp - 4, cg = cw >> 3, w8 = cw & 7;                  // group, warp in the group
+        const bool left = w8 < 4;
+        const int grp = w8 & 3;                                              // 8-row (left) / 8-column (right) group
         const int idx = grp * 8 + (lane & 7);                                // row of x / a, or column of y / b
         const int kq = lane >> 3;                                            // 8-K quarter of the 32-K block
         const bool vec = ((K & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.x) | reinterpret_cast<uintptr_t>(p.a)) & 15) == 0;
         const uint32_t poff = plane_off(idx, kq);
         const int q4 = warp & 3;                                             // TMEM lane quadrant = plane group i'
-        const int party = (warp - 4) >> 2;                                   // drain: this warp's party
+        const int party = w8 >> 2;                                           // drain (group 0): this warp's party
         // L2 prefetch of a later block: a left lane's own 64-byte runs of x_p, a_p; one lane of each
         // right warp the whole 32 x N run of one of y_0, b_0, y_1, b_1 (contiguous)
         auto prefetch = [&](int i) {
-            if (i >= nblk) return;
+            if (i >= nblk || p.pf_mode == 0) return;
             const int kt = kt_of(i);
             const int64_t kbase = (int64_t)kt * 32 + kq * 8;
-            if (p.pf_mode == 0) return;
             if (left) {
                 if (idx < M && kbase < K) {
                     const int64_t o = idx * K + kbase;
@@ -272,9 +277,23 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const __grid_c
                 prefetch_l2(base, (uint32_t)(kl * N * 8));
             }
         };
-        // this thread's 8 K values of its row / column from the four share inputs
-        auto load = [&](int kt, uint64_t (&v0)[8], uint64_t (&v1)[8], uint64_t (&v2)[8], uint64_t (&v3)[8]) {
-            const int64_t kbase = (int64_t)kt * 32 + kq * 8;
+        // TMEM drain target (group 0): the output sums [party][row][32] in shared memory, added to by
+        // the four lane-group warps of each party (shared-memory atomics; once per unit)
+        unsigned long long* runb = reinterpret_cast<unsigned long long*>(smem + kStages * kStageBytes);
+        unsigned long long* mine = runb + ((int64_t)party * kRows + lane) * kRows;
+        if (cg == 0) {
+            for (int i = threadIdx.x - 128; i < 2 * kRows * kRows; i += 256) runb[i] = 0ull;
+            conv_sync();
+        }
+        int s = cg; uint32_t ph = 0; uint32_t u = 0;                        // block i uses stage i % kStages
+        long long dbg_empty = 0;
+        const long long t_conv0 = clock64();
+        for (int j = 0; j < p.pf_dist; ++j) prefetch(cg + NG * j);
+        for (int i = cg; i < nblk; i += NG) {
+            prefetch(i + NG * p.pf_dist);
+            // this thread's 8 K values of its row / column from the four share inputs
+            uint64_t v0[8], v1[8], v2[8], v3[8];
+            const int64_t kbase = (int64_t)kt_of(i) * 32 + kq * 8;
             if (left) {
                 if (idx < M) {
                     const int64_t o = idx * K + kbase, lft = K - kbase;
@@ -299,19 +318,6 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const __grid_c
                     v3[m] = ok ? __ldg(pb + sKN + m * N) : 0ull;
                 }
             }
-        };
-        // TMEM drain target: the output sums [party][row][32] in shared memory, added to by the four
-        // lane-group warps of each party (shared-memory atomics; once per unit), so no registers
-        // stay live across the conversion loop
-        unsigned long long* runb = reinterpret_cast<unsigned long long*>(smem + kStages * kStageBytes);
-        unsigned long long* mine = runb + ((int64_t)party * kRows + lane) * kRows;
-        for (int i = threadIdx.x - 128; i < 2 * kRows * kRows; i += 32 * kConvWarps) runb[i] = 0ull;
-        conv_sync();
-        int s = 0; uint32_t ph = 0; uint32_t u = 0;
-        long long dbg_empty = 0;
-        const long long t_conv0 = clock64();
-        // convert the CTA's i-th block into stage s, hand it to the MMA issuer; at a unit end drain TMEM
-        auto convert = [&](int i, uint64_t (&v0)[8], uint64_t (&v1)[8], uint64_t (&v2)[8], uint64_t (&v3)[8]) {
             // mask + local reveal: v0 <- sum_p (plus_p - minus_p)
 #pragma unroll
             for (int m = 0; m < 8; ++m) v0[m] = v0[m] - v1[m] + v2[m] - v3[m];
@@ -333,9 +339,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const __grid_c
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[s]);
-            if (++s == kStages) { s = 0; ph ^= 1; }
-            if ((i + 1) % p.unit != 0 && i + 1 != nblk) return;
-            // drain the unit: lane group i' = q4 of D_j holds shift q4 + j (> 7 vanishes mod 2^64)
+            s += NG;
+            if (s >= kStages) { s -= kStages; ph ^= 1; }
+            // group 0 drains each unit after its own last block of the unit (every unit starts at an
+            // even block, so group 0 has one); tfull follows the unit's last MMA, whichever group fed it
+            if (cg != 0) continue;
+            const int uend = min((i / U + 1) * U, nblk);
+            if (i + NG < uend) continue;
+            // lane group i' = q4 of D_j holds shift q4 + j (> 7 vanishes mod 2^64)
             mbar_wait(tfull, u & 1);
             tc_fence_after();
             const uint32_t tq = tmem_base + ((uint32_t)(q4 * 32) << 16) + party * 32;
@@ -361,60 +372,26 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const __grid_c
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty);
             ++u;
-        };
-        for (int i = 0; i < p.pf_dist; ++i) prefetch(i);
-        // two blocks in flight per thread: the loads of block kt + 1 are issued before block kt is
-        // converted (the converters are latency-bound: one block's loads alone leave HBM half idle)
-        uint64_t a0[8], a1[8], a2[8], a3[8], b0[8], b1[8], b2[8], b3[8];
-        if (DEPTH == 1) {
-            long long t_ld = 0, t_cv = 0;
-            for (int i = 0; i < nblk; ++i) {
-                prefetch(i + p.pf_dist);
-                const long long c0 = p.dbg ? clock64() : 0;
-                load(kt_of(i), a0, a1, a2, a3);
-                long long c1 = 0;
-                if (p.dbg) {                                                  // after every load has landed
-                    uint64_t chk = 0;
-#pragma unroll
-                    for (int m = 0; m < 8; ++m) chk += a0[m] ^ a1[m] ^ a2[m] ^ a3[m];
-                    c1 = chk == 0x123456789abcdefull ? 0 : clock64();
-                }
-                convert(i, a0, a1, a2, a3);
-                if (p.dbg) { t_ld += c1 - c0; t_cv += clock64() - c1; }
-            }
-            if (p.dbg && lane == 0) {
-                atomicAdd(&p.dbg[left ? 4 : 6], (unsigned long long)t_ld);
-                atomicAdd(&p.dbg[left ? 5 : 7], (unsigned long long)t_cv);
-            }
-        } else {
-            if (nblk > 0) load(kt_of(0), a0, a1, a2, a3);
-            for (int i = 0; i < nblk; i += 2) {
-                if (i + 1 < nblk) load(kt_of(i + 1), b0, b1, b2, b3);
-                prefetch(i + p.pf_dist);
-                convert(i, a0, a1, a2, a3);
-                if (i + 1 >= nblk) break;
-                if (i + 2 < nblk) load(kt_of(i + 2), a0, a1, a2, a3);
-                prefetch(i + 1 + p.pf_dist);
-                convert(i + 1, b0, b1, b2, b3);
-            }
         }
         if (p.dbg && lane == 0) {
             atomicAdd(&p.dbg[2], (unsigned long long)dbg_empty);
             atomicAdd(&p.dbg[3], (unsigned long long)(clock64() - t_conv0));
         }
-        conv_sync();                                                         // every drain has added
-        const int et = threadIdx.x - 128;
-        const bool split = G > 1;
-        for (int e = et; e < 2 * kRows * kRows; e += 32 * kConvWarps) {
-            const int pq = e >> 10, r = (e >> 5) & 31, col = e & 31;
-            if (r >= M || col >= N) continue;
-            uint64_t v = runb[((int64_t)pq * kRows + r) * kRows + col];
-            const int64_t o = (int64_t)pq * M * N + r * N + col;
-            if (split) {
-                p.partials[(int64_t)g * 2 * M * N + o] = v;
-            } else {
-                if (p.C) v += p.C[o];
-                p.Z[o] = p.trunc_bits ? div_pow2_round(v, p.trunc_bits) : v;
+        if (cg == 0) {
+            conv_sync();                                                     // every drain has added
+            const int et = threadIdx.x - 128;
+            const bool split = G > 1;
+            for (int e = et; e < 2 * kRows * kRows; e += 256) {
+                const int pq = e >> 10, r = (e >> 5) & 31, col = e & 31;
+                if (r >= M || col >= N) continue;
+                uint64_t v = runb[((int64_t)pq * kRows + r) * kRows + col];
+                const int64_t o = (int64_t)pq * M * N + r * N + col;
+                if (split) {
+                    p.partials[(int64_t)g * 2 * M * N + o] = v;
+                } else {
+                    if (p.C) v += p.C[o];
+                    p.Z[o] = p.trunc_bits ? div_pow2_round(v, p.trunc_bits) : v;
+                }
             }
         }
     }
@@ -463,43 +440,40 @@ cudaError_t fused_small_launch(const FusedSmallParams& p, cudaStream_t stream) {
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(gemm_fused::fused_small_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(gemm_fused::fused_small_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem);
         if (e != cudaSuccess) return e;
         attr_dev = dev;
     }
     const int G = fused_small_ctas(p.K, sms < 148 ? sms : 148);
     if (G > 1 && !p.partials) return cudaErrorInvalidValue;
     FusedSmallParams q0 = p;
-    static const int env_unit = getenv("MPC_FUSED_UNIT") ? atoi(getenv("MPC_FUSED_UNIT")) : 0;   // test knob
-    q0.unit = env_unit > 0 && env_unit < gemm_fused::kMaxUnit ? env_unit : gemm_fused::kMaxUnit;
-    static const int env_pf = getenv("MPC_FUSED_PF") ? atoi(getenv("MPC_FUSED_PF")) : 1;         // tuning knob
+    // tuning / test knobs (read once): converter groups, unit length, L2 prefetch, block order
+    static const int env_ng = getenv("MPC_FUSED_GROUPS") ? atoi(getenv("MPC_FUSED_GROUPS")) : 2;
+    const int ng = env_ng == 1 ? 1 : 2;
+    static const int env_unit = getenv("MPC_FUSED_UNIT") ? atoi(getenv("MPC_FUSED_UNIT")) : 0;
+    int unit = env_unit > 0 && env_unit < gemm_fused::kMaxUnit ? env_unit : gemm_fused::kMaxUnit;
+    if (ng == 2) unit = unit < 2 ? 2 : unit & ~1;       // every unit starts at a block of converter group 0
+    q0.unit = unit;
+    static const int env_pf = getenv("MPC_FUSED_PF") ? atoi(getenv("MPC_FUSED_PF")) : 1;
     q0.pf_mode = env_pf;
     static const int env_pfd = getenv("MPC_FUSED_PFD") ? atoi(getenv("MPC_FUSED_PFD")) : gemm_fused::kPrefetch;
     q0.pf_dist = env_pfd;
     static const int env_cyc = getenv("MPC_FUSED_CYCLIC") ? atoi(getenv("MPC_FUSED_CYCLIC")) : 1;
     q0.cyclic = env_cyc;
-    static const int env_depth = getenv("MPC_FUSED_DEPTH") ? atoi(getenv("MPC_FUSED_DEPTH")) : 1;  // tuning knob
     static const bool debug = getenv("MPC_FUSED_DEBUG") != nullptr;      // stall attribution (synchronises)
-    unsigned long long h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long h[4] = {0, 0, 0, 0};
     if (debug) {
         cudaMalloc(&q0.dbg, sizeof(h));
         cudaMemsetAsync(q0.dbg, 0, sizeof(h), stream);
     }
-    cudaError_t e = launch_pdl(env_depth == 3 ? gemm_fused::fused_small_kernel<3>
-                               : env_depth == 2 ? gemm_fused::fused_small_kernel<2> : gemm_fused::fused_small_kernel<1>,
-                               dim3((unsigned)G), dim3(gemm_fused::kThreads), smem, stream, q0);
+    cudaError_t e = launch_pdl(ng == 2 ? gemm_fused::fused_small_kernel<2> : gemm_fused::fused_small_kernel<1>,
+                               dim3((unsigned)G), dim3(gemm_fused::kThreadsOf(ng)), smem, stream, q0);
     if (debug) {
         cudaMemcpyAsync(h, q0.dbg, sizeof(h), cudaMemcpyDeviceToHost, stream);
         cudaStreamSynchronize(stream);
         cudaFree(q0.dbg);
-        fprintf(stderr, "[fused_small] G=%d: MMA thread %.0f cyc (waiting for stages %.1f%%); converter warps %.0f cyc "
-                "(waiting for free stages %.1f%%)\n", G, (double)h[1] / G, 100.0 * h[0] / (h[1] ? h[1] : 1),
-                (double)h[3] / (8.0 * G), 100.0 * h[2] / (h[3] ? h[3] : 1));
-        fprintf(stderr, "[fused_small] per warp: left loads %.0f cyc, left convert %.0f; right loads %.0f, right "
-                "convert %.0f (convert includes the free-stage wait)\n", h[4] / (4.0 * G), h[5] / (4.0 * G),
-                h[6] / (4.0 * G), h[7] / (4.0 * G));
+        fprintf(stderr, "[fused_small] G=%d groups=%d: MMA thread %.0f cyc (waiting for stages %.1f%%); converter "
+                "warps %.0f cyc (waiting for free stages %.1f%%)\n", G, ng, (double)h[1] / G,
+                100.0 * h[0] / (h[1] ? h[1] : 1), (double)h[3] / (8.0 * ng * G), 100.0 * h[2] / (h[3] ? h[3] : 1));
     }
     if (e != cudaSuccess || G <= 1) return e;
     RingGemmParams q{};
