@@ -11,21 +11,21 @@
 // (32 x 32 each) straight into registers, form (R7/R8)
 //     eps = sum_p (x_p - a_p),   delta = sum_p (y_p - b_p),   b'_0 = b_0 + delta,
 // and write the u8 limb planes of eps, a_0, a_1, delta, b'_0, b'_1 into a shared-
-// memory stage in the UMMA canonical K-major layout; one elected thread issues
+// memory stage in the UMMA canonical K-major layout; one thread issues
 //     z_p = c_p + a_p @ delta + eps @ b'_p          (mod 2^64, p = 0, 1)
-// as stacked-plane MMAs (ring_gemm_small.cu): A = 4 left planes stacked along M
-// (M = 128: lanes 32 i' + r), B = one right plane.  Both parties accumulate into
-// the SAME 8 TMEM accumulators D_0..D_7 of 64 columns (party p: columns 32p..):
-//   eps @ b'_p : one N = 64 MMA covers both parties (b'_0 / b'_1 plane j stored
-//                as one 64-row operand), A_lo = eps planes 0-3 -> D_j (j = 0..7),
-//                A_hi = eps planes 4-7 -> D_{j+4} (j = 0..3);
-//   a_p @ delta: N = 32 per party, A_lo(a_p) -> D_j, A_hi(a_p) -> D_{j+4}.
-// Lane group i' of D_j then holds shift i' + j for both A_lo (plane i', right
-// plane j) and A_hi (plane 4 + i', right plane j - 4), so 8 accumulators x 64
-// columns = all 512 TMEM columns hold both parties (the stacked kernel needs 12
-// per party).  Exactness: an entry sums at most 2 products per K for shifts
-// <= 3 (no A_hi term), so reading it as u32 is exact for units of <= 1032 32-K
-// blocks; shifts >= 4 only need the entry mod 2^(64 - 8s) (<= 2^32).
+// as stacked-plane MMAs: A_lo / A_hi = left planes 0-3 / 4-7 stacked along M
+// (M = 128: lanes 32 i' + r) and B = all 8 planes of a right operand stacked
+// along N (N = 256: column 32 j + n), so ONE MMA forms every plane product
+// L_i' @ R_j of a stack; party p owns 256 TMEM columns (both parties: all 512):
+//   A_lo x R (N = 256)  -> columns 32 j + n,         lane group i' shift i' + j
+//   A_hi x R_0..3 (N = 128) -> columns 128 + 32 j + n, lane group i' shift 4 + i' + j
+// — the same shift per (lane, column) for both, so they share the accumulator —
+// for eps @ b'_p and a_p @ delta: 4 MMAs per party and 32-K block (8 in all)
+// instead of 36 plane-pair MMAs (ring_gemm_small.cu issues 12 per party with N =
+// 32); products with i + j >= 8 are computed and ignored (64 issued, 36 needed).
+// Exactness: an entry with shift <= 3 sums <= 2 products per K (no A_hi term),
+// so reading it as u32 is exact for units of <= 1032 32-K blocks; shifts >= 4
+// only need the entry mod 2^(64 - 8s) (<= 2^32).
 //
 // Split-K over the CTAs (one per SM), the 32-K blocks dealt round-robin so the
 // CTAs stream neighbouring 256-byte row pieces of x / a through DRAM together;
@@ -34,27 +34,27 @@
 // R10).  Bit-identical to the planes-based path: the same ring sums, and
 // unsigned addition commutes.
 //
-// Warps: 0 = TMEM allocator and MMA issuer (one thread), 1..3 idle, then NG = 2
-// groups of 8 converter warps taking alternate blocks (so one group's loads are in
-// flight while the other converts): in each group 4 warps for x / a rows (8 rows
-// each) and 4 for y / b columns (8 columns each).  A converter prefetches its next
-// block into L2; group 0 also drains TMEM at unit ends into shared-memory output
-// sums (a warp reads the TMEM lane quadrant warp % 4; its warps 4..7 hold party 0,
-// 8..11 party 1) and writes the slab.
+// Warps: 0 = TMEM allocator and MMA issuer (one thread), 1..3 idle, then NG (1 by
+// default) groups of 8 converter warps taking alternate blocks: in each group 4
+// warps for x / a rows (8 rows each) and 4 for y / b columns (8 columns each).
+// A converter prefetches its next block into L2; group 0 also drains TMEM at unit
+// ends into shared-memory output sums (a warp reads the TMEM lane quadrant
+// warp % 4; its warps 4..7 hold party 0, 8..11 party 1) and writes the slab.
 //
-// Measured (text 32 x 519,820 x 32, one B200; scripts/gpu/fused*.sh): 0.49 ms for
-// the planes-based path -> 0.29-0.31 ms.  A read-only probe of the same access
-// pattern (scripts/fused_read_probe.cu) streams the 1.06 GB at 6.5 TB/s (164 us),
-// so the pattern is not the limit; MPC_FUSED_DEBUG stall attribution puts the
-// converter warps busy ~90% (load latency) and the MMA thread ~55% (36 MMAs per
-// block, the N = 32 ones shared-memory bound at ~70 cycles each), and neither two
-// blocks of loads in flight per thread (setmaxnreg-moved registers) nor the second
-// converter group shortens a block (per-group block time doubles): the shared
-// L1TEX / shared-memory data path (load fills, plane stores, the tensor core's
-// operand reads) is the suspected co-bottleneck.  Kept as knobs: MPC_FUSED_GROUPS
-// (1: 0.30 ms), MPC_FUSED_PFD (prefetch distance; 4+ blocks: 0.35-0.40 ms),
-// MPC_FUSED_PF (2: bulk row prefetches, message-rate bound, slower),
-// MPC_FUSED_CYCLIC=0 (contiguous K ranges, +2-4%); L1::no_allocate loads: 0.55 ms.
+// Measured (text 32 x 519,820 x 32, one B200; scripts/gpu/fused*.sh,
+// profiles/r02/fused_small/): 0.49 ms for the planes-based path -> 0.271 ms (0.61
+// of the HBM floor; kernel 267 µs under ncu, 1.065 GB DRAM = the algorithmic
+// bytes).  With 36 N = 32/64 plane-pair MMAs per block the MMA thread was busy
+// 58% and the tensor core's shared-memory operand reads (192 KB per block) shared
+// the L1TEX data path with the converters' loads and plane stores (LSU 68% +
+// tensor core 35% of its wavefronts); the 8 stacked MMAs read 80 KB (MMA thread
+// 18% busy).  The converters now bound the kernel (load latency; a read-only
+// probe of the access pattern, scripts/fused_read_probe.cu, streams at 6.5 TB/s).
+// Kept as knobs: MPC_FUSED_GROUPS=2 (two converter groups on alternate blocks:
+// 0.280 ms), MPC_FUSED_PFD (prefetch distance; 0: 0.298, 2: 0.296 ms), MPC_FUSED_PF
+// (2: bulk row prefetches, message-rate bound), MPC_FUSED_CYCLIC=0 (contiguous K
+// ranges, +2-4%).  Tried and dropped: two blocks of loads in flight per thread
+// (setmaxnreg-moved registers; no faster), L1::no_allocate loads (2x slower).
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
@@ -72,9 +72,9 @@ using namespace tc;
 constexpr int kRows = 32;                         // output rows and columns of the tile
 constexpr int kPlane = 1024;                      // one limb plane of 32 rows x 32 K
 constexpr int kSet = 8 * kPlane;                  // the 8 planes of one operand
-// stage: [eps][a_0][a_1][delta] sets, then the b' pair set (plane j of b'_0 at
-// j * 2 KiB, of b'_1 1 KiB after it: the 64-row B operand of the eps @ b' MMA)
-constexpr int kOffEps = 0, kOffA0 = kSet, kOffA1 = 2 * kSet, kOffDelta = 3 * kSet, kOffPair = 4 * kSet;
+// stage: [eps][a_0][a_1][delta][b'_0][b'_1] plane sets (plane j of a set at j KiB: the 8 planes of a
+// right operand form one 256-row B operand, planes 0..3 / 4..7 of a left one the A_lo / A_hi stacks)
+constexpr int kOffEps = 0, kOffA0 = kSet, kOffDelta = 3 * kSet, kOffB0 = 4 * kSet;
 constexpr int kStageBytes = 6 * kSet;             // 48 KiB
 constexpr int kStages = 4;
 // warp 0: TMEM allocator + MMA issuer; 1..3 idle; 4..: NG groups of 8 converter warps
@@ -208,26 +208,20 @@ __global__ void __launch_bounds__(kThreadsOf(NG), 1) fused_small_kernel(const __
                     asm volatile("mov.b32 %0, %0;" : "+r"(tb));
                     const uint64_t d0 = smem_desc(st);                       // eps set; +offset>>4 for the rest
                     const uint32_t first = kt == k0 ? 0u : 1u;
-                    // eps @ b'_p, both parties in one N = 64 MMA; the lo MMAs open every accumulator
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        mma_u8(tb + j * 64, d0, d0 + (uint64_t)((kOffPair + j * 2 * kPlane) >> 4), idesc(64), first);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        mma_u8(tb + (j + 4) * 64, d0 + (uint64_t)((4 * kPlane) >> 4),
-                               d0 + (uint64_t)((kOffPair + j * 2 * kPlane) >> 4), idesc(64), 1u);
-                    // a_p @ delta, per party (N = 32, the party's 32 columns)
+                    // party q's accumulator: 256 TMEM columns (column 32 j + n holds right plane j).
+                    // Per party 4 MMAs: A_lo (planes 0-3) against all 8 right planes (N = 256) and
+                    // A_hi (planes 4-7) against right planes 0-3 into columns 128.. (N = 128), for
+                    // eps @ b'_q and a_q @ delta; the first one opens the party's accumulator
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
-                        const int offA = q ? kOffA1 : kOffA0;
-#pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            mma_u8(tb + j * 64 + q * 32, d0 + (uint64_t)(offA >> 4),
-                                   d0 + (uint64_t)((kOffDelta + j * kPlane) >> 4), idesc(32), 1u);
-#pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            mma_u8(tb + (j + 4) * 64 + q * 32, d0 + (uint64_t)((offA + 4 * kPlane) >> 4),
-                                   d0 + (uint64_t)((kOffDelta + j * kPlane) >> 4), idesc(32), 1u);
+                        const uint32_t dq = tb + q * 256;
+                        const uint64_t dB = d0 + (uint64_t)((kOffB0 + q * kSet) >> 4);
+                        const uint64_t dA = d0 + (uint64_t)((kOffA0 + q * kSet) >> 4);
+                        const uint64_t dD = d0 + (uint64_t)(kOffDelta >> 4);
+                        mma_u8(dq, d0, dB, idesc(256), first);
+                        mma_u8(dq + 128, d0 + (uint64_t)((4 * kPlane) >> 4), dB, idesc(128), 1u);
+                        mma_u8(dq, dA, dD, idesc(256), 1u);
+                        mma_u8(dq + 128, dA + (uint64_t)((4 * kPlane) >> 4), dD, idesc(128), 1u);
                     }
                     tc_commit(&empty[s]);
                     if (++s == kStages) { s = 0; ph ^= 1; }
@@ -328,13 +322,13 @@ __global__ void __launch_bounds__(kThreadsOf(NG), 1) fused_small_kernel(const __
             if (left) {
                 st_planes8(st + kOffEps, poff, kPlane, v0);                 // eps
                 st_planes8(st + kOffA0, poff, kPlane, v1);                  // a_0
-                st_planes8(st + kOffA1, poff, kPlane, v3);                  // a_1
+                st_planes8(st + kOffA0 + kSet, poff, kPlane, v3);           // a_1
             } else {
 #pragma unroll
                 for (int m = 0; m < 8; ++m) v1[m] += v0[m];                 // b'_0 = b_0 + delta (R8)
                 st_planes8(st + kOffDelta, poff, kPlane, v0);               // delta
-                st_planes8(st + kOffPair, poff, 2 * kPlane, v1);            // b'_0 plane j at j * 2 KiB
-                st_planes8(st + kOffPair + kPlane, poff, 2 * kPlane, v3);   // b'_1 1 KiB after it
+                st_planes8(st + kOffB0, poff, kPlane, v1);                  // b'_0
+                st_planes8(st + kOffB0 + kSet, poff, kPlane, v3);           // b'_1
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
             __syncwarp();
@@ -349,7 +343,7 @@ __global__ void __launch_bounds__(kThreadsOf(NG), 1) fused_small_kernel(const __
             // lane group i' = q4 of D_j holds shift q4 + j (> 7 vanishes mod 2^64)
             mbar_wait(tfull, u & 1);
             tc_fence_after();
-            const uint32_t tq = tmem_base + ((uint32_t)(q4 * 32) << 16) + party * 32;
+            const uint32_t tq = tmem_base + ((uint32_t)(q4 * 32) << 16) + party * 256;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 uint64_t run[16];
@@ -359,7 +353,7 @@ __global__ void __launch_bounds__(kThreadsOf(NG), 1) fused_small_kernel(const __
                 for (int j = 0; j < 8; ++j) {
                     if (q4 + j > 7) continue;                                // warp-uniform
                     uint32_t a[16];
-                    tmem_ld16(tq + j * 64 + 16 * h, a);
+                    tmem_ld16(tq + j * 32 + 16 * h, a);
                     tmem_wait_ld();
                     const int sh = 8 * (q4 + j);
 #pragma unroll
@@ -447,8 +441,8 @@ cudaError_t fused_small_launch(const FusedSmallParams& p, cudaStream_t stream) {
     if (G > 1 && !p.partials) return cudaErrorInvalidValue;
     FusedSmallParams q0 = p;
     // tuning / test knobs (read once): converter groups, unit length, L2 prefetch, block order
-    static const int env_ng = getenv("MPC_FUSED_GROUPS") ? atoi(getenv("MPC_FUSED_GROUPS")) : 2;
-    const int ng = env_ng == 1 ? 1 : 2;
+    static const int env_ng = getenv("MPC_FUSED_GROUPS") ? atoi(getenv("MPC_FUSED_GROUPS")) : 1;
+    const int ng = env_ng == 2 ? 2 : 1;
     static const int env_unit = getenv("MPC_FUSED_UNIT") ? atoi(getenv("MPC_FUSED_UNIT")) : 0;
     int unit = env_unit > 0 && env_unit < gemm_fused::kMaxUnit ? env_unit : gemm_fused::kMaxUnit;
     if (ng == 2) unit = unit < 2 ? 2 : unit & ~1;       // every unit starts at a block of converter group 0

@@ -1,0 +1,7 @@
+python -c "import __graft_entry__ as g; g.build()"
+timeout 1200 python -m pytest tests/test_gpu_fused_small.py tests/test_gpu_configs.py -k "fused or text" -m gpu -x -q -p no:cacheprovider 2>&1 | tail -2
+for ng in 1 2; do for pfd in 0 1 2; do
+ echo "groups=$ng pfd=$pfd"; MPC_FUSED_GROUPS=$ng MPC_FUSED_PFD=$pfd python scripts/bench_layers.py --model text --chain --reps 100 2>&1 | grep "chain of"
+done; done
+for ng in 1 2; do MPC_FUSED_GROUPS=$ng MPC_FUSED_DEBUG=1 python scripts/bench_layers.py --model text --chain --reps 1 2>&1 | grep fused_small | head -1; done
+ncu --set full --clock-control none -k regex:fused_small -c 1 -o gpurun_out/ncu_fused_text_n256 python scripts/bench_layers.py --model text --chain --reps 2 > /dev/null 2>&1

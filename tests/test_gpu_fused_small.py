@@ -5,8 +5,8 @@ wide-K text matmul runs on it) against the oracle, bit for bit.
 In-process cases use the default launch (split-K over the SMs + finalize);
 subprocess cases force the knobs read once per process: one CTA (no split-K,
 z written by the kernel), one 32-K block per CTA, short drained TMEM units
-(the multi-unit path the full-size text matmul needs only past 4.9 M K), one
-converter group instead of two, contiguous K ranges, bulk prefetches and
+(the multi-unit path the full-size text matmul needs only past 4.9 M K), two
+converter groups instead of one, contiguous K ranges, bulk prefetches and
 MPC_FUSED_SMALL=0 (the planes-based path) — every variant must give the
 oracle's shares.
 """
@@ -107,7 +107,7 @@ print(hashlib.sha256(z.view(torch.int64).cpu().numpy().tobytes()).hexdigest())
 
 @pytest.mark.parametrize("env", [{"MPC_FUSED_CTAS": "1"}, {"MPC_FUSED_CTAS": "148"},
                                  {"MPC_FUSED_UNIT": "3"}, {"MPC_FUSED_UNIT": "7", "MPC_FUSED_CTAS": "5"},
-                                 {"MPC_FUSED_GROUPS": "1"}, {"MPC_FUSED_GROUPS": "1", "MPC_FUSED_UNIT": "3"},
+                                 {"MPC_FUSED_GROUPS": "2"}, {"MPC_FUSED_GROUPS": "2", "MPC_FUSED_UNIT": "3"},
                                  {"MPC_FUSED_CYCLIC": "0", "MPC_FUSED_UNIT": "5"}, {"MPC_FUSED_PF": "2"},
                                  {"MPC_FUSED_SMALL": "0"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
