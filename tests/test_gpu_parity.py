@@ -61,7 +61,7 @@ def test_encode_decode_parity(mpc):
 
 # ------------------------------------------------------------------ share / reveal
 @pytest.mark.parametrize("P", [1, 2, 3, 8])
-@pytest.mark.parametrize("n", [1, 7, 4097, 100003])
+@pytest.mark.parametrize("n", [1, 7, 4096, 4097, 100003, 262144])   # n % 4 == 0: the 32-byte path
 def test_share_parity_all_parties(mpc, P, n):
     c = ctx(mpc, P)
     x = synth.uniform_ring((n,), seed=n + P)
