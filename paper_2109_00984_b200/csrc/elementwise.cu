@@ -227,11 +227,146 @@ __device__ __forceinline__ void load16(const uint64_t* __restrict__ src, bool fu
     }
 }
 
+// MPC_SPLIT2=0 turns the two-party split paths below off (A/B measurements); set once per
+// process by the first split launch (a constant-bank flag, so captured graphs see it too).
+__constant__ int g_split2 = 1;
+__device__ __forceinline__ bool split2_enabled() { return g_split2 != 0; }
+static void split2_config() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+    const char* e = getenv("MPC_SPLIT2");
+    if (e && atoi(e) == 0) {
+        const int zero = 0;
+        cudaMemcpyToSymbol(g_split2, &zero, sizeof(zero));
+    }
+}
+
+// host mirror of the device-side choice: the two-party paths run twice as many (half-size)
+// warp tasks, so the launchers size their grids for them
+static bool split2_host() {
+    static const bool on = !(getenv("MPC_SPLIT2") && atoi(getenv("MPC_SPLIT2")) == 0);
+    return on;
+}
+static bool left2(const LeftSplitArgs& a) {
+    return split2_host() && a.cp_src == a.minus && a.minus && a.Pcopy == 2 && a.Psum == 2 && a.sum_planes && a.cp_planes;
+}
+static bool right2(const RightSplitArgs& a) {
+    return split2_host() && a.cp_src == a.minus && a.minus && a.Pcopy == 2 && a.Psum == 2 && a.cp_planes;
+}
+
+// Two parties with the copies fused into the mask (the common all-parties Beaver case):
+// every share load of a task is issued before any is used, so a task costs one memory
+// round trip instead of one per (party, operand); tasks are half the generic ones
+// (8 K values per lane) so the loads fit in the registers of two 256-thread blocks per SM.
+// Left: a warp covers 8 rows x 32 K (lane -> row lane & 7, 8-K chunk lane >> 3).
+template <Layout LO>
+__device__ __forceinline__ void split_left2_body(const LeftSplitArgs& a, int64_t bid, int64_t nblk) {
+    const int64_t KB = num_kb(a.K);
+    const int64_t row_groups = (a.M + 7) / 8;
+    const int64_t warps_total = row_groups * KB;                 // whole padded K: pad limbs must be 0
+    const int64_t nb = a.batch > 1 ? a.batch : 1;
+    const int lane = threadIdx.x & 31;
+    const bool vec = (a.K & 1) == 0 && (a.party_stride & 1) == 0 && (a.in_bstride & 1) == 0;
+    for (int64_t bw = (bid * blockDim.x + threadIdx.x) >> 5; bw < warps_total * nb; bw += (nblk * blockDim.x) >> 5) {
+        const int64_t bi = bw / warps_total, w = bw - bi * warps_total;
+        const uint64_t* plus = a.plus + bi * a.in_bstride;
+        const uint64_t* minus = a.minus + bi * a.in_bstride;
+        uint8_t* sum_planes = a.sum_planes + bi * a.sum_bstride;
+        uint8_t* cp_planes = a.cp_planes + bi * a.cp_bstride;
+        const int64_t row = (w / KB) * 8 + (lane & 7);
+        const int64_t k0 = (w % KB) * 32 + (lane >> 3) * 8;
+        if (row >= a.M) continue;
+        const int64_t kleft = a.K - k0;                          // <= 0: pure K padding
+        uint64_t x0[8], a0[8], x1[8], a1[8];
+        const int64_t o = row * a.K + k0;
+        if (vec && kleft >= 8) {
+            const ulonglong2* p0 = reinterpret_cast<const ulonglong2*>(plus + o);
+            const ulonglong2* p1 = reinterpret_cast<const ulonglong2*>(minus + o);
+            const ulonglong2* p2 = reinterpret_cast<const ulonglong2*>(plus + a.party_stride + o);
+            const ulonglong2* p3 = reinterpret_cast<const ulonglong2*>(minus + a.party_stride + o);
+            ulonglong2 t0[4], t1[4], t2[4], t3[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) { t0[m] = __ldg(p0 + m); t1[m] = __ldg(p1 + m); t2[m] = __ldg(p2 + m); t3[m] = __ldg(p3 + m); }
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                x0[2 * m] = t0[m].x; x0[2 * m + 1] = t0[m].y; a0[2 * m] = t1[m].x; a0[2 * m + 1] = t1[m].y;
+                x1[2 * m] = t2[m].x; x1[2 * m + 1] = t2[m].y; a1[2 * m] = t3[m].x; a1[2 * m + 1] = t3[m].y;
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const bool ok = m < kleft;
+                x0[m] = ok ? __ldg(plus + o + m) : 0ull;
+                a0[m] = ok ? __ldg(minus + o + m) : 0ull;
+                x1[m] = ok ? __ldg(plus + a.party_stride + o + m) : 0ull;
+                a1[m] = ok ? __ldg(minus + a.party_stride + o + m) : 0ull;
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < 8; ++m) x0[m] = x0[m] - a0[m] + x1[m] - a1[m];
+        if (a.add_sum_first) {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) a0[m] += x0[m];
+        }
+        store_limbs8<LO>(cp_planes, row, k0, KB, a0);
+        store_limbs8<LO>(cp_planes + a.cp_planes_stride, row, k0, KB, a1);
+        store_limbs8<LO>(sum_planes, row, k0, KB, x0);
+    }
+}
+// Right (K x N row-major -> planes with rows = N): a warp covers 32 n x 8 K (lane -> n);
+// every load is 8 B per lane, 256 B contiguous per warp and K row.
+template <Layout LO>
+__device__ __forceinline__ void split_right2_body(const RightSplitArgs& a, int64_t bid, int64_t nblk) {
+    const int64_t KB = num_kb(a.K);
+    const int64_t ngroups = (a.N + 31) / 32;
+    const int64_t warps_total = ngroups * KB * 4;               // whole padded K, 8 per task
+    const int64_t nb = a.batch > 1 ? a.batch : 1;
+    const int lane = threadIdx.x & 31;
+    for (int64_t bw = (bid * blockDim.x + threadIdx.x) >> 5; bw < warps_total * nb; bw += (nblk * blockDim.x) >> 5) {
+        const int64_t bi = bw / warps_total, w = bw - bi * warps_total;
+        const uint64_t* plus = a.plus + bi * a.in_bstride;
+        const uint64_t* minus = a.minus + bi * a.in_bstride;
+        uint8_t* sum_planes = a.sum_planes ? a.sum_planes + bi * a.sum_bstride : nullptr;
+        uint8_t* cp_planes = a.cp_planes + bi * a.cp_bstride;
+        const int64_t kc = w / ngroups, ng = w % ngroups;
+        const int64_t n = ng * 32 + lane;
+        const int64_t k0 = kc * 8;
+        if (n >= a.N) continue;
+        const int lim = (int)(a.K - k0 < 8 ? (a.K - k0 > 0 ? a.K - k0 : 0) : 8);
+        const uint64_t* py = plus + k0 * a.N + n;
+        const uint64_t* pb = minus + k0 * a.N + n;
+        uint64_t y0[8], b0[8], y1[8], b1[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const bool ok = m < lim;
+            y0[m] = ok ? __ldg(py + m * a.N) : 0ull;
+            b0[m] = ok ? __ldg(pb + m * a.N) : 0ull;
+            y1[m] = ok ? __ldg(py + a.party_stride + m * a.N) : 0ull;
+            b1[m] = ok ? __ldg(pb + a.party_stride + m * a.N) : 0ull;
+        }
+#pragma unroll
+        for (int m = 0; m < 8; ++m) y0[m] = y0[m] - b0[m] + y1[m] - b1[m];
+        if (a.add_delta_first) {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) b0[m] += y0[m];
+        }
+        store_limbs8<LO>(cp_planes, n, k0, KB, b0);
+        store_limbs8<LO>(cp_planes + a.cp_planes_stride, n, k0, KB, b1);
+        if (sum_planes) store_limbs8<LO>(sum_planes, n, k0, KB, y0);
+    }
+}
+
 // (bid, nblk): this block's index among the nblk blocks working on the left split.
 // LO: plane layout of the output (Layout::Left normally; Layout::Right when the
 // ring GEMM runs transposed, see RingGemmParams::transpose_out).
 template <Layout LO>
 __device__ __forceinline__ void split_left_body(const LeftSplitArgs& a, int64_t bid, int64_t nblk) {
+    if (a.cp_src == a.minus && a.minus && a.Pcopy == 2 && a.Psum == 2 && a.sum_planes && a.cp_planes &&
+        split2_enabled()) {
+        split_left2_body<LO>(a, bid, nblk);
+        return;
+    }
     const int64_t KB = num_kb(a.K);
     const int64_t row_groups = (a.M + 7) / 8;
     const int64_t kgroups = (KB * kKBlock + 63) / 64;      // whole padded K: pad limbs must be 0
@@ -289,8 +424,10 @@ __global__ void __launch_bounds__(256) split_left_kernel(LeftSplitArgs a) {
     split_left_body<LO>(a, blockIdx.x, gridDim.x);
 }
 cudaError_t launch_split_left(const LeftSplitArgs& a, cudaStream_t st) {
+    split2_config();
     if (a.M == 0 || a.K == 0) return cudaSuccess;
-    const int64_t warps = ((a.M + 7) / 8) * ((num_kb(a.K) * kKBlock + 63) / 64) * (a.batch > 1 ? a.batch : 1);
+    const int64_t warps = ((a.M + 7) / 8) * ((num_kb(a.K) * kKBlock + 63) / 64) * (a.batch > 1 ? a.batch : 1) *
+                          (left2(a) ? 2 : 1);
     if (a.swap == 2) split_left_kernel<Layout::Small><<<grid_for(warps * 32), 256, 0, st>>>(a);
     else if (a.swap) split_left_kernel<Layout::Right><<<grid_for(warps * 32), 256, 0, st>>>(a);
     else split_left_kernel<Layout::Left><<<grid_for(warps * 32), 256, 0, st>>>(a);
@@ -332,6 +469,10 @@ __device__ __forceinline__ void load_cols(const uint64_t* __restrict__ base, int
 
 template <Layout LO>
 __device__ __forceinline__ void split_right_body(const RightSplitArgs& a, int64_t bid, int64_t nblk) {
+    if (a.cp_src == a.minus && a.minus && a.Pcopy == 2 && a.Psum == 2 && a.cp_planes && split2_enabled()) {
+        split_right2_body<LO>(a, bid, nblk);
+        return;
+    }
     const int64_t KB = num_kb(a.K);
     const int64_t ngroups = (a.N + 31) / 32;
     const int64_t kchunks = KB * 2;                         // whole padded K, 16 per chunk
@@ -394,8 +535,9 @@ __global__ void __launch_bounds__(256, 2) split_right_kernel(RightSplitArgs a) {
     split_right_body<LO>(a, blockIdx.x, gridDim.x);
 }
 cudaError_t launch_split_right(const RightSplitArgs& a, cudaStream_t st) {
+    split2_config();
     if (a.N == 0 || a.K == 0) return cudaSuccess;
-    const int64_t warps = ((a.N + 31) / 32) * (num_kb(a.K) * 2) * (a.batch > 1 ? a.batch : 1);
+    const int64_t warps = ((a.N + 31) / 32) * (num_kb(a.K) * 2) * (a.batch > 1 ? a.batch : 1) * (right2(a) ? 2 : 1);
     if (a.swap == 2) split_right_kernel<Layout::Small><<<grid_for(warps * 32), 256, 0, st>>>(a);
     else if (a.swap) split_right_kernel<Layout::Left><<<grid_for(warps * 32), 256, 0, st>>>(a);
     else split_right_kernel<Layout::Right><<<grid_for(warps * 32), 256, 0, st>>>(a);
@@ -417,13 +559,14 @@ __global__ void __launch_bounds__(256, 2) split_both_kernel(LeftSplitArgs l, Rig
     asm volatile("griddepcontrol.launch_dependents;");
 }
 cudaError_t launch_split_both(const LeftSplitArgs& l, const RightSplitArgs& r, cudaStream_t st) {
+    split2_config();
     const bool dl = l.M > 0 && l.K > 0, dr = r.N > 0 && r.K > 0;
     if (!dl && !dr) return cudaSuccess;
     if (!dr) return launch_split_left(l, st);
     if (!dl) return launch_split_right(r, st);
     const int64_t bl = l.batch > 1 ? l.batch : 1, br = r.batch > 1 ? r.batch : 1;
-    const int64_t wl = ((l.M + 7) / 8) * ((num_kb(l.K) * kKBlock + 63) / 64) * 32 * bl;
-    const int64_t wr = ((r.N + 31) / 32) * (num_kb(r.K) * 2) * 32 * br;
+    const int64_t wl = ((l.M + 7) / 8) * ((num_kb(l.K) * kKBlock + 63) / 64) * 32 * bl * (left2(l) ? 2 : 1);
+    const int64_t wr = ((r.N + 31) / 32) * (num_kb(r.K) * 2) * 32 * br * (right2(r) ? 2 : 1);
     // share the block budget in proportion to the bytes each side moves
     const int64_t bytes_l = l.M * l.K * (int64_t)(2 * l.Psum + l.Pcopy + 1) * bl;
     const int64_t bytes_r = r.N * r.K * (int64_t)(2 * r.Psum + r.Pcopy + 1) * br;
@@ -527,12 +670,13 @@ __global__ void __launch_bounds__(256, 2) split_conv_kernel(Im2colSplitArgs im, 
     asm volatile("griddepcontrol.launch_dependents;");
 }
 cudaError_t launch_split_conv(const Im2colSplitArgs& im, const LeftSplitArgs& wt, cudaStream_t st) {
+    split2_config();
     const bool di = im.g.M() > 0 && im.g.K() > 0, dw = wt.M > 0 && wt.K > 0;
     if (!dw) return launch_split_im2col(im, st);
     if (!di) return launch_split_left(wt, st);
     if ((im.layout_right != 0) == (wt.swap != 0)) return cudaErrorInvalidValue;   // one left, one right operand
     const int64_t wi = ((im.g.M() + 31) / 32) * num_kb(im.g.K()) * 2 * 32;
-    const int64_t ww = ((wt.M + 7) / 8) * ((num_kb(wt.K) * kKBlock + 63) / 64) * 32;
+    const int64_t ww = ((wt.M + 7) / 8) * ((num_kb(wt.K) * kKBlock + 63) / 64) * 32 * (left2(wt) ? 2 : 1);
     // blocks in proportion to the bytes each side moves (the im2col side re-reads each input kh*kw times)
     const int64_t bytes_i = im.g.M() * im.g.K() * (int64_t)(2 * im.Psum + im.Pcopy + 1);
     const int64_t bytes_w = wt.M * wt.K * (int64_t)(2 * wt.Psum + wt.Pcopy + 1);
