@@ -8,26 +8,30 @@
 //     L @ R^T = sum_i sum_{j <= 7-i} 2^(8(i+j)) L_i @ R_j^T      (mod 2^64)
 // with the 32 rows of the 8 planes L_0..L_7 stacked into two 128-row MMA
 // operands: A_lo = [L_0; L_1; L_2; L_3] and A_hi = [L_4; L_5; L_6; L_7]
-// (rows 32 i' + r).  One tcgen05.mma.cta_group::1.kind::i8 (M = 128, N = 32,
-// K = 32) with right plane R_j gives L_i @ R_j^T for four planes i at once, in
-// TMEM lanes 32 i' + r:
-//     D_lo,j = A_lo @ R_j^T  (j = 0..7)     D_hi,j = A_hi @ R_j^T  (j = 0..3)
-// — 12 MMAs per 32-K block (j <= 3 for A_hi: pairs with i + j >= 8 vanish),
-// 12 accumulators of 32 columns in TMEM.  Each epilogue thread owns TMEM lane
-// 32 i' + r (plane i = i' or 4 + i', output row r) and adds
-//     run[c] += D_j[lane][c] << 8(i + j)        (read as u32, i + j <= 7)
+// (rows 32 i' + r), and the 8 right planes stacked along N (the 32 rows of
+// R_0..R_7 of one 32-K block are 8 KiB contiguous in Layout::Small: one
+// 256-row B operand).  Two tcgen05.mma.cta_group::1.kind::i8 per 32-K block:
+//     A_lo @ [R_0..R_7]^T (N = 256) -> columns 32 j + c: L_i' @ R_j^T,
+//     A_hi @ [R_0..R_3]^T (N = 128) -> columns 128 + 32 j + c: L_{4+i'} @ R_j^T,
+// so TMEM lane 32 i' + r, column block j holds shift i' + j from both (A_hi's
+// block j + 4 has shift 4 + i' + j = i' + (j + 4)).  Each epilogue thread owns
+// TMEM lane 32 i' + r and adds
+//     run[c] += D[lane][32 j + c] << 8(i' + j)        (read as u32, i' + j <= 7)
 // into u64 running sums; at the tile end the four planes of a row are summed
 // through shared memory and c_p / the truncation applied (the store mapping,
-// split-K slabs and finalize are those of ring_gemm.cu).
+// split-K slabs and finalize are those of ring_gemm.cu).  Round 1 issued 12 MMAs
+// (one per right plane, N = 32) into 12 accumulators; the stacked B operand
+// reads the A stacks 2 instead of 12 times per block.
 //
-// Exactness: every D entry is a single limb product sum, D <= K_r * 255^2, so
-// the s32 accumulator read as u32 is exact for K_r <= 66052 (2064 32-K
-// blocks, the unit length cap); for i + j >= 4 only D mod 2^(64-8(i+j)) matters.
+// Exactness: an entry with shift i' + j <= 3 is a single limb product sum
+// (no A_hi term there), D <= K_r * 255^2, so the s32 accumulator read as u32 is
+// exact for K_r <= 66052 (2064 32-K blocks, the unit length cap); for shifts
+// >= 4 only D mod 2^(64-8(i+j)) matters.
 //
 // Why: a 256 x 128 tile holding 32 x 32 useful outputs (the 32 x 519,820 x 32
 // text matmul) wastes 31/32 of the tensor work; stacking wastes
-// only the plane pairs with i + j >= 8 that share an MMA with needed ones
-// (12 of the 48 plane products issued per 32-K block).
+// only the plane pairs with i + j >= 8 (28 of the 64 plane products issued per
+// 32-K block).
 //
 // Operands in Layout::Small (common.cuh): one 32-K block of the 32 rows of all
 // 8 planes is 8 KiB contiguous, so a stage is two bulk copies (16 x 1 KiB
@@ -56,19 +60,21 @@ constexpr int kStageBytes = 16 * kChunk;          // A: 8 planes, B: 8 planes
 constexpr int kStages = 8;
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 128 + 32 * kEpiWarps;
-constexpr int kTmemCols = 512;                    // 12 accumulators x 32 columns used
+constexpr int kTmemCols = 512;                    // 256 columns used (8 column blocks of 32)
 constexpr int kMaxUnit = 2048;                    // 32-K blocks per accumulation unit (<= 2064)
-constexpr uint32_t kIdesc = (2u << 4)             // D: S32; A, B: unsigned 8-bit
-                          | ((uint32_t)(kTileN >> 3) << 17)
-                          | ((uint32_t)(128 >> 4) << 24);
+// instruction descriptor: D S32; A, B unsigned 8-bit; M = 128; N = 8 right planes x 32
+// columns (A_lo against R_0..R_7) or 4 x 32 (A_hi against R_0..R_3)
+constexpr uint32_t idesc_n(int n) { return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24); }
+constexpr uint32_t kIdescLo = idesc_n(8 * kTileN), kIdescHi = idesc_n(4 * kTileN);
 
-__device__ __forceinline__ void mma_u8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+__device__ __forceinline__ void mma_u8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p, e;\n\t"
         "elect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
-        :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate) : "memory");
+        :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
 }
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
     asm volatile(
@@ -175,13 +181,11 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_small_kernel(const __gr
                     const uint64_t da = smem_desc(smem_u32(smem + s * kStageBytes));
                     const uint64_t db = da + ((8 * kChunk) >> 4);
                     const uint32_t acc = kt == k0 ? 0u : 1u;
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        mma_u8(tmem_base + j * kTileN, da, db + (uint64_t)(j * (kChunk >> 4)), acc);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        mma_u8(tmem_base + (8 + j) * kTileN, da + (uint64_t)((4 * kChunk) >> 4),
-                               db + (uint64_t)(j * (kChunk >> 4)), acc);
+                    // the 8 right planes of a 32-K block are 8 KiB contiguous (Layout::Small): one
+                    // 256-row B operand.  A_lo x R_0..7 -> columns 32 j (shift i' + j), A_hi x R_0..3
+                    // -> columns 128 + 32 j (shift 4 + i' + j: the same as A_lo's there), 2 MMAs
+                    mma_u8(tmem_base, da, db, kIdescLo, acc);
+                    mma_u8(tmem_base + 4 * kTileN, da + (uint64_t)((4 * kChunk) >> 4), db, kIdescHi, 1u);
                     tc_commit(&empty[s]);
                     if (++s == kStages) { s = 0; ph ^= 1; }
                 }
@@ -210,10 +214,8 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_small_kernel(const __gr
                 mbar_wait(tfull, u & 1);
                 tc_fence_after();
 #pragma unroll
-                for (int a = 0; a < 12; ++a) {
-                    const int i = a < 8 ? q : 4 + q;                // plane of this lane in accumulator a
-                    const int j = a < 8 ? a : a - 8;
-                    const int sh = i + j;
+                for (int a = 0; a < 8; ++a) {
+                    const int sh = q + a;                           // lane group i' = q, column block j = a
                     if (sh > 7) continue;                           // warp-uniform (q is per warp)
                     uint32_t v[16];
                     tmem_ld16(tq + a * kTileN, v);
@@ -296,8 +298,11 @@ int ring_gemm_splits(int parties, int64_t M, int64_t N, int tkb, int64_t max_clu
 }
 
 // The 2-CTA kernel issues 36 MMAs of 64 cycles per 256 x 128 tile and 32-K
-// block on a CTA pair; the stacked one 12 MMAs of ~48 cycles (N = 32 MMAs are
-// shared-memory bound) per 32 x 32 tile and block on one SM.
+// block on a CTA pair.  The stacked one is costed at 576 cycles per 32 x 32 tile
+// and block on one SM — the round-1 figure (12 N = 32 MMAs of ~48 cycles): its
+// two stacked MMAs now take ~192, but a tile then needs its 16 KiB of planes
+// every ~200 cycles, more than the L2 -> SM feed gives one SM (~36-70 B/clk), so
+// the old figure stays as the conservative cost that selected the shapes it wins.
 double ring_gemm_model_cycles(int parties, int64_t M, int64_t N, int tkb, int64_t max_clusters, bool small) {
     const int s = ring_gemm_splits(parties, M, N, tkb, max_clusters, small);
     if (small)
