@@ -107,6 +107,9 @@ struct FusedSmallParams {
     int cyclic;                         // set by the launcher: 32-K blocks dealt to the CTAs round-robin
     unsigned long long* dbg;            // MPC_FUSED_DEBUG: [0] MMA full-wait, [1] MMA total, [2] converter
                                         // empty-wait, [3] converter total cycles (summed over CTAs / warps)
+    // set by the launcher for the TMA-staged kernel: 3-D maps over x, a ([2][M][K], boxes of 16 K x
+    // 32 rows, 128-byte swizzle) and y, b ([2][K][N], boxes of N x 32 K rows)
+    CUtensorMap tm_x, tm_a, tm_y, tm_b;
 };
 size_t fused_small_smem_bytes();
 int fused_small_ctas(int64_t K, int sms);

@@ -41,25 +41,29 @@
 // ends into shared-memory output sums (a warp reads the TMEM lane quadrant
 // warp % 4; its warps 4..7 hold party 0, 8..11 party 1) and writes the slab.
 //
+// Two kernels.  The register path (any K, N) is described above; the TMA-staged one
+// (K and N even: 16-byte tensor-map strides) lets one producer thread bring each
+// block's shares into shared memory by TMA (x / a in 128-byte-swizzled boxes) and
+// the converters read them from there — the default where it applies.
+//
 // Measured (text 32 x 519,820 x 32, one B200; scripts/gpu/fused*.sh,
-// profiles/r02/fused_small/): 0.49 ms for the planes-based path -> 0.271 ms (0.61
-// of the HBM floor; kernel 267 µs under ncu, 1.065 GB DRAM = the algorithmic
-// bytes).  With 36 N = 32/64 plane-pair MMAs per block the MMA thread was busy
-// 58% and the tensor core's shared-memory operand reads (192 KB per block) shared
-// the L1TEX data path with the converters' loads and plane stores (LSU 68% +
-// tensor core 35% of its wavefronts); the 8 stacked MMAs read 80 KB (MMA thread
-// 18% busy).  The converters now bound the kernel (load latency; a read-only
-// probe of the access pattern, scripts/fused_read_probe.cu, streams at 6.5 TB/s).
-// Kept as knobs: MPC_FUSED_GROUPS=2 (two converter groups on alternate blocks:
-// 0.280 ms), MPC_FUSED_PFD (prefetch distance; 0: 0.298, 2: 0.296 ms), MPC_FUSED_PF
-// (2: bulk row prefetches, message-rate bound), MPC_FUSED_CYCLIC=0 (contiguous K
-// ranges, +2-4%).  Tried and dropped: two blocks of loads in flight per thread
-// (setmaxnreg-moved registers; no faster), L1::no_allocate loads (2x slower).
+// profiles/r02/fused_small/): planes-based path 0.49 ms; register path 0.271 ms;
+// TMA-staged 0.193 ms = 0.86 of the HBM floor (kernel 174 µs under ncu: 1.065 GB
+// DRAM = the algorithmic bytes at 6.1 TB/s).  The register path's converters
+// wait on scattered global loads (long-scoreboard) whose fills share the L1TEX
+// data path with the plane stores and the tensor core's operand reads; with 36
+// N = 32/64 plane-pair MMAs per block (before the stacked B operand) that path
+// ran 0.286 ms (LSU 68% + tensor core 35% of the L1TEX wavefronts).  Knobs:
+// MPC_FUSED_TMA=0 (register path), MPC_FUSED_GROUPS=2 (register path: two
+// converter groups on alternate blocks), MPC_FUSED_PFD / MPC_FUSED_PF (its L2
+// prefetch), MPC_FUSED_CYCLIC=0 (contiguous K ranges); dropped: two blocks of
+// loads in flight per thread (setmaxnreg), L1::no_allocate loads (2x slower).
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include "common.cuh"
 #include "ring_gemm.h"
@@ -398,7 +402,280 @@ __global__ void __launch_bounds__(kThreadsOf(NG), 1) fused_small_kernel(const __
     }
 }
 
+// ---------------------------------------------------------------- TMA-staged variant
+// The same product, the shares brought into shared memory by the tensor-memory
+// accelerator instead of the converters' own loads: one producer thread issues, per
+// 32-K block, 8 boxes of 16 K x 32 rows of x_p / a_p (128-byte swizzle, so the
+// converters' 16-byte reads of one row piece per lane hit distinct banks) and 4
+// boxes of N x 32 K rows of y_p / b_p into a raw stage (64 KiB, 2 stages; rows past
+// M / K are zero-filled by the TMA); the converters read their 8 K values of each
+// input from shared memory, free the raw stage, and write the planes into a plane
+// stage (48 KiB, 2 stages) as before.  The MMAs and the drain are the register
+// path's; the drained sums stay in registers and are summed across lane groups in
+// a raw stage at the end.  Needs K and N even (16-byte tensor-map strides).
+constexpr int kRawStages = 2, kPlaneStages = 2;
+constexpr int kRawBytes = 64 * 1024;                 // 4 x 8 KiB left boxes, 4 x (32 N 8 B) right boxes
+constexpr int kRawRight = 32 * 1024;
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        :: "r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(384, 1) fused_small_tma_kernel(const __grid_constant__ FusedSmallParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");   // the finalize may launch
+    uint8_t* planes = smem;                                                    // [kPlaneStages][48 KiB]
+    uint8_t* raw = smem + kPlaneStages * kStageBytes;                          // [kRawStages][64 KiB]
+    uint64_t* pfull = reinterpret_cast<uint64_t*>(raw + kRawStages * kRawBytes);
+    uint64_t* pempty = pfull + kPlaneStages;
+    uint64_t* rfull = pempty + kPlaneStages;
+    uint64_t* rempty = rfull + kRawStages;
+    uint64_t* tfull = rempty + kRawStages;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t M = p.M, K = p.K, N = p.N;
+    const int KB = (int)num_kb(K);
+    const int g = blockIdx.x, G = gridDim.x;
+    const int nblk = KB > g ? (KB - g + G - 1) / G : 0;                       // blocks g, g + G, ...
+    const int U = p.unit;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kPlaneStages; ++s) { mbar_init(&pfull[s], 8); mbar_init(&pempty[s], 1); }
+        for (int s = 0; s < kRawStages; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 8); }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 8);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(smem_u32(tmem_slot)), "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------ MMA issuer (one thread)
+        if (lane == 0) {
+            int s = 0; uint32_t ph = 0; uint32_t u = 0;
+            for (int k0 = 0; k0 < nblk; k0 += U, ++u) {
+                const int k1 = min(nblk, k0 + U);
+                mbar_wait(tempty, (u & 1) ^ 1);
+                tc_fence_after();
+                for (int kt = k0; kt < k1; ++kt) {
+                    mbar_wait(&pfull[s], ph);
+                    tc_fence_after();
+                    uint32_t st = smem_u32(planes + s * kStageBytes), tb = tmem_base;
+                    asm volatile("mov.b32 %0, %0;" : "+r"(st));
+                    asm volatile("mov.b32 %0, %0;" : "+r"(tb));
+                    const uint64_t d0 = smem_desc(st);
+                    const uint32_t first = kt == k0 ? 0u : 1u;
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const uint32_t dq = tb + q * 256;
+                        const uint64_t dB = d0 + (uint64_t)((kOffB0 + q * kSet) >> 4);
+                        const uint64_t dA = d0 + (uint64_t)((kOffA0 + q * kSet) >> 4);
+                        const uint64_t dD = d0 + (uint64_t)(kOffDelta >> 4);
+                        mma_u8(dq, d0, dB, idesc(256), first);
+                        mma_u8(dq + 128, d0 + (uint64_t)((4 * kPlane) >> 4), dB, idesc(128), 1u);
+                        mma_u8(dq, dA, dD, idesc(256), 1u);
+                        mma_u8(dq + 128, dA + (uint64_t)((4 * kPlane) >> 4), dD, idesc(128), 1u);
+                    }
+                    tc_commit(&pempty[s]);
+                    if (++s == kPlaneStages) { s = 0; ph ^= 1; }
+                }
+                tc_commit(tfull);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ------------------------------------------------ TMA producer (one thread)
+        asm volatile("griddepcontrol.wait;" ::: "memory");                  // shares written by earlier kernels
+        if (lane == 0) {
+            int s = 0; uint32_t ph = 0;
+            const uint32_t bytes = 8 * 4096 + 4 * (uint32_t)(32 * N * 8);
+            for (int i = 0; i < nblk; ++i) {
+                const int k0 = (g + i * G) * 32;
+                mbar_wait(&rempty[s], ph ^ 1);
+                mbar_expect_tx(&rfull[s], bytes);
+                const uint32_t dst = smem_u32(raw + s * kRawBytes);
+#pragma unroll
+                for (int src = 0; src < 4; ++src) {                          // x_0, a_0, x_1, a_1
+                    const CUtensorMap* m = (src & 1) ? &p.tm_a : &p.tm_x;
+                    tma_load_3d(dst + src * 8192, m, k0, 0, src >> 1, &rfull[s]);
+                    tma_load_3d(dst + src * 8192 + 4096, m, k0 + 16, 0, src >> 1, &rfull[s]);
+                }
+#pragma unroll
+                for (int src = 0; src < 4; ++src) {                          // y_0, b_0, y_1, b_1
+                    const CUtensorMap* m = (src & 1) ? &p.tm_b : &p.tm_y;
+                    tma_load_3d(dst + kRawRight + src * (uint32_t)(32 * N * 8), m, 0, k0, src >> 1, &rfull[s]);
+                }
+                if (++s == kRawStages) { s = 0; ph ^= 1; }
+            }
+        }
+        __syncwarp();
+    } else if (warp >= 4) {
+        // ------------------------------------------------ converters (shared memory -> planes), drain
+        const int w8 = warp - 4;
+        const bool left = w8 < 4;
+        const int grp = w8 & 3;
+        const int idx = grp * 8 + (lane & 7);
+        const int kq = lane >> 3;
+        const uint32_t poff = plane_off(idx, kq);
+        const int q4 = warp & 3;
+        const int party = w8 >> 2;
+        uint64_t run[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) run[c] = 0ull;
+        int rs = 0, ps = 0; uint32_t rph = 0, pph = 0, u = 0;
+        for (int i = 0; i < nblk; ++i) {
+            uint64_t v0[8], v1[8], v2[8], v3[8];
+            mbar_wait(&rfull[rs], rph);
+            const uint8_t* rb = raw + rs * kRawBytes;
+            if (left) {
+                // row idx, K values 8 kq .. 8 kq + 7: half kq >> 1, 16-byte chunks (kq & 1) * 4 + j,
+                // stored at chunk ^ (row & 7) (128-byte swizzle)
+                const uint8_t* hb = rb + (kq >> 1) * 4096 + idx * 128;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int ch = (((kq & 1) * 4 + j) ^ (idx & 7)) * 16;
+                    const ulonglong2 t0 = *reinterpret_cast<const ulonglong2*>(hb + ch);
+                    const ulonglong2 t1 = *reinterpret_cast<const ulonglong2*>(hb + 8192 + ch);
+                    const ulonglong2 t2 = *reinterpret_cast<const ulonglong2*>(hb + 16384 + ch);
+                    const ulonglong2 t3 = *reinterpret_cast<const ulonglong2*>(hb + 24576 + ch);
+                    v0[2 * j] = t0.x; v0[2 * j + 1] = t0.y; v1[2 * j] = t1.x; v1[2 * j + 1] = t1.y;
+                    v2[2 * j] = t2.x; v2[2 * j + 1] = t2.y; v3[2 * j] = t3.x; v3[2 * j + 1] = t3.y;
+                }
+            } else {
+                const uint64_t* r0 = reinterpret_cast<const uint64_t*>(rb + kRawRight);
+                const int64_t sstride = 32 * N;                              // elements per right box
+                const bool ok = idx < N;
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    const int64_t o = (int64_t)(kq * 8 + m) * N + idx;
+                    v0[m] = ok ? r0[o] : 0ull;
+                    v1[m] = ok ? r0[sstride + o] : 0ull;
+                    v2[m] = ok ? r0[2 * sstride + o] : 0ull;
+                    v3[m] = ok ? r0[3 * sstride + o] : 0ull;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&rempty[rs]);                         // this warp is done reading
+            if (++rs == kRawStages) { rs = 0; rph ^= 1; }
+#pragma unroll
+            for (int m = 0; m < 8; ++m) v0[m] = v0[m] - v1[m] + v2[m] - v3[m];
+            mbar_wait(&pempty[ps], pph ^ 1);
+            uint8_t* st = planes + ps * kStageBytes;
+            if (left) {
+                st_planes8(st + kOffEps, poff, kPlane, v0);
+                st_planes8(st + kOffA0, poff, kPlane, v1);
+                st_planes8(st + kOffA0 + kSet, poff, kPlane, v3);
+            } else {
+#pragma unroll
+                for (int m = 0; m < 8; ++m) v1[m] += v0[m];                 // b'_0 = b_0 + delta (R8)
+                st_planes8(st + kOffDelta, poff, kPlane, v0);
+                st_planes8(st + kOffB0, poff, kPlane, v1);
+                st_planes8(st + kOffB0 + kSet, poff, kPlane, v3);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pfull[ps]);
+            if (++ps == kPlaneStages) { ps = 0; pph ^= 1; }
+            if ((i + 1) % U != 0 && i + 1 != nblk) continue;
+            mbar_wait(tfull, u & 1);
+            tc_fence_after();
+            const uint32_t tq = tmem_base + ((uint32_t)(q4 * 32) << 16) + party * 256;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (q4 + j > 7) continue;
+                uint32_t a[16], b[16];
+                tmem_ld16(tq + j * 32, a);
+                tmem_ld16(tq + j * 32 + 16, b);
+                tmem_wait_ld();
+                const int sh = 8 * (q4 + j);
+#pragma unroll
+                for (int c = 0; c < 16; ++c) { run[c] += (uint64_t)a[c] << sh; run[16 + c] += (uint64_t)b[c] << sh; }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty);
+            ++u;
+        }
+        // every TMA write has landed (each was waited on) and every MMA completed: the raw stages are
+        // free; sum the four lane groups of each output row there
+        uint64_t* red = reinterpret_cast<uint64_t*>(raw);                    // [party][i'][row][32]
+        uint64_t* mine = red + (((int64_t)party * 4 + q4) * kRows + lane) * kRows;
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) *reinterpret_cast<ulonglong2*>(mine + c) = make_ulonglong2(run[c], run[c + 1]);
+        conv_sync();
+        asm volatile("griddepcontrol.wait;" ::: "memory");                  // C / Z / partials after the predecessor
+        for (int e = threadIdx.x - 128; e < 2 * kRows * kRows; e += 256) {
+            const int pq = e >> 10, r = (e >> 5) & 31, col = e & 31;
+            if (r >= M || col >= N) continue;
+            uint64_t v = 0;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) v += red[(((int64_t)pq * 4 + qq) * kRows + r) * kRows + col];
+            const int64_t o = (int64_t)pq * M * N + r * N + col;
+            if (G > 1) {
+                p.partials[(int64_t)g * 2 * M * N + o] = v;
+            } else {
+                if (p.C) v += p.C[o];
+                p.Z[o] = p.trunc_bits ? div_pow2_round(v, p.trunc_bits) : v;
+            }
+        }
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem_base), "r"(kTmemCols));
+    }
+}
+
 }  // namespace gemm_fused
+
+static size_t fused_small_tma_smem_bytes() {
+    return (size_t)gemm_fused::kPlaneStages * gemm_fused::kStageBytes + (size_t)gemm_fused::kRawStages * gemm_fused::kRawBytes +
+           1024 /*align*/ + 256 /*barriers*/;
+}
+
+// 3-D tensor maps of the TMA-staged kernel (false: not encodable here -> the register path)
+static bool fused_small_maps(FusedSmallParams& q) {
+    static const PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr) != cudaSuccess ||
+            qr != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    if (!enc || (q.K & 1) || (q.N & 1) || q.K < 32) return false;
+    for (const void* ptr : {(const void*)q.x, (const void*)q.a, (const void*)q.y, (const void*)q.b})
+        if (reinterpret_cast<uintptr_t>(ptr) & 15) return false;
+    const cuuint32_t es[3] = {1, 1, 1};
+    auto left = [&](CUtensorMap* m, const uint64_t* base) {
+        const cuuint64_t dims[3] = {(cuuint64_t)q.K, (cuuint64_t)q.M, 2};
+        const cuuint64_t strides[2] = {(cuuint64_t)q.K * 8, (cuuint64_t)(q.M * q.K * 8)};
+        const cuuint32_t box[3] = {16, 32, 1};
+        return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint64_t*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    auto right = [&](CUtensorMap* m, const uint64_t* base) {
+        const cuuint64_t dims[3] = {(cuuint64_t)q.N, (cuuint64_t)q.K, 2};
+        const cuuint64_t strides[2] = {(cuuint64_t)q.N * 8, (cuuint64_t)(q.K * q.N * 8)};
+        const cuuint32_t box[3] = {(cuuint32_t)q.N, 32, 1};
+        return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint64_t*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    return left(&q.tm_x, q.x) && left(&q.tm_a, q.a) && right(&q.tm_y, q.y) && right(&q.tm_b, q.b);
+}
 
 size_t fused_small_smem_bytes() {
     return (size_t)gemm_fused::kStages * gemm_fused::kStageBytes + 2 * 32 * 32 * 8 /*output sums*/ +
@@ -434,6 +711,9 @@ cudaError_t fused_small_launch(const FusedSmallParams& p, cudaStream_t stream) {
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(gemm_fused::fused_small_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(gemm_fused::fused_small_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)fused_small_tma_smem_bytes());
         if (e != cudaSuccess) return e;
         attr_dev = dev;
     }
@@ -459,8 +739,13 @@ cudaError_t fused_small_launch(const FusedSmallParams& p, cudaStream_t stream) {
         cudaMalloc(&q0.dbg, sizeof(h));
         cudaMemsetAsync(q0.dbg, 0, sizeof(h), stream);
     }
-    cudaError_t e = launch_pdl(ng == 2 ? gemm_fused::fused_small_kernel<2> : gemm_fused::fused_small_kernel<1>,
-                               dim3((unsigned)G), dim3(gemm_fused::kThreadsOf(ng)), smem, stream, q0);
+    // TMA-staged kernel where the maps encode (K, N even; MPC_FUSED_TMA=0: the register path)
+    static const int env_tma = getenv("MPC_FUSED_TMA") ? atoi(getenv("MPC_FUSED_TMA")) : 1;
+    const bool tma = env_tma != 0 && fused_small_maps(q0);
+    cudaError_t e = tma ? launch_pdl(gemm_fused::fused_small_tma_kernel, dim3((unsigned)G), dim3(384),
+                                     fused_small_tma_smem_bytes(), stream, q0)
+                        : launch_pdl(ng == 2 ? gemm_fused::fused_small_kernel<2> : gemm_fused::fused_small_kernel<1>,
+                                     dim3((unsigned)G), dim3(gemm_fused::kThreadsOf(ng)), smem, stream, q0);
     if (debug) {
         cudaMemcpyAsync(h, q0.dbg, sizeof(h), cudaMemcpyDeviceToHost, stream);
         cudaStreamSynchronize(stream);

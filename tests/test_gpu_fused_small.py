@@ -8,7 +8,8 @@ z written by the kernel), one 32-K block per CTA, short drained TMEM units
 (the multi-unit path the full-size text matmul needs only past 4.9 M K), two
 converter groups instead of one, contiguous K ranges, bulk prefetches and
 MPC_FUSED_SMALL=0 (the planes-based path) — every variant must give the
-oracle's shares.
+oracle's shares.  Shapes with even K and N run the TMA-staged kernel, the others
+the register path.
 """
 import hashlib
 import os
@@ -52,8 +53,11 @@ def _oracle_z(M, K, N, gen, tid, truncate=True):
     return X, Y, (oracle.truncate(z, 16) if truncate else z)
 
 
-@pytest.mark.parametrize("M,K,N", [(32, 2048, 32),      # exactly 64 32-K blocks, full tile
-                                   (32, 70001, 32),     # ragged K tail, 148 CTAs
+@pytest.mark.parametrize("M,K,N", [(32, 2048, 32),      # exactly 64 32-K blocks, full tile (TMA-staged)
+                                   (32, 70001, 32),     # ragged K tail, 148 CTAs (odd K: register path)
+                                   (32, 70002, 32),     # the same on the TMA-staged kernel
+                                   (20, 9000, 30),      # ragged rows / columns / K tail, TMA-staged
+                                   (7, 4096, 2),        # TMA boxes mostly out of bounds (zero-filled)
                                    (17, 4099, 5),       # ragged rows / columns
                                    (1, 6000, 32),       # a single row
                                    (32, 5000, 1)])      # a single column
@@ -109,10 +113,12 @@ print(hashlib.sha256(z.view(torch.int64).cpu().numpy().tobytes()).hexdigest())
                                  {"MPC_FUSED_UNIT": "3"}, {"MPC_FUSED_UNIT": "7", "MPC_FUSED_CTAS": "5"},
                                  {"MPC_FUSED_GROUPS": "2"}, {"MPC_FUSED_GROUPS": "2", "MPC_FUSED_UNIT": "3"},
                                  {"MPC_FUSED_CYCLIC": "0", "MPC_FUSED_UNIT": "5"}, {"MPC_FUSED_PF": "2"},
-                                 {"MPC_FUSED_SMALL": "0"}],
+                                 {"MPC_FUSED_TMA": "0"}, {"MPC_FUSED_SMALL": "0"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
-def test_fused_small_launch_variants(mpc, env):
-    M, K, N = 29, 9000, 31                  # 282 32-K blocks, ragged everywhere
+@pytest.mark.parametrize("shape", [(29, 9000, 31), (30, 9002, 32)],
+                         ids=["register-path", "tma-staged"])
+def test_fused_small_launch_variants(mpc, env, shape):
+    M, K, N = shape                         # 282 32-K blocks, ragged (odd N: register path; even: TMA)
     _, _, ez = _oracle_z(M, K, N, synth.uniform_ring, 5, truncate=False)
     want = hashlib.sha256(np.ascontiguousarray(ez).view(np.int64).tobytes()).hexdigest()
     out = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, M=M, K=K, N=N)], capture_output=True,
