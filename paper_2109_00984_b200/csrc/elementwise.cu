@@ -562,6 +562,10 @@ cudaError_t launch_split_both(const LeftSplitArgs& l, const RightSplitArgs& r, c
     split2_config();
     const bool dl = l.M > 0 && l.K > 0, dr = r.N > 0 && r.K > 0;
     if (!dl && !dr) return cudaSuccess;
+    if (dl && dr && left2(l) && right2(r)) {
+        const cudaError_t e = launch_split2_tma(l, r, st);
+        if (e != cudaErrorNotSupported) return e;
+    }
     if (!dr) return launch_split_left(l, st);
     if (!dl) return launch_split_right(r, st);
     const int64_t bl = l.batch > 1 ? l.batch : 1, br = r.batch > 1 ? r.batch : 1;
