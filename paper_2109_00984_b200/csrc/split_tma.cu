@@ -6,15 +6,16 @@
 // and for the y side (R7/R8)
 //     delta = sum_p (y_p - b_p) -> delta planes,  b'_0 = b_0 + delta,  b'_1 = b_1 -> planes,
 // in the ring GEMM's operand layout (common.cuh: Layout::Left for the x side, 128-row
-// blocks; Layout::Right for the y side, 64-row blocks).  A CTA (one per SM) walks tiles
-// of 64 rows (x) / 64 columns (y) x one 32-K block: a loader thread brings the tile of
+// blocks; Layout::Right for the y side, 64-row blocks; exchanged for the transposed
+// GEMM).  A CTA (one per SM) walks tiles of 64 rows (x) / 64 columns (y) x one 32-K
+// block: a loader thread brings the tile of
 // all four share inputs into a raw stage with 3-D tensor maps (x / a: two 16-K boxes of
 // 64 rows with 128-byte swizzle, y / b: a 64 x 32 box; K past the end, rows past M and
 // columns past N are zero-filled — the planes' K padding must be 0), the 256 converter
 // threads (one per (row or column, 8-K quarter)) read their 8 values per input from
 // shared memory, form the sums and write the limb planes into a staging stage already
 // in the global layout, and a storer thread writes them back with bulk copies (per set:
-// 8 x 2 KiB pieces for x-side tiles, one 16 KiB run for y-side tiles).  Two raw and two
+// 8 x 2 KiB pieces into 128-row blocks, one 16 KiB run into a 64-row block).  Two raw and two
 // staging stages keep the load of tile t + 1 and the stores of tile t - 1 in flight while
 // tile t converts.  The split kernels it replaces keep one tile's loads in flight per
 // thread and run at ~0.8 of the HBM copy rate on large weight splits (ncu, ViT fc1:
@@ -45,7 +46,10 @@ struct Params {
     int64_t M, K, N;
     int KB, lt, rt;                               // 32-K blocks; x-side tiles (64 rows x block), y-side tiles
     int sum_first;                                // b'_0 = b_0 + delta (1 in the Beaver matmul)
+    int xl, yl;                                   // plane layout of each side: 0 Layout::Left (128-row blocks),
+                                                  // 1 Layout::Right (64-row blocks; swapped for the transposed GEMM)
 };
+
 
 __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, uint64_t* bar) {
     asm volatile(
@@ -74,6 +78,19 @@ __device__ __forceinline__ void st_planes8(uint8_t* set, uint32_t off, const uin
     }
 #pragma unroll
     for (int l = 0; l < 8; ++l) *reinterpret_cast<uint2*>(set + off + l * 2048) = make_uint2(w[l][0], w[l][1]);
+}
+
+// Bulk stores of one 64-row tile's 8 planes (staging: plane l at l x 2 KiB) into a plane buffer:
+// Layout::Right (64-row blocks) takes them as one 16 KiB run, Layout::Left (128-row blocks) as
+// 8 pieces of 2 KiB at the row half of each 4 KiB plane
+__device__ __forceinline__ void store_set(uint8_t* planes, int layout, int r0, int kb, int KB, uint32_t src) {
+    if (layout) {
+        bulk_s2g(planes + ((int64_t)(r0 / 64) * KB + kb) * 8 * 2048, src, 16384);
+    } else {
+        uint8_t* blk = planes + ((int64_t)(r0 / 128) * KB + kb) * 8 * 4096 + (r0 % 128) / 64 * 2048;
+#pragma unroll
+        for (int l = 0; l < 8; ++l) bulk_s2g(blk + l * 4096, src + l * 2048, 2048);
+    }
 }
 
 __global__ void __launch_bounds__(kThreads, 1) split2_tma_kernel(const __grid_constant__ Params p) {
@@ -133,22 +150,15 @@ __global__ void __launch_bounds__(kThreads, 1) split2_tma_kernel(const __grid_co
                 mbar_wait(&sfull[s], ph);
                 const uint32_t src = smem_u32(stg + s * kStage);
                 if (t < p.lt) {
-                    // x side: each set's 8 planes of rows r0 .. r0 + 63: 2 KiB at the row half of the
-                    // 128-row block's 4 KiB plane
                     const int kb = t % p.KB, r0 = (t / p.KB) * 64;
-                    const int64_t blk = ((int64_t)(r0 / 128) * p.KB + kb) * 8 * 4096 + (r0 % 128) / 64 * 2048;
-                    uint8_t* dsts[3] = {p.eps_pl + blk, p.a_pl + blk, p.a_pl + p.a_stride + blk};
-#pragma unroll
-                    for (int set = 0; set < 3; ++set)
-#pragma unroll
-                        for (int l = 0; l < 8; ++l) bulk_s2g(dsts[set] + l * 4096, src + set * 16384 + l * 2048, 2048);
+                    store_set(p.eps_pl, p.xl, r0, kb, p.KB, src);
+                    store_set(p.a_pl, p.xl, r0, kb, p.KB, src + 16384);
+                    store_set(p.a_pl + p.a_stride, p.xl, r0, kb, p.KB, src + 32768);
                 } else {
-                    // y side: a 64-row block's 8 planes are one contiguous 16 KiB run
                     const int tt = t - p.lt, kb = tt % p.KB, n0 = (tt / p.KB) * 64;
-                    const int64_t blk = ((int64_t)(n0 / 64) * p.KB + kb) * 8 * 2048;
-                    bulk_s2g(p.delta_pl + blk, src, 16384);
-                    bulk_s2g(p.b_pl + blk, src + 16384, 16384);
-                    bulk_s2g(p.b_pl + p.b_stride + blk, src + 32768, 16384);
+                    store_set(p.delta_pl, p.yl, n0, kb, p.KB, src);
+                    store_set(p.b_pl, p.yl, n0, kb, p.KB, src + 16384);
+                    store_set(p.b_pl + p.b_stride, p.yl, n0, kb, p.KB, src + 32768);
                 }
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging readable again
@@ -233,10 +243,10 @@ cudaError_t launch_split2_tma(const LeftSplitArgs& l, const RightSplitArgs& r, c
     static const bool off = getenv("MPC_SPLIT_TMA") && atoi(getenv("MPC_SPLIT_TMA")) == 0;   // A/B switch
     const PFN_cuTensorMapEncodeTiled_v12000 enc = split_tma_encoder();
     if (off || !enc) return cudaErrorNotSupported;
-    // exactly the Beaver matmul's all-parties split, normal orientation, one matrix
+    // exactly the Beaver matmul's all-parties split, either orientation of the 2-CTA GEMM, one matrix
     if (l.Psum != 2 || l.Pcopy != 2 || l.cp_src != l.minus || !l.minus || !l.sum_planes || !l.cp_planes ||
-        l.add_sum_first || l.swap != 0 || l.batch > 1 || r.Psum != 2 || r.Pcopy != 2 || r.cp_src != r.minus ||
-        !r.minus || !r.sum_planes || !r.cp_planes || r.swap != 0 || r.batch > 1 || l.K != r.K)
+        l.add_sum_first || l.swap > 1 || l.batch > 1 || r.Psum != 2 || r.Pcopy != 2 || r.cp_src != r.minus ||
+        !r.minus || !r.sum_planes || !r.cp_planes || r.swap != l.swap || r.batch > 1 || l.K != r.K)
         return cudaErrorNotSupported;
     const int64_t M = l.M, K = l.K, N = r.N;
     if (M < 1 || N < 1 || K < 32 || (K & 1) || (N & 1) || l.party_stride != M * K || r.party_stride != K * N)
@@ -270,6 +280,8 @@ cudaError_t launch_split2_tma(const LeftSplitArgs& l, const RightSplitArgs& r, c
     p.lt = (int)((M + 63) / 64) * p.KB;
     p.rt = (int)((N + 63) / 64) * p.KB;
     p.sum_first = r.add_delta_first;
+    p.xl = l.swap ? 1 : 0;                                    // transposed GEMM: x side right-operand planes
+    p.yl = r.swap ? 0 : 1;
     static int attr_dev = -1;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
