@@ -425,6 +425,10 @@ __global__ void __launch_bounds__(256) split_left_kernel(LeftSplitArgs a) {
 }
 cudaError_t launch_split_left(const LeftSplitArgs& a, cudaStream_t st) {
     split2_config();
+    if (a.M > 0 && a.K > 0 && left2(a)) {
+        const cudaError_t e = launch_split2_tma(&a, nullptr, st);
+        if (e != cudaErrorNotSupported) return e;
+    }
     if (a.M == 0 || a.K == 0) return cudaSuccess;
     const int64_t warps = ((a.M + 7) / 8) * ((num_kb(a.K) * kKBlock + 63) / 64) * (a.batch > 1 ? a.batch : 1) *
                           (left2(a) ? 2 : 1);
@@ -563,7 +567,7 @@ cudaError_t launch_split_both(const LeftSplitArgs& l, const RightSplitArgs& r, c
     const bool dl = l.M > 0 && l.K > 0, dr = r.N > 0 && r.K > 0;
     if (!dl && !dr) return cudaSuccess;
     if (dl && dr && left2(l) && right2(r)) {
-        const cudaError_t e = launch_split2_tma(l, r, st);
+        const cudaError_t e = launch_split2_tma(&l, &r, st);
         if (e != cudaErrorNotSupported) return e;
     }
     if (!dr) return launch_split_left(l, st);

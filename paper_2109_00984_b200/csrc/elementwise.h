@@ -68,9 +68,9 @@ cudaError_t launch_mask(const uint64_t* x, const uint64_t* a, int64_t n1, const 
 cudaError_t launch_split_left(const LeftSplitArgs& a, cudaStream_t st);
 cudaError_t launch_split_right(const RightSplitArgs& a, cudaStream_t st);
 cudaError_t launch_split_both(const LeftSplitArgs& l, const RightSplitArgs& r, cudaStream_t st);
-// the two-party Beaver split streamed through shared memory by TMA (split_tma.cu);
-// cudaErrorNotSupported when the shapes / buffers do not fit it
-cudaError_t launch_split2_tma(const LeftSplitArgs& l, const RightSplitArgs& r, cudaStream_t st);
+// the two-party Beaver split streamed through shared memory by TMA (split_tma.cu), either side
+// optional; cudaErrorNotSupported when the shapes / buffers do not fit it
+cudaError_t launch_split2_tma(const LeftSplitArgs* l, const RightSplitArgs* r, cudaStream_t st);
 cudaError_t launch_ttp_left(const TtpGenArgs& g, cudaStream_t st);
 cudaError_t launch_ttp_right(const TtpGenArgs& g, cudaStream_t st);
 cudaError_t launch_ttp_c(uint64_t key, uint64_t id, int P, int out_lo, int out_hi, uint64_t* out, uint64_t* c0,

@@ -236,23 +236,31 @@ static PFN_cuTensorMapEncodeTiled_v12000 split_tma_encoder() {
     return fn;
 }
 
-// The two-party Beaver split (left: x, a -> eps, a_p planes in Layout::Left; right: y, b ->
-// delta, b'_p planes in Layout::Right) through split2_tma_kernel; cudaErrorNotSupported when
-// the shapes or buffers do not fit it (the caller then uses the register split).
-cudaError_t launch_split2_tma(const LeftSplitArgs& l, const RightSplitArgs& r, cudaStream_t st) {
+// The two-party Beaver split (left: x, a -> eps, a_p planes; right: y, b -> delta, b'_p planes;
+// either side may be absent, e.g. the x side of mpc_beaver_matmul_prepared) through
+// split2_tma_kernel; cudaErrorNotSupported when the shapes or buffers do not fit it (the
+// caller then uses the register split).
+cudaError_t launch_split2_tma(const LeftSplitArgs* lp, const RightSplitArgs* rp, cudaStream_t st) {
     static const bool off = getenv("MPC_SPLIT_TMA") && atoi(getenv("MPC_SPLIT_TMA")) == 0;   // A/B switch
     const PFN_cuTensorMapEncodeTiled_v12000 enc = split_tma_encoder();
-    if (off || !enc) return cudaErrorNotSupported;
+    if (off || !enc || (!lp && !rp)) return cudaErrorNotSupported;
     // exactly the Beaver matmul's all-parties split, either orientation of the 2-CTA GEMM, one matrix
-    if (l.Psum != 2 || l.Pcopy != 2 || l.cp_src != l.minus || !l.minus || !l.sum_planes || !l.cp_planes ||
-        l.add_sum_first || l.swap > 1 || l.batch > 1 || r.Psum != 2 || r.Pcopy != 2 || r.cp_src != r.minus ||
-        !r.minus || !r.sum_planes || !r.cp_planes || r.swap != l.swap || r.batch > 1 || l.K != r.K)
-        return cudaErrorNotSupported;
-    const int64_t M = l.M, K = l.K, N = r.N;
-    if (M < 1 || N < 1 || K < 32 || (K & 1) || (N & 1) || l.party_stride != M * K || r.party_stride != K * N)
-        return cudaErrorNotSupported;
-    for (const void* ptr : {(const void*)l.plus, (const void*)l.minus, (const void*)r.plus, (const void*)r.minus})
-        if (reinterpret_cast<uintptr_t>(ptr) & 15) return cudaErrorNotSupported;
+    if (lp) {
+        const LeftSplitArgs& l = *lp;
+        if (l.Psum != 2 || l.Pcopy != 2 || l.cp_src != l.minus || !l.minus || !l.sum_planes || !l.cp_planes ||
+            l.add_sum_first || l.swap > 1 || l.batch > 1 || l.M < 1 || l.K < 32 || (l.K & 1) ||
+            l.party_stride != l.M * l.K || ((reinterpret_cast<uintptr_t>(l.plus) | reinterpret_cast<uintptr_t>(l.minus)) & 15))
+            return cudaErrorNotSupported;
+    }
+    if (rp) {
+        const RightSplitArgs& r = *rp;
+        if (r.Psum != 2 || r.Pcopy != 2 || r.cp_src != r.minus || !r.minus || !r.sum_planes || !r.cp_planes ||
+            r.swap > 1 || r.batch > 1 || r.N < 1 || r.K < 32 || (r.N & 1) || r.party_stride != r.K * r.N ||
+            ((reinterpret_cast<uintptr_t>(r.plus) | reinterpret_cast<uintptr_t>(r.minus)) & 15))
+            return cudaErrorNotSupported;
+    }
+    if (lp && rp && (lp->K != rp->K || lp->swap != rp->swap)) return cudaErrorNotSupported;
+    const int64_t K = lp ? lp->K : rp->K, M = lp ? lp->M : 0, N = rp ? rp->N : 0;
     split_tma::Params p{};
     const cuuint32_t es[3] = {1, 1, 1};
     auto left = [&](CUtensorMap* m, const uint64_t* base) {
@@ -271,17 +279,18 @@ cudaError_t launch_split2_tma(const LeftSplitArgs& l, const RightSplitArgs& r, c
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     };
-    if (!left(&p.tm_x, l.plus) || !left(&p.tm_a, l.minus) || !right(&p.tm_y, r.plus) || !right(&p.tm_b, r.minus))
-        return cudaErrorNotSupported;
-    p.eps_pl = l.sum_planes; p.a_pl = l.cp_planes; p.a_stride = l.cp_planes_stride;
-    p.delta_pl = r.sum_planes; p.b_pl = r.cp_planes; p.b_stride = r.cp_planes_stride;
+    if (lp && (!left(&p.tm_x, lp->plus) || !left(&p.tm_a, lp->minus))) return cudaErrorNotSupported;
+    if (rp && (!right(&p.tm_y, rp->plus) || !right(&p.tm_b, rp->minus))) return cudaErrorNotSupported;
+    if (lp) { p.eps_pl = lp->sum_planes; p.a_pl = lp->cp_planes; p.a_stride = lp->cp_planes_stride; }
+    if (rp) { p.delta_pl = rp->sum_planes; p.b_pl = rp->cp_planes; p.b_stride = rp->cp_planes_stride; }
     p.M = M; p.K = K; p.N = N;
     p.KB = (int)num_kb(K);
-    p.lt = (int)((M + 63) / 64) * p.KB;
-    p.rt = (int)((N + 63) / 64) * p.KB;
-    p.sum_first = r.add_delta_first;
-    p.xl = l.swap ? 1 : 0;                                    // transposed GEMM: x side right-operand planes
-    p.yl = r.swap ? 0 : 1;
+    p.lt = lp ? (int)((M + 63) / 64) * p.KB : 0;
+    p.rt = rp ? (int)((N + 63) / 64) * p.KB : 0;
+    p.sum_first = rp ? rp->add_delta_first : 0;
+    const int swap = lp ? lp->swap : rp->swap;
+    p.xl = swap ? 1 : 0;                                      // transposed GEMM: x side right-operand planes
+    p.yl = swap ? 0 : 1;
     static int attr_dev = -1;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
