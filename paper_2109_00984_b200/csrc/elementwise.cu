@@ -987,14 +987,43 @@ __device__ __forceinline__ void acc_carry(uint64_t& s, uint64_t v, uint32_t& cnt
 }
 __device__ __forceinline__ uint32_t msb(uint64_t v) { return (uint32_t)(v >> 63); }
 
-template <int P, bool PAIRS>
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                 :: "r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// PF (prefetch; n even, 16-byte aligned shares): the x pairs of a thread's NEXT grid-stride
+// iteration are copied into shared memory (cp.async, 16 bytes per party) while it expands
+// the Philox blocks of the current one, so every warp keeps P loads in flight through its
+// ALU phase instead of alternating load -> compute -> store (dynamic shared memory:
+// 2 buffers x P x blockDim pairs; each thread reads only the slots it filled).
+template <int P, bool PAIRS, bool PF>
 __global__ void __launch_bounds__(256, (P <= 8 ? 2 : 1)) trunc_alg1_all_w32_kernel(
         uint64_t* __restrict__ x, int64_t n, int bits, const PhiloxRK rk, uint64_t id, const uint64_t* __restrict__ rin,
         const uint64_t* __restrict__ thin) {
+    extern __shared__ ulonglong2 pf_buf[];
     const int64_t npairs = (n + 1) / 2;
     const bool vec = (n & 1) == 0 && aligned16(x) && (!PAIRS || (aligned16(rin) && aligned16(thin)));
     const uint32_t hshift = 32 - bits;                                  // theta_x lands in the high word
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npairs; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    auto prefetch = [&](int64_t jj, int buf) {
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+            cp_async16(&pf_buf[(buf * P + q) * blockDim.x + threadIdx.x], x + (int64_t)q * n + 2 * jj);
+    };
+    if (PF) {
+        if (j < npairs) prefetch(j, 0);
+        cp_async_commit();
+    }
+    for (int it = 0; j < npairs; j += stride, ++it) {
+        if (PF) {
+            if (j + stride < npairs) prefetch(j + stride, (it + 1) & 1);
+            cp_async_commit();
+            cp_async_wait1();                                            // this iteration's group has landed
+        }
         const int64_t i0 = 2 * j;
         const bool has1 = i0 + 1 < n;
         uint32_t beta[P][2];
@@ -1006,7 +1035,14 @@ __global__ void __launch_bounds__(256, (P <= 8 ? 2 : 1)) trunc_alg1_all_w32_kern
         // dominated when each load was consumed right after its own block)
         uint64_t rv[PAIRS ? P : 1][2];                                  // the wrap pair's r_q (PAIRS)
 #pragma unroll
-        for (int q = 0; q < P; ++q) ld_pair(x + (int64_t)q * n, i0, vec, has1, xv[q]);
+        for (int q = 0; q < P; ++q) {
+            if (PF) {
+                const ulonglong2 t = pf_buf[((it & 1) * P + q) * blockDim.x + threadIdx.x];
+                xv[q][0] = t.x; xv[q][1] = t.y;
+            } else {
+                ld_pair(x + (int64_t)q * n, i0, vec, has1, xv[q]);
+            }
+        }
         if (PAIRS) {
 #pragma unroll
             for (int q = 0; q < P; ++q) ld_pair(rin + (int64_t)q * n, i0, vec, has1, rv[PAIRS ? q : 0]);
@@ -1062,6 +1098,31 @@ __global__ void __launch_bounds__(256, (P <= 8 ? 2 : 1)) trunc_alg1_all_w32_kern
     }
 }
 
+template <int Q, bool PAIRS>
+static cudaError_t launch_alg1_w32(uint64_t* x, int64_t n, int bits, const PhiloxRK& rk, uint64_t id,
+                                   const uint64_t* r, const uint64_t* th, unsigned g, cudaStream_t st) {
+    // prefetching variant when every pair is one aligned 16-byte load (MPC_ALG1_PREFETCH=0: A/B)
+    static const bool pf_env = !getenv("MPC_ALG1_PREFETCH") || atoi(getenv("MPC_ALG1_PREFETCH")) != 0;
+    auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    const bool pf = pf_env && (n & 1) == 0 && al(x) && (!PAIRS || (al(r) && al(th)));
+    if (!pf) {
+        trunc_alg1_all_w32_kernel<Q, PAIRS, false><<<g, 256, 0, st>>>(x, n, bits, rk, id, r, th);
+        return cudaGetLastError();
+    }
+    const int smem = 2 * Q * 256 * (int)sizeof(ulonglong2);
+    static int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
+        const cudaError_t e = cudaFuncSetAttribute(trunc_alg1_all_w32_kernel<Q, PAIRS, true>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr_dev = dev;
+    }
+    trunc_alg1_all_w32_kernel<Q, PAIRS, true><<<g, 256, smem, st>>>(x, n, bits, rk, id, r, th);
+    return cudaGetLastError();
+}
+
 template <bool PAIRS>
 static cudaError_t launch_alg1_all_t(uint64_t* x, int P, int64_t n, int bits, uint64_t key, uint64_t id,
                                      const uint64_t* r, const uint64_t* th, cudaStream_t st) {
@@ -1070,8 +1131,8 @@ static cudaError_t launch_alg1_all_t(uint64_t* x, int P, int64_t n, int bits, ui
     const bool w32 = bits <= 32 && !getenv("MPC_ALG1_INT128");        // A/B switch for measurements
     switch (P) {
 #define MPC_ALG1_CASE(Q) case Q:                                                                         \
-        if (w32) trunc_alg1_all_w32_kernel<Q, PAIRS><<<g, 256, 0, st>>>(x, n, bits, rk, id, r, th);        \
-        else trunc_alg1_all_kernel<Q, PAIRS><<<g, 256, 0, st>>>(x, n, bits, rk, id, r, th);                \
+        if (w32) return launch_alg1_w32<Q, PAIRS>(x, n, bits, rk, id, r, th, g, st);                      \
+        trunc_alg1_all_kernel<Q, PAIRS><<<g, 256, 0, st>>>(x, n, bits, rk, id, r, th);                     \
         break;
         MPC_ALG1_CASE(3) MPC_ALG1_CASE(4) MPC_ALG1_CASE(5) MPC_ALG1_CASE(6) MPC_ALG1_CASE(7) MPC_ALG1_CASE(8)
         MPC_ALG1_CASE(9) MPC_ALG1_CASE(10) MPC_ALG1_CASE(11) MPC_ALG1_CASE(12) MPC_ALG1_CASE(13) MPC_ALG1_CASE(14)
