@@ -7,7 +7,8 @@ few times, for ncu captures (all parties on one GPU):
       python scripts/profile_elementwise.py share 2
 
 alg1 P: Alg. 1 truncation of P parties x 8192^2 shares (wrap pair from its id,
-then from memory); share P: P-party sharing of 4096^2 elements."""
+then from memory); share P: P-party sharing of 4096^2 elements; relu P: the fused
+all-parties ReLU of 2^24 elements (NEXT-3, Philox-bound)."""
 import os
 import sys
 
@@ -46,3 +47,13 @@ elif what == "share":
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     print(f"share P={P}: {ms:.4f} ms, {(8 * n * (P + 1)) / ms / 1e6:.0f} GB/s")
+elif what == "relu":
+    n = 1 << 24
+    x = torch.randint(-(1 << 40), 1 << 40, (P, n), dtype=torch.int64, device="cuda").view(torch.uint64)
+    z = torch.empty_like(x)
+    for i in range(reps + 1):
+        if i == 1:
+            torch.cuda.synchronize(); e0.record()
+        ctx.relu(x, relu_id=9, out=z)
+    e1.record(); torch.cuda.synchronize()
+    print(f"relu P={P}: {e0.elapsed_time(e1) / reps:.4f} ms per call")
