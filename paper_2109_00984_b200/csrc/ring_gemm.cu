@@ -185,7 +185,7 @@ __device__ __forceinline__ void issue_kblock(uint64_t da, uint64_t db, uint32_t 
 // FAULT: the fault-injection instantiation (MPC_GEMM_FAULT_INJECT, watchdog test).  A
 // compile-time switch: a runtime check in the producer's copy loop cost the
 // 8192^3 GEMMs 8-10% (measured: 108 vs 117-121 ms for 4-party 8192^3).
-template <bool FAULT, bool TMA>
+template <bool FAULT, bool TMA, bool SERP>
 __device__ __forceinline__ void control_roles(const RingGemmParams& p, const WorkMap& wm, int warp, int lane,
                                               uint32_t rank, uint32_t tmem_base, const Bars& B) {
     const bool leader = rank == 0;
@@ -197,6 +197,7 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
         asm volatile("griddepcontrol.wait;" ::: "memory");
         int s = 0; uint32_t ph = 0;
         long long st_empty = 0;
+        int item_no = 0;                                 // this cluster's items so far (K-serpentine parity)
         const uint64_t l2pol = l2_policy(p.tma_l2);
         for (int w = cluster_id(); w < wm.items(); w += nclusters()) {
             int party, m, n, klo, khi;
@@ -216,7 +217,9 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
                                 (int64_t)kb0 * (8 * GL::kBlock);
             const uint8_t* b1 = S1.B + party * S1.party_stride_B + bi * S1.batch_stride_B + rbB * S1.kb * (8 * GR::kBlock) -
                                 (int64_t)kb0 * (8 * GR::kBlock);
-            for (int k0 = klo; k0 < khi; k0 += kc) {
+            const bool rev = SERP && (item_no++ & 1);
+            const int kstep = rev ? -kc : kc;
+            for (int k0 = rev ? klo + (khi - klo - 1) / kc * kc : klo; rev ? k0 >= klo : k0 < khi; k0 += kstep) {
                 const int k1 = min(khi, k0 + kc);
                 for (int g = 0; g < kPasses; ++g) {
                     const uint32_t bytesA = (uint32_t)pass_planes(g) * GL::kBlock;
@@ -285,12 +288,15 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
     } else if (warp == 1) {
         // ------------------------------------------------ leader: MMA issuer (one elected lane)
         int s = 0; uint32_t ph = 0; uint32_t u = 0;
+        int item_no = 0;
         long long st_tempty = 0, st_full = 0;
         const long long t_start = clock64();
         for (int w = cluster_id(); w < wm.items(); w += nclusters()) {
             int party, m, n, klo, khi;
             wm.decode(w, party, m, n, klo, khi);
-            for (int k0 = klo; k0 < khi; k0 += kc) {
+            const bool rev = SERP && (item_no++ & 1);
+            const int kstep = rev ? -kc : kc;
+            for (int k0 = rev ? klo + (khi - klo - 1) / kc * kc : klo; rev ? k0 >= klo : k0 < khi; k0 += kstep) {
                 const int k1 = min(khi, k0 + kc);
                 for (int g = 0; g < kPasses; ++g, ++u) {
                     for (int kt = k0; kt < k1; ++kt) {
@@ -467,7 +473,7 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Wor
     }
 }
 
-template <bool FAULT, bool TMA>
+template <bool FAULT, bool TMA, bool SERP = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -515,7 +521,7 @@ ring_gemm_kernel(const __grid_constant__ RingGemmParams p, int parties) {
     // register budget: the control warpgroup needs few, the epilogue holds 64 u64 sums per thread
     if (warp < 4) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
-        control_roles<FAULT, TMA>(p, wm, warp, lane, rank, tmem_base, B);
+        control_roles<FAULT, TMA, SERP>(p, wm, warp, lane, rank, tmem_base, B);
         if (p.dbg && warp == 1 && lane == 0 && rank == 0) atomicMax(&p.dbg[6], globaltimer());
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
@@ -631,7 +637,7 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     if (attr_dev != dev) {
         cudaError_t e = cudaSuccess;
         for (auto k : {gemm::ring_gemm_kernel<false, true>, gemm::ring_gemm_kernel<false, false>,
-                       gemm::ring_gemm_kernel<true, false>})
+                       gemm::ring_gemm_kernel<false, false, true>, gemm::ring_gemm_kernel<true, false>})
             if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr_dev = dev;
@@ -694,11 +700,17 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
             q.party_major = 1;
             if (prm.group_m <= 0 && env_group <= 0) q.group_m = 8;
         }
+        // ... and walk K in alternate directions on consecutive waves: a wave ends with the last
+        // K units of its row strips in L2, and the next wave (same 8 row tiles, the next column
+        // tiles) starts there (MPC_GEMM_SERPENTINE=0 / 1 forces either)
+        static const int env_serp = getenv("MPC_GEMM_SERPENTINE") ? atoi(getenv("MPC_GEMM_SERPENTINE")) : -1;
+        q.serpentine = env_serp >= 0 ? (env_serp != 0) : (plane_bytes > (2ull << 30) ? 1 : 0);
         const bool tma = want_tma && !q.fault_inject && fill_tma(q, parties);
         static const int env_l2 = getenv("MPC_GEMM_TMA_L2") ? atoi(getenv("MPC_GEMM_TMA_L2")) : 3;
         q.tma_l2 = env_l2;
         auto kern = q.fault_inject ? gemm::ring_gemm_kernel<true, false>
                   : tma            ? gemm::ring_gemm_kernel<false, true>
+                  : q.serpentine   ? gemm::ring_gemm_kernel<false, false, true>
                                    : gemm::ring_gemm_kernel<false, false>;
         cudaError_t e = launch_pdl(kern, dim3((unsigned)(clusters * 2)), dim3(gemm::kThreads), smem, stream, q, parties);
         if (e != cudaSuccess || q.splits <= 1) return e;

@@ -50,6 +50,7 @@ struct RingGemmParams {
                                         // convolution whose im2col rows are (b, pixel s).  C likewise.
     int small;                          // 1: stacked-plane kernel (M <= 32, planes in Layout::Small)
     int group_m;                        // row tiles per scheduling group of the 2-CTA kernel (0: default 4)
+    int serpentine;                     // set by the launcher: alternate K direction per wave (MPC_GEMM_SERPENTINE)
     int party_major;                    // set by the launcher: tile order instance-major (MPC_GEMM_PARTY_MAJOR)
     int batch;                          // independent GEMMs of the same shape (0/1 = one); instance
                                         // (b, p) reads planes at b * batch_stride_A/B + p * party_stride_A/B

@@ -6,7 +6,7 @@ Each configuration runs in its own process because the GEMM's tuning knobs
 (K-chunk length MPC_GEMM_KC, split-K factor MPC_GEMM_SPLITS, programmatic
 dependent launch MPC_NO_PDL, transposed GEMM for small M MPC_NO_SWAP, the
 2-CTA GEMM's operand producer MPC_GEMM_TMA, its tile order MPC_GEMM_PARTY_MAJOR /
-MPC_GEMM_GROUPM) are
+MPC_GEMM_GROUPM / MPC_GEMM_SERPENTINE) are
 read once per process.  Every run must
 produce the oracle's shares bit for bit.
 """
@@ -75,12 +75,15 @@ def case(request):
     {"MPC_GEMM_TMA": "1", "MPC_GEMM_TMA_L2": "1"},
     {"MPC_GEMM_PARTY_MAJOR": "1"},          # instance-major tile order (the > 2 GiB default)
     {"MPC_GEMM_PARTY_MAJOR": "1", "MPC_GEMM_GROUPM": "3"},
+    # K-serpentine (the > 2 GiB default): odd items of a cluster walk their units backwards
+    {"MPC_GEMM_SERPENTINE": "1", "MPC_GEMM_TMA": "0"},
+    {"MPC_GEMM_SERPENTINE": "1", "MPC_GEMM_TMA": "0", "MPC_GEMM_SPLITS": "7", "MPC_GEMM_KC": "5"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 def test_same_shares_under_every_launch_config(case, env):
     (M, K, N), expected = case
     full = dict(os.environ)
     for k in ("MPC_GEMM_KC", "MPC_GEMM_SPLITS", "MPC_NO_PDL", "MPC_NO_SWAP", "MPC_GEMM_DEBUG", "MPC_GEMM_SMALL",
-              "MPC_GEMM_TMA", "MPC_GEMM_TMA_L2", "MPC_GEMM_PARTY_MAJOR", "MPC_GEMM_GROUPM"):
+              "MPC_GEMM_TMA", "MPC_GEMM_TMA_L2", "MPC_GEMM_PARTY_MAJOR", "MPC_GEMM_GROUPM", "MPC_GEMM_SERPENTINE"):
         full.pop(k, None)
     full.update(env)
     out = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, M=M, K=K, N=N, P=P)], env=full,
