@@ -15,7 +15,10 @@
  *           aligned; ring elements are little-endian uint64.  The library never
  *           allocates or frees caller memory.  Work buffers are passed in as
  *           `workspace` (size from mpc_workspace_bytes / mpc_ttp_workspace_bytes,
- *           256-byte aligned).
+ *           256-byte aligned).  workspace == NULL with workspace_bytes == 0 asks
+ *           mpc_ttp_triples, mpc_beaver_matmul(_batched), mpc_beaver_finish and
+ *           mpc_ring_matmul to use a workspace the context allocates, grows and
+ *           frees in mpc_destroy (stream-ordered; the one library-owned buffer).
  * Parties.  A context is either
  *             - one party of P (rank in [0, P)): one process and one GPU per
  *               party, reveals are NCCL sum-allreduces (P:64, P:72 footnote,

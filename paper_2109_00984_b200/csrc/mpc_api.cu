@@ -60,6 +60,10 @@ struct mpc_ctx_s {
     size_t scratch_bytes = 0;
     cudaStream_t scratch_stream = nullptr;  // last stream that used the scratch
     cudaEvent_t scratch_ev = nullptr;
+    void* ows = nullptr;                    // the context's own workspace (entry points called with
+    size_t ows_bytes = 0;                   // workspace NULL and workspace_bytes 0)
+    cudaStream_t ows_stream = nullptr;
+    cudaEvent_t ows_ev = nullptr;
 };
 
 namespace {
@@ -492,6 +496,29 @@ mpc_status ensure_scratch(mpc_ctx c, size_t bytes) {
     return MPC_OK;
 }
 
+// An entry point called with workspace == NULL and workspace_bytes == 0 uses the
+// context's own workspace, grown to `need` bytes and kept (stream-ordered like the
+// scratch: a call on another stream first waits for the previous user's work).
+mpc_status own_workspace(mpc_ctx c, size_t need, void*& ws, size_t& ws_bytes) {
+    if (ws || ws_bytes || need == 0) return MPC_OK;
+    if (c->ows_stream != c->stream && c->ows) {
+        if (!c->ows_ev && cudaEventCreateWithFlags(&c->ows_ev, cudaEventDisableTiming) != cudaSuccess)
+            return fail(c, MPC_ERR_CUDA, "workspace event");
+        cudaEventRecord(c->ows_ev, c->ows_stream);
+        cudaStreamWaitEvent(c->stream, c->ows_ev, 0);
+    }
+    c->ows_stream = c->stream;
+    if (c->ows_bytes < need) {
+        if (c->ows) { cudaStreamSynchronize(c->stream); cudaFree(c->ows); c->ows = nullptr; c->ows_bytes = 0; }
+        const cudaError_t e = cudaMalloc(&c->ows, need);
+        if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "workspace alloc (%zu B): %s", need, cudaGetErrorString(e));
+        c->ows_bytes = need;
+    }
+    ws = c->ows;
+    ws_bytes = c->ows_bytes;
+    return MPC_OK;
+}
+
 // Truncation of x ([P][n] or n) by `bits` with the wrap pair `wrap_id` (seeded
 // TTP: regenerated from k_ttp) or, when r / th are given, the wrap pair in memory
 // (materialised offline by mpc_ttp_wrap_pairs; Alg. 1 takes [r], [theta_r] as
@@ -687,6 +714,8 @@ mpc_status mpc_destroy(mpc_ctx c) {
     if (c->d_err) cudaFree(c->d_err);
     if (c->scratch) cudaFree(c->scratch);
     if (c->scratch_ev) cudaEventDestroy(c->scratch_ev);
+    if (c->ows) cudaFree(c->ows);
+    if (c->ows_ev) cudaEventDestroy(c->ows_ev);
     delete c;
     return MPC_OK;
 }
@@ -808,6 +837,7 @@ mpc_status mpc_ttp_triples(mpc_ctx c, uint64_t id, int64_t M, int64_t K, int64_t
     if (M < 0 || K < 0 || N < 0) return fail(c, MPC_ERR_SHAPE, "ttp_triples: negative size");
     if ((M * K && !a) || (K * N && !b) || (M * N && !cc)) return fail(c, MPC_ERR_ARG, "ttp_triples: null output");
     const bool ttp = c->all || c->rank == 0;       // holds the TTP view: needs a, b sums and c
+    if (ttp) CHECK(own_workspace(c, mpc_ttp_workspace_bytes(c, M, K, N), ws, ws_bytes));
     if (ttp && ws_bytes < mpc_ttp_workspace_bytes(c, M, K, N)) return fail(c, MPC_ERR_SHAPE, "ttp_triples: workspace too small");
     if (ttp && !ws && (M * K + K * N) > 0) return fail(c, MPC_ERR_ARG, "ttp_triples: null workspace");
     const int lo = c->all ? 0 : c->rank, hi = c->all ? c->P : c->rank + 1;
@@ -863,6 +893,7 @@ mpc_status mpc_beaver_matmul(mpc_ctx c, const uint64_t* x, const uint64_t* y, co
     CHECK(enter(c));
     if (M < 0 || K < 0 || N < 0) return fail(c, MPC_ERR_SHAPE, "beaver_matmul: negative size");
     if (K > (int64_t)1 << 30 || M > (int64_t)1 << 31 || N > (int64_t)1 << 31) return fail(c, MPC_ERR_SHAPE, "beaver_matmul: too large");
+    CHECK(own_workspace(c, carve_beaver(c, nullptr, M, K, N, -1, true, true, 1, true).total, ws, ws_bytes));
     const BeaverWs w = carve_beaver(c, ws, M, K, N, -1, true, true, 1, true);
     if (ws_bytes < w.total) return fail(c, MPC_ERR_SHAPE, "beaver_matmul: workspace %zu < %zu", ws_bytes, w.total);
     const int Pl = c->all ? c->P : 1;
@@ -909,6 +940,7 @@ mpc_status mpc_beaver_finish(mpc_ctx c, const uint64_t* ed, const uint64_t* a, c
     if (c->all) return fail(c, MPC_ERR_UNSUPPORTED, "beaver_finish: one-party contexts only");
     if (truncate && c->P > 2) return fail(c, MPC_ERR_UNSUPPORTED, "beaver_finish: P > 2 truncation needs mpc_truncate");
     if (M < 0 || K < 0 || N < 0) return fail(c, MPC_ERR_SHAPE, "beaver_finish: negative size");
+    CHECK(own_workspace(c, carve_beaver(c, nullptr, M, K, N).total, ws, ws_bytes));
     const BeaverWs w = carve_beaver(c, ws, M, K, N);
     if (ws_bytes < w.total) return fail(c, MPC_ERR_SHAPE, "beaver_finish: workspace %zu < %zu", ws_bytes, w.total);
     c->rounds += 1;                                   // the caller's reveal of eps || delta
@@ -928,6 +960,7 @@ mpc_status mpc_beaver_matmul_batched(mpc_ctx c, int64_t batch, const uint64_t* x
     if (batch > 65536 || K > (int64_t)1 << 30 || M > (int64_t)1 << 31 || N > (int64_t)1 << 31)
         return fail(c, MPC_ERR_SHAPE, "beaver_matmul_batched: too large");
     const int nb = (int)batch;                        // <= 65536 (checked above)
+    CHECK(own_workspace(c, carve_beaver(c, nullptr, M, K, N, -1, true, true, batch < 1 ? 1 : batch).total, ws, ws_bytes));
     const BeaverWs w = carve_beaver(c, ws, M, K, N, -1, true, true, batch < 1 ? 1 : batch);
     if (ws_bytes < w.total) return fail(c, MPC_ERR_SHAPE, "beaver_matmul_batched: workspace %zu < %zu", ws_bytes, w.total);
     const int Pl = c->all ? c->P : 1;
@@ -1128,6 +1161,7 @@ mpc_status mpc_ring_matmul(mpc_ctx c, const uint64_t* A, const uint64_t* B, uint
                            int64_t N, void* ws, size_t ws_bytes) {
     CHECK(enter(c));
     if (M < 0 || K < 0 || N < 0) return fail(c, MPC_ERR_SHAPE, "ring_matmul: negative size");
+    CHECK(own_workspace(c, mpc_ring_matmul_workspace_bytes(M, K, N), ws, ws_bytes));
     if (ws_bytes < mpc_ring_matmul_workspace_bytes(M, K, N)) return fail(c, MPC_ERR_SHAPE, "ring_matmul: workspace too small");
     if (M == 0 || N == 0) return MPC_OK;
     if (!C || (K && (!A || !B || !ws))) return fail(c, MPC_ERR_ARG, "ring_matmul: null pointer");

@@ -111,6 +111,10 @@ __global__ void __launch_bounds__(kThreads, 1) split2_tma_kernel(const __grid_co
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (warp == kConv / 32 && lane < 4) {     // the loader's tensor maps, fetched before the wait
+        const CUtensorMap* m = lane == 0 ? &p.tm_x : lane == 1 ? &p.tm_a : lane == 2 ? &p.tm_y : &p.tm_b;
+        asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(m)) : "memory");
+    }
     __syncthreads();
     // launched as a programmatic dependent: the inputs may come from, and the plane buffers
     // still be read by, the previous kernels

@@ -453,3 +453,36 @@ def test_beaver_matmul_batched_parity(mpc, P, B, M, K, N):
     ez = np.stack([oracle.beaver_matmul(xs[:, i], ys[:, i], a[:, i], b[:, i], cc[:, i]) for i in range(B)], axis=1)
     assert np.array_equal(oracle.reveal(ez), np.stack([X[i] @ Y[i] for i in range(B)]))   # Beaver identity
     assert np.array_equal(z, oracle.truncate(ez, 16, MASTER, wrap_id=17))
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_null_workspace_uses_context_buffer(mpc, P):
+    """The north-star calls through the raw C-ABI with workspace NULL and
+    workspace_bytes 0 (SURVEY §8(b)'s signatures): the context allocates its own
+    workspace, grows it for a larger shape, and the shares equal the oracle's."""
+    import ctypes
+    c = ctx(mpc, P)
+    lib, h = c._lib, c._h
+    p = lambda t: ctypes.c_void_p(t.data_ptr())                                 # noqa: E731
+    for (M, K, N), tid in (((64, 96, 40), 41), ((300, 100, 260), 42)):
+        X, Y, xs, ys, a, b, cc = _beaver_case(P, M, K, N, seed=5 + M, tid=tid)
+        ga = torch.empty((P, M, K), dtype=torch.uint64, device="cuda")
+        gb = torch.empty((P, K, N), dtype=torch.uint64, device="cuda")
+        gc = torch.empty((P, M, N), dtype=torch.uint64, device="cuda")
+        st = lib.mpc_ttp_triples(h, ctypes.c_uint64(tid), ctypes.c_int64(M), ctypes.c_int64(K), ctypes.c_int64(N),
+                                 p(ga), p(gb), p(gc), None, ctypes.c_size_t(0))
+        assert st == 0, lib.mpc_last_error(h)
+        z = torch.empty((P, M, N), dtype=torch.uint64, device="cuda")
+        gx, gy = dev(xs), dev(ys)                  # kept alive: the call only sees raw pointers
+        st = lib.mpc_beaver_matmul(h, p(gx), p(gy), p(ga), p(gb), p(gc), p(z), ctypes.c_int64(M),
+                                   ctypes.c_int64(K), ctypes.c_int64(N), 0, ctypes.c_uint64(0), None,
+                                   ctypes.c_size_t(0))
+        assert st == 0, lib.mpc_last_error(h)
+        torch.cuda.synchronize()
+        assert np.array_equal(host(gc), cc)
+        assert np.array_equal(host(z), oracle.beaver_matmul(xs, ys, a, b, cc))
+    # a non-NULL workspace that is too small is still an error
+    tiny = torch.empty(16, dtype=torch.uint8, device="cuda")
+    st = lib.mpc_beaver_matmul(h, p(z), p(z), p(z), p(z), p(z), p(z), ctypes.c_int64(300), ctypes.c_int64(100),
+                               ctypes.c_int64(260), 0, ctypes.c_uint64(0), p(tiny), ctypes.c_size_t(16))
+    assert st != 0
