@@ -794,10 +794,35 @@ size_t ring_gemm_partials_bytes(int parties, int64_t M, int64_t N, int total_kb,
 }
 
 namespace gemm {
-__global__ void finalize_kernel(uint64_t* __restrict__ z, const uint64_t* __restrict__ c,
-                                const uint64_t* __restrict__ part, int splits, int64_t n, int bits) {
+__global__ void finalize_kernel(uint64_t* z, const uint64_t* c, const uint64_t* __restrict__ part, int splits,
+                                int64_t n, int bits) {
     asm volatile("griddepcontrol.wait;" ::: "memory");     // programmatic dependent of the GEMM
     asm volatile("griddepcontrol.launch_dependents;");      // the next split kernel may be scheduled
+    const bool vec = (n & 1) == 0 && ((reinterpret_cast<uintptr_t>(z) | reinterpret_cast<uintptr_t>(part) |
+                                       (c ? reinterpret_cast<uintptr_t>(c) : 0)) & 15) == 0;
+    if (vec) {
+        // two elements per thread (16-byte accesses) and four slabs' loads in flight per step
+        // (ring addition: any grouping is exact); z may alias c — each pair is read first
+        const int64_t n2 = n / 2;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
+            ulonglong2 v = c ? reinterpret_cast<const ulonglong2*>(c)[i] : make_ulonglong2(0ull, 0ull);
+            int s = 0;
+            for (; s + 4 <= splits; s += 4) {
+                ulonglong2 t[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) t[q] = __ldcs(reinterpret_cast<const ulonglong2*>(part + (int64_t)(s + q) * n) + i);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) { v.x += t[q].x; v.y += t[q].y; }
+            }
+            for (; s < splits; ++s) {
+                const ulonglong2 t = __ldcs(reinterpret_cast<const ulonglong2*>(part + (int64_t)s * n) + i);
+                v.x += t.x; v.y += t.y;
+            }
+            if (bits) { v.x = div_pow2_round(v.x, bits); v.y = div_pow2_round(v.y, bits); }
+            reinterpret_cast<ulonglong2*>(z)[i] = v;
+        }
+        return;
+    }
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         uint64_t v = c ? c[i] : 0ull;
         for (int s = 0; s < splits; ++s) v += part[(int64_t)s * n + i];
@@ -818,7 +843,7 @@ cudaError_t ring_gemm_finalize(const RingGemmParams& q, int parties, cudaStream_
     if ((parties > 1 && (q.party_stride_z != per_party || (q.C && q.party_stride_c != q.party_stride_z))) ||
         (q.batch > 1 && (q.batch_stride_z != q.M * q.N || (q.C && q.batch_stride_c != q.batch_stride_z))))
         return cudaErrorInvalidValue;                   // the finalize pass needs z (and c) contiguous
-    int64_t blocks = (n + 255) / 256;
+    int64_t blocks = ((n % 2 == 0 ? n / 2 : n) + 255) / 256;     // element pairs when n is even
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
     return launch_pdl(gemm::finalize_kernel, dim3((unsigned)blocks), dim3(256), 0, stream, q.Z, q.C,
