@@ -75,7 +75,8 @@ def case(request):
     {"MPC_GEMM_TMA": "1", "MPC_GEMM_TMA_L2": "1"},
     {"MPC_GEMM_PARTY_MAJOR": "1"},          # instance-major tile order (the > 2 GiB default)
     {"MPC_GEMM_PARTY_MAJOR": "1", "MPC_GEMM_GROUPM": "3"},
-    # K-serpentine (the > 2 GiB default): odd items of a cluster walk their units backwards
+    # K-serpentine (the default): odd items of a cluster walk their units backwards
+    {"MPC_GEMM_SERPENTINE": "0"},
     {"MPC_GEMM_SERPENTINE": "1", "MPC_GEMM_TMA": "0"},
     {"MPC_GEMM_SERPENTINE": "1", "MPC_GEMM_TMA": "0", "MPC_GEMM_SPLITS": "7", "MPC_GEMM_KC": "5"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
