@@ -295,7 +295,6 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
         // ------------------------------------------------ leader: MMA issuer (one elected lane)
         int s = 0; uint32_t ph = 0; uint32_t u = 0;
         int item_no = 0;
-        bool first_stage = true;
         long long st_tempty = 0, st_full = 0;
         const long long t_start = clock64();
         for (int w = cluster_id(); w < wm.items(); w += nclusters()) {
@@ -310,11 +309,7 @@ __device__ __forceinline__ void control_roles(const RingGemmParams& p, const Wor
                         {
                             const long long w0 = p.dbg ? clock64() : 0;
                             mbar_wait_cluster(&B.full[s], ph);
-                            if (p.dbg) {
-                                st_full += clock64() - w0;
-                                if (first_stage && lane == 0) atomicMax(&p.dbg[8], globaltimer());   // pipeline filled
-                                first_stage = false;
-                            }
+                            if (p.dbg) st_full += clock64() - w0;
                         }
                         tc_fence_after();
                         const uint64_t da = smem_desc(smem_u32(B.stage_base + s * kStageBytes));
@@ -399,7 +394,6 @@ __device__ __forceinline__ void epilogue_role(const RingGemmParams& p, const Wor
         for (int k0 = klo; k0 < khi; k0 += wm.kc) {
             for (int g = 0; g < kPasses; ++g, ++u) {
                 mbar_wait(B.tfull, u & 1);
-                if (p.dbg && lane == 0) atomicMax(&p.dbg[9], globaltimer());          // last MMAs complete
                 tc_fence_after();
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -739,7 +733,7 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     }
     // diagnostic mode (the same kernel variant, launched without PDL): stall-cycle attribution of the
     // producer and MMA threads and a globaltimer timeline
-    unsigned long long h[10] = {0, 0, 0, 0, ~0ull, 0, 0, 0, 0, 0};
+    unsigned long long h[8] = {0, 0, 0, 0, ~0ull, 0, 0, 0};
     cudaMalloc(&q.dbg, sizeof(h));
     cudaMemcpyAsync(q.dbg, h, sizeof(h), cudaMemcpyHostToDevice, stream);
     cudaEvent_t e0, e1;
@@ -757,10 +751,10 @@ cudaError_t ring_gemm_launch(const RingGemmParams& prm, int parties, cudaStream_
     const double n = (double)clusters;
     fprintf(stderr, "[ring_gemm] M=%lld N=%lld kb=%d kc=%d splits=%d clusters=%lld  per MMA thread: total %.0f cyc, "
             "wait tempty %.1f%%, wait full %.1f%%; producer wait empty %.0f cyc | event %.1f us, timeline us: "
-            "setup done %.1f, first stage %.1f, MMA issue end %.1f, MMAs complete %.1f, epilogue end %.1f\n",
+            "setup done %.1f, MMA issue end %.1f, epilogue end %.1f\n",
             (long long)prm.M, (long long)prm.N, tkb, q.kc, q.splits, (long long)clusters, h[3] / n,
             100.0 * h[1] / h[3], 100.0 * h[2] / h[3], h[0] / (2 * n), kms * 1e3, (h[5] - h[4]) * 1e-3,
-            (h[8] - h[4]) * 1e-3, (h[6] - h[4]) * 1e-3, (h[9] - h[4]) * 1e-3, (h[7] - h[4]) * 1e-3);
+            (h[6] - h[4]) * 1e-3, (h[7] - h[4]) * 1e-3);
     q.dbg = nullptr;
     if (e != cudaSuccess || q.splits <= 1) return e;
     return ring_gemm_finalize(q, parties, stream);

@@ -35,8 +35,7 @@ struct RingGemmParams {
     int kc;                             // 32-K blocks per accumulation unit (<= ring_gemm_max_kc())
     unsigned long long* dbg;            // optional (MPC_GEMM_DEBUG): [0..3] stall cycles (producer empty, MMA
                                         // tempty, MMA full, MMA total); [4..7] globaltimer: first entry, last
-                                        // setup done, last MMA issue end, last epilogue end; [8] last first-stage
-                                        // arrival (pipeline filled), [9] last tile-pass completion (MMAs done)
+                                        // setup done, last MMA issue end, last epilogue end
     int splits;                         // K ranges per output tile (split-K); 0/1 = none.  Set by the launcher.
     uint64_t* partials;                 // split-K slabs [splits][parties][M][N] (workspace,
                                         // ring_gemm_partials_bytes); unused when splits <= 1
