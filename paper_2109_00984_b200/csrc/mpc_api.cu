@@ -234,7 +234,8 @@ struct Carve {
 // either way (the same ring sums).  MPC_NO_SWAP=1 disables the transposition,
 // MPC_GEMM_SMALL=0/1 disables / forces (where possible) the stacked kernel.
 struct GemmChoice { bool swap, small; };
-GemmChoice choose_gemm(int parties, int64_t M, int64_t N, int64_t K, bool allow_swap, bool allow_small) {
+GemmChoice choose_gemm(int parties, int64_t M, int64_t N, int64_t K, bool allow_swap, bool allow_small,
+                       bool conv_out = false) {
     static const bool no_swap = getenv("MPC_NO_SWAP") != nullptr;
     static const int small_env = getenv("MPC_GEMM_SMALL") ? atoi(getenv("MPC_GEMM_SMALL")) : -1;
     allow_swap = allow_swap && !no_swap;
@@ -247,11 +248,22 @@ GemmChoice choose_gemm(int parties, int64_t M, int64_t N, int64_t K, bool allow_
     // item, a 32 x 32 epilogue): measured faster than the 2-CTA kernel for every
     // M <= 32 shape tried (scripts/gemm_kernel_compare.py) even where the
     // tensor-time model rates it up to ~1.2x slower, so it is preferred within 1.3x.
+    // The transposed 2-CTA GEMM is taken only when the model rates it more than twice as cheap:
+    // measured, its 32-K blocks run ~1.9-2x slower than the plain orientation's on the small-M
+    // shapes where the model sees exactly half the MMA time (ResNet 49 x 4608 x 512: GEMM 47.7
+    // vs 37.6 us; ResNet-50 chain 1.934 -> 1.876 ms, ResNet-18 0.879 -> 0.849 ms with the factor;
+    // Wav2Letter 51 x 8000 x 2000 is the one shape that lost: 348 -> 374 us, chain 0.688 -> 0.703).
+    // MPC_SWAP_GAIN overrides the factor (1.0: the plain model, 0.5 the default).
+    static const double swap_gain = getenv("MPC_SWAP_GAIN") ? atof(getenv("MPC_SWAP_GAIN")) : 0.5;
     auto consider = [&](bool sw, bool sm) {
         const int64_t gm = sw ? N : M, gn = sw ? M : N;
         if (sm && gm > kSmallMaxRows) return;
-        const double t = ring_gemm_model_cycles(parties, gm, gn, tkb, 74, sm) / (sm ? 1.3 : 1.0);
-        if (t < cost) { cost = t; best = GemmChoice{sw, sm}; }
+        // a convolution of one image keeps the plain model: its transposed output is already NCHW,
+        // the other orientation stores through the strided NCHW epilogue (ResNet-50 convs 2.41 ->
+        // 2.54 ms, Wav2Letter b1 0.84 -> 1.05 ms without transposition)
+        const double gain = conv_out ? 1.0 : swap_gain;
+        const double t = ring_gemm_model_cycles(parties, gm, gn, tkb, 74, sm) / (sm ? 1.3 : (sw ? gain : 1.0));
+        if (t < cost - 1e-9) { cost = t; best = GemmChoice{sw, sm}; }
     };
     if (allow_swap) consider(true, false);
     if (allow_small) consider(false, true);
@@ -343,7 +355,7 @@ BeaverWs carve_beaver(mpc_ctx c, void* ws, int64_t M, int64_t K, int64_t N, int6
         return w;
     }
     const int inst = (int)(Pl * w.batch);                     // GEMM instances
-    const GemmChoice gc = choose_gemm(inst, M, N, K, allow_swap, allow_small);
+    const GemmChoice gc = choose_gemm(inst, M, N, K, allow_swap, allow_small, ed_elems >= 0);
     w.swap = gc.swap;
     w.small = gc.small;
     if (ed_elems < 0) ed_elems = M * K + K * N;

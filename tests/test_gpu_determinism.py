@@ -4,7 +4,7 @@ configs; ring addition is associative, so any order is exact).
 
 Each configuration runs in its own process because the GEMM's tuning knobs
 (K-chunk length MPC_GEMM_KC, split-K factor MPC_GEMM_SPLITS, programmatic
-dependent launch MPC_NO_PDL, transposed GEMM for small M MPC_NO_SWAP, the
+dependent launch MPC_NO_PDL, transposed GEMM for small M MPC_NO_SWAP / MPC_SWAP_GAIN, the
 2-CTA GEMM's operand producer MPC_GEMM_TMA, its tile order MPC_GEMM_PARTY_MAJOR /
 MPC_GEMM_GROUPM / MPC_GEMM_SERPENTINE) are
 read once per process.  Every run must
@@ -68,6 +68,8 @@ def case(request):
     {"MPC_GEMM_SPLITS": "7", "MPC_GEMM_KC": "5"},
     {"MPC_NO_PDL": "1"},
     {"MPC_NO_SWAP": "1"},
+    {"MPC_SWAP_GAIN": "1.0"},               # the plain model: small-M shapes run transposed
+    {"MPC_SWAP_GAIN": "100"},               # transposed wherever allowed
     {"MPC_GEMM_SMALL": "0"},
     {"MPC_GEMM_SMALL": "1"},
     {"MPC_GEMM_TMA": "0"},                  # bulk-copy producer with the peer relay everywhere
@@ -84,7 +86,7 @@ def test_same_shares_under_every_launch_config(case, env):
     (M, K, N), expected = case
     full = dict(os.environ)
     for k in ("MPC_GEMM_KC", "MPC_GEMM_SPLITS", "MPC_NO_PDL", "MPC_NO_SWAP", "MPC_GEMM_DEBUG", "MPC_GEMM_SMALL",
-              "MPC_GEMM_TMA", "MPC_GEMM_TMA_L2", "MPC_GEMM_PARTY_MAJOR", "MPC_GEMM_GROUPM", "MPC_GEMM_SERPENTINE"):
+              "MPC_GEMM_TMA", "MPC_GEMM_TMA_L2", "MPC_GEMM_PARTY_MAJOR", "MPC_GEMM_GROUPM", "MPC_GEMM_SERPENTINE", "MPC_SWAP_GAIN"):
         full.pop(k, None)
     full.update(env)
     out = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, M=M, K=K, N=N, P=P)], env=full,
