@@ -43,6 +43,7 @@
 // issuer, warp 2 TMEM allocator, warps 4..11 epilogue (two per TMEM lane
 // quadrant, 16 columns each).
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -303,12 +304,20 @@ int ring_gemm_splits(int parties, int64_t M, int64_t N, int tkb, int64_t max_clu
 // two stacked MMAs now take ~192, but a tile then needs its 16 KiB of planes
 // every ~200 cycles, more than the L2 -> SM feed gives one SM (~36-70 B/clk), so
 // the old figure stays as the conservative cost that selected the shapes it wins.
+// A split-K launch also pays its partial-sum stores and the finalize pass: ~12000 cycles
+// (≈ 7 µs: measured per-layer, the stacked kernel without split-K beats the 2-CTA kernel
+// with it on exactly the ResNet-50 shapes where this term flips the choice — 3136 x 576 x 64
+// 59.6 -> 49.6 us, 196 x 1024 x 256 30.8 -> 24.6 us — and loses everywhere it does not;
+// MPC_SPLIT_PENALTY overrides, 0 restores the MMA-only model).
 double ring_gemm_model_cycles(int parties, int64_t M, int64_t N, int tkb, int64_t max_clusters, bool small) {
+    static const double pen = getenv("MPC_SPLIT_PENALTY") ? atof(getenv("MPC_SPLIT_PENALTY")) : 12000.0;
     const int s = ring_gemm_splits(parties, M, N, tkb, max_clusters, small);
+    const double split_cost = s > 1 ? pen : 0.0;
     if (small)
-        return (double)waves(small_tiles(parties, M, N) * s, 2 * max_clusters) * ((tkb + s - 1) / s) * 12.0 * 48.0;
+        return (double)waves(small_tiles(parties, M, N) * s, 2 * max_clusters) * ((tkb + s - 1) / s) * 12.0 * 48.0 +
+               split_cost;
     const int64_t tiles = (int64_t)parties * (pad_rows<Layout::Left>(M) / 256) * (pad_rows<Layout::Right>(N) / 128);
-    return (double)waves(tiles * s, max_clusters) * ((tkb + s - 1) / s) * 2304.0;
+    return (double)waves(tiles * s, max_clusters) * ((tkb + s - 1) / s) * 2304.0 + split_cost;
 }
 
 cudaError_t ring_gemm_small_launch(const RingGemmParams& q, int parties, int64_t max_ctas, cudaStream_t stream) {
