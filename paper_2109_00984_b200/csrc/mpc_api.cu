@@ -249,10 +249,11 @@ GemmChoice choose_gemm(int parties, int64_t M, int64_t N, int64_t K, bool allow_
     // M <= 32 shape tried (scripts/gemm_kernel_compare.py) even where the
     // tensor-time model rates it up to ~1.2x slower, so it is preferred within 1.3x.
     // The transposed 2-CTA GEMM is taken only when the model rates it more than twice as cheap:
-    // measured, its 32-K blocks run ~1.9-2x slower than the plain orientation's on the small-M
-    // shapes where the model sees exactly half the MMA time (ResNet 49 x 4608 x 512: GEMM 47.7
-    // vs 37.6 us; ResNet-50 chain 1.934 -> 1.876 ms, ResNet-18 0.879 -> 0.849 ms with the factor;
-    // Wav2Letter 51 x 8000 x 2000 is the one shape that lost: 348 -> 374 us, chain 0.688 -> 0.703).
+    // measured in graph replay, the small-M layers where the model sees exactly half the MMA
+    // time run slower transposed (ResNet 49 x 4608 x 512: 65.7 vs 61.9 us per layer; alone,
+    // without PDL, its GEMM is the faster one — DESIGN §8d); ResNet-50 chain 1.934 -> 1.876 ms,
+    // ResNet-18 0.879 -> 0.849 ms with the factor; Wav2Letter 51 x 8000 x 2000 is the one shape
+    // that lost: 348 -> 374 us, chain 0.688 -> 0.703.
     // MPC_SWAP_GAIN overrides the factor (1.0: the plain model, 0.5 the default).
     static const double swap_gain = getenv("MPC_SWAP_GAIN") ? atof(getenv("MPC_SWAP_GAIN")) : 0.5;
     auto consider = [&](bool sw, bool sm) {
