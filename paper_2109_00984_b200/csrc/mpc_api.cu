@@ -262,7 +262,10 @@ GemmChoice choose_gemm(int parties, int64_t M, int64_t N, int64_t K, bool allow_
         // a convolution of one image keeps the plain model: its transposed output is already NCHW,
         // the other orientation stores through the strided NCHW epilogue (ResNet-50 convs 2.41 ->
         // 2.54 ms, Wav2Letter b1 0.84 -> 1.05 ms without transposition)
-        const double gain = conv_out ? 1.0 : swap_gain;
+        // long GEMMs (> 200k modelled cycles, ~0.1 ms) keep the plain model: there the MMA time
+        // dominates and the transposition pays as modelled (Wav2Letter 51 x 8000 x 2000: 348 vs
+        // 374 us transposed / not)
+        const double gain = (conv_out || cost > 200000.0) ? 1.0 : swap_gain;
         const double t = ring_gemm_model_cycles(parties, gm, gn, tkb, 74, sm) / (sm ? 1.3 : (sw ? gain : 1.0));
         if (t < cost - 1e-9) { cost = t; best = GemmChoice{sw, sm}; }
     };
