@@ -607,7 +607,7 @@ def main():
         # Triples are the offline phase (SURVEY 8(d) "triples pre-generated"): a pool of distinct
         # triples, one per e2e step (single use), is generated before the timed region when it fits in
         # HBM; the same loop with each step's triple generated inline is timed too (incl_ttp).
-        ke = max(4, args.steps // 4)
+        ke = max(4, min(32, args.steps // 4))             # e2e steps: their triple pool must fit in HBM
         trip_bytes = 8 * (M * K + K * N + M * N) * (P if world == 1 else 1)
         pool = None
         if (ke + 2) * trip_bytes < 0.4 * torch.cuda.mem_get_info(dev)[0]:
